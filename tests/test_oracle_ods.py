@@ -1,0 +1,241 @@
+"""Pins for the oracle's ODS replay (§5.2; readings R-O1..R-O20).
+
+What fixes the oracle here:
+  * SPEC's hand-worked example of the six fig:cache_aware_sampling steps;
+  * closed forms: static tiers (cap_A = 0) give exactly cap_E + cap_D hits per
+    job-epoch whatever the sampler; J = 1 pays every A hit with one refill;
+    cache-less jobs decode every sample (P:L428's 7.16 M = 4 x 1.79 M);
+  * invariants I1-I10 (each job-epoch delivers [0,N) exactly once, capacities,
+    conservation, determinism, |seen_j| = n_j);
+  * agreement with the independent literal transcription oracle/literal.py.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+from oracle import literal as L
+
+S, E, D, A, SUB = 0, 1, 2, 3, 4
+
+
+def caps_for(cfg):
+    p = O.make_profile(t_gpu=1, t_decode_augment=1, t_augment=1, b_nic=1, b_pcie=1, b_cache=1,
+                       b_storage=1, cache_bytes=cfg["cache_bytes"], n_total=cfg["n_total"],
+                       s_data=cfg["s_data"], m_num=cfg["m_num"], m_den=cfg["m_den"], nodes=1,
+                       gpus_per_node=1)
+    na, nd, ne, ns = O.split_counts(p, *cfg["split"])
+    return ne, nd, na
+
+
+def test_config_capacities_match_survey_table():
+    # SURVEY §8(d) caps E / D / A (derived from Eqs. 5-7 with the paper's splits)
+    assert caps_for(synth.ods_config("toy")) == (80, 11, 11)
+    assert caps_for(synth.ods_config("imagenet1k")) == (0, 42_038, 45_541)
+    assert caps_for(synth.ods_config("openimages")) == (658_561, 118_731, 0)
+    assert caps_for(synth.ods_config("imagenet22k")) == (4_376_846, 0, 0)
+
+
+def test_spec_worked_example():
+    """10 samples, A cache = {A,B,C}, job's seen = {A}, request {D,B,E}
+    -> response {C,B,E}: C substituted from A, B a hit, E from storage, D deferred."""
+    o = O.ODS(10, [3], [1], 0, 0, 3, seed=1)
+    tier = np.zeros(10, np.uint8); tier[[0, 1, 2]] = A          # A,B,C = ids 0,1,2
+    seen = np.zeros((1, 10), np.uint8); seen[0, 0] = 1           # job has seen A
+    o.set_state(tier, seen, np.zeros((1, 10), np.uint8))
+    rc, ids, src, lens = o.round([0], requested=[[3, 1, 4]])     # D, B, E
+    assert rc == 0 and lens[0] == 3
+    assert list(ids[0, :3]) == [2, 1, 4]
+    assert list(src[0, :3]) == [A | SUB, A, S]
+    t, sn, cn = o.state()
+    assert sn[0, 3] == 0                                          # D deferred (unseen)
+    assert sn[0, [0, 1, 2, 4]].all()
+    # maintain: J = 1 -> threshold 1 -> B and C evicted; refill restores |A| = 3
+    assert (t == A).sum() == 3 and t[1] != A and t[2] != A and t[0] == A
+
+
+def test_all_hits_and_empty_cache_trivia():
+    o = O.ODS(20, [4], [1], 20, 0, 0, seed=3)                     # everything encoded-cached
+    rc, ids, src, lens = o.round([0], requested=[[5, 9, 1, 0]])
+    assert list(ids[0]) == [5, 9, 1, 0] and list(src[0]) == [E] * 4
+    o = O.ODS(20, [4], [1], 0, 0, 0, seed=3)                      # empty cache
+    rc, ids, src, lens = o.round([0], requested=[[5, 9, 1, 0]])
+    assert list(ids[0]) == [5, 9, 1, 0] and list(src[0]) == [S] * 4
+
+
+def test_protocol_violations():
+    o = O.ODS(20, [4], [1], 0, 0, 0, seed=3)
+    assert o.round([0], requested=[[5, 5, 1, 0]])[0] == 3         # duplicate -> EPROTO
+    assert o.round([0], requested=[[5, 9, 1, 20]])[0] == 3        # out of range
+    assert o.round([0], requested=[[5, 9, 1, 0]])[0] == 0
+    assert o.round([0], requested=[[5, 2, 3, 4]])[0] == 3         # 5 already seen
+    assert o.round([1])[0] == 1                                    # unknown job -> EINVAL
+
+
+def test_departed_job_is_invalid_state():
+    o = O.ODS(8, [8, 4], [1, 2], 0, 0, 2, seed=3)
+    o.round([0, 1])                                               # job 0 finishes its only epoch
+    assert o.round([0])[0] == 2
+
+
+def test_threshold_two_evicts_after_both_jobs():
+    """threshold 2, a sample served to both jobs is evicted at the round end
+    and the A occupancy restored by refill."""
+    o = O.ODS(50, [5, 5], [2, 2], 0, 0, 10, seed=4)
+    tier0, _, _ = o.state()
+    A0 = set(np.flatnonzero(tier0 == A))
+    x = sorted(A0)[0]
+    rest = [i for i in range(50) if i not in A0][:4]
+    o.round([0, 1], requested=[[x] + rest, [x] + rest[::-1]])
+    t, _, c = o.state()
+    assert t[x] != A and not c[:, x].any()                        # evicted, consumers cleared
+    assert (t == A).sum() == 10                                   # refilled to cap_A
+    o2 = O.ODS(50, [5, 5], [2, 2], 0, 0, 10, seed=4)
+    o2.round([0], requested=[[x] + rest])                         # only one consumer
+    t2, _, c2 = o2.state()
+    assert t2[x] == A and c2[0, x] == 1 and c2[1, x] == 0
+
+
+def _check_invariants(o, cfg):
+    """I1 (exact-once per job-epoch), I4, I5, I9, I10 on a finished replay."""
+    tr = o.transcript()
+    st, ev, rf = o.stats()
+    N = cfg["n_total"]
+    for j in range(len(cfg["batch"])):
+        for e in range(cfg["target"][j]):
+            row = tr[j, e]
+            ids = (row & 0xFFFFFFFF).astype(np.int64)
+            assert np.array_equal(np.sort(ids), np.arange(N))      # I1 + I3
+            s = st[j, e]
+            assert s["served"].sum() == N                          # I5
+            srcs = (row >> np.uint64(32)).astype(np.int64)
+            for t in range(4):
+                assert s["served"][t] == ((srcs & 3) == t).sum()
+                assert s["subst"][t] == ((srcs == (t | SUB))).sum()
+            digest = 0
+            for q in range(N):
+                digest = (digest + O.splitmix64((q << 35) | int(row[q]))) & ((1 << 64) - 1)
+            assert digest == int(s["digest"])
+    t, seen, cons = o.state()
+    assert (t == E).sum() <= cfg["cap_e"] and (t == D).sum() <= cfg["cap_d"]
+    assert (t == A).sum() <= cfg["cap_a"]                          # I4
+    assert (t == A).sum() == cfg["cap_a"] + rf - ev                # A occupancy conservation
+    assert (t == E).sum() == cfg["cap_e"] and (t == D).sum() == cfg["cap_d"]   # static E/D (R-O4)
+
+
+def run_oracle(cfg, transcript=True):
+    o = O.ODS(cfg["n_total"], cfg["batch"], cfg["target"], cfg["cap_e"], cfg["cap_d"], cfg["cap_a"],
+              cfg["seed"], transcript=transcript)
+    return o
+
+
+def test_toy_config_invariants_and_determinism():
+    base = synth.ods_config("toy", seed=1)
+    ce, cd, ca = caps_for(base)
+    cfg = dict(base, cap_e=ce, cap_d=cd, cap_a=ca)
+    o = run_oracle(cfg)
+    rounds = o.replay_epochs(3)
+    assert rounds == 3 * ((1000 + 31) // 32)
+    _check_invariants(o, cfg)
+    o2 = run_oracle(cfg)
+    o2.replay_epochs(3)
+    assert np.array_equal(o.transcript(), o2.transcript())            # I6
+    assert np.array_equal(o.stats()[0], o2.stats()[0])
+
+
+def test_seen_count_tracks_progress_every_round():
+    cfg = dict(n_total=300, batch=[7, 16, 32], target=[2, 1, 3], cap_e=40, cap_d=30, cap_a=30, seed=9)
+    o = run_oracle(cfg, transcript=False)
+    while True:
+        c, e, n, act = o.job_state()
+        if not act.any():
+            break
+        _, seen, _ = o.state()
+        for j in range(3):
+            if act[j]:
+                assert seen[j].sum() == n[j]                          # I10
+        t, _, _ = o.state()
+        assert (t == A).sum() <= 30
+        o.replay_rounds(1)
+
+
+def test_static_tiers_closed_form():
+    """cap_A = 0: per job-epoch served[E] + served[D] = cap_E + cap_D exactly and
+    served[S] = N - cap_E - cap_D, for any seed (P:L1294 'roughly equal to the
+    percentage of cached data')."""
+    for seed in (1, 2, 3):
+        cfg = dict(n_total=500, batch=[16, 32, 64], target=[2, 2, 2], cap_e=60, cap_d=40, cap_a=0, seed=seed)
+        o = run_oracle(cfg)
+        o.replay_epochs(2)
+        st, ev, rf = o.stats()
+        for j in range(3):
+            for e in range(2):
+                s = st[j, e]
+                assert s["served"][E] == 60 and s["served"][D] == 40 and s["served"][S] == 400
+        assert ev == 0 and rf == 0
+        _check_invariants(o, cfg)
+
+
+def test_single_job_refill_pays_every_augmented_hit():
+    """J = 1 -> threshold 1: every A-served sample is evicted at its round end and
+    one storage sample refilled, so storage fetches + refills = delivered, except
+    the A-served of the final round (the job departs, no maintain work)."""
+    cfg = dict(n_total=1000, batch=[32], target=[2], cap_e=0, cap_d=0, cap_a=200, seed=5)
+    o = run_oracle(cfg)
+    rounds = o.replay_epochs(2)
+    st, ev, rf = o.stats()
+    tr = o.transcript()
+    delivered = 2 * 1000
+    storage = int(st[0, :, ]["served"][:, S].sum())
+    last_round = tr[0, 1, 1000 - (1000 % 32 or 32):]
+    a_last = int((((last_round >> np.uint64(32)) & np.uint64(3)) == A).sum())
+    assert storage + rf == delivered - a_last
+    assert ev == rf
+
+
+def test_cacheless_jobs_decode_everything():
+    """4 concurrent jobs, no cache, 1.79 M samples -> 7.16 M decode+augment ops."""
+    cfg = dict(n_total=1_790_000, batch=[4096] * 4, target=[1] * 4, cap_e=0, cap_d=0, cap_a=0, seed=2)
+    o = run_oracle(cfg, transcript=False)
+    o.replay_epochs(1)
+    st, _, _ = o.stats()
+    ops = int(st["served"][:, 0, S].sum() + st["served"][:, 0, E].sum())   # decode+augment
+    assert ops == 7_160_000
+
+
+def test_ods_uplift_direction():
+    """P:L1294 / S:L480: 3 jobs, 20 % cached in A -> stable-epoch hit rate well above
+    the cached fraction (the uniform no-evict baseline sits at the fraction)."""
+    cfg = dict(n_total=1000, batch=[32] * 3, target=[3] * 3, cap_e=0, cap_d=0, cap_a=200, seed=7)
+    o = run_oracle(cfg, transcript=False)
+    o.replay_epochs(3)
+    st, _, _ = o.stats()
+    for j in range(3):
+        for e in (1, 2):
+            hits = st[j, e]["served"][1:].sum()
+            assert hits / 1000 >= 0.30
+
+
+@pytest.mark.parametrize("block", range(8))
+def test_cross_check_with_literal_transcription(block):
+    """Agreement with oracle/literal.py on random tiny configs (N <= 64, J <= 3, B <= 8,
+    random caps and targets so departures happen mid-replay)."""
+    st = synth.Stream(1000 + block)
+    for _ in range(60):
+        cfg = synth.random_tiny_ods(st)
+        o = run_oracle(cfg)
+        o.replay_epochs(max(cfg["target"]))
+        lit = L.LiteralODS(cfg["n_total"], cfg["batch"], cfg["target"], cfg["cap_e"], cfg["cap_d"],
+                           cfg["cap_a"], cfg["seed"])
+        lit.replay_all()
+        tr = o.transcript()
+        for j in range(len(cfg["batch"])):
+            for e in range(cfg["target"][j]):
+                got = [(int(x) & 0xFFFFFFFF, int(x) >> 32) for x in tr[j, e]]
+                assert got == lit.deliveries[j][e], cfg
+        t, seen, cons = o.state()
+        assert list(t) == lit.tier
+        _, ev, rf = o.stats()
+        assert (ev, rf) == (lit.evicted, lit.refilled)
+        # I2 on the literal side: no A entry served twice to a job between admission and eviction
+        _check_invariants(o, cfg)
