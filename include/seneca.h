@@ -1,0 +1,231 @@
+/*
+ * seneca.h -- C-ABI of libseneca.so, the B200 (sm_100a) hot path of Seneca
+ * (arXiv 2511.13724, "Preparation Meets Opportunity: Enhancing Data
+ * Preprocessing for ML Training With Seneca").
+ *
+ * Two parts:
+ *   - MDP, Model-Driven Partitioning (§5.1; §5.3): the
+ *     DSI throughput model (Eqs. 1-9) evaluated for every (x_E, x_D, x_A) split
+ *     of a grid and every hardware profile, followed by an argmax.
+ *   - ODS, Opportunistic Data Sampling (§5.2): trace-driven replay
+ *     of N concurrent jobs over a cache partitioned into encoded (E), decoded
+ *     (D) and augmented (A) forms.
+ *
+ * "P:Lnnn" cites /root/reference/PAPER.md line nnn; "R-xx" a reading recorded in
+ * DESIGN.md §3 where the paper is silent or ambiguous.
+ *
+ * Conventions for every call:
+ *   - Device memory is CALLER-OWNED.  Pointers prefixed d_ are device pointers
+ *     (e.g. a torch tensor's data_ptr()); h_ are host pointers.  The library
+ *     never allocates device memory: seneca_state_bytes() sizes one workspace.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     Device work is enqueued and the call returns; device outputs are valid
+ *     after the stream synchronises.  Host outputs that do not depend on device
+ *     data (batch lengths, round counts) are returned synchronously.
+ *   - Every call returns a seneca_status.  seneca_last_error() returns a
+ *     thread-local message for the last failing call.  Invalid arguments never
+ *     touch device memory.
+ *   - A context is single-stream and not thread-safe; distinct contexts are
+ *     independent (one process per GPU; see DESIGN.md §8 for multi-GPU).
+ */
+#ifndef SENECA_H
+#define SENECA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SENECA_OK = 0,
+    SENECA_EINVAL = 1,  /* invalid argument (SPEC "invalid-argument")                      */
+    SENECA_ESTATE = 2,  /* call not valid in the current state (e.g. a departed job)       */
+    SENECA_EPROTO = 3,  /* protocol violation by caller-supplied request ids       */
+    SENECA_ECUDA = 4,   /* CUDA runtime error (message in seneca_last_error)                */
+    SENECA_ENOSPC = 6   /* workspace smaller than seneca_state_bytes()                     */
+} seneca_status;
+
+/* ------------------------------------------------------------------------- */
+/* MDP                                                                        */
+/* ------------------------------------------------------------------------- */
+
+/* One row of tab:model_vars: hardware x dataset x job.  Units are
+ * canonical (bytes, bytes/s, samples/s; decimal SI, R-M11).  Layout: 112 bytes,
+ * 8-byte aligned, no implicit padding.                                         */
+typedef struct {
+    double   t_gpu;            /* T_GPU    samples/s per node; finite, > 0           */
+    double   t_decode_augment; /* T_{D+A}  samples/s per node; finite, > 0           */
+    double   t_augment;        /* T_A      samples/s per node; finite, > 0           */
+    double   b_nic;            /* B_NIC    bytes/s per node; finite, > 0             */
+    double   b_pcie;           /* B_PCIe   bytes/s per node; finite, > 0             */
+    double   b_cache;          /* B_cache  bytes/s; finite, > 0                      */
+    double   b_storage;        /* B_storage bytes/s; finite, > 0                     */
+    double   model_bytes;      /* beta*N in bytes (R-M2); finite, >= 0               */
+    uint64_t cache_bytes;      /* S_cache = S_mem (R-M5); 100*cache_bytes*m_den < 2^64 */
+    uint64_t n_total;          /* N_total >= 1                                       */
+    uint64_t s_data;           /* S_data >= 1 bytes; 100*m_num*s_data < 2^64          */
+    uint32_t m_num, m_den;     /* M = m_num/m_den >= 1 (5.12 = 128/25)        */
+    uint32_t nodes;            /* n >= 1                                             */
+    uint32_t gpus_per_node;    /* >= 1                                               */
+    uint8_t  nvlink_intra;     /* intra-node NVLink -> C_PCIe = 0             */
+    uint8_t  nvlink_inter;     /* inter-node NVLink -> C_PCIe = C_nw = 0      */
+    uint8_t  comm_mapping;     /* R-M1: 0 network<->nodes, PCIe<->gpus_per_node;
+                                  1 the literal (swapped) text of P:L529             */
+    uint8_t  _pad[5];
+} seneca_mdp_profile;
+
+/* Argmax of Eq. 9 over the grid for one profile.  48 bytes.                  */
+typedef struct {
+    uint8_t p_e, p_d, p_a;     /* argmax split in integer percent, sums to 100        */
+    uint8_t lim_a, lim_d, lim_e, lim_s; /* limiting term of Eqs. 1-4: 0 cache-bw, 1 nic,
+                                  2 pcie, 3 cpu-augment, 4 cpu-decode-augment, 5 gpu,
+                                  6 storage-bw (first minimal term wins, R-M8)       */
+    uint8_t status;            /* 0 ok; 1 the profile violates the constraints above
+                                  (all other fields then undefined)                  */
+    double  v_best;            /* DSI_overall at the argmax (Eq. 9), samples/s        */
+    double  dsi_a, dsi_d, dsi_e, dsi_s; /* Eqs. 1-4, samples/s                        */
+} seneca_mdp_result;
+
+/* Number of splits on a grid of step g percent (g divides 100):
+ * (100/g + 1)(100/g + 2)/2, i.e. 5151 at 1 % and 66 at 10 %.          */
+uint64_t seneca_mdp_num_splits(uint32_t grid_step_pct);
+
+/* MDP sweep (a9-a12).  For every profile i < n_profiles: the tier throughputs
+ * DSI_A/D/E/S (Eqs. 1-4, with the ring overhead 2(n-1)/n*betaN of
+ * P:L529), the capacity-clamped counts N_A, N_D, N_E, N_S (Eqs. 5-8, floored
+ * exactly in integers, R-M6) and DSI_overall (Eq. 9) for every split
+ * of the grid, enumerated p_E = 100, 100-g, ..., 0 and, for each, p_D = 100-p_E,
+ * ..., 0 (R-M9); then the argmax, exact ties to the smallest enumeration index
+ * (R-M8).  Arithmetic is IEEE binary64 with one rounding per operation in the
+ * literal order of R-M7 (bit-identical to the oracle).
+ *   d_profiles  [n_profiles] device, read-only.
+ *   d_results   [n_profiles] device, written.
+ *   d_grid      NULL, or device [n_profiles][num_splits] doubles, row-major in
+ *               enumeration order, written.
+ * Errors: EINVAL if grid_step_pct does not divide 100, n_profiles == 0 or a
+ * required pointer is NULL.  Per-profile constraint violations are reported in
+ * seneca_mdp_result.status, not as a call error.                              */
+seneca_status seneca_mdp_sweep(const seneca_mdp_profile* d_profiles, uint32_t n_profiles,
+                               uint32_t grid_step_pct, seneca_mdp_result* d_results,
+                               double* d_grid, void* stream);
+
+/* Eqs. 5-8 for one split on the host, in exact integer arithmetic (R-M6):
+ * caps[0..3] = {N_E, N_D, N_A, N_storage} for a dataset of n_total samples of
+ * s_data bytes, a cache of cache_bytes and M = m_num/m_den.  Used to size the
+ * ODS tiers of seneca_cache_config.  EINVAL on p_e+p_d+p_a != 100, zero sizes,
+ * m_num < m_den, or 100*cache_bytes*m_den / 100*m_num*s_data overflowing u64.  */
+seneca_status seneca_split_capacities(uint64_t n_total, uint64_t s_data, uint32_t m_num,
+                                      uint32_t m_den, uint64_t cache_bytes, uint32_t p_e,
+                                      uint32_t p_d, uint32_t p_a, uint64_t caps[4]);
+
+/* ODS metadata footprint as the paper counts it: 1 bit per sample
+ * per job for `seen` plus 1 byte per sample for status+reference:
+ * n_jobs*ceil(n_total/8) + n_total.  (This library's own layout is reported by
+ * seneca_state_bytes; R-O14.)                                                   */
+uint64_t seneca_metadata_bytes(uint64_t n_total, uint32_t n_jobs);
+
+/* ------------------------------------------------------------------------- */
+/* ODS                                                                        */
+/* ------------------------------------------------------------------------- */
+
+typedef struct seneca_ctx seneca_ctx;
+
+typedef struct {
+    uint64_t        n_total;       /* N, 1 <= N < 2^31 (and N/32768 + batch <= 51200)    */
+    uint32_t        n_jobs;        /* J, 1..32                                           */
+    uint32_t        request_mode;  /* 0: requests generated from each job's keyed
+                                      permutation (R-O1, R-O3); 1: caller-supplied ids
+                                      in seneca_ods_next_batch (R-O20)                   */
+    const uint32_t* batch_size;    /* host [n_jobs], 1..4096 ("up to 1024")     */
+    const uint32_t* target_epochs; /* host [n_jobs], >= 1; job departs after these     */
+    uint64_t        cap_e, cap_d, cap_a; /* tier capacities in samples (Eqs. 5-7), sum <= N */
+    uint64_t        seed;          /* all randomness derives from (seed, purpose, ...) R-O17 */
+} seneca_cache_config;
+
+/* Per job-epoch counters (R-O10; digest in DESIGN.md §3).  104 bytes.       */
+typedef struct {
+    uint64_t served[4];    /* delivered samples by source tier: [0] storage, [1] E, [2] D, [3] A */
+    uint64_t subst[4];     /* of which substituted for a miss, by tier                          */
+    uint64_t req_hits[4];  /* requested samples that hit, by tier                               */
+    uint64_t digest;       /* sum over delivery position q of splitmix64(q<<35 | src<<32 | id)  */
+} seneca_job_epoch_stats;
+
+/* Device views into the workspace, valid until seneca_destroy.              */
+typedef struct {
+    uint64_t n_total;
+    uint32_t n_jobs, max_target;
+    uint64_t words;                     /* 32-bit words per bitmap (bit i of word i/32)    */
+    const uint32_t* d_tier_e;           /* residency bitmaps ("status")           */
+    const uint32_t* d_tier_d;
+    const uint32_t* d_tier_a;
+    const uint32_t* d_seen;             /* [n_jobs][words] per-job seen           */
+    const uint32_t* d_cons;             /* [n_jobs][words] consumer sets of A entries (R-O5) */
+    const seneca_job_epoch_stats* d_stats; /* [n_jobs][max_target]                        */
+    const uint64_t* d_evicted;          /* total evictions                                 */
+    const uint64_t* d_refilled;         /* total refills                                   */
+    uint64_t round;                     /* rounds executed                                 */
+    uint64_t epoch[32];                 /* host mirror: current epoch of each job          */
+    uint64_t consumed[32];              /* host mirror: samples consumed in current epoch  */
+    uint32_t active_mask;               /* bit j set while job j has not departed          */
+} seneca_state_view;
+
+/* Workspace size for cfg (bytes, 256-aligned pieces).  EINVAL on a bad cfg.   */
+seneca_status seneca_state_bytes(const seneca_cache_config* cfg, size_t* bytes);
+
+/* init_cache (a warm start, R-O9): carve d_workspace (caller-owned, >= the
+ * seneca_state_bytes size, 256-byte aligned), fill tiers with iota =
+ * perm(key(seed, INIT), N, .) -- positions [0,cap_A) -> A, the next cap_D -> D,
+ * the next cap_E -> E --, clear seen/consumer sets, build the pool counts and
+ * every job's first permutation.  *out receives a host handle (free with
+ * seneca_destroy).  EINVAL / ENOSPC on bad arguments.                          */
+seneca_status seneca_init_cache(const seneca_cache_config* cfg, void* d_workspace,
+                                size_t workspace_bytes, void* stream, seneca_ctx** out);
+
+/* One round (R-O11): a batch for each job of h_jobs (distinct, active), then
+ * maintain (eviction + refill, R-O7).  Per job j: need = min(B_j, N - n_j)
+ * ids are requested (generated, or read from d_requested[x][0..need) when
+ * request_mode = 1), misses are replaced by unseen cached samples tier by tier
+ * A -> D -> E (§5.2 steps 1-4) and the response is written to
+ * d_out_ids[x][s] / d_out_src[x][s] (x = position in h_jobs, row stride =
+ * max batch size; src bits 0-1 tier 0 S 1 E 2 D 3 A, bit 2 substituted).
+ * h_out_lens[x] = need (host, synchronous).  A job whose epoch ends is reset
+ * (step 6) and departs after its target epoch.
+ * Errors: EINVAL (bad/duplicate job, NULL outputs, d_requested given in mode 0
+ * or missing in mode 1), ESTATE (departed job), EPROTO (mode 1: a supplied id
+ * out of range, duplicated or already seen -- checked synchronously, the round
+ * is then not applied).                                                        */
+seneca_status seneca_ods_next_batch(seneca_ctx* ctx, const uint32_t* h_jobs, uint32_t n_jobs,
+                                    const uint32_t* d_requested, uint32_t* d_out_ids,
+                                    uint8_t* d_out_src, uint32_t* h_out_lens, void* stream);
+
+/* Replay whole rounds over all active jobs (request_mode 0 only) until every
+ * job active at the call has completed n_epochs more epochs or departed.
+ * d_transcript: NULL, or device [n_jobs][max_target][n_total] uint64 receiving
+ * src<<32 | id at each delivery position.  *h_rounds = rounds executed.
+ * ESTATE if no job is active or request_mode = 1.                            */
+seneca_status seneca_replay_epochs(seneca_ctx* ctx, uint32_t n_epochs, uint64_t* d_transcript,
+                                   uint64_t* h_rounds, void* stream);
+
+/* As seneca_replay_epochs but for exactly n_rounds rounds (fewer if every job
+ * departs).                                                                    */
+seneca_status seneca_replay_rounds(seneca_ctx* ctx, uint64_t n_rounds, uint64_t* d_transcript,
+                                   uint64_t* h_rounds, void* stream);
+
+seneca_status seneca_read_state(const seneca_ctx* ctx, seneca_state_view* out);
+
+/* Synchronise `stream` and report a latched device-side error (an internal
+ * consistency check failing) as ESTATE.                                        */
+seneca_status seneca_sync_status(seneca_ctx* ctx, void* stream);
+
+/* Number of kernel launches this context has issued (for gpu_launches).      */
+uint64_t seneca_launch_count(const seneca_ctx* ctx);
+
+void        seneca_destroy(seneca_ctx* ctx);
+const char* seneca_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SENECA_H */

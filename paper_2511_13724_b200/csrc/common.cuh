@@ -1,0 +1,131 @@
+// common.cuh -- shared device helpers of libseneca.so (sm_100a).
+//
+// Counter-based randomness for the ODS replay (reading R-O17; the
+// paper only says "a pseudo-random number generator", §5.2, and a
+// "predetermined pseudo-random sequence", §1):
+//   philox4x32-10 (Salmon et al., SC'11), splitmix64 key derivation, and a
+//   6-round balanced Feistel network on 2^bits restricted to [0,n) by cycle
+//   walking -- a keyed bijection, so "a permutation slice" needs no sort.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/seneca.h"
+
+namespace seneca {
+
+// ---------------------------------------------------------------- error plumbing
+void set_error(const char* fmt, ...);
+seneca_status cuda_status(cudaError_t e, const char* what);
+
+#define SENECA_CUDA_TRY(expr)                                              \
+    do {                                                                   \
+        cudaError_t _e = (expr);                                           \
+        if (_e != cudaSuccess) return ::seneca::cuda_status(_e, #expr);    \
+    } while (0)
+
+// ---------------------------------------------------------------- PRNG (device)
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    uint64_t z = x + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+enum : uint32_t { PUR_INIT = 1, PUR_REQ = 2, PUR_SUB = 3, PUR_REFILL = 4 };
+
+// key(seed, purpose, a, b, c) = splitmix64(seed ^ splitmix64(purpose<<56 ^ a<<48 ^ c<<44 ^ b))
+__device__ __forceinline__ uint64_t derive_key(uint64_t seed, uint64_t purpose, uint64_t a,
+                                               uint64_t b, uint64_t c) {
+    return splitmix64(seed ^ splitmix64((purpose << 56) ^ (a << 48) ^ (c << 44) ^ b));
+}
+
+// philox4x32-10 on counter (c0, c1, 0, 0); only word 0 of the output is used.
+__device__ __forceinline__ uint32_t philox_w0(uint32_t c0, uint32_t c1, uint32_t k0, uint32_t k1) {
+    uint32_t c2 = 0, c3 = 0;
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+        const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+        c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+        k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+    }
+    return c0;
+}
+
+// Domain of a keyed permutation of [0, n): bits = max(2, ceil(log2 n)) rounded
+// up to even, half width h, mask 2^h - 1.
+struct PermDomain {
+    uint32_t n, h, mask;
+};
+
+__device__ __forceinline__ PermDomain perm_domain(uint32_t n) {
+    uint32_t bits = n <= 1 ? 0u : 32u - __clz(n - 1u);
+    bits = bits < 2u ? 2u : bits;
+    bits += bits & 1u;
+    PermDomain d;
+    d.n = n;
+    d.h = bits >> 1;
+    d.mask = (1u << d.h) - 1u;
+    return d;
+}
+
+__device__ __forceinline__ uint32_t perm_apply(uint64_t key, const PermDomain& d, uint32_t x) {
+    if (d.n <= 1u) return 0u;
+    const uint32_t k0 = (uint32_t)key, k1 = (uint32_t)(key >> 32);
+    do {
+        uint32_t hl = x >> d.h, hr = x & d.mask;
+#pragma unroll
+        for (uint32_t rd = 0; rd < 6; ++rd) {
+            const uint32_t f = philox_w0(hr, rd, k0, k1) & d.mask;
+            const uint32_t t = hl ^ f;
+            hl = hr;
+            hr = t;
+        }
+        x = (hl << d.h) | hr;
+    } while (x >= d.n);
+    return x;
+}
+
+// ---------------------------------------------------------------- block scan
+// Exclusive scan of one uint32 per thread across the block (blockDim.x a
+// multiple of 32, <= 1024).  scratch: 33 uint32 of shared memory.  Every
+// thread must call it; it ends with a barrier so scratch can be reused.
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* total, uint32_t* scratch) {
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint32_t nwarps = blockDim.x >> 5;
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= (uint32_t)o) incl += y;
+    }
+    if (lane == 31) scratch[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = lane < nwarps ? scratch[lane] : 0u;
+        uint32_t wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= (uint32_t)o) wi += y;
+        }
+        if (lane < nwarps) scratch[lane] = wi - w;
+        if (lane == 31) scratch[32] = wi;
+    }
+    __syncthreads();
+    const uint32_t res = scratch[warp] + incl - v;
+    if (total) *total = scratch[32];
+    __syncthreads();
+    return res;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+}  // namespace seneca

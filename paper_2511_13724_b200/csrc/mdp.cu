@@ -1,0 +1,234 @@
+// mdp.cu -- Model-Driven Partitioning sweep.
+//
+// One CTA per hardware profile:
+//   prologue  Eqs. 1-4 tier throughputs with the ring-reduce
+//             overhead C = 2(n-1)/n * betaN; integer capacity tables
+//             capAD[p], capE[p] (Eqs. 5-7 floored exactly, R-M6) and the Eq. 9
+//             terms that depend on one coordinate only, all in shared memory;
+//   main loop every split of the grid: clamped counts (Eqs. 5-8) and
+//             DSI_overall (Eq. 9) in the literal order of R-M7; optional
+//             coalesced write of the full grid row;
+//   epilogue  block argmax, exact ties -> smallest enumeration index (R-M8).
+//
+// Bit-exactness with the oracle: every binary64 operation is an explicit
+// round-to-nearest intrinsic (__dadd_rn/__dmul_rn/__ddiv_rn, never contracted
+// into an FMA), integer->double conversions are __ull2double_rn, and a term
+// taken from a table is the same operation on the same operands as the one the
+// oracle performs per split.
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace seneca {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kMaxSteps = 101;  // grid step 1 % -> 101 values per coordinate
+
+enum : uint8_t { L_CACHE = 0, L_NIC = 1, L_PCIE = 2, L_CPU_AUG = 3, L_CPU_DEC_AUG = 4, L_GPU = 5, L_STORAGE = 6 };
+
+__device__ __forceinline__ double u2d(uint64_t x) { return __ull2double_rn(x); }
+
+__device__ __forceinline__ void take_min(double term, uint8_t code, double& best, uint8_t& lim) {
+    if (term < best) { best = term; lim = code; }
+}
+
+// C = 2(n-1)/n x betaN
+__device__ __forceinline__ double comm_overhead(uint64_t p, double model_bytes) {
+    if (p <= 1) return 0.0;
+    const double frac = __ddiv_rn(u2d(2ull * (p - 1ull)), u2d(p));
+    return __dmul_rn(frac, model_bytes);
+}
+
+__device__ __forceinline__ bool finite_pos(double x) { return isfinite(x) && x > 0.0; }
+
+__device__ bool profile_valid(const seneca_mdp_profile& p) {
+    if (!finite_pos(p.t_gpu) || !finite_pos(p.t_decode_augment) || !finite_pos(p.t_augment)) return false;
+    if (!finite_pos(p.b_nic) || !finite_pos(p.b_pcie) || !finite_pos(p.b_cache) || !finite_pos(p.b_storage)) return false;
+    if (!isfinite(p.model_bytes) || p.model_bytes < 0.0) return false;
+    if (p.n_total == 0 || p.s_data == 0 || p.m_den == 0 || p.m_num < p.m_den) return false;
+    if (p.nodes == 0 || p.gpus_per_node == 0) return false;
+    if (p.cache_bytes > (~0ull / 100ull) / p.m_den) return false;   // 100*cache*m_den < 2^64
+    if (p.s_data > (~0ull / 100ull) / p.m_num) return false;        // 100*m_num*s_data < 2^64
+    return true;
+}
+
+// Eqs. 1-4; dsi/lim index 0 A, 1 D, 2 E, 3 S.
+__device__ void tier_throughputs(const seneca_mdp_profile& p, double dsi[4], uint8_t lim[4]) {
+    const double Sd = u2d(p.s_data);
+    const double MS = __ddiv_rn(u2d((uint64_t)p.m_num * p.s_data), u2d(p.m_den));   // M x S_data
+    const uint64_t p_nw = p.comm_mapping ? p.gpus_per_node : p.nodes;                 // R-M1
+    const uint64_t p_pc = p.comm_mapping ? p.nodes : p.gpus_per_node;
+    const double C_nw = p.nvlink_inter ? 0.0 : comm_overhead(p_nw, p.model_bytes);
+    const double C_pc = (p.nvlink_intra || p.nvlink_inter) ? 0.0 : comm_overhead(p_pc, p.model_bytes);
+    const double nd = u2d(p.nodes);
+    const double nic = __dmul_rn(nd, p.b_nic);
+    const double pcie = __dmul_rn(nd, p.b_pcie);
+    const double gpu = __dmul_rn(nd, p.t_gpu);
+    const double cache_ms = __ddiv_rn(p.b_cache, MS);
+    const double nic_ms = __ddiv_rn(nic, __dadd_rn(MS, C_nw));
+    const double pcie_ms = __ddiv_rn(pcie, __dadd_rn(MS, C_pc));
+
+    // Eq. 1
+    double a = __longlong_as_double(0x7ff0000000000000ll); uint8_t la = 0xff;
+    take_min(cache_ms, L_CACHE, a, la);
+    take_min(nic_ms, L_NIC, a, la);
+    take_min(pcie_ms, L_PCIE, a, la);
+    take_min(gpu, L_GPU, a, la);
+    // Eq. 2 (R-M4: the PCIe and GPU terms are separate)
+    double d = __longlong_as_double(0x7ff0000000000000ll); uint8_t ld = 0xff;
+    take_min(cache_ms, L_CACHE, d, ld);
+    take_min(nic_ms, L_NIC, d, ld);
+    take_min(__dmul_rn(nd, p.t_augment), L_CPU_AUG, d, ld);
+    take_min(pcie_ms, L_PCIE, d, ld);
+    take_min(gpu, L_GPU, d, ld);
+    // Eq. 3: cache and NIC terms over the encoded size S_data
+    double e = __longlong_as_double(0x7ff0000000000000ll); uint8_t le = 0xff;
+    take_min(__ddiv_rn(p.b_cache, Sd), L_CACHE, e, le);
+    take_min(__ddiv_rn(nic, __dadd_rn(Sd, C_nw)), L_NIC, e, le);
+    take_min(__dmul_rn(nd, p.t_decode_augment), L_CPU_DEC_AUG, e, le);
+    take_min(pcie_ms, L_PCIE, e, le);
+    take_min(gpu, L_GPU, e, le);
+    // Eq. 4
+    const double st = __ddiv_rn(p.b_storage, Sd);
+    double s = e; uint8_t ls = le;
+    if (st < e) { s = st; ls = L_STORAGE; }
+    dsi[0] = a; dsi[1] = d; dsi[2] = e; dsi[3] = s;
+    lim[0] = la; lim[1] = ld; lim[2] = le; lim[3] = ls;
+}
+
+__global__ void __launch_bounds__(kThreads)
+mdp_sweep_kernel(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_profiles, uint32_t g,
+                 uint32_t steps, uint32_t n_splits, seneca_mdp_result* __restrict__ results,
+                 double* __restrict__ grid) {
+    __shared__ uint64_t s_capAD[kMaxSteps], s_capE[kMaxSteps];
+    __shared__ double s_tA[kMaxSteps], s_tD[kMaxSteps], s_tE[kMaxSteps];
+    __shared__ double s_dsi[4];
+    __shared__ uint8_t s_lim[4];
+    __shared__ int s_valid;
+    __shared__ double s_rv[kThreads / 32];
+    __shared__ uint32_t s_ri[kThreads / 32];
+
+    for (uint32_t pi = blockIdx.x; pi < n_profiles; pi += gridDim.x) {
+        const seneca_mdp_profile p = profiles[pi];
+        if (threadIdx.x == 0) {
+            s_valid = profile_valid(p);
+            if (s_valid) {
+                double dsi[4]; uint8_t lim[4];
+                tier_throughputs(p, dsi, lim);
+                for (int k = 0; k < 4; ++k) { s_dsi[k] = dsi[k]; s_lim[k] = lim[k]; }
+            }
+        }
+        __syncthreads();
+        if (!s_valid) {
+            if (threadIdx.x == 0) {
+                seneca_mdp_result r = {};
+                r.status = 1;
+                results[pi] = r;
+            }
+            __syncthreads();
+            continue;
+        }
+        const uint64_t N = p.n_total;
+        const double dN = u2d(N);
+        // capacity tables, exact floors (Eqs. 5-7, R-M6)
+        if (threadIdx.x <= steps) {
+            const uint64_t pct = (uint64_t)threadIdx.x * g;
+            s_capAD[threadIdx.x] = (pct * p.cache_bytes * p.m_den) / (100ull * p.m_num * p.s_data);
+            s_capE[threadIdx.x] = (pct * p.cache_bytes) / (100ull * p.s_data);
+        }
+        __syncthreads();
+        // one-coordinate Eq. 9 terms: (N_t/N) * DSI_t for an unclamped count
+        if (threadIdx.x <= steps) {
+            const uint64_t ca = s_capAD[threadIdx.x] < N ? s_capAD[threadIdx.x] : N;
+            s_tA[threadIdx.x] = __dmul_rn(__ddiv_rn(u2d(ca), dN), s_dsi[0]);
+            s_tD[threadIdx.x] = __dmul_rn(__ddiv_rn(u2d(s_capAD[threadIdx.x]), dN), s_dsi[1]);
+            s_tE[threadIdx.x] = __dmul_rn(__ddiv_rn(u2d(s_capE[threadIdx.x]), dN), s_dsi[2]);
+        }
+        __syncthreads();
+        const double dsiD = s_dsi[1], dsiE = s_dsi[2], dsiS = s_dsi[3];
+
+        double best = __longlong_as_double(0xfff0000000000000ll);   // -inf
+        uint32_t best_i = 0xffffffffu;
+        double* grow = grid ? grid + (uint64_t)pi * n_splits : nullptr;
+        for (uint32_t idx = threadIdx.x; idx < n_splits; idx += kThreads) {
+            // idx -> (row a, position b): row a has p_E = 100 - a*g and a+1 entries
+            uint32_t a = (uint32_t)((sqrtf(8.0f * (float)idx + 1.0f) - 1.0f) * 0.5f);
+            while ((a + 1) * (a + 2) / 2 <= idx) ++a;
+            while (a * (a + 1) / 2 > idx) --a;
+            const uint32_t b = idx - a * (a + 1) / 2;
+            const uint32_t ie = steps - a, id = a - b, ia = b;      // table indices of p_E, p_D, p_A
+            const uint64_t capA = s_capAD[ia], capD = s_capAD[id], capE = s_capE[ie];
+            const uint64_t nA = capA < N ? capA : N;                 // Eq. 5
+            const uint64_t r1 = N - nA;
+            const uint64_t nD = capD < r1 ? capD : r1;               // Eq. 6
+            const uint64_t r2 = r1 - nD;
+            const uint64_t nE = capE < r2 ? capE : r2;               // Eq. 7
+            const uint64_t nS = r2 - nE;                             // Eq. 8
+            const double tA = s_tA[ia];
+            const double tD = (nD == capD) ? s_tD[id] : __dmul_rn(__ddiv_rn(u2d(nD), dN), dsiD);
+            const double tE = (nE == capE) ? s_tE[ie] : __dmul_rn(__ddiv_rn(u2d(nE), dN), dsiE);
+            const double tS = __dmul_rn(__ddiv_rn(u2d(nS), dN), dsiS);
+            const double v = __dadd_rn(__dadd_rn(__dadd_rn(tA, tD), tE), tS);   // Eq. 9, R-M7
+            if (grow) __stcs(grow + idx, v);
+            if (v > best) { best = v; best_i = idx; }               // idx increases per thread
+        }
+        // block argmax: larger v, then smaller index
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+            const uint32_t oi = __shfl_xor_sync(0xffffffffu, best_i, o);
+            if (ov > best || (ov == best && oi < best_i)) { best = ov; best_i = oi; }
+        }
+        if ((threadIdx.x & 31) == 0) { s_rv[threadIdx.x >> 5] = best; s_ri[threadIdx.x >> 5] = best_i; }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < kThreads / 32; ++w)
+                if (s_rv[w] > best || (s_rv[w] == best && s_ri[w] < best_i)) { best = s_rv[w]; best_i = s_ri[w]; }
+            uint32_t a = 0;
+            while ((a + 1) * (a + 2) / 2 <= best_i) ++a;
+            const uint32_t b = best_i - a * (a + 1) / 2;
+            seneca_mdp_result r;
+            r.p_e = (uint8_t)(100 - a * g);
+            r.p_d = (uint8_t)((a - b) * g);
+            r.p_a = (uint8_t)(b * g);
+            r.lim_a = s_lim[0]; r.lim_d = s_lim[1]; r.lim_e = s_lim[2]; r.lim_s = s_lim[3];
+            r.status = 0;
+            r.v_best = best;
+            r.dsi_a = s_dsi[0]; r.dsi_d = s_dsi[1]; r.dsi_e = s_dsi[2]; r.dsi_s = s_dsi[3];
+            results[pi] = r;
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace
+}  // namespace seneca
+
+extern "C" uint64_t seneca_mdp_num_splits(uint32_t g) {
+    if (g == 0 || g > 100 || 100 % g) return 0;
+    const uint64_t s = 100 / g;
+    return (s + 1) * (s + 2) / 2;
+}
+
+extern "C" seneca_status seneca_mdp_sweep(const seneca_mdp_profile* d_profiles, uint32_t n_profiles,
+                                          uint32_t grid_step_pct, seneca_mdp_result* d_results,
+                                          double* d_grid, void* stream) {
+    using namespace seneca;
+    if (grid_step_pct == 0 || grid_step_pct > 100 || 100 % grid_step_pct) {
+        set_error("seneca_mdp_sweep: grid_step_pct %u does not divide 100", grid_step_pct);
+        return SENECA_EINVAL;
+    }
+    if (n_profiles == 0 || !d_profiles || !d_results) {
+        set_error("seneca_mdp_sweep: empty input or NULL pointer");
+        return SENECA_EINVAL;
+    }
+    const uint32_t steps = 100 / grid_step_pct;
+    const uint32_t ns = (uint32_t)seneca_mdp_num_splits(grid_step_pct);
+    const uint32_t blocks = n_profiles < 65535u * 8u ? n_profiles : 65535u * 8u;
+    mdp_sweep_kernel<<<blocks, kThreads, 0, (cudaStream_t)stream>>>(d_profiles, n_profiles, grid_step_pct,
+                                                                   steps, ns, d_results, d_grid);
+    SENECA_CUDA_TRY(cudaGetLastError());
+    return SENECA_OK;
+}

@@ -1,0 +1,97 @@
+"""CPU checks of the boundary: libseneca.so loads, exports every function that
+include/seneca.h declares, and its host-only helpers agree with the oracle.
+No device compute is called here."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import oracle as O
+import synth
+from paper_2511_13724_b200 import seneca as S
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions():
+    src = open(os.path.join(ROOT, "include", "seneca.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(seneca_[a-z_0-9]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2511_13724_b200 import build
+    build.build()
+    return S.lib()
+
+
+def test_every_declared_symbol_is_exported(lib):
+    names = declared_functions()
+    assert len(names) >= 14
+    for n in names:
+        assert hasattr(lib, n), n
+    assert sorted(S.EXPORTED) == names
+
+
+def test_struct_sizes_match_header(lib):
+    assert S.PROFILE_DTYPE.itemsize == 112
+    assert S.RESULT_DTYPE.itemsize == 48
+    assert S.STATS_DTYPE.itemsize == 104
+
+
+def test_metadata_bytes_paper_pin(lib):
+    assert S.metadata_bytes(1_300_000, 8) == 2_600_000
+    assert S.metadata_bytes(8, 1) == 9
+
+
+def test_split_capacities_match_oracle(lib):
+    st = synth.Stream(21)
+    for _ in range(300):
+        n = int(st.u64(1)[0] % 10**8) + 1
+        s = int(st.u64(1)[0] % 10**6) + 1
+        cache = int(st.u64(1)[0] % 10**13)
+        a = int(st.u64(1)[0] % 101); b = int(st.u64(1)[0] % (101 - a)); e = 100 - a - b
+        caps = S.split_capacities(n, s, 128, 25, cache, e, b, a)
+        p = O.make_profile(t_gpu=1, t_decode_augment=1, t_augment=1, b_nic=1, b_pcie=1, b_cache=1,
+                           b_storage=1, cache_bytes=cache, n_total=n, s_data=s, m_num=128, m_den=25,
+                           nodes=1, gpus_per_node=1)
+        na, nd, ne, ns = O.split_counts(p, e, b, a)
+        assert caps == [ne, nd, na, ns]
+
+
+def test_config_capacities(lib):
+    for name, want in [("toy", (80, 11, 11)), ("imagenet1k", (0, 42_038, 45_541)),
+                       ("openimages", (658_561, 118_731, 0)), ("imagenet22k", (4_376_846, 0, 0))]:
+        c = synth.ods_config(name)
+        caps = S.split_capacities(c["n_total"], c["s_data"], c["m_num"], c["m_den"], c["cache_bytes"], *c["split"])
+        assert tuple(caps[:3]) == want
+
+
+def test_invalid_arguments_rejected_on_host(lib):
+    with pytest.raises(S.SenecaError) as ei:
+        S.split_capacities(10, 10, 128, 25, 10**9, 50, 50, 1)
+    assert ei.value.status == S.EINVAL
+    with pytest.raises(S.SenecaError) as ei:
+        S.mdp_sweep(1, 1, 7, 1, None, 0)                    # 7 does not divide 100
+    assert ei.value.status == S.EINVAL
+    assert S.mdp_num_splits(1) == 5151 and S.mdp_num_splits(10) == 66 and S.mdp_num_splits(7) == 0
+    bad = [dict(n_total=0), dict(n_total=2**31), dict(batch=[0]), dict(batch=[5000]),
+           dict(cap_e=600, cap_d=600), dict(target=[0])]
+    for over in bad:
+        kw = dict(n_total=1000, batch=[32], target=[1], cap_e=10, cap_d=10, cap_a=10, seed=1)
+        kw.update(over)
+        cfg = S.make_config(kw["n_total"], kw["batch"], kw["target"], kw["cap_e"], kw["cap_d"],
+                            kw["cap_a"], kw["seed"])
+        with pytest.raises(S.SenecaError):
+            S.state_bytes(cfg)
+
+
+def test_state_bytes_scale(lib):
+    c = synth.ods_config("imagenet22k")
+    caps = S.split_capacities(c["n_total"], c["s_data"], c["m_num"], c["m_den"], c["cache_bytes"], *c["split"])
+    cfg = S.make_config(c["n_total"], c["batch"], c["target"], caps[0], caps[1], caps[2], 1)
+    nbytes = S.state_bytes(cfg)
+    # 3 + 2J bitmaps (R-O14) + 3 permutation/lap lists per job dominate; fits easily in 180 GB
+    assert 1.3e9 < nbytes < 2e9

@@ -1,0 +1,145 @@
+"""GPU parity: seneca_mdp_sweep (C-ABI) vs the oracle, bit-exact.
+
+north_star tolerance for FP64 throughputs is 1e-9 relative; the kernel is
+bit-identical by construction (explicit round-to-nearest ops in the oracle's
+order, R-M7), so every value is compared with ==.  Argmax splits and limiting
+factors are exact integers."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2511_13724_b200 as P  # noqa: E402
+from paper_2511_13724_b200 import seneca as S  # noqa: E402
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "table4_nominal_vals.json")))
+
+
+def to_dev_rows(oracle_rows):
+    """The two sides define their profile structs independently; convert by field name."""
+    out = np.zeros(len(oracle_rows), S.PROFILE_DTYPE)
+    for f in O.PROFILE_FIELDS:
+        out[f] = oracle_rows[f]
+    return out
+
+
+def run_gpu(rows, g, grid=True):
+    d_res, d_grid = P.mdp_sweep_device(to_dev_rows(rows), g, want_grid=grid)
+    torch.cuda.synchronize()
+    res = P.results_to_numpy(d_res)
+    return res, (d_grid.cpu().numpy() if grid else None)
+
+
+def assert_same(res, ores, grid=None, ogrid=None):
+    assert np.all(res["status"] == 0)
+    for a, b in [("p_e", "p_e"), ("p_d", "p_d"), ("p_a", "p_a"), ("lim_a", "lim_a"), ("lim_d", "lim_d"),
+                 ("lim_e", "lim_e"), ("lim_s", "lim_s")]:
+        np.testing.assert_array_equal(res[a], ores[b], err_msg=a)
+    for a, b in [("v_best", "v"), ("dsi_a", "dsi_a"), ("dsi_d", "dsi_d"), ("dsi_e", "dsi_e"), ("dsi_s", "dsi_s")]:
+        assert np.array_equal(res[a].view(np.uint64), ores[b].view(np.uint64)), a      # bit-exact
+    if grid is not None:
+        assert np.array_equal(grid.view(np.uint64), ogrid.view(np.uint64))
+
+
+def table4_rows():
+    rows = []
+    for server in ("in_house", "aws", "azure"):
+        g = {k: v for k, v in GOLD[server].items() if not k.startswith("_")}
+        for ds in ("imagenet1k", "openimages", "imagenet22k"):
+            for nodes in (1, 2):
+                for cache in (64, 115, 400):
+                    kw = dict(g, model_bytes=102.4e6, nodes=nodes, gpus_per_node=4, cache_bytes=cache * 10**9,
+                              **GOLD["datasets"][ds])
+                    rows.append(kw)
+    arr = np.zeros(len(rows), O.PROFILE_DTYPE)
+    for i, kw in enumerate(rows):
+        for k, v in kw.items():
+            arr[i][k] = v
+    return arr
+
+
+@pytest.mark.parametrize("g", [1, 2, 5, 10, 20, 25, 50, 100])
+def test_table4_profiles_all_grids(g):
+    rows = table4_rows()
+    ores, ogrid = O.mdp_sweep(rows, g, want_grid=True)
+    res, grid = run_gpu(rows, g)
+    assert_same(res, ores, grid, ogrid)
+
+
+def test_imagenet22k_azure_pin_on_device():
+    rows = table4_rows()
+    g = {k: v for k, v in GOLD["azure"].items() if not k.startswith("_")}
+    one = np.zeros(1, O.PROFILE_DTYPE)
+    for k, v in dict(g, model_bytes=0.0, nodes=1, gpus_per_node=1, n_total=14_000_000, s_data=91_390).items():
+        one[0][k] = v
+    res, _ = run_gpu(one, 1, grid=False)
+    assert (res[0]["p_e"], res[0]["p_d"], res[0]["p_a"]) == (100, 0, 0)
+    assert res[0]["v_best"] == 3088.051099033303
+
+
+def test_synthetic_10k_profiles_1pct_full_grid():
+    """BASELINE.json configs[4]: 10,000 profiles x 5151 splits, every value."""
+    cols = synth.mdp_profiles(10_000, seed=synth.PERF_SEED)
+    rows = O.profiles_from_columns(cols)
+    ores, ogrid = O.mdp_sweep(rows, 1, want_grid=True)
+    res, grid = run_gpu(rows, 1)
+    assert_same(res, ores, grid, ogrid)
+
+
+@pytest.mark.parametrize("seed", synth.PARITY_SEEDS)
+def test_synthetic_profiles_toy_grid(seed):
+    cols = synth.mdp_profiles(3000, seed=seed)
+    rows = O.profiles_from_columns(cols)
+    for g in (10, 1):
+        ores, ogrid = O.mdp_sweep(rows, g, want_grid=True)
+        res, grid = run_gpu(rows, g)
+        assert_same(res, ores, grid, ogrid)
+
+
+def test_edge_profiles():
+    """Zero cache (all ties), tiny datasets (full fit everywhere), huge model (comm-bound),
+    both comm mappings, NVLink flags."""
+    cols = synth.mdp_profiles(600, seed=99)
+    rows = O.profiles_from_columns(cols)
+    rows["cache_bytes"][:100] = 0
+    rows["n_total"][100:200] = np.arange(1, 101)
+    rows["model_bytes"][200:300] = 5e11
+    rows["comm_mapping"][300:400] = 1
+    rows["nvlink_inter"][400:500] = 1
+    rows["cache_bytes"][500:600] = np.uint64(10**15)
+    for g in (1, 4):
+        ores, ogrid = O.mdp_sweep(rows, g, want_grid=True)
+        res, grid = run_gpu(rows, g)
+        assert_same(res, ores, grid, ogrid)
+
+
+def test_invalid_profiles_flagged():
+    cols = synth.mdp_profiles(8, seed=3)
+    rows = to_dev_rows(O.profiles_from_columns(cols))
+    rows["t_gpu"][0] = 0.0
+    rows["b_cache"][1] = np.inf
+    rows["n_total"][2] = 0
+    rows["m_num"][3] = 1              # M < 1
+    rows["cache_bytes"][4] = np.uint64(2**62)
+    rows["model_bytes"][5] = -1.0
+    d_res, _ = P.mdp_sweep_device(rows, 1)
+    res = P.results_to_numpy(d_res)
+    assert list(res["status"]) == [1, 1, 1, 1, 1, 1, 0, 0]
+
+
+def test_results_without_grid_match():
+    cols = synth.mdp_profiles(2000, seed=5)
+    rows = O.profiles_from_columns(cols)
+    ores, _ = O.mdp_sweep(rows, 1)
+    res, _ = run_gpu(rows, 1, grid=False)
+    assert_same(res, ores)

@@ -1,0 +1,239 @@
+"""GPU parity: the ODS replay through the C-ABI vs the oracle.
+
+Bit-exact for every decision: delivered id and source per position (transcript),
+residency / seen / consumer bitmaps, per job-epoch counters and digests,
+eviction and refill totals.  Sizes: the toy config and random tiny configs in
+full; N/64-scaled versions of every config in full; the full-size configs for a
+prefix of rounds (oracle one by one) and, where tests/golden holds the oracle's
+full replay (written by tests/golden/make_oracle_golden.py, oracle only), the
+whole replay."""
+import glob
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2511_13724_b200 as P  # noqa: E402
+from paper_2511_13724_b200 import seneca as S  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def caps_of(c):
+    caps = S.split_capacities(c["n_total"], c["s_data"], c["m_num"], c["m_den"], c["cache_bytes"], *c["split"])
+    return caps[0], caps[1], caps[2]
+
+
+def make_pair(n, batch, target, ce, cd, ca, seed, transcript=True):
+    o = O.ODS(n, batch, target, ce, cd, ca, seed, transcript=transcript)
+    g = P.ODSContext(n, batch, target, ce, cd, ca, seed)
+    return o, g
+
+
+def compare_state(o, g, check_transcript=None):
+    st_o, ev_o, rf_o = o.stats()
+    st_g, ev_g, rf_g = g.stats()
+    assert (ev_g, rf_g) == (ev_o, rf_o)
+    assert st_g.tobytes() == st_o.tobytes()
+    t_o, s_o, c_o = o.state()
+    t_g, s_g, c_g = g.state()
+    np.testing.assert_array_equal(t_g, t_o)
+    np.testing.assert_array_equal(s_g, s_o)
+    np.testing.assert_array_equal(c_g, c_o)
+    if check_transcript is not None:
+        tr_o = o.transcript()
+        tr_g = check_transcript.cpu().numpy().view(np.uint64)
+        if not np.array_equal(tr_g, tr_o):
+            j, e, q = np.argwhere(tr_g != tr_o)[0]
+            raise AssertionError(f"first transcript mismatch job {j} epoch {e} pos {q}: "
+                                 f"gpu {int(tr_g[j, e, q]):#x} oracle {int(tr_o[j, e, q]):#x}")
+    g.sync()
+
+
+def replay_pair(n, batch, target, ce, cd, ca, seed):
+    o, g = make_pair(n, batch, target, ce, cd, ca, seed)
+    tr = g.new_transcript()
+    r_g = g.replay_epochs(max(target), tr)
+    r_o = o.replay_epochs(max(target))
+    torch.cuda.synchronize()
+    assert r_g == r_o
+    compare_state(o, g, tr)
+    return o, g
+
+
+@pytest.mark.parametrize("seed", synth.PARITY_SEEDS)
+def test_toy_config(seed):
+    c = synth.ods_config("toy", seed=seed)
+    ce, cd, ca = caps_of(c)
+    assert (ce, cd, ca) == (80, 11, 11)
+    replay_pair(c["n_total"], c["batch"], c["target"], ce, cd, ca, seed)
+
+
+@pytest.mark.parametrize("block", range(6))
+def test_random_tiny_configs(block):
+    st = synth.Stream(5000 + block)
+    for _ in range(50):
+        c = synth.random_tiny_ods(st)
+        replay_pair(c["n_total"], c["batch"], c["target"], c["cap_e"], c["cap_d"], c["cap_a"], c["seed"])
+
+
+@pytest.mark.parametrize("name", ["imagenet1k", "openimages", "imagenet22k"])
+def test_scaled_configs_full_replay(name):
+    """N/64 with split 34-33-33: every tier populated, A churn, mixed batches (OI),
+    ragged tails, several superblocks."""
+    c = synth.ods_config(name, scale=64, seed=1)
+    ce, cd, ca = caps_of(c)
+    replay_pair(c["n_total"], c["batch"], c["target"], ce, cd, ca, 1)
+
+
+def test_ragged_and_edge_shapes():
+    cases = [
+        (1, [1], [3], 0, 0, 1),            # single sample
+        (33, [33], [2], 0, 0, 33),         # whole dataset in A, one batch per epoch
+        (1025, [1024, 7], [2, 3], 100, 100, 100),
+        (32768 + 5, [4096, 1000], [1, 2], 2000, 1000, 3000),   # superblock boundary, max batch
+        (5000, [17, 33, 64], [1, 1, 1], 0, 0, 0),               # no cache at all
+        (5000, [17, 33, 64], [2, 1, 1], 5000, 0, 0),            # everything encoded-cached
+    ]
+    for n, b, t, ce, cd, ca in cases:
+        replay_pair(n, b, t, ce, cd, ca, 7)
+
+
+@pytest.mark.parametrize("name,rounds", [("imagenet1k", 400), ("openimages", 300), ("imagenet22k", 120)])
+def test_full_size_prefix(name, rounds):
+    """Full-size configs, first rounds, in the launch configuration bench.py times."""
+    seed = synth.PERF_SEED
+    c = synth.ods_config(name, seed=seed)
+    ce, cd, ca = caps_of(c)
+    o, g = make_pair(c["n_total"], c["batch"], c["target"], ce, cd, ca, seed, transcript=False)
+    assert g.replay_rounds(rounds) == rounds
+    assert o.replay_rounds(rounds) == rounds
+    torch.cuda.synchronize()
+    compare_state(o, g)
+
+
+def _golden_files():
+    return sorted(glob.glob(os.path.join(HERE, "golden", "oracle_*_seed*.json")))
+
+
+@pytest.mark.parametrize("path", _golden_files(), ids=lambda p: os.path.basename(p))
+def test_full_replay_against_oracle_golden(path):
+    gold = json.load(open(path))
+    c = synth.ods_config(gold["config"].split("/")[0], seed=gold["seed"])
+    ce, cd, ca = caps_of(c)
+    assert [ce, cd, ca] == gold["caps"]
+    g = P.ODSContext(c["n_total"], c["batch"], c["target"], ce, cd, ca, gold["seed"])
+    rounds = g.replay_epochs(max(c["target"]))
+    torch.cuda.synchronize()
+    g.sync()
+    assert rounds == gold["rounds"]
+    st, ev, rf = g.stats()
+    assert (ev, rf) == (gold["evicted"], gold["refilled"])
+    for j, row in enumerate(gold["stats"]):
+        for e, s in enumerate(row):
+            assert [int(v) for v in st[j, e]["served"]] == s["served"]
+            assert [int(v) for v in st[j, e]["subst"]] == s["subst"]
+            assert [int(v) for v in st[j, e]["req_hits"]] == s["req_hits"]
+            assert int(st[j, e]["digest"]) == int(s["digest"])
+    tier, seen, cons = g.state()
+    h = hashlib.sha256()
+    h.update(tier.tobytes()); h.update(seen.tobytes()); h.update(cons.tobytes())
+    assert h.hexdigest() == gold["state_sha256"]
+
+
+def test_next_batch_subsets_of_jobs():
+    """seneca_ods_next_batch with changing job subsets (R-O11) vs oracle rounds."""
+    n, batch, target = 700, [16, 40, 9], [2, 2, 3]
+    o, g = make_pair(n, batch, target, 60, 50, 90, 11, transcript=False)
+    st = synth.Stream(77)
+    for _ in range(150):
+        _, _, _, act = o.job_state()
+        live = [j for j in range(3) if act[j]]
+        if not live:
+            break
+        pick = [j for j in live if st.uniform(1)[0] < 0.7] or live[:1]
+        rc, ids_o, src_o, lens_o = o.round(pick)
+        assert rc == 0
+        ids_g, src_g, lens_g = g.next_batch(pick)
+        torch.cuda.synchronize()
+        assert list(lens_o) == lens_g
+        for x, L_ in enumerate(lens_g):
+            assert np.array_equal(ids_g[x, :L_].cpu().numpy().view(np.uint32), ids_o[x, :L_])
+            assert np.array_equal(src_g[x, :L_].cpu().numpy(), src_o[x, :L_])
+    compare_state(o, g)
+
+
+def test_caller_supplied_requests():
+    """request_mode 1 (R-O20): ids chosen by the caller; the SPEC request_batch path."""
+    n, batch, target = 400, [12, 20], [2, 2]
+    o = O.ODS(n, batch, target, 40, 30, 50, 5)
+    g = P.ODSContext(n, batch, target, 40, 30, 50, 5, request_mode=1)
+    st = synth.Stream(8)
+    for _ in range(80):
+        _, _, _, act = o.job_state()
+        live = [j for j in range(2) if act[j]]
+        if not live:
+            break
+        _, seen, _ = o.state()
+        reqs = []
+        for j in live:
+            unseen = np.flatnonzero(seen[j] == 0)
+            need = o.need(j)
+            order = np.argsort(st.u64(len(unseen)))
+            reqs.append([int(v) for v in unseen[order[:need]]])
+        rc, ids_o, src_o, lens_o = o.round(live, requested=reqs)
+        assert rc == 0
+        ids_g, src_g, lens_g = g.next_batch(live, requested=reqs)
+        torch.cuda.synchronize()
+        for x, L_ in enumerate(lens_g):
+            assert np.array_equal(ids_g[x, :L_].cpu().numpy().view(np.uint32), ids_o[x, :L_])
+            assert np.array_equal(src_g[x, :L_].cpu().numpy(), src_o[x, :L_])
+    compare_state(o, g)
+
+
+def test_protocol_violations_and_state_errors():
+    g = P.ODSContext(100, [4, 4], [1, 1], 10, 10, 10, 3, request_mode=1)
+    with pytest.raises(S.SenecaError) as ei:
+        g.next_batch([0], requested=[[1, 1, 2, 3]])          # duplicate
+    assert ei.value.status == S.EPROTO
+    with pytest.raises(S.SenecaError) as ei:
+        g.next_batch([0], requested=[[1, 2, 3, 100]])        # out of range
+    assert ei.value.status == S.EPROTO
+    g.next_batch([0, 1], requested=[[1, 2, 3, 4], [1, 2, 3, 4]])   # two jobs may request the same ids
+    with pytest.raises(S.SenecaError) as ei:
+        g.next_batch([0], requested=[[4, 5, 6, 7]])          # 4 already seen by job 0
+    assert ei.value.status == S.EPROTO
+    with pytest.raises(S.SenecaError) as ei:
+        g.next_batch([0, 0], requested=[[5, 6, 7, 8], [9, 10, 11, 12]])
+    assert ei.value.status == S.EINVAL
+    h = P.ODSContext(8, [8, 4], [1, 2], 0, 0, 2, 3)
+    h.next_batch([0, 1])
+    with pytest.raises(S.SenecaError) as ei:
+        h.next_batch([0])                                    # job 0 departed
+    assert ei.value.status == S.ESTATE
+    g.sync()
+    h.sync()
+
+
+def test_determinism_and_launch_count():
+    c = synth.ods_config("imagenet1k", scale=64, seed=2)
+    ce, cd, ca = caps_of(c)
+    outs = []
+    for _ in range(2):
+        g = P.ODSContext(c["n_total"], c["batch"], c["target"], ce, cd, ca, 2)
+        g.replay_epochs(2)
+        torch.cuda.synchronize()
+        outs.append(g.stats()[0].tobytes())
+        assert g.launches() > 0
+    assert outs[0] == outs[1]
