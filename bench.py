@@ -1,0 +1,461 @@
+#!/usr/bin/env python3
+"""Benchmark of Seneca's hot path on B200 (BASELINE.json metric:
+"ODS sample decisions/sec & MDP split evals/sec (1/2/4/8 B200), % of HBM roofline").
+
+A step = one pass of the whole hot path over one
+batch of synthetic input:
+  * ODS: init_cache + the full trace-driven replay of the workload (default
+    BASELINE configs[1], the ImageNet-1K-shaped trace: 1,281,167 samples, 4 jobs
+    x 256, cache 35 % at split 0-48-52, 10 epochs = 50,050 rounds,
+    51.25 M sample decisions) -- the headline `value` (decisions/s);
+  * MDP: the sweep over 10,000 synthetic hardware profiles x 5,151 splits (1 %
+    grid, configs[4]) with the full grid written to HBM -- reported in `mdp`.
+
+    python bench.py [--gpus N --steps K --warmup W] [--workload imagenet1k]
+    python bench.py --impl reference      # the oracle (CPU) as the reference arm
+
+N > 1 (torchrun, one process per GPU): every rank replays its own instance
+(seed + rank) and sweeps its own 10,000 profiles -- the path partitions into
+independent problems, so there is no data-path collective (weak scaling).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "ODS sample decisions/sec & MDP split evals/sec (1/2/4/8 B200), % of HBM roofline"
+WORKLOADS = {
+    "imagenet1k": "ImageNet-1K-shaped trace (BASELINE configs[1])",
+    "openimages": "OpenImages-shaped trace (BASELINE configs[2])",
+    "imagenet22k": "ImageNet-22K-shaped trace (BASELINE configs[3], one GPU)",
+    "toy": "toy trace (BASELINE configs[0])",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="imagenet1k", choices=sorted(WORKLOADS))
+    ap.add_argument("--mdp-profiles", type=int, default=10_000)
+    ap.add_argument("--mdp-grid-step", type=int, default=1)
+    ap.add_argument("--no-grid", action="store_true", help="MDP argmax only (no grid write)")
+    ap.add_argument("--profile-every", type=int, default=64, help="sample kernel timings every k rounds")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample duration")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def caps_of(c):
+    from paper_2511_13724_b200 import seneca as S
+    caps = S.split_capacities(c["n_total"], c["s_data"], c["m_num"], c["m_den"], c["cache_bytes"], *c["split"])
+    return caps[0], caps[1], caps[2]
+
+
+def decisions_of(c):
+    return sum(c["n_total"] * e for e in c["target"])
+
+
+def workload_config(c, name, extra):
+    return dict(workload=f"{name}: {WORKLOADS[name]}", n_total=c["n_total"], jobs=len(c["batch"]),
+                batch=c["batch"] if len(set(c["batch"])) > 1 else c["batch"][0],
+                epochs=c["target"][0], split="-".join(map(str, c["split"])), seed=hex(c["seed"]), **extra)
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if not self.proc:
+            return dict(sm_mhz=None, sm_max_mhz=None, reasons=["nvidia-smi unavailable"], samples=0)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = self.rows
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[3 + k].lower() == "active"})
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(r[0]) for r in rows if num(r[0]) is not None]
+        mx = [num(r[1]) for r in rows if num(r[1]) is not None]
+        return dict(sm_mhz=float(np.median(sm)) if sm else None, sm_max_mhz=max(mx) if mx else None,
+                    reasons=reasons, samples=len(rows))
+
+
+# --------------------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    """The oracle (plain single-threaded C, oracle/) timed on the host cores, as it
+    stands, on the same workload: each step replays a bounded prefix of rounds."""
+    if rank != 0:
+        return 0
+    import oracle as O
+    c = synth.ods_config(args.workload, seed=synth.PERF_SEED)
+    ce, cd, ca = caps_of(c)
+    rounds_per_step = {"toy": 96, "imagenet1k": 800, "openimages": 500, "imagenet22k": 40}[args.workload]
+    decisions = 0
+    t_tot = 0.0
+    for s in range(args.warmup + args.steps):
+        o = O.ODS(c["n_total"], c["batch"], c["target"], ce, cd, ca, c["seed"])
+        t0 = time.perf_counter()
+        done = o.replay_rounds(rounds_per_step)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            _, e, n, _ = o.job_state()
+            decisions += int(sum(int(e[j]) * c["n_total"] + int(n[j]) for j in range(len(c["batch"]))))
+            t_tot += dt
+    val = decisions / t_tot
+    sample = f"first {rounds_per_step} rounds of the {args.workload} replay per step (oracle, 1 thread)"
+    line = dict(metric=METRIC, value=val, unit="decisions/s", impl="reference", n_gpus=args.gpus,
+                steps=args.steps, warmup=args.warmup, ms_per_step=1e3 * t_tot / args.steps,
+                higher_is_better=True, scaling="weak", vs_baseline=None, dtype="u32", data="synthetic",
+                config=workload_config(c, args.workload, dict(note="reference arm = the CPU oracle")),
+                cpu_baseline=dict(value=val, unit="decisions/s", cores=1, kind="oracle", sample=sample),
+                e2e=dict(value=val, unit="decisions/s", h2d_bytes_per_step=0, d2h_bytes_per_step=0))
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------- cpu baseline
+def cpu_baseline(args, c, caps):
+    import oracle as O
+    ce, cd, ca = caps
+    # calibrate: a short run, then scale to ~args.cpu_seconds
+    o = O.ODS(c["n_total"], c["batch"], c["target"], ce, cd, ca, c["seed"])
+    t0 = time.perf_counter()
+    o.replay_rounds(50)
+    per = (time.perf_counter() - t0) / 50
+    rounds = max(50, int(args.cpu_seconds / max(per, 1e-6)))
+    o = O.ODS(c["n_total"], c["batch"], c["target"], ce, cd, ca, c["seed"])
+    t0 = time.perf_counter()
+    done = o.replay_rounds(rounds)
+    dt = time.perf_counter() - t0
+    _, e, n, _ = o.job_state()
+    dec = int(sum(int(e[j]) * c["n_total"] + int(n[j]) for j in range(len(c["batch"]))))
+    # MDP oracle on a profile sample
+    rows = O.profiles_from_columns(synth.mdp_profiles(1000, seed=synth.PERF_SEED))
+    t1 = time.perf_counter()
+    O.mdp_sweep(rows, args.mdp_grid_step, want_grid=False)
+    dm = time.perf_counter() - t1
+    ns = O.num_splits(args.mdp_grid_step)
+    return dict(value=dec / dt, unit="decisions/s", cores=1, kind="oracle",
+                sample=f"oracle replay of the first {done} rounds ({dec} decisions, {dt:.1f} s) of the same "
+                       f"workload; MDP oracle 1,000 profiles x {ns} splits in {dm:.2f} s",
+                mdp_value=1000 * ns / dm, mdp_unit="split-evals/s")
+
+
+# --------------------------------------------------------------------------- roofline models
+def algorithmic_bytes(name, info):
+    """Algorithmic (logical) bytes one launch of `name` must move, DESIGN.md §7.
+    info: per-step workload facts (rounds, decisions, substitutes, bitmap words...)."""
+    W4 = info["words"] * 4                          # bytes of one bitmap
+    if name == "mdp_sweep":
+        return info["mdp_profiles"] * (112 + 48) + (8 * info["mdp_profiles"] * info["mdp_splits"]
+                                                   if info["mdp_grid"] else 0)
+    if name == "ods_request_classify":
+        # per requested sample: list entry 4 + seen word 4 + 3 residency words 12 + consumer word 4
+        # + seen RMW 8 + id/src out 5 + request/miss index 8 = 45 B
+        return 45 * info["decisions"] / info["rounds"]
+    if name == "ods_select_apply":
+        # per substitute: block-count row 128 + pool words (2-3 bitmaps x 128 B, take 3) 384 + seen/consumer
+        # RMW 8 + count updates 16 + out 5 = 541 B; per CTA the superblock counts 4 x NS
+        subs = info["substitutes"] / info["rounds"]
+        return 541 * subs + 3 * info["jobs"] * 4 * info["superblocks"]
+    if name == "ods_maintain":
+        # per A-served candidate: id/src 5 + J consumer words 4J; per refill: pool words 128 x 3 + count row
+        # 128 + bitmap RMW 8 + J seen words 4J
+        cand = info["a_served"] / info["rounds"]
+        ref = info["refilled"] / info["rounds"]
+        return cand * (5 + 4 * info["jobs"]) + ref * (384 + 128 + 8 + 4 * info["jobs"])
+    if name == "ods_recount":
+        # per recounted job: residency x3 + seen + consumers = 5 bitmaps read; counts written
+        return info["jobs"] * (5 * W4 + 12 * info["blocks"])
+    if name == "ods_perm_fill":
+        return 4 * info["n_total"]                  # ALU-bound (Philox); bytes = the permutation written
+    if name == "ods_init_tiers":
+        return 4 * info["cache_entries"]
+    return 0
+
+
+def roofline_for(name, k, info, hbm_peak, peak_src, traffic=None):
+    bpl = algorithmic_bytes(name, info)
+    avg_s = (k["avg_us"] or 0.0) / 1e6
+    ach = bpl / avg_s / 1e9 if avg_s > 0 else 0.0
+    return dict(kernel=name, bound="hbm", achieved=ach, peak=hbm_peak, unit="GB/s",
+                frac=ach / hbm_peak, traffic=traffic, bytes_per_launch=bpl, avg_launch_us=k["avg_us"],
+                peak_source=peak_src)
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import paper_2511_13724_b200 as P
+    from paper_2511_13724_b200 import seneca as S
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    c = synth.ods_config(args.workload, seed=synth.PERF_SEED + rank)
+    caps = caps_of(c)
+    ce, cd, ca = caps
+    dec_per_step = decisions_of(c)
+
+    # ---- inputs resident in HBM before timing
+    mdp_cols = synth.mdp_profiles(args.mdp_profiles, seed=synth.PERF_SEED + rank)
+    prof_host = S.profiles_from_columns(mdp_cols)
+    d_prof = torch.from_numpy(prof_host.view(np.uint8).copy()).to(dev)
+    nsplit = S.mdp_num_splits(args.mdp_grid_step)
+    d_res = torch.empty(args.mdp_profiles * S.RESULT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+    d_grid = None if args.no_grid else torch.empty((args.mdp_profiles, nsplit), dtype=torch.float64, device=dev)
+    cfg = S.make_config(c["n_total"], c["batch"], c["target"], ce, cd, ca, c["seed"])
+    ws_bytes = S.state_bytes(cfg)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)      # > 126 MB L2
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    def one_step(profile_every=0, timed=None):
+        ctx = S.init_cache(cfg, ws, ws_bytes, stream)
+        if profile_every:
+            S.profile(ctx, profile_every)
+        rounds = S.replay_epochs(ctx, max(c["target"]), None, stream)
+        if timed is not None:
+            timed[1].record(stream)
+        S.mdp_sweep(d_prof, args.mdp_profiles, args.mdp_grid_step, d_res, d_grid, stream)
+        return ctx, rounds
+
+    # ---- warm-up
+    for _ in range(max(args.warmup, 0)):
+        ctx, _ = one_step()
+        torch.cuda.synchronize(dev)
+        S.destroy(ctx)
+
+    # ---- timed steps (device time, CUDA events on the launch stream)
+    clocks = ClockSampler(local)
+    clocks.start()
+    ods_ms, mdp_ms, launches, rounds_tot = [], [], 0, 0
+    kstats = {}
+    last_ctx = None
+    for s in range(args.steps):
+        flush.fill_(s & 0xFF)                                      # evict L2 between steps
+        barrier()
+        torch.cuda.synchronize(dev)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record(stream)
+        ctx, rounds = one_step(args.profile_every, (ev, ev[1]))
+        ev[2].record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+        ods_ms.append(ev[0].elapsed_time(ev[1]))
+        mdp_ms.append(ev[1].elapsed_time(ev[2]))
+        launches += S.launch_count(ctx) + 1
+        rounds_tot += rounds
+        for k, v in S.profile_read(ctx).items():
+            a = kstats.setdefault(k, dict(launches=0, sampled=0, sampled_ms=0.0))
+            for f in a:
+                a[f] += v[f]
+        if last_ctx:
+            S.destroy(last_ctx)
+        last_ctx = ctx
+    clk = clocks.stop()
+
+    # ---- parity gates (outside the timed region)
+    parity = {}
+    S.sync_status(last_ctx, stream)
+    gold_path = os.path.join(ROOT, "tests", "golden", f"oracle_{args.workload}_seed{c['seed']}.json")
+    st_raw = None
+    v = S.read_state(last_ctx)
+    off = v.d_stats - ws.data_ptr()
+    st_raw = ws[off:off + len(c["batch"]) * v.max_target * S.STATS_DTYPE.itemsize].cpu().numpy().view(S.STATS_DTYPE)
+    st_raw = st_raw.reshape(len(c["batch"]), v.max_target)
+    served_ok = bool(np.all(st_raw["served"].sum(axis=2) == c["n_total"]))
+    parity["ods_served_per_job_epoch_equals_N"] = served_ok
+    if os.path.exists(gold_path):
+        gold = json.load(open(gold_path))
+        ok = all(int(st_raw[j, e]["digest"]) == int(s_["digest"]) and
+                 [int(x) for x in st_raw[j, e]["served"]] == s_["served"]
+                 for j, row in enumerate(gold["stats"]) for e, s_ in enumerate(row))
+        parity["ods_vs_oracle_golden"] = "bit-exact" if ok else "MISMATCH"
+    else:
+        parity["ods_vs_oracle_golden"] = "no golden for this seed (rank>0 or not generated)"
+    try:
+        import oracle as O
+        k = min(200, args.mdp_profiles)
+        orow = O.profiles_from_columns({f: mdp_cols[f][:k] for f in mdp_cols})
+        ores, ogrid = O.mdp_sweep(orow, args.mdp_grid_step, want_grid=d_grid is not None)
+        res = d_res.cpu().numpy().view(S.RESULT_DTYPE)[:k]
+        ok = np.array_equal(res["v_best"].view(np.uint64), ores["v"].view(np.uint64)) and \
+            all(np.array_equal(res[f], ores[f]) for f in ("p_e", "p_d", "p_a"))
+        if d_grid is not None:
+            ok = ok and np.array_equal(d_grid[:k].cpu().numpy().view(np.uint64), ogrid.view(np.uint64))
+        parity["mdp_vs_oracle_first_200_profiles"] = "bit-exact" if ok else "MISMATCH"
+    except Exception as e:  # the oracle is only a checker; report, do not fall back
+        parity["mdp_vs_oracle_first_200_profiles"] = f"unchecked: {e}"
+
+    # ---- e2e through the public API with host buffers (pinned), copies inside
+    pin_prof = torch.from_numpy(prof_host.view(np.uint8).copy()).pin_memory()
+    pin_res = torch.empty(d_res.numel(), dtype=torch.uint8).pin_memory()
+    nst = len(c["batch"]) * v.max_target * S.STATS_DTYPE.itemsize
+    pin_stats = torch.empty(nst, dtype=torch.uint8).pin_memory()
+    e2e_ods, e2e_mdp = [], []
+    for s in range(args.steps):
+        flush.fill_(s & 0xFF)
+        barrier()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        ctx = S.init_cache(cfg, ws, ws_bytes, stream)
+        S.replay_epochs(ctx, max(c["target"]), None, stream)
+        vv = S.read_state(ctx)
+        o2 = vv.d_stats - ws.data_ptr()
+        pin_stats.copy_(ws[o2:o2 + nst], non_blocking=True)
+        torch.cuda.synchronize(dev)
+        t1 = time.perf_counter()
+        d_prof.copy_(pin_prof, non_blocking=True)
+        S.mdp_sweep(d_prof, args.mdp_profiles, args.mdp_grid_step, d_res, d_grid, stream)
+        pin_res.copy_(d_res, non_blocking=True)
+        torch.cuda.synchronize(dev)
+        t2 = time.perf_counter()
+        e2e_ods.append(t1 - t0)
+        e2e_mdp.append(t2 - t1)
+        S.destroy(ctx)
+
+    # ---- aggregate over ranks (max time)
+    ods_s = sum(ods_ms) / 1e3
+    mdp_s = sum(mdp_ms) / 1e3
+    e2e_s = sum(e2e_ods)
+    e2e_m = sum(e2e_mdp)
+    if world > 1:
+        t = torch.tensor([ods_s, mdp_s, e2e_s, e2e_m], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ods_s, mdp_s, e2e_s, e2e_m = t.tolist()
+    total_dec = dec_per_step * args.steps * world
+    total_evals = args.mdp_profiles * nsplit * args.steps * world
+
+    # ---- roofline of the dominant kernel (sampled CUDA-event durations)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        pass
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    peak_src = "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"
+    kernels = {}
+    for name, kv in kstats.items():
+        if kv["launches"] == 0:
+            continue
+        avg = kv["sampled_ms"] / kv["sampled"] if kv["sampled"] else None
+        kernels[name] = dict(launches_per_step=kv["launches"] / args.steps,
+                             avg_us=None if avg is None else 1e3 * avg,
+                             est_ms_per_step=None if avg is None else avg * kv["launches"] / args.steps)
+    mdp_ms_step = mdp_s * 1e3 / args.steps
+    kernels["mdp_sweep"] = dict(launches_per_step=1, avg_us=1e3 * mdp_ms_step, est_ms_per_step=mdp_ms_step)
+    dom = max(kernels, key=lambda k: kernels[k]["est_ms_per_step"] or 0.0)
+    info = dict(words=v.words, blocks=(c["n_total"] + 1023) // 1024,
+                superblocks=(c["n_total"] + 32767) // 32768, jobs=len(c["batch"]), n_total=c["n_total"],
+                rounds=rounds_tot / args.steps, decisions=dec_per_step,
+                substitutes=int(st_raw["subst"].sum()), a_served=int(st_raw["served"][:, :, 3].sum()),
+                refilled=int(ws[v.d_refilled - ws.data_ptr():v.d_refilled - ws.data_ptr() + 8].cpu().numpy().view(np.uint64)[0]),
+                cache_entries=ce + cd + ca, mdp_profiles=args.mdp_profiles, mdp_splits=nsplit,
+                mdp_grid=d_grid is not None)
+    roof = roofline_for(dom, kernels[dom], info, hbm_peak, peak_src)
+    mdp_roof = roofline_for("mdp_sweep", kernels["mdp_sweep"], info, hbm_peak, peak_src)
+    for name in kernels:
+        kernels[name]["algorithmic_bytes_per_launch"] = algorithmic_bytes(name, info)
+
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline(args, synth.ods_config(args.workload, seed=synth.PERF_SEED), caps)
+        ms_per_step = 1e3 * (ods_s + mdp_s) / args.steps
+        line = dict(
+            metric=METRIC, value=total_dec / ods_s, unit="decisions/s", n_gpus=world, steps=args.steps,
+            warmup=args.warmup, ms_per_step=ms_per_step, higher_is_better=True, scaling="weak",
+            vs_baseline=None, dtype="u32", data="synthetic",
+            config=workload_config(c, args.workload, dict(
+                rounds_per_step=rounds_tot // args.steps, decisions_per_step=dec_per_step,
+                mdp_profiles=args.mdp_profiles, mdp_grid_step_pct=args.mdp_grid_step,
+                mdp_grid_written=d_grid is not None,
+                parallelism=f"{world} independent replays (seed+rank) + {world} MDP profile slices",
+                l2="flushed between timed steps (512 MiB write)")),
+            e2e=dict(value=total_dec / e2e_s, unit="decisions/s",
+                     h2d_bytes_per_step=int(pin_prof.numel()), d2h_bytes_per_step=int(nst + pin_res.numel()),
+                     mdp_value=total_evals / e2e_m, mdp_unit="split-evals/s",
+                     note="public API from Python: init_cache + replay_epochs + stats D2H; MDP profiles "
+                          "H2D from pinned memory + sweep + results D2H; host wall clock"),
+            roofline=roof,
+            mdp=dict(value=total_evals / mdp_s, unit="split-evals/s", dtype="f64", ms_per_step=mdp_ms_step,
+                     roofline=mdp_roof),
+            cpu_baseline=cpu,
+            clocks=clk,
+            gpu_launches=int(launches),
+            kernels=kernels,
+            parity=parity,
+        )
+        print(json.dumps(line), flush=True)
+    S.destroy(last_ctx)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

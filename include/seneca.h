@@ -222,6 +222,22 @@ seneca_status seneca_sync_status(seneca_ctx* ctx, void* stream);
 /* Number of kernel launches this context has issued (for gpu_launches).      */
 uint64_t seneca_launch_count(const seneca_ctx* ctx);
 
+/* Kernel timing, sampled: when enabled, the launches of every
+ * sample_every_rounds-th round (and every launch of the per-epoch kernels) are
+ * bracketed by CUDA events on the launch stream; seneca_profile_read resolves
+ * them (synchronising on pending events) and reports, per kernel class, the
+ * launch count, the number of timed launches and their summed duration.
+ * sample_every_rounds = 0 disables sampling (launch counts are always kept).  */
+typedef struct {
+    const char* name;      /* kernel name (static string)                       */
+    uint64_t launches;     /* launches issued                                   */
+    uint64_t sampled;      /* launches timed                                    */
+    double   sampled_ms;   /* summed event-measured duration of timed launches  */
+} seneca_kernel_stat;
+
+seneca_status seneca_profile(seneca_ctx* ctx, uint32_t sample_every_rounds);
+seneca_status seneca_profile_read(seneca_ctx* ctx, seneca_kernel_stat* out, uint32_t cap, uint32_t* n_classes);
+
 void        seneca_destroy(seneca_ctx* ctx);
 const char* seneca_last_error(void);
 

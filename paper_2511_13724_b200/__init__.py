@@ -96,6 +96,12 @@ class ODSContext:
     def launches(self):
         return seneca.launch_count(self.ctx)
 
+    def profile(self, sample_every_rounds: int):
+        seneca.profile(self.ctx, sample_every_rounds)
+
+    def profile_read(self) -> dict:
+        return seneca.profile_read(self.ctx)
+
     # -- readback
     def _slice(self, ptr, nbytes):
         off = ptr - self.ws.data_ptr()

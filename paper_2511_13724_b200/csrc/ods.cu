@@ -675,7 +675,48 @@ inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 // ===========================================================================
 using namespace seneca;
 
+namespace {
+enum KernelClass { K_REQUEST = 0, K_SELECT, K_MAINTAIN, K_RECOUNT, K_PERM, K_INIT, K_VALIDATE, K_NCLASS };
+const char* const kKernelNames[K_NCLASS] = {"ods_request_classify", "ods_select_apply", "ods_maintain",
+                                            "ods_recount", "ods_perm_fill", "ods_init_tiers",
+                                            "ods_validate_requests"};
+
+// Sampled kernel timing: CUDA events around the launches of every k-th round
+// (and around every launch of the rare classes), on the launch stream, kept in
+// a ring and resolved lazily so the host never waits on recent work.
+struct KernelProfiler {
+    struct Slot { cudaEvent_t a = nullptr, b = nullptr; int cls = -1; };
+    uint32_t every = 0;
+    std::vector<Slot> ring;
+    size_t head = 0;
+    uint64_t launches[K_NCLASS] = {};
+    uint64_t sampled[K_NCLASS] = {};
+    double ms[K_NCLASS] = {};
+
+    void resolve(Slot& s) {
+        if (s.cls < 0) return;
+        float t = 0.f;
+        cudaEventSynchronize(s.b);
+        if (cudaEventElapsedTime(&t, s.a, s.b) == cudaSuccess) { sampled[s.cls]++; ms[s.cls] += t; }
+        s.cls = -1;
+    }
+    Slot* acquire() {
+        if (ring.empty()) {
+            ring.resize(4096);
+            for (auto& s : ring) { cudaEventCreate(&s.a); cudaEventCreate(&s.b); }
+        }
+        Slot& s = ring[head];
+        head = (head + 1) % ring.size();
+        resolve(s);
+        return &s;
+    }
+    void flush() { for (auto& s : ring) resolve(s); }
+    ~KernelProfiler() { for (auto& s : ring) { if (s.a) cudaEventDestroy(s.a); if (s.b) cudaEventDestroy(s.b); } }
+};
+}  // namespace
+
 struct seneca_ctx {
+    KernelProfiler prof;
     Cfg C;
     Lay L;
     uint32_t mode;
@@ -804,6 +845,18 @@ int num_sms() {
     return g_num_sms;
 }
 
+template <class F>
+void timed_launch(seneca_ctx* c, int cls, bool sample, cudaStream_t st, F&& launch) {
+    c->launches++;
+    c->prof.launches[cls]++;
+    if (!sample || !c->prof.every) { launch(); return; }
+    auto* s = c->prof.acquire();
+    cudaEventRecord(s->a, st);
+    launch();
+    cudaEventRecord(s->b, st);
+    s->cls = cls;
+}
+
 seneca_status launch_recount(seneca_ctx* c, uint32_t jobs_mask, bool storage, cudaStream_t st) {
     const uint32_t ny = __builtin_popcount(jobs_mask) + (storage ? 1 : 0);
     if (!ny) return SENECA_OK;
@@ -814,8 +867,9 @@ seneca_status launch_recount(seneca_ctx* c, uint32_t jobs_mask, bool storage, cu
     }
     if (storage) SENECA_CUDA_TRY(cudaMemsetAsync(c->L.cnt_tot + 3 * c->C.J, 0, 4, st));
     dim3 grid(c->C.NS, ny);
-    ods_recount<<<grid, kRecountThreads, 0, st>>>(c->L, c->C, jobs_mask, storage ? 1u : 0u);
-    c->launches++;
+    timed_launch(c, K_RECOUNT, true, st, [&] {
+        ods_recount<<<grid, kRecountThreads, 0, st>>>(c->L, c->C, jobs_mask, storage ? 1u : 0u);
+    });
     SENECA_CUDA_TRY(cudaGetLastError());
     return SENECA_OK;
 }
@@ -824,8 +878,7 @@ seneca_status launch_perm_fill(seneca_ctx* c, uint32_t j, uint32_t epoch, cudaSt
     const uint32_t threads = 256;
     uint32_t blocks = (c->C.N + threads - 1) / threads;
     blocks = std::min<uint32_t>(blocks, (uint32_t)num_sms() * 8);
-    ods_perm_fill<<<blocks, threads, 0, st>>>(c->L, c->C, j, epoch);
-    c->launches++;
+    timed_launch(c, K_PERM, true, st, [&] { ods_perm_fill<<<blocks, threads, 0, st>>>(c->L, c->C, j, epoch); });
     SENECA_CUDA_TRY(cudaGetLastError());
     return SENECA_OK;
 }
@@ -861,8 +914,9 @@ seneca_status run_round(seneca_ctx* c, const uint32_t* jobs, uint32_t nj, const 
     P.full_scan = departing ? 1u : 0u;
 
     if (c->mode == 1) {
-        ods_validate_requests<<<nj, 256, (size_t)c->C.Bmax * 4, st>>>(c->L, c->C, P);
-        c->launches++;
+        timed_launch(c, K_VALIDATE, false, st, [&] {
+            ods_validate_requests<<<nj, 256, (size_t)c->C.Bmax * 4, st>>>(c->L, c->C, P);
+        });
         SENECA_CUDA_TRY(cudaGetLastError());
         uint32_t err = 0;
         SENECA_CUDA_TRY(cudaMemcpyAsync(&err, c->L.err, 4, cudaMemcpyDeviceToHost, st));
@@ -873,10 +927,16 @@ seneca_status run_round(seneca_ctx* c, const uint32_t* jobs, uint32_t nj, const 
             return SENECA_EPROTO;
         }
     }
-    ods_request_classify<<<nj, kReqThreads, c->req_smem, st>>>(c->L, c->C, P, c->mode);
-    ods_select_apply<<<nj * 3, kSelThreads, c->sel_smem, st>>>(c->L, c->C, P);
-    ods_maintain<<<1, kMaintThreads, c->maint_smem, st>>>(c->L, c->C, P);
-    c->launches += 3;
+    const bool sample = c->prof.every && (c->r % c->prof.every) == 0;
+    timed_launch(c, K_REQUEST, sample, st, [&] {
+        ods_request_classify<<<nj, kReqThreads, c->req_smem, st>>>(c->L, c->C, P, c->mode);
+    });
+    timed_launch(c, K_SELECT, sample, st, [&] {
+        ods_select_apply<<<nj * 3, kSelThreads, c->sel_smem, st>>>(c->L, c->C, P);
+    });
+    timed_launch(c, K_MAINTAIN, sample, st, [&] {
+        ods_maintain<<<1, kMaintThreads, c->maint_smem, st>>>(c->L, c->C, P);
+    });
     SENECA_CUDA_TRY(cudaGetLastError());
     // epoch ends (a8, R-O16): reset seen, rebuild the job's pool counts, next permutation
     if (ending) {
@@ -958,8 +1018,9 @@ extern "C" seneca_status seneca_init_cache(const seneca_cache_config* cfg, void*
     {
         const uint32_t total = (uint32_t)(cfg->cap_a + cfg->cap_d + cfg->cap_e);
         uint32_t blocks = std::max<uint32_t>(1, std::min<uint32_t>((total + 255) / 256, num_sms() * 8));
-        ods_init_tiers<<<blocks, 256, 0, st>>>(c->L, c->C, (uint32_t)cfg->cap_e, (uint32_t)cfg->cap_d);
-        c->launches++;
+        timed_launch(c, K_INIT, false, st, [&] {
+            ods_init_tiers<<<blocks, 256, 0, st>>>(c->L, c->C, (uint32_t)cfg->cap_e, (uint32_t)cfg->cap_d);
+        });
         INIT_TRY(cudaGetLastError());
     }
     s = launch_recount(c, c->active, true, st);
@@ -1069,5 +1130,25 @@ extern "C" seneca_status seneca_sync_status(seneca_ctx* c, void* stream) {
 }
 
 extern "C" uint64_t seneca_launch_count(const seneca_ctx* c) { return c ? c->launches : 0; }
+
+extern "C" seneca_status seneca_profile(seneca_ctx* c, uint32_t sample_every_rounds) {
+    if (!c) { set_error("bad arguments"); return SENECA_EINVAL; }
+    c->prof.every = sample_every_rounds;
+    return SENECA_OK;
+}
+
+extern "C" seneca_status seneca_profile_read(seneca_ctx* c, seneca_kernel_stat* out, uint32_t cap, uint32_t* n_out) {
+    if (!c || (!out && cap)) { set_error("bad arguments"); return SENECA_EINVAL; }
+    c->prof.flush();
+    const uint32_t n = std::min<uint32_t>(cap, K_NCLASS);
+    for (uint32_t k = 0; k < n; ++k) {
+        out[k].name = kKernelNames[k];
+        out[k].launches = c->prof.launches[k];
+        out[k].sampled = c->prof.sampled[k];
+        out[k].sampled_ms = c->prof.ms[k];
+    }
+    if (n_out) *n_out = K_NCLASS;
+    return SENECA_OK;
+}
 
 extern "C" void seneca_destroy(seneca_ctx* c) { delete c; }

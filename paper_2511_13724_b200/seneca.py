@@ -74,6 +74,11 @@ class StateView(C.Structure):
     ]
 
 
+class KernelStat(C.Structure):
+    _fields_ = [("name", C.c_char_p), ("launches", C.c_uint64), ("sampled", C.c_uint64),
+                ("sampled_ms", C.c_double)]
+
+
 PROFILE_DTYPE = np.dtype(MdpProfile)
 RESULT_DTYPE = np.dtype(MdpResult)
 STATS_DTYPE = np.dtype(JobEpochStats)
@@ -109,6 +114,9 @@ def lib() -> C.CDLL:
         L.seneca_read_state.argtypes = [vp, C.POINTER(StateView)]; L.seneca_read_state.restype = C.c_int
         L.seneca_sync_status.argtypes = [vp, vp]; L.seneca_sync_status.restype = C.c_int
         L.seneca_launch_count.argtypes = [vp]; L.seneca_launch_count.restype = u64
+        L.seneca_profile.argtypes = [vp, u32]; L.seneca_profile.restype = C.c_int
+        L.seneca_profile_read.argtypes = [vp, C.POINTER(KernelStat), u32, C.POINTER(u32)]
+        L.seneca_profile_read.restype = C.c_int
         L.seneca_destroy.argtypes = [vp]; L.seneca_destroy.restype = None
         L.seneca_last_error.argtypes = []; L.seneca_last_error.restype = C.c_char_p
         _lib = L
@@ -119,7 +127,7 @@ EXPORTED = ["seneca_mdp_num_splits", "seneca_mdp_sweep", "seneca_split_capacitie
             "seneca_metadata_bytes", "seneca_state_bytes", "seneca_init_cache",
             "seneca_ods_next_batch", "seneca_replay_epochs", "seneca_replay_rounds",
             "seneca_read_state", "seneca_sync_status", "seneca_launch_count", "seneca_destroy",
-            "seneca_last_error"]
+            "seneca_last_error", "seneca_profile", "seneca_profile_read"]
 
 
 def _check(status: int):
@@ -226,6 +234,18 @@ def sync_status(ctx: int, stream=None):
 
 def launch_count(ctx: int) -> int:
     return lib().seneca_launch_count(ctx)
+
+
+def profile(ctx: int, sample_every_rounds: int):
+    _check(lib().seneca_profile(ctx, sample_every_rounds))
+
+
+def profile_read(ctx: int) -> dict:
+    out = (KernelStat * 16)()
+    n = C.c_uint32()
+    _check(lib().seneca_profile_read(ctx, out, 16, C.byref(n)))
+    return {out[k].name.decode(): dict(launches=out[k].launches, sampled=out[k].sampled,
+                                       sampled_ms=out[k].sampled_ms) for k in range(min(n.value, 16))}
 
 
 def destroy(ctx: int):
