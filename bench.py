@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--mdp-profiles", type=int, default=10_000)
     ap.add_argument("--mdp-grid-step", type=int, default=1)
     ap.add_argument("--no-grid", action="store_true", help="MDP argmax only (no grid write)")
-    ap.add_argument("--profile-every", type=int, default=64, help="sample kernel timings every k rounds")
+    ap.add_argument("--no-profile", action="store_true", help="no CUDA-event kernel timing in the timed steps")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample duration")
     return ap.parse_args()
@@ -195,32 +195,28 @@ def cpu_baseline(args, c, caps):
 
 # --------------------------------------------------------------------------- roofline models
 def algorithmic_bytes(name, info):
-    """Algorithmic (logical) bytes one launch of `name` must move, DESIGN.md §7.
+    """Algorithmic (logical) bytes one launch of `name` must move.
     info: per-step workload facts (rounds, decisions, substitutes, bitmap words...)."""
     W4 = info["words"] * 4                          # bytes of one bitmap
+    J = info["jobs"]
     if name == "mdp_sweep":
         return info["mdp_profiles"] * (112 + 48) + (8 * info["mdp_profiles"] * info["mdp_splits"]
                                                    if info["mdp_grid"] else 0)
-    if name == "ods_request_classify":
+    if name == "ods_rounds":
         # per requested sample: list entry 4 + seen word 4 + 3 residency words 12 + consumer word 4
-        # + seen RMW 8 + id/src out 5 + request/miss index 8 = 45 B
-        return 45 * info["decisions"] / info["rounds"]
-    if name == "ods_select_apply":
-        # per substitute: block-count row 128 + pool words (2-3 bitmaps x 128 B, take 3) 384 + seen/consumer
-        # RMW 8 + count updates 16 + out 5 = 541 B; per CTA the superblock counts 4 x NS
-        subs = info["substitutes"] / info["rounds"]
-        return 541 * subs + 3 * info["jobs"] * 4 * info["superblocks"]
-    if name == "ods_maintain":
-        # per A-served candidate: id/src 5 + J consumer words 4J; per refill: pool words 128 x 3 + count row
-        # 128 + bitmap RMW 8 + J seen words 4J
-        cand = info["a_served"] / info["rounds"]
-        ref = info["refilled"] / info["rounds"]
-        return cand * (5 + 4 * info["jobs"]) + ref * (384 + 128 + 8 + 4 * info["jobs"])
-    if name == "ods_recount":
-        # per recounted job: residency x3 + seen + consumers = 5 bitmaps read; counts written
-        return info["jobs"] * (5 * W4 + 12 * info["blocks"])
-    if name == "ods_perm_fill":
-        return 4 * info["n_total"]                  # ALU-bound (Philox); bytes = the permutation written
+        #   + seen RMW 8 + id/src out 5 + digest/transcript-free stats 0 = 37 B
+        # per substitute: block-count row 128 + pool words (<= 3 bitmaps x 32 B) 96 + seen/consumer
+        #   RMW 16 + count updates 16 + out 5 = 261 B
+        # per A-served candidate: id 4 + residency 4 + J consumer words 4J
+        # per refill (selected): block-count row 128 + 3 x 32 B words + bitmap RMW 8 + count updates 16
+        #   + J seen words 4J
+        # per job-epoch: seen clear W4 + recount (residency x3 + consumers + seen) 5 W4
+        return (37 * info["decisions"] + 261 * info["substitutes"] + (8 + 4 * J) * info["a_served"]
+                + (248 + 4 * J) * info["refilled"] + 6 * W4 * info["job_epochs"])
+    if name == "ods_perm_all":
+        return 4 * info["n_total"] * info["job_epochs"]     # ALU-bound (Philox); bytes written
+    if name == "ods_recount_all":
+        return (3 * J + 1) * 5 * W4
     if name == "ods_init_tiers":
         return 4 * info["cache_entries"]
     return 0
@@ -273,10 +269,10 @@ def main():
         if world > 1:
             torch.distributed.barrier()
 
-    def one_step(profile_every=0, timed=None):
+    def one_step(profile=False, timed=None):
         ctx = S.init_cache(cfg, ws, ws_bytes, stream)
-        if profile_every:
-            S.profile(ctx, profile_every)
+        if profile:
+            S.profile(ctx, 1)
         rounds = S.replay_epochs(ctx, max(c["target"]), None, stream)
         if timed is not None:
             timed[1].record(stream)
@@ -301,7 +297,7 @@ def main():
         torch.cuda.synchronize(dev)
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         ev[0].record(stream)
-        ctx, rounds = one_step(args.profile_every, (ev, ev[1]))
+        ctx, rounds = one_step(not args.no_profile, (ev, ev[1]))
         ev[2].record(stream)
         torch.cuda.synchronize(dev)
         barrier()
@@ -328,6 +324,14 @@ def main():
     st_raw = ws[off:off + len(c["batch"]) * v.max_target * S.STATS_DTYPE.itemsize].cpu().numpy().view(S.STATS_DTYPE)
     st_raw = st_raw.reshape(len(c["batch"]), v.max_target)
     served_ok = bool(np.all(st_raw["served"].sum(axis=2) == c["n_total"]))
+    ph = ws[v.d_phase_cycles - ws.data_ptr():v.d_phase_cycles - ws.data_ptr() + 64].cpu().numpy().view(np.uint64)
+    ph_names = ["job_phase", "job_barrier1_wait", "walk_next", "job_barrier2_wait",
+                "maint_spec_refill", "maint_barrier1_wait", "maint_apply", "maint_barrier2_wait"]
+    phase_share = {}
+    for base in (0, 4):
+        tot = float(ph[base:base + 4].sum())
+        for k in range(4):
+            phase_share[ph_names[base + k]] = round(float(ph[base + k]) / tot, 4) if tot else None
     parity["ods_served_per_job_epoch_equals_N"] = served_ok
     if os.path.exists(gold_path):
         gold = json.load(open(gold_path))
@@ -415,6 +419,7 @@ def main():
                 substitutes=int(st_raw["subst"].sum()), a_served=int(st_raw["served"][:, :, 3].sum()),
                 refilled=int(ws[v.d_refilled - ws.data_ptr():v.d_refilled - ws.data_ptr() + 8].cpu().numpy().view(np.uint64)[0]),
                 cache_entries=ce + cd + ca, mdp_profiles=args.mdp_profiles, mdp_splits=nsplit,
+                job_epochs=sum(c["target"]),
                 mdp_grid=d_grid is not None)
     roof = roofline_for(dom, kernels[dom], info, hbm_peak, peak_src)
     mdp_roof = roofline_for("mdp_sweep", kernels["mdp_sweep"], info, hbm_peak, peak_src)
@@ -448,6 +453,7 @@ def main():
             clocks=clk,
             gpu_launches=int(launches),
             kernels=kernels,
+            ods_round_phase_share=phase_share,
             parity=parity,
         )
         print(json.dumps(line), flush=True)

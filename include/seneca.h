@@ -165,6 +165,9 @@ typedef struct {
     const seneca_job_epoch_stats* d_stats; /* [n_jobs][max_target]                        */
     const uint64_t* d_evicted;          /* total evictions                                 */
     const uint64_t* d_refilled;         /* total refills                                   */
+    const uint64_t* d_phase_cycles;     /* [8] per-phase SM cycles when profiling: job CTA 0
+                                           {job phase, barrier 1, walk, barrier 2}, maintain
+                                           CTA {speculative refill, barrier 1, apply, barrier 2} */
     uint64_t round;                     /* rounds executed                                 */
     uint64_t epoch[32];                 /* host mirror: current epoch of each job          */
     uint64_t consumed[32];              /* host mirror: samples consumed in current epoch  */
@@ -222,12 +225,13 @@ seneca_status seneca_sync_status(seneca_ctx* ctx, void* stream);
 /* Number of kernel launches this context has issued (for gpu_launches).      */
 uint64_t seneca_launch_count(const seneca_ctx* ctx);
 
-/* Kernel timing, sampled: when enabled, the launches of every
- * sample_every_rounds-th round (and every launch of the per-epoch kernels) are
- * bracketed by CUDA events on the launch stream; seneca_profile_read resolves
- * them (synchronising on pending events) and reports, per kernel class, the
- * launch count, the number of timed launches and their summed duration.
- * sample_every_rounds = 0 disables sampling (launch counts are always kept).  */
+/* Kernel timing: when enabled, every kernel launch of this context is
+ * bracketed by CUDA events on its launch stream and the host waits for the
+ * end event (launches become synchronous; the replay is one launch), and the
+ * round kernel accumulates per-phase SM cycles into d_phase_cycles of the state
+ * view.  seneca_profile_read reports, per kernel, launches issued, launches
+ * timed and their summed event-measured duration.  Launch counts are always
+ * kept.                                                                        */
 typedef struct {
     const char* name;      /* kernel name (static string)                       */
     uint64_t launches;     /* launches issued                                   */
@@ -235,7 +239,7 @@ typedef struct {
     double   sampled_ms;   /* summed event-measured duration of timed launches  */
 } seneca_kernel_stat;
 
-seneca_status seneca_profile(seneca_ctx* ctx, uint32_t sample_every_rounds);
+seneca_status seneca_profile(seneca_ctx* ctx, uint32_t enable);
 seneca_status seneca_profile_read(seneca_ctx* ctx, seneca_kernel_stat* out, uint32_t cap, uint32_t* n_classes);
 
 void        seneca_destroy(seneca_ctx* ctx);

@@ -96,8 +96,12 @@ class ODSContext:
     def launches(self):
         return seneca.launch_count(self.ctx)
 
-    def profile(self, sample_every_rounds: int):
-        seneca.profile(self.ctx, sample_every_rounds)
+    def profile(self, enable: int = 1):
+        seneca.profile(self.ctx, enable)
+
+    def phase_cycles(self):
+        v = self.view()
+        return self._slice(v.d_phase_cycles, 64).cpu().numpy().view(np.uint64).copy()
 
     def profile_read(self) -> dict:
         return seneca.profile_read(self.ctx)

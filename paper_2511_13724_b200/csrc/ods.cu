@@ -1,37 +1,42 @@
 // ods.cu -- Opportunistic Data Sampling replay on B200.
 //
 // §5.2 of the paper made concrete by readings R-O1..R-O20
-// (DESIGN.md §3).  One round = one batch for each listed job, then maintain:
+// (DESIGN.md §3).  A round is one batch for each listed job, then maintain.
 //
-//   ods_request_classify  <<<jobs, 1024>>>  a1-a3: walk the job's current lap
-//        list (its keyed permutation, then the lists of deferred misses) from
-//        the cursor, test seen bits, compact the first `need` unseen ids
-//        (ballot/scan), classify hits vs misses against the residency bitmaps and
-//        the job's consumer set, mark hits seen and update the pool counts; the
-//        number of substitutes per tier k_A, k_D, k_E follows from the pool sizes.
-//   ods_select_apply      <<<jobs x 3, 512>>>  a4-a6: one CTA per (job, tier):
-//        keyed ranks sigma(u) over the ascending pool, located through the
-//        superblock/block count hierarchy (superblock prefix in shared memory,
-//        then one 128-B row of block counts, then one 128-B row of bitmap words);
-//        the last CTA of a job finishes it: storage misses, deferral lists,
-//        counters, digest, transcript.
-//   ods_maintain          <<<1, 1024>>>  a7: eviction of A entries consumed by
-//        every active job, keyed refill from the storage pool, count updates.
-//   epoch end (a8): memset of seen_j, ods_recount (pool counts of the job),
-//        ods_perm_fill (the next epoch's permutation, whole-GPU, ALU-bound).
+// Execution:
+//   ods_perm_all      side stream, at init: every (job, epoch) permutation
+//                     pi_j,e(pos) = perm(key(seed, REQ, j, e), N, pos) (R-O3),
+//                     epoch-major, publishing a ready flag per (job, epoch).
+//   ods_rounds        ONE cooperative launch runs R rounds.  CTA x < J owns job
+//                     x; CTA J is the maintain CTA.  Per round:
+//       job CTAs      classify (a3) -> select (a4, a5) -> finish (a6, a8)
+//       maintain CTA  speculative refill selection from the round-start storage
+//                     pool (it cannot change before maintain)            [overlapped]
+//       -- barrier 1 --
+//       maintain CTA  eviction of A entries consumed by every active job, apply
+//                     evictions + refills (a7)
+//       job CTAs      walk of the NEXT round (a1, a2): it reads only the job's
+//                     own seen bitmap and lists                          [overlapped]
+//       -- barrier 2 --
+//   The barrier is a sense-reversing software barrier among the J+1 CTAs.
 //
-// Pool counts: for every pool (job x {A, D, E}, plus the storage pool) a count
-// per 1024-id block, per 32-block superblock and a total, kept exact
-// incrementally; a pool member is an id whose pool word bit is set:
+// Pool counts: for each pool (job x {A, D, E}, plus the storage pool S) a count
+// per 256-id block, per 32-block superblock and a total, kept exact
+// incrementally.  A pool member is an id whose pool word bit is set:
 //   A: tier_A & ~seen_j & ~cons_j    D: tier_D & ~seen_j    E: tier_E & ~seen_j
 //   S: ~(tier_E | tier_D | tier_A)   (R-O2, R-O8)
+// Selecting the rank-th member is a binary search over the superblock prefix
+// (shared memory), one 128-B row of block counts, one 32-B row per bitmap.
+//
+// Mutable state shared between CTAs of the persistent kernel is read with
+// ld.global.cg (L2, never a stale L1 line); the barrier is release/acquire.
 #include <algorithm>
 #include <cstdint>
-#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
 
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -42,74 +47,77 @@ namespace {
 constexpr uint32_t T_S = 0, T_E = 1, T_D = 2, T_A = 3, SUBST = 4;
 constexpr uint32_t kMaxJobs = 32;
 constexpr uint32_t kMaxBatch = 4096;
-constexpr uint32_t kReqThreads = 1024;
-constexpr uint32_t kSelThreads = 512;
-constexpr uint32_t kMaintThreads = 1024;
-constexpr uint32_t kRecountThreads = 1024;   // one warp per block, 32 blocks = one superblock
+constexpr uint32_t kThreads = 512;           // CTA size of the persistent kernel
+constexpr uint32_t kBlockShift = 8;          // 256 ids (8 words) per count block
+constexpr uint32_t kSuperShift = 13;         // 32 blocks = 8192 ids per superblock
+constexpr uint32_t kWordsPerBlock = 8;
+constexpr uint32_t kWalkPerThread = 8;       // list entries examined per thread per walk step
 
-struct JobDev {
-    uint32_t cur_buf;    // list being walked: 0 the permutation, 1/2 deferral lists
-    uint32_t nxt_buf;    // list receiving this lap's deferred misses
-    uint32_t cursor;     // position in the current list
+// ------------------------------------------------------------------ layouts
+struct JobDev {           // per-job persistent walk state (workspace)
+    uint32_t cur_buf;     // 0: this epoch's permutation; 1/2: deferral (lap) lists
+    uint32_t nxt_buf;     // lap list receiving this lap's deferred misses (1/2)
+    uint32_t cursor;      // position in the current list
     uint32_t cur_len;
     uint32_t nxt_len;
-    uint32_t wrap_slot;  // this round: first slot taken after a lap wrap (0 = no wrap)
-    uint32_t m;          // this round: misses
-    uint32_t k[3];       // this round: substitutes from A, D, E
-    uint32_t done;       // select CTAs finished (last one finishes the job)
-    uint32_t pad[5];
+    uint32_t recount;     // pools must be rebuilt before the next classify (epoch start)
+    uint32_t pad[2];
 };
-static_assert(sizeof(JobDev) == 64, "JobDev layout");
 
 struct Cfg {
-    uint32_t N, NW, NB, NS, NBp;  // samples, words/bitmap, blocks, superblocks, padded blocks
-    uint32_t J, Bmax, maxT;
-    uint32_t cap_a;
+    uint32_t N, NW, NB, NS, NBp;     // samples, words/bitmap, blocks, superblocks, padded blocks
+    uint32_t J, Bmax, maxT, cap_a;
     uint32_t pad;
     uint64_t seed;
+    uint32_t batch[kMaxJobs];
+    uint32_t target[kMaxJobs];
 };
 
 struct Lay {
-    uint32_t *bm_e, *bm_d, *bm_a;   // [NW]
-    uint32_t *seen, *cons;          // [J][NW]
-    uint32_t *evmark;               // [NW]
-    uint32_t *cnt_blk;              // [3J+1][NBp]
-    uint32_t *cnt_sup;              // [3J+1][NS]
-    uint32_t *cnt_tot;              // [3J+1]
-    uint32_t *a_size;               // [1]
-    uint32_t *lists;                // [J][3][N]
-    JobDev *jobs;                   // [J]
-    uint32_t *req;                  // [J][Bmax]
-    uint32_t *miss;                 // [J][Bmax]
-    uint32_t *out_ids;              // [J][Bmax] (replay scratch)
-    uint8_t *out_src;               // [J][Bmax]
-    uint32_t *evict_list;           // [max(cap_a,1)]
-    uint32_t *fill_list;            // [max(cap_a,1)]
-    seneca_job_epoch_stats *stats;  // [J][maxT]
+    uint32_t *bm_e, *bm_d, *bm_a;    // [NW]
+    uint32_t *seen, *cons;           // [J][NW]
+    uint32_t *evmark;                // [NW]
+    uint32_t *cnt_blk;               // [3J+1][NBp]
+    uint32_t *cnt_sup;               // [3J+1][NS]
+    uint32_t *cnt_tot;               // [3J+1]
+    uint32_t *a_size;                // [1]
+    uint32_t *perms;                 // [J][maxT][N]
+    uint32_t *laps;                  // [J][2][N]
+    uint32_t *perm_ready;            // [J][maxT]
+    uint32_t *perm_done;             // [J][maxT] positions finished
+    JobDev *jobs;                    // [J]
+    uint32_t *out_ids;               // [J][Bmax] replay scratch
+    uint8_t *out_src;                // [J][Bmax]
+    uint32_t *aserved;               // [J][Bmax] A-served ids of the round
+    uint32_t *n_aserved;             // [J]
+    uint32_t *evict_list;            // [max(cap_a,1)]
+    uint32_t *fill_list;             // [max(cap_a,1) + J*Bmax]
+    seneca_job_epoch_stats *stats;   // [J][maxT]
     unsigned long long *evicted, *refilled;
     uint32_t *err;
-    uint32_t *claim;                // [NW] scratch for request validation
+    uint32_t *bar;                   // [2] barrier count, generation
+    unsigned long long *phase;       // [8] accumulated cycles per phase
 };
 
-struct RoundParams {
-    uint64_t r;
-    uint32_t nj;
-    uint32_t active_after;   // active mask after this round's departures
-    uint32_t full_scan;      // the active set changed: every A entry is a candidate (R-O6)
-    uint32_t out_stride;     // row stride of out_ids / out_src / requested
-    uint32_t job[kMaxJobs];
-    uint32_t need[kMaxJobs];
-    uint32_t nbase[kMaxJobs];
-    uint32_t epoch[kMaxJobs];
+struct Launch {
+    uint64_t r0;
+    uint32_t rounds;
+    uint32_t subset;                 // jobs taking part in every round (& active)
+    uint32_t mode;                   // 0 generated requests, 1 caller-supplied
+    uint32_t active0;
+    uint32_t n0[kMaxJobs];           // consumed samples of the current epoch at launch
+    uint32_t e0[kMaxJobs];           // epoch at launch
+    uint32_t row_of_job[kMaxJobs];   // output row of each job
+    uint32_t out_stride;
+    uint32_t timing;
     uint32_t* out_ids;
     uint8_t* out_src;
-    const uint32_t* requested;   // mode 1: [nj][out_stride]
-    unsigned long long* transcript;
+    const uint32_t* requested;       // mode 1: [row][out_stride]
+    unsigned long long* transcript;  // [J][maxT][N] or null
 };
 
-__device__ __forceinline__ uint32_t pidx_of(uint32_t j, uint32_t t) {
-    return j * 3u + (t == T_A ? 0u : (t == T_D ? 1u : 2u));
-}
+__device__ __forceinline__ uint32_t ldcg(const uint32_t* p) { return __ldcg(p); }
+__device__ __forceinline__ uint4 ldcg4(const uint32_t* p) { return __ldcg(reinterpret_cast<const uint4*>(p)); }
 
 __device__ __forceinline__ uint32_t valid_mask(const Cfg& C, uint32_t w) {
     const uint64_t lo = (uint64_t)w * 32u;
@@ -118,169 +126,284 @@ __device__ __forceinline__ uint32_t valid_mask(const Cfg& C, uint32_t w) {
     return (1u << (C.N - lo)) - 1u;
 }
 
-// word w of pool (t, j)
-__device__ __forceinline__ uint32_t pool_word(const Lay& L, const Cfg& C, uint32_t t, uint32_t j, uint32_t w) {
-    if (t == T_S) return ~(L.bm_e[w] | L.bm_d[w] | L.bm_a[w]) & valid_mask(C, w);
-    const uint32_t s = L.seen[(size_t)j * C.NW + w];
-    if (t == T_A) return L.bm_a[w] & ~s & ~L.cons[(size_t)j * C.NW + w];
-    if (t == T_D) return L.bm_d[w] & ~s;
-    return L.bm_e[w] & ~s;
+__device__ __forceinline__ uint32_t pool_of(uint32_t j, uint32_t t) {   // t: T_A, T_D, T_E
+    return j * 3u + (t == T_A ? 0u : (t == T_D ? 1u : 2u));
 }
 
-__device__ __forceinline__ void count_add(const Lay& L, const Cfg& C, uint32_t pidx, uint32_t id, int delta) {
-    atomicAdd(L.cnt_blk + (size_t)pidx * C.NBp + (id >> 10), (uint32_t)delta);
-    atomicAdd(L.cnt_sup + (size_t)pidx * C.NS + (id >> 15), (uint32_t)delta);
+__device__ __forceinline__ void count_add(const Lay& L, const Cfg& C, uint32_t pidx, uint32_t id, uint32_t delta) {
+    atomicAdd(L.cnt_blk + (size_t)pidx * C.NBp + (id >> kBlockShift), delta);
+    atomicAdd(L.cnt_sup + (size_t)pidx * C.NS + (id >> kSuperShift), delta);
 }
 
-// Exclusive prefix of the superblock counts of pool pidx into shared memory.
+// Exclusive prefix of the superblock counts of pool pidx, into shared memory.
 __device__ void load_sup_prefix(const Lay& L, const Cfg& C, uint32_t pidx, uint32_t* s_pre, uint32_t* scratch) {
     const uint32_t per = (C.NS + blockDim.x - 1) / blockDim.x;
     const uint32_t lo = threadIdx.x * per;
     const uint32_t* src = L.cnt_sup + (size_t)pidx * C.NS;
+    uint32_t v[16];
     uint32_t sum = 0;
-    for (uint32_t k = 0; k < per && lo + k < C.NS; ++k) sum += src[lo + k];
+    for (uint32_t k = 0; k < per && k < 16; ++k) {
+        v[k] = lo + k < C.NS ? ldcg(src + lo + k) : 0u;
+        sum += v[k];
+    }
+    for (uint32_t k = 16; k < per; ++k) sum += lo + k < C.NS ? ldcg(src + lo + k) : 0u;
     uint32_t run = block_exclusive_scan(sum, nullptr, scratch);
     for (uint32_t k = 0; k < per && lo + k < C.NS; ++k) {
-        const uint32_t v = src[lo + k];
+        const uint32_t x = k < 16 ? v[k] : ldcg(src + lo + k);
         s_pre[lo + k] = run;
-        run += v;
+        run += x;
     }
     __syncthreads();
 }
 
-// The rank-th (0-based) member, in ascending id order, of pool (t, j).
+// The rank-th (0-based) member, in ascending id order, of pool (t, j):
+// superblock by binary search in shared memory, then two batches of
+// independent loads (the 32 block counts of the superblock; the 8 words of
+// each bitmap of the block).
 __device__ uint32_t pool_select(const Lay& L, const Cfg& C, uint32_t pidx, uint32_t t, uint32_t j,
                                 const uint32_t* s_pre, uint32_t rank) {
     uint32_t lo = 0, hi = C.NS - 1;
-    while (lo < hi) {                                   // last superblock with prefix <= rank
+    while (lo < hi) {
         const uint32_t mid = (lo + hi + 1) >> 1;
         if (s_pre[mid] <= rank) lo = mid; else hi = mid - 1;
     }
     uint32_t r = rank - s_pre[lo];
-    const uint4* cb = reinterpret_cast<const uint4*>(L.cnt_blk + (size_t)pidx * C.NBp + (size_t)lo * 32u);
-    uint32_t blk = lo * 32u;
+    const uint32_t* crow = L.cnt_blk + (size_t)pidx * C.NBp + (size_t)lo * 32u;
+    uint4 cv[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) cv[q] = ldcg4(crow + 4 * q);
+    uint32_t blk = lo * 32u, k_found = 0;
     bool found = false;
-#pragma unroll 1
-    for (int q = 0; q < 8 && !found; ++q) {
-        const uint4 v = cb[q];
-        const uint32_t c[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const uint32_t c4[4] = {cv[q].x, cv[q].y, cv[q].z, cv[q].w};
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             if (!found) {
-                if (r < c[k]) { found = true; blk = lo * 32u + q * 4 + k; }
-                else r -= c[k];
+                if (r < c4[k]) { found = true; k_found = q * 4 + k; }
+                else r -= c4[k];
             }
         }
     }
-    const uint32_t w0 = blk * 32u;
-#pragma unroll 1
-    for (uint32_t k = 0; k < 32; ++k) {
-        uint32_t pw = pool_word(L, C, t, j, w0 + k);
-        const uint32_t pc = __popc(pw);
+    blk += k_found;
+    const uint32_t w0 = blk * kWordsPerBlock;
+    uint32_t pw[8];
+    {
+        const uint4 a0 = ldcg4(L.bm_a + w0), a1 = ldcg4(L.bm_a + w0 + 4);
+        if (t == T_S) {
+            const uint4 e0 = ldcg4(L.bm_e + w0), e1 = ldcg4(L.bm_e + w0 + 4);
+            const uint4 d0 = ldcg4(L.bm_d + w0), d1 = ldcg4(L.bm_d + w0 + 4);
+            pw[0] = ~(a0.x | e0.x | d0.x); pw[1] = ~(a0.y | e0.y | d0.y);
+            pw[2] = ~(a0.z | e0.z | d0.z); pw[3] = ~(a0.w | e0.w | d0.w);
+            pw[4] = ~(a1.x | e1.x | d1.x); pw[5] = ~(a1.y | e1.y | d1.y);
+            pw[6] = ~(a1.z | e1.z | d1.z); pw[7] = ~(a1.w | e1.w | d1.w);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) pw[k] &= valid_mask(C, w0 + k);
+        } else {
+            const uint32_t* sj = L.seen + (size_t)j * C.NW + w0;
+            const uint4 s0 = ldcg4(sj), s1 = ldcg4(sj + 4);
+            uint4 b0, b1;
+            if (t == T_A) { b0 = a0; b1 = a1; }
+            else if (t == T_D) { b0 = ldcg4(L.bm_d + w0); b1 = ldcg4(L.bm_d + w0 + 4); }
+            else { b0 = ldcg4(L.bm_e + w0); b1 = ldcg4(L.bm_e + w0 + 4); }
+            pw[0] = b0.x & ~s0.x; pw[1] = b0.y & ~s0.y; pw[2] = b0.z & ~s0.z; pw[3] = b0.w & ~s0.w;
+            pw[4] = b1.x & ~s1.x; pw[5] = b1.y & ~s1.y; pw[6] = b1.z & ~s1.z; pw[7] = b1.w & ~s1.w;
+            if (t == T_A) {
+                const uint32_t* cj = L.cons + (size_t)j * C.NW + w0;
+                const uint4 c0 = ldcg4(cj), c1 = ldcg4(cj + 4);
+                pw[0] &= ~c0.x; pw[1] &= ~c0.y; pw[2] &= ~c0.z; pw[3] &= ~c0.w;
+                pw[4] &= ~c1.x; pw[5] &= ~c1.y; pw[6] &= ~c1.z; pw[7] &= ~c1.w;
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const uint32_t pc = __popc(pw[k]);
         if (r < pc) {
-            for (uint32_t s = 0; s < r; ++s) pw &= pw - 1u;
-            return (w0 + k) * 32u + (uint32_t)(__ffs(pw) - 1);
+            uint32_t x = pw[k];
+            for (uint32_t s = 0; s < r; ++s) x &= x - 1u;
+            return (w0 + k) * 32u + (uint32_t)(__ffs(x) - 1);
         }
         r -= pc;
     }
-    atomicOr(L.err, 1u);   // counts inconsistent with bitmaps
+    atomicOr(L.err, 1u);   // counts inconsistent with the bitmaps
     return 0;
 }
 
-// ---------------------------------------------------------------------------
-// a1-a3: request + classify.  One CTA per job of the round.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kReqThreads)
-ods_request_classify(Lay L, Cfg C, RoundParams P, uint32_t mode) {
-    extern __shared__ uint32_t smem[];
-    uint32_t* s_req = smem;                         // [Bmax]
-    __shared__ uint32_t s_scan[33];
-    __shared__ uint32_t s_state[6];                 // cur_buf, nxt_buf, cursor, cur_len, nxt_len, wrap
-    __shared__ uint32_t s_newcursor;
-    __shared__ uint32_t s_hits[3];
-    __shared__ uint32_t s_tot[3];
+// ------------------------------------------------------------------ barrier among the round CTAs
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 
-    const uint32_t x = blockIdx.x;
-    const uint32_t j = P.job[x];
-    const uint32_t need = P.need[x];
+__device__ void round_barrier(uint32_t* bar, uint32_t nctas, uint32_t& gen) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const uint32_t g = gen;
+        if (atomicAdd(bar, 1u) == nctas - 1) {
+            bar[0] = 0;
+            __threadfence();
+            atomicExch(bar + 1, g + 1);
+        } else {
+            while (ld_acquire(bar + 1) == g) { }
+        }
+        __threadfence();
+    }
+    gen += 1;
+    __syncthreads();
+}
+
+// ------------------------------------------------------------------ shared state of a job CTA
+struct JobSmem {
+    uint32_t cur_buf, nxt_buf, cursor, cur_len, nxt_len;
+    uint32_t wrap_slot, need, newcursor, walk_err;
+    uint32_t m, k[3], tot[3], hits[3];
+    uint32_t recount;
+    uint32_t n_as;
+    uint32_t scan[33];
+    unsigned long long red[(kThreads / 32) * 13];
+};
+
+__device__ __forceinline__ const uint32_t* list_ptr(const Lay& L, const Cfg& C, uint32_t j, uint32_t e, uint32_t buf) {
+    return buf == 0 ? L.perms + ((size_t)j * C.maxT + e) * C.N : L.laps + ((size_t)j * 2 + (buf - 1)) * C.N;
+}
+
+// a1/a2 (R-O1): the first `need` ids of the job's current lap list, from the
+// cursor, that are not in seen_j.  At a lap end the walk continues with the
+// list of deferred misses of the lap (slot order = position order).
+__device__ void job_walk(const Lay& L, const Cfg& C, JobSmem& S, uint32_t* s_req, uint32_t j, uint32_t e, uint32_t need) {
     const uint32_t tid = threadIdx.x, T = blockDim.x;
-    uint32_t* seen_j = L.seen + (size_t)j * C.NW;
-    uint32_t* cons_j = L.cons + (size_t)j * C.NW;
-
-    if (tid == 0) {
-        const JobDev& jd = L.jobs[j];
-        s_state[0] = jd.cur_buf; s_state[1] = jd.nxt_buf; s_state[2] = jd.cursor;
-        s_state[3] = jd.cur_len; s_state[4] = jd.nxt_len; s_state[5] = 0;
-        s_hits[0] = s_hits[1] = s_hits[2] = 0;
-        for (int k = 0; k < 3; ++k) s_tot[k] = L.cnt_tot[j * 3 + k];
+    const uint32_t* seen_j = L.seen + (size_t)j * C.NW;
+    if (tid == 0) { S.wrap_slot = 0; S.need = need; }
+    if (S.cur_buf == 0 && tid == 0) {            // the epoch's permutation must be published
+        const uint32_t* f = L.perm_ready + (size_t)j * C.maxT + e;
+        while (ld_acquire(f) == 0) { }
     }
     __syncthreads();
-
-    if (mode == 1) {
-        for (uint32_t s = tid; s < need; s += T) s_req[s] = P.requested[(size_t)x * P.out_stride + s];
-        __syncthreads();
-    } else {
-        // a1/a2: first `need` unseen ids of the lap list from the cursor (R-O1)
-        uint32_t taken = 0;
-        bool wrapped = false;
-        while (taken < need) {
-            if (s_state[2] >= s_state[3]) {         // lap ends: continue with the deferred list
-                __syncthreads();
-                if (wrapped || s_state[4] == 0) {
-                    if (tid == 0) atomicOr(L.err, 2u);
-                    break;
-                }
-                if (tid == 0) {
-                    s_state[5] = taken;
-                    s_state[0] = s_state[1];
-                    s_state[3] = s_state[4];
-                    s_state[2] = 0;
-                    s_state[1] = s_state[0] == 1 ? 2 : 1;
-                    s_state[4] = 0;
-                }
-                wrapped = true;
-                __syncthreads();
-            }
-            const uint32_t cursor = s_state[2], len = s_state[3];
-            const uint32_t* list = L.lists + ((size_t)j * 3 + s_state[0]) * C.N;
-            uint32_t ids[4];
-            uint32_t flags = 0, cnt = 0;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const uint32_t e = cursor + tid * 4 + k;
-                ids[k] = 0;
-                if (e < len) {
-                    const uint32_t id = list[e];
-                    ids[k] = id;
-                    if (!((seen_j[id >> 5] >> (id & 31)) & 1u)) { flags |= 1u << k; ++cnt; }
-                }
-            }
-            uint32_t tot;
-            const uint32_t ex = block_exclusive_scan(cnt, &tot, s_scan);
-            const uint32_t remaining = need - taken;
-            uint32_t r = ex;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                if (flags & (1u << k)) {
-                    if (r < remaining) s_req[taken + r] = ids[k];
-                    if (r == remaining - 1) s_newcursor = cursor + tid * 4 + k + 1;
-                    ++r;
-                }
-            }
+    uint32_t taken = 0;
+    bool wrapped = false;
+    while (taken < need) {
+        if (S.cursor >= S.cur_len) {
             __syncthreads();
-            if (tot >= remaining) {
-                if (tid == 0) s_state[2] = s_newcursor;
-                taken = need;
-            } else {
-                if (tid == 0) s_state[2] = min(cursor + 4 * T, len);
-                taken += tot;
+            if (wrapped || S.nxt_len == 0) {
+                if (tid == 0) atomicOr(L.err, 2u);
+                break;
             }
+            if (tid == 0) {
+                S.wrap_slot = taken;
+                S.cur_buf = S.nxt_buf;
+                S.cur_len = S.nxt_len;
+                S.cursor = 0;
+                S.nxt_buf = S.cur_buf == 1 ? 2 : 1;
+                S.nxt_len = 0;
+            }
+            wrapped = true;
             __syncthreads();
         }
+        const uint32_t cursor = S.cursor, len = S.cur_len;
+        const uint32_t* list = list_ptr(L, C, j, e, S.cur_buf);
+        uint32_t ids[kWalkPerThread];
+        uint32_t flags = 0, cnt = 0;
+#pragma unroll
+        for (uint32_t k = 0; k < kWalkPerThread; ++k) {
+            const uint32_t p = cursor + tid * kWalkPerThread + k;
+            ids[k] = p < len ? ldcg(list + p) : 0xffffffffu;
+        }
+#pragma unroll
+        for (uint32_t k = 0; k < kWalkPerThread; ++k) {
+            if (ids[k] != 0xffffffffu) {
+                const uint32_t id = ids[k];
+                if (!((ldcg(seen_j + (id >> 5)) >> (id & 31)) & 1u)) { flags |= 1u << k; ++cnt; }
+            }
+        }
+        uint32_t tot;
+        const uint32_t ex = block_exclusive_scan(cnt, &tot, S.scan);
+        const uint32_t remaining = need - taken;
+        uint32_t r = ex;
+#pragma unroll
+        for (uint32_t k = 0; k < kWalkPerThread; ++k) {
+            if (flags & (1u << k)) {
+                if (r < remaining) s_req[taken + r] = ids[k];
+                if (r == remaining - 1) S.newcursor = cursor + tid * kWalkPerThread + k + 1;
+                ++r;
+            }
+        }
+        __syncthreads();
+        if (tot >= remaining) {
+            if (tid == 0) S.cursor = S.newcursor;
+            taken = need;
+        } else {
+            if (tid == 0) S.cursor = min(cursor + kWalkPerThread * T, len);
+            taken += tot;
+        }
+        __syncthreads();
     }
+}
 
-    // a3: classify.  Hits (E, D, or A not consumed by j, R-O13) join seen_j now.
-    uint32_t* miss_j = L.miss + (size_t)j * C.Bmax;
+// Rebuild the three pool counts of job j (epoch start: seen_j is empty).
+__device__ void job_recount(const Lay& L, const Cfg& C, uint32_t j, uint32_t* s_sup /* [3][NS] */) {
+    const uint32_t tid = threadIdx.x, T = blockDim.x;
+    for (uint32_t k = tid; k < 3 * C.NS; k += T) s_sup[k] = 0;
+    __syncthreads();
+    const uint32_t* cj = L.cons + (size_t)j * C.NW;
+    const uint32_t* sj = L.seen + (size_t)j * C.NW;
+    for (uint32_t b = tid; b < C.NBp; b += T) {
+        const uint32_t w0 = b * kWordsPerBlock;
+        uint32_t ca = 0, cd = 0, ce = 0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint4 a = ldcg4(L.bm_a + w0 + 4 * h), d = ldcg4(L.bm_d + w0 + 4 * h), e = ldcg4(L.bm_e + w0 + 4 * h);
+            const uint4 c = ldcg4(cj + w0 + 4 * h), s = ldcg4(sj + w0 + 4 * h);
+            ca += __popc(a.x & ~c.x & ~s.x) + __popc(a.y & ~c.y & ~s.y) + __popc(a.z & ~c.z & ~s.z) + __popc(a.w & ~c.w & ~s.w);
+            cd += __popc(d.x & ~s.x) + __popc(d.y & ~s.y) + __popc(d.z & ~s.z) + __popc(d.w & ~s.w);
+            ce += __popc(e.x & ~s.x) + __popc(e.y & ~s.y) + __popc(e.z & ~s.z) + __popc(e.w & ~s.w);
+        }
+        L.cnt_blk[(size_t)(j * 3 + 0) * C.NBp + b] = ca;
+        L.cnt_blk[(size_t)(j * 3 + 1) * C.NBp + b] = cd;
+        L.cnt_blk[(size_t)(j * 3 + 2) * C.NBp + b] = ce;
+        const uint32_t s = b >> 5;
+        if (ca) atomicAdd(s_sup + s, ca);
+        if (cd) atomicAdd(s_sup + C.NS + s, cd);
+        if (ce) atomicAdd(s_sup + 2 * C.NS + s, ce);
+    }
+    __syncthreads();
+    uint32_t ta = 0, td = 0, te = 0;
+    for (uint32_t s = tid; s < C.NS; s += T) {
+        const uint32_t a = s_sup[s], d = s_sup[C.NS + s], e = s_sup[2 * C.NS + s];
+        L.cnt_sup[(size_t)(j * 3 + 0) * C.NS + s] = a;
+        L.cnt_sup[(size_t)(j * 3 + 1) * C.NS + s] = d;
+        L.cnt_sup[(size_t)(j * 3 + 2) * C.NS + s] = e;
+        ta += a; td += d; te += e;
+    }
+    ta = warp_sum(ta); td = warp_sum(td); te = warp_sum(te);
+    __shared__ uint32_t s_t[3];
+    if (tid == 0) s_t[0] = s_t[1] = s_t[2] = 0;
+    __syncthreads();
+    if ((tid & 31) == 0) { atomicAdd(&s_t[0], ta); atomicAdd(&s_t[1], td); atomicAdd(&s_t[2], te); }
+    __syncthreads();
+    if (tid == 0) {
+        L.cnt_tot[j * 3 + 0] = s_t[0];
+        L.cnt_tot[j * 3 + 1] = s_t[1];
+        L.cnt_tot[j * 3 + 2] = s_t[2];
+    }
+    __syncthreads();
+}
+
+// a3-a6 for job j in round r: classify, substitute, respond.
+__device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& S, uint32_t* s_req, uint32_t* s_miss,
+                          uint32_t* s_sub, uint32_t* s_pre, uint32_t j, uint64_t r, uint32_t e, uint32_t nbase) {
+    const uint32_t tid = threadIdx.x, T = blockDim.x;
+    const uint32_t need = S.need;
+    uint32_t* seen_j = L.seen + (size_t)j * C.NW;
+    uint32_t* cons_j = L.cons + (size_t)j * C.NW;
+    const size_t row = (size_t)P.row_of_job[j] * P.out_stride;
+    if (tid < 3) { S.hits[tid] = 0; S.tot[tid] = ldcg(L.cnt_tot + j * 3 + tid); }
+    if (tid == 0) S.n_as = 0;
+    __syncthreads();
+
+    // a3: hits (E, D, or A not consumed by j, R-O13) join seen_j now
     uint32_t mbase = 0;
     for (uint32_t base = 0; base < need; base += T) {
         const uint32_t s = base + tid;
@@ -288,88 +411,102 @@ ods_request_classify(Lay L, Cfg C, RoundParams P, uint32_t mode) {
         if (s < need) {
             const uint32_t i = s_req[s];
             const uint32_t w = i >> 5, b = 1u << (i & 31);
-            const uint32_t t = (L.bm_a[w] & b) ? T_A : (L.bm_d[w] & b) ? T_D : (L.bm_e[w] & b) ? T_E : T_S;
-            const bool hit = (t == T_E || t == T_D || (t == T_A && !(cons_j[w] & b)));
+            const uint32_t wa = ldcg(L.bm_a + w), wd = ldcg(L.bm_d + w), we = ldcg(L.bm_e + w), wc = ldcg(cons_j + w);
+            const uint32_t t = (wa & b) ? T_A : (wd & b) ? T_D : (we & b) ? T_E : T_S;
+            const bool hit = (t == T_E || t == T_D || (t == T_A && !(wc & b)));
             if (hit) {
-                P.out_ids[(size_t)x * P.out_stride + s] = i;
-                P.out_src[(size_t)x * P.out_stride + s] = (uint8_t)t;
+                P.out_ids[row + s] = i;
+                P.out_src[row + s] = (uint8_t)t;
                 atomicOr(seen_j + w, b);
                 if (t == T_A) atomicOr(cons_j + w, b);
-                count_add(L, C, pidx_of(j, t), i, -1);
-                atomicAdd(&s_hits[t == T_A ? 0 : (t == T_D ? 1 : 2)], 1u);
+                count_add(L, C, pool_of(j, t), i, 0xffffffffu);
+                atomicAdd(&S.hits[t == T_A ? 0 : (t == T_D ? 1 : 2)], 1u);
             } else {
                 is_miss = true;
             }
         }
         uint32_t tot;
-        const uint32_t ex = block_exclusive_scan(is_miss ? 1u : 0u, &tot, s_scan);
-        if (is_miss) miss_j[mbase + ex] = s;
+        const uint32_t ex = block_exclusive_scan(is_miss ? 1u : 0u, &tot, S.scan);
+        if (is_miss) s_miss[mbase + ex] = s;
         mbase += tot;
     }
-    if (mode == 1) {  // keep request ids for the storage / deferral phase
-        for (uint32_t s = tid; s < need; s += T) L.req[(size_t)j * C.Bmax + s] = s_req[s];
-    } else {
-        for (uint32_t s = tid; s < need; s += T) L.req[(size_t)j * C.Bmax + s] = s_req[s];
+    if (tid == 0) {
+        const uint32_t pa = S.tot[0] - S.hits[0], pd = S.tot[1] - S.hits[1], pe = S.tot[2] - S.hits[2];
+        S.tot[0] = pa; S.tot[1] = pd; S.tot[2] = pe;
+        const uint32_t m = mbase;
+        S.m = m;
+        S.k[0] = min(m, pa);
+        S.k[1] = min(m - S.k[0], pd);
+        S.k[2] = min(m - S.k[0] - S.k[1], pe);
     }
     __syncthreads();
-    if (tid == 0) {
-        // pool totals after the hits; substitutes per tier A -> D -> E (R-O2)
-        uint32_t pa = s_tot[0] - s_hits[0], pd = s_tot[1] - s_hits[1], pe = s_tot[2] - s_hits[2];
-        L.cnt_tot[j * 3 + 0] = pa; L.cnt_tot[j * 3 + 1] = pd; L.cnt_tot[j * 3 + 2] = pe;
-        const uint32_t m = mbase;
-        const uint32_t ka = min(m, pa), kd = min(m - ka, pd), ke = min(m - ka - kd, pe);
-        JobDev& jd = L.jobs[j];
-        jd.cur_buf = s_state[0]; jd.nxt_buf = s_state[1]; jd.cursor = s_state[2];
-        jd.cur_len = s_state[3]; jd.nxt_len = s_state[4]; jd.wrap_slot = s_state[5];
-        jd.m = m; jd.k[0] = ka; jd.k[1] = kd; jd.k[2] = ke;
+
+    // a4/a5: misses in slot order take substitutes A -> D -> E at keyed ranks (R-O2)
+    const uint32_t k0 = S.k[0], k1 = S.k[1], k2 = S.k[2];
+    const uint32_t q = k0 + k1 + k2;
+    if (q > 0) {
+        for (uint32_t tt = 0; tt < 3; ++tt)
+            if (S.k[tt]) load_sup_prefix(L, C, j * 3 + tt, s_pre + tt * C.NS, S.scan);
+        for (uint32_t u = tid; u < q; u += T) {
+            const uint32_t tt = u < k0 ? 0u : (u < k0 + k1 ? 1u : 2u);
+            const uint32_t ul = u - (tt == 0 ? 0u : (tt == 1 ? k0 : k0 + k1));
+            const uint32_t t = tt == 0 ? T_A : (tt == 1 ? T_D : T_E);
+            const uint64_t key = derive_key(C.seed, PUR_SUB, j, r, t);
+            const uint32_t rank = perm_apply(key, perm_domain(S.tot[tt]), ul);
+            const uint32_t id = pool_select(L, C, j * 3 + tt, t, j, s_pre + tt * C.NS, rank);
+            const uint32_t s = s_miss[u];
+            P.out_ids[row + s] = id;
+            P.out_src[row + s] = (uint8_t)(t | SUBST);
+            s_sub[u] = id;
+        }
+        __syncthreads();
+        for (uint32_t u = tid; u < q; u += T) {
+            const uint32_t tt = u < k0 ? 0u : (u < k0 + k1 ? 1u : 2u);
+            const uint32_t id = s_sub[u];
+            const uint32_t w = id >> 5, b = 1u << (id & 31);
+            atomicOr(seen_j + w, b);
+            if (tt == 0) atomicOr(cons_j + w, b);
+            count_add(L, C, j * 3 + tt, id, 0xffffffffu);
+        }
     }
-}
-
-// ---------------------------------------------------------------------------
-// a4-a6: substitution by keyed rank + apply; the last CTA of a job finishes it.
-// ---------------------------------------------------------------------------
-__device__ void finish_job(const Lay& L, const Cfg& C, const RoundParams& P, uint32_t x, uint32_t* s_scan,
-                           unsigned long long* s_red) {
-    const uint32_t j = P.job[x], need = P.need[x], tid = threadIdx.x, T = blockDim.x;
-    const JobDev jd = L.jobs[j];
-    const uint32_t q = jd.k[0] + jd.k[1] + jd.k[2];
-    const uint32_t m = jd.m;
-    const uint32_t* miss_j = L.miss + (size_t)j * C.Bmax;
-    const uint32_t* req_j = L.req + (size_t)j * C.Bmax;
-    uint32_t* seen_j = L.seen + (size_t)j * C.NW;
-    const size_t row = (size_t)x * P.out_stride;
-
     // remaining misses are fetched from storage (R-O18)
-    for (uint32_t u = q + tid; u < m; u += T) {
-        const uint32_t s = miss_j[u], i = req_j[s];
+    for (uint32_t u = q + tid; u < S.m; u += T) {
+        const uint32_t s = s_miss[u], i = s_req[s];
         P.out_ids[row + s] = i;
         P.out_src[row + s] = (uint8_t)T_S;
         atomicOr(seen_j + (i >> 5), 1u << (i & 31));
     }
     // deferred (replaced) misses are requested again on the next lap (R-O1):
-    // slots before the wrap belong to the lap that just ended -> end of the
-    // (new) current list; the rest -> the next list.  Slot order = list order.
+    // before a wrap -> the end of the (new) current list, after -> the next list
     uint32_t q1 = 0;
-    if (jd.wrap_slot > 0) {
+    if (S.wrap_slot > 0) {
         uint32_t c = 0;
-        for (uint32_t u = tid; u < q; u += T) c += miss_j[u] < jd.wrap_slot;
-        block_exclusive_scan(c, &q1, s_scan);
+        for (uint32_t u = tid; u < q; u += T) c += s_miss[u] < S.wrap_slot;
+        block_exclusive_scan(c, &q1, S.scan);
     }
-    uint32_t* cur_list = L.lists + ((size_t)j * 3 + jd.cur_buf) * C.N;
-    uint32_t* nxt_list = L.lists + ((size_t)j * 3 + jd.nxt_buf) * C.N;
-    for (uint32_t u = tid; u < q; u += T) {
-        const uint32_t id = req_j[miss_j[u]];
-        if (u < q1) cur_list[jd.cur_len + u] = id;
-        else nxt_list[jd.nxt_len + (u - q1)] = id;
+    if (P.mode == 0 && q > 0) {
+        uint32_t* cur_list = L.laps + ((size_t)j * 2 + (S.cur_buf - 1)) * C.N;   // only used if q1 > 0
+        uint32_t* nxt_list = L.laps + ((size_t)j * 2 + (S.nxt_buf - 1)) * C.N;
+        for (uint32_t u = tid; u < q; u += T) {
+            const uint32_t id = s_req[s_miss[u]];
+            if (u < q1) cur_list[S.cur_len + u] = id;
+            else nxt_list[S.nxt_len + (u - q1)] = id;
+        }
     }
     __syncthreads();
+    if (tid == 0) {
+        if (P.mode == 0) { S.cur_len += q1; S.nxt_len += q - q1; }
+        L.cnt_tot[j * 3 + 0] = S.tot[0] - k0;
+        L.cnt_tot[j * 3 + 1] = S.tot[1] - k1;
+        L.cnt_tot[j * 3 + 2] = S.tot[2] - k2;
+    }
 
-    // counters, digest, transcript (a6)
+    // a6: counters, digest, transcript, A-served list for maintain
     unsigned long long acc[13];
 #pragma unroll
     for (int k = 0; k < 13; ++k) acc[k] = 0;
-    const uint32_t e = P.epoch[x], nbase = P.nbase[x];
     unsigned long long* trow = P.transcript ? P.transcript + ((size_t)j * C.maxT + e) * C.N : nullptr;
+    uint32_t* as_j = L.aserved + (size_t)j * C.Bmax;
     for (uint32_t s = tid; s < need; s += T) {
         const uint32_t i = P.out_ids[row + s];
         const uint32_t src = P.out_src[row + s];
@@ -377,262 +514,273 @@ __device__ void finish_job(const Lay& L, const Cfg& C, const RoundParams& P, uin
         acc[t] += 1;
         if (src & SUBST) acc[4 + t] += 1;
         else if (t != T_S) acc[8 + t] += 1;
-        const uint64_t word = ((uint64_t)(nbase + s) << 35) | ((uint64_t)src << 32) | i;
-        acc[12] += splitmix64(word);
+        acc[12] += splitmix64(((uint64_t)(nbase + s) << 35) | ((uint64_t)src << 32) | i);
         if (trow) trow[nbase + s] = ((unsigned long long)src << 32) | i;
+        if (t == T_A) as_j[atomicAdd(&S.n_as, 1u)] = i;
     }
 #pragma unroll
     for (int k = 0; k < 13; ++k) {
-        unsigned long long v = warp_sum(acc[k]);
-        if ((tid & 31) == 0) s_red[(tid >> 5) * 13 + k] = v;
+        const unsigned long long v = warp_sum(acc[k]);
+        if ((tid & 31) == 0) S.red[(tid >> 5) * 13 + k] = v;
     }
     __syncthreads();
     if (tid < 13) {
         unsigned long long v = 0;
-        for (uint32_t w = 0; w < T / 32; ++w) v += s_red[w * 13 + tid];
+        for (uint32_t w = 0; w < T / 32; ++w) v += S.red[w * 13 + tid];
         unsigned long long* st = reinterpret_cast<unsigned long long*>(L.stats + (size_t)j * C.maxT + e);
         st[tid] += v;
     }
-    if (tid == 0) {
-        JobDev& w = L.jobs[j];
-        w.cur_len = jd.cur_len + q1;
-        w.nxt_len = jd.nxt_len + (q - q1);
-        w.done = 0;
-    }
+    if (tid == 0) L.n_aserved[j] = S.n_as;
+    __syncthreads();
 }
 
-__global__ void __launch_bounds__(kSelThreads)
-ods_select_apply(Lay L, Cfg C, RoundParams P) {
-    extern __shared__ uint32_t smem[];
-    uint32_t* s_pre = smem;                  // [NS]
-    uint32_t* s_sub = smem + C.NS;           // [Bmax]
-    __shared__ uint32_t s_scan[33];
-    __shared__ unsigned long long s_red[(kSelThreads / 32) * 13];
-    __shared__ int s_last;
+// ------------------------------------------------------------------ maintain (a7)
+struct MaintSmem {
+    uint32_t ne, kmax, deficit0, PS, sizeA;
+    uint32_t add[kMaxJobs];
+    uint32_t scan[33];
+};
 
-    const uint32_t x = blockIdx.x / 3, tt = blockIdx.x % 3;
-    const uint32_t t = tt == 0 ? T_A : (tt == 1 ? T_D : T_E);
-    const uint32_t j = P.job[x];
-    const uint32_t tid = threadIdx.x, T = blockDim.x;
-    const JobDev jd = L.jobs[j];
-    const uint32_t k = jd.k[tt];
-    const uint32_t qoff = tt == 0 ? 0u : (tt == 1 ? jd.k[0] : jd.k[0] + jd.k[1]);
-
-    if (k > 0) {
-        const uint32_t pidx = j * 3 + tt;
-        const uint32_t P_t = L.cnt_tot[pidx];
-        load_sup_prefix(L, C, pidx, s_pre, s_scan);
-        const uint64_t key = derive_key(C.seed, PUR_SUB, j, P.r, t);
-        const PermDomain dom = perm_domain(P_t);
-        const uint32_t* miss_j = L.miss + (size_t)j * C.Bmax;
-        const size_t row = (size_t)x * P.out_stride;
-        for (uint32_t u = tid; u < k; u += T) {
-            const uint32_t rank = perm_apply(key, dom, u);
-            const uint32_t id = pool_select(L, C, pidx, t, j, s_pre, rank);
-            const uint32_t s = miss_j[qoff + u];
-            P.out_ids[row + s] = id;
-            P.out_src[row + s] = (uint8_t)(t | SUBST);
-            s_sub[u] = id;
-        }
-        __syncthreads();
-        uint32_t* seen_j = L.seen + (size_t)j * C.NW;
-        uint32_t* cons_j = L.cons + (size_t)j * C.NW;
-        for (uint32_t u = tid; u < k; u += T) {
-            const uint32_t id = s_sub[u];
-            const uint32_t w = id >> 5, b = 1u << (id & 31);
-            atomicOr(seen_j + w, b);
-            if (t == T_A) atomicOr(cons_j + w, b);
-            count_add(L, C, pidx, id, -1);
-        }
-        if (tid == 0) L.cnt_tot[pidx] = P_t - k;
-    }
+__device__ void maint_refill_select(const Lay& L, const Cfg& C, MaintSmem& M, uint32_t* s_pre, uint64_t r, uint32_t k) {
+    if (k == 0) return;
+    load_sup_prefix(L, C, 3 * C.J, s_pre, M.scan);
+    const uint64_t key = derive_key(C.seed, PUR_REFILL, 0, r, 0);
+    const PermDomain dom = perm_domain(M.PS);
+    for (uint32_t u = threadIdx.x; u < k; u += blockDim.x)
+        L.fill_list[u] = pool_select(L, C, 3 * C.J, T_S, 0, s_pre, perm_apply(key, dom, u));
     __syncthreads();
-    if (tid == 0) {
-        __threadfence();
-        const uint32_t old = atomicAdd(&L.jobs[j].done, 1u);
-        s_last = (old == 2);
-        if (s_last) __threadfence();
-    }
-    __syncthreads();
-    if (s_last) finish_job(L, C, P, x, s_scan, s_red);
 }
 
-// ---------------------------------------------------------------------------
-// a7: maintain -- eviction of A entries consumed by every active job (R-O5,
-// R-O6) and keyed refill from the storage pool as of round start (R-O8).
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kMaintThreads)
-ods_maintain(Lay L, Cfg C, RoundParams P) {
-    extern __shared__ uint32_t smem[];
-    uint32_t* s_pre = smem;                        // [NS]
-    __shared__ uint32_t s_scan[33];
-    __shared__ uint32_t s_ne;
-    __shared__ uint32_t s_add[kMaxJobs];
+// eviction of A entries consumed by every active job (R-O5, R-O6), refill from
+// the storage pool as of round start (R-O8), counts kept exact.
+__device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSmem& M, uint32_t* s_pre,
+                            uint64_t r, uint32_t part, uint32_t active, bool full_scan, bool speculated) {
     const uint32_t tid = threadIdx.x, T = blockDim.x;
-    const uint32_t active = P.active_after;
-    if (active == 0) return;                       // replay over: no maintain work (R-O7)
-    if (tid == 0) s_ne = 0;
-    if (tid < kMaxJobs) s_add[tid] = 0;
+    if (tid == 0) M.ne = 0;
+    if (tid < kMaxJobs) M.add[tid] = 0;
     __syncthreads();
-
-    auto consumed_by_all = [&](uint32_t w, uint32_t b) -> bool {
-        for (uint32_t m = active; m; m &= m - 1) {
-            const uint32_t a = __ffs(m) - 1;
-            if (!(L.cons[(size_t)a * C.NW + w] & b)) return false;
-        }
-        return true;
-    };
-
-    if (P.full_scan) {
-        // the active set changed: every A entry is a candidate
+    if (full_scan) {
         for (uint32_t w = tid; w < C.NW; w += T) {
-            uint32_t ev = L.bm_a[w];
-            for (uint32_t m = active; m && ev; m &= m - 1) ev &= L.cons[(size_t)(__ffs(m) - 1) * C.NW + w];
+            uint32_t ev = ldcg(L.bm_a + w);
+            for (uint32_t m = active; m && ev; m &= m - 1) ev &= ldcg(L.cons + (size_t)(__ffs(m) - 1) * C.NW + w);
             if (ev) {
-                const uint32_t base = atomicAdd(&s_ne, (uint32_t)__popc(ev));
+                const uint32_t base = atomicAdd(&M.ne, (uint32_t)__popc(ev));
                 uint32_t c = 0;
                 for (uint32_t v = ev; v; v &= v - 1) L.evict_list[base + c++] = w * 32u + (__ffs(v) - 1);
             }
         }
     } else {
-        // candidates: the A-served ids of this round (deduplicated by claiming)
-        uint32_t total = 0;
-        for (uint32_t x = 0; x < P.nj; ++x) total += P.need[x];
-        for (uint32_t f = tid; f < total; f += T) {
-            uint32_t x = 0, s = f;
-            while (s >= P.need[x]) { s -= P.need[x]; ++x; }
-            const size_t at = (size_t)x * P.out_stride + s;
-            if ((P.out_src[at] & 3u) != T_A) continue;
-            const uint32_t i = P.out_ids[at];
-            const uint32_t w = i >> 5, b = 1u << (i & 31);
-            if (!(L.bm_a[w] & b) || !consumed_by_all(w, b)) continue;
-            if (atomicOr(L.evmark + w, b) & b) continue;      // already claimed
-            L.evict_list[atomicAdd(&s_ne, 1u)] = i;
+        for (uint32_t pm = part; pm; pm &= pm - 1) {
+            const uint32_t j = __ffs(pm) - 1;
+            const uint32_t na = ldcg(L.n_aserved + j);
+            const uint32_t* as_j = L.aserved + (size_t)j * C.Bmax;
+            for (uint32_t f = tid; f < na; f += T) {
+                const uint32_t i = ldcg(as_j + f);
+                const uint32_t w = i >> 5, b = 1u << (i & 31);
+                uint32_t all = ldcg(L.bm_a + w);
+                for (uint32_t m = active; m; m &= m - 1) all &= ldcg(L.cons + (size_t)(__ffs(m) - 1) * C.NW + w);
+                if (!(all & b)) continue;
+                if (atomicOr(L.evmark + w, b) & b) continue;      // claimed by another job's entry
+                L.evict_list[atomicAdd(&M.ne, 1u)] = i;
+            }
         }
     }
     __syncthreads();
-    const uint32_t ne = s_ne;
-    const uint32_t size_a = *L.a_size;
-    const uint32_t deficit = C.cap_a - (size_a - ne);
-    const uint32_t PS = L.cnt_tot[3 * C.J];
-    const uint32_t k = min(deficit, PS);
+    const uint32_t ne = M.ne;
+    const uint32_t k = min(M.deficit0 + ne, M.PS);
+    if (!speculated) maint_refill_select(L, C, M, s_pre, r, k);
     const uint32_t spidx = 3 * C.J;
-    if (k > 0) {
-        load_sup_prefix(L, C, spidx, s_pre, s_scan);
-        const uint64_t key = derive_key(C.seed, PUR_REFILL, 0, P.r, 0);
-        const PermDomain dom = perm_domain(PS);
-        for (uint32_t u = tid; u < k; u += T)
-            L.fill_list[u] = pool_select(L, C, spidx, T_S, 0, s_pre, perm_apply(key, dom, u));
-    }
-    __syncthreads();
-    // apply evictions: A -> S, consumers cleared; the storage pool gains them
     for (uint32_t u = tid; u < ne; u += T) {
         const uint32_t i = L.evict_list[u];
         const uint32_t w = i >> 5, b = 1u << (i & 31);
         atomicAnd(L.bm_a + w, ~b);
-        if (!P.full_scan) atomicAnd(L.evmark + w, ~b);
+        if (!full_scan) atomicAnd(L.evmark + w, ~b);
         for (uint32_t a = 0; a < C.J; ++a) atomicAnd(L.cons + (size_t)a * C.NW + w, ~b);
-        count_add(L, C, spidx, i, +1);
+        count_add(L, C, spidx, i, 1u);
     }
-    // apply refills: S -> A with empty consumers; every active job that has not
-    // seen the id gains it in its A pool
     for (uint32_t u = tid; u < k; u += T) {
-        const uint32_t i = L.fill_list[u];
+        const uint32_t i = ldcg(L.fill_list + u);
         const uint32_t w = i >> 5, b = 1u << (i & 31);
         atomicOr(L.bm_a + w, b);
-        count_add(L, C, spidx, i, -1);
+        count_add(L, C, spidx, i, 0xffffffffu);
         for (uint32_t m = active; m; m &= m - 1) {
             const uint32_t a = __ffs(m) - 1;
-            if (!(L.seen[(size_t)a * C.NW + w] & b)) {
-                count_add(L, C, a * 3 + 0, i, +1);
-                atomicAdd(&s_add[a], 1u);
+            if (!(ldcg(L.seen + (size_t)a * C.NW + w) & b)) {
+                count_add(L, C, a * 3 + 0, i, 1u);
+                atomicAdd(&M.add[a], 1u);
             }
         }
     }
     __syncthreads();
-    if (tid < C.J && s_add[tid]) L.cnt_tot[tid * 3 + 0] += s_add[tid];
+    if (tid < C.J && M.add[tid]) atomicAdd(L.cnt_tot + tid * 3 + 0, M.add[tid]);
     if (tid == 0) {
-        L.cnt_tot[spidx] = PS + ne - k;
-        *L.a_size = size_a - ne + k;
+        L.cnt_tot[spidx] = M.PS + ne - k;
+        *L.a_size = M.sizeA - ne + k;
         *L.evicted += ne;
         *L.refilled += k;
     }
+    __syncthreads();
 }
 
-// ---------------------------------------------------------------------------
-// pool recount: one CTA per superblock; one warp per 1024-id block.
-// blockIdx.y selects a job of jobs_mask (in order); y == popc(mask) -> storage pool.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kRecountThreads)
-ods_recount(Lay L, Cfg C, uint32_t jobs_mask, uint32_t with_storage) {
-    __shared__ uint32_t s_c[32][3];
-    const uint32_t sblk = blockIdx.x;
-    const uint32_t nmask = __popc(jobs_mask);
-    const uint32_t y = blockIdx.y;
-    const bool storage = y >= nmask;
-    if (storage && !with_storage) return;
-    uint32_t j = 0;
-    if (!storage) {
-        uint32_t m = jobs_mask;
-        for (uint32_t k = 0; k < y; ++k) m &= m - 1;
-        j = __ffs(m) - 1;
-    }
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t blk = sblk * 32 + warp;
-    const uint32_t w = blk * 32 + lane;
-    uint32_t ca = 0, cd = 0, ce = 0;
-    if (blk < C.NB) {
-        if (storage) {
-            ca = __popc(~(L.bm_e[w] | L.bm_d[w] | L.bm_a[w]) & valid_mask(C, w));
-        } else {
-            const uint32_t s = L.seen[(size_t)j * C.NW + w];
-            ca = __popc(L.bm_a[w] & ~s & ~L.cons[(size_t)j * C.NW + w]);
-            cd = __popc(L.bm_d[w] & ~s);
-            ce = __popc(L.bm_e[w] & ~s);
-        }
-    }
-    ca = warp_sum(ca); cd = warp_sum(cd); ce = warp_sum(ce);
-    if (lane == 0) {
-        s_c[warp][0] = ca; s_c[warp][1] = cd; s_c[warp][2] = ce;
-        if (storage) L.cnt_blk[(size_t)(3 * C.J) * C.NBp + blk] = ca;
-        else {
-            L.cnt_blk[(size_t)(j * 3 + 0) * C.NBp + blk] = ca;
-            L.cnt_blk[(size_t)(j * 3 + 1) * C.NBp + blk] = cd;
-            L.cnt_blk[(size_t)(j * 3 + 2) * C.NBp + blk] = ce;
-        }
+// ------------------------------------------------------------------ the persistent round kernel
+__global__ void __launch_bounds__(kThreads, 1)
+ods_rounds(Lay L, Cfg C, Launch P) {
+    extern __shared__ uint32_t smem[];
+    __shared__ JobSmem S;
+    __shared__ MaintSmem M;
+    __shared__ uint32_t s_n[kMaxJobs], s_e[kMaxJobs], s_active;
+    const uint32_t tid = threadIdx.x;
+    const uint32_t cta = blockIdx.x, nctas = gridDim.x;
+    const bool is_maint = cta == C.J;
+    const uint32_t j = cta;
+    uint32_t gen = ldcg(L.bar + 1);
+    long long t_mark = 0;
+    unsigned long long t_acc[4] = {0, 0, 0, 0};
+
+    // shared memory carve: job CTA s_req | s_miss | s_sub [Bmax] + s_pre [3][NS]; maintain CTA s_pre [NS]
+    uint32_t* s_req = smem;
+    uint32_t* s_miss = smem + C.Bmax;
+    uint32_t* s_sub = smem + 2 * C.Bmax;
+    uint32_t* s_pre = smem + 3 * C.Bmax;
+
+    if (tid < kMaxJobs) { s_n[tid] = P.n0[tid]; s_e[tid] = P.e0[tid]; }
+    if (tid == 0) s_active = P.active0;
+    if (!is_maint && tid == 0) {
+        const JobDev jd = L.jobs[j];
+        S.cur_buf = jd.cur_buf; S.nxt_buf = jd.nxt_buf; S.cursor = jd.cursor;
+        S.cur_len = jd.cur_len; S.nxt_len = jd.nxt_len; S.recount = jd.recount;
     }
     __syncthreads();
-    if (warp == 0) {
-        uint32_t a = s_c[lane][0], d = s_c[lane][1], e = s_c[lane][2];
-        a = warp_sum(a); d = warp_sum(d); e = warp_sum(e);
-        if (lane == 0) {
-            if (storage) {
-                L.cnt_sup[(size_t)(3 * C.J) * C.NS + sblk] = a;
-                atomicAdd(L.cnt_tot + 3 * C.J, a);
-            } else {
-                L.cnt_sup[(size_t)(j * 3 + 0) * C.NS + sblk] = a;
-                L.cnt_sup[(size_t)(j * 3 + 1) * C.NS + sblk] = d;
-                L.cnt_sup[(size_t)(j * 3 + 2) * C.NS + sblk] = e;
-                atomicAdd(L.cnt_tot + j * 3 + 0, a);
-                atomicAdd(L.cnt_tot + j * 3 + 1, d);
-                atomicAdd(L.cnt_tot + j * 3 + 2, e);
+
+    auto need_of = [&](uint32_t jj) -> uint32_t { return min(C.batch[jj], C.N - s_n[jj]); };
+
+    // prologue: the walk of the first round
+    if (!is_maint && ((s_active & P.subset) >> j & 1u)) {
+        const uint32_t need = need_of(j);
+        if (P.mode == 1) {
+            for (uint32_t s = tid; s < need; s += blockDim.x)
+                s_req[s] = P.requested[(size_t)P.row_of_job[j] * P.out_stride + s];
+            if (tid == 0) { S.need = need; S.wrap_slot = 0; }
+            __syncthreads();
+        } else {
+            job_walk(L, C, S, s_req, j, s_e[j], need);
+        }
+    }
+
+    for (uint32_t rr = 0; rr < P.rounds; ++rr) {
+        const uint64_t r = P.r0 + rr;
+        const uint32_t part = s_active & P.subset;
+        // round schedule (data-independent, R-O12): who ends an epoch / departs
+        uint32_t departing = 0;
+        for (uint32_t m = part; m; m &= m - 1) {
+            const uint32_t jj = __ffs(m) - 1;
+            if (s_n[jj] + need_of(jj) == C.N && s_e[jj] + 1 == C.target[jj]) departing |= 1u << jj;
+        }
+        const uint32_t active_after = s_active & ~departing;
+        const bool full_scan = departing != 0;
+        if (P.timing && tid == 0) t_mark = clock64();
+
+        bool spec = false;
+        if (is_maint) {
+            if (active_after && C.cap_a > 0) {
+                if (tid == 0) {
+                    M.PS = ldcg(L.cnt_tot + 3 * C.J);
+                    M.sizeA = ldcg(L.a_size);
+                    M.deficit0 = C.cap_a - M.sizeA;
+                    uint32_t cand = 0;
+                    for (uint32_t m = part; m; m &= m - 1) cand += need_of(__ffs(m) - 1);
+                    M.kmax = min(M.deficit0 + cand, M.PS);
+                }
+                __syncthreads();
+                if (!full_scan) { maint_refill_select(L, C, M, s_pre, r, M.kmax); spec = true; }
+            }
+        } else if ((part >> j) & 1u) {
+            if (S.recount) { job_recount(L, C, j, s_pre); if (tid == 0) S.recount = 0; __syncthreads(); }
+            job_round(L, C, P, S, s_req, s_miss, s_sub, s_pre, j, r, s_e[j], s_n[j]);
+            // a8 (R-O16): the epoch ends with this batch -> reset seen_j and the walk
+            if (s_n[j] + S.need == C.N) {
+                uint4* sj = reinterpret_cast<uint4*>(L.seen + (size_t)j * C.NW);
+                for (uint32_t k = tid; k < C.NW / 4; k += blockDim.x) sj[k] = make_uint4(0, 0, 0, 0);
+                if (tid == 0) {
+                    S.cur_buf = 0; S.nxt_buf = 1; S.cursor = 0; S.cur_len = C.N; S.nxt_len = 0;
+                    S.recount = 1;
+                }
+                __syncthreads();
             }
         }
+        if (P.timing && tid == 0) { const long long t = clock64(); t_acc[0] += t - t_mark; t_mark = t; }
+        round_barrier(L.bar, nctas, gen);
+        if (P.timing && tid == 0) { const long long t = clock64(); t_acc[1] += t - t_mark; t_mark = t; }
+
+        // schedule update (every CTA, identically)
+        if (tid == 0) {
+            for (uint32_t m = part; m; m &= m - 1) {
+                const uint32_t jj = __ffs(m) - 1;
+                s_n[jj] += need_of(jj);
+                if (s_n[jj] == C.N) { s_n[jj] = 0; s_e[jj] += 1; }
+            }
+            s_active = active_after;
+        }
+        __syncthreads();
+
+        if (is_maint) {
+            if (active_after && C.cap_a > 0) {
+                if (!spec && tid == 0) {
+                    M.PS = ldcg(L.cnt_tot + 3 * C.J);
+                    M.sizeA = ldcg(L.a_size);
+                    M.deficit0 = C.cap_a - M.sizeA;
+                }
+                __syncthreads();
+                maint_apply(L, C, P, M, s_pre, r, part, active_after, full_scan, spec);
+            }
+        } else if (rr + 1 < P.rounds && ((active_after & P.subset) >> j & 1u)) {
+            job_walk(L, C, S, s_req, j, s_e[j], need_of(j));   // the next round's request
+        }
+        if (P.timing && tid == 0) { const long long t = clock64(); t_acc[2] += t - t_mark; t_mark = t; }
+        round_barrier(L.bar, nctas, gen);
+        if (P.timing && tid == 0) { const long long t = clock64(); t_acc[3] += t - t_mark; t_mark = t; }
+    }
+    // persist the walk state
+    if (!is_maint && tid == 0) {
+        JobDev& jd = L.jobs[j];
+        jd.cur_buf = S.cur_buf; jd.nxt_buf = S.nxt_buf; jd.cursor = S.cursor;
+        jd.cur_len = S.cur_len; jd.nxt_len = S.nxt_len; jd.recount = S.recount;
+    }
+    if (P.timing && tid == 0) {
+        const uint32_t base = is_maint ? 4 : 0;
+        if (is_maint || cta == 0)
+            for (int k = 0; k < 4; ++k) atomicAdd(L.phase + base + k, t_acc[k]);
     }
 }
 
-// pi_j for epoch e: list[pos] = perm(key(seed, REQ, j, e), N, pos) (R-O3).
-// Also resets the job's lap-list state (block 0, thread 0).
-__global__ void ods_perm_fill(Lay L, Cfg C, uint32_t j, uint32_t epoch) {
-    const uint64_t key = derive_key(C.seed, PUR_REQ, j, epoch, 0);
+// ------------------------------------------------------------------ one-off kernels
+// pi_j,e for every (job, epoch), epoch-major, in chunks; the CTA finishing the
+// last chunk of (j, e) publishes perm_ready[j][e] (release).
+__global__ void ods_perm_all(Lay L, Cfg C, uint32_t chunk) {
+    const uint32_t per = (C.N + chunk - 1) / chunk;
+    const uint64_t total = (uint64_t)C.maxT * C.J * per;
     const PermDomain dom = perm_domain(C.N);
-    uint32_t* out = L.lists + (size_t)j * 3 * C.N;
-    for (uint32_t pos = blockIdx.x * blockDim.x + threadIdx.x; pos < C.N; pos += gridDim.x * blockDim.x)
-        out[pos] = perm_apply(key, dom, pos);
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        JobDev& jd = L.jobs[j];
-        jd.cur_buf = 0; jd.nxt_buf = 1; jd.cursor = 0; jd.cur_len = C.N; jd.nxt_len = 0;
-        jd.wrap_slot = 0; jd.m = 0; jd.k[0] = jd.k[1] = jd.k[2] = 0; jd.done = 0;
+    __shared__ uint32_t s_last;
+    for (uint64_t c = blockIdx.x; c < total; c += gridDim.x) {
+        const uint32_t e = (uint32_t)(c / ((uint64_t)C.J * per));
+        const uint32_t j = (uint32_t)((c / per) % C.J);
+        const uint32_t part = (uint32_t)(c % per);
+        if (e >= C.target[j]) continue;
+        const uint64_t key = derive_key(C.seed, PUR_REQ, j, e, 0);
+        uint32_t* out = L.perms + ((size_t)j * C.maxT + e) * C.N;
+        const uint32_t lo = part * chunk, hi = min(lo + chunk, C.N);
+        for (uint32_t pos = lo + threadIdx.x; pos < hi; pos += blockDim.x) out[pos] = perm_apply(key, dom, pos);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            const uint32_t old = atomicAdd(L.perm_done + (size_t)j * C.maxT + e, hi - lo);
+            s_last = old + (hi - lo) == C.N;
+            if (s_last) {
+                __threadfence();
+                atomicExch(L.perm_ready + (size_t)j * C.maxT + e, 1u);
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -649,11 +797,58 @@ __global__ void ods_init_tiers(Lay L, Cfg C, uint32_t cap_e, uint32_t cap_d) {
     if (blockIdx.x == 0 && threadIdx.x == 0) *L.a_size = C.cap_a;
 }
 
+// Pool counts of every job and of the storage pool (init): one CTA per
+// superblock (256 threads, one word each; 8 threads per 256-id block).
+__global__ void __launch_bounds__(256)
+ods_recount_all(Lay L, Cfg C) {
+    const uint32_t sblk = blockIdx.x, pool = blockIdx.y;    // pool < 3J: (j, tier); == 3J: storage
+    const uint32_t w = sblk * 256 + threadIdx.x;
+    uint32_t word;
+    const uint32_t a = L.bm_a[w], d = L.bm_d[w], e = L.bm_e[w];
+    if (pool == 3 * C.J) {
+        word = ~(a | d | e) & valid_mask(C, w);
+    } else {
+        const uint32_t j = pool / 3, tt = pool % 3;
+        const uint32_t s = L.seen[(size_t)j * C.NW + w];
+        word = tt == 0 ? (a & ~s & ~L.cons[(size_t)j * C.NW + w]) : (tt == 1 ? (d & ~s) : (e & ~s));
+    }
+    uint32_t c = __popc(word);
+    c += __shfl_xor_sync(0xffffffffu, c, 1);
+    c += __shfl_xor_sync(0xffffffffu, c, 2);
+    c += __shfl_xor_sync(0xffffffffu, c, 4);
+    if ((threadIdx.x & 7) == 0) L.cnt_blk[(size_t)pool * C.NBp + (w >> 3)] = c;
+    __shared__ uint32_t s_w[8];
+    const uint32_t ws = warp_sum(__popc(word));
+    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = ws;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int k = 0; k < 8; ++k) t += s_w[k];
+        L.cnt_sup[(size_t)pool * C.NS + sblk] = t;
+        if (t) atomicAdd(L.cnt_tot + pool, t);
+    }
+}
+
+__global__ void ods_init_jobs(Lay L, Cfg C) {
+    const uint32_t j = threadIdx.x;
+    if (j < C.J) {
+        JobDev& jd = L.jobs[j];
+        jd.cur_buf = 0; jd.nxt_buf = 1; jd.cursor = 0; jd.cur_len = C.N; jd.nxt_len = 0; jd.recount = 0;
+    }
+}
+
 // caller-supplied requests (mode 1): range, duplicates within the row, seen
-__global__ void ods_validate_requests(Lay L, Cfg C, RoundParams P) {
+__global__ void ods_validate_requests(Lay L, Cfg C, Launch P) {
     extern __shared__ uint32_t s_row[];
-    const uint32_t x = blockIdx.x, j = P.job[x], need = P.need[x];
-    const uint32_t* R = P.requested + (size_t)x * P.out_stride;
+    uint32_t x = 0;
+    uint32_t j = 0xffffffffu;
+    for (uint32_t m = P.subset; m; m &= m - 1) {
+        if (x == blockIdx.x) { j = __ffs(m) - 1; break; }
+        ++x;
+    }
+    if (j == 0xffffffffu) return;
+    const uint32_t need = min(C.batch[j], C.N - P.n0[j]);
+    const uint32_t* R = P.requested + (size_t)P.row_of_job[j] * P.out_stride;
     for (uint32_t s = threadIdx.x; s < need; s += blockDim.x) s_row[s] = R[s];
     __syncthreads();
     for (uint32_t s = threadIdx.x; s < need; s += blockDim.x) {
@@ -667,6 +862,10 @@ __global__ void ods_validate_requests(Lay L, Cfg C, RoundParams P) {
 
 inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
+enum KernelClass { K_ROUNDS = 0, K_PERM, K_RECOUNT, K_INIT, K_VALIDATE, K_NCLASS };
+const char* const kKernelNames[K_NCLASS] = {"ods_rounds", "ods_perm_all", "ods_recount_all", "ods_init_tiers",
+                                            "ods_validate_requests"};
+
 }  // namespace
 }  // namespace seneca
 
@@ -675,67 +874,31 @@ inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 // ===========================================================================
 using namespace seneca;
 
-namespace {
-enum KernelClass { K_REQUEST = 0, K_SELECT, K_MAINTAIN, K_RECOUNT, K_PERM, K_INIT, K_VALIDATE, K_NCLASS };
-const char* const kKernelNames[K_NCLASS] = {"ods_request_classify", "ods_select_apply", "ods_maintain",
-                                            "ods_recount", "ods_perm_fill", "ods_init_tiers",
-                                            "ods_validate_requests"};
-
-// Sampled kernel timing: CUDA events around the launches of every k-th round
-// (and around every launch of the rare classes), on the launch stream, kept in
-// a ring and resolved lazily so the host never waits on recent work.
-struct KernelProfiler {
-    struct Slot { cudaEvent_t a = nullptr, b = nullptr; int cls = -1; };
-    uint32_t every = 0;
-    std::vector<Slot> ring;
-    size_t head = 0;
-    uint64_t launches[K_NCLASS] = {};
-    uint64_t sampled[K_NCLASS] = {};
-    double ms[K_NCLASS] = {};
-
-    void resolve(Slot& s) {
-        if (s.cls < 0) return;
-        float t = 0.f;
-        cudaEventSynchronize(s.b);
-        if (cudaEventElapsedTime(&t, s.a, s.b) == cudaSuccess) { sampled[s.cls]++; ms[s.cls] += t; }
-        s.cls = -1;
-    }
-    Slot* acquire() {
-        if (ring.empty()) {
-            ring.resize(4096);
-            for (auto& s : ring) { cudaEventCreate(&s.a); cudaEventCreate(&s.b); }
-        }
-        Slot& s = ring[head];
-        head = (head + 1) % ring.size();
-        resolve(s);
-        return &s;
-    }
-    void flush() { for (auto& s : ring) resolve(s); }
-    ~KernelProfiler() { for (auto& s : ring) { if (s.a) cudaEventDestroy(s.a); if (s.b) cudaEventDestroy(s.b); } }
-};
-}  // namespace
-
 struct seneca_ctx {
-    KernelProfiler prof;
     Cfg C;
     Lay L;
     uint32_t mode;
-    uint32_t batch[kMaxJobs], target[kMaxJobs];
     uint64_t cap_e, cap_d;
     uint64_t e[kMaxJobs], n[kMaxJobs];
     uint32_t active;
     uint64_t r;
     uint64_t launches;
-    size_t sel_smem, req_smem, maint_smem;
+    uint64_t klaunch[K_NCLASS];
+    double kms[K_NCLASS];
+    uint64_t ksampled[K_NCLASS];
+    uint32_t profiling;
+    size_t round_smem;
+    int device;
+    cudaStream_t side;
+    cudaEvent_t ev_init;
+    cudaEvent_t ev_a, ev_b;
 };
 
 namespace {
 
 seneca_status check_cfg(const seneca_cache_config* cfg) {
     if (!cfg) { set_error("NULL config"); return SENECA_EINVAL; }
-    if (cfg->n_total == 0 || cfg->n_total >= (1ull << 31)) {
-        set_error("n_total must be in [1, 2^31)"); return SENECA_EINVAL;
-    }
+    if (cfg->n_total == 0 || cfg->n_total >= (1ull << 31)) { set_error("n_total must be in [1, 2^31)"); return SENECA_EINVAL; }
     if (cfg->n_jobs == 0 || cfg->n_jobs > kMaxJobs) { set_error("n_jobs must be in [1, 32]"); return SENECA_EINVAL; }
     if (cfg->request_mode > 1) { set_error("request_mode must be 0 or 1"); return SENECA_EINVAL; }
     if (!cfg->batch_size || !cfg->target_epochs) { set_error("NULL batch_size/target_epochs"); return SENECA_EINVAL; }
@@ -743,8 +906,8 @@ seneca_status check_cfg(const seneca_cache_config* cfg) {
         if (cfg->batch_size[j] == 0 || cfg->batch_size[j] > kMaxBatch) {
             set_error("batch_size[%u] must be in [1, %u]", j, kMaxBatch); return SENECA_EINVAL;
         }
-        if (cfg->target_epochs[j] == 0 || cfg->target_epochs[j] > 1000000) {
-            set_error("target_epochs[%u] must be in [1, 1e6]", j); return SENECA_EINVAL;
+        if (cfg->target_epochs[j] == 0 || cfg->target_epochs[j] > 100000) {
+            set_error("target_epochs[%u] must be in [1, 1e5]", j); return SENECA_EINVAL;
         }
     }
     if (cfg->cap_e > cfg->n_total || cfg->cap_d > cfg->n_total || cfg->cap_a > cfg->n_total ||
@@ -756,7 +919,7 @@ seneca_status check_cfg(const seneca_cache_config* cfg) {
 
 struct Sizes {
     Cfg C;
-    size_t off[32];
+    size_t off[40];
     size_t total;
 };
 
@@ -764,37 +927,38 @@ Sizes compute_sizes(const seneca_cache_config* cfg) {
     Sizes z{};
     Cfg& C = z.C;
     C.N = (uint32_t)cfg->n_total;
-    C.NB = (C.N + 1023) / 1024;
+    C.NB = (C.N + 255) / 256;
     C.NS = (C.NB + 31) / 32;
     C.NBp = C.NS * 32;
-    C.NW = C.NBp * 32;              // bitmaps padded to whole superblocks
+    C.NW = C.NBp * kWordsPerBlock;          // bitmaps padded to whole superblocks
     C.J = cfg->n_jobs;
     C.Bmax = 0;
     C.maxT = 0;
     for (uint32_t j = 0; j < C.J; ++j) {
         C.Bmax = std::max(C.Bmax, cfg->batch_size[j]);
         C.maxT = std::max(C.maxT, cfg->target_epochs[j]);
+        C.batch[j] = cfg->batch_size[j];
+        C.target[j] = cfg->target_epochs[j];
     }
     C.cap_a = (uint32_t)cfg->cap_a;
     C.seed = cfg->seed;
     const size_t W = (size_t)C.NW * 4, P = 3 * (size_t)C.J + 1;
     const size_t capl = std::max<size_t>(cfg->cap_a, 1) * 4;
     const size_t sz[] = {
-        W, W, W,                                   // 0-2 bm_e, bm_d, bm_a
-        W * C.J, W * C.J,                          // 3-4 seen, cons
-        W,                                         // 5 evmark
-        P * C.NBp * 4, P * C.NS * 4, P * 4,        // 6-8 counts
-        4,                                         // 9 a_size
-        (size_t)C.J * 3 * C.N * 4,                 // 10 lists
-        (size_t)C.J * sizeof(JobDev),              // 11 jobs
-        (size_t)C.J * C.Bmax * 4,                  // 12 req
-        (size_t)C.J * C.Bmax * 4,                  // 13 miss
-        (size_t)C.J * C.Bmax * 4,                  // 14 out_ids
-        (size_t)C.J * C.Bmax,                      // 15 out_src
-        capl, capl,                                // 16-17 evict, fill
-        (size_t)C.J * C.maxT * sizeof(seneca_job_epoch_stats),  // 18 stats
-        8, 8, 4,                                   // 19-21 evicted, refilled, err
-        W,                                         // 22 claim
+        W, W, W,                                            // 0-2 bm_e, bm_d, bm_a
+        W * C.J, W * C.J,                                   // 3-4 seen, cons
+        W,                                                  // 5 evmark
+        P * C.NBp * 4, P * C.NS * 4, P * 4,                 // 6-8 counts
+        4,                                                  // 9 a_size
+        (size_t)C.J * C.maxT * C.N * 4,                     // 10 perms
+        (size_t)C.J * 2 * C.N * 4,                          // 11 laps
+        (size_t)C.J * C.maxT * 4, (size_t)C.J * C.maxT * 4, // 12-13 perm_ready, perm_done
+        (size_t)C.J * sizeof(JobDev),                       // 14 jobs
+        (size_t)C.J * C.Bmax * 4, (size_t)C.J * C.Bmax,     // 15-16 out_ids, out_src
+        (size_t)C.J * C.Bmax * 4, (size_t)C.J * 4,          // 17-18 aserved, n_aserved
+        capl, capl + (size_t)C.J * C.Bmax * 4,              // 19-20 evict, fill
+        (size_t)C.J * C.maxT * sizeof(seneca_job_epoch_stats),  // 21 stats
+        8, 8, 4, 8, 64,                                     // 22-26 evicted, refilled, err, bar, phase
     };
     size_t at = 0;
     for (size_t k = 0; k < sizeof(sz) / sizeof(sz[0]); ++k) {
@@ -817,105 +981,75 @@ Lay carve(const Sizes& z, char* base) {
     L.cnt_sup = (uint32_t*)(base + z.off[7]);
     L.cnt_tot = (uint32_t*)(base + z.off[8]);
     L.a_size = (uint32_t*)(base + z.off[9]);
-    L.lists = (uint32_t*)(base + z.off[10]);
-    L.jobs = (JobDev*)(base + z.off[11]);
-    L.req = (uint32_t*)(base + z.off[12]);
-    L.miss = (uint32_t*)(base + z.off[13]);
-    L.out_ids = (uint32_t*)(base + z.off[14]);
-    L.out_src = (uint8_t*)(base + z.off[15]);
-    L.evict_list = (uint32_t*)(base + z.off[16]);
-    L.fill_list = (uint32_t*)(base + z.off[17]);
-    L.stats = (seneca_job_epoch_stats*)(base + z.off[18]);
-    L.evicted = (unsigned long long*)(base + z.off[19]);
-    L.refilled = (unsigned long long*)(base + z.off[20]);
-    L.err = (uint32_t*)(base + z.off[21]);
-    L.claim = (uint32_t*)(base + z.off[22]);
+    L.perms = (uint32_t*)(base + z.off[10]);
+    L.laps = (uint32_t*)(base + z.off[11]);
+    L.perm_ready = (uint32_t*)(base + z.off[12]);
+    L.perm_done = (uint32_t*)(base + z.off[13]);
+    L.jobs = (JobDev*)(base + z.off[14]);
+    L.out_ids = (uint32_t*)(base + z.off[15]);
+    L.out_src = (uint8_t*)(base + z.off[16]);
+    L.aserved = (uint32_t*)(base + z.off[17]);
+    L.n_aserved = (uint32_t*)(base + z.off[18]);
+    L.evict_list = (uint32_t*)(base + z.off[19]);
+    L.fill_list = (uint32_t*)(base + z.off[20]);
+    L.stats = (seneca_job_epoch_stats*)(base + z.off[21]);
+    L.evicted = (unsigned long long*)(base + z.off[22]);
+    L.refilled = (unsigned long long*)(base + z.off[23]);
+    L.err = (uint32_t*)(base + z.off[24]);
+    L.bar = (uint32_t*)(base + z.off[25]);
+    L.phase = (unsigned long long*)(base + z.off[26]);
     return L;
 }
 
-int g_num_sms = 0;
-
 int num_sms() {
-    if (!g_num_sms) {
+    static int n = 0;
+    if (!n) {
         int dev = 0;
         cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (g_num_sms <= 0) g_num_sms = 148;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
     }
-    return g_num_sms;
+    return n;
 }
 
 template <class F>
-void timed_launch(seneca_ctx* c, int cls, bool sample, cudaStream_t st, F&& launch) {
+void timed(seneca_ctx* c, int cls, cudaStream_t st, F&& launch) {
     c->launches++;
-    c->prof.launches[cls]++;
-    if (!sample || !c->prof.every) { launch(); return; }
-    auto* s = c->prof.acquire();
-    cudaEventRecord(s->a, st);
+    c->klaunch[cls]++;
+    if (!c->profiling) { launch(); return; }
+    cudaEventRecord(c->ev_a, st);
     launch();
-    cudaEventRecord(s->b, st);
-    s->cls = cls;
+    cudaEventRecord(c->ev_b, st);
+    cudaEventSynchronize(c->ev_b);
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, c->ev_a, c->ev_b) == cudaSuccess) { c->kms[cls] += ms; c->ksampled[cls]++; }
 }
 
-seneca_status launch_recount(seneca_ctx* c, uint32_t jobs_mask, bool storage, cudaStream_t st) {
-    const uint32_t ny = __builtin_popcount(jobs_mask) + (storage ? 1 : 0);
-    if (!ny) return SENECA_OK;
-    // zero the totals being rebuilt
-    for (uint32_t m = jobs_mask; m; m &= m - 1) {
-        const uint32_t j = __builtin_ctz(m);
-        SENECA_CUDA_TRY(cudaMemsetAsync(c->L.cnt_tot + j * 3, 0, 12, st));
-    }
-    if (storage) SENECA_CUDA_TRY(cudaMemsetAsync(c->L.cnt_tot + 3 * c->C.J, 0, 4, st));
-    dim3 grid(c->C.NS, ny);
-    timed_launch(c, K_RECOUNT, true, st, [&] {
-        ods_recount<<<grid, kRecountThreads, 0, st>>>(c->L, c->C, jobs_mask, storage ? 1u : 0u);
-    });
-    SENECA_CUDA_TRY(cudaGetLastError());
-    return SENECA_OK;
-}
-
-seneca_status launch_perm_fill(seneca_ctx* c, uint32_t j, uint32_t epoch, cudaStream_t st) {
-    const uint32_t threads = 256;
-    uint32_t blocks = (c->C.N + threads - 1) / threads;
-    blocks = std::min<uint32_t>(blocks, (uint32_t)num_sms() * 8);
-    timed_launch(c, K_PERM, true, st, [&] { ods_perm_fill<<<blocks, threads, 0, st>>>(c->L, c->C, j, epoch); });
-    SENECA_CUDA_TRY(cudaGetLastError());
-    return SENECA_OK;
-}
-
-// One round (R-O11) with the host's data-independent schedule.
-seneca_status run_round(seneca_ctx* c, const uint32_t* jobs, uint32_t nj, const uint32_t* d_requested,
-                        uint32_t* out_ids, uint8_t* out_src, uint32_t out_stride, unsigned long long* transcript,
-                        uint32_t* h_lens, cudaStream_t st) {
-    RoundParams P;
+// Launch R rounds.  jobs_mask: the jobs of every round (replay: all active).
+seneca_status launch_rounds(seneca_ctx* c, uint64_t R, uint32_t jobs_mask, const uint32_t* d_requested,
+                            uint32_t* out_ids, uint8_t* out_src, uint32_t out_stride, const uint32_t* row_of_job,
+                            unsigned long long* transcript, cudaStream_t st) {
+    Launch P;
     std::memset(&P, 0, sizeof P);
-    P.r = c->r;
-    P.nj = nj;
+    P.r0 = c->r;
+    P.rounds = (uint32_t)R;
+    P.subset = jobs_mask;
+    P.mode = c->mode;
+    P.active0 = c->active;
+    for (uint32_t j = 0; j < c->C.J; ++j) {
+        P.n0[j] = (uint32_t)c->n[j];
+        P.e0[j] = (uint32_t)c->e[j];
+        P.row_of_job[j] = row_of_job ? row_of_job[j] : j;
+    }
     P.out_stride = out_stride;
     P.out_ids = out_ids;
     P.out_src = out_src;
     P.requested = d_requested;
     P.transcript = transcript;
-    uint32_t departing = 0, ending = 0;
-    for (uint32_t x = 0; x < nj; ++x) {
-        const uint32_t j = jobs[x];
-        const uint64_t need = std::min<uint64_t>(c->batch[j], (uint64_t)c->C.N - c->n[j]);
-        P.job[x] = j;
-        P.need[x] = (uint32_t)need;
-        P.nbase[x] = (uint32_t)c->n[j];
-        P.epoch[x] = (uint32_t)c->e[j];
-        if (c->n[j] + need == c->C.N) {
-            ending |= 1u << j;
-            if (c->e[j] + 1 == c->target[j]) departing |= 1u << j;
-        }
-        if (h_lens) h_lens[x] = (uint32_t)need;
-    }
-    P.active_after = c->active & ~departing;
-    P.full_scan = departing ? 1u : 0u;
-
+    P.timing = c->profiling;
     if (c->mode == 1) {
-        timed_launch(c, K_VALIDATE, false, st, [&] {
-            ods_validate_requests<<<nj, 256, (size_t)c->C.Bmax * 4, st>>>(c->L, c->C, P);
+        timed(c, K_VALIDATE, st, [&] {
+            ods_validate_requests<<<__builtin_popcount(jobs_mask), 256, (size_t)c->C.Bmax * 4, st>>>(c->L, c->C, P);
         });
         SENECA_CUDA_TRY(cudaGetLastError());
         uint32_t err = 0;
@@ -927,45 +1061,29 @@ seneca_status run_round(seneca_ctx* c, const uint32_t* jobs, uint32_t nj, const 
             return SENECA_EPROTO;
         }
     }
-    const bool sample = c->prof.every && (c->r % c->prof.every) == 0;
-    timed_launch(c, K_REQUEST, sample, st, [&] {
-        ods_request_classify<<<nj, kReqThreads, c->req_smem, st>>>(c->L, c->C, P, c->mode);
+    void* args[] = {&c->L, &c->C, &P};
+    cudaError_t le = cudaSuccess;
+    timed(c, K_ROUNDS, st, [&] {
+        le = cudaLaunchCooperativeKernel((void*)ods_rounds, dim3(c->C.J + 1), dim3(kThreads), args, c->round_smem, st);
     });
-    timed_launch(c, K_SELECT, sample, st, [&] {
-        ods_select_apply<<<nj * 3, kSelThreads, c->sel_smem, st>>>(c->L, c->C, P);
-    });
-    timed_launch(c, K_MAINTAIN, sample, st, [&] {
-        ods_maintain<<<1, kMaintThreads, c->maint_smem, st>>>(c->L, c->C, P);
-    });
-    SENECA_CUDA_TRY(cudaGetLastError());
-    // epoch ends (a8, R-O16): reset seen, rebuild the job's pool counts, next permutation
-    if (ending) {
-        uint32_t recount = 0;
-        for (uint32_t m = ending; m; m &= m - 1) {
+    if (le != cudaSuccess) return cuda_status(le, "cudaLaunchCooperativeKernel(ods_rounds)");
+    // host mirror of the data-independent schedule
+    for (uint64_t k = 0; k < R; ++k) {
+        const uint32_t part = c->active & jobs_mask;
+        uint32_t departing = 0;
+        for (uint32_t m = part; m; m &= m - 1) {
             const uint32_t j = __builtin_ctz(m);
-            SENECA_CUDA_TRY(cudaMemsetAsync(c->L.seen + (size_t)j * c->C.NW, 0, (size_t)c->C.NW * 4, st));
-            if (!(departing & (1u << j))) {
-                recount |= 1u << j;
-                if (c->mode == 0) {
-                    seneca_status s = launch_perm_fill(c, j, (uint32_t)(c->e[j] + 1), st);
-                    if (s) return s;
-                }
+            const uint64_t need = std::min<uint64_t>(c->C.batch[j], (uint64_t)c->C.N - c->n[j]);
+            c->n[j] += need;
+            if (c->n[j] == c->C.N) {
+                c->n[j] = 0;
+                c->e[j] += 1;
+                if (c->e[j] == c->C.target[j]) departing |= 1u << j;
             }
         }
-        seneca_status s = launch_recount(c, recount, false, st);
-        if (s) return s;
+        c->active &= ~departing;
+        c->r += 1;
     }
-    // host mirror of the schedule
-    for (uint32_t x = 0; x < nj; ++x) {
-        const uint32_t j = jobs[x];
-        c->n[j] += P.need[x];
-        if (c->n[j] == c->C.N) {
-            c->n[j] = 0;
-            c->e[j] += 1;
-        }
-    }
-    c->active &= ~departing;
-    c->r += 1;
     return SENECA_OK;
 }
 
@@ -986,50 +1104,48 @@ extern "C" seneca_status seneca_init_cache(const seneca_cache_config* cfg, void*
     if (!out || !d_workspace) { set_error("NULL workspace or out"); return SENECA_EINVAL; }
     if ((uintptr_t)d_workspace & 255) { set_error("workspace must be 256-byte aligned"); return SENECA_EINVAL; }
     Sizes z = compute_sizes(cfg);
-    if (ws_bytes < z.total) {
-        set_error("workspace %zu bytes < required %zu", ws_bytes, z.total);
-        return SENECA_ENOSPC;
-    }
-    if ((size_t)z.C.NS * 4 + (size_t)z.C.Bmax * 4 > 200 * 1024) {
-        set_error("dataset too large for the shared-memory superblock index");
-        return SENECA_EINVAL;
-    }
+    if (ws_bytes < z.total) { set_error("workspace %zu bytes < required %zu", ws_bytes, z.total); return SENECA_ENOSPC; }
+    const size_t round_smem = (size_t)3 * z.C.Bmax * 4 + (size_t)3 * z.C.NS * 4;
+    if (round_smem > 200 * 1024) { set_error("batch/dataset too large for the shared-memory indices"); return SENECA_EINVAL; }
     seneca_ctx* c = new (std::nothrow) seneca_ctx();
     if (!c) { set_error("out of host memory"); return SENECA_EINVAL; }
     c->C = z.C;
     c->L = carve(z, (char*)d_workspace);
     c->mode = cfg->request_mode;
-    for (uint32_t j = 0; j < cfg->n_jobs; ++j) {
-        c->batch[j] = cfg->batch_size[j];
-        c->target[j] = cfg->target_epochs[j];
-    }
     c->cap_e = cfg->cap_e;
     c->cap_d = cfg->cap_d;
     c->active = cfg->n_jobs == 32 ? 0xffffffffu : ((1u << cfg->n_jobs) - 1);
-    c->req_smem = (size_t)c->C.Bmax * 4;
-    c->sel_smem = (size_t)c->C.NS * 4 + (size_t)c->C.Bmax * 4;
-    c->maint_smem = (size_t)c->C.NS * 4;
+    c->round_smem = round_smem;
     cudaStream_t st = (cudaStream_t)stream;
+    cudaGetDevice(&c->device);
 #define INIT_TRY(expr) do { cudaError_t _e = (expr); if (_e != cudaSuccess) { delete c; return cuda_status(_e, #expr); } } while (0)
-    INIT_TRY(cudaFuncSetAttribute(ods_request_classify, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    INIT_TRY(cudaFuncSetAttribute(ods_select_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    INIT_TRY(cudaFuncSetAttribute(ods_maintain, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    INIT_TRY(cudaFuncSetAttribute(ods_rounds, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    INIT_TRY(cudaFuncSetAttribute(ods_validate_requests, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    INIT_TRY(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    INIT_TRY(cudaEventCreateWithFlags(&c->ev_init, cudaEventDisableTiming));
+    INIT_TRY(cudaEventCreate(&c->ev_a));
+    INIT_TRY(cudaEventCreate(&c->ev_b));
     INIT_TRY(cudaMemsetAsync(d_workspace, 0, z.total, st));
     {
         const uint32_t total = (uint32_t)(cfg->cap_a + cfg->cap_d + cfg->cap_e);
-        uint32_t blocks = std::max<uint32_t>(1, std::min<uint32_t>((total + 255) / 256, num_sms() * 8));
-        timed_launch(c, K_INIT, false, st, [&] {
+        const uint32_t blocks = std::max<uint32_t>(1, std::min<uint32_t>((total + 255) / 256, num_sms() * 8));
+        timed(c, K_INIT, st, [&] {
             ods_init_tiers<<<blocks, 256, 0, st>>>(c->L, c->C, (uint32_t)cfg->cap_e, (uint32_t)cfg->cap_d);
         });
         INIT_TRY(cudaGetLastError());
+        timed(c, K_RECOUNT, st, [&] { ods_recount_all<<<dim3(c->C.NS, 3 * c->C.J + 1), 256, 0, st>>>(c->L, c->C); });
+        INIT_TRY(cudaGetLastError());
+        ods_init_jobs<<<1, 32, 0, st>>>(c->L, c->C);
+        c->launches++;
+        INIT_TRY(cudaGetLastError());
     }
-    s = launch_recount(c, c->active, true, st);
-    if (s) { delete c; return s; }
-    for (uint32_t j = 0; j < cfg->n_jobs; ++j) {
-        if (c->mode == 0) {
-            s = launch_perm_fill(c, j, 0, st);
-            if (s) { delete c; return s; }
-        }
+    // every epoch's permutation, generated on a side stream; rounds wait on the flags
+    INIT_TRY(cudaEventRecord(c->ev_init, st));
+    INIT_TRY(cudaStreamWaitEvent(c->side, c->ev_init, 0));
+    if (c->mode == 0) {
+        const uint32_t chunk = 16384;
+        timed(c, K_PERM, c->side, [&] { ods_perm_all<<<num_sms() * 4, 512, 0, c->side>>>(c->L, c->C, chunk); });
+        INIT_TRY(cudaGetLastError());
     }
 #undef INIT_TRY
     *out = c;
@@ -1045,43 +1161,56 @@ extern "C" seneca_status seneca_ods_next_batch(seneca_ctx* c, const uint32_t* h_
     if ((c->mode == 1) != (d_requested != nullptr)) {
         set_error("d_requested must be given exactly when request_mode = 1"); return SENECA_EINVAL;
     }
-    uint32_t seenmask = 0;
+    uint32_t mask = 0, rows[kMaxJobs] = {0};
     for (uint32_t x = 0; x < n_jobs; ++x) {
         const uint32_t j = h_jobs[x];
-        if (j >= c->C.J || (seenmask & (1u << j))) { set_error("bad or duplicate job %u", j); return SENECA_EINVAL; }
-        seenmask |= 1u << j;
+        if (j >= c->C.J || (mask & (1u << j))) { set_error("bad or duplicate job %u", j); return SENECA_EINVAL; }
+        mask |= 1u << j;
+        rows[j] = x;
         if (!(c->active & (1u << j))) { set_error("job %u has departed", j); return SENECA_ESTATE; }
     }
-    return run_round(c, h_jobs, n_jobs, d_requested, d_out_ids, d_out_src, c->C.Bmax, nullptr, h_out_lens,
-                     (cudaStream_t)stream);
+    for (uint32_t x = 0; x < n_jobs; ++x) {
+        const uint32_t j = h_jobs[x];
+        if (h_out_lens) h_out_lens[x] = (uint32_t)std::min<uint64_t>(c->C.batch[j], (uint64_t)c->C.N - c->n[j]);
+    }
+    return launch_rounds(c, 1, mask, d_requested, d_out_ids, d_out_src, c->C.Bmax, rows, nullptr,
+                         (cudaStream_t)stream);
 }
 
-static seneca_status replay(seneca_ctx* c, uint64_t max_rounds, uint32_t n_epochs, bool by_epochs,
-                            uint64_t* d_transcript, uint64_t* h_rounds, cudaStream_t st) {
+// Rounds needed until every tracked job completed n more epochs (or departed).
+static uint64_t rounds_for_epochs(const seneca_ctx* c, uint32_t n_epochs) {
+    uint64_t n[kMaxJobs], e[kMaxJobs], goal[kMaxJobs];
+    uint32_t active = c->active;
+    const uint32_t tracked = active;
+    for (uint32_t j = 0; j < c->C.J; ++j) { n[j] = c->n[j]; e[j] = c->e[j]; goal[j] = c->e[j] + n_epochs; }
+    uint64_t R = 0;
+    for (;;) {
+        bool pending = false;
+        for (uint32_t m = tracked & active; m; m &= m - 1) if (e[__builtin_ctz(m)] < goal[__builtin_ctz(m)]) pending = true;
+        if (!pending || !active) break;
+        uint32_t departing = 0;
+        for (uint32_t m = active; m; m &= m - 1) {
+            const uint32_t j = __builtin_ctz(m);
+            n[j] += std::min<uint64_t>(c->C.batch[j], (uint64_t)c->C.N - n[j]);
+            if (n[j] == c->C.N) { n[j] = 0; e[j] += 1; if (e[j] == c->C.target[j]) departing |= 1u << j; }
+        }
+        active &= ~departing;
+        ++R;
+    }
+    return R;
+}
+
+static seneca_status replay(seneca_ctx* c, uint64_t R, uint64_t* d_transcript, uint64_t* h_rounds, cudaStream_t st) {
     if (c->mode != 0) { set_error("replay requires request_mode 0"); return SENECA_ESTATE; }
     if (!c->active) { set_error("no active job"); return SENECA_ESTATE; }
-    uint64_t goal[kMaxJobs];
-    const uint32_t tracked = c->active;
-    for (uint32_t j = 0; j < c->C.J; ++j) goal[j] = c->e[j] + n_epochs;
     uint64_t done = 0;
-    uint32_t jobs[kMaxJobs];
-    for (;;) {
-        if (!by_epochs && done >= max_rounds) break;
-        if (by_epochs) {
-            bool pending = false;
-            for (uint32_t m = tracked & c->active; m; m &= m - 1) {
-                const uint32_t j = __builtin_ctz(m);
-                if (c->e[j] < goal[j]) pending = true;
-            }
-            if (!pending) break;
-        }
-        if (!c->active) break;
-        uint32_t nj = 0;
-        for (uint32_t m = c->active; m; m &= m - 1) jobs[nj++] = __builtin_ctz(m);
-        seneca_status s = run_round(c, jobs, nj, nullptr, c->L.out_ids, c->L.out_src, c->C.Bmax,
-                                    (unsigned long long*)d_transcript, nullptr, st);
+    const uint64_t kChunk = 1u << 30;
+    while (done < R && c->active) {
+        const uint64_t n = std::min<uint64_t>(R - done, kChunk);
+        seneca_status s = launch_rounds(c, n, 0xffffffffu, nullptr, c->L.out_ids, c->L.out_src, c->C.Bmax, nullptr,
+                                        (unsigned long long*)d_transcript, st);
         if (s) return s;
-        ++done;
+        done += n;
     }
     if (h_rounds) *h_rounds = done;
     return SENECA_OK;
@@ -1090,13 +1219,34 @@ static seneca_status replay(seneca_ctx* c, uint64_t max_rounds, uint32_t n_epoch
 extern "C" seneca_status seneca_replay_epochs(seneca_ctx* c, uint32_t n_epochs, uint64_t* d_transcript,
                                               uint64_t* h_rounds, void* stream) {
     if (!c || n_epochs == 0) { set_error("bad arguments"); return SENECA_EINVAL; }
-    return replay(c, 0, n_epochs, true, d_transcript, h_rounds, (cudaStream_t)stream);
+    if (c->mode != 0) { set_error("replay requires request_mode 0"); return SENECA_ESTATE; }
+    if (!c->active) { set_error("no active job"); return SENECA_ESTATE; }
+    return replay(c, rounds_for_epochs(c, n_epochs), d_transcript, h_rounds, (cudaStream_t)stream);
 }
 
 extern "C" seneca_status seneca_replay_rounds(seneca_ctx* c, uint64_t n_rounds, uint64_t* d_transcript,
                                               uint64_t* h_rounds, void* stream) {
     if (!c) { set_error("bad arguments"); return SENECA_EINVAL; }
-    return replay(c, n_rounds, 0, false, d_transcript, h_rounds, (cudaStream_t)stream);
+    if (c->mode != 0) { set_error("replay requires request_mode 0"); return SENECA_ESTATE; }
+    if (!c->active) { set_error("no active job"); return SENECA_ESTATE; }
+    // stop early when every job has departed
+    uint64_t R = 0;
+    {
+        uint64_t n[kMaxJobs], e[kMaxJobs];
+        uint32_t active = c->active;
+        for (uint32_t j = 0; j < c->C.J; ++j) { n[j] = c->n[j]; e[j] = c->e[j]; }
+        while (R < n_rounds && active) {
+            uint32_t departing = 0;
+            for (uint32_t m = active; m; m &= m - 1) {
+                const uint32_t j = __builtin_ctz(m);
+                n[j] += std::min<uint64_t>(c->C.batch[j], (uint64_t)c->C.N - n[j]);
+                if (n[j] == c->C.N) { n[j] = 0; e[j] += 1; if (e[j] == c->C.target[j]) departing |= 1u << j; }
+            }
+            active &= ~departing;
+            ++R;
+        }
+    }
+    return replay(c, R, d_transcript, h_rounds, (cudaStream_t)stream);
 }
 
 extern "C" seneca_status seneca_read_state(const seneca_ctx* c, seneca_state_view* v) {
@@ -1114,6 +1264,7 @@ extern "C" seneca_status seneca_read_state(const seneca_ctx* c, seneca_state_vie
     v->d_stats = c->L.stats;
     v->d_evicted = (const uint64_t*)c->L.evicted;
     v->d_refilled = (const uint64_t*)c->L.refilled;
+    v->d_phase_cycles = (const uint64_t*)c->L.phase;
     v->round = c->r;
     for (uint32_t j = 0; j < c->C.J; ++j) { v->epoch[j] = c->e[j]; v->consumed[j] = c->n[j]; }
     v->active_mask = c->active;
@@ -1131,24 +1282,30 @@ extern "C" seneca_status seneca_sync_status(seneca_ctx* c, void* stream) {
 
 extern "C" uint64_t seneca_launch_count(const seneca_ctx* c) { return c ? c->launches : 0; }
 
-extern "C" seneca_status seneca_profile(seneca_ctx* c, uint32_t sample_every_rounds) {
+extern "C" seneca_status seneca_profile(seneca_ctx* c, uint32_t enable) {
     if (!c) { set_error("bad arguments"); return SENECA_EINVAL; }
-    c->prof.every = sample_every_rounds;
+    c->profiling = enable ? 1u : 0u;
     return SENECA_OK;
 }
 
 extern "C" seneca_status seneca_profile_read(seneca_ctx* c, seneca_kernel_stat* out, uint32_t cap, uint32_t* n_out) {
     if (!c || (!out && cap)) { set_error("bad arguments"); return SENECA_EINVAL; }
-    c->prof.flush();
     const uint32_t n = std::min<uint32_t>(cap, K_NCLASS);
     for (uint32_t k = 0; k < n; ++k) {
         out[k].name = kKernelNames[k];
-        out[k].launches = c->prof.launches[k];
-        out[k].sampled = c->prof.sampled[k];
-        out[k].sampled_ms = c->prof.ms[k];
+        out[k].launches = c->klaunch[k];
+        out[k].sampled = c->ksampled[k];
+        out[k].sampled_ms = c->kms[k];
     }
     if (n_out) *n_out = K_NCLASS;
     return SENECA_OK;
 }
 
-extern "C" void seneca_destroy(seneca_ctx* c) { delete c; }
+extern "C" void seneca_destroy(seneca_ctx* c) {
+    if (!c) return;
+    if (c->side) { cudaStreamSynchronize(c->side); cudaStreamDestroy(c->side); }
+    if (c->ev_init) cudaEventDestroy(c->ev_init);
+    if (c->ev_a) cudaEventDestroy(c->ev_a);
+    if (c->ev_b) cudaEventDestroy(c->ev_b);
+    delete c;
+}

@@ -68,7 +68,7 @@ class StateView(C.Structure):
         ("words", C.c_uint64),
         ("d_tier_e", C.c_void_p), ("d_tier_d", C.c_void_p), ("d_tier_a", C.c_void_p),
         ("d_seen", C.c_void_p), ("d_cons", C.c_void_p), ("d_stats", C.c_void_p),
-        ("d_evicted", C.c_void_p), ("d_refilled", C.c_void_p),
+        ("d_evicted", C.c_void_p), ("d_refilled", C.c_void_p), ("d_phase_cycles", C.c_void_p),
         ("round", C.c_uint64), ("epoch", C.c_uint64 * 32), ("consumed", C.c_uint64 * 32),
         ("active_mask", C.c_uint32),
     ]
@@ -236,8 +236,8 @@ def launch_count(ctx: int) -> int:
     return lib().seneca_launch_count(ctx)
 
 
-def profile(ctx: int, sample_every_rounds: int):
-    _check(lib().seneca_profile(ctx, sample_every_rounds))
+def profile(ctx: int, enable: int):
+    _check(lib().seneca_profile(ctx, enable))
 
 
 def profile_read(ctx: int) -> dict:
