@@ -42,16 +42,17 @@ def perm(K, n, x):
     if n <= 1:
         return 0
     bits = max(2, (n - 1).bit_length())
-    bits += bits & 1
-    h = bits // 2
-    mask = (1 << h) - 1
+    a = bits // 2
+    c = bits - a
     kk = (K & M32, K >> 32)
     while True:
-        hl, hr = x >> h, x & mask
-        for rd in range(6):
-            f = philox((hr, rd, 0, 0), kk)[0] & mask
-            hl, hr = hr, hl ^ f
-        x = (hl << h) | hr
+        left, right = x >> c, x & ((1 << c) - 1)
+        for rd in range(4):
+            if rd % 2 == 0:
+                left ^= philox((right, rd, 0, 0), kk)[0] & ((1 << a) - 1)
+            else:
+                right ^= philox((left, rd, 0, 0), kk)[0] & ((1 << c) - 1)
+        x = (left << c) | right
         if x < n:
             return x
 

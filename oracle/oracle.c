@@ -78,30 +78,36 @@ uint64_t oracle_key(uint64_t seed, uint64_t purpose, uint64_t a, uint64_t b, uin
     return oracle_splitmix64(seed ^ oracle_splitmix64(word));
 }
 
-/* perm(K, n, x): keyed bijection of [0, n), 0 <= x < n.  Balanced Feistel on
- * 2^bits (bits = max(2, ceil(log2 n)) rounded up to even) restricted to [0,n)
- * by cycle walking.                                                          */
+/* perm(K, n, x): keyed bijection of [0, n), 0 <= x < n (R-O17).  A 4-round
+ * Feistel network on bits = max(2, ceil(log2 n)) bits -- left part a = bits/2
+ * bits, right part c = bits - a bits, rounds alternately xor
+ * philox((other part, round, 0, 0), K)[0] into the left (even rounds) and the
+ * right part (odd rounds) -- restricted to [0, n) by cycle walking (expected
+ * walk 2^bits / n < 2).                                                      */
 uint64_t oracle_perm(uint64_t K, uint64_t n, uint64_t x)
 {
     if (n <= 1) return 0;
     unsigned bits = 0;
     while (((uint64_t)1 << bits) < n) ++bits;
     if (bits < 2) bits = 2;
-    if (bits & 1) ++bits;
-    unsigned h = bits / 2;
-    uint64_t mask = ((uint64_t)1 << h) - 1;
+    unsigned a = bits / 2, c = bits - a;
+    uint64_t maskL = ((uint64_t)1 << a) - 1, maskR = ((uint64_t)1 << c) - 1;
     uint32_t key[2] = { (uint32_t)K, (uint32_t)(K >> 32) };
     do {
-        uint64_t hl = x >> h, hr = x & mask;
-        for (uint32_t rd = 0; rd < 6; ++rd) {
-            uint32_t ctr[4] = { (uint32_t)hr, rd, 0, 0 }, o[4];
-            oracle_philox4x32_10(ctr, key, o);
-            uint64_t F = (uint64_t)o[0] & mask;
-            uint64_t t = hl ^ F;
-            hl = hr;
-            hr = t;
+        uint64_t L = x >> c, R = x & maskR;
+        for (uint32_t rd = 0; rd < 4; ++rd) {
+            uint32_t o[4];
+            if ((rd & 1) == 0) {
+                uint32_t ctr[4] = { (uint32_t)R, rd, 0, 0 };
+                oracle_philox4x32_10(ctr, key, o);
+                L ^= (uint64_t)o[0] & maskL;
+            } else {
+                uint32_t ctr[4] = { (uint32_t)L, rd, 0, 0 };
+                oracle_philox4x32_10(ctr, key, o);
+                R ^= (uint64_t)o[0] & maskR;
+            }
         }
-        x = (hl << h) | hr;
+        x = (L << c) | R;
     } while (x >= n);
     return x;
 }

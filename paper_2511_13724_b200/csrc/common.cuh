@@ -4,8 +4,9 @@
 // paper only says "a pseudo-random number generator", §5.2, and a
 // "predetermined pseudo-random sequence", §1):
 //   philox4x32-10 (Salmon et al., SC'11), splitmix64 key derivation, and a
-//   6-round balanced Feistel network on 2^bits restricted to [0,n) by cycle
-//   walking -- a keyed bijection, so "a permutation slice" needs no sort.
+//   4-round alternating Feistel network on 2^bits restricted to [0,n) by cycle
+//   walking (expected walk < 2) -- a keyed bijection, so "a permutation slice"
+//   needs no sort.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -54,36 +55,36 @@ __device__ __forceinline__ uint32_t philox_w0(uint32_t c0, uint32_t c1, uint32_t
     return c0;
 }
 
-// Domain of a keyed permutation of [0, n): bits = max(2, ceil(log2 n)) rounded
-// up to even, half width h, mask 2^h - 1.
+// Domain of a keyed permutation of [0, n): bits = max(2, ceil(log2 n)); left
+// part a = bits/2 bits, right part c = bits - a bits.
 struct PermDomain {
-    uint32_t n, h, mask;
+    uint32_t n, c, maskL, maskR;
 };
 
 __device__ __forceinline__ PermDomain perm_domain(uint32_t n) {
     uint32_t bits = n <= 1 ? 0u : 32u - __clz(n - 1u);
     bits = bits < 2u ? 2u : bits;
-    bits += bits & 1u;
+    const uint32_t a = bits >> 1;
     PermDomain d;
     d.n = n;
-    d.h = bits >> 1;
-    d.mask = (1u << d.h) - 1u;
+    d.c = bits - a;
+    d.maskL = (1u << a) - 1u;
+    d.maskR = d.c >= 32 ? 0xffffffffu : (1u << d.c) - 1u;
     return d;
 }
 
+// 4-round alternating Feistel (even rounds update the left part from the
+// right, odd rounds the right from the left), cycle-walked into [0, n).
 __device__ __forceinline__ uint32_t perm_apply(uint64_t key, const PermDomain& d, uint32_t x) {
     if (d.n <= 1u) return 0u;
     const uint32_t k0 = (uint32_t)key, k1 = (uint32_t)(key >> 32);
     do {
-        uint32_t hl = x >> d.h, hr = x & d.mask;
-#pragma unroll
-        for (uint32_t rd = 0; rd < 6; ++rd) {
-            const uint32_t f = philox_w0(hr, rd, k0, k1) & d.mask;
-            const uint32_t t = hl ^ f;
-            hl = hr;
-            hr = t;
-        }
-        x = (hl << d.h) | hr;
+        uint32_t L = x >> d.c, R = x & d.maskR;
+        L ^= philox_w0(R, 0u, k0, k1) & d.maskL;
+        R ^= philox_w0(L, 1u, k0, k1) & d.maskR;
+        L ^= philox_w0(R, 2u, k0, k1) & d.maskL;
+        R ^= philox_w0(L, 3u, k0, k1) & d.maskR;
+        x = (L << d.c) | R;
     } while (x >= d.n);
     return x;
 }

@@ -1,14 +1,15 @@
 // mdp.cu -- Model-Driven Partitioning sweep.
 //
-// One CTA per hardware profile:
+// One warp per hardware profile:
 //   prologue  Eqs. 1-4 tier throughputs with the ring-reduce
 //             overhead C = 2(n-1)/n * betaN; integer capacity tables
 //             capAD[p], capE[p] (Eqs. 5-7 floored exactly, R-M6) and the Eq. 9
-//             terms that depend on one coordinate only, all in shared memory;
+//             terms that depend on one coordinate only, in the warp's slice of
+//             shared memory;
 //   main loop every split of the grid: clamped counts (Eqs. 5-8) and
 //             DSI_overall (Eq. 9) in the literal order of R-M7; optional
 //             coalesced write of the full grid row;
-//   epilogue  block argmax, exact ties -> smallest enumeration index (R-M8).
+//   epilogue  warp argmax, exact ties -> smallest enumeration index (R-M8).
 //
 // Bit-exactness with the oracle: every binary64 operation is an explicit
 // round-to-nearest intrinsic (__dadd_rn/__dmul_rn/__ddiv_rn, never contracted
@@ -98,108 +99,96 @@ __device__ void tier_throughputs(const seneca_mdp_profile& p, double dsi[4], uin
     lim[0] = la; lim[1] = ld; lim[2] = le; lim[3] = ls;
 }
 
+// One WARP per profile (8 profiles per CTA in flight): the prologue needs only
+// warp-level synchronisation, so one warp's setup overlaps the other warps'
+// sweeps; each warp iteration stores 32 consecutive grid values (256 B).
 __global__ void __launch_bounds__(kThreads)
 mdp_sweep_kernel(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_profiles, uint32_t g,
                  uint32_t steps, uint32_t n_splits, seneca_mdp_result* __restrict__ results,
                  double* __restrict__ grid) {
-    __shared__ uint64_t s_capAD[kMaxSteps], s_capE[kMaxSteps];
-    __shared__ double s_tA[kMaxSteps], s_tD[kMaxSteps], s_tE[kMaxSteps];
-    __shared__ double s_dsi[4];
-    __shared__ uint8_t s_lim[4];
-    __shared__ int s_valid;
-    __shared__ double s_rv[kThreads / 32];
-    __shared__ uint32_t s_ri[kThreads / 32];
+    constexpr int kWarps = kThreads / 32;
+    __shared__ uint64_t s_capAD[kWarps][kMaxSteps], s_capE[kWarps][kMaxSteps];
+    __shared__ double s_tA[kWarps][kMaxSteps], s_tD[kWarps][kMaxSteps], s_tE[kWarps][kMaxSteps];
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint64_t* capAD = s_capAD[w];
+    uint64_t* capE = s_capE[w];
+    double* tAv = s_tA[w];
+    double* tDv = s_tD[w];
+    double* tEv = s_tE[w];
 
-    for (uint32_t pi = blockIdx.x; pi < n_profiles; pi += gridDim.x) {
+    for (uint32_t pi = blockIdx.x * kWarps + w; pi < n_profiles; pi += gridDim.x * kWarps) {
         const seneca_mdp_profile p = profiles[pi];
-        if (threadIdx.x == 0) {
-            s_valid = profile_valid(p);
-            if (s_valid) {
-                double dsi[4]; uint8_t lim[4];
-                tier_throughputs(p, dsi, lim);
-                for (int k = 0; k < 4; ++k) { s_dsi[k] = dsi[k]; s_lim[k] = lim[k]; }
-            }
-        }
-        __syncthreads();
-        if (!s_valid) {
-            if (threadIdx.x == 0) {
+        const bool valid = profile_valid(p);
+        if (!valid) {
+            if (lane == 0) {
                 seneca_mdp_result r = {};
                 r.status = 1;
                 results[pi] = r;
             }
-            __syncthreads();
             continue;
         }
+        double dsi[4];
+        uint8_t lim[4];
+        tier_throughputs(p, dsi, lim);            // every lane (no shared state, no barrier)
         const uint64_t N = p.n_total;
         const double dN = u2d(N);
-        // capacity tables, exact floors (Eqs. 5-7, R-M6)
-        if (threadIdx.x <= steps) {
-            const uint64_t pct = (uint64_t)threadIdx.x * g;
-            s_capAD[threadIdx.x] = (pct * p.cache_bytes * p.m_den) / (100ull * p.m_num * p.s_data);
-            s_capE[threadIdx.x] = (pct * p.cache_bytes) / (100ull * p.s_data);
+        const uint64_t Xad = p.cache_bytes * p.m_den, Dad = 100ull * p.m_num * p.s_data;
+        const uint64_t De = 100ull * p.s_data;
+        for (uint32_t k = lane; k <= steps; k += 32) {
+            const uint64_t pct = (uint64_t)k * g;
+            const uint64_t cad = (pct * Xad) / Dad, ce = (pct * p.cache_bytes) / De;   // Eqs. 5-7, exact
+            capAD[k] = cad;
+            capE[k] = ce;
+            tAv[k] = __dmul_rn(__ddiv_rn(u2d(cad < N ? cad : N), dN), dsi[0]);
+            tDv[k] = __dmul_rn(__ddiv_rn(u2d(cad), dN), dsi[1]);
+            tEv[k] = __dmul_rn(__ddiv_rn(u2d(ce), dN), dsi[2]);
         }
-        __syncthreads();
-        // one-coordinate Eq. 9 terms: (N_t/N) * DSI_t for an unclamped count
-        if (threadIdx.x <= steps) {
-            const uint64_t ca = s_capAD[threadIdx.x] < N ? s_capAD[threadIdx.x] : N;
-            s_tA[threadIdx.x] = __dmul_rn(__ddiv_rn(u2d(ca), dN), s_dsi[0]);
-            s_tD[threadIdx.x] = __dmul_rn(__ddiv_rn(u2d(s_capAD[threadIdx.x]), dN), s_dsi[1]);
-            s_tE[threadIdx.x] = __dmul_rn(__ddiv_rn(u2d(s_capE[threadIdx.x]), dN), s_dsi[2]);
-        }
-        __syncthreads();
-        const double dsiD = s_dsi[1], dsiE = s_dsi[2], dsiS = s_dsi[3];
-
-        double best = __longlong_as_double(0xfff0000000000000ll);   // -inf
+        __syncwarp();
+        // enumeration index idx -> row a (p_E = 100 - a g), position b in the row (p_A = b g)
+        uint32_t a = 0, b = lane;
+        while (b > a) { b -= a + 1; ++a; }
+        double best = __longlong_as_double(0xfff0000000000000ll);
         uint32_t best_i = 0xffffffffu;
         double* grow = grid ? grid + (uint64_t)pi * n_splits : nullptr;
-        for (uint32_t idx = threadIdx.x; idx < n_splits; idx += kThreads) {
-            // idx -> (row a, position b): row a has p_E = 100 - a*g and a+1 entries
-            uint32_t a = (uint32_t)((sqrtf(8.0f * (float)idx + 1.0f) - 1.0f) * 0.5f);
-            while ((a + 1) * (a + 2) / 2 <= idx) ++a;
-            while (a * (a + 1) / 2 > idx) --a;
-            const uint32_t b = idx - a * (a + 1) / 2;
-            const uint32_t ie = steps - a, id = a - b, ia = b;      // table indices of p_E, p_D, p_A
-            const uint64_t capA = s_capAD[ia], capD = s_capAD[id], capE = s_capE[ie];
-            const uint64_t nA = capA < N ? capA : N;                 // Eq. 5
+        for (uint32_t idx = lane; idx < n_splits; idx += 32) {
+            const uint32_t ie = steps - a, id = a - b, ia = b;
+            const uint64_t cA = capAD[ia], cD = capAD[id], cE = capE[ie];
+            const uint64_t nA = cA < N ? cA : N;                 // Eq. 5
             const uint64_t r1 = N - nA;
-            const uint64_t nD = capD < r1 ? capD : r1;               // Eq. 6
+            const uint64_t nD = cD < r1 ? cD : r1;               // Eq. 6
             const uint64_t r2 = r1 - nD;
-            const uint64_t nE = capE < r2 ? capE : r2;               // Eq. 7
-            const uint64_t nS = r2 - nE;                             // Eq. 8
-            const double tA = s_tA[ia];
-            const double tD = (nD == capD) ? s_tD[id] : __dmul_rn(__ddiv_rn(u2d(nD), dN), dsiD);
-            const double tE = (nE == capE) ? s_tE[ie] : __dmul_rn(__ddiv_rn(u2d(nE), dN), dsiE);
-            const double tS = __dmul_rn(__ddiv_rn(u2d(nS), dN), dsiS);
+            const uint64_t nE = cE < r2 ? cE : r2;               // Eq. 7
+            const uint64_t nS = r2 - nE;                         // Eq. 8
+            const double tA = tAv[ia];
+            const double tD = (nD == cD) ? tDv[id] : __dmul_rn(__ddiv_rn(u2d(nD), dN), dsi[1]);
+            const double tE = (nE == cE) ? tEv[ie] : __dmul_rn(__ddiv_rn(u2d(nE), dN), dsi[2]);
+            const double tS = __dmul_rn(__ddiv_rn(u2d(nS), dN), dsi[3]);
             const double v = __dadd_rn(__dadd_rn(__dadd_rn(tA, tD), tE), tS);   // Eq. 9, R-M7
             if (grow) __stcs(grow + idx, v);
-            if (v > best) { best = v; best_i = idx; }               // idx increases per thread
+            if (v > best) { best = v; best_i = idx; }           // idx increases per lane
+            b += 32;                                             // advance the lane by 32 splits
+            while (b > a) { b -= a + 1; ++a; }
         }
-        // block argmax: larger v, then smaller index
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             const double ov = __shfl_xor_sync(0xffffffffu, best, o);
             const uint32_t oi = __shfl_xor_sync(0xffffffffu, best_i, o);
             if (ov > best || (ov == best && oi < best_i)) { best = ov; best_i = oi; }
         }
-        if ((threadIdx.x & 31) == 0) { s_rv[threadIdx.x >> 5] = best; s_ri[threadIdx.x >> 5] = best_i; }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            for (int w = 1; w < kThreads / 32; ++w)
-                if (s_rv[w] > best || (s_rv[w] == best && s_ri[w] < best_i)) { best = s_rv[w]; best_i = s_ri[w]; }
-            uint32_t a = 0;
-            while ((a + 1) * (a + 2) / 2 <= best_i) ++a;
-            const uint32_t b = best_i - a * (a + 1) / 2;
+        if (lane == 0) {
+            uint32_t ra = 0, rb = best_i;
+            while (rb > ra) { rb -= ra + 1; ++ra; }
             seneca_mdp_result r;
-            r.p_e = (uint8_t)(100 - a * g);
-            r.p_d = (uint8_t)((a - b) * g);
-            r.p_a = (uint8_t)(b * g);
-            r.lim_a = s_lim[0]; r.lim_d = s_lim[1]; r.lim_e = s_lim[2]; r.lim_s = s_lim[3];
+            r.p_e = (uint8_t)(100 - ra * g);
+            r.p_d = (uint8_t)((ra - rb) * g);
+            r.p_a = (uint8_t)(rb * g);
+            r.lim_a = lim[0]; r.lim_d = lim[1]; r.lim_e = lim[2]; r.lim_s = lim[3];
             r.status = 0;
             r.v_best = best;
-            r.dsi_a = s_dsi[0]; r.dsi_d = s_dsi[1]; r.dsi_e = s_dsi[2]; r.dsi_s = s_dsi[3];
+            r.dsi_a = dsi[0]; r.dsi_d = dsi[1]; r.dsi_e = dsi[2]; r.dsi_s = dsi[3];
             results[pi] = r;
         }
-        __syncthreads();
+        __syncwarp();
     }
 }
 
@@ -226,7 +215,9 @@ extern "C" seneca_status seneca_mdp_sweep(const seneca_mdp_profile* d_profiles, 
     }
     const uint32_t steps = 100 / grid_step_pct;
     const uint32_t ns = (uint32_t)seneca_mdp_num_splits(grid_step_pct);
-    const uint32_t blocks = n_profiles < 65535u * 8u ? n_profiles : 65535u * 8u;
+    const uint32_t per_cta = kThreads / 32;
+    uint32_t blocks = (n_profiles + per_cta - 1) / per_cta;
+    blocks = blocks < 65535u * 8u ? blocks : 65535u * 8u;
     mdp_sweep_kernel<<<blocks, kThreads, 0, (cudaStream_t)stream>>>(d_profiles, n_profiles, grid_step_pct,
                                                                    steps, ns, d_results, d_grid);
     SENECA_CUDA_TRY(cudaGetLastError());

@@ -67,7 +67,7 @@ struct JobDev {           // per-job persistent walk state (workspace)
 struct Cfg {
     uint32_t N, NW, NB, NS, NBp;     // samples, words/bitmap, blocks, superblocks, padded blocks
     uint32_t J, Bmax, maxT, cap_a;
-    uint32_t pad;
+    uint32_t Nrow;                   // row stride of the permutation / lap lists (N rounded up to 64)
     uint64_t seed;
     uint32_t batch[kMaxJobs];
     uint32_t target[kMaxJobs];
@@ -267,7 +267,7 @@ struct JobSmem {
 };
 
 __device__ __forceinline__ const uint32_t* list_ptr(const Lay& L, const Cfg& C, uint32_t j, uint32_t e, uint32_t buf) {
-    return buf == 0 ? L.perms + ((size_t)j * C.maxT + e) * C.N : L.laps + ((size_t)j * 2 + (buf - 1)) * C.N;
+    return buf == 0 ? L.perms + ((size_t)j * C.maxT + e) * C.Nrow : L.laps + ((size_t)j * 2 + (buf - 1)) * C.Nrow;
 }
 
 // a1/a2 (R-O1): the first `need` ids of the job's current lap list, from the
@@ -304,16 +304,24 @@ __device__ void job_walk(const Lay& L, const Cfg& C, JobSmem& S, uint32_t* s_req
         }
         const uint32_t cursor = S.cursor, len = S.cur_len;
         const uint32_t* list = list_ptr(L, C, j, e, S.cur_buf);
+        // window [base, base + 8T), base = cursor rounded down to 4 entries (16 B),
+        // two aligned 16-B loads per thread; entries before the cursor are ignored
+        const uint32_t base = cursor & ~3u;
+        const uint32_t p0 = base + tid * kWalkPerThread;
         uint32_t ids[kWalkPerThread];
         uint32_t flags = 0, cnt = 0;
+        if (p0 + kWalkPerThread <= len) {
+            const uint4 v0 = ldcg4(list + p0), v1 = ldcg4(list + p0 + 4);
+            ids[0] = v0.x; ids[1] = v0.y; ids[2] = v0.z; ids[3] = v0.w;
+            ids[4] = v1.x; ids[5] = v1.y; ids[6] = v1.z; ids[7] = v1.w;
+        } else {
 #pragma unroll
-        for (uint32_t k = 0; k < kWalkPerThread; ++k) {
-            const uint32_t p = cursor + tid * kWalkPerThread + k;
-            ids[k] = p < len ? ldcg(list + p) : 0xffffffffu;
+            for (uint32_t k = 0; k < kWalkPerThread; ++k) ids[k] = p0 + k < len ? ldcg(list + p0 + k) : 0u;
         }
 #pragma unroll
         for (uint32_t k = 0; k < kWalkPerThread; ++k) {
-            if (ids[k] != 0xffffffffu) {
+            const uint32_t p = p0 + k;
+            if (p >= cursor && p < len) {
                 const uint32_t id = ids[k];
                 if (!((ldcg(seen_j + (id >> 5)) >> (id & 31)) & 1u)) { flags |= 1u << k; ++cnt; }
             }
@@ -326,7 +334,7 @@ __device__ void job_walk(const Lay& L, const Cfg& C, JobSmem& S, uint32_t* s_req
         for (uint32_t k = 0; k < kWalkPerThread; ++k) {
             if (flags & (1u << k)) {
                 if (r < remaining) s_req[taken + r] = ids[k];
-                if (r == remaining - 1) S.newcursor = cursor + tid * kWalkPerThread + k + 1;
+                if (r == remaining - 1) S.newcursor = p0 + k + 1;
                 ++r;
             }
         }
@@ -335,7 +343,7 @@ __device__ void job_walk(const Lay& L, const Cfg& C, JobSmem& S, uint32_t* s_req
             if (tid == 0) S.cursor = S.newcursor;
             taken = need;
         } else {
-            if (tid == 0) S.cursor = min(cursor + kWalkPerThread * T, len);
+            if (tid == 0) S.cursor = min(base + kWalkPerThread * T, len);
             taken += tot;
         }
         __syncthreads();
@@ -485,8 +493,8 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
         block_exclusive_scan(c, &q1, S.scan);
     }
     if (P.mode == 0 && q > 0) {
-        uint32_t* cur_list = L.laps + ((size_t)j * 2 + (S.cur_buf - 1)) * C.N;   // only used if q1 > 0
-        uint32_t* nxt_list = L.laps + ((size_t)j * 2 + (S.nxt_buf - 1)) * C.N;
+        uint32_t* cur_list = L.laps + ((size_t)j * 2 + (S.cur_buf - 1)) * C.Nrow;   // only used if q1 > 0
+        uint32_t* nxt_list = L.laps + ((size_t)j * 2 + (S.nxt_buf - 1)) * C.Nrow;
         for (uint32_t u = tid; u < q; u += T) {
             const uint32_t id = s_req[s_miss[u]];
             if (u < q1) cur_list[S.cur_len + u] = id;
@@ -536,17 +544,19 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
 
 // ------------------------------------------------------------------ maintain (a7)
 struct MaintSmem {
-    uint32_t ne, kmax, deficit0, PS, sizeA;
+    uint32_t ne, kmax, kspec, deficit0, PS, sizeA;
     uint32_t add[kMaxJobs];
     uint32_t scan[33];
 };
 
-__device__ void maint_refill_select(const Lay& L, const Cfg& C, MaintSmem& M, uint32_t* s_pre, uint64_t r, uint32_t k) {
-    if (k == 0) return;
-    load_sup_prefix(L, C, 3 * C.J, s_pre, M.scan);
+// keyed refill ranks rho(u) over the storage pool as of round start (R-O8),
+// located through the S-pool counts; the prefix s_pre must be loaded.
+__device__ void maint_refill_select(const Lay& L, const Cfg& C, MaintSmem& M, const uint32_t* s_pre, uint64_t r,
+                                    uint32_t u0, uint32_t u1) {
+    if (u1 <= u0) return;
     const uint64_t key = derive_key(C.seed, PUR_REFILL, 0, r, 0);
     const PermDomain dom = perm_domain(M.PS);
-    for (uint32_t u = threadIdx.x; u < k; u += blockDim.x)
+    for (uint32_t u = u0 + threadIdx.x; u < u1; u += blockDim.x)
         L.fill_list[u] = pool_select(L, C, 3 * C.J, T_S, 0, s_pre, perm_apply(key, dom, u));
     __syncthreads();
 }
@@ -588,7 +598,12 @@ __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSm
     __syncthreads();
     const uint32_t ne = M.ne;
     const uint32_t k = min(M.deficit0 + ne, M.PS);
-    if (!speculated) maint_refill_select(L, C, M, s_pre, r, k);
+    if (!speculated) {
+        if (k) load_sup_prefix(L, C, 3 * C.J, s_pre, M.scan);
+        maint_refill_select(L, C, M, s_pre, r, 0, k);
+    } else if (k > M.kspec) {
+        maint_refill_select(L, C, M, s_pre, r, M.kspec, k);      // beyond the speculated ranks
+    }
     const uint32_t spidx = 3 * C.J;
     for (uint32_t u = tid; u < ne; u += T) {
         const uint32_t i = L.evict_list[u];
@@ -692,7 +707,14 @@ ods_rounds(Lay L, Cfg C, Launch P) {
                     M.kmax = min(M.deficit0 + cand, M.PS);
                 }
                 __syncthreads();
-                if (!full_scan) { maint_refill_select(L, C, M, s_pre, r, M.kmax); spec = true; }
+                if (!full_scan) {
+                    // one rank per thread ahead of time; the rest (if any) after eviction
+                    if (tid == 0) M.kspec = min(M.kmax, blockDim.x);
+                    __syncthreads();
+                    if (M.kspec) load_sup_prefix(L, C, 3 * C.J, s_pre, M.scan);
+                    maint_refill_select(L, C, M, s_pre, r, 0, M.kspec);
+                    spec = true;
+                }
             }
         } else if ((part >> j) & 1u) {
             if (S.recount) { job_recount(L, C, j, s_pre); if (tid == 0) S.recount = 0; __syncthreads(); }
@@ -767,7 +789,7 @@ __global__ void ods_perm_all(Lay L, Cfg C, uint32_t chunk) {
         const uint32_t part = (uint32_t)(c % per);
         if (e >= C.target[j]) continue;
         const uint64_t key = derive_key(C.seed, PUR_REQ, j, e, 0);
-        uint32_t* out = L.perms + ((size_t)j * C.maxT + e) * C.N;
+        uint32_t* out = L.perms + ((size_t)j * C.maxT + e) * C.Nrow;
         const uint32_t lo = part * chunk, hi = min(lo + chunk, C.N);
         for (uint32_t pos = lo + threadIdx.x; pos < hi; pos += blockDim.x) out[pos] = perm_apply(key, dom, pos);
         __syncthreads();
@@ -942,6 +964,7 @@ Sizes compute_sizes(const seneca_cache_config* cfg) {
     }
     C.cap_a = (uint32_t)cfg->cap_a;
     C.seed = cfg->seed;
+    C.Nrow = (C.N + 63) & ~63u;
     const size_t W = (size_t)C.NW * 4, P = 3 * (size_t)C.J + 1;
     const size_t capl = std::max<size_t>(cfg->cap_a, 1) * 4;
     const size_t sz[] = {
@@ -950,8 +973,8 @@ Sizes compute_sizes(const seneca_cache_config* cfg) {
         W,                                                  // 5 evmark
         P * C.NBp * 4, P * C.NS * 4, P * 4,                 // 6-8 counts
         4,                                                  // 9 a_size
-        (size_t)C.J * C.maxT * C.N * 4,                     // 10 perms
-        (size_t)C.J * 2 * C.N * 4,                          // 11 laps
+        (size_t)C.J * C.maxT * C.Nrow * 4,                  // 10 perms
+        (size_t)C.J * 2 * C.Nrow * 4,                       // 11 laps
         (size_t)C.J * C.maxT * 4, (size_t)C.J * C.maxT * 4, // 12-13 perm_ready, perm_done
         (size_t)C.J * sizeof(JobDev),                       // 14 jobs
         (size_t)C.J * C.Bmax * 4, (size_t)C.J * C.Bmax,     // 15-16 out_ids, out_src
