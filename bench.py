@@ -324,15 +324,18 @@ def main():
     st_raw = ws[off:off + len(c["batch"]) * v.max_target * S.STATS_DTYPE.itemsize].cpu().numpy().view(S.STATS_DTYPE)
     st_raw = st_raw.reshape(len(c["batch"]), v.max_target)
     served_ok = bool(np.all(st_raw["served"].sum(axis=2) == c["n_total"]))
-    ph = ws[v.d_phase_cycles - ws.data_ptr():v.d_phase_cycles - ws.data_ptr() + 64].cpu().numpy().view(np.uint64)
-    ph_names = ["job_phase", "job_barrier1_wait", "walk_next", "job_barrier2_wait",
-                "maint_spec_refill", "maint_barrier1_wait", "maint_apply", "maint_barrier2_wait"]
-    phase_share = {}
-    for base in (0, 4):
-        tot = float(ph[base:base + 4].sum())
-        for k in range(4):
-            phase_share[ph_names[base + k]] = round(float(ph[base + k]) / tot, 4) if tot else None
     parity["ods_served_per_job_epoch_equals_N"] = served_ok
+    ph = ws[v.d_phase_cycles - ws.data_ptr():v.d_phase_cycles - ws.data_ptr() + 128].cpu().numpy().view(np.uint64)
+    ph_names = {0: "job_epoch_start", 1: "job_classify", 2: "job_substitute", 3: "job_respond",
+                4: "job_barrier1_wait", 5: "job_walk_next", 6: "job_barrier2_wait",
+                8: "maint_spec_prefix", 9: "maint_spec_refill_ranks", 10: "maint_barrier1_wait",
+                11: "maint_evict_decide", 12: "maint_apply", 13: "maint_barrier2_wait"}
+    phase_share = {}
+    for base in (0, 8):
+        tot = float(ph[base:base + 8].sum())
+        for k in range(8):
+            if base + k in ph_names:
+                phase_share[ph_names[base + k]] = round(float(ph[base + k]) / tot, 4) if tot else None
     if os.path.exists(gold_path):
         gold = json.load(open(gold_path))
         ok = all(int(st_raw[j, e]["digest"]) == int(s_["digest"]) and

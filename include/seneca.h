@@ -165,9 +165,13 @@ typedef struct {
     const seneca_job_epoch_stats* d_stats; /* [n_jobs][max_target]                        */
     const uint64_t* d_evicted;          /* total evictions                                 */
     const uint64_t* d_refilled;         /* total refills                                   */
-    const uint64_t* d_phase_cycles;     /* [8] per-phase SM cycles when profiling: job CTA 0
-                                           {job phase, barrier 1, walk, barrier 2}, maintain
-                                           CTA {speculative refill, barrier 1, apply, barrier 2} */
+    const uint64_t* d_phase_cycles;     /* [16] SM cycles per phase when profiling.  Job CTA 0:
+                                           [0] recount/epoch end [1] classify [2] substitute
+                                           [3] respond [4] barrier-1 wait [5] next walk
+                                           [6] barrier-2 wait; maintain CTA: [8] speculative
+                                           prefix [9] speculative refill ranks [10] barrier-1
+                                           wait [11] eviction decision [12] remaining refill
+                                           ranks + apply [13] barrier-2 wait                    */
     uint64_t round;                     /* rounds executed                                 */
     uint64_t epoch[32];                 /* host mirror: current epoch of each job          */
     uint64_t consumed[32];              /* host mirror: samples consumed in current epoch  */

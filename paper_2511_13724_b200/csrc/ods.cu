@@ -96,7 +96,7 @@ struct Lay {
     unsigned long long *evicted, *refilled;
     uint32_t *err;
     uint32_t *bar;                   // [2] barrier count, generation
-    unsigned long long *phase;       // [8] accumulated cycles per phase
+    unsigned long long *phase;       // [16] accumulated cycles per phase (see seneca.h)
 };
 
 struct Launch {
@@ -255,6 +255,20 @@ __device__ void round_barrier(uint32_t* bar, uint32_t nctas, uint32_t& gen) {
     __syncthreads();
 }
 
+// ------------------------------------------------------------------ per-CTA phase timer (profiling)
+struct PhaseTimer {
+    long long last;
+    unsigned long long acc[8];
+    uint32_t on;
+    __device__ __forceinline__ void tick(uint32_t slot) {
+        if (on && threadIdx.x == 0) {
+            const long long t = clock64();
+            acc[slot] += (unsigned long long)(t - last);
+            last = t;
+        }
+    }
+};
+
 // ------------------------------------------------------------------ shared state of a job CTA
 struct JobSmem {
     uint32_t cur_buf, nxt_buf, cursor, cur_len, nxt_len;
@@ -401,7 +415,8 @@ __device__ void job_recount(const Lay& L, const Cfg& C, uint32_t j, uint32_t* s_
 
 // a3-a6 for job j in round r: classify, substitute, respond.
 __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& S, uint32_t* s_req, uint32_t* s_miss,
-                          uint32_t* s_sub, uint32_t* s_pre, uint32_t j, uint64_t r, uint32_t e, uint32_t nbase) {
+                          uint32_t* s_sub, uint32_t* s_pre, uint32_t j, uint64_t r, uint32_t e, uint32_t nbase,
+                          PhaseTimer& TM) {
     const uint32_t tid = threadIdx.x, T = blockDim.x;
     const uint32_t need = S.need;
     uint32_t* seen_j = L.seen + (size_t)j * C.NW;
@@ -448,6 +463,7 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
         S.k[2] = min(m - S.k[0] - S.k[1], pe);
     }
     __syncthreads();
+    TM.tick(1);
 
     // a4/a5: misses in slot order take substitutes A -> D -> E at keyed ranks (R-O2)
     const uint32_t k0 = S.k[0], k1 = S.k[1], k2 = S.k[2];
@@ -477,6 +493,7 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
             count_add(L, C, j * 3 + tt, id, 0xffffffffu);
         }
     }
+    TM.tick(2);
     // remaining misses are fetched from storage (R-O18)
     for (uint32_t u = q + tid; u < S.m; u += T) {
         const uint32_t s = s_miss[u], i = s_req[s];
@@ -540,6 +557,7 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
     }
     if (tid == 0) L.n_aserved[j] = S.n_as;
     __syncthreads();
+    TM.tick(3);
 }
 
 // ------------------------------------------------------------------ maintain (a7)
@@ -564,7 +582,8 @@ __device__ void maint_refill_select(const Lay& L, const Cfg& C, MaintSmem& M, co
 // eviction of A entries consumed by every active job (R-O5, R-O6), refill from
 // the storage pool as of round start (R-O8), counts kept exact.
 __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSmem& M, uint32_t* s_pre,
-                            uint64_t r, uint32_t part, uint32_t active, bool full_scan, bool speculated) {
+                            uint64_t r, uint32_t part, uint32_t active, bool full_scan, bool speculated,
+                            PhaseTimer& TM) {
     const uint32_t tid = threadIdx.x, T = blockDim.x;
     if (tid == 0) M.ne = 0;
     if (tid < kMaxJobs) M.add[tid] = 0;
@@ -596,6 +615,7 @@ __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSm
         }
     }
     __syncthreads();
+    TM.tick(3);
     const uint32_t ne = M.ne;
     const uint32_t k = min(M.deficit0 + ne, M.PS);
     if (!speculated) {
@@ -635,6 +655,7 @@ __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSm
         *L.refilled += k;
     }
     __syncthreads();
+    TM.tick(4);
 }
 
 // ------------------------------------------------------------------ the persistent round kernel
@@ -649,8 +670,12 @@ ods_rounds(Lay L, Cfg C, Launch P) {
     const bool is_maint = cta == C.J;
     const uint32_t j = cta;
     uint32_t gen = ldcg(L.bar + 1);
-    long long t_mark = 0;
-    unsigned long long t_acc[4] = {0, 0, 0, 0};
+    __shared__ PhaseTimer TM;
+    if (tid == 0) {
+        TM.on = P.timing;
+        TM.last = clock64();
+        for (int k = 0; k < 8; ++k) TM.acc[k] = 0;
+    }
 
     // shared memory carve: job CTA s_req | s_miss | s_sub [Bmax] + s_pre [3][NS]; maintain CTA s_pre [NS]
     uint32_t* s_req = smem;
@@ -693,7 +718,6 @@ ods_rounds(Lay L, Cfg C, Launch P) {
         }
         const uint32_t active_after = s_active & ~departing;
         const bool full_scan = departing != 0;
-        if (P.timing && tid == 0) t_mark = clock64();
 
         bool spec = false;
         if (is_maint) {
@@ -712,13 +736,16 @@ ods_rounds(Lay L, Cfg C, Launch P) {
                     if (tid == 0) M.kspec = min(M.kmax, blockDim.x);
                     __syncthreads();
                     if (M.kspec) load_sup_prefix(L, C, 3 * C.J, s_pre, M.scan);
+                    TM.tick(0);
                     maint_refill_select(L, C, M, s_pre, r, 0, M.kspec);
+                    TM.tick(1);
                     spec = true;
                 }
             }
         } else if ((part >> j) & 1u) {
             if (S.recount) { job_recount(L, C, j, s_pre); if (tid == 0) S.recount = 0; __syncthreads(); }
-            job_round(L, C, P, S, s_req, s_miss, s_sub, s_pre, j, r, s_e[j], s_n[j]);
+            TM.tick(0);
+            job_round(L, C, P, S, s_req, s_miss, s_sub, s_pre, j, r, s_e[j], s_n[j], TM);
             // a8 (R-O16): the epoch ends with this batch -> reset seen_j and the walk
             if (s_n[j] + S.need == C.N) {
                 uint4* sj = reinterpret_cast<uint4*>(L.seen + (size_t)j * C.NW);
@@ -729,10 +756,11 @@ ods_rounds(Lay L, Cfg C, Launch P) {
                 }
                 __syncthreads();
             }
+            TM.tick(0);
         }
-        if (P.timing && tid == 0) { const long long t = clock64(); t_acc[0] += t - t_mark; t_mark = t; }
+        if (is_maint) TM.tick(1);
         round_barrier(L.bar, nctas, gen);
-        if (P.timing && tid == 0) { const long long t = clock64(); t_acc[1] += t - t_mark; t_mark = t; }
+        TM.tick(is_maint ? 2 : 4);
 
         // schedule update (every CTA, identically)
         if (tid == 0) {
@@ -753,14 +781,15 @@ ods_rounds(Lay L, Cfg C, Launch P) {
                     M.deficit0 = C.cap_a - M.sizeA;
                 }
                 __syncthreads();
-                maint_apply(L, C, P, M, s_pre, r, part, active_after, full_scan, spec);
+                TM.tick(2);
+                maint_apply(L, C, P, M, s_pre, r, part, active_after, full_scan, spec, TM);
             }
         } else if (rr + 1 < P.rounds && ((active_after & P.subset) >> j & 1u)) {
             job_walk(L, C, S, s_req, j, s_e[j], need_of(j));   // the next round's request
         }
-        if (P.timing && tid == 0) { const long long t = clock64(); t_acc[2] += t - t_mark; t_mark = t; }
+        TM.tick(is_maint ? 4 : 5);
         round_barrier(L.bar, nctas, gen);
-        if (P.timing && tid == 0) { const long long t = clock64(); t_acc[3] += t - t_mark; t_mark = t; }
+        TM.tick(is_maint ? 5 : 6);
     }
     // persist the walk state
     if (!is_maint && tid == 0) {
@@ -768,10 +797,9 @@ ods_rounds(Lay L, Cfg C, Launch P) {
         jd.cur_buf = S.cur_buf; jd.nxt_buf = S.nxt_buf; jd.cursor = S.cursor;
         jd.cur_len = S.cur_len; jd.nxt_len = S.nxt_len; jd.recount = S.recount;
     }
-    if (P.timing && tid == 0) {
-        const uint32_t base = is_maint ? 4 : 0;
-        if (is_maint || cta == 0)
-            for (int k = 0; k < 4; ++k) atomicAdd(L.phase + base + k, t_acc[k]);
+    if (P.timing && tid == 0 && (is_maint || cta == 0)) {
+        const uint32_t base = is_maint ? 8 : 0;
+        for (int k = 0; k < 8; ++k) atomicAdd(L.phase + base + k, TM.acc[k]);
     }
 }
 
@@ -981,7 +1009,7 @@ Sizes compute_sizes(const seneca_cache_config* cfg) {
         (size_t)C.J * C.Bmax * 4, (size_t)C.J * 4,          // 17-18 aserved, n_aserved
         capl, capl + (size_t)C.J * C.Bmax * 4,              // 19-20 evict, fill
         (size_t)C.J * C.maxT * sizeof(seneca_job_epoch_stats),  // 21 stats
-        8, 8, 4, 8, 64,                                     // 22-26 evicted, refilled, err, bar, phase
+        8, 8, 4, 8, 128,                                    // 22-26 evicted, refilled, err, bar, phase
     };
     size_t at = 0;
     for (size_t k = 0; k < sizeof(sz) / sizeof(sz[0]); ++k) {

@@ -210,9 +210,11 @@ def test_protocol_violations_and_state_errors():
     with pytest.raises(S.SenecaError) as ei:
         g.next_batch([0], requested=[[1, 2, 3, 100]])        # out of range
     assert ei.value.status == S.EPROTO
-    g.next_batch([0, 1], requested=[[1, 2, 3, 4], [1, 2, 3, 4]])   # two jobs may request the same ids
+    ids, src, lens = g.next_batch([0, 1], requested=[[1, 2, 3, 4], [1, 2, 3, 4]])  # same ids, two jobs: fine
+    delivered = int(ids[0, 0].item())                           # seen by job 0 now (a replaced miss is not)
+    fresh = [i for i in range(100) if i not in ids[0, :4].tolist() and i not in (1, 2, 3, 4)][:3]
     with pytest.raises(S.SenecaError) as ei:
-        g.next_batch([0], requested=[[4, 5, 6, 7]])          # 4 already seen by job 0
+        g.next_batch([0], requested=[[delivered] + fresh])      # already seen by job 0
     assert ei.value.status == S.EPROTO
     with pytest.raises(S.SenecaError) as ei:
         g.next_batch([0, 0], requested=[[5, 6, 7, 8], [9, 10, 11, 12]])
