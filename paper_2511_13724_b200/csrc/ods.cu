@@ -76,7 +76,7 @@ struct Cfg {
 struct Lay {
     uint32_t *bm_e, *bm_d, *bm_a;    // [NW]
     uint32_t *seen, *cons;           // [J][NW]
-    uint32_t *evmark;                // [NW]
+    uint32_t *cons_cnt;              // [N] active consumers of each A entry (R-O5)
     uint32_t *cnt_blk;               // [3J+1][NBp]
     uint32_t *cnt_sup;               // [3J+1][NS]
     uint32_t *cnt_tot;               // [3J+1]
@@ -88,8 +88,8 @@ struct Lay {
     JobDev *jobs;                    // [J]
     uint32_t *out_ids;               // [J][Bmax] replay scratch
     uint8_t *out_src;                // [J][Bmax]
-    uint32_t *aserved;               // [J][Bmax] A-served ids of the round
-    uint32_t *n_aserved;             // [J]
+    uint32_t *evict_push;            // [J*Bmax] entries whose consumer count reached |active| this round
+    uint32_t *ne_ctr;                // [1] length of evict_push
     uint32_t *evict_list;            // [max(cap_a,1)]
     uint32_t *fill_list;             // [max(cap_a,1) + J*Bmax]
     seneca_job_epoch_stats *stats;   // [J][maxT]
@@ -275,7 +275,7 @@ struct JobSmem {
     uint32_t wrap_slot, need, newcursor, walk_err;
     uint32_t m, k[3], tot[3], hits[3];
     uint32_t recount;
-    uint32_t n_as;
+    uint32_t hist[8];
     uint32_t scan[33];
     unsigned long long red[(kThreads / 32) * 13];
 };
@@ -415,15 +415,15 @@ __device__ void job_recount(const Lay& L, const Cfg& C, uint32_t j, uint32_t* s_
 
 // a3-a6 for job j in round r: classify, substitute, respond.
 __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& S, uint32_t* s_req, uint32_t* s_miss,
-                          uint32_t* s_sub, uint32_t* s_pre, uint32_t j, uint64_t r, uint32_t e, uint32_t nbase,
-                          PhaseTimer& TM) {
+                          uint32_t* s_sub, uint32_t* s_oid, uint8_t* s_osrc, uint32_t* s_pre, uint32_t j, uint64_t r,
+                          uint32_t e, uint32_t nbase, uint32_t n_act, PhaseTimer& TM) {
     const uint32_t tid = threadIdx.x, T = blockDim.x;
     const uint32_t need = S.need;
     uint32_t* seen_j = L.seen + (size_t)j * C.NW;
     uint32_t* cons_j = L.cons + (size_t)j * C.NW;
     const size_t row = (size_t)P.row_of_job[j] * P.out_stride;
     if (tid < 3) { S.hits[tid] = 0; S.tot[tid] = ldcg(L.cnt_tot + j * 3 + tid); }
-    if (tid == 0) S.n_as = 0;
+    if (tid < 8) S.hist[tid] = 0;
     __syncthreads();
 
     // a3: hits (E, D, or A not consumed by j, R-O13) join seen_j now
@@ -440,6 +440,8 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
             if (hit) {
                 P.out_ids[row + s] = i;
                 P.out_src[row + s] = (uint8_t)t;
+                s_oid[s] = i;
+                s_osrc[s] = (uint8_t)t;
                 atomicOr(seen_j + w, b);
                 if (t == T_A) atomicOr(cons_j + w, b);
                 count_add(L, C, pool_of(j, t), i, 0xffffffffu);
@@ -481,6 +483,8 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
             const uint32_t s = s_miss[u];
             P.out_ids[row + s] = id;
             P.out_src[row + s] = (uint8_t)(t | SUBST);
+            s_oid[s] = id;
+            s_osrc[s] = (uint8_t)(t | SUBST);
             s_sub[u] = id;
         }
         __syncthreads();
@@ -499,6 +503,8 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
         const uint32_t s = s_miss[u], i = s_req[s];
         P.out_ids[row + s] = i;
         P.out_src[row + s] = (uint8_t)T_S;
+        s_oid[s] = i;
+        s_osrc[s] = (uint8_t)T_S;
         atomicOr(seen_j + (i >> 5), 1u << (i & 31));
     }
     // deferred (replaced) misses are requested again on the next lap (R-O1):
@@ -526,36 +532,44 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
         L.cnt_tot[j * 3 + 2] = S.tot[2] - k2;
     }
 
-    // a6: counters, digest, transcript, A-served list for maintain
-    unsigned long long acc[13];
-#pragma unroll
-    for (int k = 0; k < 13; ++k) acc[k] = 0;
+    // a6: counters (per-warp ballot histogram of the 8 source codes), digest,
+    // transcript; an A entry whose consumer count reaches |active| is pushed
+    // for eviction at the round end (R-O5)
+    unsigned long long dig = 0;
     unsigned long long* trow = P.transcript ? P.transcript + ((size_t)j * C.maxT + e) * C.N : nullptr;
-    uint32_t* as_j = L.aserved + (size_t)j * C.Bmax;
-    for (uint32_t s = tid; s < need; s += T) {
-        const uint32_t i = P.out_ids[row + s];
-        const uint32_t src = P.out_src[row + s];
-        const uint32_t t = src & 3u;
-        acc[t] += 1;
-        if (src & SUBST) acc[4 + t] += 1;
-        else if (t != T_S) acc[8 + t] += 1;
-        acc[12] += splitmix64(((uint64_t)(nbase + s) << 35) | ((uint64_t)src << 32) | i);
-        if (trow) trow[nbase + s] = ((unsigned long long)src << 32) | i;
-        if (t == T_A) as_j[atomicAdd(&S.n_as, 1u)] = i;
-    }
+    const uint32_t lane = tid & 31;
+    for (uint32_t base = 0; base < need; base += T) {
+        const uint32_t s = base + tid;
+        uint32_t src = 0xffu;
+        if (s < need) {
+            const uint32_t i = s_oid[s];
+            src = s_osrc[s];
+            dig += splitmix64(((uint64_t)(nbase + s) << 35) | ((uint64_t)src << 32) | i);
+            if (trow) trow[nbase + s] = ((unsigned long long)src << 32) | i;
+            if ((src & 3u) == T_A) {
+                if (atomicAdd(L.cons_cnt + i, 1u) + 1u == n_act) L.evict_push[atomicAdd(L.ne_ctr, 1u)] = i;
+            }
+        }
 #pragma unroll
-    for (int k = 0; k < 13; ++k) {
-        const unsigned long long v = warp_sum(acc[k]);
-        if ((tid & 31) == 0) S.red[(tid >> 5) * 13 + k] = v;
+        for (uint32_t v = 0; v < 8; ++v) {
+            const uint32_t bal = __ballot_sync(0xffffffffu, src == v);
+            if (lane == 0 && bal) atomicAdd(&S.hist[v], (uint32_t)__popc(bal));
+        }
     }
+    dig = warp_sum(dig);
+    if (lane == 0) S.red[tid >> 5] = dig;
     __syncthreads();
-    if (tid < 13) {
-        unsigned long long v = 0;
-        for (uint32_t w = 0; w < T / 32; ++w) v += S.red[w * 13 + tid];
-        unsigned long long* st = reinterpret_cast<unsigned long long*>(L.stats + (size_t)j * C.maxT + e);
-        st[tid] += v;
+    if (tid == 0) {
+        unsigned long long d = 0;
+        for (uint32_t w = 0; w < T / 32; ++w) d += S.red[w];
+        seneca_job_epoch_stats* st = L.stats + (size_t)j * C.maxT + e;
+        for (uint32_t t = 0; t < 4; ++t) {
+            st->served[t] += S.hist[t] + S.hist[t | SUBST];
+            st->subst[t] += S.hist[t | SUBST];
+            if (t != T_S) st->req_hits[t] += S.hist[t];
+        }
+        st->digest += d;
     }
-    if (tid == 0) L.n_aserved[j] = S.n_as;
     __syncthreads();
     TM.tick(3);
 }
@@ -582,39 +596,38 @@ __device__ void maint_refill_select(const Lay& L, const Cfg& C, MaintSmem& M, co
 // eviction of A entries consumed by every active job (R-O5, R-O6), refill from
 // the storage pool as of round start (R-O8), counts kept exact.
 __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSmem& M, uint32_t* s_pre,
-                            uint64_t r, uint32_t part, uint32_t active, bool full_scan, bool speculated,
-                            PhaseTimer& TM) {
+                            uint64_t r, uint32_t active, bool full_scan, bool speculated, PhaseTimer& TM) {
     const uint32_t tid = threadIdx.x, T = blockDim.x;
-    if (tid == 0) M.ne = 0;
+    if (tid == 0) M.ne = full_scan ? 0u : ldcg(L.ne_ctr);
     if (tid < kMaxJobs) M.add[tid] = 0;
     __syncthreads();
+    const uint32_t* ev_list = L.evict_push;
     if (full_scan) {
+        // the active set changed (R-O6): every A entry is a candidate; the consumer
+        // counts of the survivors are rebuilt for the new active set
         for (uint32_t w = tid; w < C.NW; w += T) {
-            uint32_t ev = ldcg(L.bm_a + w);
-            for (uint32_t m = active; m && ev; m &= m - 1) ev &= ldcg(L.cons + (size_t)(__ffs(m) - 1) * C.NW + w);
+            const uint32_t a_w = ldcg(L.bm_a + w);
+            if (!a_w) continue;
+            uint32_t ev = a_w;
+            uint32_t cw[kMaxJobs];
+            uint32_t na = 0;
+            for (uint32_t m = active; m; m &= m - 1) { cw[na] = ldcg(L.cons + (size_t)(__ffs(m) - 1) * C.NW + w); ev &= cw[na]; ++na; }
             if (ev) {
                 const uint32_t base = atomicAdd(&M.ne, (uint32_t)__popc(ev));
                 uint32_t c = 0;
                 for (uint32_t v = ev; v; v &= v - 1) L.evict_list[base + c++] = w * 32u + (__ffs(v) - 1);
             }
-        }
-    } else {
-        for (uint32_t pm = part; pm; pm &= pm - 1) {
-            const uint32_t j = __ffs(pm) - 1;
-            const uint32_t na = ldcg(L.n_aserved + j);
-            const uint32_t* as_j = L.aserved + (size_t)j * C.Bmax;
-            for (uint32_t f = tid; f < na; f += T) {
-                const uint32_t i = ldcg(as_j + f);
-                const uint32_t w = i >> 5, b = 1u << (i & 31);
-                uint32_t all = ldcg(L.bm_a + w);
-                for (uint32_t m = active; m; m &= m - 1) all &= ldcg(L.cons + (size_t)(__ffs(m) - 1) * C.NW + w);
-                if (!(all & b)) continue;
-                if (atomicOr(L.evmark + w, b) & b) continue;      // claimed by another job's entry
-                L.evict_list[atomicAdd(&M.ne, 1u)] = i;
+            for (uint32_t v = a_w & ~ev; v; v &= v - 1) {
+                const uint32_t bit = __ffs(v) - 1;
+                uint32_t cnt = 0;
+                for (uint32_t k = 0; k < na; ++k) cnt += (cw[k] >> bit) & 1u;
+                L.cons_cnt[w * 32u + bit] = cnt;
             }
         }
+        ev_list = L.evict_list;
     }
     __syncthreads();
+    if (tid == 0) *L.ne_ctr = 0;
     TM.tick(3);
     const uint32_t ne = M.ne;
     const uint32_t k = min(M.deficit0 + ne, M.PS);
@@ -626,11 +639,11 @@ __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSm
     }
     const uint32_t spidx = 3 * C.J;
     for (uint32_t u = tid; u < ne; u += T) {
-        const uint32_t i = L.evict_list[u];
+        const uint32_t i = ldcg(ev_list + u);
         const uint32_t w = i >> 5, b = 1u << (i & 31);
         atomicAnd(L.bm_a + w, ~b);
-        if (!full_scan) atomicAnd(L.evmark + w, ~b);
         for (uint32_t a = 0; a < C.J; ++a) atomicAnd(L.cons + (size_t)a * C.NW + w, ~b);
+        L.cons_cnt[i] = 0;
         count_add(L, C, spidx, i, 1u);
     }
     for (uint32_t u = tid; u < k; u += T) {
@@ -681,7 +694,13 @@ ods_rounds(Lay L, Cfg C, Launch P) {
     uint32_t* s_req = smem;
     uint32_t* s_miss = smem + C.Bmax;
     uint32_t* s_sub = smem + 2 * C.Bmax;
-    uint32_t* s_pre = smem + 3 * C.Bmax;
+    uint32_t* s_oid = smem + 3 * C.Bmax;
+    uint32_t* s_pre = smem + 4 * C.Bmax;
+    uint8_t* s_osrc = reinterpret_cast<uint8_t*>(smem + 4 * C.Bmax + 3 * C.NS);
+    // with no augmented tier there is no cross-job interaction at all (E and D are
+    // static, maintain has nothing to do): the job CTAs run their rounds independently
+    const bool coupled = C.cap_a > 0;
+    if (is_maint && !coupled) return;
 
     if (tid < kMaxJobs) { s_n[tid] = P.n0[tid]; s_e[tid] = P.e0[tid]; }
     if (tid == 0) s_active = P.active0;
@@ -745,7 +764,8 @@ ods_rounds(Lay L, Cfg C, Launch P) {
         } else if ((part >> j) & 1u) {
             if (S.recount) { job_recount(L, C, j, s_pre); if (tid == 0) S.recount = 0; __syncthreads(); }
             TM.tick(0);
-            job_round(L, C, P, S, s_req, s_miss, s_sub, s_pre, j, r, s_e[j], s_n[j], TM);
+            job_round(L, C, P, S, s_req, s_miss, s_sub, s_oid, s_osrc, s_pre, j, r, s_e[j], s_n[j],
+                      __popc(active_after), TM);
             // a8 (R-O16): the epoch ends with this batch -> reset seen_j and the walk
             if (s_n[j] + S.need == C.N) {
                 uint4* sj = reinterpret_cast<uint4*>(L.seen + (size_t)j * C.NW);
@@ -759,7 +779,7 @@ ods_rounds(Lay L, Cfg C, Launch P) {
             TM.tick(0);
         }
         if (is_maint) TM.tick(1);
-        round_barrier(L.bar, nctas, gen);
+        if (coupled) round_barrier(L.bar, nctas, gen);
         TM.tick(is_maint ? 2 : 4);
 
         // schedule update (every CTA, identically)
@@ -782,13 +802,13 @@ ods_rounds(Lay L, Cfg C, Launch P) {
                 }
                 __syncthreads();
                 TM.tick(2);
-                maint_apply(L, C, P, M, s_pre, r, part, active_after, full_scan, spec, TM);
+                maint_apply(L, C, P, M, s_pre, r, active_after, full_scan, spec, TM);
             }
         } else if (rr + 1 < P.rounds && ((active_after & P.subset) >> j & 1u)) {
             job_walk(L, C, S, s_req, j, s_e[j], need_of(j));   // the next round's request
         }
         TM.tick(is_maint ? 4 : 5);
-        round_barrier(L.bar, nctas, gen);
+        if (coupled) round_barrier(L.bar, nctas, gen);
         TM.tick(is_maint ? 5 : 6);
     }
     // persist the walk state
@@ -998,7 +1018,7 @@ Sizes compute_sizes(const seneca_cache_config* cfg) {
     const size_t sz[] = {
         W, W, W,                                            // 0-2 bm_e, bm_d, bm_a
         W * C.J, W * C.J,                                   // 3-4 seen, cons
-        W,                                                  // 5 evmark
+        (size_t)C.Nrow * 4,                                 // 5 cons_cnt
         P * C.NBp * 4, P * C.NS * 4, P * 4,                 // 6-8 counts
         4,                                                  // 9 a_size
         (size_t)C.J * C.maxT * C.Nrow * 4,                  // 10 perms
@@ -1006,7 +1026,7 @@ Sizes compute_sizes(const seneca_cache_config* cfg) {
         (size_t)C.J * C.maxT * 4, (size_t)C.J * C.maxT * 4, // 12-13 perm_ready, perm_done
         (size_t)C.J * sizeof(JobDev),                       // 14 jobs
         (size_t)C.J * C.Bmax * 4, (size_t)C.J * C.Bmax,     // 15-16 out_ids, out_src
-        (size_t)C.J * C.Bmax * 4, (size_t)C.J * 4,          // 17-18 aserved, n_aserved
+        (size_t)C.J * C.Bmax * 4, 4,                        // 17-18 evict_push, ne_ctr
         capl, capl + (size_t)C.J * C.Bmax * 4,              // 19-20 evict, fill
         (size_t)C.J * C.maxT * sizeof(seneca_job_epoch_stats),  // 21 stats
         8, 8, 4, 8, 128,                                    // 22-26 evicted, refilled, err, bar, phase
@@ -1027,7 +1047,7 @@ Lay carve(const Sizes& z, char* base) {
     L.bm_a = (uint32_t*)(base + z.off[2]);
     L.seen = (uint32_t*)(base + z.off[3]);
     L.cons = (uint32_t*)(base + z.off[4]);
-    L.evmark = (uint32_t*)(base + z.off[5]);
+    L.cons_cnt = (uint32_t*)(base + z.off[5]);
     L.cnt_blk = (uint32_t*)(base + z.off[6]);
     L.cnt_sup = (uint32_t*)(base + z.off[7]);
     L.cnt_tot = (uint32_t*)(base + z.off[8]);
@@ -1039,8 +1059,8 @@ Lay carve(const Sizes& z, char* base) {
     L.jobs = (JobDev*)(base + z.off[14]);
     L.out_ids = (uint32_t*)(base + z.off[15]);
     L.out_src = (uint8_t*)(base + z.off[16]);
-    L.aserved = (uint32_t*)(base + z.off[17]);
-    L.n_aserved = (uint32_t*)(base + z.off[18]);
+    L.evict_push = (uint32_t*)(base + z.off[17]);
+    L.ne_ctr = (uint32_t*)(base + z.off[18]);
     L.evict_list = (uint32_t*)(base + z.off[19]);
     L.fill_list = (uint32_t*)(base + z.off[20]);
     L.stats = (seneca_job_epoch_stats*)(base + z.off[21]);
@@ -1156,7 +1176,7 @@ extern "C" seneca_status seneca_init_cache(const seneca_cache_config* cfg, void*
     if ((uintptr_t)d_workspace & 255) { set_error("workspace must be 256-byte aligned"); return SENECA_EINVAL; }
     Sizes z = compute_sizes(cfg);
     if (ws_bytes < z.total) { set_error("workspace %zu bytes < required %zu", ws_bytes, z.total); return SENECA_ENOSPC; }
-    const size_t round_smem = (size_t)3 * z.C.Bmax * 4 + (size_t)3 * z.C.NS * 4;
+    const size_t round_smem = (size_t)4 * z.C.Bmax * 4 + (size_t)3 * z.C.NS * 4 + z.C.Bmax;
     if (round_smem > 200 * 1024) { set_error("batch/dataset too large for the shared-memory indices"); return SENECA_EINVAL; }
     seneca_ctx* c = new (std::nothrow) seneca_ctx();
     if (!c) { set_error("out of host memory"); return SENECA_EINVAL; }
