@@ -9,6 +9,8 @@ the pin for the C oracle's exact decisions.  Only for tiny N.
 """
 from __future__ import annotations
 
+import math
+
 M32 = 0xFFFFFFFF
 M64 = 0xFFFFFFFFFFFFFFFF
 S, E, D, A, SUBST = 0, 1, 2, 3, 4
@@ -41,18 +43,17 @@ def key(seed, purpose, a=0, b=0, c=0):
 def perm(K, n, x):
     if n <= 1:
         return 0
-    bits = max(2, (n - 1).bit_length())
-    a = bits // 2
-    c = bits - a
+    a = math.isqrt(n - 1) + 1          # ceil(sqrt(n))
+    b = -(-n // a)
     kk = (K & M32, K >> 32)
     while True:
-        left, right = x >> c, x & ((1 << c) - 1)
+        left, right = divmod(x, b)
         for rd in range(4):
             if rd % 2 == 0:
-                left ^= philox((right, rd, 0, 0), kk)[0] & ((1 << a) - 1)
+                left = (left + ((philox((right, rd, 0, 0), kk)[0] * a) >> 32)) % a
             else:
-                right ^= philox((left, rd, 0, 0), kk)[0] & ((1 << c) - 1)
-        x = (left << c) | right
+                right = (right + ((philox((left, rd, 0, 0), kk)[0] * b) >> 32)) % b
+        x = left * b + right
         if x < n:
             return x
 

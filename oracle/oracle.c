@@ -19,7 +19,7 @@
  *
  * Parity status per function:
  *   philox4x32_10 ........ pinned (Random123 known-answer vectors)
- *   perm ................. pinned (exhaustive bijection, tiny n; independent Python re-derivation)
+ *   perm ................. pinned (exhaustive bijection; uniformity; independent Python transcription)
  *   MDP (Eqs. 1-9, grid) . pinned (Table 4 values, closed forms, exact-rational brute force)
  *   ODS replay ........... pinned by the SPEC worked example, closed forms (static tiers,
  *                          J=1 refill accounting), invariants I1-I10; exact decisions with
@@ -29,6 +29,7 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <math.h>
 
 /* ------------------------------------------------------------------------- */
 /* Status codes (mirrors the meaning of the C-ABI codes; defined here anew).  */
@@ -79,35 +80,40 @@ uint64_t oracle_key(uint64_t seed, uint64_t purpose, uint64_t a, uint64_t b, uin
 }
 
 /* perm(K, n, x): keyed bijection of [0, n), 0 <= x < n (R-O17).  A 4-round
- * Feistel network on bits = max(2, ceil(log2 n)) bits -- left part a = bits/2
- * bits, right part c = bits - a bits, rounds alternately xor
- * philox((other part, round, 0, 0), K)[0] into the left (even rounds) and the
- * right part (odd rounds) -- restricted to [0, n) by cycle walking (expected
- * walk 2^bits / n < 2).                                                      */
+ * Feistel network on Z_a x Z_b with a = ceil(sqrt(n)), b = ceil(n / a)
+ * (a*b >= n, a*b - n < a): x = L*b + R; even rounds L = (L + F) mod a with
+ * F = floor(philox((R, rd, 0, 0), K)[0] * a / 2^32), odd rounds
+ * R = (R + floor(philox((L, rd, 0, 0), K)[0] * b / 2^32)) mod b; restricted to
+ * [0, n) by cycle walking (probability of a step < 1/b).                    */
+static uint64_t isqrt_ceil(uint64_t n)   /* smallest a with a*a >= n */
+{
+    uint64_t a = (uint64_t)sqrt((double)n);
+    while (a * a < n) ++a;
+    while (a > 0 && (a - 1) * (a - 1) >= n) --a;
+    return a;
+}
+
 uint64_t oracle_perm(uint64_t K, uint64_t n, uint64_t x)
 {
     if (n <= 1) return 0;
-    unsigned bits = 0;
-    while (((uint64_t)1 << bits) < n) ++bits;
-    if (bits < 2) bits = 2;
-    unsigned a = bits / 2, c = bits - a;
-    uint64_t maskL = ((uint64_t)1 << a) - 1, maskR = ((uint64_t)1 << c) - 1;
+    uint64_t a = isqrt_ceil(n);
+    uint64_t b = (n + a - 1) / a;
     uint32_t key[2] = { (uint32_t)K, (uint32_t)(K >> 32) };
     do {
-        uint64_t L = x >> c, R = x & maskR;
+        uint64_t L = x / b, R = x % b;
         for (uint32_t rd = 0; rd < 4; ++rd) {
             uint32_t o[4];
             if ((rd & 1) == 0) {
                 uint32_t ctr[4] = { (uint32_t)R, rd, 0, 0 };
                 oracle_philox4x32_10(ctr, key, o);
-                L ^= (uint64_t)o[0] & maskL;
+                L = (L + (((uint64_t)o[0] * a) >> 32)) % a;
             } else {
                 uint32_t ctr[4] = { (uint32_t)L, rd, 0, 0 };
                 oracle_philox4x32_10(ctr, key, o);
-                R ^= (uint64_t)o[0] & maskR;
+                R = (R + (((uint64_t)o[0] * b) >> 32)) % b;
             }
         }
-        x = (L << c) | R;
+        x = L * b + R;
     } while (x >= n);
     return x;
 }
