@@ -99,6 +99,49 @@ __device__ void tier_throughputs(const seneca_mdp_profile& p, double dsi[4], uin
     lim[0] = la; lim[1] = ld; lim[2] = le; lim[3] = ls;
 }
 
+// Per-warp shared tables for one profile: capacities clamped to N (exact
+// integers), and the Eq. 9 terms that depend on a single coordinate.
+struct WarpTables {
+    uint64_t capc[kMaxSteps];    // min(N, capAD(p))  -- A and D tiers (M x S_data per sample)
+    uint64_t cape[kMaxSteps];    // min(N, capE(p))   -- E tier (S_data per sample)
+    double tA[kMaxSteps];        // (capc/N) DSI_A
+    double tD[kMaxSteps];        // (capc/N) DSI_D
+    double tE[kMaxSteps];        // (cape/N) DSI_E
+};
+
+// The sweep of one profile by one warp; U = uint32_t when N < 2^31 (every
+// count fits, 32-bit integer ops), uint64_t otherwise.  Same binary64
+// operations on the same operands as the oracle (R-M7).
+template <typename U>
+__device__ __forceinline__ void sweep_profile(const WarpTables& W, uint64_t N64, const double dsi[4], uint32_t steps,
+                                              uint32_t n_splits, double* grow, double& best, uint32_t& best_i) {
+    const uint32_t lane = threadIdx.x & 31;
+    const U N = (U)N64;
+    const double dN = u2d(N64);
+    uint32_t a = 0, b = lane;
+    while (b > a) { b -= a + 1; ++a; }
+    for (uint32_t idx = lane; idx < n_splits; idx += 32) {
+        const uint32_t ie = steps - a, id = a - b, ia = b;          // table indices of p_E, p_D, p_A
+        const U nA = (U)W.capc[ia];                                  // Eq. 5 (clamped)
+        const U r1 = N - nA;
+        const U cD = (U)W.capc[id];
+        const U nD = cD < r1 ? cD : r1;                              // Eq. 6
+        const U r2 = r1 - nD;
+        const U cE = (U)W.cape[ie];
+        const U nE = cE < r2 ? cE : r2;                              // Eq. 7
+        const U nS = r2 - nE;                                        // Eq. 8
+        const double tA = W.tA[ia];
+        const double tD = (nD == cD) ? W.tD[id] : __dmul_rn(__ddiv_rn(u2d(nD), dN), dsi[1]);
+        const double tE = (nE == cE) ? W.tE[ie] : __dmul_rn(__ddiv_rn(u2d(nE), dN), dsi[2]);
+        const double tS = __dmul_rn(__ddiv_rn(u2d(nS), dN), dsi[3]);
+        const double v = __dadd_rn(__dadd_rn(__dadd_rn(tA, tD), tE), tS);   // Eq. 9, R-M7
+        if (grow) __stcs(grow + idx, v);
+        if (v > best) { best = v; best_i = idx; }                   // idx increases per lane
+        b += 32;                                                     // next split of this lane
+        while (b > a) { b -= a + 1; ++a; }
+    }
+}
+
 // One WARP per profile (8 profiles per CTA in flight): the prologue needs only
 // warp-level synchronisation, so one warp's setup overlaps the other warps'
 // sweeps; each warp iteration stores 32 consecutive grid values (256 B).
@@ -107,19 +150,13 @@ mdp_sweep_kernel(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_pro
                  uint32_t steps, uint32_t n_splits, seneca_mdp_result* __restrict__ results,
                  double* __restrict__ grid) {
     constexpr int kWarps = kThreads / 32;
-    __shared__ uint64_t s_capAD[kWarps][kMaxSteps], s_capE[kWarps][kMaxSteps];
-    __shared__ double s_tA[kWarps][kMaxSteps], s_tD[kWarps][kMaxSteps], s_tE[kWarps][kMaxSteps];
+    __shared__ WarpTables s_tab[kWarps];
     const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    uint64_t* capAD = s_capAD[w];
-    uint64_t* capE = s_capE[w];
-    double* tAv = s_tA[w];
-    double* tDv = s_tD[w];
-    double* tEv = s_tE[w];
+    WarpTables& W = s_tab[w];
 
     for (uint32_t pi = blockIdx.x * kWarps + w; pi < n_profiles; pi += gridDim.x * kWarps) {
         const seneca_mdp_profile p = profiles[pi];
-        const bool valid = profile_valid(p);
-        if (!valid) {
+        if (!profile_valid(p)) {
             if (lane == 0) {
                 seneca_mdp_result r = {};
                 r.status = 1;
@@ -136,39 +173,21 @@ mdp_sweep_kernel(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_pro
         const uint64_t De = 100ull * p.s_data;
         for (uint32_t k = lane; k <= steps; k += 32) {
             const uint64_t pct = (uint64_t)k * g;
-            const uint64_t cad = (pct * Xad) / Dad, ce = (pct * p.cache_bytes) / De;   // Eqs. 5-7, exact
-            capAD[k] = cad;
-            capE[k] = ce;
-            tAv[k] = __dmul_rn(__ddiv_rn(u2d(cad < N ? cad : N), dN), dsi[0]);
-            tDv[k] = __dmul_rn(__ddiv_rn(u2d(cad), dN), dsi[1]);
-            tEv[k] = __dmul_rn(__ddiv_rn(u2d(ce), dN), dsi[2]);
+            uint64_t cad = (pct * Xad) / Dad, ce = (pct * p.cache_bytes) / De;   // Eqs. 5-7, exact floors
+            cad = cad < N ? cad : N;
+            ce = ce < N ? ce : N;
+            W.capc[k] = cad;
+            W.cape[k] = ce;
+            W.tA[k] = __dmul_rn(__ddiv_rn(u2d(cad), dN), dsi[0]);
+            W.tD[k] = __dmul_rn(__ddiv_rn(u2d(cad), dN), dsi[1]);
+            W.tE[k] = __dmul_rn(__ddiv_rn(u2d(ce), dN), dsi[2]);
         }
         __syncwarp();
-        // enumeration index idx -> row a (p_E = 100 - a g), position b in the row (p_A = b g)
-        uint32_t a = 0, b = lane;
-        while (b > a) { b -= a + 1; ++a; }
         double best = __longlong_as_double(0xfff0000000000000ll);
         uint32_t best_i = 0xffffffffu;
         double* grow = grid ? grid + (uint64_t)pi * n_splits : nullptr;
-        for (uint32_t idx = lane; idx < n_splits; idx += 32) {
-            const uint32_t ie = steps - a, id = a - b, ia = b;
-            const uint64_t cA = capAD[ia], cD = capAD[id], cE = capE[ie];
-            const uint64_t nA = cA < N ? cA : N;                 // Eq. 5
-            const uint64_t r1 = N - nA;
-            const uint64_t nD = cD < r1 ? cD : r1;               // Eq. 6
-            const uint64_t r2 = r1 - nD;
-            const uint64_t nE = cE < r2 ? cE : r2;               // Eq. 7
-            const uint64_t nS = r2 - nE;                         // Eq. 8
-            const double tA = tAv[ia];
-            const double tD = (nD == cD) ? tDv[id] : __dmul_rn(__ddiv_rn(u2d(nD), dN), dsi[1]);
-            const double tE = (nE == cE) ? tEv[ie] : __dmul_rn(__ddiv_rn(u2d(nE), dN), dsi[2]);
-            const double tS = __dmul_rn(__ddiv_rn(u2d(nS), dN), dsi[3]);
-            const double v = __dadd_rn(__dadd_rn(__dadd_rn(tA, tD), tE), tS);   // Eq. 9, R-M7
-            if (grow) __stcs(grow + idx, v);
-            if (v > best) { best = v; best_i = idx; }           // idx increases per lane
-            b += 32;                                             // advance the lane by 32 splits
-            while (b > a) { b -= a + 1; ++a; }
-        }
+        if (N < (1ull << 31)) sweep_profile<uint32_t>(W, N, dsi, steps, n_splits, grow, best, best_i);
+        else sweep_profile<uint64_t>(W, N, dsi, steps, n_splits, grow, best, best_i);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             const double ov = __shfl_xor_sync(0xffffffffu, best, o);
