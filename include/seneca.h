@@ -168,7 +168,8 @@ typedef struct {
     const uint64_t* d_phase_cycles;     /* [16] SM cycles per phase when profiling.  Job CTA 0:
                                            [0] recount/epoch end [1] classify [2] substitute
                                            [3] respond [4] barrier-1 wait [5] next walk
-                                           [6] barrier-2 wait; maintain CTA: [8] speculative
+                                           [6] barrier-2 wait [7] walk steps (a count);
+                                           maintain CTA: [8] speculative
                                            prefix [9] speculative refill ranks [10] barrier-1
                                            wait [11] eviction decision [12] remaining refill
                                            ranks + apply [13] barrier-2 wait                    */

@@ -135,23 +135,25 @@ __device__ __forceinline__ void count_add(const Lay& L, const Cfg& C, uint32_t p
     atomicAdd(L.cnt_sup + (size_t)pidx * C.NS + (id >> kSuperShift), delta);
 }
 
-// Exclusive prefix of the superblock counts of pool pidx, into shared memory.
+// Exclusive prefix of the superblock counts of pool pidx, into shared memory
+// (each thread a contiguous run; the run is re-read from L2 instead of being
+// kept in a dynamically indexed local array).
 __device__ void load_sup_prefix(const Lay& L, const Cfg& C, uint32_t pidx, uint32_t* s_pre, uint32_t* scratch) {
     const uint32_t per = (C.NS + blockDim.x - 1) / blockDim.x;
     const uint32_t lo = threadIdx.x * per;
+    const uint32_t hi = min(lo + per, C.NS);
     const uint32_t* src = L.cnt_sup + (size_t)pidx * C.NS;
-    uint32_t v[16];
     uint32_t sum = 0;
-    for (uint32_t k = 0; k < per && k < 16; ++k) {
-        v[k] = lo + k < C.NS ? ldcg(src + lo + k) : 0u;
-        sum += v[k];
+    for (uint32_t k = lo; k < hi; ++k) {
+        const uint32_t v = ldcg(src + k);
+        s_pre[k] = v;                               // counts first, prefix below
+        sum += v;
     }
-    for (uint32_t k = 16; k < per; ++k) sum += lo + k < C.NS ? ldcg(src + lo + k) : 0u;
     uint32_t run = block_exclusive_scan(sum, nullptr, scratch);
-    for (uint32_t k = 0; k < per && lo + k < C.NS; ++k) {
-        const uint32_t x = k < 16 ? v[k] : ldcg(src + lo + k);
-        s_pre[lo + k] = run;
-        run += x;
+    for (uint32_t k = lo; k < hi; ++k) {
+        const uint32_t v = s_pre[k];
+        s_pre[k] = run;
+        run += v;
     }
     __syncthreads();
 }
@@ -275,6 +277,7 @@ struct JobSmem {
     uint32_t wrap_slot, need, newcursor, walk_err;
     uint32_t m, k[3], tot[3], hits[3];
     uint32_t recount;
+    uint32_t perm_seen;   // epoch+1 whose permutation was observed published (0: none)
     uint32_t hist[8];
     uint32_t scan[33];
     unsigned long long red[(kThreads / 32) * 13];
@@ -287,13 +290,17 @@ __device__ __forceinline__ const uint32_t* list_ptr(const Lay& L, const Cfg& C, 
 // a1/a2 (R-O1): the first `need` ids of the job's current lap list, from the
 // cursor, that are not in seen_j.  At a lap end the walk continues with the
 // list of deferred misses of the lap (slot order = position order).
-__device__ void job_walk(const Lay& L, const Cfg& C, JobSmem& S, uint32_t* s_req, uint32_t j, uint32_t e, uint32_t need) {
+__device__ void job_walk(const Lay& L, const Cfg& C, JobSmem& S, uint32_t* s_req, uint32_t j, uint32_t e, uint32_t need,
+                         unsigned long long* iters) {
     const uint32_t tid = threadIdx.x, T = blockDim.x;
     const uint32_t* seen_j = L.seen + (size_t)j * C.NW;
     if (tid == 0) { S.wrap_slot = 0; S.need = need; }
-    if (S.cur_buf == 0 && tid == 0) {            // the epoch's permutation must be published
-        const uint32_t* f = L.perm_ready + (size_t)j * C.maxT + e;
-        while (ld_acquire(f) == 0) { }
+    if (S.cur_buf == 0 && S.perm_seen != e + 1) {   // the epoch's permutation must be published
+        if (tid == 0) {
+            const uint32_t* f = L.perm_ready + (size_t)j * C.maxT + e;
+            while (ld_acquire(f) == 0) { }
+            S.perm_seen = e + 1;
+        }
     }
     __syncthreads();
     uint32_t taken = 0;
@@ -318,6 +325,7 @@ __device__ void job_walk(const Lay& L, const Cfg& C, JobSmem& S, uint32_t* s_req
         }
         const uint32_t cursor = S.cursor, len = S.cur_len;
         const uint32_t* list = list_ptr(L, C, j, e, S.cur_buf);
+        if (iters && tid == 0) *iters += 1;
         // window [base, base + 8T), base = cursor rounded down to 4 entries (16 B),
         // two aligned 16-B loads per thread; entries before the cursor are ignored
         const uint32_t base = cursor & ~3u;
@@ -609,9 +617,7 @@ __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSm
             const uint32_t a_w = ldcg(L.bm_a + w);
             if (!a_w) continue;
             uint32_t ev = a_w;
-            uint32_t cw[kMaxJobs];
-            uint32_t na = 0;
-            for (uint32_t m = active; m; m &= m - 1) { cw[na] = ldcg(L.cons + (size_t)(__ffs(m) - 1) * C.NW + w); ev &= cw[na]; ++na; }
+            for (uint32_t m = active; m; m &= m - 1) ev &= ldcg(L.cons + (size_t)(__ffs(m) - 1) * C.NW + w);
             if (ev) {
                 const uint32_t base = atomicAdd(&M.ne, (uint32_t)__popc(ev));
                 uint32_t c = 0;
@@ -620,7 +626,8 @@ __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSm
             for (uint32_t v = a_w & ~ev; v; v &= v - 1) {
                 const uint32_t bit = __ffs(v) - 1;
                 uint32_t cnt = 0;
-                for (uint32_t k = 0; k < na; ++k) cnt += (cw[k] >> bit) & 1u;
+                for (uint32_t m = active; m; m &= m - 1)
+                    cnt += (ldcg(L.cons + (size_t)(__ffs(m) - 1) * C.NW + w) >> bit) & 1u;
                 L.cons_cnt[w * 32u + bit] = cnt;
             }
         }
@@ -708,6 +715,7 @@ ods_rounds(Lay L, Cfg C, Launch P) {
         const JobDev jd = L.jobs[j];
         S.cur_buf = jd.cur_buf; S.nxt_buf = jd.nxt_buf; S.cursor = jd.cursor;
         S.cur_len = jd.cur_len; S.nxt_len = jd.nxt_len; S.recount = jd.recount;
+        S.perm_seen = 0;
     }
     __syncthreads();
 
@@ -722,7 +730,7 @@ ods_rounds(Lay L, Cfg C, Launch P) {
             if (tid == 0) { S.need = need; S.wrap_slot = 0; }
             __syncthreads();
         } else {
-            job_walk(L, C, S, s_req, j, s_e[j], need);
+            job_walk(L, C, S, s_req, j, s_e[j], need, TM.on ? &TM.acc[7] : nullptr);
         }
     }
 
@@ -805,7 +813,7 @@ ods_rounds(Lay L, Cfg C, Launch P) {
                 maint_apply(L, C, P, M, s_pre, r, active_after, full_scan, spec, TM);
             }
         } else if (rr + 1 < P.rounds && ((active_after & P.subset) >> j & 1u)) {
-            job_walk(L, C, S, s_req, j, s_e[j], need_of(j));   // the next round's request
+            job_walk(L, C, S, s_req, j, s_e[j], need_of(j), TM.on ? &TM.acc[7] : nullptr);   // next round's request
         }
         TM.tick(is_maint ? 4 : 5);
         if (coupled) round_barrier(L.bar, nctas, gen);
