@@ -325,17 +325,19 @@ def main():
     st_raw = st_raw.reshape(len(c["batch"]), v.max_target)
     served_ok = bool(np.all(st_raw["served"].sum(axis=2) == c["n_total"]))
     parity["ods_served_per_job_epoch_equals_N"] = served_ok
-    ph = ws[v.d_phase_cycles - ws.data_ptr():v.d_phase_cycles - ws.data_ptr() + 128].cpu().numpy().view(np.uint64)
-    ph_names = {0: "job_epoch_start", 1: "job_classify", 2: "job_substitute", 3: "job_respond",
-                4: "job_barrier1_wait", 5: "job_walk_next", 6: "job_barrier2_wait",
-                8: "maint_spec_prefix", 9: "maint_spec_refill_ranks", 10: "maint_barrier1_wait",
-                11: "maint_evict_decide", 12: "maint_apply", 13: "maint_barrier2_wait"}
+    ph = ws[v.d_phase_cycles - ws.data_ptr():v.d_phase_cycles - ws.data_ptr() + 256].cpu().numpy().view(np.uint64)
+    ph_names = {0: "job_epoch_start", 1: "job_classify", 8: "job_subst_prefix", 9: "job_subst_ranks_locate",
+                2: "job_subst_apply", 3: "job_respond", 4: "job_barrier1_wait", 5: "job_walk_next",
+                6: "job_barrier2_wait",
+                16: "maint_spec_prefix", 17: "maint_spec_refill_ranks", 18: "maint_barrier1_wait",
+                19: "maint_evict_decide", 20: "maint_apply", 21: "maint_barrier2_wait"}
     phase_share = {}
-    for base in (0, 8):
-        tot = float(ph[base:base + 8].sum())
-        for k in range(8):
-            if base + k in ph_names:
-                phase_share[ph_names[base + k]] = round(float(ph[base + k]) / tot, 4) if tot else None
+    for base in (0, 16):
+        keys = [k for k in ph_names if base <= k < base + 16]
+        tot = float(sum(ph[k] for k in keys))
+        for k in keys:
+            phase_share[ph_names[k]] = round(float(ph[k]) / tot, 4) if tot else None
+    phase_share["walk_steps_per_round"] = round(float(ph[7]) / max(1, rounds_tot / args.steps), 3)
     if os.path.exists(gold_path):
         gold = json.load(open(gold_path))
         ok = all(int(st_raw[j, e]["digest"]) == int(s_["digest"]) and

@@ -165,14 +165,15 @@ typedef struct {
     const seneca_job_epoch_stats* d_stats; /* [n_jobs][max_target]                        */
     const uint64_t* d_evicted;          /* total evictions                                 */
     const uint64_t* d_refilled;         /* total refills                                   */
-    const uint64_t* d_phase_cycles;     /* [16] SM cycles per phase when profiling.  Job CTA 0:
+    const uint64_t* d_phase_cycles;     /* [32] SM cycles per phase when profiling.  Job CTA 0:
                                            [0] recount/epoch end [1] classify [2] substitute
-                                           [3] respond [4] barrier-1 wait [5] next walk
-                                           [6] barrier-2 wait [7] walk steps (a count);
-                                           maintain CTA: [8] speculative
-                                           prefix [9] speculative refill ranks [10] barrier-1
-                                           wait [11] eviction decision [12] remaining refill
-                                           ranks + apply [13] barrier-2 wait                    */
+                                           (apply) [3] respond [4] barrier-1 wait [5] next walk
+                                           [6] barrier-2 wait [7] walk steps (a count)
+                                           [8] substitute: pool prefixes [9] substitute: ranks
+                                           and locate.  Maintain CTA (+16): [16] speculative
+                                           prefix [17] speculative refill ranks [18] barrier-1
+                                           wait [19] eviction decision [20] remaining refill
+                                           ranks + apply [21] barrier-2 wait                    */
     uint64_t round;                     /* rounds executed                                 */
     uint64_t epoch[32];                 /* host mirror: current epoch of each job          */
     uint64_t consumed[32];              /* host mirror: samples consumed in current epoch  */

@@ -101,7 +101,7 @@ class ODSContext:
 
     def phase_cycles(self):
         v = self.view()
-        return self._slice(v.d_phase_cycles, 128).cpu().numpy().view(np.uint64).copy()
+        return self._slice(v.d_phase_cycles, 256).cpu().numpy().view(np.uint64).copy()
 
     def profile_read(self) -> dict:
         return seneca.profile_read(self.ctx)

@@ -66,7 +66,7 @@ struct JobDev {           // per-job persistent walk state (workspace)
 
 struct Cfg {
     uint32_t N, NW, NB, NS, NBp;     // samples, words/bitmap, blocks, superblocks, padded blocks
-    uint32_t J, Bmax, maxT, cap_a;
+    uint32_t J, Bmax, maxT, cap_a, cap_d, cap_e;
     uint32_t Nrow;                   // row stride of the permutation / lap lists (N rounded up to 64)
     uint64_t seed;
     uint32_t batch[kMaxJobs];
@@ -96,7 +96,7 @@ struct Lay {
     unsigned long long *evicted, *refilled;
     uint32_t *err;
     uint32_t *bar;                   // [2] barrier count, generation
-    unsigned long long *phase;       // [16] accumulated cycles per phase (see seneca.h)
+    unsigned long long *phase;       // [32] accumulated cycles per phase (see seneca.h)
 };
 
 struct Launch {
@@ -260,7 +260,7 @@ __device__ void round_barrier(uint32_t* bar, uint32_t nctas, uint32_t& gen) {
 // ------------------------------------------------------------------ per-CTA phase timer (profiling)
 struct PhaseTimer {
     long long last;
-    unsigned long long acc[8];
+    unsigned long long acc[16];
     uint32_t on;
     __device__ __forceinline__ void tick(uint32_t slot) {
         if (on && threadIdx.x == 0) {
@@ -278,6 +278,7 @@ struct JobSmem {
     uint32_t m, k[3], tot[3], hits[3];
     uint32_t recount;
     uint32_t perm_seen;   // epoch+1 whose permutation was observed published (0: none)
+    float dens;           // unseen fraction observed by the last walk step (window sizing)
     uint32_t hist[8];
     uint32_t scan[33];
     unsigned long long red[(kThreads / 32) * 13];
@@ -326,26 +327,31 @@ __device__ void job_walk(const Lay& L, const Cfg& C, JobSmem& S, uint32_t* s_req
         const uint32_t cursor = S.cursor, len = S.cur_len;
         const uint32_t* list = list_ptr(L, C, j, e, S.cur_buf);
         if (iters && tid == 0) *iters += 1;
-        // window [base, base + 8T), base = cursor rounded down to 4 entries (16 B),
-        // two aligned 16-B loads per thread; entries before the cursor are ignored
+        // window [base, base + 8*nt): base = cursor rounded down to 4 entries (16 B);
+        // nt threads load two aligned 16-B vectors each; the window is sized from the
+        // last observed unseen density (scattered seen gathers cost ~1 L1 wavefront each)
         const uint32_t base = cursor & ~3u;
+        const float want = (float)(need - taken) / fmaxf(S.dens, 1.0f / 64.0f) * 1.15f + 64.0f;
+        const uint32_t nt = min(T, max(32u, ((uint32_t)want + (cursor - base) + 8 * 32 - 1) / (8 * 32) * 32));
         const uint32_t p0 = base + tid * kWalkPerThread;
         uint32_t ids[kWalkPerThread];
         uint32_t flags = 0, cnt = 0;
-        if (p0 + kWalkPerThread <= len) {
-            const uint4 v0 = ldcg4(list + p0), v1 = ldcg4(list + p0 + 4);
-            ids[0] = v0.x; ids[1] = v0.y; ids[2] = v0.z; ids[3] = v0.w;
-            ids[4] = v1.x; ids[5] = v1.y; ids[6] = v1.z; ids[7] = v1.w;
-        } else {
+        if (tid < nt) {
+            if (p0 + kWalkPerThread <= len) {
+                const uint4 v0 = ldcg4(list + p0), v1 = ldcg4(list + p0 + 4);
+                ids[0] = v0.x; ids[1] = v0.y; ids[2] = v0.z; ids[3] = v0.w;
+                ids[4] = v1.x; ids[5] = v1.y; ids[6] = v1.z; ids[7] = v1.w;
+            } else {
 #pragma unroll
-            for (uint32_t k = 0; k < kWalkPerThread; ++k) ids[k] = p0 + k < len ? ldcg(list + p0 + k) : 0u;
-        }
+                for (uint32_t k = 0; k < kWalkPerThread; ++k) ids[k] = p0 + k < len ? ldcg(list + p0 + k) : 0u;
+            }
 #pragma unroll
-        for (uint32_t k = 0; k < kWalkPerThread; ++k) {
-            const uint32_t p = p0 + k;
-            if (p >= cursor && p < len) {
-                const uint32_t id = ids[k];
-                if (!((ldcg(seen_j + (id >> 5)) >> (id & 31)) & 1u)) { flags |= 1u << k; ++cnt; }
+            for (uint32_t k = 0; k < kWalkPerThread; ++k) {
+                const uint32_t p = p0 + k;
+                if (p >= cursor && p < len) {
+                    const uint32_t id = ids[k];
+                    if (!((ldcg(seen_j + (id >> 5)) >> (id & 31)) & 1u)) { flags |= 1u << k; ++cnt; }
+                }
             }
         }
         uint32_t tot;
@@ -361,11 +367,18 @@ __device__ void job_walk(const Lay& L, const Cfg& C, JobSmem& S, uint32_t* s_req
             }
         }
         __syncthreads();
+        const uint32_t wend = min(base + kWalkPerThread * nt, len);
         if (tot >= remaining) {
-            if (tid == 0) S.cursor = S.newcursor;
+            if (tid == 0) {
+                S.cursor = S.newcursor;
+                S.dens = (float)remaining / (float)max(1u, S.newcursor - cursor);
+            }
             taken = need;
         } else {
-            if (tid == 0) S.cursor = min(base + kWalkPerThread * T, len);
+            if (tid == 0) {
+                S.cursor = wend;
+                S.dens = (float)tot / (float)max(1u, wend - cursor);
+            }
             taken += tot;
         }
         __syncthreads();
@@ -442,9 +455,12 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
         if (s < need) {
             const uint32_t i = s_req[s];
             const uint32_t w = i >> 5, b = 1u << (i & 31);
-            const uint32_t wa = ldcg(L.bm_a + w), wd = ldcg(L.bm_d + w), we = ldcg(L.bm_e + w), wc = ldcg(cons_j + w);
+            // only the tiers that exist are gathered; the consumer word only for A ids
+            const uint32_t wa = C.cap_a ? ldcg(L.bm_a + w) : 0u;
+            const uint32_t wd = C.cap_d ? ldcg(L.bm_d + w) : 0u;
+            const uint32_t we = C.cap_e ? ldcg(L.bm_e + w) : 0u;
             const uint32_t t = (wa & b) ? T_A : (wd & b) ? T_D : (we & b) ? T_E : T_S;
-            const bool hit = (t == T_E || t == T_D || (t == T_A && !(wc & b)));
+            const bool hit = (t == T_E || t == T_D || (t == T_A && !(ldcg(cons_j + w) & b)));
             if (hit) {
                 P.out_ids[row + s] = i;
                 P.out_src[row + s] = (uint8_t)t;
@@ -481,6 +497,7 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
     if (q > 0) {
         for (uint32_t tt = 0; tt < 3; ++tt)
             if (S.k[tt]) load_sup_prefix(L, C, j * 3 + tt, s_pre + tt * C.NS, S.scan);
+        TM.tick(8);
         for (uint32_t u = tid; u < q; u += T) {
             const uint32_t tt = u < k0 ? 0u : (u < k0 + k1 ? 1u : 2u);
             const uint32_t ul = u - (tt == 0 ? 0u : (tt == 1 ? k0 : k0 + k1));
@@ -496,6 +513,7 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
             s_sub[u] = id;
         }
         __syncthreads();
+        TM.tick(9);
         for (uint32_t u = tid; u < q; u += T) {
             const uint32_t tt = u < k0 ? 0u : (u < k0 + k1 ? 1u : 2u);
             const uint32_t id = s_sub[u];
@@ -694,7 +712,7 @@ ods_rounds(Lay L, Cfg C, Launch P) {
     if (tid == 0) {
         TM.on = P.timing;
         TM.last = clock64();
-        for (int k = 0; k < 8; ++k) TM.acc[k] = 0;
+        for (int k = 0; k < 16; ++k) TM.acc[k] = 0;
     }
 
     // shared memory carve: job CTA s_req | s_miss | s_sub [Bmax] + s_pre [3][NS]; maintain CTA s_pre [NS]
@@ -716,6 +734,7 @@ ods_rounds(Lay L, Cfg C, Launch P) {
         S.cur_buf = jd.cur_buf; S.nxt_buf = jd.nxt_buf; S.cursor = jd.cursor;
         S.cur_len = jd.cur_len; S.nxt_len = jd.nxt_len; S.recount = jd.recount;
         S.perm_seen = 0;
+        S.dens = 1.0f;
     }
     __syncthreads();
 
@@ -826,8 +845,8 @@ ods_rounds(Lay L, Cfg C, Launch P) {
         jd.cur_len = S.cur_len; jd.nxt_len = S.nxt_len; jd.recount = S.recount;
     }
     if (P.timing && tid == 0 && (is_maint || cta == 0)) {
-        const uint32_t base = is_maint ? 8 : 0;
-        for (int k = 0; k < 8; ++k) atomicAdd(L.phase + base + k, TM.acc[k]);
+        const uint32_t base = is_maint ? 16 : 0;
+        for (int k = 0; k < 16; ++k) atomicAdd(L.phase + base + k, TM.acc[k]);
     }
 }
 
@@ -1019,6 +1038,8 @@ Sizes compute_sizes(const seneca_cache_config* cfg) {
         C.target[j] = cfg->target_epochs[j];
     }
     C.cap_a = (uint32_t)cfg->cap_a;
+    C.cap_d = (uint32_t)cfg->cap_d;
+    C.cap_e = (uint32_t)cfg->cap_e;
     C.seed = cfg->seed;
     C.Nrow = (C.N + 63) & ~63u;
     const size_t W = (size_t)C.NW * 4, P = 3 * (size_t)C.J + 1;
@@ -1037,7 +1058,7 @@ Sizes compute_sizes(const seneca_cache_config* cfg) {
         (size_t)C.J * C.Bmax * 4, 4,                        // 17-18 evict_push, ne_ctr
         capl, capl + (size_t)C.J * C.Bmax * 4,              // 19-20 evict, fill
         (size_t)C.J * C.maxT * sizeof(seneca_job_epoch_stats),  // 21 stats
-        8, 8, 4, 8, 128,                                    // 22-26 evicted, refilled, err, bar, phase
+        8, 8, 4, 8, 256,                                    // 22-26 evicted, refilled, err, bar, phase
     };
     size_t at = 0;
     for (size_t k = 0; k < sizeof(sz) / sizeof(sz[0]); ++k) {
