@@ -12,13 +12,15 @@
 //       job CTAs      classify (a3) -> select (a4, a5) -> finish (a6, a8)
 //       maintain CTA  speculative refill selection from the round-start storage
 //                     pool (it cannot change before maintain)            [overlapped]
-//       -- barrier 1 --
+//       -- signal "job phases of round r done" (job CTAs -> maintain CTA) --
 //       maintain CTA  eviction of A entries consumed by every active job, apply
 //                     evictions + refills (a7)
 //       job CTAs      walk of the NEXT round (a1, a2): it reads only the job's
 //                     own seen bitmap and lists                          [overlapped]
-//       -- barrier 2 --
-//   The barrier is a sense-reversing software barrier among the J+1 CTAs.
+//       -- signal "maintain(r) applied" (maintain CTA -> job CTAs) --
+//   The signals are release/acquire counters; nobody waits for anything it does
+//   not depend on.  With no augmented tier (cap_A = 0) jobs never interact and
+//   the job CTAs run their rounds without any signal.
 //
 // Pool counts: for each pool (job x {A, D, E}, plus the storage pool S) a count
 // per 256-id block, per 32-block superblock and a total, kept exact
@@ -239,24 +241,6 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
     return v;
 }
 
-__device__ void round_barrier(uint32_t* bar, uint32_t nctas, uint32_t& gen) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        const uint32_t g = gen;
-        if (atomicAdd(bar, 1u) == nctas - 1) {
-            bar[0] = 0;
-            __threadfence();
-            atomicExch(bar + 1, g + 1);
-        } else {
-            while (ld_acquire(bar + 1) == g) { }
-        }
-        __threadfence();
-    }
-    gen += 1;
-    __syncthreads();
-}
-
 // ------------------------------------------------------------------ per-CTA phase timer (profiling)
 struct PhaseTimer {
     long long last;
@@ -443,7 +427,8 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
     uint32_t* seen_j = L.seen + (size_t)j * C.NW;
     uint32_t* cons_j = L.cons + (size_t)j * C.NW;
     const size_t row = (size_t)P.row_of_job[j] * P.out_stride;
-    if (tid < 3) { S.hits[tid] = 0; S.tot[tid] = ldcg(L.cnt_tot + j * 3 + tid); }
+    const uint32_t tot_reg = tid < 3 ? ldcg(L.cnt_tot + j * 3 + tid) : 0u;   // consumed after classify
+    if (tid < 3) S.hits[tid] = 0;
     if (tid < 8) S.hist[tid] = 0;
     __syncthreads();
 
@@ -479,6 +464,8 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
         if (is_miss) s_miss[mbase + ex] = s;
         mbase += tot;
     }
+    if (tid < 3) S.tot[tid] = tot_reg;
+    __syncthreads();
     if (tid == 0) {
         const uint32_t pa = S.tot[0] - S.hits[0], pd = S.tot[1] - S.hits[1], pe = S.tot[2] - S.hits[2];
         S.tot[0] = pa; S.tot[1] = pd; S.tot[2] = pe;
@@ -585,16 +572,15 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
     dig = warp_sum(dig);
     if (lane == 0) S.red[tid >> 5] = dig;
     __syncthreads();
-    if (tid == 0) {
-        unsigned long long d = 0;
-        for (uint32_t w = 0; w < T / 32; ++w) d += S.red[w];
+    if (tid < 13) {           // fire-and-forget adds into this job-epoch's counters
         seneca_job_epoch_stats* st = L.stats + (size_t)j * C.maxT + e;
-        for (uint32_t t = 0; t < 4; ++t) {
-            st->served[t] += S.hist[t] + S.hist[t | SUBST];
-            st->subst[t] += S.hist[t | SUBST];
-            if (t != T_S) st->req_hits[t] += S.hist[t];
-        }
-        st->digest += d;
+        unsigned long long* f = reinterpret_cast<unsigned long long*>(st);
+        unsigned long long v;
+        if (tid < 4) v = S.hist[tid] + S.hist[tid | SUBST];             // served[t]
+        else if (tid < 8) v = S.hist[(tid - 4) | SUBST];                // subst[t]
+        else if (tid < 12) v = tid == 8 ? 0ull : S.hist[tid - 8];       // req_hits[t]
+        else { v = 0; for (uint32_t w = 0; w < T / 32; ++w) v += S.red[w]; }   // digest
+        if (v) atomicAdd(f + tid, v);
     }
     __syncthreads();
     TM.tick(3);
@@ -602,7 +588,7 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
 
 // ------------------------------------------------------------------ maintain (a7)
 struct MaintSmem {
-    uint32_t ne, kmax, kspec, deficit0, PS, sizeA;
+    uint32_t ne, kmax, kspec, deficit0, PS, sizeA, prev_k;
     uint32_t add[kMaxJobs];
     uint32_t scan[33];
 };
@@ -691,6 +677,7 @@ __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSm
         *L.a_size = M.sizeA - ne + k;
         *L.evicted += ne;
         *L.refilled += k;
+        M.prev_k = k;
     }
     __syncthreads();
     TM.tick(4);
@@ -704,10 +691,9 @@ ods_rounds(Lay L, Cfg C, Launch P) {
     __shared__ MaintSmem M;
     __shared__ uint32_t s_n[kMaxJobs], s_e[kMaxJobs], s_active;
     const uint32_t tid = threadIdx.x;
-    const uint32_t cta = blockIdx.x, nctas = gridDim.x;
+    const uint32_t cta = blockIdx.x;
     const bool is_maint = cta == C.J;
     const uint32_t j = cta;
-    uint32_t gen = ldcg(L.bar + 1);
     __shared__ PhaseTimer TM;
     if (tid == 0) {
         TM.on = P.timing;
@@ -715,7 +701,8 @@ ods_rounds(Lay L, Cfg C, Launch P) {
         for (int k = 0; k < 16; ++k) TM.acc[k] = 0;
     }
 
-    // shared memory carve: job CTA s_req | s_miss | s_sub [Bmax] + s_pre [3][NS]; maintain CTA s_pre [NS]
+    // shared memory carve: job CTA s_req | s_miss | s_sub | s_oid [Bmax] + s_pre [3][NS] + s_osrc [Bmax];
+    // maintain CTA s_pre [NS]
     uint32_t* s_req = smem;
     uint32_t* s_miss = smem + C.Bmax;
     uint32_t* s_sub = smem + 2 * C.Bmax;
@@ -736,91 +723,76 @@ ods_rounds(Lay L, Cfg C, Launch P) {
         S.perm_seen = 0;
         S.dens = 1.0f;
     }
+    if (is_maint && tid == 0) M.prev_k = blockDim.x;
     __syncthreads();
 
     auto need_of = [&](uint32_t jj) -> uint32_t { return min(C.batch[jj], C.N - s_n[jj]); };
-
-    // prologue: the walk of the first round
-    if (!is_maint && ((s_active & P.subset) >> j & 1u)) {
-        const uint32_t need = need_of(j);
-        if (P.mode == 1) {
-            for (uint32_t s = tid; s < need; s += blockDim.x)
-                s_req[s] = P.requested[(size_t)P.row_of_job[j] * P.out_stride + s];
-            if (tid == 0) { S.need = need; S.wrap_slot = 0; }
-            __syncthreads();
-        } else {
-            job_walk(L, C, S, s_req, j, s_e[j], need, TM.on ? &TM.acc[7] : nullptr);
-        }
-    }
-
-    for (uint32_t rr = 0; rr < P.rounds; ++rr) {
-        const uint64_t r = P.r0 + rr;
-        const uint32_t part = s_active & P.subset;
-        // round schedule (data-independent, R-O12): who ends an epoch / departs
-        uint32_t departing = 0;
+    // data-independent schedule of the current round (R-O12)
+    auto schedule = [&](uint32_t& part, uint32_t& departing) {
+        part = s_active & P.subset;
+        departing = 0;
         for (uint32_t m = part; m; m &= m - 1) {
             const uint32_t jj = __ffs(m) - 1;
             if (s_n[jj] + need_of(jj) == C.N && s_e[jj] + 1 == C.target[jj]) departing |= 1u << jj;
         }
-        const uint32_t active_after = s_active & ~departing;
-        const bool full_scan = departing != 0;
-
-        bool spec = false;
-        if (is_maint) {
-            if (active_after && C.cap_a > 0) {
-                if (tid == 0) {
-                    M.PS = ldcg(L.cnt_tot + 3 * C.J);
-                    M.sizeA = ldcg(L.a_size);
-                    M.deficit0 = C.cap_a - M.sizeA;
-                    uint32_t cand = 0;
-                    for (uint32_t m = part; m; m &= m - 1) cand += need_of(__ffs(m) - 1);
-                    M.kmax = min(M.deficit0 + cand, M.PS);
-                }
-                __syncthreads();
-                if (!full_scan) {
-                    // one rank per thread ahead of time; the rest (if any) after eviction
-                    if (tid == 0) M.kspec = min(M.kmax, blockDim.x);
-                    __syncthreads();
-                    if (M.kspec) load_sup_prefix(L, C, 3 * C.J, s_pre, M.scan);
-                    TM.tick(0);
-                    maint_refill_select(L, C, M, s_pre, r, 0, M.kspec);
-                    TM.tick(1);
-                    spec = true;
-                }
-            }
-        } else if ((part >> j) & 1u) {
-            if (S.recount) { job_recount(L, C, j, s_pre); if (tid == 0) S.recount = 0; __syncthreads(); }
-            TM.tick(0);
-            job_round(L, C, P, S, s_req, s_miss, s_sub, s_oid, s_osrc, s_pre, j, r, s_e[j], s_n[j],
-                      __popc(active_after), TM);
-            // a8 (R-O16): the epoch ends with this batch -> reset seen_j and the walk
-            if (s_n[j] + S.need == C.N) {
-                uint4* sj = reinterpret_cast<uint4*>(L.seen + (size_t)j * C.NW);
-                for (uint32_t k = tid; k < C.NW / 4; k += blockDim.x) sj[k] = make_uint4(0, 0, 0, 0);
-                if (tid == 0) {
-                    S.cur_buf = 0; S.nxt_buf = 1; S.cursor = 0; S.cur_len = C.N; S.nxt_len = 0;
-                    S.recount = 1;
-                }
-                __syncthreads();
-            }
-            TM.tick(0);
-        }
-        if (is_maint) TM.tick(1);
-        if (coupled) round_barrier(L.bar, nctas, gen);
-        TM.tick(is_maint ? 2 : 4);
-
-        // schedule update (every CTA, identically)
+    };
+    auto advance = [&](uint32_t part, uint32_t departing) {
+        __syncthreads();
         if (tid == 0) {
             for (uint32_t m = part; m; m &= m - 1) {
                 const uint32_t jj = __ffs(m) - 1;
                 s_n[jj] += need_of(jj);
                 if (s_n[jj] == C.N) { s_n[jj] = 0; s_e[jj] += 1; }
             }
-            s_active = active_after;
+            s_active &= ~departing;
         }
         __syncthreads();
+    };
 
-        if (is_maint) {
+    // Coupled rounds synchronise through two one-directional signals (zeroed by
+    // the host before every launch): L.bar[0] counts job phases completed, L.bar[1]
+    // counts rounds whose maintain has been applied.  A job CTA only waits for
+    // maintain(r-1) before classifying round r; the maintain CTA only waits for
+    // the job phases of round r -- the next round's walk and speculative refill
+    // overlap everything else.
+    if (is_maint) {
+        uint32_t expect = 0;
+        bool spec = false;
+        // speculative refill ranks for the round about to be played: the storage
+        // pool as of round start cannot change before this round's maintain
+        auto speculate = [&](uint64_t r, uint32_t part, uint32_t departing) -> bool {
+            const uint32_t active_after = s_active & ~departing;
+            if (!(active_after && C.cap_a > 0) || departing) return false;
+            if (tid == 0) {
+                M.PS = ldcg(L.cnt_tot + 3 * C.J);
+                M.sizeA = ldcg(L.a_size);
+                M.deficit0 = C.cap_a - M.sizeA;
+                uint32_t cand = 0;
+                for (uint32_t m = part; m; m &= m - 1) cand += need_of(__ffs(m) - 1);
+                M.kmax = min(M.deficit0 + cand, M.PS);
+                M.kspec = min(M.kmax, min(blockDim.x, M.deficit0 + M.prev_k + 64u));
+            }
+            __syncthreads();
+            if (M.kspec) load_sup_prefix(L, C, 3 * C.J, s_pre, M.scan);
+            TM.tick(0);
+            maint_refill_select(L, C, M, s_pre, r, 0, M.kspec);
+            TM.tick(1);
+            return true;
+        };
+        {
+            uint32_t part, departing;
+            schedule(part, departing);
+            spec = speculate(P.r0, part, departing);
+        }
+        for (uint32_t rr = 0; rr < P.rounds; ++rr) {
+            const uint64_t r = P.r0 + rr;
+            uint32_t part, departing;
+            schedule(part, departing);
+            const uint32_t active_after = s_active & ~departing;
+            expect += __popc(part);
+            if (tid == 0) { while (ld_acquire(L.bar) < expect) { } }
+            __syncthreads();
+            TM.tick(2);
             if (active_after && C.cap_a > 0) {
                 if (!spec && tid == 0) {
                     M.PS = ldcg(L.cnt_tot + 3 * C.J);
@@ -828,15 +800,67 @@ ods_rounds(Lay L, Cfg C, Launch P) {
                     M.deficit0 = C.cap_a - M.sizeA;
                 }
                 __syncthreads();
-                TM.tick(2);
-                maint_apply(L, C, P, M, s_pre, r, active_after, full_scan, spec, TM);
+                maint_apply(L, C, P, M, s_pre, r, active_after, departing != 0, spec, TM);
+            } else {
+                if (tid == 0) *L.ne_ctr = 0;
             }
-        } else if (rr + 1 < P.rounds && ((active_after & P.subset) >> j & 1u)) {
-            job_walk(L, C, S, s_req, j, s_e[j], need_of(j), TM.on ? &TM.acc[7] : nullptr);   // next round's request
+            __syncthreads();
+            if (tid == 0) { __threadfence(); atomicExch(L.bar + 1, rr + 1); }     // release round r's tiers
+            TM.tick(5);
+            advance(part, departing);
+            spec = false;
+            if (rr + 1 < P.rounds) {
+                uint32_t part2, departing2;
+                schedule(part2, departing2);
+                spec = speculate(r + 1, part2, departing2);
+            }
         }
-        TM.tick(is_maint ? 4 : 5);
-        if (coupled) round_barrier(L.bar, nctas, gen);
-        TM.tick(is_maint ? 5 : 6);
+    } else {
+        // prologue: the walk of the first round
+        if ((s_active & P.subset) >> j & 1u) {
+            const uint32_t need = need_of(j);
+            if (P.mode == 1) {
+                for (uint32_t s = tid; s < need; s += blockDim.x)
+                    s_req[s] = P.requested[(size_t)P.row_of_job[j] * P.out_stride + s];
+                if (tid == 0) { S.need = need; S.wrap_slot = 0; }
+                __syncthreads();
+            } else {
+                job_walk(L, C, S, s_req, j, s_e[j], need, TM.on ? &TM.acc[7] : nullptr);
+            }
+        }
+        for (uint32_t rr = 0; rr < P.rounds; ++rr) {
+            const uint64_t r = P.r0 + rr;
+            uint32_t part, departing;
+            schedule(part, departing);
+            const uint32_t active_after = s_active & ~departing;
+            if (coupled && rr > 0) {                   // maintain(r-1) applied?
+                if (tid == 0) { while (ld_acquire(L.bar + 1) < rr) { } }
+                __syncthreads();
+            }
+            TM.tick(4);
+            if ((part >> j) & 1u) {
+                if (S.recount) { job_recount(L, C, j, s_pre); if (tid == 0) S.recount = 0; __syncthreads(); }
+                TM.tick(0);
+                job_round(L, C, P, S, s_req, s_miss, s_sub, s_oid, s_osrc, s_pre, j, r, s_e[j], s_n[j],
+                          __popc(active_after), TM);
+                // a8 (R-O16): the epoch ends with this batch -> reset seen_j and the walk
+                if (s_n[j] + S.need == C.N) {
+                    uint4* sj = reinterpret_cast<uint4*>(L.seen + (size_t)j * C.NW);
+                    for (uint32_t k = tid; k < C.NW / 4; k += blockDim.x) sj[k] = make_uint4(0, 0, 0, 0);
+                    if (tid == 0) {
+                        S.cur_buf = 0; S.nxt_buf = 1; S.cursor = 0; S.cur_len = C.N; S.nxt_len = 0;
+                        S.recount = 1;
+                    }
+                    __syncthreads();
+                }
+                if (coupled && tid == 0) { __threadfence(); atomicAdd(L.bar, 1u); }   // job phase done
+                TM.tick(0);
+            }
+            advance(part, departing);
+            if (rr + 1 < P.rounds && ((s_active & P.subset) >> j & 1u))
+                job_walk(L, C, S, s_req, j, s_e[j], need_of(j), TM.on ? &TM.acc[7] : nullptr);   // next request
+            TM.tick(5);
+        }
     }
     // persist the walk state
     if (!is_maint && tid == 0) {
@@ -1161,6 +1185,7 @@ seneca_status launch_rounds(seneca_ctx* c, uint64_t R, uint32_t jobs_mask, const
             return SENECA_EPROTO;
         }
     }
+    SENECA_CUDA_TRY(cudaMemsetAsync(c->L.bar, 0, 8, st));
     void* args[] = {&c->L, &c->C, &P};
     cudaError_t le = cudaSuccess;
     timed(c, K_ROUNDS, st, [&] {
