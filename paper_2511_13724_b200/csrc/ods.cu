@@ -70,6 +70,7 @@ struct Cfg {
     uint32_t N, NW, NB, NS, NBp;     // samples, words/bitmap, blocks, superblocks, padded blocks
     uint32_t J, Bmax, maxT, cap_a, cap_d, cap_e;
     uint32_t Nrow;                   // row stride of the permutation / lap lists (N rounded up to 64)
+    uint32_t FL;                     // capacity of one refill buffer
     uint64_t seed;
     uint32_t batch[kMaxJobs];
     uint32_t target[kMaxJobs];
@@ -90,14 +91,15 @@ struct Lay {
     JobDev *jobs;                    // [J]
     uint32_t *out_ids;               // [J][Bmax] replay scratch
     uint8_t *out_src;                // [J][Bmax]
-    uint32_t *evict_push;            // [J*Bmax] entries whose consumer count reached |active| this round
-    uint32_t *ne_ctr;                // [1] length of evict_push
+    uint32_t *evict_push;            // ring [J*Bmax]: entries whose consumer count reached |active|
+    uint32_t *fill_n;                // [2] refills of the rounds using fill buffer 0 / 1
     uint32_t *evict_list;            // [max(cap_a,1)]
-    uint32_t *fill_list;             // [max(cap_a,1) + J*Bmax]
+    uint32_t *fill_list;             // [2][FL], FL = max(cap_a,1) + J*Bmax; buffer = round parity
     seneca_job_epoch_stats *stats;   // [J][maxT]
     unsigned long long *evicted, *refilled;
     uint32_t *err;
-    uint32_t *bar;                   // [2] barrier count, generation
+    uint32_t *bar;                   // [4] signals: u64 {job phases done | evictions pushed << 32},
+                                     //     maintain rounds applied, eviction ring position
     unsigned long long *phase;       // [32] accumulated cycles per phase (see seneca.h)
 };
 
@@ -241,6 +243,12 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
     return v;
 }
 
+__device__ __forceinline__ unsigned long long ld_acquire64(const uint32_t* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
 // ------------------------------------------------------------------ per-CTA phase timer (profiling)
 struct PhaseTimer {
     long long last;
@@ -264,6 +272,7 @@ struct JobSmem {
     uint32_t perm_seen;   // epoch+1 whose permutation was observed published (0: none)
     float dens;           // unseen fraction observed by the last walk step (window sizing)
     uint32_t hist[8];
+    uint32_t npush;       // evictions pushed by this job this round
     uint32_t scan[33];
     unsigned long long red[(kThreads / 32) * 13];
 };
@@ -370,7 +379,7 @@ __device__ void job_walk(const Lay& L, const Cfg& C, JobSmem& S, uint32_t* s_req
 }
 
 // Rebuild the three pool counts of job j (epoch start: seen_j is empty).
-__device__ void job_recount(const Lay& L, const Cfg& C, uint32_t j, uint32_t* s_sup /* [3][NS] */) {
+__device__ void job_recount(const Lay& L, const Cfg& C, uint32_t j, uint32_t* s_sup /* [3][NS] */, uint32_t* tot3) {
     const uint32_t tid = threadIdx.x, T = blockDim.x;
     for (uint32_t k = tid; k < 3 * C.NS; k += T) s_sup[k] = 0;
     __syncthreads();
@@ -411,9 +420,9 @@ __device__ void job_recount(const Lay& L, const Cfg& C, uint32_t j, uint32_t* s_
     if ((tid & 31) == 0) { atomicAdd(&s_t[0], ta); atomicAdd(&s_t[1], td); atomicAdd(&s_t[2], te); }
     __syncthreads();
     if (tid == 0) {
-        L.cnt_tot[j * 3 + 0] = s_t[0];
-        L.cnt_tot[j * 3 + 1] = s_t[1];
-        L.cnt_tot[j * 3 + 2] = s_t[2];
+        L.cnt_tot[j * 3 + 0] = tot3[0] = s_t[0];
+        L.cnt_tot[j * 3 + 1] = tot3[1] = s_t[1];
+        L.cnt_tot[j * 3 + 2] = tot3[2] = s_t[2];
     }
     __syncthreads();
 }
@@ -427,9 +436,9 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
     uint32_t* seen_j = L.seen + (size_t)j * C.NW;
     uint32_t* cons_j = L.cons + (size_t)j * C.NW;
     const size_t row = (size_t)P.row_of_job[j] * P.out_stride;
-    const uint32_t tot_reg = tid < 3 ? ldcg(L.cnt_tot + j * 3 + tid) : 0u;   // consumed after classify
-    if (tid < 3) S.hits[tid] = 0;
+    if (tid < 3) S.hits[tid] = 0;       // the pool totals S.tot persist across rounds in shared memory
     if (tid < 8) S.hist[tid] = 0;
+    if (tid == 0) S.npush = 0;
     __syncthreads();
 
     // a3: hits (E, D, or A not consumed by j, R-O13) join seen_j now
@@ -464,8 +473,6 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
         if (is_miss) s_miss[mbase + ex] = s;
         mbase += tot;
     }
-    if (tid < 3) S.tot[tid] = tot_reg;
-    __syncthreads();
     if (tid == 0) {
         const uint32_t pa = S.tot[0] - S.hits[0], pd = S.tot[1] - S.hits[1], pe = S.tot[2] - S.hits[2];
         S.tot[0] = pa; S.tot[1] = pd; S.tot[2] = pe;
@@ -540,9 +547,9 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
     __syncthreads();
     if (tid == 0) {
         if (P.mode == 0) { S.cur_len += q1; S.nxt_len += q - q1; }
-        L.cnt_tot[j * 3 + 0] = S.tot[0] - k0;
-        L.cnt_tot[j * 3 + 1] = S.tot[1] - k1;
-        L.cnt_tot[j * 3 + 2] = S.tot[2] - k2;
+        S.tot[0] -= k0;
+        S.tot[1] -= k1;
+        S.tot[2] -= k2;
     }
 
     // a6: counters (per-warp ballot histogram of the 8 source codes), digest,
@@ -560,7 +567,10 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
             dig += splitmix64(((uint64_t)(nbase + s) << 35) | ((uint64_t)src << 32) | i);
             if (trow) trow[nbase + s] = ((unsigned long long)src << 32) | i;
             if ((src & 3u) == T_A) {
-                if (atomicAdd(L.cons_cnt + i, 1u) + 1u == n_act) L.evict_push[atomicAdd(L.ne_ctr, 1u)] = i;
+                if (atomicAdd(L.cons_cnt + i, 1u) + 1u == n_act) {
+                    L.evict_push[atomicAdd(L.bar + 3, 1u) % (C.J * C.Bmax)] = i;
+                    atomicAdd(&S.npush, 1u);
+                }
             }
         }
 #pragma unroll
@@ -589,6 +599,7 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
 // ------------------------------------------------------------------ maintain (a7)
 struct MaintSmem {
     uint32_t ne, kmax, kspec, deficit0, PS, sizeA, prev_k;
+    uint32_t ne_push, push_base;
     uint32_t add[kMaxJobs];
     uint32_t scan[33];
 };
@@ -600,20 +611,20 @@ __device__ void maint_refill_select(const Lay& L, const Cfg& C, MaintSmem& M, co
     if (u1 <= u0) return;
     const uint64_t key = derive_key(C.seed, PUR_REFILL, 0, r, 0);
     const PermDomain dom = perm_domain(M.PS);
+    uint32_t* fill = L.fill_list + (size_t)(r & 1) * C.FL;
     for (uint32_t u = u0 + threadIdx.x; u < u1; u += blockDim.x)
-        L.fill_list[u] = pool_select(L, C, 3 * C.J, T_S, 0, s_pre, perm_apply(key, dom, u));
+        fill[u] = pool_select(L, C, 3 * C.J, T_S, 0, s_pre, perm_apply(key, dom, u));
     __syncthreads();
 }
 
 // eviction of A entries consumed by every active job (R-O5, R-O6), refill from
 // the storage pool as of round start (R-O8), counts kept exact.
 __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSmem& M, uint32_t* s_pre,
-                            uint64_t r, uint32_t active, bool full_scan, bool speculated, PhaseTimer& TM) {
+                            uint64_t r, uint32_t active, bool full_scan, bool speculated, uint32_t ne_push,
+                            uint32_t push_base, PhaseTimer& TM) {
     const uint32_t tid = threadIdx.x, T = blockDim.x;
-    if (tid == 0) M.ne = full_scan ? 0u : ldcg(L.ne_ctr);
-    if (tid < kMaxJobs) M.add[tid] = 0;
+    if (tid == 0) M.ne = full_scan ? 0u : ne_push;
     __syncthreads();
-    const uint32_t* ev_list = L.evict_push;
     if (full_scan) {
         // the active set changed (R-O6): every A entry is a candidate; the consumer
         // counts of the survivors are rebuilt for the new active set
@@ -635,10 +646,8 @@ __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSm
                 L.cons_cnt[w * 32u + bit] = cnt;
             }
         }
-        ev_list = L.evict_list;
+        __syncthreads();
     }
-    __syncthreads();
-    if (tid == 0) *L.ne_ctr = 0;
     TM.tick(3);
     const uint32_t ne = M.ne;
     const uint32_t k = min(M.deficit0 + ne, M.PS);
@@ -649,30 +658,26 @@ __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSm
         maint_refill_select(L, C, M, s_pre, r, M.kspec, k);      // beyond the speculated ranks
     }
     const uint32_t spidx = 3 * C.J;
+    const uint32_t ring = C.J * C.Bmax;
     for (uint32_t u = tid; u < ne; u += T) {
-        const uint32_t i = ldcg(ev_list + u);
+        const uint32_t i = full_scan ? L.evict_list[u] : ldcg(L.evict_push + (push_base + u) % ring);
         const uint32_t w = i >> 5, b = 1u << (i & 31);
         atomicAnd(L.bm_a + w, ~b);
         for (uint32_t a = 0; a < C.J; ++a) atomicAnd(L.cons + (size_t)a * C.NW + w, ~b);
         L.cons_cnt[i] = 0;
         count_add(L, C, spidx, i, 1u);
     }
+    // refills enter A with no consumers; each job CTA adds them to its own A pool
+    // before its next classification (R-O8)
+    const uint32_t* fill = L.fill_list + (size_t)(r & 1) * C.FL;
     for (uint32_t u = tid; u < k; u += T) {
-        const uint32_t i = ldcg(L.fill_list + u);
-        const uint32_t w = i >> 5, b = 1u << (i & 31);
-        atomicOr(L.bm_a + w, b);
+        const uint32_t i = ldcg(fill + u);
+        atomicOr(L.bm_a + (i >> 5), 1u << (i & 31));
         count_add(L, C, spidx, i, 0xffffffffu);
-        for (uint32_t m = active; m; m &= m - 1) {
-            const uint32_t a = __ffs(m) - 1;
-            if (!(ldcg(L.seen + (size_t)a * C.NW + w) & b)) {
-                count_add(L, C, a * 3 + 0, i, 1u);
-                atomicAdd(&M.add[a], 1u);
-            }
-        }
     }
     __syncthreads();
-    if (tid < C.J && M.add[tid]) atomicAdd(L.cnt_tot + tid * 3 + 0, M.add[tid]);
     if (tid == 0) {
+        L.fill_n[r & 1] = k;
         L.cnt_tot[spidx] = M.PS + ne - k;
         *L.a_size = M.sizeA - ne + k;
         *L.evicted += ne;
@@ -681,6 +686,24 @@ __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSm
     }
     __syncthreads();
     TM.tick(4);
+}
+
+// Job j's A pool gains the refills of round r it has not seen (its CTA alone
+// owns its pool counts; recount at an epoch start covers them instead).
+__device__ void job_take_refills(const Lay& L, const Cfg& C, JobSmem& S, uint32_t j, uint64_t r) {
+    const uint32_t kf = ldcg(L.fill_n + (r & 1));
+    const uint32_t* fill = L.fill_list + (size_t)(r & 1) * C.FL;
+    const uint32_t* seen_j = L.seen + (size_t)j * C.NW;
+    uint32_t add = 0;
+    for (uint32_t u = threadIdx.x; u < kf; u += blockDim.x) {
+        const uint32_t i = ldcg(fill + u);
+        if (!((ldcg(seen_j + (i >> 5)) >> (i & 31)) & 1u)) {
+            count_add(L, C, j * 3 + 0, i, 1u);
+            ++add;
+        }
+    }
+    add = warp_sum(add);
+    if ((threadIdx.x & 31) == 0 && add) atomicAdd(&S.tot[0], add);
 }
 
 // ------------------------------------------------------------------ the persistent round kernel
@@ -723,6 +746,7 @@ ods_rounds(Lay L, Cfg C, Launch P) {
         S.perm_seen = 0;
         S.dens = 1.0f;
     }
+    if (!is_maint && tid < 3) S.tot[tid] = ldcg(L.cnt_tot + j * 3 + tid);
     if (is_maint && tid == 0) M.prev_k = blockDim.x;
     __syncthreads();
 
@@ -756,7 +780,7 @@ ods_rounds(Lay L, Cfg C, Launch P) {
     // the job phases of round r -- the next round's walk and speculative refill
     // overlap everything else.
     if (is_maint) {
-        uint32_t expect = 0;
+        uint32_t expect = 0, push_total = 0;
         bool spec = false;
         // speculative refill ranks for the round about to be played: the storage
         // pool as of round start cannot change before this round's maintain
@@ -790,7 +814,14 @@ ods_rounds(Lay L, Cfg C, Launch P) {
             schedule(part, departing);
             const uint32_t active_after = s_active & ~departing;
             expect += __popc(part);
-            if (tid == 0) { while (ld_acquire(L.bar) < expect) { } }
+            if (tid == 0) {                  // job phases of round r done; evictions they pushed
+                unsigned long long v;
+                while ((uint32_t)(v = ld_acquire64(L.bar)) < expect) { }
+                const uint32_t pushed = (uint32_t)(v >> 32);
+                M.ne_push = pushed - push_total;
+                M.push_base = push_total;
+                push_total = pushed;
+            }
             __syncthreads();
             TM.tick(2);
             if (active_after && C.cap_a > 0) {
@@ -800,12 +831,10 @@ ods_rounds(Lay L, Cfg C, Launch P) {
                     M.deficit0 = C.cap_a - M.sizeA;
                 }
                 __syncthreads();
-                maint_apply(L, C, P, M, s_pre, r, active_after, departing != 0, spec, TM);
-            } else {
-                if (tid == 0) *L.ne_ctr = 0;
+                maint_apply(L, C, P, M, s_pre, r, active_after, departing != 0, spec, M.ne_push, M.push_base, TM);
             }
             __syncthreads();
-            if (tid == 0) { __threadfence(); atomicExch(L.bar + 1, rr + 1); }     // release round r's tiers
+            if (tid == 0) { __threadfence(); atomicExch(L.bar + 2, rr + 1); }     // release round r's tiers
             TM.tick(5);
             advance(part, departing);
             spec = false;
@@ -834,12 +863,13 @@ ods_rounds(Lay L, Cfg C, Launch P) {
             schedule(part, departing);
             const uint32_t active_after = s_active & ~departing;
             if (coupled && rr > 0) {                   // maintain(r-1) applied?
-                if (tid == 0) { while (ld_acquire(L.bar + 1) < rr) { } }
+                if (tid == 0) { while (ld_acquire(L.bar + 2) < rr) { } }
                 __syncthreads();
             }
             TM.tick(4);
             if ((part >> j) & 1u) {
-                if (S.recount) { job_recount(L, C, j, s_pre); if (tid == 0) S.recount = 0; __syncthreads(); }
+                if (S.recount) { job_recount(L, C, j, s_pre, S.tot); if (tid == 0) S.recount = 0; __syncthreads(); }
+                else if (coupled && rr > 0) { job_take_refills(L, C, S, j, r - 1); __syncthreads(); }
                 TM.tick(0);
                 job_round(L, C, P, S, s_req, s_miss, s_sub, s_oid, s_osrc, s_pre, j, r, s_e[j], s_n[j],
                           __popc(active_after), TM);
@@ -853,7 +883,10 @@ ods_rounds(Lay L, Cfg C, Launch P) {
                     }
                     __syncthreads();
                 }
-                if (coupled && tid == 0) { __threadfence(); atomicAdd(L.bar, 1u); }   // job phase done
+                if (coupled && tid == 0) {                 // job phase done (+ evictions pushed)
+                    __threadfence();
+                    atomicAdd(reinterpret_cast<unsigned long long*>(L.bar), 1ull + ((unsigned long long)S.npush << 32));
+                }
                 TM.tick(0);
             }
             advance(part, departing);
@@ -861,6 +894,16 @@ ods_rounds(Lay L, Cfg C, Launch P) {
                 job_walk(L, C, S, s_req, j, s_e[j], need_of(j), TM.on ? &TM.acc[7] : nullptr);   // next request
             TM.tick(5);
         }
+    }
+    // epilogue: the last round's refills into this job's A pool; persist the totals
+    if (!is_maint) {
+        if (coupled && P.rounds > 0 && (s_active >> j & 1u)) {
+            if (tid == 0) { while (ld_acquire(L.bar + 2) < P.rounds) { } }
+            __syncthreads();
+            if (!S.recount) job_take_refills(L, C, S, j, P.r0 + P.rounds - 1);
+            __syncthreads();
+        }
+        if (tid < 3) L.cnt_tot[j * 3 + tid] = S.tot[tid];
     }
     // persist the walk state
     if (!is_maint && tid == 0) {
@@ -1066,6 +1109,7 @@ Sizes compute_sizes(const seneca_cache_config* cfg) {
     C.cap_e = (uint32_t)cfg->cap_e;
     C.seed = cfg->seed;
     C.Nrow = (C.N + 63) & ~63u;
+    C.FL = (uint32_t)(std::max<size_t>(cfg->cap_a, 1) + (size_t)C.J * C.Bmax);
     const size_t W = (size_t)C.NW * 4, P = 3 * (size_t)C.J + 1;
     const size_t capl = std::max<size_t>(cfg->cap_a, 1) * 4;
     const size_t sz[] = {
@@ -1079,10 +1123,10 @@ Sizes compute_sizes(const seneca_cache_config* cfg) {
         (size_t)C.J * C.maxT * 4, (size_t)C.J * C.maxT * 4, // 12-13 perm_ready, perm_done
         (size_t)C.J * sizeof(JobDev),                       // 14 jobs
         (size_t)C.J * C.Bmax * 4, (size_t)C.J * C.Bmax,     // 15-16 out_ids, out_src
-        (size_t)C.J * C.Bmax * 4, 4,                        // 17-18 evict_push, ne_ctr
-        capl, capl + (size_t)C.J * C.Bmax * 4,              // 19-20 evict, fill
+        (size_t)C.J * C.Bmax * 4, 8,                        // 17-18 evict_push, fill_n
+        capl, 2 * (capl + (size_t)C.J * C.Bmax * 4),        // 19-20 evict, fill [2]
         (size_t)C.J * C.maxT * sizeof(seneca_job_epoch_stats),  // 21 stats
-        8, 8, 4, 8, 256,                                    // 22-26 evicted, refilled, err, bar, phase
+        8, 8, 4, 16, 256,                                   // 22-26 evicted, refilled, err, bar, phase
     };
     size_t at = 0;
     for (size_t k = 0; k < sizeof(sz) / sizeof(sz[0]); ++k) {
@@ -1113,7 +1157,7 @@ Lay carve(const Sizes& z, char* base) {
     L.out_ids = (uint32_t*)(base + z.off[15]);
     L.out_src = (uint8_t*)(base + z.off[16]);
     L.evict_push = (uint32_t*)(base + z.off[17]);
-    L.ne_ctr = (uint32_t*)(base + z.off[18]);
+    L.fill_n = (uint32_t*)(base + z.off[18]);
     L.evict_list = (uint32_t*)(base + z.off[19]);
     L.fill_list = (uint32_t*)(base + z.off[20]);
     L.stats = (seneca_job_epoch_stats*)(base + z.off[21]);
@@ -1185,7 +1229,7 @@ seneca_status launch_rounds(seneca_ctx* c, uint64_t R, uint32_t jobs_mask, const
             return SENECA_EPROTO;
         }
     }
-    SENECA_CUDA_TRY(cudaMemsetAsync(c->L.bar, 0, 8, st));
+    SENECA_CUDA_TRY(cudaMemsetAsync(c->L.bar, 0, 16, st));
     void* args[] = {&c->L, &c->C, &P};
     cudaError_t le = cudaSuccess;
     timed(c, K_ROUNDS, st, [&] {
