@@ -54,6 +54,7 @@ constexpr uint32_t kBlockShift = 8;          // 256 ids (8 words) per count bloc
 constexpr uint32_t kSuperShift = 13;         // 32 blocks = 8192 ids per superblock
 constexpr uint32_t kWordsPerBlock = 8;
 constexpr uint32_t kWalkPerThread = 8;       // list entries examined per thread per walk step
+constexpr uint32_t kWinMax = 1024;           // prefetched walk window (list entries)
 
 // ------------------------------------------------------------------ layouts
 struct JobDev {           // per-job persistent walk state (workspace)
@@ -71,6 +72,7 @@ struct Cfg {
     uint32_t J, Bmax, maxT, cap_a, cap_d, cap_e;
     uint32_t Nrow;                   // row stride of the permutation / lap lists (N rounded up to 64)
     uint32_t FL;                     // capacity of one refill buffer
+    uint32_t HS;                     // served-set hash slots (power of two >= 2 Bmax)
     uint64_t seed;
     uint32_t batch[kMaxJobs];
     uint32_t target[kMaxJobs];
@@ -122,6 +124,14 @@ struct Launch {
 
 __device__ __forceinline__ uint32_t ldcg(const uint32_t* p) { return __ldcg(p); }
 __device__ __forceinline__ uint4 ldcg4(const uint32_t* p) { return __ldcg(reinterpret_cast<const uint4*>(p)); }
+
+// asynchronous 16-B global -> shared copies (L2 only, never a stale L1 line)
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 __device__ __forceinline__ uint32_t valid_mask(const Cfg& C, uint32_t w) {
     const uint64_t lo = (uint64_t)w * 32u;
@@ -273,6 +283,10 @@ struct JobSmem {
     float dens;           // unseen fraction observed by the last walk step (window sizing)
     uint32_t hist[8];
     uint32_t npush;       // evictions pushed by this job this round
+    // prefetch of the next walk window (R-O1 walk, see job_walk_prefetched)
+    uint32_t pf_state;    // 0 none, 1 list window requested, 2 seen chunks requested
+    uint32_t pf_buf, pf_epoch, pf_base, pf_len, pf_vlen;
+    uint32_t hs_mask;     // served-set hash size - 1
     uint32_t scan[33];
     unsigned long long red[(kThreads / 32) * 13];
 };
@@ -281,11 +295,67 @@ __device__ __forceinline__ const uint32_t* list_ptr(const Lay& L, const Cfg& C, 
     return buf == 0 ? L.perms + ((size_t)j * C.maxT + e) * C.Nrow : L.laps + ((size_t)j * 2 + (buf - 1)) * C.Nrow;
 }
 
+// Set of ids served to the job in the current round (shared-memory open
+// addressing, load factor <= 1/2): the walk that follows corrects prefetched
+// seen words with it, since only this job's CTA ever sets seen_j bits.
+__device__ __forceinline__ uint32_t hash_slot(uint32_t id, uint32_t mask) { return (id * 2654435761u >> 7) & mask; }
+__device__ __forceinline__ void hash_insert(uint32_t* h, uint32_t mask, uint32_t id) {
+    for (uint32_t s = hash_slot(id, mask);; s = (s + 1) & mask) {
+        const uint32_t old = atomicCAS(h + s, 0u, id + 1);
+        if (old == 0 || old == id + 1) return;
+    }
+}
+__device__ __forceinline__ bool hash_has(const uint32_t* h, uint32_t mask, uint32_t id) {
+    for (uint32_t s = hash_slot(id, mask);; s = (s + 1) & mask) {
+        const uint32_t v = h[s];
+        if (v == id + 1) return true;
+        if (v == 0) return false;
+    }
+}
+
+// Stage 1 (right after a walk): the next walk window of the current list into
+// shared memory.  The list content below cur_len never changes.
+__device__ void prefetch_window(const Lay& L, const Cfg& C, JobSmem& S, uint32_t* s_win, uint32_t j, uint32_t e,
+                                uint32_t want) {
+    const uint32_t tid = threadIdx.x;
+    const uint32_t base = S.cursor & ~3u;
+    uint32_t len = min(kWinMax, (want + (S.cursor - base) + 3) & ~3u);
+    len = min(len, C.Nrow - base);
+    const uint32_t* list = list_ptr(L, C, j, e, S.cur_buf);
+    for (uint32_t t = tid; t * 4 < len; t += blockDim.x) cp_async16(s_win + 4 * t, list + base + 4 * t);
+    cp_async_commit();
+    if (tid == 0) {
+        S.pf_state = 1; S.pf_buf = S.cur_buf; S.pf_epoch = e; S.pf_base = base; S.pf_len = len;
+    }
+}
+
+// Stage 2 (mid job phase, once the window has landed): the 16-B seen chunk of
+// every window id, asynchronously.
+__device__ void prefetch_seen(const Lay& L, const Cfg& C, JobSmem& S, const uint32_t* s_win, uint4* s_wseen, uint32_t j) {
+    const uint32_t tid = threadIdx.x;
+    cp_async_wait_all();
+    __syncthreads();
+    const uint32_t vlen = S.cur_len > S.pf_base ? min(S.pf_len, S.cur_len - S.pf_base) : 0u;
+    const uint32_t* seen_j = L.seen + (size_t)j * C.NW;
+    for (uint32_t t = tid; t < vlen; t += blockDim.x) {
+        const uint32_t id = s_win[t];
+        cp_async16(s_wseen + t, seen_j + ((id >> 5) & ~3u));
+    }
+    cp_async_commit();
+    __syncthreads();
+    if (tid == 0) { S.pf_state = 2; S.pf_vlen = vlen; }
+}
+
 // a1/a2 (R-O1): the first `need` ids of the job's current lap list, from the
 // cursor, that are not in seen_j.  At a lap end the walk continues with the
 // list of deferred misses of the lap (slot order = position order).
+struct WalkPrefetch {
+    const uint4* wseen;      // [kWinMax] prefetched 16-B seen chunks
+    const uint32_t* hash;    // served-set hash
+};
+
 __device__ void job_walk(const Lay& L, const Cfg& C, JobSmem& S, uint32_t* s_req, uint32_t j, uint32_t e, uint32_t need,
-                         unsigned long long* iters) {
+                         unsigned long long* iters, const uint32_t* s_win, const WalkPrefetch* pf) {
     const uint32_t tid = threadIdx.x, T = blockDim.x;
     const uint32_t* seen_j = L.seen + (size_t)j * C.NW;
     if (tid == 0) { S.wrap_slot = 0; S.need = need; }
@@ -299,6 +369,60 @@ __device__ void job_walk(const Lay& L, const Cfg& C, JobSmem& S, uint32_t* s_req
     __syncthreads();
     uint32_t taken = 0;
     bool wrapped = false;
+    if (pf && S.pf_state != 0) {
+        // first step from the prefetched window: seen = prefetched seen word OR served
+        // since the prefetch (the served set of the round just played)
+        cp_async_wait_all();
+        __syncthreads();
+        const bool usable = S.pf_state == 2 && S.pf_buf == S.cur_buf && S.pf_epoch == e &&
+                            S.cursor >= S.pf_base && S.cursor < S.pf_base + S.pf_vlen;
+        if (usable) {
+            const uint32_t cursor = S.cursor, wend = S.pf_base + S.pf_vlen;
+            if (iters && tid == 0) *iters += 1;
+            const uint32_t p0 = S.pf_base + tid * 2;
+            uint32_t flags = 0, cnt = 0, ids[2];
+#pragma unroll
+            for (uint32_t k = 0; k < 2; ++k) {
+                const uint32_t p = p0 + k;
+                ids[k] = 0;
+                if (p >= cursor && p < wend) {
+                    const uint32_t t = p - S.pf_base, id = s_win[t];
+                    const uint4 ch = pf->wseen[t];
+                    const uint32_t q = (id >> 5) & 3u;
+                    const uint32_t w = q == 0 ? ch.x : (q == 1 ? ch.y : (q == 2 ? ch.z : ch.w));
+                    ids[k] = id;
+                    if (!((w >> (id & 31)) & 1u) && !hash_has(pf->hash, S.hs_mask, id)) { flags |= 1u << k; ++cnt; }
+                }
+            }
+            uint32_t tot;
+            const uint32_t ex = block_exclusive_scan(cnt, &tot, S.scan);
+            uint32_t r = ex;
+#pragma unroll
+            for (uint32_t k = 0; k < 2; ++k) {
+                if (flags & (1u << k)) {
+                    if (r < need) s_req[r] = ids[k];
+                    if (r == need - 1) S.newcursor = p0 + k + 1;
+                    ++r;
+                }
+            }
+            __syncthreads();
+            if (tot >= need) {
+                if (tid == 0) {
+                    S.cursor = S.newcursor;
+                    S.dens = (float)need / (float)max(1u, S.newcursor - cursor);
+                }
+                taken = need;
+            } else {
+                if (tid == 0) {
+                    S.cursor = wend;
+                    S.dens = (float)tot / (float)max(1u, wend - cursor);
+                }
+                taken = tot;
+            }
+        }
+        if (tid == 0) S.pf_state = 0;
+        __syncthreads();
+    }
     while (taken < need) {
         if (S.cursor >= S.cur_len) {
             __syncthreads();
@@ -430,7 +554,8 @@ __device__ void job_recount(const Lay& L, const Cfg& C, uint32_t j, uint32_t* s_
 // a3-a6 for job j in round r: classify, substitute, respond.
 __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& S, uint32_t* s_req, uint32_t* s_miss,
                           uint32_t* s_sub, uint32_t* s_oid, uint8_t* s_osrc, uint32_t* s_pre, uint32_t j, uint64_t r,
-                          uint32_t e, uint32_t nbase, uint32_t n_act, PhaseTimer& TM) {
+                          uint32_t e, uint32_t nbase, uint32_t n_act, PhaseTimer& TM, const uint32_t* s_win,
+                          uint4* s_wseen, uint32_t* s_hash) {
     const uint32_t tid = threadIdx.x, T = blockDim.x;
     const uint32_t need = S.need;
     uint32_t* seen_j = L.seen + (size_t)j * C.NW;
@@ -439,6 +564,7 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
     if (tid < 3) S.hits[tid] = 0;       // the pool totals S.tot persist across rounds in shared memory
     if (tid < 8) S.hist[tid] = 0;
     if (tid == 0) S.npush = 0;
+    if (P.mode == 0) for (uint32_t k = tid; k <= S.hs_mask; k += T) s_hash[k] = 0;
     __syncthreads();
 
     // a3: hits (E, D, or A not consumed by j, R-O13) join seen_j now
@@ -483,6 +609,7 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
         S.k[2] = min(m - S.k[0] - S.k[1], pe);
     }
     __syncthreads();
+    if (P.mode == 0 && S.pf_state == 1) prefetch_seen(L, C, S, s_win, s_wseen, j);   // next walk, stage 2
     TM.tick(1);
 
     // a4/a5: misses in slot order take substitutes A -> D -> E at keyed ranks (R-O2)
@@ -566,6 +693,7 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
             src = s_osrc[s];
             dig += splitmix64(((uint64_t)(nbase + s) << 35) | ((uint64_t)src << 32) | i);
             if (trow) trow[nbase + s] = ((unsigned long long)src << 32) | i;
+            if (P.mode == 0) hash_insert(s_hash, S.hs_mask, i);
             if ((src & 3u) == T_A) {
                 if (atomicAdd(L.cons_cnt + i, 1u) + 1u == n_act) {
                     L.evict_push[atomicAdd(L.bar + 3, 1u) % (C.J * C.Bmax)] = i;
@@ -709,7 +837,7 @@ __device__ void job_take_refills(const Lay& L, const Cfg& C, JobSmem& S, uint32_
 // ------------------------------------------------------------------ the persistent round kernel
 __global__ void __launch_bounds__(kThreads, 1)
 ods_rounds(Lay L, Cfg C, Launch P) {
-    extern __shared__ uint32_t smem[];
+    extern __shared__ __align__(16) uint32_t smem[];
     __shared__ JobSmem S;
     __shared__ MaintSmem M;
     __shared__ uint32_t s_n[kMaxJobs], s_e[kMaxJobs], s_active;
@@ -731,7 +859,16 @@ ods_rounds(Lay L, Cfg C, Launch P) {
     uint32_t* s_sub = smem + 2 * C.Bmax;
     uint32_t* s_oid = smem + 3 * C.Bmax;
     uint32_t* s_pre = smem + 4 * C.Bmax;
-    uint8_t* s_osrc = reinterpret_cast<uint8_t*>(smem + 4 * C.Bmax + 3 * C.NS);
+    const uint32_t o_win = 4 * C.Bmax + 3 * C.NS;
+    uint32_t* s_win = smem + o_win;
+    uint32_t* s_hash = s_win + kWinMax;
+    const uint32_t o_wseen = (o_win + kWinMax + C.HS + 3) & ~3u;
+    uint4* s_wseen = reinterpret_cast<uint4*>(smem + o_wseen);
+    uint8_t* s_osrc = reinterpret_cast<uint8_t*>(smem + o_wseen + 4 * kWinMax);
+    WalkPrefetch pfs;
+    pfs.wseen = s_wseen;
+    pfs.hash = s_hash;
+    const WalkPrefetch* pf = P.mode == 0 ? &pfs : nullptr;
     // with no augmented tier there is no cross-job interaction at all (E and D are
     // static, maintain has nothing to do): the job CTAs run their rounds independently
     const bool coupled = C.cap_a > 0;
@@ -745,6 +882,8 @@ ods_rounds(Lay L, Cfg C, Launch P) {
         S.cur_len = jd.cur_len; S.nxt_len = jd.nxt_len; S.recount = jd.recount;
         S.perm_seen = 0;
         S.dens = 1.0f;
+        S.pf_state = 0;
+        S.hs_mask = C.HS - 1;
     }
     if (!is_maint && tid < 3) S.tot[tid] = ldcg(L.cnt_tot + j * 3 + tid);
     if (is_maint && tid == 0) M.prev_k = blockDim.x;
@@ -854,7 +993,9 @@ ods_rounds(Lay L, Cfg C, Launch P) {
                 if (tid == 0) { S.need = need; S.wrap_slot = 0; }
                 __syncthreads();
             } else {
-                job_walk(L, C, S, s_req, j, s_e[j], need, TM.on ? &TM.acc[7] : nullptr);
+                job_walk(L, C, S, s_req, j, s_e[j], need, TM.on ? &TM.acc[7] : nullptr, s_win, nullptr);
+                if (P.rounds > 1)
+                    prefetch_window(L, C, S, s_win, j, s_e[j], (uint32_t)(C.batch[j] / fmaxf(S.dens, 1.0f / 64.0f) * 1.15f) + 64);
             }
         }
         for (uint32_t rr = 0; rr < P.rounds; ++rr) {
@@ -872,7 +1013,7 @@ ods_rounds(Lay L, Cfg C, Launch P) {
                 else if (coupled && rr > 0) { job_take_refills(L, C, S, j, r - 1); __syncthreads(); }
                 TM.tick(0);
                 job_round(L, C, P, S, s_req, s_miss, s_sub, s_oid, s_osrc, s_pre, j, r, s_e[j], s_n[j],
-                          __popc(active_after), TM);
+                          __popc(active_after), TM, s_win, s_wseen, s_hash);
                 // a8 (R-O16): the epoch ends with this batch -> reset seen_j and the walk
                 if (s_n[j] + S.need == C.N) {
                     uint4* sj = reinterpret_cast<uint4*>(L.seen + (size_t)j * C.NW);
@@ -890,8 +1031,11 @@ ods_rounds(Lay L, Cfg C, Launch P) {
                 TM.tick(0);
             }
             advance(part, departing);
-            if (rr + 1 < P.rounds && ((s_active & P.subset) >> j & 1u))
-                job_walk(L, C, S, s_req, j, s_e[j], need_of(j), TM.on ? &TM.acc[7] : nullptr);   // next request
+            if (rr + 1 < P.rounds && ((s_active & P.subset) >> j & 1u)) {
+                job_walk(L, C, S, s_req, j, s_e[j], need_of(j), TM.on ? &TM.acc[7] : nullptr, s_win, pf);   // next request
+                if (rr + 2 < P.rounds)
+                    prefetch_window(L, C, S, s_win, j, s_e[j], (uint32_t)(C.batch[j] / fmaxf(S.dens, 1.0f / 64.0f) * 1.15f) + 64);
+            }
             TM.tick(5);
         }
     }
@@ -905,6 +1049,7 @@ ods_rounds(Lay L, Cfg C, Launch P) {
         }
         if (tid < 3) L.cnt_tot[j * 3 + tid] = S.tot[tid];
     }
+    cp_async_wait_all();
     // persist the walk state
     if (!is_maint && tid == 0) {
         JobDev& jd = L.jobs[j];
@@ -1110,6 +1255,8 @@ Sizes compute_sizes(const seneca_cache_config* cfg) {
     C.seed = cfg->seed;
     C.Nrow = (C.N + 63) & ~63u;
     C.FL = (uint32_t)(std::max<size_t>(cfg->cap_a, 1) + (size_t)C.J * C.Bmax);
+    C.HS = 64;
+    while (C.HS < 2 * C.Bmax) C.HS <<= 1;
     const size_t W = (size_t)C.NW * 4, P = 3 * (size_t)C.J + 1;
     const size_t capl = std::max<size_t>(cfg->cap_a, 1) * 4;
     const size_t sz[] = {
@@ -1274,7 +1421,8 @@ extern "C" seneca_status seneca_init_cache(const seneca_cache_config* cfg, void*
     if ((uintptr_t)d_workspace & 255) { set_error("workspace must be 256-byte aligned"); return SENECA_EINVAL; }
     Sizes z = compute_sizes(cfg);
     if (ws_bytes < z.total) { set_error("workspace %zu bytes < required %zu", ws_bytes, z.total); return SENECA_ENOSPC; }
-    const size_t round_smem = (size_t)4 * z.C.Bmax * 4 + (size_t)3 * z.C.NS * 4 + z.C.Bmax;
+    const size_t o_wseen = ((size_t)4 * z.C.Bmax + 3 * z.C.NS + kWinMax + z.C.HS + 3) & ~(size_t)3;
+    const size_t round_smem = (o_wseen + 4 * kWinMax) * 4 + z.C.Bmax;
     if (round_smem > 200 * 1024) { set_error("batch/dataset too large for the shared-memory indices"); return SENECA_EINVAL; }
     seneca_ctx* c = new (std::nothrow) seneca_ctx();
     if (!c) { set_error("out of host memory"); return SENECA_EINVAL; }
