@@ -859,7 +859,7 @@ ods_rounds(Lay L, Cfg C, Launch P) {
     uint32_t* s_sub = smem + 2 * C.Bmax;
     uint32_t* s_oid = smem + 3 * C.Bmax;
     uint32_t* s_pre = smem + 4 * C.Bmax;
-    const uint32_t o_win = 4 * C.Bmax + 3 * C.NS;
+    const uint32_t o_win = (4 * C.Bmax + 3 * C.NS + 3) & ~3u;       // 16-B aligned (cp.async)
     uint32_t* s_win = smem + o_win;
     uint32_t* s_hash = s_win + kWinMax;
     const uint32_t o_wseen = (o_win + kWinMax + C.HS + 3) & ~3u;
@@ -1421,7 +1421,8 @@ extern "C" seneca_status seneca_init_cache(const seneca_cache_config* cfg, void*
     if ((uintptr_t)d_workspace & 255) { set_error("workspace must be 256-byte aligned"); return SENECA_EINVAL; }
     Sizes z = compute_sizes(cfg);
     if (ws_bytes < z.total) { set_error("workspace %zu bytes < required %zu", ws_bytes, z.total); return SENECA_ENOSPC; }
-    const size_t o_wseen = ((size_t)4 * z.C.Bmax + 3 * z.C.NS + kWinMax + z.C.HS + 3) & ~(size_t)3;
+    const size_t o_win = ((size_t)4 * z.C.Bmax + 3 * z.C.NS + 3) & ~(size_t)3;
+    const size_t o_wseen = (o_win + kWinMax + z.C.HS + 3) & ~(size_t)3;
     const size_t round_smem = (o_wseen + 4 * kWinMax) * 4 + z.C.Bmax;
     if (round_smem > 200 * 1024) { set_error("batch/dataset too large for the shared-memory indices"); return SENECA_EINVAL; }
     seneca_ctx* c = new (std::nothrow) seneca_ctx();
