@@ -355,7 +355,8 @@ struct WalkPrefetch {
 };
 
 __device__ void job_walk(const Lay& L, const Cfg& C, JobSmem& S, uint32_t* s_req, uint32_t j, uint32_t e, uint32_t need,
-                         unsigned long long* iters, const uint32_t* s_win, const WalkPrefetch* pf) {
+                         PhaseTimer& TM, const uint32_t* s_win, const WalkPrefetch* pf) {
+    unsigned long long* iters = TM.on ? &TM.acc[7] : nullptr;
     const uint32_t tid = threadIdx.x, T = blockDim.x;
     const uint32_t* seen_j = L.seen + (size_t)j * C.NW;
     if (tid == 0) { S.wrap_slot = 0; S.need = need; }
@@ -422,6 +423,7 @@ __device__ void job_walk(const Lay& L, const Cfg& C, JobSmem& S, uint32_t* s_req
         }
         if (tid == 0) S.pf_state = 0;
         __syncthreads();
+        TM.tick(12);
     }
     while (taken < need) {
         if (S.cursor >= S.cur_len) {
@@ -672,6 +674,7 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
         }
     }
     __syncthreads();
+    TM.tick(10);
     if (tid == 0) {
         if (P.mode == 0) { S.cur_len += q1; S.nxt_len += q - q1; }
         S.tot[0] -= k0;
@@ -710,6 +713,7 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
     dig = warp_sum(dig);
     if (lane == 0) S.red[tid >> 5] = dig;
     __syncthreads();
+    TM.tick(11);
     if (tid < 13) {           // fire-and-forget adds into this job-epoch's counters
         seneca_job_epoch_stats* st = L.stats + (size_t)j * C.maxT + e;
         unsigned long long* f = reinterpret_cast<unsigned long long*>(st);
@@ -993,7 +997,7 @@ ods_rounds(Lay L, Cfg C, Launch P) {
                 if (tid == 0) { S.need = need; S.wrap_slot = 0; }
                 __syncthreads();
             } else {
-                job_walk(L, C, S, s_req, j, s_e[j], need, TM.on ? &TM.acc[7] : nullptr, s_win, nullptr);
+                job_walk(L, C, S, s_req, j, s_e[j], need, TM, s_win, nullptr);
                 if (P.rounds > 1)
                     prefetch_window(L, C, S, s_win, j, s_e[j], (uint32_t)(C.batch[j] / fmaxf(S.dens, 1.0f / 64.0f) * 1.15f) + 64);
             }
@@ -1032,9 +1036,11 @@ ods_rounds(Lay L, Cfg C, Launch P) {
             }
             advance(part, departing);
             if (rr + 1 < P.rounds && ((s_active & P.subset) >> j & 1u)) {
-                job_walk(L, C, S, s_req, j, s_e[j], need_of(j), TM.on ? &TM.acc[7] : nullptr, s_win, pf);   // next request
+                job_walk(L, C, S, s_req, j, s_e[j], need_of(j), TM, s_win, pf);   // next request
+                TM.tick(13);
                 if (rr + 2 < P.rounds)
                     prefetch_window(L, C, S, s_win, j, s_e[j], (uint32_t)(C.batch[j] / fmaxf(S.dens, 1.0f / 64.0f) * 1.15f) + 64);
+                TM.tick(14);
             }
             TM.tick(5);
         }
