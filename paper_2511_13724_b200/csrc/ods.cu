@@ -72,7 +72,6 @@ struct Cfg {
     uint32_t J, Bmax, maxT, cap_a, cap_d, cap_e;
     uint32_t Nrow;                   // row stride of the permutation / lap lists (N rounded up to 64)
     uint32_t FL;                     // capacity of one refill buffer
-    uint32_t HS;                     // served-set hash slots (power of two >= 2 Bmax)
     uint64_t seed;
     uint32_t batch[kMaxJobs];
     uint32_t target[kMaxJobs];
@@ -281,36 +280,16 @@ struct JobSmem {
     uint32_t recount;
     uint32_t perm_seen;   // epoch+1 whose permutation was observed published (0: none)
     float dens;           // unseen fraction observed by the last walk step (window sizing)
-    uint32_t hist[8];
     uint32_t npush;       // evictions pushed by this job this round
     // prefetch of the next walk window (R-O1 walk, see job_walk_prefetched)
     uint32_t pf_state;    // 0 none, 1 list window requested, 2 seen chunks requested
     uint32_t pf_buf, pf_epoch, pf_base, pf_len, pf_vlen;
-    uint32_t hs_mask;     // served-set hash size - 1
     uint32_t scan[33];
     unsigned long long red[(kThreads / 32) * 13];
 };
 
 __device__ __forceinline__ const uint32_t* list_ptr(const Lay& L, const Cfg& C, uint32_t j, uint32_t e, uint32_t buf) {
     return buf == 0 ? L.perms + ((size_t)j * C.maxT + e) * C.Nrow : L.laps + ((size_t)j * 2 + (buf - 1)) * C.Nrow;
-}
-
-// Set of ids served to the job in the current round (shared-memory open
-// addressing, load factor <= 1/2): the walk that follows corrects prefetched
-// seen words with it, since only this job's CTA ever sets seen_j bits.
-__device__ __forceinline__ uint32_t hash_slot(uint32_t id, uint32_t mask) { return (id * 2654435761u >> 7) & mask; }
-__device__ __forceinline__ void hash_insert(uint32_t* h, uint32_t mask, uint32_t id) {
-    for (uint32_t s = hash_slot(id, mask);; s = (s + 1) & mask) {
-        const uint32_t old = atomicCAS(h + s, 0u, id + 1);
-        if (old == 0 || old == id + 1) return;
-    }
-}
-__device__ __forceinline__ bool hash_has(const uint32_t* h, uint32_t mask, uint32_t id) {
-    for (uint32_t s = hash_slot(id, mask);; s = (s + 1) & mask) {
-        const uint32_t v = h[s];
-        if (v == id + 1) return true;
-        if (v == 0) return false;
-    }
 }
 
 // Stage 1 (right after a walk): the next walk window of the current list into
@@ -329,8 +308,10 @@ __device__ void prefetch_window(const Lay& L, const Cfg& C, JobSmem& S, uint32_t
     }
 }
 
-// Stage 2 (mid job phase, once the window has landed): the 16-B seen chunk of
-// every window id, asynchronously.
+// Stage 2 (once this round's hits and substitutes are marked seen): the 16-B
+// seen chunk of every window id, asynchronously.  Exactness: seen_j is written
+// only by this CTA, and the only bits set after this point in the round belong
+// to storage-served requested ids, which lie before the window in the list.
 __device__ void prefetch_seen(const Lay& L, const Cfg& C, JobSmem& S, const uint32_t* s_win, uint4* s_wseen, uint32_t j) {
     const uint32_t tid = threadIdx.x;
     cp_async_wait_all();
@@ -351,7 +332,6 @@ __device__ void prefetch_seen(const Lay& L, const Cfg& C, JobSmem& S, const uint
 // list of deferred misses of the lap (slot order = position order).
 struct WalkPrefetch {
     const uint4* wseen;      // [kWinMax] prefetched 16-B seen chunks
-    const uint32_t* hash;    // served-set hash
 };
 
 __device__ void job_walk(const Lay& L, const Cfg& C, JobSmem& S, uint32_t* s_req, uint32_t j, uint32_t e, uint32_t need,
@@ -371,8 +351,7 @@ __device__ void job_walk(const Lay& L, const Cfg& C, JobSmem& S, uint32_t* s_req
     uint32_t taken = 0;
     bool wrapped = false;
     if (pf && S.pf_state != 0) {
-        // first step from the prefetched window: seen = prefetched seen word OR served
-        // since the prefetch (the served set of the round just played)
+        // first step from the prefetched window and its prefetched seen chunks
         cp_async_wait_all();
         __syncthreads();
         const bool usable = S.pf_state == 2 && S.pf_buf == S.cur_buf && S.pf_epoch == e &&
@@ -392,7 +371,7 @@ __device__ void job_walk(const Lay& L, const Cfg& C, JobSmem& S, uint32_t* s_req
                     const uint32_t q = (id >> 5) & 3u;
                     const uint32_t w = q == 0 ? ch.x : (q == 1 ? ch.y : (q == 2 ? ch.z : ch.w));
                     ids[k] = id;
-                    if (!((w >> (id & 31)) & 1u) && !hash_has(pf->hash, S.hs_mask, id)) { flags |= 1u << k; ++cnt; }
+                    if (!((w >> (id & 31)) & 1u)) { flags |= 1u << k; ++cnt; }
                 }
             }
             uint32_t tot;
@@ -557,16 +536,14 @@ __device__ void job_recount(const Lay& L, const Cfg& C, uint32_t j, uint32_t* s_
 __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& S, uint32_t* s_req, uint32_t* s_miss,
                           uint32_t* s_sub, uint32_t* s_oid, uint8_t* s_osrc, uint32_t* s_pre, uint32_t j, uint64_t r,
                           uint32_t e, uint32_t nbase, uint32_t n_act, PhaseTimer& TM, const uint32_t* s_win,
-                          uint4* s_wseen, uint32_t* s_hash) {
+                          uint4* s_wseen) {
     const uint32_t tid = threadIdx.x, T = blockDim.x;
     const uint32_t need = S.need;
     uint32_t* seen_j = L.seen + (size_t)j * C.NW;
     uint32_t* cons_j = L.cons + (size_t)j * C.NW;
     const size_t row = (size_t)P.row_of_job[j] * P.out_stride;
     if (tid < 3) S.hits[tid] = 0;       // the pool totals S.tot persist across rounds in shared memory
-    if (tid < 8) S.hist[tid] = 0;
     if (tid == 0) S.npush = 0;
-    if (P.mode == 0) for (uint32_t k = tid; k <= S.hs_mask; k += T) s_hash[k] = 0;
     __syncthreads();
 
     // a3: hits (E, D, or A not consumed by j, R-O13) join seen_j now
@@ -611,7 +588,6 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
         S.k[2] = min(m - S.k[0] - S.k[1], pe);
     }
     __syncthreads();
-    if (P.mode == 0 && S.pf_state == 1) prefetch_seen(L, C, S, s_win, s_wseen, j);   // next walk, stage 2
     TM.tick(1);
 
     // a4/a5: misses in slot order take substitutes A -> D -> E at keyed ranks (R-O2)
@@ -646,6 +622,8 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
             count_add(L, C, j * 3 + tt, id, 0xffffffffu);
         }
     }
+    __syncthreads();
+    if (P.mode == 0 && S.pf_state == 1) prefetch_seen(L, C, S, s_win, s_wseen, j);   // next walk, stage 2
     TM.tick(2);
     // remaining misses are fetched from storage (R-O18)
     for (uint32_t u = q + tid; u < S.m; u += T) {
@@ -682,32 +660,22 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
         S.tot[2] -= k2;
     }
 
-    // a6: counters (per-warp ballot histogram of the 8 source codes), digest,
-    // transcript; an A entry whose consumer count reaches |active| is pushed
-    // for eviction at the round end (R-O5)
+    // a6: digest, transcript; an A entry whose consumer count reaches |active| is
+    // pushed for eviction at the round end (R-O5).  The per-tier counters follow
+    // from the phase counts: hits per tier, k_t substitutes, m - q storage.
     unsigned long long dig = 0;
     unsigned long long* trow = P.transcript ? P.transcript + ((size_t)j * C.maxT + e) * C.N : nullptr;
     const uint32_t lane = tid & 31;
-    for (uint32_t base = 0; base < need; base += T) {
-        const uint32_t s = base + tid;
-        uint32_t src = 0xffu;
-        if (s < need) {
-            const uint32_t i = s_oid[s];
-            src = s_osrc[s];
-            dig += splitmix64(((uint64_t)(nbase + s) << 35) | ((uint64_t)src << 32) | i);
-            if (trow) trow[nbase + s] = ((unsigned long long)src << 32) | i;
-            if (P.mode == 0) hash_insert(s_hash, S.hs_mask, i);
-            if ((src & 3u) == T_A) {
-                if (atomicAdd(L.cons_cnt + i, 1u) + 1u == n_act) {
-                    L.evict_push[atomicAdd(L.bar + 3, 1u) % (C.J * C.Bmax)] = i;
-                    atomicAdd(&S.npush, 1u);
-                }
+    for (uint32_t s = tid; s < need; s += T) {
+        const uint32_t i = s_oid[s];
+        const uint32_t src = s_osrc[s];
+        dig += splitmix64(((uint64_t)(nbase + s) << 35) | ((uint64_t)src << 32) | i);
+        if (trow) trow[nbase + s] = ((unsigned long long)src << 32) | i;
+        if ((src & 3u) == T_A) {
+            if (atomicAdd(L.cons_cnt + i, 1u) + 1u == n_act) {
+                L.evict_push[atomicAdd(L.bar + 3, 1u) % (C.J * C.Bmax)] = i;
+                atomicAdd(&S.npush, 1u);
             }
-        }
-#pragma unroll
-        for (uint32_t v = 0; v < 8; ++v) {
-            const uint32_t bal = __ballot_sync(0xffffffffu, src == v);
-            if (lane == 0 && bal) atomicAdd(&S.hist[v], (uint32_t)__popc(bal));
         }
     }
     dig = warp_sum(dig);
@@ -717,11 +685,23 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
     if (tid < 13) {           // fire-and-forget adds into this job-epoch's counters
         seneca_job_epoch_stats* st = L.stats + (size_t)j * C.maxT + e;
         unsigned long long* f = reinterpret_cast<unsigned long long*>(st);
-        unsigned long long v;
-        if (tid < 4) v = S.hist[tid] + S.hist[tid | SUBST];             // served[t]
-        else if (tid < 8) v = S.hist[(tid - 4) | SUBST];                // subst[t]
-        else if (tid < 12) v = tid == 8 ? 0ull : S.hist[tid - 8];       // req_hits[t]
-        else { v = 0; for (uint32_t w = 0; w < T / 32; ++w) v += S.red[w]; }   // digest
+        // hits/k indexed A=0, D=1, E=2; counter tiers S=0, E=1, D=2, A=3
+        const uint32_t hA = S.hits[0], hD = S.hits[1], hE = S.hits[2];
+        unsigned long long v = 0;
+        switch (tid) {
+            case 0: v = S.m - (k0 + k1 + k2); break;           // served[S]
+            case 1: v = hE + k2; break;                        // served[E]
+            case 2: v = hD + k1; break;                        // served[D]
+            case 3: v = hA + k0; break;                        // served[A]
+            case 5: v = k2; break;                             // subst[E]
+            case 6: v = k1; break;                             // subst[D]
+            case 7: v = k0; break;                             // subst[A]
+            case 9: v = hE; break;                             // req_hits[E]
+            case 10: v = hD; break;                            // req_hits[D]
+            case 11: v = hA; break;                            // req_hits[A]
+            case 12: for (uint32_t w = 0; w < T / 32; ++w) v += S.red[w]; break;   // digest
+            default: break;
+        }
         if (v) atomicAdd(f + tid, v);
     }
     __syncthreads();
@@ -865,13 +845,11 @@ ods_rounds(Lay L, Cfg C, Launch P) {
     uint32_t* s_pre = smem + 4 * C.Bmax;
     const uint32_t o_win = (4 * C.Bmax + 3 * C.NS + 3) & ~3u;       // 16-B aligned (cp.async)
     uint32_t* s_win = smem + o_win;
-    uint32_t* s_hash = s_win + kWinMax;
-    const uint32_t o_wseen = (o_win + kWinMax + C.HS + 3) & ~3u;
+    const uint32_t o_wseen = o_win + kWinMax;
     uint4* s_wseen = reinterpret_cast<uint4*>(smem + o_wseen);
     uint8_t* s_osrc = reinterpret_cast<uint8_t*>(smem + o_wseen + 4 * kWinMax);
     WalkPrefetch pfs;
     pfs.wseen = s_wseen;
-    pfs.hash = s_hash;
     const WalkPrefetch* pf = P.mode == 0 ? &pfs : nullptr;
     // with no augmented tier there is no cross-job interaction at all (E and D are
     // static, maintain has nothing to do): the job CTAs run their rounds independently
@@ -887,7 +865,6 @@ ods_rounds(Lay L, Cfg C, Launch P) {
         S.perm_seen = 0;
         S.dens = 1.0f;
         S.pf_state = 0;
-        S.hs_mask = C.HS - 1;
     }
     if (!is_maint && tid < 3) S.tot[tid] = ldcg(L.cnt_tot + j * 3 + tid);
     if (is_maint && tid == 0) M.prev_k = blockDim.x;
@@ -1017,7 +994,7 @@ ods_rounds(Lay L, Cfg C, Launch P) {
                 else if (coupled && rr > 0) { job_take_refills(L, C, S, j, r - 1); __syncthreads(); }
                 TM.tick(0);
                 job_round(L, C, P, S, s_req, s_miss, s_sub, s_oid, s_osrc, s_pre, j, r, s_e[j], s_n[j],
-                          __popc(active_after), TM, s_win, s_wseen, s_hash);
+                          __popc(active_after), TM, s_win, s_wseen);
                 // a8 (R-O16): the epoch ends with this batch -> reset seen_j and the walk
                 if (s_n[j] + S.need == C.N) {
                     uint4* sj = reinterpret_cast<uint4*>(L.seen + (size_t)j * C.NW);
@@ -1261,8 +1238,6 @@ Sizes compute_sizes(const seneca_cache_config* cfg) {
     C.seed = cfg->seed;
     C.Nrow = (C.N + 63) & ~63u;
     C.FL = (uint32_t)(std::max<size_t>(cfg->cap_a, 1) + (size_t)C.J * C.Bmax);
-    C.HS = 64;
-    while (C.HS < 2 * C.Bmax) C.HS <<= 1;
     const size_t W = (size_t)C.NW * 4, P = 3 * (size_t)C.J + 1;
     const size_t capl = std::max<size_t>(cfg->cap_a, 1) * 4;
     const size_t sz[] = {
@@ -1428,7 +1403,7 @@ extern "C" seneca_status seneca_init_cache(const seneca_cache_config* cfg, void*
     Sizes z = compute_sizes(cfg);
     if (ws_bytes < z.total) { set_error("workspace %zu bytes < required %zu", ws_bytes, z.total); return SENECA_ENOSPC; }
     const size_t o_win = ((size_t)4 * z.C.Bmax + 3 * z.C.NS + 3) & ~(size_t)3;
-    const size_t o_wseen = (o_win + kWinMax + z.C.HS + 3) & ~(size_t)3;
+    const size_t o_wseen = o_win + kWinMax;
     const size_t round_smem = (o_wseen + 4 * kWinMax) * 4 + z.C.Bmax;
     if (round_smem > 200 * 1024) { set_error("batch/dataset too large for the shared-memory indices"); return SENECA_EINVAL; }
     seneca_ctx* c = new (std::nothrow) seneca_ctx();
