@@ -50,9 +50,9 @@ constexpr uint32_t T_S = 0, T_E = 1, T_D = 2, T_A = 3, SUBST = 4;
 constexpr uint32_t kMaxJobs = 32;
 constexpr uint32_t kMaxBatch = 4096;
 constexpr uint32_t kThreads = 512;           // CTA size of the persistent kernel
-constexpr uint32_t kBlockShift = 8;          // 256 ids (8 words) per count block
-constexpr uint32_t kSuperShift = 13;         // 32 blocks = 8192 ids per superblock
-constexpr uint32_t kWordsPerBlock = 8;
+constexpr uint32_t kBlockShift = 7;          // 128 ids (4 words, one 16-B vector) per count block
+constexpr uint32_t kSuperShift = 12;         // 32 blocks = 4096 ids per superblock
+constexpr uint32_t kWordsPerBlock = 4;
 constexpr uint32_t kWalkPerThread = 8;       // list entries examined per thread per walk step
 constexpr uint32_t kWinMax = 1024;           // prefetched walk window (list entries)
 
@@ -81,8 +81,8 @@ struct Lay {
     uint32_t *bm_e, *bm_d, *bm_a;    // [NW]
     uint32_t *seen, *cons;           // [J][NW]
     uint32_t *cons_cnt;              // [N] active consumers of each A entry (R-O5)
-    uint32_t *cnt_blk;               // [3J+1][NBp]
-    uint32_t *cnt_sup;               // [3J+1][NS]
+    uint32_t *cnt8;                  // [3J+1][NBp] u8 block counts, 4 per word (one 32-B row per superblock)
+    uint32_t *cnt_sup;               // [3J+1][NS] superblock counts (kept in shared memory while running)
     uint32_t *cnt_tot;               // [3J+1]
     uint32_t *a_size;                // [1]
     uint32_t *perms;                 // [J][maxT][N]
@@ -143,38 +143,35 @@ __device__ __forceinline__ uint32_t pool_of(uint32_t j, uint32_t t) {   // t: T_
     return j * 3u + (t == T_A ? 0u : (t == T_D ? 1u : 2u));
 }
 
-__device__ __forceinline__ void count_add(const Lay& L, const Cfg& C, uint32_t pidx, uint32_t id, uint32_t delta) {
-    atomicAdd(L.cnt_blk + (size_t)pidx * C.NBp + (id >> kBlockShift), delta);
-    atomicAdd(L.cnt_sup + (size_t)pidx * C.NS + (id >> kSuperShift), delta);
+// Pool counts: a u8 count per 128-id block in global memory (L2-resident; the
+// byte is updated with a 32-bit add of +-1 shifted into place -- a count never
+// leaves [0, 128], so no carry/borrow crosses bytes), and a u32 count per
+// 4096-id superblock in the shared memory of the CTA that owns the pool.
+__device__ __forceinline__ void count_add(const Lay& L, const Cfg& C, uint32_t pidx, uint32_t id, uint32_t delta,
+                                          uint32_t* s_sup_pool) {
+    const uint32_t blk = id >> kBlockShift;
+    atomicAdd(L.cnt8 + (size_t)pidx * (C.NBp >> 2) + (blk >> 2), delta << (8u * (blk & 3u)));
+    atomicAdd(s_sup_pool + (id >> kSuperShift), delta);
 }
 
-// Exclusive prefix of the superblock counts of pool pidx, into shared memory
-// (each thread a contiguous run; the run is re-read from L2 instead of being
-// kept in a dynamically indexed local array).
-__device__ void load_sup_prefix(const Lay& L, const Cfg& C, uint32_t pidx, uint32_t* s_pre, uint32_t* scratch) {
+// Exclusive prefix of the superblock counts (shared memory -> shared memory).
+__device__ void prefix_from_smem(const Cfg& C, const uint32_t* s_sup_pool, uint32_t* s_pre_pool, uint32_t* scratch) {
     const uint32_t per = (C.NS + blockDim.x - 1) / blockDim.x;
     const uint32_t lo = threadIdx.x * per;
     const uint32_t hi = min(lo + per, C.NS);
-    const uint32_t* src = L.cnt_sup + (size_t)pidx * C.NS;
     uint32_t sum = 0;
-    for (uint32_t k = lo; k < hi; ++k) {
-        const uint32_t v = ldcg(src + k);
-        s_pre[k] = v;                               // counts first, prefix below
-        sum += v;
-    }
+    for (uint32_t k = lo; k < hi; ++k) sum += s_sup_pool[k];
     uint32_t run = block_exclusive_scan(sum, nullptr, scratch);
     for (uint32_t k = lo; k < hi; ++k) {
-        const uint32_t v = s_pre[k];
-        s_pre[k] = run;
-        run += v;
+        s_pre_pool[k] = run;
+        run += s_sup_pool[k];
     }
     __syncthreads();
 }
 
 // The rank-th (0-based) member, in ascending id order, of pool (t, j):
-// superblock by binary search in shared memory, then two batches of
-// independent loads (the 32 block counts of the superblock; the 8 words of
-// each bitmap of the block).
+// superblock by binary search in shared memory, then the superblock's 32-B
+// row of block counts (two 16-B loads), then one 16-B vector of each bitmap.
 __device__ uint32_t pool_select(const Lay& L, const Cfg& C, uint32_t pidx, uint32_t t, uint32_t j,
                                 const uint32_t* s_pre, uint32_t rank) {
     uint32_t lo = 0, hi = C.NS - 1;
@@ -183,60 +180,45 @@ __device__ uint32_t pool_select(const Lay& L, const Cfg& C, uint32_t pidx, uint3
         if (s_pre[mid] <= rank) lo = mid; else hi = mid - 1;
     }
     uint32_t r = rank - s_pre[lo];
-    const uint32_t* crow = L.cnt_blk + (size_t)pidx * C.NBp + (size_t)lo * 32u;
-    uint4 cv[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) cv[q] = ldcg4(crow + 4 * q);
-    uint32_t blk = lo * 32u, k_found = 0;
+    const uint32_t* crow = L.cnt8 + (size_t)pidx * (C.NBp >> 2) + (size_t)lo * 8u;
+    const uint4 c0 = ldcg4(crow), c1 = ldcg4(crow + 4);
+    const uint32_t cw[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+    uint32_t k_found = 0;
     bool found = false;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-        const uint32_t c4[4] = {cv[q].x, cv[q].y, cv[q].z, cv[q].w};
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
+            const uint32_t c = (cw[q] >> (8 * k)) & 0xffu;
             if (!found) {
-                if (r < c4[k]) { found = true; k_found = q * 4 + k; }
-                else r -= c4[k];
+                if (r < c) { found = true; k_found = q * 4 + k; }
+                else r -= c;
             }
         }
     }
-    blk += k_found;
-    const uint32_t w0 = blk * kWordsPerBlock;
-    uint32_t pw[8];
-    {
-        const uint4 a0 = ldcg4(L.bm_a + w0), a1 = ldcg4(L.bm_a + w0 + 4);
-        if (t == T_S) {
-            const uint4 e0 = ldcg4(L.bm_e + w0), e1 = ldcg4(L.bm_e + w0 + 4);
-            const uint4 d0 = ldcg4(L.bm_d + w0), d1 = ldcg4(L.bm_d + w0 + 4);
-            pw[0] = ~(a0.x | e0.x | d0.x); pw[1] = ~(a0.y | e0.y | d0.y);
-            pw[2] = ~(a0.z | e0.z | d0.z); pw[3] = ~(a0.w | e0.w | d0.w);
-            pw[4] = ~(a1.x | e1.x | d1.x); pw[5] = ~(a1.y | e1.y | d1.y);
-            pw[6] = ~(a1.z | e1.z | d1.z); pw[7] = ~(a1.w | e1.w | d1.w);
-#pragma unroll
-            for (int k = 0; k < 8; ++k) pw[k] &= valid_mask(C, w0 + k);
-        } else {
-            const uint32_t* sj = L.seen + (size_t)j * C.NW + w0;
-            const uint4 s0 = ldcg4(sj), s1 = ldcg4(sj + 4);
-            uint4 b0, b1;
-            if (t == T_A) { b0 = a0; b1 = a1; }
-            else if (t == T_D) { b0 = ldcg4(L.bm_d + w0); b1 = ldcg4(L.bm_d + w0 + 4); }
-            else { b0 = ldcg4(L.bm_e + w0); b1 = ldcg4(L.bm_e + w0 + 4); }
-            pw[0] = b0.x & ~s0.x; pw[1] = b0.y & ~s0.y; pw[2] = b0.z & ~s0.z; pw[3] = b0.w & ~s0.w;
-            pw[4] = b1.x & ~s1.x; pw[5] = b1.y & ~s1.y; pw[6] = b1.z & ~s1.z; pw[7] = b1.w & ~s1.w;
-            if (t == T_A) {
-                const uint32_t* cj = L.cons + (size_t)j * C.NW + w0;
-                const uint4 c0 = ldcg4(cj), c1 = ldcg4(cj + 4);
-                pw[0] &= ~c0.x; pw[1] &= ~c0.y; pw[2] &= ~c0.z; pw[3] &= ~c0.w;
-                pw[4] &= ~c1.x; pw[5] &= ~c1.y; pw[6] &= ~c1.z; pw[7] &= ~c1.w;
-            }
+    const uint32_t w0 = (lo * 32u + k_found) * kWordsPerBlock;
+    uint32_t pw[4];
+    if (t == T_S) {
+        const uint4 a = ldcg4(L.bm_a + w0), e = ldcg4(L.bm_e + w0), d = ldcg4(L.bm_d + w0);
+        pw[0] = ~(a.x | e.x | d.x) & valid_mask(C, w0 + 0);
+        pw[1] = ~(a.y | e.y | d.y) & valid_mask(C, w0 + 1);
+        pw[2] = ~(a.z | e.z | d.z) & valid_mask(C, w0 + 2);
+        pw[3] = ~(a.w | e.w | d.w) & valid_mask(C, w0 + 3);
+    } else {
+        const uint4 sv = ldcg4(L.seen + (size_t)j * C.NW + w0);
+        const uint4 b = ldcg4((t == T_A ? L.bm_a : (t == T_D ? L.bm_d : L.bm_e)) + w0);
+        pw[0] = b.x & ~sv.x; pw[1] = b.y & ~sv.y; pw[2] = b.z & ~sv.z; pw[3] = b.w & ~sv.w;
+        if (t == T_A) {
+            const uint4 cv = ldcg4(L.cons + (size_t)j * C.NW + w0);
+            pw[0] &= ~cv.x; pw[1] &= ~cv.y; pw[2] &= ~cv.z; pw[3] &= ~cv.w;
         }
     }
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < 4; ++k) {
         const uint32_t pc = __popc(pw[k]);
         if (r < pc) {
             uint32_t x = pw[k];
-            for (uint32_t s = 0; s < r; ++s) x &= x - 1u;
+            for (uint32_t s2 = 0; s2 < r; ++s2) x &= x - 1u;
             return (w0 + k) * 32u + (uint32_t)(__ffs(x) - 1);
         }
         r -= pc;
@@ -483,40 +465,35 @@ __device__ void job_walk(const Lay& L, const Cfg& C, JobSmem& S, uint32_t* s_req
     }
 }
 
-// Rebuild the three pool counts of job j (epoch start: seen_j is empty).
+// Rebuild the three pool counts of job j (epoch start): block bytes in global
+// memory, superblock counts in this CTA's shared memory, totals in tot3.
 __device__ void job_recount(const Lay& L, const Cfg& C, uint32_t j, uint32_t* s_sup /* [3][NS] */, uint32_t* tot3) {
     const uint32_t tid = threadIdx.x, T = blockDim.x;
     for (uint32_t k = tid; k < 3 * C.NS; k += T) s_sup[k] = 0;
     __syncthreads();
     const uint32_t* cj = L.cons + (size_t)j * C.NW;
     const uint32_t* sj = L.seen + (size_t)j * C.NW;
-    for (uint32_t b = tid; b < C.NBp; b += T) {
-        const uint32_t w0 = b * kWordsPerBlock;
-        uint32_t ca = 0, cd = 0, ce = 0;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const uint4 a = ldcg4(L.bm_a + w0 + 4 * h), d = ldcg4(L.bm_d + w0 + 4 * h), e = ldcg4(L.bm_e + w0 + 4 * h);
-            const uint4 c = ldcg4(cj + w0 + 4 * h), s = ldcg4(sj + w0 + 4 * h);
-            ca += __popc(a.x & ~c.x & ~s.x) + __popc(a.y & ~c.y & ~s.y) + __popc(a.z & ~c.z & ~s.z) + __popc(a.w & ~c.w & ~s.w);
-            cd += __popc(d.x & ~s.x) + __popc(d.y & ~s.y) + __popc(d.z & ~s.z) + __popc(d.w & ~s.w);
-            ce += __popc(e.x & ~s.x) + __popc(e.y & ~s.y) + __popc(e.z & ~s.z) + __popc(e.w & ~s.w);
-        }
-        L.cnt_blk[(size_t)(j * 3 + 0) * C.NBp + b] = ca;
-        L.cnt_blk[(size_t)(j * 3 + 1) * C.NBp + b] = cd;
-        L.cnt_blk[(size_t)(j * 3 + 2) * C.NBp + b] = ce;
-        const uint32_t s = b >> 5;
-        if (ca) atomicAdd(s_sup + s, ca);
-        if (cd) atomicAdd(s_sup + C.NS + s, cd);
-        if (ce) atomicAdd(s_sup + 2 * C.NS + s, ce);
-    }
-    __syncthreads();
     uint32_t ta = 0, td = 0, te = 0;
-    for (uint32_t s = tid; s < C.NS; s += T) {
-        const uint32_t a = s_sup[s], d = s_sup[C.NS + s], e = s_sup[2 * C.NS + s];
-        L.cnt_sup[(size_t)(j * 3 + 0) * C.NS + s] = a;
-        L.cnt_sup[(size_t)(j * 3 + 1) * C.NS + s] = d;
-        L.cnt_sup[(size_t)(j * 3 + 2) * C.NS + s] = e;
-        ta += a; td += d; te += e;
+    for (uint32_t g = tid; g < (C.NBp >> 2); g += T) {          // 4 blocks = 16 words per step
+        uint32_t pa = 0, pd = 0, pe = 0;
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            const uint32_t w0 = (g * 4 + h) * kWordsPerBlock;
+            const uint4 a = ldcg4(L.bm_a + w0), d = ldcg4(L.bm_d + w0), e = ldcg4(L.bm_e + w0);
+            const uint4 c = ldcg4(cj + w0), s = ldcg4(sj + w0);
+            const uint32_t ca = __popc(a.x & ~c.x & ~s.x) + __popc(a.y & ~c.y & ~s.y) + __popc(a.z & ~c.z & ~s.z) + __popc(a.w & ~c.w & ~s.w);
+            const uint32_t cd = __popc(d.x & ~s.x) + __popc(d.y & ~s.y) + __popc(d.z & ~s.z) + __popc(d.w & ~s.w);
+            const uint32_t ce = __popc(e.x & ~s.x) + __popc(e.y & ~s.y) + __popc(e.z & ~s.z) + __popc(e.w & ~s.w);
+            pa |= ca << (8 * h); pd |= cd << (8 * h); pe |= ce << (8 * h);
+            ta += ca; td += cd; te += ce;
+            const uint32_t sb = (g * 4 + h) >> 5;
+            if (ca) atomicAdd(s_sup + sb, ca);
+            if (cd) atomicAdd(s_sup + C.NS + sb, cd);
+            if (ce) atomicAdd(s_sup + 2 * C.NS + sb, ce);
+        }
+        L.cnt8[(size_t)(j * 3 + 0) * (C.NBp >> 2) + g] = pa;
+        L.cnt8[(size_t)(j * 3 + 1) * (C.NBp >> 2) + g] = pd;
+        L.cnt8[(size_t)(j * 3 + 2) * (C.NBp >> 2) + g] = pe;
     }
     ta = warp_sum(ta); td = warp_sum(td); te = warp_sum(te);
     __shared__ uint32_t s_t[3];
@@ -524,11 +501,7 @@ __device__ void job_recount(const Lay& L, const Cfg& C, uint32_t j, uint32_t* s_
     __syncthreads();
     if ((tid & 31) == 0) { atomicAdd(&s_t[0], ta); atomicAdd(&s_t[1], td); atomicAdd(&s_t[2], te); }
     __syncthreads();
-    if (tid == 0) {
-        L.cnt_tot[j * 3 + 0] = tot3[0] = s_t[0];
-        L.cnt_tot[j * 3 + 1] = tot3[1] = s_t[1];
-        L.cnt_tot[j * 3 + 2] = tot3[2] = s_t[2];
-    }
+    if (tid == 0) { tot3[0] = s_t[0]; tot3[1] = s_t[1]; tot3[2] = s_t[2]; }
     __syncthreads();
 }
 
@@ -536,7 +509,7 @@ __device__ void job_recount(const Lay& L, const Cfg& C, uint32_t j, uint32_t* s_
 __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& S, uint32_t* s_req, uint32_t* s_miss,
                           uint32_t* s_sub, uint32_t* s_oid, uint8_t* s_osrc, uint32_t* s_pre, uint32_t j, uint64_t r,
                           uint32_t e, uint32_t nbase, uint32_t n_act, PhaseTimer& TM, const uint32_t* s_win,
-                          uint4* s_wseen) {
+                          uint4* s_wseen, uint32_t* s_sup) {
     const uint32_t tid = threadIdx.x, T = blockDim.x;
     const uint32_t need = S.need;
     uint32_t* seen_j = L.seen + (size_t)j * C.NW;
@@ -567,7 +540,7 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
                 s_osrc[s] = (uint8_t)t;
                 atomicOr(seen_j + w, b);
                 if (t == T_A) atomicOr(cons_j + w, b);
-                count_add(L, C, pool_of(j, t), i, 0xffffffffu);
+                count_add(L, C, pool_of(j, t), i, 0xffffffffu, s_sup + (pool_of(j, t) - j * 3) * C.NS);
                 atomicAdd(&S.hits[t == T_A ? 0 : (t == T_D ? 1 : 2)], 1u);
             } else {
                 is_miss = true;
@@ -595,7 +568,7 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
     const uint32_t q = k0 + k1 + k2;
     if (q > 0) {
         for (uint32_t tt = 0; tt < 3; ++tt)
-            if (S.k[tt]) load_sup_prefix(L, C, j * 3 + tt, s_pre + tt * C.NS, S.scan);
+            if (S.k[tt]) prefix_from_smem(C, s_sup + tt * C.NS, s_pre + tt * C.NS, S.scan);
         TM.tick(8);
         for (uint32_t u = tid; u < q; u += T) {
             const uint32_t tt = u < k0 ? 0u : (u < k0 + k1 ? 1u : 2u);
@@ -619,7 +592,7 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
             const uint32_t w = id >> 5, b = 1u << (id & 31);
             atomicOr(seen_j + w, b);
             if (tt == 0) atomicOr(cons_j + w, b);
-            count_add(L, C, j * 3 + tt, id, 0xffffffffu);
+            count_add(L, C, j * 3 + tt, id, 0xffffffffu, s_sup + tt * C.NS);
         }
     }
     __syncthreads();
@@ -732,8 +705,8 @@ __device__ void maint_refill_select(const Lay& L, const Cfg& C, MaintSmem& M, co
 // eviction of A entries consumed by every active job (R-O5, R-O6), refill from
 // the storage pool as of round start (R-O8), counts kept exact.
 __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSmem& M, uint32_t* s_pre,
-                            uint64_t r, uint32_t active, bool full_scan, bool speculated, uint32_t ne_push,
-                            uint32_t push_base, PhaseTimer& TM) {
+                            uint32_t* s_supS, uint64_t r, uint32_t active, bool full_scan, bool speculated,
+                            uint32_t ne_push, uint32_t push_base, PhaseTimer& TM) {
     const uint32_t tid = threadIdx.x, T = blockDim.x;
     if (tid == 0) M.ne = full_scan ? 0u : ne_push;
     __syncthreads();
@@ -764,7 +737,7 @@ __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSm
     const uint32_t ne = M.ne;
     const uint32_t k = min(M.deficit0 + ne, M.PS);
     if (!speculated) {
-        if (k) load_sup_prefix(L, C, 3 * C.J, s_pre, M.scan);
+        if (k) prefix_from_smem(C, s_supS, s_pre, M.scan);
         maint_refill_select(L, C, M, s_pre, r, 0, k);
     } else if (k > M.kspec) {
         maint_refill_select(L, C, M, s_pre, r, M.kspec, k);      // beyond the speculated ranks
@@ -777,7 +750,7 @@ __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSm
         atomicAnd(L.bm_a + w, ~b);
         for (uint32_t a = 0; a < C.J; ++a) atomicAnd(L.cons + (size_t)a * C.NW + w, ~b);
         L.cons_cnt[i] = 0;
-        count_add(L, C, spidx, i, 1u);
+        count_add(L, C, spidx, i, 1u, s_supS);
     }
     // refills enter A with no consumers; each job CTA adds them to its own A pool
     // before its next classification (R-O8)
@@ -785,13 +758,13 @@ __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSm
     for (uint32_t u = tid; u < k; u += T) {
         const uint32_t i = ldcg(fill + u);
         atomicOr(L.bm_a + (i >> 5), 1u << (i & 31));
-        count_add(L, C, spidx, i, 0xffffffffu);
+        count_add(L, C, spidx, i, 0xffffffffu, s_supS);
     }
     __syncthreads();
     if (tid == 0) {
         L.fill_n[r & 1] = k;
-        L.cnt_tot[spidx] = M.PS + ne - k;
-        *L.a_size = M.sizeA - ne + k;
+        M.PS = M.PS + ne - k;          // storage pool and |A| live in shared memory while running
+        M.sizeA = M.sizeA - ne + k;
         *L.evicted += ne;
         *L.refilled += k;
         M.prev_k = k;
@@ -802,7 +775,7 @@ __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSm
 
 // Job j's A pool gains the refills of round r it has not seen (its CTA alone
 // owns its pool counts; recount at an epoch start covers them instead).
-__device__ void job_take_refills(const Lay& L, const Cfg& C, JobSmem& S, uint32_t j, uint64_t r) {
+__device__ void job_take_refills(const Lay& L, const Cfg& C, JobSmem& S, uint32_t j, uint64_t r, uint32_t* s_sup) {
     const uint32_t kf = ldcg(L.fill_n + (r & 1));
     const uint32_t* fill = L.fill_list + (size_t)(r & 1) * C.FL;
     const uint32_t* seen_j = L.seen + (size_t)j * C.NW;
@@ -810,7 +783,7 @@ __device__ void job_take_refills(const Lay& L, const Cfg& C, JobSmem& S, uint32_
     for (uint32_t u = threadIdx.x; u < kf; u += blockDim.x) {
         const uint32_t i = ldcg(fill + u);
         if (!((ldcg(seen_j + (i >> 5)) >> (i & 31)) & 1u)) {
-            count_add(L, C, j * 3 + 0, i, 1u);
+            count_add(L, C, j * 3 + 0, i, 1u, s_sup);
             ++add;
         }
     }
@@ -842,8 +815,9 @@ ods_rounds(Lay L, Cfg C, Launch P) {
     uint32_t* s_miss = smem + C.Bmax;
     uint32_t* s_sub = smem + 2 * C.Bmax;
     uint32_t* s_oid = smem + 3 * C.Bmax;
-    uint32_t* s_pre = smem + 4 * C.Bmax;
-    const uint32_t o_win = (4 * C.Bmax + 3 * C.NS + 3) & ~3u;       // 16-B aligned (cp.async)
+    uint32_t* s_sup = smem + 4 * C.Bmax;                            // [3][NS] superblock counts (maint: S pool)
+    uint32_t* s_pre = s_sup + 3 * C.NS;                             // [3][NS] prefixes
+    const uint32_t o_win = (4 * C.Bmax + 6 * C.NS + 3) & ~3u;       // 16-B aligned (cp.async)
     uint32_t* s_win = smem + o_win;
     const uint32_t o_wseen = o_win + kWinMax;
     uint4* s_wseen = reinterpret_cast<uint4*>(smem + o_wseen);
@@ -866,8 +840,17 @@ ods_rounds(Lay L, Cfg C, Launch P) {
         S.dens = 1.0f;
         S.pf_state = 0;
     }
-    if (!is_maint && tid < 3) S.tot[tid] = ldcg(L.cnt_tot + j * 3 + tid);
-    if (is_maint && tid == 0) M.prev_k = blockDim.x;
+    if (!is_maint) {
+        if (tid < 3) S.tot[tid] = ldcg(L.cnt_tot + j * 3 + tid);
+        for (uint32_t k = tid; k < 3 * C.NS; k += blockDim.x) s_sup[k] = ldcg(L.cnt_sup + (size_t)j * 3 * C.NS + k);
+    } else {
+        if (tid == 0) {
+            M.prev_k = blockDim.x;
+            M.PS = ldcg(L.cnt_tot + 3 * C.J);
+            M.sizeA = ldcg(L.a_size);
+        }
+        for (uint32_t k = tid; k < C.NS; k += blockDim.x) s_sup[k] = ldcg(L.cnt_sup + (size_t)3 * C.J * C.NS + k);
+    }
     __syncthreads();
 
     auto need_of = [&](uint32_t jj) -> uint32_t { return min(C.batch[jj], C.N - s_n[jj]); };
@@ -908,8 +891,6 @@ ods_rounds(Lay L, Cfg C, Launch P) {
             const uint32_t active_after = s_active & ~departing;
             if (!(active_after && C.cap_a > 0) || departing) return false;
             if (tid == 0) {
-                M.PS = ldcg(L.cnt_tot + 3 * C.J);
-                M.sizeA = ldcg(L.a_size);
                 M.deficit0 = C.cap_a - M.sizeA;
                 uint32_t cand = 0;
                 for (uint32_t m = part; m; m &= m - 1) cand += need_of(__ffs(m) - 1);
@@ -917,7 +898,7 @@ ods_rounds(Lay L, Cfg C, Launch P) {
                 M.kspec = min(M.kmax, min(blockDim.x, M.deficit0 + M.prev_k + 64u));
             }
             __syncthreads();
-            if (M.kspec) load_sup_prefix(L, C, 3 * C.J, s_pre, M.scan);
+            if (M.kspec) prefix_from_smem(C, s_sup, s_pre, M.scan);
             TM.tick(0);
             maint_refill_select(L, C, M, s_pre, r, 0, M.kspec);
             TM.tick(1);
@@ -945,13 +926,9 @@ ods_rounds(Lay L, Cfg C, Launch P) {
             __syncthreads();
             TM.tick(2);
             if (active_after && C.cap_a > 0) {
-                if (!spec && tid == 0) {
-                    M.PS = ldcg(L.cnt_tot + 3 * C.J);
-                    M.sizeA = ldcg(L.a_size);
-                    M.deficit0 = C.cap_a - M.sizeA;
-                }
+                if (!spec && tid == 0) M.deficit0 = C.cap_a - M.sizeA;
                 __syncthreads();
-                maint_apply(L, C, P, M, s_pre, r, active_after, departing != 0, spec, M.ne_push, M.push_base, TM);
+                maint_apply(L, C, P, M, s_pre, s_sup, r, active_after, departing != 0, spec, M.ne_push, M.push_base, TM);
             }
             __syncthreads();
             if (tid == 0) { __threadfence(); atomicExch(L.bar + 2, rr + 1); }     // release round r's tiers
@@ -990,11 +967,11 @@ ods_rounds(Lay L, Cfg C, Launch P) {
             }
             TM.tick(4);
             if ((part >> j) & 1u) {
-                if (S.recount) { job_recount(L, C, j, s_pre, S.tot); if (tid == 0) S.recount = 0; __syncthreads(); }
-                else if (coupled && rr > 0) { job_take_refills(L, C, S, j, r - 1); __syncthreads(); }
+                if (S.recount) { job_recount(L, C, j, s_sup, S.tot); if (tid == 0) S.recount = 0; __syncthreads(); }
+                else if (coupled && rr > 0) { job_take_refills(L, C, S, j, r - 1, s_sup); __syncthreads(); }
                 TM.tick(0);
                 job_round(L, C, P, S, s_req, s_miss, s_sub, s_oid, s_osrc, s_pre, j, r, s_e[j], s_n[j],
-                          __popc(active_after), TM, s_win, s_wseen);
+                          __popc(active_after), TM, s_win, s_wseen, s_sup);
                 // a8 (R-O16): the epoch ends with this batch -> reset seen_j and the walk
                 if (s_n[j] + S.need == C.N) {
                     uint4* sj = reinterpret_cast<uint4*>(L.seen + (size_t)j * C.NW);
@@ -1027,10 +1004,14 @@ ods_rounds(Lay L, Cfg C, Launch P) {
         if (coupled && P.rounds > 0 && (s_active >> j & 1u)) {
             if (tid == 0) { while (ld_acquire(L.bar + 2) < P.rounds) { } }
             __syncthreads();
-            if (!S.recount) job_take_refills(L, C, S, j, P.r0 + P.rounds - 1);
+            if (!S.recount) job_take_refills(L, C, S, j, P.r0 + P.rounds - 1, s_sup);
             __syncthreads();
         }
         if (tid < 3) L.cnt_tot[j * 3 + tid] = S.tot[tid];
+        for (uint32_t k = tid; k < 3 * C.NS; k += blockDim.x) L.cnt_sup[(size_t)j * 3 * C.NS + k] = s_sup[k];
+    } else {
+        if (tid == 0) { L.cnt_tot[3 * C.J] = M.PS; *L.a_size = M.sizeA; }
+        for (uint32_t k = tid; k < C.NS; k += blockDim.x) L.cnt_sup[(size_t)3 * C.J * C.NS + k] = s_sup[k];
     }
     cp_async_wait_all();
     // persist the walk state
@@ -1089,12 +1070,12 @@ __global__ void ods_init_tiers(Lay L, Cfg C, uint32_t cap_e, uint32_t cap_d) {
     if (blockIdx.x == 0 && threadIdx.x == 0) *L.a_size = C.cap_a;
 }
 
-// Pool counts of every job and of the storage pool (init): one CTA per
-// superblock (256 threads, one word each; 8 threads per 256-id block).
-__global__ void __launch_bounds__(256)
+// Pool counts of every job and of the storage pool (init): one CTA of 128
+// threads per superblock (one word each; 4 threads per 128-id block).
+__global__ void __launch_bounds__(128)
 ods_recount_all(Lay L, Cfg C) {
     const uint32_t sblk = blockIdx.x, pool = blockIdx.y;    // pool < 3J: (j, tier); == 3J: storage
-    const uint32_t w = sblk * 256 + threadIdx.x;
+    const uint32_t w = sblk * 128 + threadIdx.x;
     uint32_t word;
     const uint32_t a = L.bm_a[w], d = L.bm_d[w], e = L.bm_e[w];
     if (pool == 3 * C.J) {
@@ -1104,18 +1085,22 @@ ods_recount_all(Lay L, Cfg C) {
         const uint32_t s = L.seen[(size_t)j * C.NW + w];
         word = tt == 0 ? (a & ~s & ~L.cons[(size_t)j * C.NW + w]) : (tt == 1 ? (d & ~s) : (e & ~s));
     }
-    uint32_t c = __popc(word);
+    uint32_t c = __popc(word);                                 // block count over 4 lanes
     c += __shfl_xor_sync(0xffffffffu, c, 1);
     c += __shfl_xor_sync(0xffffffffu, c, 2);
-    c += __shfl_xor_sync(0xffffffffu, c, 4);
-    if ((threadIdx.x & 7) == 0) L.cnt_blk[(size_t)pool * C.NBp + (w >> 3)] = c;
-    __shared__ uint32_t s_w[8];
+    // pack 4 consecutive block counts (lanes 0,4,8,12 of each 16-lane group) into a word
+    const uint32_t b0 = __shfl_sync(0xffffffffu, c, (threadIdx.x & 16) + 0);
+    const uint32_t b1 = __shfl_sync(0xffffffffu, c, (threadIdx.x & 16) + 4);
+    const uint32_t b2 = __shfl_sync(0xffffffffu, c, (threadIdx.x & 16) + 8);
+    const uint32_t b3 = __shfl_sync(0xffffffffu, c, (threadIdx.x & 16) + 12);
+    if ((threadIdx.x & 15) == 0)
+        L.cnt8[(size_t)pool * (C.NBp >> 2) + (w >> 4)] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
+    __shared__ uint32_t s_w[4];
     const uint32_t ws = warp_sum(__popc(word));
     if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = ws;
     __syncthreads();
     if (threadIdx.x == 0) {
-        uint32_t t = 0;
-        for (int k = 0; k < 8; ++k) t += s_w[k];
+        const uint32_t t = s_w[0] + s_w[1] + s_w[2] + s_w[3];
         L.cnt_sup[(size_t)pool * C.NS + sblk] = t;
         if (t) atomicAdd(L.cnt_tot + pool, t);
     }
@@ -1219,7 +1204,7 @@ Sizes compute_sizes(const seneca_cache_config* cfg) {
     Sizes z{};
     Cfg& C = z.C;
     C.N = (uint32_t)cfg->n_total;
-    C.NB = (C.N + 255) / 256;
+    C.NB = (C.N + 127) / 128;
     C.NS = (C.NB + 31) / 32;
     C.NBp = C.NS * 32;
     C.NW = C.NBp * kWordsPerBlock;          // bitmaps padded to whole superblocks
@@ -1244,7 +1229,7 @@ Sizes compute_sizes(const seneca_cache_config* cfg) {
         W, W, W,                                            // 0-2 bm_e, bm_d, bm_a
         W * C.J, W * C.J,                                   // 3-4 seen, cons
         (size_t)C.Nrow * 4,                                 // 5 cons_cnt
-        P * C.NBp * 4, P * C.NS * 4, P * 4,                 // 6-8 counts
+        P * C.NBp, P * C.NS * 4, P * 4,                     // 6-8 counts
         4,                                                  // 9 a_size
         (size_t)C.J * C.maxT * C.Nrow * 4,                  // 10 perms
         (size_t)C.J * 2 * C.Nrow * 4,                       // 11 laps
@@ -1273,7 +1258,7 @@ Lay carve(const Sizes& z, char* base) {
     L.seen = (uint32_t*)(base + z.off[3]);
     L.cons = (uint32_t*)(base + z.off[4]);
     L.cons_cnt = (uint32_t*)(base + z.off[5]);
-    L.cnt_blk = (uint32_t*)(base + z.off[6]);
+    L.cnt8 = (uint32_t*)(base + z.off[6]);
     L.cnt_sup = (uint32_t*)(base + z.off[7]);
     L.cnt_tot = (uint32_t*)(base + z.off[8]);
     L.a_size = (uint32_t*)(base + z.off[9]);
@@ -1402,7 +1387,7 @@ extern "C" seneca_status seneca_init_cache(const seneca_cache_config* cfg, void*
     if ((uintptr_t)d_workspace & 255) { set_error("workspace must be 256-byte aligned"); return SENECA_EINVAL; }
     Sizes z = compute_sizes(cfg);
     if (ws_bytes < z.total) { set_error("workspace %zu bytes < required %zu", ws_bytes, z.total); return SENECA_ENOSPC; }
-    const size_t o_win = ((size_t)4 * z.C.Bmax + 3 * z.C.NS + 3) & ~(size_t)3;
+    const size_t o_win = ((size_t)4 * z.C.Bmax + 6 * z.C.NS + 3) & ~(size_t)3;
     const size_t o_wseen = o_win + kWinMax;
     const size_t round_smem = (o_wseen + 4 * kWinMax) * 4 + z.C.Bmax;
     if (round_smem > 200 * 1024) { set_error("batch/dataset too large for the shared-memory indices"); return SENECA_EINVAL; }
@@ -1432,7 +1417,7 @@ extern "C" seneca_status seneca_init_cache(const seneca_cache_config* cfg, void*
             ods_init_tiers<<<blocks, 256, 0, st>>>(c->L, c->C, (uint32_t)cfg->cap_e, (uint32_t)cfg->cap_d);
         });
         INIT_TRY(cudaGetLastError());
-        timed(c, K_RECOUNT, st, [&] { ods_recount_all<<<dim3(c->C.NS, 3 * c->C.J + 1), 256, 0, st>>>(c->L, c->C); });
+        timed(c, K_RECOUNT, st, [&] { ods_recount_all<<<dim3(c->C.NS, 3 * c->C.J + 1), 128, 0, st>>>(c->L, c->C); });
         INIT_TRY(cudaGetLastError());
         ods_init_jobs<<<1, 32, 0, st>>>(c->L, c->C);
         c->launches++;
