@@ -534,8 +534,7 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
             const uint32_t t = (wa & b) ? T_A : (wd & b) ? T_D : (we & b) ? T_E : T_S;
             const bool hit = (t == T_E || t == T_D || (t == T_A && !(ldcg(cons_j + w) & b)));
             if (hit) {
-                P.out_ids[row + s] = i;
-                P.out_src[row + s] = (uint8_t)t;
+                if (P.out_ids) { P.out_ids[row + s] = i; P.out_src[row + s] = (uint8_t)t; }
                 s_oid[s] = i;
                 s_osrc[s] = (uint8_t)t;
                 atomicOr(seen_j + w, b);
@@ -578,8 +577,7 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
             const uint32_t rank = perm_apply(key, perm_domain(S.tot[tt]), ul);
             const uint32_t id = pool_select(L, C, j * 3 + tt, t, j, s_pre + tt * C.NS, rank);
             const uint32_t s = s_miss[u];
-            P.out_ids[row + s] = id;
-            P.out_src[row + s] = (uint8_t)(t | SUBST);
+            if (P.out_ids) { P.out_ids[row + s] = id; P.out_src[row + s] = (uint8_t)(t | SUBST); }
             s_oid[s] = id;
             s_osrc[s] = (uint8_t)(t | SUBST);
             s_sub[u] = id;
@@ -601,8 +599,7 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
     // remaining misses are fetched from storage (R-O18)
     for (uint32_t u = q + tid; u < S.m; u += T) {
         const uint32_t s = s_miss[u], i = s_req[s];
-        P.out_ids[row + s] = i;
-        P.out_src[row + s] = (uint8_t)T_S;
+        if (P.out_ids) { P.out_ids[row + s] = i; P.out_src[row + s] = (uint8_t)T_S; }
         s_oid[s] = i;
         s_osrc[s] = (uint8_t)T_S;
         atomicOr(seen_j + (i >> 5), 1u << (i & 31));
@@ -1491,7 +1488,7 @@ static seneca_status replay(seneca_ctx* c, uint64_t R, uint64_t* d_transcript, u
     const uint64_t kChunk = 1u << 30;
     while (done < R && c->active) {
         const uint64_t n = std::min<uint64_t>(R - done, kChunk);
-        seneca_status s = launch_rounds(c, n, 0xffffffffu, nullptr, c->L.out_ids, c->L.out_src, c->C.Bmax, nullptr,
+        seneca_status s = launch_rounds(c, n, 0xffffffffu, nullptr, nullptr, nullptr, c->C.Bmax, nullptr,
                                         (unsigned long long*)d_transcript, st);
         if (s) return s;
         done += n;
