@@ -105,36 +105,57 @@ struct WarpTables {
     uint64_t capc[kMaxSteps];    // min(N, capAD(p))  -- A and D tiers (M x S_data per sample)
     uint64_t cape[kMaxSteps];    // min(N, capE(p))   -- E tier (S_data per sample)
     double tA[kMaxSteps];        // (capc/N) DSI_A
-    double tD[kMaxSteps];        // (capc/N) DSI_D
-    double tE[kMaxSteps];        // (cape/N) DSI_E
+    double tD[kMaxSteps];        // (capc/N) DSI_D        (D unclamped)
+    double tDc[kMaxSteps];       // ((N - capc)/N) DSI_D  (D clamped by the A count, indexed by p_A)
+    double tE[kMaxSteps];        // (cape/N) DSI_E        (E unclamped)
 };
 
+// x / N correctly rounded, for integers 0 <= x <= N < 2^53, with y = RN(1/N)
+// precomputed: q = RN(x y); the residual x - N q is exact; q' = RN(q + r y) is
+// RN(x/N) (Markstein).  x/N is never an exact tie between two doubles here (a
+// dyadic x/N is exactly representable), so q' equals __ddiv_rn(x, N) bit for bit.
+__device__ __forceinline__ double div_by_n(double x, double dN, double y) {
+    const double q = __dmul_rn(x, y);
+    const double r = __fma_rn(-dN, q, x);
+    return __fma_rn(r, y, q);
+}
+
 // The sweep of one profile by one warp; U = uint32_t when N < 2^31 (every
-// count fits, 32-bit integer ops), uint64_t otherwise.  Same binary64
-// operations on the same operands as the oracle (R-M7).
+// count fits, 32-bit integer ops), uint64_t otherwise.  Each split needs one
+// division at most: a clamped tier forces every later count to 0 (a zero term
+// is exactly +0.0 in the oracle's arithmetic too), so either the clamped E
+// count or the storage count is the only per-split quotient.
 template <typename U>
 __device__ __forceinline__ void sweep_profile(const WarpTables& W, uint64_t N64, const double dsi[4], uint32_t steps,
                                               uint32_t n_splits, double* grow, double& best, uint32_t& best_i) {
     const uint32_t lane = threadIdx.x & 31;
     const U N = (U)N64;
     const double dN = u2d(N64);
+    const double y = __drcp_rn(dN);
     uint32_t a = 0, b = lane;
     while (b > a) { b -= a + 1; ++a; }
     for (uint32_t idx = lane; idx < n_splits; idx += 32) {
         const uint32_t ie = steps - a, id = a - b, ia = b;          // table indices of p_E, p_D, p_A
-        const U nA = (U)W.capc[ia];                                  // Eq. 5 (clamped)
-        const U r1 = N - nA;
+        const U r1 = N - (U)W.capc[ia];                              // Eq. 5: N_A = capc[p_A]
         const U cD = (U)W.capc[id];
-        const U nD = cD < r1 ? cD : r1;                              // Eq. 6
-        const U r2 = r1 - nD;
-        const U cE = (U)W.cape[ie];
-        const U nE = cE < r2 ? cE : r2;                              // Eq. 7
-        const U nS = r2 - nE;                                        // Eq. 8
-        const double tA = W.tA[ia];
-        const double tD = (nD == cD) ? W.tD[id] : __dmul_rn(__ddiv_rn(u2d(nD), dN), dsi[1]);
-        const double tE = (nE == cE) ? W.tE[ie] : __dmul_rn(__ddiv_rn(u2d(nE), dN), dsi[2]);
-        const double tS = __dmul_rn(__ddiv_rn(u2d(nS), dN), dsi[3]);
-        const double v = __dadd_rn(__dadd_rn(__dadd_rn(tA, tD), tE), tS);   // Eq. 9, R-M7
+        double tD, tE, tS;
+        if (cD <= r1) {                                              // Eq. 6 unclamped
+            tD = W.tD[id];
+            const U r2 = r1 - cD;
+            const U cE = (U)W.cape[ie];
+            if (cE <= r2) {                                          // Eq. 7 unclamped, Eq. 8 remainder
+                tE = W.tE[ie];
+                tS = __dmul_rn(div_by_n(u2d(r2 - cE), dN, y), dsi[3]);
+            } else {                                                 // E takes the rest, N_S = 0
+                tE = __dmul_rn(div_by_n(u2d(r2), dN, y), dsi[2]);
+                tS = 0.0;
+            }
+        } else {                                                     // D takes the rest: N_E = N_S = 0
+            tD = W.tDc[ia];
+            tE = 0.0;
+            tS = 0.0;
+        }
+        const double v = __dadd_rn(__dadd_rn(__dadd_rn(W.tA[ia], tD), tE), tS);   // Eq. 9, R-M7
         if (grow) __stcs(grow + idx, v);
         if (v > best) { best = v; best_i = idx; }                   // idx increases per lane
         b += 32;                                                     // next split of this lane
@@ -180,6 +201,7 @@ mdp_sweep_kernel(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_pro
             W.cape[k] = ce;
             W.tA[k] = __dmul_rn(__ddiv_rn(u2d(cad), dN), dsi[0]);
             W.tD[k] = __dmul_rn(__ddiv_rn(u2d(cad), dN), dsi[1]);
+            W.tDc[k] = __dmul_rn(__ddiv_rn(u2d(N - cad), dN), dsi[1]);
             W.tE[k] = __dmul_rn(__ddiv_rn(u2d(ce), dN), dsi[2]);
         }
         __syncwarp();
