@@ -126,16 +126,18 @@ __device__ __forceinline__ double div_by_n(double x, double dN, double y) {
 // is exactly +0.0 in the oracle's arithmetic too), so either the clamped E
 // count or the storage count is the only per-split quotient.
 template <typename U>
-__device__ __forceinline__ void sweep_profile(const WarpTables& W, uint64_t N64, const double dsi[4], uint32_t steps,
-                                              uint32_t n_splits, double* grow, double& best, uint32_t& best_i) {
+__device__ __forceinline__ void sweep_profile(const WarpTables& W, const uint32_t* __restrict__ s_split, uint64_t N64,
+                                              const double dsi[4], uint32_t n_splits, double* grow, double& best,
+                                              uint32_t& best_i) {
     const uint32_t lane = threadIdx.x & 31;
     const U N = (U)N64;
     const double dN = u2d(N64);
     const double y = __drcp_rn(dN);
-    uint32_t a = 0, b = lane;
-    while (b > a) { b -= a + 1; ++a; }
+    constexpr bool kExact = sizeof(U) == 4;                          // div_by_n needs N < 2^53
+    if (grow) grow += lane;
     for (uint32_t idx = lane; idx < n_splits; idx += 32) {
-        const uint32_t ie = steps - a, id = a - b, ia = b;          // table indices of p_E, p_D, p_A
+        const uint32_t packed = s_split[idx];                        // p_A | p_D << 8 | p_E << 16 (table indices)
+        const uint32_t ia = packed & 0xffu, id = (packed >> 8) & 0xffu, ie = packed >> 16;
         const U r1 = N - (U)W.capc[ia];                              // Eq. 5: N_A = capc[p_A]
         const U cD = (U)W.capc[id];
         double tD, tE, tS;
@@ -145,9 +147,9 @@ __device__ __forceinline__ void sweep_profile(const WarpTables& W, uint64_t N64,
             const U cE = (U)W.cape[ie];
             if (cE <= r2) {                                          // Eq. 7 unclamped, Eq. 8 remainder
                 tE = W.tE[ie];
-                tS = __dmul_rn(div_by_n(u2d(r2 - cE), dN, y), dsi[3]);
+                tS = __dmul_rn(kExact ? div_by_n(u2d(r2 - cE), dN, y) : __ddiv_rn(u2d(r2 - cE), dN), dsi[3]);
             } else {                                                 // E takes the rest, N_S = 0
-                tE = __dmul_rn(div_by_n(u2d(r2), dN, y), dsi[2]);
+                tE = __dmul_rn(kExact ? div_by_n(u2d(r2), dN, y) : __ddiv_rn(u2d(r2), dN), dsi[2]);
                 tS = 0.0;
             }
         } else {                                                     // D takes the rest: N_E = N_S = 0
@@ -156,10 +158,8 @@ __device__ __forceinline__ void sweep_profile(const WarpTables& W, uint64_t N64,
             tS = 0.0;
         }
         const double v = __dadd_rn(__dadd_rn(__dadd_rn(W.tA[ia], tD), tE), tS);   // Eq. 9, R-M7
-        if (grow) __stcs(grow + idx, v);
+        if (grow) { __stcs(grow, v); grow += 32; }
         if (v > best) { best = v; best_i = idx; }                   // idx increases per lane
-        b += 32;                                                     // next split of this lane
-        while (b > a) { b -= a + 1; ++a; }
     }
 }
 
@@ -172,8 +172,15 @@ mdp_sweep_kernel(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_pro
                  double* __restrict__ grid) {
     constexpr int kWarps = kThreads / 32;
     __shared__ WarpTables s_tab[kWarps];
+    extern __shared__ uint32_t s_split[];                           // [n_splits] packed split coordinates
     const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     WarpTables& W = s_tab[w];
+    // enumeration index -> table indices (R-M9 order): row a has p_E = 100 - a g and
+    // positions b = 0..a with p_A = b g, p_D = (a - b) g
+    for (uint32_t a = 0, base = 0; a <= steps; base += a + 1, ++a)
+        for (uint32_t b = threadIdx.x; b <= a; b += blockDim.x)
+            s_split[base + b] = b | ((a - b) << 8) | ((steps - a) << 16);
+    __syncthreads();
 
     for (uint32_t pi = blockIdx.x * kWarps + w; pi < n_profiles; pi += gridDim.x * kWarps) {
         const seneca_mdp_profile p = profiles[pi];
@@ -192,6 +199,8 @@ mdp_sweep_kernel(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_pro
         const double dN = u2d(N);
         const uint64_t Xad = p.cache_bytes * p.m_den, Dad = 100ull * p.m_num * p.s_data;
         const uint64_t De = 100ull * p.s_data;
+        const bool exact_div = N < (1ull << 53);
+        const double yN = __drcp_rn(dN);
         for (uint32_t k = lane; k <= steps; k += 32) {
             const uint64_t pct = (uint64_t)k * g;
             uint64_t cad = (pct * Xad) / Dad, ce = (pct * p.cache_bytes) / De;   // Eqs. 5-7, exact floors
@@ -199,17 +208,20 @@ mdp_sweep_kernel(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_pro
             ce = ce < N ? ce : N;
             W.capc[k] = cad;
             W.cape[k] = ce;
-            W.tA[k] = __dmul_rn(__ddiv_rn(u2d(cad), dN), dsi[0]);
-            W.tD[k] = __dmul_rn(__ddiv_rn(u2d(cad), dN), dsi[1]);
-            W.tDc[k] = __dmul_rn(__ddiv_rn(u2d(N - cad), dN), dsi[1]);
-            W.tE[k] = __dmul_rn(__ddiv_rn(u2d(ce), dN), dsi[2]);
+            const double fa = exact_div ? div_by_n(u2d(cad), dN, yN) : __ddiv_rn(u2d(cad), dN);
+            const double fc = exact_div ? div_by_n(u2d(N - cad), dN, yN) : __ddiv_rn(u2d(N - cad), dN);
+            const double fe = exact_div ? div_by_n(u2d(ce), dN, yN) : __ddiv_rn(u2d(ce), dN);
+            W.tA[k] = __dmul_rn(fa, dsi[0]);
+            W.tD[k] = __dmul_rn(fa, dsi[1]);
+            W.tDc[k] = __dmul_rn(fc, dsi[1]);
+            W.tE[k] = __dmul_rn(fe, dsi[2]);
         }
         __syncwarp();
         double best = __longlong_as_double(0xfff0000000000000ll);
         uint32_t best_i = 0xffffffffu;
         double* grow = grid ? grid + (uint64_t)pi * n_splits : nullptr;
-        if (N < (1ull << 31)) sweep_profile<uint32_t>(W, N, dsi, steps, n_splits, grow, best, best_i);
-        else sweep_profile<uint64_t>(W, N, dsi, steps, n_splits, grow, best, best_i);
+        if (N < (1ull << 31)) sweep_profile<uint32_t>(W, s_split, N, dsi, n_splits, grow, best, best_i);
+        else sweep_profile<uint64_t>(W, s_split, N, dsi, n_splits, grow, best, best_i);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             const double ov = __shfl_xor_sync(0xffffffffu, best, o);
@@ -259,8 +271,8 @@ extern "C" seneca_status seneca_mdp_sweep(const seneca_mdp_profile* d_profiles, 
     const uint32_t per_cta = kThreads / 32;
     uint32_t blocks = (n_profiles + per_cta - 1) / per_cta;
     blocks = blocks < 65535u * 8u ? blocks : 65535u * 8u;
-    mdp_sweep_kernel<<<blocks, kThreads, 0, (cudaStream_t)stream>>>(d_profiles, n_profiles, grid_step_pct,
-                                                                   steps, ns, d_results, d_grid);
+    mdp_sweep_kernel<<<blocks, kThreads, ns * sizeof(uint32_t), (cudaStream_t)stream>>>(
+        d_profiles, n_profiles, grid_step_pct, steps, ns, d_results, d_grid);
     SENECA_CUDA_TRY(cudaGetLastError());
     return SENECA_OK;
 }
