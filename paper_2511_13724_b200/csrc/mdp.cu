@@ -271,6 +271,12 @@ extern "C" seneca_status seneca_mdp_sweep(const seneca_mdp_profile* d_profiles, 
     const uint32_t per_cta = kThreads / 32;
     uint32_t blocks = (n_profiles + per_cta - 1) / per_cta;
     blocks = blocks < 65535u * 8u ? blocks : 65535u * 8u;
+    static bool attr_set = false;
+    if (!attr_set) {
+        SENECA_CUDA_TRY(cudaFuncSetAttribute(mdp_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)(5151 * sizeof(uint32_t))));
+        attr_set = true;
+    }
     mdp_sweep_kernel<<<blocks, kThreads, ns * sizeof(uint32_t), (cudaStream_t)stream>>>(
         d_profiles, n_profiles, grid_step_pct, steps, ns, d_results, d_grid);
     SENECA_CUDA_TRY(cudaGetLastError());
