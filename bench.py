@@ -61,10 +61,8 @@ def parse():
 
 
 def dist_env():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
+    from paper_2511_13724_b200 import dist as D
+    return D.env()
 
 
 def caps_of(c):
@@ -203,16 +201,16 @@ def algorithmic_bytes(name, info):
         return info["mdp_profiles"] * (112 + 48) + (8 * info["mdp_profiles"] * info["mdp_splits"]
                                                    if info["mdp_grid"] else 0)
     if name == "ods_rounds":
-        # per requested sample: list entry 4 + seen word 4 + 3 residency words 12 + consumer word 4
-        #   + seen RMW 8 + id/src out 5 + digest/transcript-free stats 0 = 37 B
-        # per substitute: block-count row 128 + pool words (<= 3 bitmaps x 32 B) 96 + seen/consumer
-        #   RMW 16 + count updates 16 + out 5 = 261 B
-        # per A-served candidate: id 4 + residency 4 + J consumer words 4J
-        # per refill (selected): block-count row 128 + 3 x 32 B words + bitmap RMW 8 + count updates 16
-        #   + J seen words 4J
+        # per requested sample: list entry 4 + seen word 4 + residency words (<= 3) 12 + consumer word 4
+        #   + seen RMW 8 = 32 B
+        # per substitute: 32-B block-count row + one 16-B vector of each of <= 3 bitmaps 48 + seen/consumer
+        #   RMW 16 + block-count RMW 8 = 104 B
+        # per A-served sample: consumer-count RMW 8 B; per eviction: residency + J consumer RMW 8(J+1)
+        # per refill: count row 32 + 3 bitmap vectors 48 + residency RMW 8 + J seen words 4J
         # per job-epoch: seen clear W4 + recount (residency x3 + consumers + seen) 5 W4
-        return (37 * info["decisions"] + 261 * info["substitutes"] + (8 + 4 * J) * info["a_served"]
-                + (248 + 4 * J) * info["refilled"] + 6 * W4 * info["job_epochs"])
+        return (32 * info["decisions"] + 104 * info["substitutes"] + 8 * info["a_served"]
+                + 8 * (J + 1) * info["refilled"] + (88 + 4 * J) * info["refilled"]
+                + 6 * W4 * info["job_epochs"])
     if name == "ods_perm_all":
         return 4 * info["n_total"] * info["job_epochs"]     # ALU-bound (Philox); bytes written
     if name == "ods_recount_all":
@@ -248,13 +246,14 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     stream = torch.cuda.current_stream(dev)
 
-    c = synth.ods_config(args.workload, seed=synth.PERF_SEED + rank)
+    from paper_2511_13724_b200 import dist as D
+    c = synth.ods_config(args.workload, seed=D.rank_seed(synth.PERF_SEED, rank))
     caps = caps_of(c)
     ce, cd, ca = caps
     dec_per_step = decisions_of(c)
 
     # ---- inputs resident in HBM before timing
-    mdp_cols = synth.mdp_profiles(args.mdp_profiles, seed=synth.PERF_SEED + rank)
+    mdp_cols = synth.mdp_profiles(args.mdp_profiles, seed=D.rank_seed(synth.PERF_SEED, rank))
     prof_host = S.profiles_from_columns(mdp_cols)
     d_prof = torch.from_numpy(prof_host.view(np.uint8).copy()).to(dev)
     nsplit = S.mdp_num_splits(args.mdp_grid_step)
@@ -393,10 +392,7 @@ def main():
     mdp_s = sum(mdp_ms) / 1e3
     e2e_s = sum(e2e_ods)
     e2e_m = sum(e2e_mdp)
-    if world > 1:
-        t = torch.tensor([ods_s, mdp_s, e2e_s, e2e_m], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ods_s, mdp_s, e2e_s, e2e_m = t.tolist()
+    ods_s, mdp_s, e2e_s, e2e_m = D.reduce_times([ods_s, mdp_s, e2e_s, e2e_m], device=dev)   # max over ranks
     total_dec = dec_per_step * args.steps * world
     total_evals = args.mdp_profiles * nsplit * args.steps * world
 
