@@ -1,19 +1,21 @@
 // mdp.cu -- Model-Driven Partitioning sweep.
 //
-// One warp per hardware profile:
-//   prologue  Eqs. 1-4 tier throughputs with the ring-reduce
-//             overhead C = 2(n-1)/n * betaN; integer capacity tables
-//             capAD[p], capE[p] (Eqs. 5-7 floored exactly, R-M6) and the Eq. 9
-//             terms that depend on one coordinate only, in the warp's slice of
-//             shared memory;
-//   main loop every split of the grid: clamped counts (Eqs. 5-8) and
-//             DSI_overall (Eq. 9) in the literal order of R-M7; optional
-//             coalesced write of the full grid row;
-//   epilogue  warp argmax, exact ties -> smallest enumeration index (R-M8).
+// One CTA per hardware profile (persistent CTAs walk a grid-stride list):
+//   prologue  (warp 0, one profile ahead, double-buffered) Eqs. 1-4 tier
+//             throughputs with the ring-reduce overhead
+//             C = 2(n-1)/n * betaN; integer capacity tables capAD[p],
+//             capE[p] (Eqs. 5-7 floored exactly, R-M6) and the Eq. 9 terms that
+//             depend on one coordinate only, as rows in shared memory;
+//   main loop every split of the grid, 256 threads: clamped counts (Eqs. 5-8)
+//             and DSI_overall (Eq. 9) in the literal order of R-M7, branch-free;
+//             optional coalesced streaming write of the full grid row;
+//   epilogue  argmax per thread / warp / CTA, exact ties -> smallest
+//             enumeration index (R-M8).
 //
 // Bit-exactness with the oracle: every binary64 operation is an explicit
 // round-to-nearest intrinsic (__dadd_rn/__dmul_rn/__ddiv_rn, never contracted
-// into an FMA), integer->double conversions are __ull2double_rn, and a term
+// into an FMA), integer->double conversions are exact (__ull2double_rn, or the
+// 2^52 trick for 32-bit counts), and a term
 // taken from a table is the same operation on the same operands as the one the
 // oracle performs per split.
 #include <cstdint>
@@ -26,10 +28,24 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kMaxSteps = 101;  // grid step 1 % -> 101 values per coordinate
+#ifndef SENECA_MDP_CHUNK
+#define SENECA_MDP_CHUNK 512
+#endif
+#ifndef SENECA_MDP_MINB
+#define SENECA_MDP_MINB 3
+#endif
+constexpr uint32_t kChunk = SENECA_MDP_CHUNK;  // splits per sweep work item (16 per lane)
 
 enum : uint8_t { L_CACHE = 0, L_NIC = 1, L_PCIE = 2, L_CPU_AUG = 3, L_CPU_DEC_AUG = 4, L_GPU = 5, L_STORAGE = 6 };
 
 __device__ __forceinline__ double u2d(uint64_t x) { return __ull2double_rn(x); }
+
+// Exact u32 -> double on the FP64 pipe: (2^52 + x) - 2^52 is exact for x < 2^32
+// and equals __ull2double_rn(x); the I2F.F64 conversion runs on the narrow XU
+// pipe, which ncu showed to be the sweep's bottleneck.
+__device__ __forceinline__ double u32_to_d(uint32_t x) {
+    return __dsub_rn(__hiloint2double(0x43300000, (int)x), 4503599627370496.0);
+}
 
 __device__ __forceinline__ void take_min(double term, uint8_t code, double& best, uint8_t& lim) {
     if (term < best) { best = term; lim = code; }
@@ -99,15 +115,26 @@ __device__ void tier_throughputs(const seneca_mdp_profile& p, double dsi[4], uin
     lim[0] = la; lim[1] = ld; lim[2] = le; lim[3] = ls;
 }
 
-// Per-warp shared tables for one profile: capacities clamped to N (exact
-// integers), and the Eq. 9 terms that depend on a single coordinate.
-struct WarpTables {
-    uint64_t capc[kMaxSteps];    // min(N, capAD(p))  -- A and D tiers (M x S_data per sample)
-    uint64_t cape[kMaxSteps];    // min(N, capE(p))   -- E tier (S_data per sample)
-    double tA[kMaxSteps];        // (capc/N) DSI_A
-    double tD[kMaxSteps];        // (capc/N) DSI_D        (D unclamped)
-    double tDc[kMaxSteps];       // ((N - capc)/N) DSI_D  (D clamped by the A count, indexed by p_A)
-    double tE[kMaxSteps];        // (cape/N) DSI_E        (E unclamped)
+// One row per grid coordinate value k (p = k g %): the capacities clamped to N
+// (exact integers, Eqs. 5-7, R-M6) and the Eq. 9 terms that depend on a single
+// coordinate.  Array-of-rows so that one byte offset per coordinate addresses
+// every field with an immediate displacement.
+struct Row {
+    uint32_t capc;   // min(N, capAD(p))  -- A and D tiers (M x S_data per sample); used when N < 2^31
+    uint32_t cape;   // min(N, capE(p))   -- E tier (S_data per sample)
+    double tA;       // (capc/N) DSI_A
+    double tD;       // (capc/N) DSI_D        (D unclamped)
+    double tDc;      // ((N - capc)/N) DSI_D  (D clamped by the A count, indexed by p_A)
+    double tE;       // (cape/N) DSI_E        (E unclamped)
+};
+static_assert(sizeof(Row) == 40, "Row layout");
+
+// Per-profile header: Eqs. 1-4 results and what the row build needs.
+struct Header {
+    double dsi[4];
+    uint64_t N, Xad, Dad, De, cache_bytes;
+    uint8_t lim[4];
+    uint32_t valid;
 };
 
 // x / N correctly rounded, for integers 0 <= x <= N < 2^53, with y = RN(1/N)
@@ -120,128 +147,245 @@ __device__ __forceinline__ double div_by_n(double x, double dN, double y) {
     return __fma_rn(r, y, q);
 }
 
-// The sweep of one profile by one warp; U = uint32_t when N < 2^31 (every
-// count fits, 32-bit integer ops), uint64_t otherwise.  Each split needs one
-// division at most: a clamped tier forces every later count to 0 (a zero term
-// is exactly +0.0 in the oracle's arithmetic too), so either the clamped E
-// count or the storage count is the only per-split quotient.
-template <typename U>
-__device__ __forceinline__ void sweep_profile(const WarpTables& W, const uint32_t* __restrict__ s_split, uint64_t N64,
-                                              const double dsi[4], uint32_t n_splits, double* grow, double& best,
-                                              uint32_t& best_i) {
+// Eqs. 1-4 of profile `pi` into a header (one warp; every lane computes the
+// same values, lane 0 stores).
+__device__ void build_header(const seneca_mdp_profile* __restrict__ profiles, uint32_t pi, Header& H) {
     const uint32_t lane = threadIdx.x & 31;
-    const U N = (U)N64;
-    const double dN = u2d(N64);
-    const double y = __drcp_rn(dN);
-    constexpr bool kExact = sizeof(U) == 4;                          // div_by_n needs N < 2^53
-    if (grow) grow += lane;
-    for (uint32_t idx = lane; idx < n_splits; idx += 32) {
-        const uint32_t packed = s_split[idx];                        // p_A | p_D << 8 | p_E << 16 (table indices)
-        const uint32_t ia = packed & 0xffu, id = (packed >> 8) & 0xffu, ie = packed >> 16;
-        const U r1 = N - (U)W.capc[ia];                              // Eq. 5: N_A = capc[p_A]
-        const U cD = (U)W.capc[id];
-        double tD, tE, tS;
-        if (cD <= r1) {                                              // Eq. 6 unclamped
-            tD = W.tD[id];
-            const U r2 = r1 - cD;
-            const U cE = (U)W.cape[ie];
-            if (cE <= r2) {                                          // Eq. 7 unclamped, Eq. 8 remainder
-                tE = W.tE[ie];
-                tS = __dmul_rn(kExact ? div_by_n(u2d(r2 - cE), dN, y) : __ddiv_rn(u2d(r2 - cE), dN), dsi[3]);
-            } else {                                                 // E takes the rest, N_S = 0
-                tE = __dmul_rn(kExact ? div_by_n(u2d(r2), dN, y) : __ddiv_rn(u2d(r2), dN), dsi[2]);
-                tS = 0.0;
-            }
-        } else {                                                     // D takes the rest: N_E = N_S = 0
-            tD = W.tDc[ia];
-            tE = 0.0;
-            tS = 0.0;
-        }
-        const double v = __dadd_rn(__dadd_rn(__dadd_rn(W.tA[ia], tD), tE), tS);   // Eq. 9, R-M7
-        if (grow) { __stcs(grow, v); grow += 32; }
-        if (v > best) { best = v; best_i = idx; }                   // idx increases per lane
+    const seneca_mdp_profile p = profiles[pi];
+    const bool ok = profile_valid(p);
+    double dsi[4] = {0.0, 0.0, 0.0, 0.0};
+    uint8_t lim[4] = {0, 0, 0, 0};
+    if (ok) tier_throughputs(p, dsi, lim);
+    if (lane == 0) {
+        H.valid = ok;
+        for (int t = 0; t < 4; ++t) { H.dsi[t] = dsi[t]; H.lim[t] = lim[t]; }
+        H.N = p.n_total;
+        H.Xad = p.cache_bytes * p.m_den;
+        H.Dad = 100ull * p.m_num * p.s_data;
+        H.De = 100ull * p.s_data;
+        H.cache_bytes = p.cache_bytes;
     }
 }
 
-// One WARP per profile (8 profiles per CTA in flight): the prologue needs only
-// warp-level synchronisation, so one warp's setup overlaps the other warps'
-// sweeps; each warp iteration stores 32 consecutive grid values (256 B).
-__global__ void __launch_bounds__(kThreads)
+// Rows k0 .. k0+31 (one per lane, k <= steps) of a valid profile's tables.
+__device__ void build_rows(const Header& H, uint32_t k0, uint32_t g, uint32_t steps, Row* rows) {
+    const uint32_t k = k0 + (threadIdx.x & 31);
+    if (k > steps) return;
+    const uint64_t N = H.N;
+    const double dN = u2d(N);
+    const bool exact_div = N < (1ull << 53);
+    const double yN = __drcp_rn(dN);
+    const uint64_t pct = (uint64_t)k * g;
+    uint64_t cad = (pct * H.Xad) / H.Dad, ce = (pct * H.cache_bytes) / H.De;   // Eqs. 5-7, exact floors
+    cad = cad < N ? cad : N;
+    ce = ce < N ? ce : N;
+    Row& R = rows[k];
+    R.capc = (uint32_t)cad;                                          // used only when N < 2^31
+    R.cape = (uint32_t)ce;
+    const double fa = exact_div ? div_by_n(u2d(cad), dN, yN) : __ddiv_rn(u2d(cad), dN);
+    const double fc = exact_div ? div_by_n(u2d(N - cad), dN, yN) : __ddiv_rn(u2d(N - cad), dN);
+    const double fe = exact_div ? div_by_n(u2d(ce), dN, yN) : __ddiv_rn(u2d(ce), dN);
+    R.tA = __dmul_rn(fa, H.dsi[0]);
+    R.tD = __dmul_rn(fa, H.dsi[1]);
+    R.tDc = __dmul_rn(fc, H.dsi[1]);
+    R.tE = __dmul_rn(fe, H.dsi[2]);
+}
+
+__device__ __forceinline__ const Row& row_at(const Row* rows, uint32_t byte_off) {
+    return *reinterpret_cast<const Row*>(reinterpret_cast<const char*>(rows) + byte_off);
+}
+
+// One chunk of kChunk consecutive splits of one profile (N < 2^31: every count
+// fits 32 bits), kChunk / 32 per lane.  Branch-free: each split needs exactly
+// one quotient -- the clamped E count or the storage count (a clamped tier
+// forces every later count to 0) -- so the numerator and its multiplier are
+// selected.  Eq. 9 in the order of R-M7 is ((tA + tD) + tE) + tS; with E
+// clamped it is ((tA + tD) + tE) + 0 and is computed as ((tA + tD) + 0) + tE,
+// the same value (x + 0 = x for x >= +0).
+struct Sweep32 {        // per-profile constants of the 32-bit sweep, hoisted out of the chunks
+    uint32_t N;
+    double dN, y, dsiE, dsiS;
+};
+
+template <bool kGrid, bool kFull>
+__device__ __forceinline__ void sweep32_chunk(const Sweep32& P, const Row* rows, const uint2* __restrict__ s_split,
+                                              uint32_t i0, uint32_t n_splits, double* __restrict__ grow,
+                                              double& best, uint32_t& best_i) {
+    const uint32_t N = P.N;
+    const double dN = P.dN, y = P.y, dsiE = P.dsiE, dsiS = P.dsiS;
+    const uint32_t lane = threadIdx.x & 31;
+#pragma unroll 4
+    for (uint32_t u = 0; u < kChunk / 32; ++u) {
+        const uint32_t idx = i0 + u * 32 + lane;
+        if (!kFull && idx >= n_splits) break;
+        const uint2 w = s_split[idx];                              // byte offsets of rows p_A | p_D << 16, p_E
+        const Row& ra = row_at(rows, w.x & 0xffffu);
+        const Row& rd = row_at(rows, w.x >> 16);
+        const Row& re = row_at(rows, w.y);
+        const uint32_t r1 = N - ra.capc;                           // Eq. 5: N_A = capc[p_A]
+        const uint32_t cD = rd.capc;
+        const bool dfree = cD <= r1;                               // Eq. 6 unclamped
+        const uint32_t r2 = dfree ? r1 - cD : 0u;
+        const uint32_t cE = re.cape;
+        const bool efree = dfree && cE <= r2;                      // Eq. 7 unclamped
+        const uint32_t x = efree ? r2 - cE : r2;                   // N_S, or the clamped N_E (0 if D clamped)
+        const double q = div_by_n(u32_to_d(x), dN, y);
+        const double prod = __dmul_rn(q, efree ? dsiS : dsiE);
+        const double tD = dfree ? rd.tD : ra.tDc;
+        const double tX = efree ? re.tE : 0.0;
+        const double v = __dadd_rn(__dadd_rn(__dadd_rn(ra.tA, tD), tX), prod);
+        if (kGrid) __stcs(grow + idx, v);
+        if (v > best) { best = v; best_i = idx; }                 // a lane's idx only increases
+    }
+}
+
+// The general chunk (N >= 2^31): the same split arithmetic with 64-bit counts
+// and __ddiv_rn; the capacities (Eqs. 5-7 exact floors) recomputed on the fly
+// -- a rare path, kept simple rather than fast.
+__device__ void sweep64_chunk(const Header& H, const Row* rows, uint32_t g, const uint2* __restrict__ s_split,
+                              uint32_t i0, uint32_t n_splits, double* grow, double& best, uint32_t& best_i) {
+    const uint64_t N = H.N;
+    const double dN = u2d(N);
+    auto capc = [&](uint32_t k) { const uint64_t c = ((uint64_t)k * g * H.Xad) / H.Dad; return c < N ? c : N; };
+    auto cape = [&](uint32_t k) { const uint64_t c = ((uint64_t)k * g * H.cache_bytes) / H.De; return c < N ? c : N; };
+    for (uint32_t idx = i0 + (threadIdx.x & 31); idx < i0 + kChunk && idx < n_splits; idx += 32) {
+        const uint2 w = s_split[idx];
+        const uint32_t ka = (w.x & 0xffffu) / sizeof(Row), kd = (w.x >> 16) / sizeof(Row), ke = w.y / sizeof(Row);
+        const uint64_t r1 = N - capc(ka);
+        const uint64_t cD = capc(kd);
+        const bool dfree = cD <= r1;
+        const uint64_t r2 = dfree ? r1 - cD : 0ull;
+        const uint64_t cE = cape(ke);
+        const bool efree = dfree && cE <= r2;
+        const uint64_t x = efree ? r2 - cE : r2;
+        const double prod = __dmul_rn(__ddiv_rn(u2d(x), dN), efree ? H.dsi[3] : H.dsi[2]);
+        const double tD = dfree ? rows[kd].tD : rows[ka].tDc;
+        const double tX = efree ? rows[ke].tE : 0.0;
+        const double v = __dadd_rn(__dadd_rn(__dadd_rn(rows[ka].tA, tD), tX), prod);
+        if (grow) __stcs(grow + idx, v);
+        if (v > best) { best = v; best_i = idx; }
+    }
+}
+
+// One CTA per profile, persistent over a grid-stride list of profiles
+// (iteration i sweeps profile blockIdx + i gridDim).  The work of an iteration
+// is a list of items that warps take from a shared counter, so the serial
+// per-profile setup never idles the CTA:
+//   item 0                 Eqs. 1-4 header of profile i+2   (4 header buffers)
+//   items 1 .. nrow        32 table rows each of profile i+1 (2 row buffers)
+//   the rest               kChunk-split chunks of profile i's sweep
+// Rows live once per CTA (uniform addresses, immediate field displacements);
+// each iteration stores one contiguous grid row with streaming stores.  A
+// warp's items come in increasing order, so a lane's split indices increase
+// and `v > best` keeps the first maximum; argmax per lane / warp / CTA, exact
+// ties -> smallest enumeration index (R-M8).
+__global__ void __launch_bounds__(kThreads, SENECA_MDP_MINB)
 mdp_sweep_kernel(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_profiles, uint32_t g,
                  uint32_t steps, uint32_t n_splits, seneca_mdp_result* __restrict__ results,
                  double* __restrict__ grid) {
     constexpr int kWarps = kThreads / 32;
-    __shared__ WarpTables s_tab[kWarps];
-    extern __shared__ uint32_t s_split[];                           // [n_splits] packed split coordinates
+    __shared__ Header s_hdr[4];
+    __shared__ Row s_rows[2][kMaxSteps];
+    __shared__ double s_red_v[2][kWarps];
+    __shared__ uint32_t s_red_i[2][kWarps];
+    __shared__ uint32_t s_ctr[2];
+    extern __shared__ uint2 s_split[];                              // [n_splits] row byte offsets
     const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    WarpTables& W = s_tab[w];
-    // enumeration index -> table indices (R-M9 order): row a has p_E = 100 - a g and
+    const uint32_t G = gridDim.x;
+    const uint32_t nrow = (steps + 32) / 32;                        // row items per profile
+    const uint32_t nchunk = (n_splits + kChunk - 1) / kChunk;
+    const uint32_t n_items = 1 + nrow + nchunk;
+    // enumeration index -> rows (R-M9 order): row a has p_E = 100 - a g and
     // positions b = 0..a with p_A = b g, p_D = (a - b) g
-    for (uint32_t a = 0, base = 0; a <= steps; base += a + 1, ++a)
-        for (uint32_t b = threadIdx.x; b <= a; b += blockDim.x)
-            s_split[base + b] = b | ((a - b) << 8) | ((steps - a) << 16);
+    for (uint32_t idx = threadIdx.x; idx < n_splits; idx += blockDim.x) {
+        uint32_t a = (uint32_t)((sqrtf((float)(8u * idx + 1u)) - 1.0f) * 0.5f);   // row of idx, then exact fix-up
+        while ((a + 1) * (a + 2) / 2 <= idx) ++a;
+        while (a * (a + 1) / 2 > idx) --a;
+        const uint32_t b = idx - a * (a + 1) / 2;
+        s_split[idx] = make_uint2((uint32_t)(b * sizeof(Row)) | (uint32_t)((a - b) * sizeof(Row)) << 16,
+                                  (uint32_t)((steps - a) * sizeof(Row)));
+    }
+    if (threadIdx.x < 2) s_ctr[threadIdx.x] = 0;
+    if (w < 2 && blockIdx.x + w * G < n_profiles) build_header(profiles, blockIdx.x + w * G, s_hdr[w]);
+    __syncthreads();
+    if (w < nrow && s_hdr[0].valid) build_rows(s_hdr[0], w * 32, g, steps, s_rows[0]);
     __syncthreads();
 
-    for (uint32_t pi = blockIdx.x * kWarps + w; pi < n_profiles; pi += gridDim.x * kWarps) {
-        const seneca_mdp_profile p = profiles[pi];
-        if (!profile_valid(p)) {
-            if (lane == 0) {
-                seneca_mdp_result r = {};
-                r.status = 1;
-                results[pi] = r;
-            }
-            continue;
-        }
-        double dsi[4];
-        uint8_t lim[4];
-        tier_throughputs(p, dsi, lim);            // every lane (no shared state, no barrier)
-        const uint64_t N = p.n_total;
-        const double dN = u2d(N);
-        const uint64_t Xad = p.cache_bytes * p.m_den, Dad = 100ull * p.m_num * p.s_data;
-        const uint64_t De = 100ull * p.s_data;
-        const bool exact_div = N < (1ull << 53);
-        const double yN = __drcp_rn(dN);
-        for (uint32_t k = lane; k <= steps; k += 32) {
-            const uint64_t pct = (uint64_t)k * g;
-            uint64_t cad = (pct * Xad) / Dad, ce = (pct * p.cache_bytes) / De;   // Eqs. 5-7, exact floors
-            cad = cad < N ? cad : N;
-            ce = ce < N ? ce : N;
-            W.capc[k] = cad;
-            W.cape[k] = ce;
-            const double fa = exact_div ? div_by_n(u2d(cad), dN, yN) : __ddiv_rn(u2d(cad), dN);
-            const double fc = exact_div ? div_by_n(u2d(N - cad), dN, yN) : __ddiv_rn(u2d(N - cad), dN);
-            const double fe = exact_div ? div_by_n(u2d(ce), dN, yN) : __ddiv_rn(u2d(ce), dN);
-            W.tA[k] = __dmul_rn(fa, dsi[0]);
-            W.tD[k] = __dmul_rn(fa, dsi[1]);
-            W.tDc[k] = __dmul_rn(fc, dsi[1]);
-            W.tE[k] = __dmul_rn(fe, dsi[2]);
-        }
-        __syncwarp();
+    uint32_t it = 0;
+    for (uint32_t pi = blockIdx.x; pi < n_profiles; pi += G, ++it) {
+        const uint32_t buf = it & 1;
+        const Header& H = s_hdr[it & 3];
+        const bool valid = H.valid;
+        double* grow = (grid && valid) ? grid + (uint64_t)pi * n_splits : nullptr;
         double best = __longlong_as_double(0xfff0000000000000ll);
         uint32_t best_i = 0xffffffffu;
-        double* grow = grid ? grid + (uint64_t)pi * n_splits : nullptr;
-        if (N < (1ull << 31)) sweep_profile<uint32_t>(W, s_split, N, dsi, n_splits, grow, best, best_i);
-        else sweep_profile<uint64_t>(W, s_split, N, dsi, n_splits, grow, best, best_i);
+        const bool narrow = H.N < (1ull << 31);
+        Sweep32 P;
+        P.N = (uint32_t)H.N;
+        P.dN = u2d(H.N);
+        P.y = __drcp_rn(P.dN);
+        P.dsiE = H.dsi[2];
+        P.dsiS = H.dsi[3];
+        if (threadIdx.x == 0) s_ctr[buf ^ 1] = 0;                  // next iteration's counter (idle since the last barrier)
+        for (;;) {
+            uint32_t t = 0;
+            if (lane == 0) t = atomicAdd(&s_ctr[buf], 1u);
+            t = __shfl_sync(0xffffffffu, t, 0);
+            if (t >= n_items) break;
+            if (t == 0) {
+                if (pi + 2 * G < n_profiles) build_header(profiles, pi + 2 * G, s_hdr[(it + 2) & 3]);
+            } else if (t <= nrow) {
+                const Header& Hn = s_hdr[(it + 1) & 3];
+                if (pi + G < n_profiles && Hn.valid) build_rows(Hn, (t - 1) * 32, g, steps, s_rows[buf ^ 1]);
+            } else if (valid) {
+                const uint32_t i0 = (t - 1 - nrow) * kChunk;
+                if (narrow) {
+                    const bool full = i0 + kChunk <= n_splits;
+                    if (grow) {
+                        if (full) sweep32_chunk<true, true>(P, s_rows[buf], s_split, i0, n_splits, grow, best, best_i);
+                        else sweep32_chunk<true, false>(P, s_rows[buf], s_split, i0, n_splits, grow, best, best_i);
+                    } else {
+                        if (full) sweep32_chunk<false, true>(P, s_rows[buf], s_split, i0, n_splits, nullptr, best, best_i);
+                        else sweep32_chunk<false, false>(P, s_rows[buf], s_split, i0, n_splits, nullptr, best, best_i);
+                    }
+                } else {
+                    sweep64_chunk(H, s_rows[buf], g, s_split, i0, n_splits, grow, best, best_i);
+                }
+            }
+        }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             const double ov = __shfl_xor_sync(0xffffffffu, best, o);
             const uint32_t oi = __shfl_xor_sync(0xffffffffu, best_i, o);
             if (ov > best || (ov == best && oi < best_i)) { best = ov; best_i = oi; }
         }
-        if (lane == 0) {
-            uint32_t ra = 0, rb = best_i;
-            while (rb > ra) { rb -= ra + 1; ++ra; }
-            seneca_mdp_result r;
-            r.p_e = (uint8_t)(100 - ra * g);
-            r.p_d = (uint8_t)((ra - rb) * g);
-            r.p_a = (uint8_t)(rb * g);
-            r.lim_a = lim[0]; r.lim_d = lim[1]; r.lim_e = lim[2]; r.lim_s = lim[3];
-            r.status = 0;
-            r.v_best = best;
-            r.dsi_a = dsi[0]; r.dsi_d = dsi[1]; r.dsi_e = dsi[2]; r.dsi_s = dsi[3];
+        if (lane == 0) { s_red_v[buf][w] = best; s_red_i[buf][w] = best_i; }
+        __syncthreads();                                            // publishes next rows / headers, this reduction
+        if (threadIdx.x == 0) {
+            seneca_mdp_result r = {};
+            if (!valid) {
+                r.status = 1;
+            } else {
+                best = s_red_v[buf][0]; best_i = s_red_i[buf][0];
+                for (int k = 1; k < kWarps; ++k) {
+                    const double ov = s_red_v[buf][k];
+                    const uint32_t oi = s_red_i[buf][k];
+                    if (ov > best || (ov == best && oi < best_i)) { best = ov; best_i = oi; }
+                }
+                uint32_t ra = 0, rb = best_i;
+                while (rb > ra) { rb -= ra + 1; ++ra; }
+                r.p_e = (uint8_t)(100 - ra * g);
+                r.p_d = (uint8_t)((ra - rb) * g);
+                r.p_a = (uint8_t)(rb * g);
+                r.lim_a = H.lim[0]; r.lim_d = H.lim[1]; r.lim_e = H.lim[2]; r.lim_s = H.lim[3];
+                r.status = 0;
+                r.v_best = best;
+                r.dsi_a = H.dsi[0]; r.dsi_d = H.dsi[1]; r.dsi_e = H.dsi[2]; r.dsi_s = H.dsi[3];
+            }
             results[pi] = r;
         }
-        __syncwarp();
+        // header buffer (it & 3) is rewritten at iteration it + 2, after the
+        // next barrier, which thread 0 reaches only after this store
     }
 }
 
@@ -268,16 +412,20 @@ extern "C" seneca_status seneca_mdp_sweep(const seneca_mdp_profile* d_profiles, 
     }
     const uint32_t steps = 100 / grid_step_pct;
     const uint32_t ns = (uint32_t)seneca_mdp_num_splits(grid_step_pct);
-    const uint32_t per_cta = kThreads / 32;
-    uint32_t blocks = (n_profiles + per_cta - 1) / per_cta;
-    blocks = blocks < 65535u * 8u ? blocks : 65535u * 8u;
-    static bool attr_set = false;
-    if (!attr_set) {
+    // persistent grid: every resident CTA slot of the device, never more CTAs than profiles
+    static int slots = 0;
+    if (!slots) {
         SENECA_CUDA_TRY(cudaFuncSetAttribute(mdp_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)(5151 * sizeof(uint32_t))));
-        attr_set = true;
+                                             (int)(5151 * sizeof(uint2))));
+        int dev = 0, sms = 0, per_sm = 0;
+        SENECA_CUDA_TRY(cudaGetDevice(&dev));
+        SENECA_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        SENECA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mdp_sweep_kernel, kThreads,
+                                                                      5151 * sizeof(uint2)));
+        slots = sms * (per_sm > 0 ? per_sm : 1);
     }
-    mdp_sweep_kernel<<<blocks, kThreads, ns * sizeof(uint32_t), (cudaStream_t)stream>>>(
+    const uint32_t blocks = n_profiles < (uint32_t)slots ? n_profiles : (uint32_t)slots;
+    mdp_sweep_kernel<<<blocks, kThreads, ns * sizeof(uint2), (cudaStream_t)stream>>>(
         d_profiles, n_profiles, grid_step_pct, steps, ns, d_results, d_grid);
     SENECA_CUDA_TRY(cudaGetLastError());
     return SENECA_OK;
