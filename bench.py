@@ -17,6 +17,10 @@ batch of synthetic input:
 N > 1 (torchrun, one process per GPU): every rank replays its own instance
 (seed + rank) and sweeps its own 10,000 profiles -- the path partitions into
 independent problems, so there is no data-path collective (weak scaling).
+
+`replicas`: the same workload as R independent replays in ONE
+context (replica k: seed + k), one cooperative launch filling the GPU with
+R x (J + 1) round CTAs; reported beside the single-replay headline.
 """
 from __future__ import annotations
 
@@ -57,6 +61,8 @@ def parse():
     ap.add_argument("--no-profile", action="store_true", help="no CUDA-event kernel timing in the timed steps")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample duration")
+    ap.add_argument("--replicas", type=int, default=-1,
+                    help="also time R independent replays in one context (-1: as many as fit the GPU, 0: skip)")
     return ap.parse_args()
 
 
@@ -263,6 +269,7 @@ def main():
     ws_bytes = S.state_bytes(cfg)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)      # > 126 MB L2
+    ws_r_holder = []
 
     def barrier():
         if world > 1:
@@ -360,6 +367,55 @@ def main():
     except Exception as e:  # the oracle is only a checker; report, do not fall back
         parity["mdp_vs_oracle_first_200_profiles"] = f"unchecked: {e}"
 
+    # ---- R independent replays in one context (untimed warm-up, then timed steps)
+    rep_line = None
+    if args.replicas != 0:
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        R = args.replicas if args.replicas > 0 else min(64, sms // (len(c["batch"]) + 1))
+        rseed = (synth.PERF_SEED + 64 * rank) & 0xFFFFFFFFFFFFFFFF
+        rcfg = S.make_config(c["n_total"], c["batch"], c["target"], ce, cd, ca, rseed, replicas=R)
+        rbytes = S.state_bytes(rcfg)
+        del ws_r_holder[:]
+        ws_r = torch.empty(rbytes, dtype=torch.uint8, device=dev)
+        ws_r_holder.append(ws_r)
+        rep_ms = []
+        for s in range(1 + args.steps):
+            flush.fill_(s & 0xFF)
+            barrier()
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            rctx = S.init_cache(rcfg, ws_r, rbytes, stream)
+            S.replay_epochs(rctx, max(c["target"]), None, stream)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            barrier()
+            if s >= 1:
+                rep_ms.append(e0.elapsed_time(e1))
+                launches_rep = S.launch_count(rctx)
+            if s < args.steps:
+                S.destroy(rctx)
+        S.sync_status(rctx, stream)
+        rv = S.read_state(rctx)
+        served_all = True
+        rep0_digest_ok = None
+        nst1 = len(c["batch"]) * rv.max_target * S.STATS_DTYPE.itemsize
+        for k in range(R):
+            o = rv.d_stats + k * rv.replica_stride - ws_r.data_ptr()
+            stk = ws_r[o:o + nst1].cpu().numpy().view(S.STATS_DTYPE).reshape(len(c["batch"]), rv.max_target)
+            served_all &= bool(np.all(stk["served"].sum(axis=2) == c["n_total"]))
+        S.destroy(rctx)
+        (rep_s,) = D.reduce_times([sum(rep_ms) / 1e3], device=dev)
+        rep_line = dict(R=R, value=R * dec_per_step * args.steps * world / rep_s, unit="decisions/s",
+                        ms_per_step=1e3 * rep_s / args.steps, per_replica_value=dec_per_step * args.steps / rep_s,
+                        round_ctas=R * (len(c["batch"]) + 1), seeds=f"{hex(rseed)} + k, k < {R}",
+                        launches_per_step=launches_rep,
+                        parity=dict(every_replica_served_each_sample_once_per_job_epoch=served_all,
+                                    note="replica-vs-oracle bit-exactness: tests/test_gpu_ods.py::test_replicas_*"),
+                        note="init_cache + replay_epochs of R independent instances of the workload in one "
+                             "context (one cooperative launch); L2 flushed between steps")
+        del ws_r_holder[:]
+
     # ---- e2e through the public API with host buffers (pinned), copies inside
     pin_prof = torch.from_numpy(prof_host.view(np.uint8).copy()).pin_memory()
     pin_res = torch.empty(d_res.numel(), dtype=torch.uint8).pin_memory()
@@ -451,6 +507,7 @@ def main():
             roofline=roof,
             mdp=dict(value=total_evals / mdp_s, unit="split-evals/s", dtype="f64", ms_per_step=mdp_ms_step,
                      roofline=mdp_roof),
+            replicas=rep_line,
             cpu_baseline=cpu,
             clocks=clk,
             gpu_launches=int(launches),

@@ -142,6 +142,13 @@ typedef struct {
     const uint32_t* target_epochs; /* host [n_jobs], >= 1; job departs after these     */
     uint64_t        cap_e, cap_d, cap_a; /* tier capacities in samples (Eqs. 5-7), sum <= N */
     uint64_t        seed;          /* all randomness derives from (seed, purpose, ...) R-O17 */
+    uint32_t        replicas;      /* R independent replay instances in this context (0 or 1:
+                                      one), replica k with seed + k, each with its own slice
+                                      of the workspace; 1..64, R x (n_jobs + 1) CTAs must be
+                                      co-resident (EINVAL otherwise); request_mode 1 needs
+                                      R = 1.  SURVEY §8(e): replicas fill the GPU with
+                                      independent replays (weak scaling inside one device). */
+    uint32_t        _pad0;
 } seneca_cache_config;
 
 /* Per job-epoch counters (R-O10; digest in DESIGN.md §3).  104 bytes.       */
@@ -178,9 +185,12 @@ typedef struct {
     uint64_t epoch[32];                 /* host mirror: current epoch of each job          */
     uint64_t consumed[32];              /* host mirror: samples consumed in current epoch  */
     uint32_t active_mask;               /* bit j set while job j has not departed          */
+    uint32_t replicas;                  /* R; every d_ pointer above is replica 0's --      */
+    uint64_t replica_stride;            /* replica k's is at + k * replica_stride bytes     */
 } seneca_state_view;
 
-/* Workspace size for cfg (bytes, 256-aligned pieces).  EINVAL on a bad cfg.   */
+/* Workspace size for cfg (bytes, 256-aligned pieces; replicas x one replica's).
+ * EINVAL on a bad cfg.                                                         */
 seneca_status seneca_state_bytes(const seneca_cache_config* cfg, size_t* bytes);
 
 /* init_cache (a warm start, R-O9): carve d_workspace (caller-owned, >= the
@@ -197,8 +207,9 @@ seneca_status seneca_init_cache(const seneca_cache_config* cfg, void* d_workspac
  * ids are requested (generated, or read from d_requested[x][0..need) when
  * request_mode = 1), misses are replaced by unseen cached samples tier by tier
  * A -> D -> E (§5.2 steps 1-4) and the response is written to
- * d_out_ids[x][s] / d_out_src[x][s] (x = position in h_jobs, row stride =
- * max batch size; src bits 0-1 tier 0 S 1 E 2 D 3 A, bit 2 substituted).
+ * d_out_ids[k][x][s] / d_out_src[k][x][s] (k = replica, x = position in
+ * h_jobs, row stride = max batch size; src bits 0-1 tier 0 S 1 E 2 D 3 A,
+ * bit 2 substituted).  Every replica plays the same jobs.
  * h_out_lens[x] = need (host, synchronous).  A job whose epoch ends is reset
  * (step 6) and departs after its target epoch.
  * Errors: EINVAL (bad/duplicate job, NULL outputs, d_requested given in mode 0
@@ -211,7 +222,7 @@ seneca_status seneca_ods_next_batch(seneca_ctx* ctx, const uint32_t* h_jobs, uin
 
 /* Replay whole rounds over all active jobs (request_mode 0 only) until every
  * job active at the call has completed n_epochs more epochs or departed.
- * d_transcript: NULL, or device [n_jobs][max_target][n_total] uint64 receiving
+ * d_transcript: NULL, or device [replicas][n_jobs][max_target][n_total] uint64 receiving
  * src<<32 | id at each delivery position.  *h_rounds = rounds executed.
  * ESTATE if no job is active or request_mode = 1.                            */
 seneca_status seneca_replay_epochs(seneca_ctx* ctx, uint32_t n_epochs, uint64_t* d_transcript,

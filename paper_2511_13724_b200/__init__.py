@@ -42,14 +42,17 @@ def results_to_numpy(d_res) -> np.ndarray:
 
 
 class ODSContext:
-    """One replay instance: a torch-owned workspace + a libseneca context."""
+    """A torch-owned workspace + a libseneca context: `replicas` independent
+    replay instances (replica k uses seed + k), played by the same launches.
+    Readback methods take the replica index (default 0)."""
 
     def __init__(self, n_total, batch, target, cap_e, cap_d, cap_a, seed, request_mode=0,
-                 device="cuda", stream=None):
+                 device="cuda", stream=None, replicas=1):
         torch = _torch()
         self.torch = torch
         self.cfg = seneca.make_config(int(n_total), list(batch), list(target), int(cap_e), int(cap_d),
-                                      int(cap_a), int(seed), request_mode)
+                                      int(cap_a), int(seed), request_mode, int(replicas))
+        self.R = int(replicas)
         self.N, self.J = int(n_total), len(batch)
         self.bmax = max(batch)
         self.max_target = max(target)
@@ -74,13 +77,17 @@ class ODSContext:
         return seneca.replay_rounds(self.ctx, n_rounds, transcript, self.stream)
 
     def new_transcript(self):
-        return self.torch.zeros((self.J, self.max_target, self.N), dtype=self.torch.int64, device=self.device)
+        """[J][max_target][N] (one replica) or [R][J][max_target][N] int64 zeros."""
+        shape = (self.J, self.max_target, self.N) if self.R == 1 else (self.R, self.J, self.max_target, self.N)
+        return self.torch.zeros(shape, dtype=self.torch.int64, device=self.device)
 
     def next_batch(self, jobs, requested=None):
+        """One round; ids/src are [n][Bmax] (one replica) or [R][n][Bmax]."""
         torch = self.torch
         n = len(jobs)
-        ids = torch.zeros((n, self.bmax), dtype=torch.int32, device=self.device)
-        src = torch.zeros((n, self.bmax), dtype=torch.uint8, device=self.device)
+        shape = (n, self.bmax) if self.R == 1 else (self.R, n, self.bmax)
+        ids = torch.zeros(shape, dtype=torch.int32, device=self.device)
+        src = torch.zeros(shape, dtype=torch.uint8, device=self.device)
         req = None
         if requested is not None:
             r = np.zeros((n, self.bmax), np.uint32)
@@ -99,9 +106,9 @@ class ODSContext:
     def profile(self, enable: int = 1):
         seneca.profile(self.ctx, enable)
 
-    def phase_cycles(self):
+    def phase_cycles(self, k=0):
         v = self.view()
-        return self._slice(v.d_phase_cycles, 256).cpu().numpy().view(np.uint64).copy()
+        return self._slice(self._rep(v, v.d_phase_cycles, k), 256).cpu().numpy().view(np.uint64).copy()
 
     def profile_read(self) -> dict:
         return seneca.profile_read(self.ctx)
@@ -114,12 +121,19 @@ class ODSContext:
     def view(self):
         return seneca.read_state(self.ctx)
 
-    def state(self):
-        """(tier codes uint8[N], seen uint8[J][N], cons uint8[J][N]) as numpy."""
+    @staticmethod
+    def _rep(v, ptr, k):
+        if not 0 <= k < v.replicas:
+            raise IndexError(f"replica {k} of {v.replicas}")
+        return ptr + k * v.replica_stride
+
+    def state(self, k=0):
+        """Replica k: (tier codes uint8[N], seen uint8[J][N], cons uint8[J][N]) as numpy."""
         v = self.view()
         W = v.words
 
         def bits(ptr, rows):
+            ptr = self._rep(v, ptr, k)
             raw = self._slice(ptr, rows * W * 4).cpu().numpy().view(np.uint32).reshape(rows, W)
             b = np.unpackbits(raw.view(np.uint8).reshape(rows, W * 4), axis=1, bitorder="little")
             return b[:, :self.N]
@@ -131,10 +145,11 @@ class ODSContext:
         tier[a == 1] = 3
         return tier, bits(v.d_seen, self.J), bits(v.d_cons, self.J)
 
-    def stats(self):
+    def stats(self, k=0):
+        """Replica k: (per job-epoch STATS_DTYPE [J][max_target], evicted, refilled)."""
         v = self.view()
-        raw = self._slice(v.d_stats, self.J * v.max_target * STATS_DTYPE.itemsize).cpu().numpy()
+        raw = self._slice(self._rep(v, v.d_stats, k), self.J * v.max_target * STATS_DTYPE.itemsize).cpu().numpy()
         st = raw.view(STATS_DTYPE).reshape(self.J, v.max_target)
-        ev = int(self._slice(v.d_evicted, 8).cpu().numpy().view(np.uint64)[0])
-        rf = int(self._slice(v.d_refilled, 8).cpu().numpy().view(np.uint64)[0])
+        ev = int(self._slice(self._rep(v, v.d_evicted, k), 8).cpu().numpy().view(np.uint64)[0])
+        rf = int(self._slice(self._rep(v, v.d_refilled, k), 8).cpu().numpy().view(np.uint64)[0])
         return st, ev, rf

@@ -48,6 +48,7 @@ namespace {
 
 constexpr uint32_t T_S = 0, T_E = 1, T_D = 2, T_A = 3, SUBST = 4;
 constexpr uint32_t kMaxJobs = 32;
+constexpr uint32_t kMaxReplicas = 64;        // independent replay instances per context
 constexpr uint32_t kMaxBatch = 4096;
 constexpr uint32_t kThreads = 512;           // CTA size of the persistent kernel
 constexpr uint32_t kBlockShift = 7;          // 128 ids (4 words, one 16-B vector) per count block
@@ -102,6 +103,13 @@ struct Lay {
     uint32_t *bar;                   // [4] signals: u64 {job phases done | evictions pushed << 32},
                                      //     maintain rounds applied, eviction ring position
     unsigned long long *phase;       // [32] accumulated cycles per phase (see seneca.h)
+    uint64_t seed;                   // this replica's seed (cfg seed + replica index)
+};
+
+// Per-replica layouts: a kernel parameter (constant bank), indexed by the CTA's
+// replica -- no per-CTA copy, and the compiler may hoist every field.
+struct Lays {
+    Lay r[kMaxReplicas];
 };
 
 struct Launch {
@@ -118,7 +126,9 @@ struct Launch {
     uint32_t* out_ids;
     uint8_t* out_src;
     const uint32_t* requested;       // mode 1: [row][out_stride]
-    unsigned long long* transcript;  // [J][maxT][N] or null
+    unsigned long long* transcript;  // [replica][J][maxT][N] or null
+    uint64_t out_rep;                // elements of out_ids / out_src per replica
+    uint64_t tr_rep;                 // elements of transcript per replica
 };
 
 __device__ __forceinline__ uint32_t ldcg(const uint32_t* p) { return __ldcg(p); }
@@ -263,6 +273,7 @@ struct JobSmem {
     uint32_t perm_seen;   // epoch+1 whose permutation was observed published (0: none)
     float dens;           // unseen fraction observed by the last walk step (window sizing)
     uint32_t npush;       // evictions pushed by this job this round
+    uint32_t rep;         // replica of this CTA
     // prefetch of the next walk window (R-O1 walk, see job_walk_prefetched)
     uint32_t pf_state;    // 0 none, 1 list window requested, 2 seen chunks requested
     uint32_t pf_buf, pf_epoch, pf_base, pf_len, pf_vlen;
@@ -514,7 +525,7 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
     const uint32_t need = S.need;
     uint32_t* seen_j = L.seen + (size_t)j * C.NW;
     uint32_t* cons_j = L.cons + (size_t)j * C.NW;
-    const size_t row = (size_t)P.row_of_job[j] * P.out_stride;
+    const size_t row = S.rep * P.out_rep + (size_t)P.row_of_job[j] * P.out_stride;
     if (tid < 3) S.hits[tid] = 0;       // the pool totals S.tot persist across rounds in shared memory
     if (tid == 0) S.npush = 0;
     __syncthreads();
@@ -573,7 +584,7 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
             const uint32_t tt = u < k0 ? 0u : (u < k0 + k1 ? 1u : 2u);
             const uint32_t ul = u - (tt == 0 ? 0u : (tt == 1 ? k0 : k0 + k1));
             const uint32_t t = tt == 0 ? T_A : (tt == 1 ? T_D : T_E);
-            const uint64_t key = derive_key(C.seed, PUR_SUB, j, r, t);
+            const uint64_t key = derive_key(L.seed, PUR_SUB, j, r, t);
             const uint32_t rank = perm_apply(key, perm_domain(S.tot[tt]), ul);
             const uint32_t id = pool_select(L, C, j * 3 + tt, t, j, s_pre + tt * C.NS, rank);
             const uint32_t s = s_miss[u];
@@ -634,7 +645,7 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
     // pushed for eviction at the round end (R-O5).  The per-tier counters follow
     // from the phase counts: hits per tier, k_t substitutes, m - q storage.
     unsigned long long dig = 0;
-    unsigned long long* trow = P.transcript ? P.transcript + ((size_t)j * C.maxT + e) * C.N : nullptr;
+    unsigned long long* trow = P.transcript ? P.transcript + S.rep * P.tr_rep + ((size_t)j * C.maxT + e) * C.N : nullptr;
     const uint32_t lane = tid & 31;
     for (uint32_t s = tid; s < need; s += T) {
         const uint32_t i = s_oid[s];
@@ -691,7 +702,7 @@ struct MaintSmem {
 __device__ void maint_refill_select(const Lay& L, const Cfg& C, MaintSmem& M, const uint32_t* s_pre, uint64_t r,
                                     uint32_t u0, uint32_t u1) {
     if (u1 <= u0) return;
-    const uint64_t key = derive_key(C.seed, PUR_REFILL, 0, r, 0);
+    const uint64_t key = derive_key(L.seed, PUR_REFILL, 0, r, 0);
     const PermDomain dom = perm_domain(M.PS);
     uint32_t* fill = L.fill_list + (size_t)(r & 1) * C.FL;
     for (uint32_t u = u0 + threadIdx.x; u < u1; u += blockDim.x)
@@ -789,14 +800,18 @@ __device__ void job_take_refills(const Lay& L, const Cfg& C, JobSmem& S, uint32_
 }
 
 // ------------------------------------------------------------------ the persistent round kernel
+// Grid: (J + 1) CTAs per replica; replicas are independent replays (their own
+// workspace slice and seed) that share nothing but the launch.
 __global__ void __launch_bounds__(kThreads, 1)
-ods_rounds(Lay L, Cfg C, Launch P) {
+ods_rounds(const __grid_constant__ Lays LS, const __grid_constant__ Cfg C, const __grid_constant__ Launch P) {
     extern __shared__ __align__(16) uint32_t smem[];
     __shared__ JobSmem S;
     __shared__ MaintSmem M;
     __shared__ uint32_t s_n[kMaxJobs], s_e[kMaxJobs], s_active;
     const uint32_t tid = threadIdx.x;
-    const uint32_t cta = blockIdx.x;
+    const uint32_t rep = blockIdx.x / (C.J + 1);
+    const uint32_t cta = blockIdx.x - rep * (C.J + 1);
+    const Lay& L = LS.r[rep];
     const bool is_maint = cta == C.J;
     const uint32_t j = cta;
     __shared__ PhaseTimer TM;
@@ -834,6 +849,7 @@ ods_rounds(Lay L, Cfg C, Launch P) {
         S.cur_buf = jd.cur_buf; S.nxt_buf = jd.nxt_buf; S.cursor = jd.cursor;
         S.cur_len = jd.cur_len; S.nxt_len = jd.nxt_len; S.recount = jd.recount;
         S.perm_seen = 0;
+        S.rep = rep;
         S.dens = 1.0f;
         S.pf_state = 0;
     }
@@ -1026,7 +1042,8 @@ ods_rounds(Lay L, Cfg C, Launch P) {
 // ------------------------------------------------------------------ one-off kernels
 // pi_j,e for every (job, epoch), epoch-major, in chunks; the CTA finishing the
 // last chunk of (j, e) publishes perm_ready[j][e] (release).
-__global__ void ods_perm_all(Lay L, Cfg C, uint32_t chunk) {
+__global__ void ods_perm_all(const __grid_constant__ Lays LS, const __grid_constant__ Cfg C, uint32_t chunk) {
+    const Lay& L = LS.r[blockIdx.y];
     const uint32_t per = (C.N + chunk - 1) / chunk;
     const uint64_t total = (uint64_t)C.maxT * C.J * per;
     const PermDomain dom = perm_domain(C.N);
@@ -1036,7 +1053,7 @@ __global__ void ods_perm_all(Lay L, Cfg C, uint32_t chunk) {
         const uint32_t j = (uint32_t)((c / per) % C.J);
         const uint32_t part = (uint32_t)(c % per);
         if (e >= C.target[j]) continue;
-        const uint64_t key = derive_key(C.seed, PUR_REQ, j, e, 0);
+        const uint64_t key = derive_key(L.seed, PUR_REQ, j, e, 0);
         uint32_t* out = L.perms + ((size_t)j * C.maxT + e) * C.Nrow;
         const uint32_t lo = part * chunk, hi = min(lo + chunk, C.N);
         for (uint32_t pos = lo + threadIdx.x; pos < hi; pos += blockDim.x) out[pos] = perm_apply(key, dom, pos);
@@ -1055,8 +1072,10 @@ __global__ void ods_perm_all(Lay L, Cfg C, uint32_t chunk) {
 }
 
 // warm start (R-O9): positions [0,cap_A) -> A, next cap_D -> D, next cap_E -> E
-__global__ void ods_init_tiers(Lay L, Cfg C, uint32_t cap_e, uint32_t cap_d) {
-    const uint64_t key = derive_key(C.seed, PUR_INIT, 0, 0, 0);
+__global__ void ods_init_tiers(const __grid_constant__ Lays LS, const __grid_constant__ Cfg C, uint32_t cap_e,
+                               uint32_t cap_d) {
+    const Lay& L = LS.r[blockIdx.y];
+    const uint64_t key = derive_key(L.seed, PUR_INIT, 0, 0, 0);
     const PermDomain dom = perm_domain(C.N);
     const uint32_t total = C.cap_a + cap_d + cap_e;
     for (uint32_t pos = blockIdx.x * blockDim.x + threadIdx.x; pos < total; pos += gridDim.x * blockDim.x) {
@@ -1070,7 +1089,8 @@ __global__ void ods_init_tiers(Lay L, Cfg C, uint32_t cap_e, uint32_t cap_d) {
 // Pool counts of every job and of the storage pool (init): one CTA of 128
 // threads per superblock (one word each; 4 threads per 128-id block).
 __global__ void __launch_bounds__(128)
-ods_recount_all(Lay L, Cfg C) {
+ods_recount_all(const __grid_constant__ Lays LS, const __grid_constant__ Cfg C) {
+    const Lay& L = LS.r[blockIdx.z];
     const uint32_t sblk = blockIdx.x, pool = blockIdx.y;    // pool < 3J: (j, tier); == 3J: storage
     const uint32_t w = sblk * 128 + threadIdx.x;
     uint32_t word;
@@ -1103,7 +1123,8 @@ ods_recount_all(Lay L, Cfg C) {
     }
 }
 
-__global__ void ods_init_jobs(Lay L, Cfg C) {
+__global__ void ods_init_jobs(const __grid_constant__ Lays LS, const __grid_constant__ Cfg C) {
+    const Lay& L = LS.r[blockIdx.x];
     const uint32_t j = threadIdx.x;
     if (j < C.J) {
         JobDev& jd = L.jobs[j];
@@ -1112,7 +1133,9 @@ __global__ void ods_init_jobs(Lay L, Cfg C) {
 }
 
 // caller-supplied requests (mode 1): range, duplicates within the row, seen
-__global__ void ods_validate_requests(Lay L, Cfg C, Launch P) {
+__global__ void ods_validate_requests(const __grid_constant__ Lays LS, const __grid_constant__ Cfg C,
+                                      const __grid_constant__ Launch P) {
+    const Lay& L = LS.r[0];                     // caller-supplied requests: one replica
     extern __shared__ uint32_t s_row[];
     uint32_t x = 0;
     uint32_t j = 0xffffffffu;
@@ -1150,7 +1173,10 @@ using namespace seneca;
 
 struct seneca_ctx {
     Cfg C;
-    Lay L;
+    Lay L;                 // replica 0
+    Lays LS;               // every replica
+    uint32_t R;            // replicas
+    size_t rep_stride;     // workspace bytes per replica
     uint32_t mode;
     uint64_t cap_e, cap_d;
     uint64_t e[kMaxJobs], n[kMaxJobs];
@@ -1184,6 +1210,10 @@ seneca_status check_cfg(const seneca_cache_config* cfg) {
             set_error("target_epochs[%u] must be in [1, 1e5]", j); return SENECA_EINVAL;
         }
     }
+    if (cfg->replicas > kMaxReplicas) { set_error("replicas must be <= %u", kMaxReplicas); return SENECA_EINVAL; }
+    if (cfg->replicas > 1 && cfg->request_mode != 0) {
+        set_error("caller-supplied requests (request_mode 1) need replicas <= 1"); return SENECA_EINVAL;
+    }
     if (cfg->cap_e > cfg->n_total || cfg->cap_d > cfg->n_total || cfg->cap_a > cfg->n_total ||
         cfg->cap_e + cfg->cap_d + cfg->cap_a > cfg->n_total) {
         set_error("cap_e + cap_d + cap_a exceeds n_total"); return SENECA_EINVAL;
@@ -1194,7 +1224,8 @@ seneca_status check_cfg(const seneca_cache_config* cfg) {
 struct Sizes {
     Cfg C;
     size_t off[40];
-    size_t total;
+    size_t total;          // one replica
+    uint32_t R;
 };
 
 Sizes compute_sizes(const seneca_cache_config* cfg) {
@@ -1244,11 +1275,13 @@ Sizes compute_sizes(const seneca_cache_config* cfg) {
         at += align256(sz[k]);
     }
     z.total = at;
+    z.R = cfg->replicas ? cfg->replicas : 1;
     return z;
 }
 
-Lay carve(const Sizes& z, char* base) {
+Lay carve(const Sizes& z, char* base, uint64_t seed) {
     Lay L;
+    L.seed = seed;
     L.bm_e = (uint32_t*)(base + z.off[0]);
     L.bm_d = (uint32_t*)(base + z.off[1]);
     L.bm_a = (uint32_t*)(base + z.off[2]);
@@ -1324,10 +1357,12 @@ seneca_status launch_rounds(seneca_ctx* c, uint64_t R, uint32_t jobs_mask, const
     P.out_src = out_src;
     P.requested = d_requested;
     P.transcript = transcript;
+    P.out_rep = (uint64_t)out_stride * (row_of_job ? __builtin_popcount(jobs_mask) : c->C.J);
+    P.tr_rep = (uint64_t)c->C.J * c->C.maxT * c->C.N;
     P.timing = c->profiling;
     if (c->mode == 1) {
         timed(c, K_VALIDATE, st, [&] {
-            ods_validate_requests<<<__builtin_popcount(jobs_mask), 256, (size_t)c->C.Bmax * 4, st>>>(c->L, c->C, P);
+            ods_validate_requests<<<__builtin_popcount(jobs_mask), 256, (size_t)c->C.Bmax * 4, st>>>(c->LS, c->C, P);
         });
         SENECA_CUDA_TRY(cudaGetLastError());
         uint32_t err = 0;
@@ -1339,11 +1374,12 @@ seneca_status launch_rounds(seneca_ctx* c, uint64_t R, uint32_t jobs_mask, const
             return SENECA_EPROTO;
         }
     }
-    SENECA_CUDA_TRY(cudaMemsetAsync(c->L.bar, 0, 16, st));
-    void* args[] = {&c->L, &c->C, &P};
+    SENECA_CUDA_TRY(cudaMemset2DAsync(c->L.bar, c->rep_stride, 0, 16, c->R, st));
+    void* args[] = {&c->LS, &c->C, &P};
     cudaError_t le = cudaSuccess;
     timed(c, K_ROUNDS, st, [&] {
-        le = cudaLaunchCooperativeKernel((void*)ods_rounds, dim3(c->C.J + 1), dim3(kThreads), args, c->round_smem, st);
+        le = cudaLaunchCooperativeKernel((void*)ods_rounds, dim3((c->C.J + 1) * c->R), dim3(kThreads), args,
+                                         c->round_smem, st);
     });
     if (le != cudaSuccess) return cuda_status(le, "cudaLaunchCooperativeKernel(ods_rounds)");
     // host mirror of the data-independent schedule
@@ -1372,7 +1408,8 @@ extern "C" seneca_status seneca_state_bytes(const seneca_cache_config* cfg, size
     seneca_status s = check_cfg(cfg);
     if (s) return s;
     if (!bytes) { set_error("NULL bytes"); return SENECA_EINVAL; }
-    *bytes = compute_sizes(cfg).total;
+    const Sizes z = compute_sizes(cfg);
+    *bytes = z.total * z.R;
     return SENECA_OK;
 }
 
@@ -1383,7 +1420,9 @@ extern "C" seneca_status seneca_init_cache(const seneca_cache_config* cfg, void*
     if (!out || !d_workspace) { set_error("NULL workspace or out"); return SENECA_EINVAL; }
     if ((uintptr_t)d_workspace & 255) { set_error("workspace must be 256-byte aligned"); return SENECA_EINVAL; }
     Sizes z = compute_sizes(cfg);
-    if (ws_bytes < z.total) { set_error("workspace %zu bytes < required %zu", ws_bytes, z.total); return SENECA_ENOSPC; }
+    if (ws_bytes < z.total * z.R) {
+        set_error("workspace %zu bytes < required %zu", ws_bytes, z.total * z.R); return SENECA_ENOSPC;
+    }
     const size_t o_win = ((size_t)4 * z.C.Bmax + 6 * z.C.NS + 3) & ~(size_t)3;
     const size_t o_wseen = o_win + kWinMax;
     const size_t round_smem = (o_wseen + 4 * kWinMax) * 4 + z.C.Bmax;
@@ -1391,7 +1430,10 @@ extern "C" seneca_status seneca_init_cache(const seneca_cache_config* cfg, void*
     seneca_ctx* c = new (std::nothrow) seneca_ctx();
     if (!c) { set_error("out of host memory"); return SENECA_EINVAL; }
     c->C = z.C;
-    c->L = carve(z, (char*)d_workspace);
+    c->R = z.R;
+    c->rep_stride = z.total;
+    for (uint32_t k = 0; k < z.R; ++k) c->LS.r[k] = carve(z, (char*)d_workspace + k * z.total, cfg->seed + k);
+    c->L = c->LS.r[0];
     c->mode = cfg->request_mode;
     c->cap_e = cfg->cap_e;
     c->cap_d = cfg->cap_d;
@@ -1402,30 +1444,49 @@ extern "C" seneca_status seneca_init_cache(const seneca_cache_config* cfg, void*
 #define INIT_TRY(expr) do { cudaError_t _e = (expr); if (_e != cudaSuccess) { delete c; return cuda_status(_e, #expr); } } while (0)
     INIT_TRY(cudaFuncSetAttribute(ods_rounds, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     INIT_TRY(cudaFuncSetAttribute(ods_validate_requests, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+    {   // the cooperative round launch needs every replica's CTAs co-resident
+        int per_sm = 0;
+        INIT_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ods_rounds, kThreads, round_smem));
+        const uint64_t slots = (uint64_t)per_sm * num_sms();
+        if ((uint64_t)(z.C.J + 1) * z.R > slots) {
+            set_error("%u replicas x %u CTAs exceed the %llu co-resident CTA slots", z.R, z.C.J + 1,
+                      (unsigned long long)slots);
+            delete c;
+            return SENECA_EINVAL;
+        }
+    }
     INIT_TRY(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
     INIT_TRY(cudaEventCreateWithFlags(&c->ev_init, cudaEventDisableTiming));
     INIT_TRY(cudaEventCreate(&c->ev_a));
     INIT_TRY(cudaEventCreate(&c->ev_b));
-    INIT_TRY(cudaMemsetAsync(d_workspace, 0, z.total, st));
+    INIT_TRY(cudaMemsetAsync(d_workspace, 0, z.total * z.R, st));
     {
         const uint32_t total = (uint32_t)(cfg->cap_a + cfg->cap_d + cfg->cap_e);
         const uint32_t blocks = std::max<uint32_t>(1, std::min<uint32_t>((total + 255) / 256, num_sms() * 8));
         timed(c, K_INIT, st, [&] {
-            ods_init_tiers<<<blocks, 256, 0, st>>>(c->L, c->C, (uint32_t)cfg->cap_e, (uint32_t)cfg->cap_d);
+            ods_init_tiers<<<dim3(blocks, c->R), 256, 0, st>>>(c->LS, c->C, (uint32_t)cfg->cap_e, (uint32_t)cfg->cap_d);
         });
         INIT_TRY(cudaGetLastError());
-        timed(c, K_RECOUNT, st, [&] { ods_recount_all<<<dim3(c->C.NS, 3 * c->C.J + 1), 128, 0, st>>>(c->L, c->C); });
+        timed(c, K_RECOUNT, st, [&] {
+            ods_recount_all<<<dim3(c->C.NS, 3 * c->C.J + 1, c->R), 128, 0, st>>>(c->LS, c->C);
+        });
         INIT_TRY(cudaGetLastError());
-        ods_init_jobs<<<1, 32, 0, st>>>(c->L, c->C);
+        ods_init_jobs<<<c->R, 32, 0, st>>>(c->LS, c->C);
         c->launches++;
         INIT_TRY(cudaGetLastError());
     }
-    // every epoch's permutation, generated on a side stream; rounds wait on the flags
+    // every epoch's permutation.  One replica: on a side stream, overlapping the
+    // rounds, which wait on the per-(job, epoch) flags.  Several replicas may fill
+    // every SM with round CTAs, so their permutations are generated up front on
+    // the caller's stream (never a round CTA spinning on a generator that cannot
+    // get an SM).
     INIT_TRY(cudaEventRecord(c->ev_init, st));
     INIT_TRY(cudaStreamWaitEvent(c->side, c->ev_init, 0));
     if (c->mode == 0) {
         const uint32_t chunk = 16384;
-        timed(c, K_PERM, c->side, [&] { ods_perm_all<<<num_sms() * 4, 512, 0, c->side>>>(c->L, c->C, chunk); });
+        cudaStream_t ps = c->R == 1 ? c->side : st;
+        const uint32_t gx = std::max<uint32_t>(1, (uint32_t)num_sms() * 4 / c->R);
+        timed(c, K_PERM, ps, [&] { ods_perm_all<<<dim3(gx, c->R), 512, 0, ps>>>(c->LS, c->C, chunk); });
         INIT_TRY(cudaGetLastError());
     }
 #undef INIT_TRY
@@ -1549,15 +1610,19 @@ extern "C" seneca_status seneca_read_state(const seneca_ctx* c, seneca_state_vie
     v->round = c->r;
     for (uint32_t j = 0; j < c->C.J; ++j) { v->epoch[j] = c->e[j]; v->consumed[j] = c->n[j]; }
     v->active_mask = c->active;
+    v->replicas = c->R;
+    v->replica_stride = c->rep_stride;
     return SENECA_OK;
 }
 
 extern "C" seneca_status seneca_sync_status(seneca_ctx* c, void* stream) {
     if (!c) { set_error("bad arguments"); return SENECA_EINVAL; }
-    uint32_t err = 0;
-    SENECA_CUDA_TRY(cudaMemcpyAsync(&err, c->L.err, 4, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+    uint32_t err[kMaxReplicas] = {0};
+    SENECA_CUDA_TRY(cudaMemcpy2DAsync(err, 4, c->L.err, c->rep_stride, 4, c->R, cudaMemcpyDeviceToHost,
+                                      (cudaStream_t)stream));
     SENECA_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
-    if (err) { set_error("device consistency check failed (flags 0x%x)", err); return SENECA_ESTATE; }
+    for (uint32_t k = 0; k < c->R; ++k)
+        if (err[k]) { set_error("device consistency check failed (replica %u, flags 0x%x)", k, err[k]); return SENECA_ESTATE; }
     return SENECA_OK;
 }
 

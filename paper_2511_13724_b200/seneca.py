@@ -54,6 +54,7 @@ class CacheConfig(C.Structure):
         ("n_total", C.c_uint64), ("n_jobs", C.c_uint32), ("request_mode", C.c_uint32),
         ("batch_size", C.POINTER(C.c_uint32)), ("target_epochs", C.POINTER(C.c_uint32)),
         ("cap_e", C.c_uint64), ("cap_d", C.c_uint64), ("cap_a", C.c_uint64), ("seed", C.c_uint64),
+        ("replicas", C.c_uint32), ("_pad0", C.c_uint32),
     ]
 
 
@@ -70,7 +71,7 @@ class StateView(C.Structure):
         ("d_seen", C.c_void_p), ("d_cons", C.c_void_p), ("d_stats", C.c_void_p),
         ("d_evicted", C.c_void_p), ("d_refilled", C.c_void_p), ("d_phase_cycles", C.c_void_p),
         ("round", C.c_uint64), ("epoch", C.c_uint64 * 32), ("consumed", C.c_uint64 * 32),
-        ("active_mask", C.c_uint32),
+        ("active_mask", C.c_uint32), ("replicas", C.c_uint32), ("replica_stride", C.c_uint64),
     ]
 
 
@@ -179,11 +180,12 @@ def profiles_from_columns(cols: dict) -> np.ndarray:
 
 
 # ------------------------------------------------------------------ ODS
-def make_config(n_total, batch, target, cap_e, cap_d, cap_a, seed, request_mode=0):
+def make_config(n_total, batch, target, cap_e, cap_d, cap_a, seed, request_mode=0, replicas=1):
     b = (C.c_uint32 * len(batch))(*batch)
     t = (C.c_uint32 * len(target))(*target)
     cfg = CacheConfig(n_total=n_total, n_jobs=len(batch), request_mode=request_mode,
-                      batch_size=b, target_epochs=t, cap_e=cap_e, cap_d=cap_d, cap_a=cap_a, seed=seed)
+                      batch_size=b, target_epochs=t, cap_e=cap_e, cap_d=cap_d, cap_a=cap_a, seed=seed,
+                      replicas=replicas)
     cfg._keep = (b, t)
     return cfg
 

@@ -95,3 +95,45 @@ def test_state_bytes_scale(lib):
     nbytes = S.state_bytes(cfg)
     # 3 + 2J bitmaps (R-O14) + 3 permutation/lap lists per job dominate; fits easily in 180 GB
     assert 1.3e9 < nbytes < 2e9
+
+
+def test_ctypes_layouts_match_c_header(lib, tmp_path):
+    """sizeof/offsetof of every C-ABI struct as gcc sees include/seneca.h ==
+    the ctypes mirror the binding passes across the boundary."""
+    import subprocess
+    probe = tmp_path / "probe.c"
+    structs = {"seneca_cache_config": S.CacheConfig, "seneca_state_view": S.StateView,
+               "seneca_job_epoch_stats": S.JobEpochStats, "seneca_mdp_profile": S.MdpProfile,
+               "seneca_mdp_result": S.MdpResult, "seneca_kernel_stat": S.KernelStat}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "seneca.h"', "int main(void) {"]
+    for cname, ct in structs.items():
+        lines.append(f'printf("{cname} sizeof %zu\\n", sizeof({cname}));')
+        for f in ct._fields_:
+            if f[0].startswith("_pad"):
+                continue
+            lines.append(f'printf("{cname} {f[0]} %zu\\n", offsetof({cname}, {f[0]}));')
+    lines.append("return 0; }")
+    probe.write_text("\n".join(lines))
+    exe = tmp_path / "probe"
+    subprocess.run(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"), str(probe), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split("\n")
+    got = {tuple(l.split()[:2]): int(l.split()[2]) for l in out if l}
+    for cname, ct in structs.items():
+        assert got[(cname, "sizeof")] == ctypes.sizeof(ct), cname
+        for f in ct._fields_:
+            if not f[0].startswith("_pad"):
+                assert got[(cname, f[0])] == getattr(ct, f[0]).offset, (cname, f[0])
+
+
+def test_replicas_workspace_and_arguments(lib):
+    c = synth.ods_config("toy")
+    caps = S.split_capacities(c["n_total"], c["s_data"], c["m_num"], c["m_den"], c["cache_bytes"], *c["split"])
+    one = S.state_bytes(S.make_config(c["n_total"], c["batch"], c["target"], caps[0], caps[1], caps[2], 1))
+    for r in (0, 1, 2, 7, 64):
+        cfg = S.make_config(c["n_total"], c["batch"], c["target"], caps[0], caps[1], caps[2], 1, replicas=r)
+        assert S.state_bytes(cfg) == max(r, 1) * one          # one 256-aligned slice per replica
+    for r, mode in ((65, 0), (2, 1)):                          # too many; caller-supplied requests need R = 1
+        cfg = S.make_config(c["n_total"], c["batch"], c["target"], caps[0], caps[1], caps[2], 1, mode, replicas=r)
+        with pytest.raises(S.SenecaError) as ei:
+            S.state_bytes(cfg)
+        assert ei.value.status == S.EINVAL

@@ -239,3 +239,64 @@ def test_determinism_and_launch_count():
         outs.append(g.stats()[0].tobytes())
         assert g.launches() > 0
     assert outs[0] == outs[1]
+
+
+# ---------------------------------------------------------------- replicas
+def compare_replica(o, g, k, tr_k=None):
+    st_o, ev_o, rf_o = o.stats()
+    st_g, ev_g, rf_g = g.stats(k)
+    assert (ev_g, rf_g) == (ev_o, rf_o), k
+    assert st_g.tobytes() == st_o.tobytes(), k
+    for a, b in zip(g.state(k), o.state()):
+        np.testing.assert_array_equal(a, b)
+    if tr_k is not None:
+        assert np.array_equal(tr_k.cpu().numpy().view(np.uint64), o.transcript()), k
+
+
+@pytest.mark.parametrize("name,scale,R", [("toy", 1, 48), ("imagenet1k", 64, 4), ("openimages", 64, 3)])
+def test_replicas_match_independent_oracles(name, scale, R):
+    """R replicas in one context == R independent oracle replays with seeds
+    seed + k (every decision, bitmap and counter), including a launch that fills
+    the GPU with round CTAs (toy: 48 x 3 CTAs)."""
+    seed = 3
+    c = synth.ods_config(name, scale=scale, seed=seed)
+    ce, cd, ca = caps_of(c)
+    g = P.ODSContext(c["n_total"], c["batch"], c["target"], ce, cd, ca, seed, replicas=R)
+    tr = g.new_transcript()
+    rounds = g.replay_epochs(max(c["target"]), tr)
+    torch.cuda.synchronize()
+    g.sync()
+    for k in range(R):
+        o = O.ODS(c["n_total"], c["batch"], c["target"], ce, cd, ca, seed + k, transcript=True)
+        assert o.replay_epochs(max(c["target"])) == rounds
+        compare_replica(o, g, k, tr[k])
+
+
+def test_replicas_next_batch():
+    n, batch, target, R = 600, [16, 40, 9], [2, 1, 2], 3
+    g = P.ODSContext(n, batch, target, 60, 50, 90, 21, replicas=R)
+    oracles = [O.ODS(n, batch, target, 60, 50, 90, 21 + k, transcript=False) for k in range(R)]
+    st = synth.Stream(5)
+    for _ in range(120):
+        _, _, _, act = oracles[0].job_state()
+        live = [j for j in range(3) if act[j]]
+        if not live:
+            break
+        pick = [j for j in live if st.uniform(1)[0] < 0.6] or live[-1:]
+        ids_g, src_g, lens_g = g.next_batch(pick)
+        torch.cuda.synchronize()
+        assert ids_g.shape == (R, len(pick), max(batch))
+        for k, o in enumerate(oracles):
+            rc, ids_o, src_o, lens_o = o.round(pick)
+            assert rc == 0 and list(lens_o) == lens_g
+            for x, L_ in enumerate(lens_g):
+                assert np.array_equal(ids_g[k, x, :L_].cpu().numpy().view(np.uint32), ids_o[x, :L_])
+                assert np.array_equal(src_g[k, x, :L_].cpu().numpy(), src_o[x, :L_])
+    for k, o in enumerate(oracles):
+        compare_replica(o, g, k)
+
+
+def test_replicas_that_cannot_be_co_resident_are_rejected():
+    with pytest.raises(S.SenecaError) as ei:
+        P.ODSContext(1000, [32, 32], [1, 1], 10, 10, 10, 1, replicas=64)      # 64 x 3 CTAs > 148 SMs
+    assert ei.value.status == S.EINVAL
