@@ -226,6 +226,20 @@ def algorithmic_bytes(name, info):
     return 0
 
 
+NCU_TRAFFIC = os.path.join(ROOT, "profiles", "r1", "ncu_traffic.json")
+
+
+def ncu_traffic(key):
+    """DRAM bytes (read + write) of one launch, from the committed `ncu --set full`
+    capture of the same launch (tools/measure.sh -> tools/ncu_summary.py), or None."""
+    try:
+        t = json.load(open(NCU_TRAFFIC))
+    except (OSError, ValueError):
+        return None
+    e = t.get(key)
+    return None if e is None else e["dram_bytes_per_launch"]
+
+
 def roofline_for(name, k, info, hbm_peak, peak_src, traffic=None):
     bpl = algorithmic_bytes(name, info)
     avg_s = (k["avg_us"] or 0.0) / 1e6
@@ -275,14 +289,20 @@ def main():
         if world > 1:
             torch.distributed.barrier()
 
-    def one_step(profile=False, timed=None):
+    def one_step(profile=False, ev=None):
+        # MDP first: its launch is queued behind a short device sleep so the
+        # host's enqueue latency is not inside its events; the replay follows
+        # (with profiling on, its launches are host-synchronised).
+        if ev is not None:
+            torch.cuda._sleep(200_000)                              # ~0.1 ms, before the first event
+            ev[0].record(stream)
+        S.mdp_sweep(d_prof, args.mdp_profiles, args.mdp_grid_step, d_res, d_grid, stream)
+        if ev is not None:
+            ev[1].record(stream)
         ctx = S.init_cache(cfg, ws, ws_bytes, stream)
         if profile:
-            S.profile(ctx, 1)
+            S.profile(ctx, 1)                                      # event-timed launches only
         rounds = S.replay_epochs(ctx, max(c["target"]), None, stream)
-        if timed is not None:
-            timed[1].record(stream)
-        S.mdp_sweep(d_prof, args.mdp_profiles, args.mdp_grid_step, d_res, d_grid, stream)
         return ctx, rounds
 
     # ---- warm-up
@@ -302,13 +322,12 @@ def main():
         barrier()
         torch.cuda.synchronize(dev)
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-        ev[0].record(stream)
-        ctx, rounds = one_step(not args.no_profile, (ev, ev[1]))
+        ctx, rounds = one_step(not args.no_profile, ev)
         ev[2].record(stream)
         torch.cuda.synchronize(dev)
         barrier()
-        ods_ms.append(ev[0].elapsed_time(ev[1]))
-        mdp_ms.append(ev[1].elapsed_time(ev[2]))
+        mdp_ms.append(ev[0].elapsed_time(ev[1]))
+        ods_ms.append(ev[1].elapsed_time(ev[2]))
         launches += S.launch_count(ctx) + 1
         rounds_tot += rounds
         for k, v in S.profile_read(ctx).items():
@@ -331,20 +350,6 @@ def main():
     st_raw = st_raw.reshape(len(c["batch"]), v.max_target)
     served_ok = bool(np.all(st_raw["served"].sum(axis=2) == c["n_total"]))
     parity["ods_served_per_job_epoch_equals_N"] = served_ok
-    ph = ws[v.d_phase_cycles - ws.data_ptr():v.d_phase_cycles - ws.data_ptr() + 256].cpu().numpy().view(np.uint64)
-    ph_names = {0: "job_epoch_start", 1: "job_classify", 8: "job_subst_prefix", 9: "job_subst_ranks_locate",
-                2: "job_subst_apply", 10: "job_storage_deferral", 11: "job_respond_loop", 3: "job_respond_stats",
-                4: "job_wait_maint", 5: "job_advance", 12: "job_walk_prefetched_step", 13: "job_walk_rest",
-                14: "job_prefetch_issue", 6: "job_unused",
-                16: "maint_spec_prefix", 17: "maint_spec_refill_ranks", 18: "maint_barrier1_wait",
-                19: "maint_evict_decide", 20: "maint_apply", 21: "maint_barrier2_wait"}
-    phase_share = {}
-    for base in (0, 16):
-        keys = [k for k in ph_names if base <= k < base + 16]
-        tot = float(sum(ph[k] for k in keys))
-        for k in keys:
-            phase_share[ph_names[k]] = round(float(ph[k]) / tot, 4) if tot else None
-    phase_share["walk_steps_per_round"] = round(float(ph[7]) / max(1, rounds_tot / args.steps), 3)
     if os.path.exists(gold_path):
         gold = json.load(open(gold_path))
         ok = all(int(st_raw[j, e]["digest"]) == int(s_["digest"]) and
@@ -443,6 +448,29 @@ def main():
         e2e_mdp.append(t2 - t1)
         S.destroy(ctx)
 
+    # ---- phase split of the round kernel: one more, untimed replay with the
+    #      in-kernel phase counters on (they cost clock reads, so never timed)
+    ctx = S.init_cache(cfg, ws, ws_bytes, stream)
+    S.profile(ctx, 3)
+    S.replay_epochs(ctx, max(c["target"]), None, stream)
+    torch.cuda.synchronize(dev)
+    vp = S.read_state(ctx)
+    ph = ws[vp.d_phase_cycles - ws.data_ptr():vp.d_phase_cycles - ws.data_ptr() + 256].cpu().numpy().view(np.uint64)
+    ph_names = {0: "job_epoch_start", 1: "job_classify", 8: "job_subst_prefix", 9: "job_subst_ranks_locate",
+                2: "job_subst_apply", 10: "job_storage_deferral", 11: "job_respond_loop", 3: "job_respond_stats",
+                4: "job_wait_maint", 5: "job_advance", 12: "job_walk_prefetched_step", 13: "job_walk_rest",
+                14: "job_prefetch_issue", 6: "job_unused",
+                16: "maint_spec_prefix", 17: "maint_spec_refill_ranks", 18: "maint_barrier1_wait",
+                19: "maint_evict_decide", 20: "maint_apply", 21: "maint_barrier2_wait"}
+    phase_share = {}
+    for base in (0, 16):
+        keys = [k for k in ph_names if base <= k < base + 16]
+        tot = float(sum(ph[k] for k in keys))
+        for k in keys:
+            phase_share[ph_names[k]] = round(float(ph[k]) / tot, 4) if tot else None
+    phase_share["walk_steps_per_round"] = round(float(ph[7]) / max(1, rounds_tot / args.steps), 3)
+    S.destroy(ctx)
+
     # ---- aggregate over ranks (max time)
     ods_s = sum(ods_ms) / 1e3
     mdp_s = sum(mdp_ms) / 1e3
@@ -479,8 +507,11 @@ def main():
                 cache_entries=ce + cd + ca, mdp_profiles=args.mdp_profiles, mdp_splits=nsplit,
                 job_epochs=sum(c["target"]),
                 mdp_grid=d_grid is not None)
-    roof = roofline_for(dom, kernels[dom], info, hbm_peak, peak_src)
-    mdp_roof = roofline_for("mdp_sweep", kernels["mdp_sweep"], info, hbm_peak, peak_src)
+    tkey = {"ods_rounds": f"ods_rounds@{args.workload}",
+            "mdp_sweep": f"mdp_sweep@{args.mdp_profiles}x{nsplit}{'' if d_grid is not None else '-nogrid'}"}
+    roof = roofline_for(dom, kernels[dom], info, hbm_peak, peak_src, ncu_traffic(tkey.get(dom, dom)))
+    mdp_roof = roofline_for("mdp_sweep", kernels["mdp_sweep"], info, hbm_peak, peak_src,
+                            ncu_traffic(tkey["mdp_sweep"]))
     for name in kernels:
         kernels[name]["algorithmic_bytes_per_launch"] = algorithmic_bytes(name, info)
 

@@ -111,6 +111,28 @@ seneca_status seneca_mdp_sweep(const seneca_mdp_profile* d_profiles, uint32_t n_
                                uint32_t grid_step_pct, seneca_mdp_result* d_results,
                                double* d_grid, void* stream);
 
+/* Model evaluation at given splits (SPEC `evaluate`; SURVEY §8(f)
+ * NEXT-4: fixed splits x dataset sizes, the Fig. 7 curves P:L837-909, are
+ * profiles that differ in n_total).  For every profile i and every split s of
+ * h_splits: V = DSI_overall (Eq. 9) with the same arithmetic as
+ * seneca_mdp_sweep, and optionally the counts {N_A, N_D, N_E, N_S} (Eqs. 5-8).
+ *   h_splits     host [n_splits], each p_e + p_d + p_a == 100 (integer %),
+ *                1 <= n_splits <= 4096 (passed to the kernel by value).
+ *   d_values     device [n_profiles][n_splits] doubles, written (NaN for an
+ *                invalid profile).
+ *   d_counts     NULL, or device [n_profiles][n_splits][4] uint64, written.
+ *   d_tiers      NULL, or device [n_profiles] results: status, lim_* and dsi_*
+ *                written, p_* = 0 and v_best = 0.
+ * Errors: EINVAL on n_profiles == 0, NULL required pointers, n_splits out of
+ * range or a split not summing to 100.                                        */
+typedef struct {
+    uint8_t p_e, p_d, p_a, _pad;
+} seneca_split;
+
+seneca_status seneca_mdp_eval(const seneca_mdp_profile* d_profiles, uint32_t n_profiles,
+                              const seneca_split* h_splits, uint32_t n_splits, double* d_values,
+                              uint64_t* d_counts, seneca_mdp_result* d_tiers, void* stream);
+
 /* Eqs. 5-8 for one split on the host, in exact integer arithmetic (R-M6):
  * caps[0..3] = {N_E, N_D, N_A, N_storage} for a dataset of n_total samples of
  * s_data bytes, a cache of cache_bytes and M = m_num/m_den.  Used to size the
@@ -242,13 +264,16 @@ seneca_status seneca_sync_status(seneca_ctx* ctx, void* stream);
 /* Number of kernel launches this context has issued (for gpu_launches).      */
 uint64_t seneca_launch_count(const seneca_ctx* ctx);
 
-/* Kernel timing: when enabled, every kernel launch of this context is
- * bracketed by CUDA events on its launch stream and the host waits for the
- * end event (launches become synchronous; the replay is one launch), and the
- * round kernel accumulates per-phase SM cycles into d_phase_cycles of the state
- * view.  seneca_profile_read reports, per kernel, launches issued, launches
- * timed and their summed event-measured duration.  Launch counts are always
- * kept.                                                                        */
+/* Kernel timing.  seneca_profile(ctx, flags):
+ *   bit 0  every kernel launch of this context is bracketed by CUDA events on
+ *          its launch stream and the host waits for the end event (launches
+ *          become synchronous; a replay is one launch); seneca_profile_read
+ *          reports, per kernel, launches issued, launches timed and their
+ *          summed event-measured duration;
+ *   bit 1  the round kernel accumulates per-phase SM cycles into
+ *          d_phase_cycles of the state view (clock reads inside the kernel:
+ *          use for the phase split, not for timing).
+ * Launch counts are always kept.                                              */
 typedef struct {
     const char* name;      /* kernel name (static string)                       */
     uint64_t launches;     /* launches issued                                   */
@@ -256,7 +281,7 @@ typedef struct {
     double   sampled_ms;   /* summed event-measured duration of timed launches  */
 } seneca_kernel_stat;
 
-seneca_status seneca_profile(seneca_ctx* ctx, uint32_t enable);
+seneca_status seneca_profile(seneca_ctx* ctx, uint32_t flags);
 seneca_status seneca_profile_read(seneca_ctx* ctx, seneca_kernel_stat* out, uint32_t cap, uint32_t* n_classes);
 
 void        seneca_destroy(seneca_ctx* ctx);

@@ -37,6 +37,20 @@ def mdp_sweep_device(profiles: np.ndarray, grid_step_pct: int = 1, want_grid: bo
     return d_res, d_grid
 
 
+def mdp_eval_device(profiles: np.ndarray, splits, want_counts: bool = False, device="cuda", stream=None):
+    """DSI_overall of every profile at the given (p_e, p_d, p_a) splits on the
+    device: (values float64 [n, s], counts uint64 [n, s, 4] or None, tier rows
+    as RESULT_DTYPE bytes [n, 48])."""
+    torch = _torch()
+    n, ns = len(profiles), len(splits)
+    d_prof = torch.from_numpy(np.ascontiguousarray(profiles).view(np.uint8)).to(device)
+    d_val = torch.empty((n, ns), dtype=torch.float64, device=device)
+    d_cnt = torch.empty((n, ns, 4), dtype=torch.int64, device=device) if want_counts else None
+    d_tiers = torch.empty(n * RESULT_DTYPE.itemsize, dtype=torch.uint8, device=device)
+    seneca.mdp_eval(d_prof, n, splits, d_val, d_cnt, d_tiers, stream)
+    return d_val, d_cnt, d_tiers
+
+
 def results_to_numpy(d_res) -> np.ndarray:
     return d_res.cpu().numpy().view(RESULT_DTYPE)
 
@@ -103,8 +117,9 @@ class ODSContext:
     def launches(self):
         return seneca.launch_count(self.ctx)
 
-    def profile(self, enable: int = 1):
-        seneca.profile(self.ctx, enable)
+    def profile(self, flags: int = 3):
+        """bit 0: event-timed launches; bit 1: in-kernel phase counters."""
+        seneca.profile(self.ctx, flags)
 
     def phase_cycles(self, k=0):
         v = self.view()

@@ -389,6 +389,63 @@ mdp_sweep_kernel(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_pro
     }
 }
 
+// ------------------------------------------------------------------ evaluation at given splits
+constexpr uint32_t kMaxEvalSplits = 4096;
+struct EvalSplits {
+    uint32_t packed[kMaxEvalSplits];   // p_e | p_d << 8 | p_a << 16
+};
+
+// One warp per profile (grid-stride), lanes over the splits.  Eqs. 5-8 in exact
+// integers (validity keeps pct * cache * m_den < 2^64), Eq. 9 with one IEEE
+// operation per step in the order of R-M7: ((tA + tD) + tE) + tS, t = (n/N) DSI.
+__global__ void __launch_bounds__(256)
+mdp_eval_kernel(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_profiles,
+                const __grid_constant__ EvalSplits S, uint32_t n_splits, double* __restrict__ values,
+                uint64_t* __restrict__ counts, seneca_mdp_result* __restrict__ tiers) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t warps = gridDim.x * (blockDim.x / 32);
+    for (uint32_t pi = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); pi < n_profiles; pi += warps) {
+        const seneca_mdp_profile p = profiles[pi];
+        double* vrow = values + (uint64_t)pi * n_splits;
+        uint64_t* crow = counts ? counts + (uint64_t)pi * n_splits * 4 : nullptr;
+        if (!profile_valid(p)) {
+            for (uint32_t s = lane; s < n_splits; s += 32) {
+                vrow[s] = __longlong_as_double(0x7ff8000000000000ll);
+                if (crow) for (int t = 0; t < 4; ++t) crow[4 * s + t] = 0;
+            }
+            if (tiers && lane == 0) { seneca_mdp_result r = {}; r.status = 1; tiers[pi] = r; }
+            continue;
+        }
+        double dsi[4];
+        uint8_t lim[4];
+        tier_throughputs(p, dsi, lim);
+        if (tiers && lane == 0) {
+            seneca_mdp_result r = {};
+            r.lim_a = lim[0]; r.lim_d = lim[1]; r.lim_e = lim[2]; r.lim_s = lim[3];
+            r.dsi_a = dsi[0]; r.dsi_d = dsi[1]; r.dsi_e = dsi[2]; r.dsi_s = dsi[3];
+            tiers[pi] = r;
+        }
+        const uint64_t N = p.n_total;
+        const double dN = u2d(N);
+        const uint64_t Xad = p.cache_bytes * p.m_den, Dad = 100ull * p.m_num * p.s_data, De = 100ull * p.s_data;
+        for (uint32_t s = lane; s < n_splits; s += 32) {
+            const uint32_t w = S.packed[s];
+            const uint64_t pe = w & 0xff, pd = (w >> 8) & 0xff, pa = (w >> 16) & 0xff;
+            const uint64_t capA = (pa * Xad) / Dad, capD = (pd * Xad) / Dad, capE = (pe * p.cache_bytes) / De;
+            const uint64_t nA = N < capA ? N : capA;                                   // Eq. 5
+            const uint64_t nD = (N - nA) < capD ? (N - nA) : capD;                     // Eq. 6
+            const uint64_t nE = (N - nA - nD) < capE ? (N - nA - nD) : capE;           // Eq. 7
+            const uint64_t nS = N - nA - nD - nE;                                      // Eq. 8
+            const double tA = __dmul_rn(__ddiv_rn(u2d(nA), dN), dsi[0]);
+            const double tD = __dmul_rn(__ddiv_rn(u2d(nD), dN), dsi[1]);
+            const double tE = __dmul_rn(__ddiv_rn(u2d(nE), dN), dsi[2]);
+            const double tS = __dmul_rn(__ddiv_rn(u2d(nS), dN), dsi[3]);
+            vrow[s] = __dadd_rn(__dadd_rn(__dadd_rn(tA, tD), tE), tS);              // Eq. 9, R-M7
+            if (crow) { crow[4 * s] = nA; crow[4 * s + 1] = nD; crow[4 * s + 2] = nE; crow[4 * s + 3] = nS; }
+        }
+    }
+}
+
 }  // namespace
 }  // namespace seneca
 
@@ -427,6 +484,36 @@ extern "C" seneca_status seneca_mdp_sweep(const seneca_mdp_profile* d_profiles, 
     const uint32_t blocks = n_profiles < (uint32_t)slots ? n_profiles : (uint32_t)slots;
     mdp_sweep_kernel<<<blocks, kThreads, ns * sizeof(uint2), (cudaStream_t)stream>>>(
         d_profiles, n_profiles, grid_step_pct, steps, ns, d_results, d_grid);
+    SENECA_CUDA_TRY(cudaGetLastError());
+    return SENECA_OK;
+}
+
+extern "C" seneca_status seneca_mdp_eval(const seneca_mdp_profile* d_profiles, uint32_t n_profiles,
+                                         const seneca_split* h_splits, uint32_t n_splits, double* d_values,
+                                         uint64_t* d_counts, seneca_mdp_result* d_tiers, void* stream) {
+    using namespace seneca;
+    if (n_profiles == 0 || !d_profiles || !h_splits || !d_values) {
+        set_error("seneca_mdp_eval: empty input or NULL pointer");
+        return SENECA_EINVAL;
+    }
+    if (n_splits == 0 || n_splits > kMaxEvalSplits) {
+        set_error("seneca_mdp_eval: n_splits %u not in [1, %u]", n_splits, kMaxEvalSplits);
+        return SENECA_EINVAL;
+    }
+    EvalSplits S;                    // by-value kernel parameter (copied at launch)
+    for (uint32_t s = 0; s < n_splits; ++s) {
+        const seneca_split& x = h_splits[s];
+        if ((uint32_t)x.p_e + x.p_d + x.p_a != 100) {
+            set_error("seneca_mdp_eval: split %u sums to %u, not 100", s, (uint32_t)x.p_e + x.p_d + x.p_a);
+            return SENECA_EINVAL;
+        }
+        S.packed[s] = x.p_e | (uint32_t)x.p_d << 8 | (uint32_t)x.p_a << 16;
+    }
+    const uint32_t warps = 256 / 32;
+    uint32_t blocks = (n_profiles + warps - 1) / warps;
+    blocks = blocks < 148u * 16u ? blocks : 148u * 16u;
+    mdp_eval_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(d_profiles, n_profiles, S, n_splits, d_values,
+                                                              d_counts, d_tiers);
     SENECA_CUDA_TRY(cudaGetLastError());
     return SENECA_OK;
 }

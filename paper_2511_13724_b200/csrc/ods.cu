@@ -1327,7 +1327,7 @@ template <class F>
 void timed(seneca_ctx* c, int cls, cudaStream_t st, F&& launch) {
     c->launches++;
     c->klaunch[cls]++;
-    if (!c->profiling) { launch(); return; }
+    if (!(c->profiling & 1u)) { launch(); return; }
     cudaEventRecord(c->ev_a, st);
     launch();
     cudaEventRecord(c->ev_b, st);
@@ -1359,7 +1359,7 @@ seneca_status launch_rounds(seneca_ctx* c, uint64_t R, uint32_t jobs_mask, const
     P.transcript = transcript;
     P.out_rep = (uint64_t)out_stride * (row_of_job ? __builtin_popcount(jobs_mask) : c->C.J);
     P.tr_rep = (uint64_t)c->C.J * c->C.maxT * c->C.N;
-    P.timing = c->profiling;
+    P.timing = (c->profiling >> 1) & 1u;
     if (c->mode == 1) {
         timed(c, K_VALIDATE, st, [&] {
             ods_validate_requests<<<__builtin_popcount(jobs_mask), 256, (size_t)c->C.Bmax * 4, st>>>(c->LS, c->C, P);
@@ -1630,7 +1630,7 @@ extern "C" uint64_t seneca_launch_count(const seneca_ctx* c) { return c ? c->lau
 
 extern "C" seneca_status seneca_profile(seneca_ctx* c, uint32_t enable) {
     if (!c) { set_error("bad arguments"); return SENECA_EINVAL; }
-    c->profiling = enable ? 1u : 0u;
+    c->profiling = enable & 3u;
     return SENECA_OK;
 }
 

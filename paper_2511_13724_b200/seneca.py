@@ -49,6 +49,10 @@ class MdpResult(C.Structure):
     ]
 
 
+class Split(C.Structure):
+    _fields_ = [("p_e", C.c_uint8), ("p_d", C.c_uint8), ("p_a", C.c_uint8), ("_pad", C.c_uint8)]
+
+
 class CacheConfig(C.Structure):
     _fields_ = [
         ("n_total", C.c_uint64), ("n_jobs", C.c_uint32), ("request_mode", C.c_uint32),
@@ -99,6 +103,8 @@ def lib() -> C.CDLL:
         vp, u32, u64 = C.c_void_p, C.c_uint32, C.c_uint64
         L.seneca_mdp_num_splits.argtypes = [u32]; L.seneca_mdp_num_splits.restype = u64
         L.seneca_mdp_sweep.argtypes = [vp, u32, u32, vp, vp, vp]; L.seneca_mdp_sweep.restype = C.c_int
+        L.seneca_mdp_eval.argtypes = [vp, u32, C.POINTER(Split), u32, vp, vp, vp, vp]
+        L.seneca_mdp_eval.restype = C.c_int
         L.seneca_split_capacities.argtypes = [u64, u64, u32, u32, u64, u32, u32, u32, C.POINTER(u64)]
         L.seneca_split_capacities.restype = C.c_int
         L.seneca_metadata_bytes.argtypes = [u64, u32]; L.seneca_metadata_bytes.restype = u64
@@ -124,7 +130,7 @@ def lib() -> C.CDLL:
     return _lib
 
 
-EXPORTED = ["seneca_mdp_num_splits", "seneca_mdp_sweep", "seneca_split_capacities",
+EXPORTED = ["seneca_mdp_num_splits", "seneca_mdp_sweep", "seneca_mdp_eval", "seneca_split_capacities",
             "seneca_metadata_bytes", "seneca_state_bytes", "seneca_init_cache",
             "seneca_ods_next_batch", "seneca_replay_epochs", "seneca_replay_rounds",
             "seneca_read_state", "seneca_sync_status", "seneca_launch_count", "seneca_destroy",
@@ -159,6 +165,14 @@ def mdp_num_splits(grid_step_pct: int) -> int:
 def mdp_sweep(d_profiles, n_profiles: int, grid_step_pct: int, d_results, d_grid=None, stream=None):
     _check(lib().seneca_mdp_sweep(_ptr(d_profiles), n_profiles, grid_step_pct, _ptr(d_results),
                                   _ptr(d_grid), _stream(stream)))
+
+
+def mdp_eval(d_profiles, n_profiles: int, splits, d_values, d_counts=None, d_tiers=None, stream=None):
+    """splits: sequence of (p_e, p_d, p_a) integer percents summing to 100."""
+    splits = list(splits)
+    arr = (Split * len(splits))(*[Split(int(e), int(d), int(a), 0) for e, d, a in splits])
+    _check(lib().seneca_mdp_eval(_ptr(d_profiles), n_profiles, arr, len(splits), _ptr(d_values), _ptr(d_counts),
+                                 _ptr(d_tiers), _stream(stream)))
 
 
 def split_capacities(n_total, s_data, m_num, m_den, cache_bytes, p_e, p_d, p_a):

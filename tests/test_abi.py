@@ -77,6 +77,10 @@ def test_invalid_arguments_rejected_on_host(lib):
         S.mdp_sweep(1, 1, 7, 1, None, 0)                    # 7 does not divide 100
     assert ei.value.status == S.EINVAL
     assert S.mdp_num_splits(1) == 5151 and S.mdp_num_splits(10) == 66 and S.mdp_num_splits(7) == 0
+    for splits in ([(10, 20, 71)], [(50, 50, 0)] * 4097, []):    # host-side checks, before any launch
+        with pytest.raises(S.SenecaError) as ei:
+            S.mdp_eval(1, 1, splits, 1, stream=0)
+        assert ei.value.status == S.EINVAL
     bad = [dict(n_total=0), dict(n_total=2**31), dict(batch=[0]), dict(batch=[5000]),
            dict(cap_e=600, cap_d=600), dict(target=[0])]
     for over in bad:
@@ -104,7 +108,7 @@ def test_ctypes_layouts_match_c_header(lib, tmp_path):
     probe = tmp_path / "probe.c"
     structs = {"seneca_cache_config": S.CacheConfig, "seneca_state_view": S.StateView,
                "seneca_job_epoch_stats": S.JobEpochStats, "seneca_mdp_profile": S.MdpProfile,
-               "seneca_mdp_result": S.MdpResult, "seneca_kernel_stat": S.KernelStat}
+               "seneca_mdp_result": S.MdpResult, "seneca_kernel_stat": S.KernelStat, "seneca_split": S.Split}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "seneca.h"', "int main(void) {"]
     for cname, ct in structs.items():
         lines.append(f'printf("{cname} sizeof %zu\\n", sizeof({cname}));')

@@ -143,3 +143,118 @@ def test_results_without_grid_match():
     ores, _ = O.mdp_sweep(rows, 1)
     res, _ = run_gpu(rows, 1, grid=False)
     assert_same(res, ores)
+
+
+def test_wide_counts_paths():
+    """N >= 2^31 (64-bit split path), N >= 2^53 (__ddiv_rn tables) and capacities
+    near N: every path of the kernel against the oracle."""
+    cols = synth.mdp_profiles(400, seed=77)
+    rows = O.profiles_from_columns(cols)
+    big = [2**31 - 1, 2**31, 2**31 + 12345, 3 * 2**32 + 7, 2**52 + 1, 2**53 + 3, 2**60 + 11, 2**63 + 5]
+    for k in range(len(rows)):
+        rows["n_total"][k] = big[k % len(big)]
+        rows["s_data"][k] = 1 + (k % 3)                     # capacities comparable to N
+        lim = (2**64 - 1) // 100 // int(rows["m_den"][k])      # the ABI's overflow bound (EINVAL above it)
+        rows["cache_bytes"][k] = np.uint64(min(int(rows["n_total"][k]) // (1 + k % 5), lim))
+    for g in (1, 5):
+        ores, ogrid = O.mdp_sweep(rows, g, want_grid=True)
+        res, grid = run_gpu(rows, g)
+        assert_same(res, ores, grid, ogrid)
+
+
+def test_every_grid_step():
+    """Every divisor of 100: one to several row items and partial sweep chunks."""
+    rows = O.profiles_from_columns(synth.mdp_profiles(700, seed=31))
+    for g in (1, 2, 4, 5, 10, 20, 25, 50, 100):
+        ores, ogrid = O.mdp_sweep(rows, g, want_grid=True)
+        res, grid = run_gpu(rows, g)
+        assert_same(res, ores, grid, ogrid)
+
+
+def test_invalid_profiles_interleaved():
+    """Invalid rows scattered through a long list (several profiles per CTA, the
+    double-buffered tables meet invalid neighbours): status 1 for those, the
+    oracle's results for the rest."""
+    rows = O.profiles_from_columns(synth.mdp_profiles(5000, seed=12))
+    bad = np.arange(0, 5000, 7)
+    dev = to_dev_rows(rows)
+    dev["t_gpu"][bad] = 0.0
+    d_res, d_grid = P.mdp_sweep_device(dev, 1, want_grid=True)
+    torch.cuda.synchronize()
+    res = P.results_to_numpy(d_res)
+    good = np.setdiff1d(np.arange(5000), bad)
+    assert np.all(res["status"][bad] == 1) and np.all(res["status"][good] == 0)
+    ores, ogrid = O.mdp_sweep(rows[good], 1, want_grid=True)
+    assert_same(res[good], ores, d_grid.cpu().numpy()[good], ogrid)
+
+
+# ------------------------------------------------------------ seneca_mdp_eval (SPEC evaluate, NEXT-4 size curves)
+def _oracle_eval(rows, splits):
+    vals = np.zeros((len(rows), len(splits)))
+    cnts = np.zeros((len(rows), len(splits), 4), np.uint64)
+    for i in range(len(rows)):
+        p = O.profile_row(rows, i)
+        for s, (e, d, a) in enumerate(splits):
+            v, _, c = O.model_eval(p, e, d, a)
+            vals[i, s] = v
+            na, nd, ne, ns = O.split_counts(p, e, d, a)
+            cnts[i, s] = (na, nd, ne, ns)
+    return vals, cnts
+
+
+def test_eval_random_splits_bit_exact():
+    rows = O.profiles_from_columns(synth.mdp_profiles(300, seed=41))
+    st = synth.Stream(9)
+    splits = []
+    for _ in range(97):
+        e = int(st.u64(1)[0] % 101); d = int(st.u64(1)[0] % (101 - e))
+        splits.append((e, d, 100 - e - d))
+    splits += [(100, 0, 0), (0, 100, 0), (0, 0, 100), (0, 0, 100)]
+    d_val, d_cnt, d_tiers = P.mdp_eval_device(to_dev_rows(rows), splits, want_counts=True)
+    torch.cuda.synchronize()
+    ov, oc = _oracle_eval(rows, splits)
+    assert np.array_equal(d_val.cpu().numpy().view(np.uint64), ov.view(np.uint64))
+    assert np.array_equal(d_cnt.cpu().numpy().view(np.uint64), oc)
+    tiers = P.results_to_numpy(d_tiers)
+    ores, _ = O.mdp_sweep(rows, 10)
+    for f in ("dsi_a", "dsi_d", "dsi_e", "dsi_s"):
+        assert np.array_equal(tiers[f].view(np.uint64), ores[f].view(np.uint64))
+    assert np.all(tiers["status"] == 0)
+
+
+def test_eval_fig7_dataset_size_curves():
+    """NEXT-4: A-only and E-only curves over dataset sizes 8-512 GB at a 64 GB
+    cache for the three Table-4 servers (Fig. 7 axis), bit-exact; the
+    crossing rule of the oracle pins (test_oracle_mdp) then holds on the device."""
+    sizes = [int(x * 1e9 / 114_000) for x in (8, 16, 32, 64, 128, 256, 512)]
+    rows = []
+    for server in ("in_house", "aws", "azure"):
+        g = {k: v for k, v in GOLD[server].items() if not k.startswith("_")}
+        for n in sizes:
+            rows.append(dict(g, model_bytes=0.0, n_total=n, nodes=1, gpus_per_node=1))
+    arr = np.zeros(len(rows), O.PROFILE_DTYPE)
+    for i, kw in enumerate(rows):
+        for k, v in kw.items():
+            arr[i][k] = v
+    splits = [(0, 0, 100), (100, 0, 0), (0, 100, 0), (52, 48, 0)]
+    d_val, _, _ = P.mdp_eval_device(to_dev_rows(arr), splits)
+    torch.cuda.synchronize()
+    ov, _ = _oracle_eval(arr, splits)
+    got = d_val.cpu().numpy()
+    assert np.array_equal(got.view(np.uint64), ov.view(np.uint64))
+    a_minus_e = (got[:, 0] - got[:, 1]).reshape(3, len(sizes))
+    assert np.all(a_minus_e[0] > 0) and np.all(a_minus_e[1] < 0) and np.all(a_minus_e[2] < 0)   # [A.4]
+
+
+def test_eval_invalid_profile_and_arguments():
+    rows = to_dev_rows(O.profiles_from_columns(synth.mdp_profiles(4, seed=2)))
+    rows["t_gpu"][1] = 0.0
+    d_val, d_cnt, d_tiers = P.mdp_eval_device(rows, [(10, 20, 70)], want_counts=True)
+    torch.cuda.synchronize()
+    v = d_val.cpu().numpy()[:, 0]
+    assert np.isnan(v[1]) and not np.isnan(v[[0, 2, 3]]).any()
+    assert list(P.results_to_numpy(d_tiers)["status"]) == [0, 1, 0, 0]
+    for bad in ([(10, 20, 71)], [(50, 50, 0)] * 4097, []):
+        with pytest.raises(S.SenecaError) as ei:
+            P.mdp_eval_device(rows, bad)
+        assert ei.value.status == S.EINVAL

@@ -242,3 +242,63 @@ def test_cache_monotonicity_soft():
     r1, _ = O.mdp_sweep(arr, 1)
     r2, _ = O.mdp_sweep(big, 1)
     assert np.all(r2["v"] >= r1["v"] * (1 - 1e-9))
+
+
+# ------------------------------------------------------------ NEXT-4: dataset-size curves (Fig. 7)
+def _sizes():
+    """Dataset sizes 8 GB .. 512 GB at S_data = 114 KB (the Fig. 7 axis), plus
+    tiny and huge datasets so both the full-fit and neither-fits regimes occur."""
+    gb = [0.001, 0.01, 0.1, 1, 2, 4, 8, 16, 32, 64, 128, 256, 327.68, 512, 1024, 4096, 65536]
+    return [max(1, int(x * 1e9 / 114_000)) for x in gb]
+
+
+@pytest.mark.parametrize("server", ["in_house", "aws", "azure"])
+def test_single_tier_curves_move_toward_dsi_s(server):
+    """for a fixed split V(N) = DSI_S + sum_t f_t(N)(DSI_t - DSI_S)
+    with non-increasing f_t, so a single-tier curve moves monotonically toward
+    DSI_S as the dataset grows; at full fit it IS DSI_t (N_t/N = 1 exactly) and
+    beyond it equals (cap/N) DSI_t + ((N - cap)/N) DSI_S."""
+    for split in ((100, 0, 0), (0, 100, 0), (0, 0, 100)):
+        dist = []
+        for n in _sizes():
+            p = prof(server, n_total=n)
+            v, _, _ = O.model_eval(p, *split)
+            d, _ = O.tiers(p)
+            na, nd, ne, ns = O.split_counts(p, *split)
+            t = 2 if split[0] else (1 if split[1] else 0)            # dsi index: 0 A, 1 D, 2 E
+            cap = {0: na, 1: nd, 2: ne}[t]
+            if ns == 0:
+                assert v == d[t]                                     # full fit: exactly DSI_t
+            want = Fraction(cap, n) * Fraction(d[t]) + Fraction(n - cap, n) * Fraction(d[3])
+            assert abs(Fraction(v) - want) <= abs(want) * Fraction(1, 10**14)
+            dist.append(abs(v - d[3]))
+        for a, b in zip(dist, dist[1:]):
+            assert b <= a * (1 + 1e-12) + 1e-12
+
+
+@pytest.mark.parametrize("server,b_cache", [("in_house", None), ("aws", None), ("azure", None),
+                                            ("azure", 30e9)])
+def test_a_only_vs_e_only_crossing_rule(server, b_cache):
+    """M15(ii): the A-only and E-only curves cross iff sign(DSI_A - DSI_E) (both fit)
+    differs from sign((DSI_A - DSI_S) - M'(DSI_E - DSI_S)) (neither fits, M' =
+    cap_E / cap_A, the E tier's sample-count advantage).  Azure with B_cache read
+    as 30 GB/s is the profile SURVEY [A.4] names as crossing exactly once."""
+    over = {} if b_cache is None else dict(b_cache=b_cache)
+    diffs = []
+    for n in _sizes():
+        p = prof(server, n_total=n, **over)
+        va, _, _ = O.model_eval(p, 0, 0, 100)
+        ve, _, _ = O.model_eval(p, 100, 0, 0)
+        diffs.append(va - ve)
+    p = prof(server, n_total=_sizes()[-1], **over)
+    d, _ = O.tiers(p)
+    na, _, _, _ = O.split_counts(p, 0, 0, 100)
+    _, _, ne, _ = O.split_counts(p, 100, 0, 0)
+    small = np.sign(d[0] - d[2])
+    large = np.sign((d[0] - d[3]) * na - (d[2] - d[3]) * ne)
+    s = [np.sign(x) for x in diffs if x != 0]
+    changes = sum(1 for a, b in zip(s, s[1:]) if a != b)
+    assert s[0] == small and s[-1] == large
+    assert changes == (1 if small != large else 0)
+    if b_cache == 30e9:
+        assert changes == 1

@@ -16,8 +16,11 @@ timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > $OUT/bench_r
 # launch list of one bench step (cold, serialised: compare shares, not absolutes)
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
   python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-profile > /dev/null 2>&1; echo "ncu launches rc=$?"
-# full captures: the replay kernel on a bounded replay, the MDP sweep
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:ods_rounds -c 1 -o $OUT/ncu_ods_rounds \
-  python tools/profile_ods.py imagenet1k 6000 > /dev/null 2>&1; echo "ncu ods rc=$?"
+# full captures of the launches bench.py times: each workload's whole replay
+# (one ods_rounds launch) and the 10,000-profile MDP sweep with the grid
+for w in imagenet1k openimages imagenet22k; do
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:ods_rounds -c 1 -o $OUT/ncu_ods_rounds_$w \
+    python tools/profile_ods.py $w 1000000 > /dev/null 2>&1; echo "ncu ods $w rc=$?"
+done
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:mdp_sweep -c 1 -o $OUT/ncu_mdp_sweep \
   python tools/profile_ods.py toy 10 --mdp > /dev/null 2>&1; echo "ncu mdp rc=$?"
