@@ -59,10 +59,18 @@ def perm(K, n, x):
 
 
 class LiteralODS:
-    def __init__(self, n_total, batch, target, cap_e, cap_d, cap_a, seed):
+    """evict_all: SURVEY 8c.3 "evict_tiers = ALL" as read in DESIGN.md R-O21:
+    consumer sets for every cached source, every cached tier evictable, refills
+    tier by tier A -> D -> E from one keyed rank stream over the round-start
+    storage pool."""
+
+    def __init__(self, n_total, batch, target, cap_e, cap_d, cap_a, seed, evict_all=False):
         self.N, self.batch, self.target = n_total, list(batch), list(target)
         self.J = len(batch)
         self.cap_a, self.seed = cap_a, seed
+        self.cap = {A: cap_a, D: cap_d, E: cap_e}
+        self.evict_all = evict_all
+        self.cached = (A, D, E) if evict_all else (A,)        # tiers with consumer sets / eviction
         self.tier = [S] * n_total
         iota = [perm(key(seed, 1), n_total, p) for p in range(cap_a + cap_d + cap_e)]
         for p, i in enumerate(iota):
@@ -123,7 +131,7 @@ class LiteralODS:
                 out[s], src[s] = req[s], S
             for s in range(need):
                 self.seen[j].add(out[s])
-                if src[s] & 3 == A:
+                if src[s] & 3 in self.cached:
                     self.cons[j].add(out[s])
                     a_served.append(out[s])
                 self.deliveries[j][self.e[j]].append((out[s], src[s]))
@@ -139,20 +147,27 @@ class LiteralODS:
         for j in departing:
             self.active[j] = False
         if any(self.active):
-            cand = sorted(i for i in range(self.N) if self.tier[i] == A) if changed else sorted(set(a_served))
-            evict = [i for i in cand if self.tier[i] == A and
+            cand = (sorted(i for i in range(self.N) if self.tier[i] in self.cached) if changed
+                    else sorted(set(a_served)))
+            evict = [i for i in cand if self.tier[i] in self.cached and
                      all(i in self.cons[a] for a in range(self.J) if self.active[a])]
-            size_a = sum(1 for t in self.tier if t == A) - len(evict)
+            deficit = {}
+            for t in (A, D, E):
+                size = sum(1 for x in self.tier if x == t) - sum(1 for i in evict if self.tier[i] == t)
+                deficit[t] = self.cap[t] - size if t in self.cached else 0
             pool_s = self.pool(S, 0)
-            k = min(self.cap_a - size_a, len(pool_s))
+            k = min(deficit[A] + deficit[D] + deficit[E], len(pool_s))
             Kr = key(self.seed, 4, 0, self.r)
             fill = [pool_s[perm(Kr, len(pool_s), u)] for u in range(k)]
+            dest = []
+            for t in (A, D, E):                              # tier by tier from one rank stream
+                dest += [t] * min(deficit[t], k - len(dest))
             for i in evict:
                 self.tier[i] = S
                 for a in range(self.J):
                     self.cons[a].discard(i)
-            for i in fill:
-                self.tier[i] = A
+            for i, t in zip(fill, dest):
+                self.tier[i] = t
             self.evicted += len(evict)
             self.refilled += k
         self.r += 1

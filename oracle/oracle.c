@@ -333,7 +333,12 @@ typedef struct {
     oracle_stats *stats;           /* [J][max_target]                         */
     uint64_t evicted_total, refilled_total;
     uint64_t *transcript;          /* optional [J][max_target][N]: src<<32|id */
+    int      evict_all;            /* evict_tiers = ALL (R-O21): consumer sets and
+                                      eviction for every cached tier            */
 } ods_t;
+
+/* tiers that carry consumer sets and can be evicted: A (R-O5), or all (R-O21) */
+static int tracked(const ods_t *o, int t) { return t == T_A || (o->evict_all && t != T_S); }
 
 static int  bit_get(const uint64_t *bm, uint64_t i) { return (int)((bm[i >> 6] >> (i & 63)) & 1u); }
 static void bit_set(uint64_t *bm, uint64_t i)       { bm[i >> 6] |= (uint64_t)1 << (i & 63); }
@@ -418,13 +423,14 @@ void oracle_ods_destroy(void *h)
  * positions [0,cap_A) -> A, next cap_D -> D, next cap_E -> E, rest -> S. */
 void *oracle_ods_create(uint64_t N, uint32_t J, const uint32_t *batch, const uint32_t *target,
                         uint64_t cap_e, uint64_t cap_d, uint64_t cap_a, uint64_t seed,
-                        int keep_transcript)
+                        int keep_transcript, int evict_all)
 {
     if (N == 0 || N >= ((uint64_t)1 << 32) || J == 0 || J > 32) return NULL;
     if (cap_e + cap_d + cap_a > N) return NULL;
     ods_t *o = calloc(1, sizeof *o);
     o->N = N; o->J = J; o->W = (N + 63) / 64;
     o->cap_e = cap_e; o->cap_d = cap_d; o->cap_a = cap_a; o->seed = seed;
+    o->evict_all = evict_all != 0;
     o->max_target = 0;
     for (uint32_t j = 0; j < J; ++j) {
         if (batch[j] == 0 || target[j] == 0) { free(o); return NULL; }
@@ -549,13 +555,14 @@ int oracle_ods_round(void *h, const uint32_t *jobs, uint32_t n_jobs, const uint3
         /* remaining misses are fetched from storage (R-O18) */
         for (uint64_t u = q; u < m; ++u) { out[miss[u]] = (uint32_t)R[miss[u]]; src[miss[u]] = T_S; }
 
-        /* steps 3-4: respond, update seen; consumer set for A (R-O5) */
+        /* steps 3-4: respond, update seen; consumer set for A (R-O5)
+         * -- for every cached source under evict_tiers = ALL (R-O21) */
         oracle_stats *st = &o->stats[(uint64_t)j * o->max_target + o->e[j]];
         for (uint64_t s = 0; s < need; ++s) {
             uint64_t i = out[s];
             int t = src[s] & 3, sub = (src[s] & SUBST) != 0;
             bit_set(seen_j, i);
-            if (t == T_A) { bit_set(cons_j, i); a_served[n_a_served++] = i; }
+            if (tracked(o, t)) { bit_set(cons_j, i); a_served[n_a_served++] = i; }
             st->served[t]++;
             if (sub) st->subst[t]++;
             else if (t != T_S) st->req_hits[t]++;
@@ -583,13 +590,12 @@ int oracle_ods_round(void *h, const uint32_t *jobs, uint32_t n_jobs, const uint3
         if (o->active[j]) any_active = 1;
     }
     if (any_active) {
-        /* candidates, ascending and distinct */
+        /* candidates, ascending and distinct: the cached-served ids of the round,
+         * or every tracked entry when the active set changed (R-O6) */
         uint64_t *cand, nc = 0;
         if (changed) {
-            uint64_t total = 0;
-            for (uint64_t w = 0; w < o->W; ++w) total += (uint64_t)__builtin_popcountll(o->bm_a[w]);
-            cand = malloc((total + 1) * 8);
-            for (uint64_t i = 0; i < o->N; ++i) if (bit_get(o->bm_a, i)) cand[nc++] = i;
+            cand = malloc((o->N + 1) * 8);
+            for (uint64_t i = 0; i < o->N; ++i) if (tracked(o, tier_of(o, i))) cand[nc++] = i;
         } else {
             cand = malloc((n_a_served + 1) * 8);
             memcpy(cand, a_served, n_a_served * 8);
@@ -601,21 +607,31 @@ int oracle_ods_round(void *h, const uint32_t *jobs, uint32_t n_jobs, const uint3
             free(tmp);
         }
         /* evict candidates consumed by every active job */
-        uint64_t *evict = malloc((nc + 1) * 8), ne = 0;
+        uint64_t *evict = malloc((nc + 1) * 8), ne = 0, ne_t[4] = {0, 0, 0, 0};
         for (uint64_t u = 0; u < nc; ++u) {
             uint64_t i = cand[u];
-            if (!bit_get(o->bm_a, i)) continue;
+            int t = tier_of(o, i);
+            if (!tracked(o, t)) continue;
             int all = 1;
             for (uint32_t a = 0; a < o->J; ++a)
                 if (o->active[a] && !bit_get(o->cons + (uint64_t)a * o->W, i)) { all = 0; break; }
-            if (all) evict[ne++] = i;
+            if (all) { evict[ne++] = i; ne_t[t]++; }
         }
-        /* refill: k = min(cap_A - |A| after eviction, |pool_S| at round start) */
-        uint64_t sizeA = 0;
-        for (uint64_t w = 0; w < o->W; ++w) sizeA += (uint64_t)__builtin_popcountll(o->bm_a[w]);
-        uint64_t deficit = o->cap_a - (sizeA - ne);
+        /* refill (R-O8, R-O21): deficit_t = cap_t - |t| after eviction for the
+         * tracked tiers; k = min(sum of deficits, |pool_S| at round start) ranks
+         * rho(0..k-1) of one keyed stream, assigned tier by tier A -> D -> E */
+        uint64_t deficit[4] = {0, 0, 0, 0};
+        const uint64_t caps[4] = {0, o->cap_e, o->cap_d, o->cap_a};
+        const uint64_t *bms[4] = {NULL, o->bm_e, o->bm_d, o->bm_a};
+        for (int t = T_E; t <= T_A; ++t) {
+            if (!tracked(o, t)) continue;
+            uint64_t size = 0;
+            for (uint64_t w = 0; w < o->W; ++w) size += (uint64_t)__builtin_popcountll(bms[t][w]);
+            deficit[t] = caps[t] - (size - ne_t[t]);
+        }
         uint64_t PS = pool_size(o, T_S, 0);
-        uint64_t k = deficit < PS ? deficit : PS;
+        uint64_t want = deficit[T_A] + deficit[T_D] + deficit[T_E];
+        uint64_t k = want < PS ? want : PS;
         uint64_t *fill = NULL;
         if (k) {
             uint64_t K = oracle_key(o->seed, PUR_REFILL, 0, o->r, 0);
@@ -626,10 +642,20 @@ int oracle_ods_round(void *h, const uint32_t *jobs, uint32_t n_jobs, const uint3
             free(ranks);
         }
         for (uint64_t u = 0; u < ne; ++u) {
-            bit_clr(o->bm_a, evict[u]);
+            bit_clr(o->bm_a, evict[u]); bit_clr(o->bm_d, evict[u]); bit_clr(o->bm_e, evict[u]);
             for (uint32_t a = 0; a < o->J; ++a) bit_clr(o->cons + (uint64_t)a * o->W, evict[u]);
         }
-        for (uint64_t u = 0; u < k; ++u) bit_set(o->bm_a, fill[u]);
+        {
+            const int order[3] = { T_A, T_D, T_E };
+            uint64_t u = 0;
+            for (int ti = 0; ti < 3; ++ti) {
+                int t = order[ti];
+                uint64_t end = u + deficit[t];
+                if (end > k) end = k;
+                uint64_t *bm = t == T_A ? o->bm_a : (t == T_D ? o->bm_d : o->bm_e);
+                for (; u < end; ++u) bit_set(bm, fill[u]);
+            }
+        }
         o->evicted_total += ne;
         o->refilled_total += k;
         free(cand); free(evict); free(fill);

@@ -239,3 +239,100 @@ def test_cross_check_with_literal_transcription(block):
         assert (ev, rf) == (lit.evicted, lit.refilled)
         # I2 on the literal side: no A entry served twice to a job between admission and eviction
         _check_invariants(o, cfg)
+
+
+# ------------------------------------------------------------ evict_tiers = ALL (DESIGN R-O21)
+def run_all(cfg, transcript=True):
+    return O.ODS(cfg["n_total"], cfg["batch"], cfg["target"], cfg["cap_e"], cfg["cap_d"], cfg["cap_a"],
+                 cfg["seed"], transcript=transcript, evict_all=True)
+
+
+@pytest.mark.parametrize("block", range(8))
+def test_evict_all_cross_check_with_literal_transcription(block):
+    st = synth.Stream(7000 + block)
+    for _ in range(60):
+        cfg = synth.random_tiny_ods(st)
+        o = run_all(cfg)
+        o.replay_epochs(max(cfg["target"]))
+        lit = L.LiteralODS(cfg["n_total"], cfg["batch"], cfg["target"], cfg["cap_e"], cfg["cap_d"],
+                           cfg["cap_a"], cfg["seed"], evict_all=True)
+        lit.replay_all()
+        tr = o.transcript()
+        for j in range(len(cfg["batch"])):
+            for e in range(cfg["target"][j]):
+                got = [(int(x) & 0xFFFFFFFF, int(x) >> 32) for x in tr[j, e]]
+                assert got == lit.deliveries[j][e], cfg
+        t, seen, cons = o.state()
+        assert list(t) == lit.tier
+        _, ev, rf = o.stats()
+        assert (ev, rf) == (lit.evicted, lit.refilled)
+
+
+def test_evict_all_invariants():
+    """I1/I3/I5 per job-epoch, I4 per tier, and cached-occupancy conservation
+    |E| + |D| + |A| = caps + refills - evictions, for evict_tiers = ALL."""
+    for seed in (1, 2, 3):
+        cfg = dict(n_total=600, batch=[16, 40, 9], target=[2, 3, 2], cap_e=70, cap_d=50, cap_a=40, seed=seed)
+        o = run_all(cfg)
+        o.replay_epochs(3)
+        tr = o.transcript()
+        st, ev, rf = o.stats()
+        for j in range(3):
+            for e in range(cfg["target"][j]):
+                ids = (tr[j, e] & 0xFFFFFFFF).astype(np.int64)
+                assert np.array_equal(np.sort(ids), np.arange(600))
+                assert st[j, e]["served"].sum() == 600
+        t, _, _ = o.state()
+        assert (t == E).sum() <= 70 and (t == D).sum() <= 50 and (t == A).sum() <= 40
+        assert (t != S).sum() == 70 + 50 + 40 + rf - ev
+        assert ev > 0 and rf > 0
+
+
+def test_evict_all_single_job_encoded_cache_churns():
+    """J = 1 (threshold 1), E-only cache: every E-served sample is evicted at its
+    round end and one storage sample refilled into E, so storage fetches +
+    refills = delivered, except the E-served of the final round (the job departs:
+    no maintain); the E tier is back at cap_E after every round (the storage
+    pool is never short here)."""
+    cfg = dict(n_total=1000, batch=[32], target=[2], cap_e=200, cap_d=0, cap_a=0, seed=5)
+    o = run_all(cfg)
+    o.replay_epochs(2)
+    st, ev, rf = o.stats()
+    tr = o.transcript()
+    storage = int(st[0, :]["served"][:, S].sum())
+    last_round = tr[0, 1, 1000 - (1000 % 32 or 32):]
+    e_last = int((((last_round >> np.uint64(32)) & np.uint64(3)) == E).sum())
+    assert storage + rf == 2000 - e_last and ev == rf
+    t, _, _ = o.state()
+    assert (t == E).sum() == 200 and (t == A).sum() == 0 and (t == D).sum() == 0
+
+
+def test_evict_all_a_only_mode_is_the_special_case():
+    """With no E/D tiers the two modes are the same protocol: identical replays."""
+    st = synth.Stream(99)
+    for _ in range(40):
+        cfg = synth.random_tiny_ods(st)
+        cfg = dict(cfg, cap_e=0, cap_d=0)
+        a, b = run_oracle(cfg), run_all(cfg)
+        a.replay_epochs(max(cfg["target"]))
+        b.replay_epochs(max(cfg["target"]))
+        assert np.array_equal(a.transcript(), b.transcript())
+        assert np.array_equal(a.state()[0], b.state()[0])
+
+
+def test_evict_all_uplift_on_encoded_only_cache():
+    """O4: with static tiers (evict_tiers = A) an E-only cache gives hits exactly
+    cap_E per job-epoch whatever the sampler; with evict_tiers = ALL consumed E
+    entries are replaced, so 3 concurrent jobs get well above the cached fraction
+    (the direction P:L1474-1475 reports for ImageNet-22K at 100-0-0)."""
+    cfg = dict(n_total=1000, batch=[32] * 3, target=[3] * 3, cap_e=200, cap_d=0, cap_a=0, seed=7)
+    static = run_oracle(cfg, transcript=False)
+    static.replay_epochs(3)
+    churn = run_all(cfg, transcript=False)
+    churn.replay_epochs(3)
+    s0, _, _ = static.stats()
+    s1, _, _ = churn.stats()
+    for j in range(3):
+        for e in (1, 2):
+            assert s0[j, e]["served"][1:].sum() == 200
+            assert s1[j, e]["served"][1:].sum() / 1000 >= 0.30
