@@ -170,7 +170,10 @@ typedef struct {
                                       co-resident (EINVAL otherwise); request_mode 1 needs
                                       R = 1.  SURVEY §8(e): replicas fill the GPU with
                                       independent replays (weak scaling inside one device). */
-    uint32_t        _pad0;
+    uint32_t        evict_tiers;   /* 0: only augmented (A) entries carry consumer sets and are
+                                      evicted / refilled (the default); 1: every
+                                      cached tier (E, D, A) -- SURVEY 8c.3 "evict_tiers = ALL",
+                                      DESIGN.md R-O21; E/D hits stay reusable              */
 } seneca_cache_config;
 
 /* Per job-epoch counters (R-O10; digest in DESIGN.md §3).  104 bytes.       */

@@ -19,7 +19,7 @@
 //                     own seen bitmap and lists                          [overlapped]
 //       -- signal "maintain(r) applied" (maintain CTA -> job CTAs) --
 //   The signals are release/acquire counters; nobody waits for anything it does
-//   not depend on.  With no augmented tier (cap_A = 0) jobs never interact and
+//   not depend on.  With no tracked tier (cap_A = 0, evict_tiers = A) jobs never interact and
 //   the job CTAs run their rounds without any signal.
 //
 // Pool counts: for each pool (job x {A, D, E}, plus the storage pool S) a count
@@ -47,6 +47,7 @@ namespace seneca {
 namespace {
 
 constexpr uint32_t T_S = 0, T_E = 1, T_D = 2, T_A = 3, SUBST = 4;
+constexpr uint32_t kNewCons = 0x80;          // internal s_osrc flag: consumer set joined this round
 constexpr uint32_t kMaxJobs = 32;
 constexpr uint32_t kMaxReplicas = 64;        // independent replay instances per context
 constexpr uint32_t kMaxBatch = 4096;
@@ -71,6 +72,8 @@ struct JobDev {           // per-job persistent walk state (workspace)
 struct Cfg {
     uint32_t N, NW, NB, NS, NBp;     // samples, words/bitmap, blocks, superblocks, padded blocks
     uint32_t J, Bmax, maxT, cap_a, cap_d, cap_e;
+    uint32_t evict_all;              // evict_tiers = ALL (R-O21): every cached tier is tracked
+    uint32_t cap_t;                  // capacity of the tracked tiers (cap_a, or cap_a + cap_d + cap_e)
     uint32_t Nrow;                   // row stride of the permutation / lap lists (N rounded up to 64)
     uint32_t FL;                     // capacity of one refill buffer
     uint64_t seed;
@@ -85,7 +88,7 @@ struct Lay {
     uint32_t *cnt8;                  // [3J+1][NBp] u8 block counts, 4 per word (one 32-B row per superblock)
     uint32_t *cnt_sup;               // [3J+1][NS] superblock counts (kept in shared memory while running)
     uint32_t *cnt_tot;               // [3J+1]
-    uint32_t *a_size;                // [1]
+    uint32_t *tsize;                 // [4] tier sizes by tier code (E 1, D 2, A 3)
     uint32_t *perms;                 // [J][maxT][N]
     uint32_t *laps;                  // [J][2][N]
     uint32_t *perm_ready;            // [J][maxT]
@@ -94,9 +97,11 @@ struct Lay {
     uint32_t *out_ids;               // [J][Bmax] replay scratch
     uint8_t *out_src;                // [J][Bmax]
     uint32_t *evict_push;            // ring [J*Bmax]: entries whose consumer count reached |active|
-    uint32_t *fill_n;                // [2] refills of the rounds using fill buffer 0 / 1
-    uint32_t *evict_list;            // [max(cap_a,1)]
-    uint32_t *fill_list;             // [2][FL], FL = max(cap_a,1) + J*Bmax; buffer = round parity
+    uint32_t *fill_n;                // [2][4] per round parity: refills k, of which to A, to D (rest E)
+    uint32_t *evict_list;            // [max(cap_t,1)] full-scan eviction candidates
+    uint32_t *fill_list;             // [2][FL], FL = max(cap_t,1) + J*Bmax; buffer = round parity
+    uint32_t *ev_ed;                 // [2][max(cap_e+cap_d,1)] evicted E/D ids (bit 31: E) per parity
+    uint32_t *ev_ed_n;               // [2]
     seneca_job_epoch_stats *stats;   // [J][maxT]
     unsigned long long *evicted, *refilled;
     uint32_t *err;
@@ -547,9 +552,13 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
             if (hit) {
                 if (P.out_ids) { P.out_ids[row + s] = i; P.out_src[row + s] = (uint8_t)t; }
                 s_oid[s] = i;
-                s_osrc[s] = (uint8_t)t;
+                // kNewCons: j joined the consumer set now (A hits always do; E/D hits
+                // under evict_tiers = ALL unless j consumed them before, R-O21)
+                uint32_t flag = 0;
+                if (t == T_A) { atomicOr(cons_j + w, b); flag = kNewCons; }
+                else if (C.evict_all && !(atomicOr(cons_j + w, b) & b)) flag = kNewCons;
+                s_osrc[s] = (uint8_t)(t | flag);
                 atomicOr(seen_j + w, b);
-                if (t == T_A) atomicOr(cons_j + w, b);
                 count_add(L, C, pool_of(j, t), i, 0xffffffffu, s_sup + (pool_of(j, t) - j * 3) * C.NS);
                 atomicAdd(&S.hits[t == T_A ? 0 : (t == T_D ? 1 : 2)], 1u);
             } else {
@@ -600,7 +609,8 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
             const uint32_t id = s_sub[u];
             const uint32_t w = id >> 5, b = 1u << (id & 31);
             atomicOr(seen_j + w, b);
-            if (tt == 0) atomicOr(cons_j + w, b);
+            if (tt == 0) { atomicOr(cons_j + w, b); s_osrc[s_miss[u]] |= kNewCons; }
+            else if (C.evict_all && !(atomicOr(cons_j + w, b) & b)) s_osrc[s_miss[u]] |= kNewCons;
             count_add(L, C, j * 3 + tt, id, 0xffffffffu, s_sup + tt * C.NS);
         }
     }
@@ -641,18 +651,18 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
         S.tot[2] -= k2;
     }
 
-    // a6: digest, transcript; an A entry whose consumer count reaches |active| is
-    // pushed for eviction at the round end (R-O5).  The per-tier counters follow
+    // a6: digest, transcript; a tracked entry whose consumer count reaches
+    // |active| is pushed for eviction at the round end (R-O5, R-O21).  The per-tier counters follow
     // from the phase counts: hits per tier, k_t substitutes, m - q storage.
     unsigned long long dig = 0;
     unsigned long long* trow = P.transcript ? P.transcript + S.rep * P.tr_rep + ((size_t)j * C.maxT + e) * C.N : nullptr;
     const uint32_t lane = tid & 31;
     for (uint32_t s = tid; s < need; s += T) {
         const uint32_t i = s_oid[s];
-        const uint32_t src = s_osrc[s];
+        const uint32_t src = s_osrc[s] & 7u;
         dig += splitmix64(((uint64_t)(nbase + s) << 35) | ((uint64_t)src << 32) | i);
         if (trow) trow[nbase + s] = ((unsigned long long)src << 32) | i;
-        if ((src & 3u) == T_A) {
+        if (s_osrc[s] & kNewCons) {
             if (atomicAdd(L.cons_cnt + i, 1u) + 1u == n_act) {
                 L.evict_push[atomicAdd(L.bar + 3, 1u) % (C.J * C.Bmax)] = i;
                 atomicAdd(&S.npush, 1u);
@@ -691,7 +701,11 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
 
 // ------------------------------------------------------------------ maintain (a7)
 struct MaintSmem {
-    uint32_t ne, kmax, kspec, deficit0, PS, sizeA, prev_k;
+    uint32_t ne, kmax, kspec, deficit0, PS, prev_k;
+    uint32_t size[4];        // tier sizes by tier code (E 1, D 2, A 3), live while running
+    uint32_t def[4];         // round-start deficits cap_t - |t| of the tracked tiers
+    uint32_t ne_t[4];        // evictions of this round by tier
+    uint32_t ned;            // E/D evictions listed for the job CTAs
     uint32_t ne_push, push_base;
     uint32_t add[kMaxJobs];
     uint32_t scan[33];
@@ -710,19 +724,26 @@ __device__ void maint_refill_select(const Lay& L, const Cfg& C, MaintSmem& M, co
     __syncthreads();
 }
 
-// eviction of A entries consumed by every active job (R-O5, R-O6), refill from
-// the storage pool as of round start (R-O8), counts kept exact.
+// eviction of tracked entries (A, or every cached tier under evict_tiers = ALL)
+// consumed by every active job (R-O5, R-O6, R-O21), refill from the storage pool
+// as of round start, tier by tier A -> D -> E from one keyed rank stream (R-O8,
+// R-O21), counts kept exact.
 __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSmem& M, uint32_t* s_pre,
                             uint32_t* s_supS, uint64_t r, uint32_t active, bool full_scan, bool speculated,
                             uint32_t ne_push, uint32_t push_base, PhaseTimer& TM) {
     const uint32_t tid = threadIdx.x, T = blockDim.x;
-    if (tid == 0) M.ne = full_scan ? 0u : ne_push;
+    if (tid == 0) {
+        M.ne = full_scan ? 0u : ne_push;
+        M.ne_t[0] = M.ne_t[1] = M.ne_t[2] = M.ne_t[3] = 0;
+        M.ned = 0;
+    }
     __syncthreads();
     if (full_scan) {
-        // the active set changed (R-O6): every A entry is a candidate; the consumer
-        // counts of the survivors are rebuilt for the new active set
+        // the active set changed (R-O6): every tracked entry is a candidate; the
+        // consumer counts of the survivors are rebuilt for the new active set
         for (uint32_t w = tid; w < C.NW; w += T) {
-            const uint32_t a_w = ldcg(L.bm_a + w);
+            const uint32_t a_w = C.evict_all ? (ldcg(L.bm_a + w) | ldcg(L.bm_d + w) | ldcg(L.bm_e + w))
+                                             : ldcg(L.bm_a + w);
             if (!a_w) continue;
             uint32_t ev = a_w;
             for (uint32_t m = active; m; m &= m - 1) ev &= ldcg(L.cons + (size_t)(__ffs(m) - 1) * C.NW + w);
@@ -752,27 +773,43 @@ __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSm
     }
     const uint32_t spidx = 3 * C.J;
     const uint32_t ring = C.J * C.Bmax;
+    uint32_t* ev_ed = L.ev_ed + (size_t)(r & 1) * max(C.cap_e + C.cap_d, 1u);
     for (uint32_t u = tid; u < ne; u += T) {
         const uint32_t i = full_scan ? L.evict_list[u] : ldcg(L.evict_push + (push_base + u) % ring);
         const uint32_t w = i >> 5, b = 1u << (i & 31);
-        atomicAnd(L.bm_a + w, ~b);
+        uint32_t t = T_A;
+        if (C.evict_all) {
+            t = (ldcg(L.bm_a + w) & b) ? T_A : ((ldcg(L.bm_d + w) & b) ? T_D : T_E);
+            if (t != T_A) ev_ed[atomicAdd(&M.ned, 1u)] = i | (t == T_E ? 0x80000000u : 0u);
+        }
+        atomicAnd((t == T_A ? L.bm_a : (t == T_D ? L.bm_d : L.bm_e)) + w, ~b);
+        atomicAdd(&M.ne_t[t], 1u);
         for (uint32_t a = 0; a < C.J; ++a) atomicAnd(L.cons + (size_t)a * C.NW + w, ~b);
         L.cons_cnt[i] = 0;
         count_add(L, C, spidx, i, 1u, s_supS);
     }
-    // refills enter A with no consumers; each job CTA adds them to its own A pool
-    // before its next classification (R-O8)
+    __syncthreads();
+    // tier split of the k refill positions: A, then D, then E, each up to its deficit
+    const uint32_t kA = min(M.def[T_A] + M.ne_t[T_A], k);
+    const uint32_t kD = min(M.def[T_D] + M.ne_t[T_D], k - kA);
+    // refills enter their tier with no consumers; each job CTA adds them to its
+    // own pools before its next classification (R-O8)
     const uint32_t* fill = L.fill_list + (size_t)(r & 1) * C.FL;
     for (uint32_t u = tid; u < k; u += T) {
         const uint32_t i = ldcg(fill + u);
-        atomicOr(L.bm_a + (i >> 5), 1u << (i & 31));
+        uint32_t* bm = u < kA ? L.bm_a : (u < kA + kD ? L.bm_d : L.bm_e);
+        atomicOr(bm + (i >> 5), 1u << (i & 31));
         count_add(L, C, spidx, i, 0xffffffffu, s_supS);
     }
     __syncthreads();
     if (tid == 0) {
-        L.fill_n[r & 1] = k;
-        M.PS = M.PS + ne - k;          // storage pool and |A| live in shared memory while running
-        M.sizeA = M.sizeA - ne + k;
+        uint32_t* fn = L.fill_n + (r & 1) * 4;
+        fn[0] = k; fn[1] = kA; fn[2] = kD;
+        L.ev_ed_n[r & 1] = M.ned;
+        M.PS = M.PS + ne - k;          // storage pool and tier sizes live in shared memory while running
+        M.size[T_A] += kA - M.ne_t[T_A];
+        M.size[T_D] += kD - M.ne_t[T_D];
+        M.size[T_E] += (k - kA - kD) - M.ne_t[T_E];
         *L.evicted += ne;
         *L.refilled += k;
         M.prev_k = k;
@@ -781,22 +818,43 @@ __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSm
     TM.tick(4);
 }
 
-// Job j's A pool gains the refills of round r it has not seen (its CTA alone
-// owns its pool counts; recount at an epoch start covers them instead).
+// Job j's pools follow round r's maintain (its CTA alone owns its pool counts;
+// a recount at an epoch start covers everything instead): refills it has not
+// seen join the pool of their tier (empty consumer sets), and under
+// evict_tiers = ALL evicted E/D entries it has not seen leave its E/D pool (an
+// evicted A entry was consumed by j, so it was in no A pool of j).
 __device__ void job_take_refills(const Lay& L, const Cfg& C, JobSmem& S, uint32_t j, uint64_t r, uint32_t* s_sup) {
-    const uint32_t kf = ldcg(L.fill_n + (r & 1));
+    const uint32_t* fn = L.fill_n + (r & 1) * 4;
+    const uint32_t kf = ldcg(fn), kA = ldcg(fn + 1), kD = ldcg(fn + 2);
     const uint32_t* fill = L.fill_list + (size_t)(r & 1) * C.FL;
     const uint32_t* seen_j = L.seen + (size_t)j * C.NW;
-    uint32_t add = 0;
+    uint32_t addA = 0, addD = 0, addE = 0;   // registers (no indexed local array)
     for (uint32_t u = threadIdx.x; u < kf; u += blockDim.x) {
         const uint32_t i = ldcg(fill + u);
         if (!((ldcg(seen_j + (i >> 5)) >> (i & 31)) & 1u)) {
-            count_add(L, C, j * 3 + 0, i, 1u, s_sup);
-            ++add;
+            const uint32_t tt = u < kA ? 0u : (u < kA + kD ? 1u : 2u);
+            count_add(L, C, j * 3 + tt, i, 1u, s_sup + tt * C.NS);
+            addA += tt == 0; addD += tt == 1; addE += tt == 2;
         }
     }
-    add = warp_sum(add);
-    if ((threadIdx.x & 31) == 0 && add) atomicAdd(&S.tot[0], add);
+    if (C.evict_all) {
+        const uint32_t ne = ldcg(L.ev_ed_n + (r & 1));
+        const uint32_t* ev = L.ev_ed + (size_t)(r & 1) * max(C.cap_e + C.cap_d, 1u);
+        for (uint32_t u = threadIdx.x; u < ne; u += blockDim.x) {
+            const uint32_t x = ldcg(ev + u), i = x & 0x7fffffffu;
+            if (!((ldcg(seen_j + (i >> 5)) >> (i & 31)) & 1u)) {
+                const uint32_t tt = (x >> 31) ? 2u : 1u;
+                count_add(L, C, j * 3 + tt, i, 0xffffffffu, s_sup + tt * C.NS);
+                addD -= tt == 1; addE -= tt == 2;   // wraps; the sums below are mod 2^32
+            }
+        }
+    }
+    addA = warp_sum(addA); addD = warp_sum(addD); addE = warp_sum(addE);
+    if ((threadIdx.x & 31) == 0) {
+        if (addA) atomicAdd(&S.tot[0], addA);
+        if (addD) atomicAdd(&S.tot[1], addD);
+        if (addE) atomicAdd(&S.tot[2], addE);
+    }
 }
 
 // ------------------------------------------------------------------ the persistent round kernel
@@ -837,9 +895,10 @@ ods_rounds(const __grid_constant__ Lays LS, const __grid_constant__ Cfg C, const
     WalkPrefetch pfs;
     pfs.wseen = s_wseen;
     const WalkPrefetch* pf = P.mode == 0 ? &pfs : nullptr;
-    // with no augmented tier there is no cross-job interaction at all (E and D are
-    // static, maintain has nothing to do): the job CTAs run their rounds independently
-    const bool coupled = C.cap_a > 0;
+    // with no tracked tier (cap_A = 0 and evict_tiers = A) there is no cross-job
+    // interaction at all (E and D are static, maintain has nothing to do): the job
+    // CTAs run their rounds independently
+    const bool coupled = C.cap_t > 0;
     if (is_maint && !coupled) return;
 
     if (tid < kMaxJobs) { s_n[tid] = P.n0[tid]; s_e[tid] = P.e0[tid]; }
@@ -860,7 +919,7 @@ ods_rounds(const __grid_constant__ Lays LS, const __grid_constant__ Cfg C, const
         if (tid == 0) {
             M.prev_k = blockDim.x;
             M.PS = ldcg(L.cnt_tot + 3 * C.J);
-            M.sizeA = ldcg(L.a_size);
+            for (int t = 0; t < 4; ++t) M.size[t] = ldcg(L.tsize + t);
         }
         for (uint32_t k = tid; k < C.NS; k += blockDim.x) s_sup[k] = ldcg(L.cnt_sup + (size_t)3 * C.J * C.NS + k);
     }
@@ -900,11 +959,19 @@ ods_rounds(const __grid_constant__ Lays LS, const __grid_constant__ Cfg C, const
         bool spec = false;
         // speculative refill ranks for the round about to be played: the storage
         // pool as of round start cannot change before this round's maintain
+        // round-start deficits of the tracked tiers (A; D and E under evict_tiers = ALL)
+        auto set_deficits = [&]() {
+            M.def[T_S] = 0;
+            M.def[T_A] = C.cap_a - M.size[T_A];
+            M.def[T_D] = C.evict_all ? C.cap_d - M.size[T_D] : 0u;
+            M.def[T_E] = C.evict_all ? C.cap_e - M.size[T_E] : 0u;
+            M.deficit0 = M.def[T_A] + M.def[T_D] + M.def[T_E];
+        };
         auto speculate = [&](uint64_t r, uint32_t part, uint32_t departing) -> bool {
             const uint32_t active_after = s_active & ~departing;
-            if (!(active_after && C.cap_a > 0) || departing) return false;
+            if (!(active_after && C.cap_t > 0) || departing) return false;
+            if (tid == 0) set_deficits();
             if (tid == 0) {
-                M.deficit0 = C.cap_a - M.sizeA;
                 uint32_t cand = 0;
                 for (uint32_t m = part; m; m &= m - 1) cand += need_of(__ffs(m) - 1);
                 M.kmax = min(M.deficit0 + cand, M.PS);
@@ -938,8 +1005,8 @@ ods_rounds(const __grid_constant__ Lays LS, const __grid_constant__ Cfg C, const
             }
             __syncthreads();
             TM.tick(2);
-            if (active_after && C.cap_a > 0) {
-                if (!spec && tid == 0) M.deficit0 = C.cap_a - M.sizeA;
+            if (active_after && C.cap_t > 0) {
+                if (!spec && tid == 0) set_deficits();
                 __syncthreads();
                 maint_apply(L, C, P, M, s_pre, s_sup, r, active_after, departing != 0, spec, M.ne_push, M.push_base, TM);
             }
@@ -1023,7 +1090,7 @@ ods_rounds(const __grid_constant__ Lays LS, const __grid_constant__ Cfg C, const
         if (tid < 3) L.cnt_tot[j * 3 + tid] = S.tot[tid];
         for (uint32_t k = tid; k < 3 * C.NS; k += blockDim.x) L.cnt_sup[(size_t)j * 3 * C.NS + k] = s_sup[k];
     } else {
-        if (tid == 0) { L.cnt_tot[3 * C.J] = M.PS; *L.a_size = M.sizeA; }
+        if (tid == 0) { L.cnt_tot[3 * C.J] = M.PS; for (int t = 0; t < 4; ++t) L.tsize[t] = M.size[t]; }
         for (uint32_t k = tid; k < C.NS; k += blockDim.x) L.cnt_sup[(size_t)3 * C.J * C.NS + k] = s_sup[k];
     }
     cp_async_wait_all();
@@ -1083,7 +1150,9 @@ __global__ void ods_init_tiers(const __grid_constant__ Lays LS, const __grid_con
         uint32_t* bm = pos < C.cap_a ? L.bm_a : (pos < C.cap_a + cap_d ? L.bm_d : L.bm_e);
         atomicOr(bm + (i >> 5), 1u << (i & 31));
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) *L.a_size = C.cap_a;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        L.tsize[T_S] = 0; L.tsize[T_E] = cap_e; L.tsize[T_D] = cap_d; L.tsize[T_A] = C.cap_a;
+    }
 }
 
 // Pool counts of every job and of the storage pool (init): one CTA of 128
@@ -1211,6 +1280,7 @@ seneca_status check_cfg(const seneca_cache_config* cfg) {
         }
     }
     if (cfg->replicas > kMaxReplicas) { set_error("replicas must be <= %u", kMaxReplicas); return SENECA_EINVAL; }
+    if (cfg->evict_tiers > 1) { set_error("evict_tiers must be 0 (A only) or 1 (all)"); return SENECA_EINVAL; }
     if (cfg->replicas > 1 && cfg->request_mode != 0) {
         set_error("caller-supplied requests (request_mode 1) need replicas <= 1"); return SENECA_EINVAL;
     }
@@ -1248,26 +1318,30 @@ Sizes compute_sizes(const seneca_cache_config* cfg) {
     C.cap_a = (uint32_t)cfg->cap_a;
     C.cap_d = (uint32_t)cfg->cap_d;
     C.cap_e = (uint32_t)cfg->cap_e;
+    C.evict_all = cfg->evict_tiers;
+    C.cap_t = C.evict_all ? C.cap_a + C.cap_d + C.cap_e : C.cap_a;
     C.seed = cfg->seed;
     C.Nrow = (C.N + 63) & ~63u;
-    C.FL = (uint32_t)(std::max<size_t>(cfg->cap_a, 1) + (size_t)C.J * C.Bmax);
+    C.FL = (uint32_t)(std::max<size_t>(C.cap_t, 1) + (size_t)C.J * C.Bmax);
     const size_t W = (size_t)C.NW * 4, P = 3 * (size_t)C.J + 1;
-    const size_t capl = std::max<size_t>(cfg->cap_a, 1) * 4;
+    const size_t capl = std::max<size_t>(C.cap_t, 1) * 4;
+    const size_t edl = std::max<size_t>(C.cap_e + C.cap_d, 1) * 4;
     const size_t sz[] = {
         W, W, W,                                            // 0-2 bm_e, bm_d, bm_a
         W * C.J, W * C.J,                                   // 3-4 seen, cons
         (size_t)C.Nrow * 4,                                 // 5 cons_cnt
         P * C.NBp, P * C.NS * 4, P * 4,                     // 6-8 counts
-        4,                                                  // 9 a_size
+        16,                                                 // 9 tsize
         (size_t)C.J * C.maxT * C.Nrow * 4,                  // 10 perms
         (size_t)C.J * 2 * C.Nrow * 4,                       // 11 laps
         (size_t)C.J * C.maxT * 4, (size_t)C.J * C.maxT * 4, // 12-13 perm_ready, perm_done
         (size_t)C.J * sizeof(JobDev),                       // 14 jobs
         (size_t)C.J * C.Bmax * 4, (size_t)C.J * C.Bmax,     // 15-16 out_ids, out_src
-        (size_t)C.J * C.Bmax * 4, 8,                        // 17-18 evict_push, fill_n
+        (size_t)C.J * C.Bmax * 4, 32,                       // 17-18 evict_push, fill_n
         capl, 2 * (capl + (size_t)C.J * C.Bmax * 4),        // 19-20 evict, fill [2]
         (size_t)C.J * C.maxT * sizeof(seneca_job_epoch_stats),  // 21 stats
         8, 8, 4, 16, 256,                                   // 22-26 evicted, refilled, err, bar, phase
+        C.evict_all ? 2 * edl : 4, 8,                       // 27-28 ev_ed, ev_ed_n
     };
     size_t at = 0;
     for (size_t k = 0; k < sizeof(sz) / sizeof(sz[0]); ++k) {
@@ -1291,7 +1365,7 @@ Lay carve(const Sizes& z, char* base, uint64_t seed) {
     L.cnt8 = (uint32_t*)(base + z.off[6]);
     L.cnt_sup = (uint32_t*)(base + z.off[7]);
     L.cnt_tot = (uint32_t*)(base + z.off[8]);
-    L.a_size = (uint32_t*)(base + z.off[9]);
+    L.tsize = (uint32_t*)(base + z.off[9]);
     L.perms = (uint32_t*)(base + z.off[10]);
     L.laps = (uint32_t*)(base + z.off[11]);
     L.perm_ready = (uint32_t*)(base + z.off[12]);
@@ -1309,6 +1383,8 @@ Lay carve(const Sizes& z, char* base, uint64_t seed) {
     L.err = (uint32_t*)(base + z.off[24]);
     L.bar = (uint32_t*)(base + z.off[25]);
     L.phase = (unsigned long long*)(base + z.off[26]);
+    L.ev_ed = (uint32_t*)(base + z.off[27]);
+    L.ev_ed_n = (uint32_t*)(base + z.off[28]);
     return L;
 }
 

@@ -35,9 +35,9 @@ def caps_of(c):
     return caps[0], caps[1], caps[2]
 
 
-def make_pair(n, batch, target, ce, cd, ca, seed, transcript=True):
-    o = O.ODS(n, batch, target, ce, cd, ca, seed, transcript=transcript)
-    g = P.ODSContext(n, batch, target, ce, cd, ca, seed)
+def make_pair(n, batch, target, ce, cd, ca, seed, transcript=True, evict_all=False):
+    o = O.ODS(n, batch, target, ce, cd, ca, seed, transcript=transcript, evict_all=evict_all)
+    g = P.ODSContext(n, batch, target, ce, cd, ca, seed, evict_tiers=int(evict_all))
     return o, g
 
 
@@ -61,8 +61,8 @@ def compare_state(o, g, check_transcript=None):
     g.sync()
 
 
-def replay_pair(n, batch, target, ce, cd, ca, seed):
-    o, g = make_pair(n, batch, target, ce, cd, ca, seed)
+def replay_pair(n, batch, target, ce, cd, ca, seed, evict_all=False):
+    o, g = make_pair(n, batch, target, ce, cd, ca, seed, evict_all=evict_all)
     tr = g.new_transcript()
     r_g = g.replay_epochs(max(target), tr)
     r_o = o.replay_epochs(max(target))
@@ -300,3 +300,61 @@ def test_replicas_that_cannot_be_co_resident_are_rejected():
     with pytest.raises(S.SenecaError) as ei:
         P.ODSContext(1000, [32, 32], [1, 1], 10, 10, 10, 1, replicas=64)      # 64 x 3 CTAs > 148 SMs
     assert ei.value.status == S.EINVAL
+
+
+# ---------------------------------------------------------------- evict_tiers = ALL (R-O21)
+@pytest.mark.parametrize("block", range(4))
+def test_evict_all_random_tiny_configs(block):
+    st = synth.Stream(9000 + block)
+    for _ in range(50):
+        c = synth.random_tiny_ods(st)
+        replay_pair(c["n_total"], c["batch"], c["target"], c["cap_e"], c["cap_d"], c["cap_a"], c["seed"],
+                    evict_all=True)
+
+
+@pytest.mark.parametrize("name", ["toy", "imagenet1k", "openimages", "imagenet22k"])
+def test_evict_all_scaled_configs_full_replay(name):
+    """SURVEY 8(d) parity variant: every config scaled down (N/64) with split
+    34-33-33 in the second eviction mode; the toy config at its own size."""
+    scale = 1 if name == "toy" else 64
+    c = synth.ods_config(name, scale=scale, seed=2)
+    ce, cd, ca = caps_of(c)
+    o, g = replay_pair(c["n_total"], c["batch"], c["target"], ce, cd, ca, 2, evict_all=True)
+    assert o.stats()[1] > 0                                      # evictions happened
+
+
+def test_evict_all_imagenet22k_full_size_prefix():
+    """ImageNet-22K additionally runs with evict_tiers = ALL (O4):
+    full size, its own 100-0-0 split (E churns), first rounds vs the oracle."""
+    seed = synth.PERF_SEED
+    c = synth.ods_config("imagenet22k", seed=seed)
+    ce, cd, ca = caps_of(c)
+    o, g = make_pair(c["n_total"], c["batch"], c["target"], ce, cd, ca, seed, transcript=False, evict_all=True)
+    assert g.replay_rounds(60) == 60
+    assert o.replay_rounds(60) == 60
+    torch.cuda.synchronize()
+    compare_state(o, g)
+    assert o.stats()[1] > 0
+
+
+def test_evict_all_next_batch_and_replicas():
+    n, batch, target, R = 500, [16, 40, 9], [2, 1, 2], 3
+    g = P.ODSContext(n, batch, target, 60, 50, 40, 31, replicas=R, evict_tiers=1)
+    oracles = [O.ODS(n, batch, target, 60, 50, 40, 31 + k, evict_all=True) for k in range(R)]
+    st = synth.Stream(6)
+    for _ in range(100):
+        _, _, _, act = oracles[0].job_state()
+        live = [j for j in range(3) if act[j]]
+        if not live:
+            break
+        pick = [j for j in live if st.uniform(1)[0] < 0.7] or live[:1]
+        ids_g, src_g, lens_g = g.next_batch(pick)
+        torch.cuda.synchronize()
+        for k, o in enumerate(oracles):
+            rc, ids_o, src_o, lens_o = o.round(pick)
+            assert rc == 0 and list(lens_o) == lens_g
+            for x, L_ in enumerate(lens_g):
+                assert np.array_equal(ids_g[k, x, :L_].cpu().numpy().view(np.uint32), ids_o[x, :L_])
+                assert np.array_equal(src_g[k, x, :L_].cpu().numpy(), src_o[x, :L_])
+    for k, o in enumerate(oracles):
+        compare_replica(o, g, k)
