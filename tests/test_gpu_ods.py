@@ -334,6 +334,16 @@ def test_evict_all_imagenet22k_full_size_prefix():
     assert o.replay_rounds(60) == 60
     torch.cuda.synchronize()
     compare_state(o, g)
+
+
+def test_evict_all_imagenet22k_own_split_scaled_full_replay():
+    """ImageNet-22K shape at its own 100-0-0 split (an E-only cache), N/64, whole
+    replay under evict_tiers = ALL: E entries consumed by all 8 jobs churn."""
+    c = synth.ods_config("imagenet22k", scale=64, seed=5)
+    c["split"] = (100, 0, 0)
+    ce, cd, ca = caps_of(c)
+    assert cd == 0 and ca == 0 and ce > 0
+    o, g = replay_pair(c["n_total"], c["batch"], c["target"], ce, cd, ca, 5, evict_all=True)
     assert o.stats()[1] > 0
 
 
