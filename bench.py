@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--no-profile", action="store_true", help="no CUDA-event kernel timing in the timed steps")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample duration")
+    ap.add_argument("--evict-tiers", type=int, default=0, choices=[0, 1],
+                    help="0: A only (SPEC default, the headline); 1: every cached tier (R-O21)")
     ap.add_argument("--replicas", type=int, default=-1,
                     help="also time R independent replays in one context (-1: as many as fit the GPU, 0: skip)")
     return ap.parse_args()
@@ -149,7 +151,7 @@ def run_reference(args, rank, world):
     decisions = 0
     t_tot = 0.0
     for s in range(args.warmup + args.steps):
-        o = O.ODS(c["n_total"], c["batch"], c["target"], ce, cd, ca, c["seed"])
+        o = O.ODS(c["n_total"], c["batch"], c["target"], ce, cd, ca, c["seed"], evict_all=bool(args.evict_tiers))
         t0 = time.perf_counter()
         done = o.replay_rounds(rounds_per_step)
         dt = time.perf_counter() - t0
@@ -174,12 +176,12 @@ def cpu_baseline(args, c, caps):
     import oracle as O
     ce, cd, ca = caps
     # calibrate: a short run, then scale to ~args.cpu_seconds
-    o = O.ODS(c["n_total"], c["batch"], c["target"], ce, cd, ca, c["seed"])
+    o = O.ODS(c["n_total"], c["batch"], c["target"], ce, cd, ca, c["seed"], evict_all=bool(args.evict_tiers))
     t0 = time.perf_counter()
     o.replay_rounds(50)
     per = (time.perf_counter() - t0) / 50
     rounds = max(50, int(args.cpu_seconds / max(per, 1e-6)))
-    o = O.ODS(c["n_total"], c["batch"], c["target"], ce, cd, ca, c["seed"])
+    o = O.ODS(c["n_total"], c["batch"], c["target"], ce, cd, ca, c["seed"], evict_all=bool(args.evict_tiers))
     t0 = time.perf_counter()
     done = o.replay_rounds(rounds)
     dt = time.perf_counter() - t0
@@ -279,7 +281,7 @@ def main():
     nsplit = S.mdp_num_splits(args.mdp_grid_step)
     d_res = torch.empty(args.mdp_profiles * S.RESULT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
     d_grid = None if args.no_grid else torch.empty((args.mdp_profiles, nsplit), dtype=torch.float64, device=dev)
-    cfg = S.make_config(c["n_total"], c["batch"], c["target"], ce, cd, ca, c["seed"])
+    cfg = S.make_config(c["n_total"], c["batch"], c["target"], ce, cd, ca, c["seed"], evict_tiers=args.evict_tiers)
     ws_bytes = S.state_bytes(cfg)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)      # > 126 MB L2
@@ -342,7 +344,8 @@ def main():
     # ---- parity gates (outside the timed region)
     parity = {}
     S.sync_status(last_ctx, stream)
-    gold_path = os.path.join(ROOT, "tests", "golden", f"oracle_{args.workload}_seed{c['seed']}.json")
+    gold_path = os.path.join(ROOT, "tests", "golden", f"oracle_{args.workload}_seed{c['seed']}"
+                             f"{'_evictall' if args.evict_tiers else ''}.json")
     st_raw = None
     v = S.read_state(last_ctx)
     off = v.d_stats - ws.data_ptr()
@@ -378,7 +381,8 @@ def main():
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
         R = args.replicas if args.replicas > 0 else min(64, sms // (len(c["batch"]) + 1))
         rseed = (synth.PERF_SEED + 64 * rank) & 0xFFFFFFFFFFFFFFFF
-        rcfg = S.make_config(c["n_total"], c["batch"], c["target"], ce, cd, ca, rseed, replicas=R)
+        rcfg = S.make_config(c["n_total"], c["batch"], c["target"], ce, cd, ca, rseed, replicas=R,
+                             evict_tiers=args.evict_tiers)
         rbytes = S.state_bytes(rcfg)
         del ws_r_holder[:]
         ws_r = torch.empty(rbytes, dtype=torch.uint8, device=dev)
@@ -526,6 +530,7 @@ def main():
             vs_baseline=None, dtype="u32", data="synthetic",
             config=workload_config(c, args.workload, dict(
                 rounds_per_step=rounds_tot // args.steps, decisions_per_step=dec_per_step,
+                evict_tiers="all" if args.evict_tiers else "A",
                 mdp_profiles=args.mdp_profiles, mdp_grid_step_pct=args.mdp_grid_step,
                 mdp_grid_written=d_grid is not None,
                 parallelism=f"{world} independent replays (seed+rank) + {world} MDP profile slices",

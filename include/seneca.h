@@ -184,6 +184,30 @@ typedef struct {
     uint64_t digest;       /* sum over delivery position q of splitmix64(q<<35 | src<<32 | id)  */
 } seneca_job_epoch_stats;
 
+/* Epoch model on top of a replay (SPEC `run` and
+ * `preprocessing_ops`).  For every per job-epoch counter row:
+ *   epoch_seconds  = served_A/DSI_A + served_D/DSI_D + served_E/DSI_E + served_S/DSI_S
+ *                    (epoch time accounted over tiers), summed in that order;
+ *   dsi_mix        = Eq. 9 with N_t := the epoch's served_t:
+ *                    ((sA/N) DSI_A + (sD/N) DSI_D) + (sE/N) DSI_E) + (sS/N) DSI_S;
+ *   decode_aug_ops = served_S + served_E, aug_only_ops = served_D;
+ *   hit_rate       = (served_E + served_D + served_A) / N.
+ * IEEE binary64, one rounding per operation, bit-identical to the oracle.    */
+typedef struct {
+    double   epoch_seconds;
+    double   dsi_mix;
+    uint64_t decode_aug_ops;
+    uint64_t aug_only_ops;
+    double   hit_rate;
+} seneca_epoch_metrics;
+
+/* d_stats: device [n_rows] counter rows (e.g. seneca_state_view.d_stats),
+ * h_dsi: host {DSI_A, DSI_D, DSI_E, DSI_S} (finite, > 0; e.g. from
+ * seneca_mdp_eval's d_tiers), d_out: device [n_rows].  EINVAL on NULL
+ * pointers, n_rows == 0, n_total == 0 or a non-positive / non-finite DSI.   */
+seneca_status seneca_epoch_model(const seneca_job_epoch_stats* d_stats, uint32_t n_rows, uint64_t n_total,
+                                 const double h_dsi[4], seneca_epoch_metrics* d_out, void* stream);
+
 /* Device views into the workspace, valid until seneca_destroy.              */
 typedef struct {
     uint64_t n_total;

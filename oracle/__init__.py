@@ -100,6 +100,8 @@ def _declare(L):
     L.oracle_mdp_sweep.argtypes = [C.c_void_p, C.c_uint64, C.c_uint32, C.c_void_p, C.c_void_p]
     L.oracle_mdp_sweep.restype = C.c_int
     L.oracle_metadata_bytes.argtypes = [C.c_uint64, C.c_uint32]; L.oracle_metadata_bytes.restype = C.c_uint64
+    L.oracle_epoch_metrics.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.POINTER(C.c_double), C.c_void_p]
+    L.oracle_epoch_metrics.restype = None
     L.oracle_ods_create.argtypes = [C.c_uint64, C.c_uint32, u32p, u32p, C.c_uint64, C.c_uint64,
                                     C.c_uint64, C.c_uint64, C.c_int, C.c_int]
     L.oracle_ods_create.restype = C.c_void_p
@@ -199,6 +201,20 @@ def mdp_sweep(profiles: np.ndarray, g: int, want_grid: bool = False):
     if rc != 0:
         raise ValueError(f"oracle_mdp_sweep rc={rc}")
     return res, grid
+
+
+EPOCH_DTYPE = np.dtype([("epoch_seconds", "<f8"), ("dsi_mix", "<f8"), ("decode_aug_ops", "<u8"),
+                        ("aug_only_ops", "<u8"), ("hit_rate", "<f8")])
+
+
+def epoch_metrics(stats: np.ndarray, n_total: int, dsi) -> np.ndarray:
+    """Per job-epoch model metrics (NEXT-1) from oracle stats rows (any shape);
+    dsi = (DSI_A, DSI_D, DSI_E, DSI_S)."""
+    st = np.ascontiguousarray(stats).reshape(-1)
+    out = np.zeros(len(st), EPOCH_DTYPE)
+    d = (C.c_double * 4)(*[float(x) for x in dsi])
+    lib().oracle_epoch_metrics(st.ctypes.data, len(st), int(n_total), d, out.ctypes.data)
+    return out.reshape(stats.shape)
 
 
 def metadata_bytes(n_total: int, n_jobs: int) -> int:

@@ -770,3 +770,42 @@ int oracle_ods_read_transcript(void *h, uint64_t *out)
     memcpy(out, o->transcript, (size_t)o->J * o->max_target * o->N * 8);
     return 1;
 }
+
+/* ========================================================================= */
+/* 4. Epoch model on top of a replay (SPEC run and       */
+/*    preprocessing_ops; hit rate P:L1293).                      */
+/* ========================================================================= */
+
+typedef struct {
+    double   epoch_seconds;   /* sum over tiers of served_t / DSI_t         */
+    double   dsi_mix;         /* Eq. 9 with N_t := served_t of the epoch */
+    uint64_t decode_aug_ops;  /* storage fetches + encoded-tier hits         */
+    uint64_t aug_only_ops;    /* decoded-tier hits                                    */
+    double   hit_rate;        /* (served_E + served_D + served_A) / N       */
+} oracle_epoch_row;
+
+/* dsi[] = {DSI_A, DSI_D, DSI_E, DSI_S} (oracle_tiers order).  Served counts
+ * are indexed by tier code S 0, E 1, D 2, A 3.  Sums in the tier order of
+ * Eq. 9 (A, D, E, S), one IEEE operation per step.                           */
+void oracle_epoch_metrics(const oracle_stats *st, uint64_t n_rows, uint64_t N, const double dsi[4],
+                          oracle_epoch_row *out)
+{
+    double dN = (double)N;
+    for (uint64_t r = 0; r < n_rows; ++r) {
+        const uint64_t *sv = st[r].served;
+        double cA = (double)sv[T_A], cD = (double)sv[T_D], cE = (double)sv[T_E], cS = (double)sv[T_S];
+        double t = cA / dsi[0];
+        t = t + cD / dsi[1];
+        t = t + cE / dsi[2];
+        t = t + cS / dsi[3];
+        double v = (cA / dN) * dsi[0];
+        v = v + (cD / dN) * dsi[1];
+        v = v + (cE / dN) * dsi[2];
+        v = v + (cS / dN) * dsi[3];
+        out[r].epoch_seconds = t;
+        out[r].dsi_mix = v;
+        out[r].decode_aug_ops = sv[T_S] + sv[T_E];
+        out[r].aug_only_ops = sv[T_D];
+        out[r].hit_rate = (double)(sv[T_E] + sv[T_D] + sv[T_A]) / dN;
+    }
+}

@@ -160,6 +160,15 @@ class ODSContext:
         tier[a == 1] = 3
         return tier, bits(v.d_seen, self.J), bits(v.d_cons, self.J)
 
+    def epoch_model(self, dsi, k=0) -> np.ndarray:
+        """Replica k's per job-epoch model metrics (NEXT-1) on the device:
+        EPOCH_DTYPE [J][max_target]; dsi = (DSI_A, DSI_D, DSI_E, DSI_S)."""
+        v = self.view()
+        n = self.J * v.max_target
+        out = self.torch.empty(n * seneca.EPOCH_DTYPE.itemsize, dtype=self.torch.uint8, device=self.device)
+        seneca.epoch_model(self._rep(v, v.d_stats, k), n, self.N, dsi, out, self.stream)
+        return out.cpu().numpy().view(seneca.EPOCH_DTYPE).reshape(self.J, v.max_target)
+
     def stats(self, k=0):
         """Replica k: (per job-epoch STATS_DTYPE [J][max_target], evicted, refilled)."""
         v = self.view()

@@ -1,4 +1,6 @@
-// capi.cu -- error plumbing and host-side integer helpers of libseneca.so.
+// capi.cu -- error plumbing, host-side integer helpers and the epoch model
+// (seneca_epoch_model, NEXT-1) of libseneca.so.
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 
@@ -55,5 +57,53 @@ extern "C" seneca_status seneca_split_capacities(uint64_t n_total, uint64_t s_da
     caps[1] = n_d;
     caps[2] = n_a;
     caps[3] = n_total - n_a - n_d - n_e;
+    return SENECA_OK;
+}
+
+// ------------------------------------------------------------------ epoch model (NEXT-1)
+namespace seneca {
+namespace {
+__global__ void epoch_model_kernel(const seneca_job_epoch_stats* __restrict__ st, uint32_t n, uint64_t N,
+                                   double dA, double dD, double dE, double dS, seneca_epoch_metrics* __restrict__ out) {
+    const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const uint64_t sS = st[r].served[0], sE = st[r].served[1], sD = st[r].served[2], sA = st[r].served[3];
+    const double dN = __ull2double_rn(N);
+    const double cA = __ull2double_rn(sA), cD = __ull2double_rn(sD), cE = __ull2double_rn(sE),
+                 cS = __ull2double_rn(sS);
+    double t = __ddiv_rn(cA, dA);
+    t = __dadd_rn(t, __ddiv_rn(cD, dD));
+    t = __dadd_rn(t, __ddiv_rn(cE, dE));
+    t = __dadd_rn(t, __ddiv_rn(cS, dS));
+    double v = __dmul_rn(__ddiv_rn(cA, dN), dA);
+    v = __dadd_rn(v, __dmul_rn(__ddiv_rn(cD, dN), dD));
+    v = __dadd_rn(v, __dmul_rn(__ddiv_rn(cE, dN), dE));
+    v = __dadd_rn(v, __dmul_rn(__ddiv_rn(cS, dN), dS));
+    seneca_epoch_metrics m;
+    m.epoch_seconds = t;
+    m.dsi_mix = v;
+    m.decode_aug_ops = sS + sE;
+    m.aug_only_ops = sD;
+    m.hit_rate = __ddiv_rn(__ull2double_rn(sE + sD + sA), dN);
+    out[r] = m;
+}
+}  // namespace
+}  // namespace seneca
+
+extern "C" seneca_status seneca_epoch_model(const seneca_job_epoch_stats* d_stats, uint32_t n_rows, uint64_t n_total,
+                                            const double h_dsi[4], seneca_epoch_metrics* d_out, void* stream) {
+    using namespace seneca;
+    if (!d_stats || !h_dsi || !d_out || n_rows == 0 || n_total == 0) {
+        set_error("seneca_epoch_model: NULL pointer or empty input");
+        return SENECA_EINVAL;
+    }
+    for (int t = 0; t < 4; ++t)
+        if (!(h_dsi[t] > 0.0) || !std::isfinite(h_dsi[t])) {
+            set_error("seneca_epoch_model: DSI[%d] must be finite and > 0", t);
+            return SENECA_EINVAL;
+        }
+    epoch_model_kernel<<<(n_rows + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+        d_stats, n_rows, n_total, h_dsi[0], h_dsi[1], h_dsi[2], h_dsi[3], d_out);
+    SENECA_CUDA_TRY(cudaGetLastError());
     return SENECA_OK;
 }

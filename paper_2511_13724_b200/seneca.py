@@ -105,6 +105,8 @@ def lib() -> C.CDLL:
         L.seneca_mdp_sweep.argtypes = [vp, u32, u32, vp, vp, vp]; L.seneca_mdp_sweep.restype = C.c_int
         L.seneca_mdp_eval.argtypes = [vp, u32, C.POINTER(Split), u32, vp, vp, vp, vp]
         L.seneca_mdp_eval.restype = C.c_int
+        L.seneca_epoch_model.argtypes = [vp, u32, u64, C.POINTER(C.c_double), vp, vp]
+        L.seneca_epoch_model.restype = C.c_int
         L.seneca_split_capacities.argtypes = [u64, u64, u32, u32, u64, u32, u32, u32, C.POINTER(u64)]
         L.seneca_split_capacities.restype = C.c_int
         L.seneca_metadata_bytes.argtypes = [u64, u32]; L.seneca_metadata_bytes.restype = u64
@@ -130,7 +132,8 @@ def lib() -> C.CDLL:
     return _lib
 
 
-EXPORTED = ["seneca_mdp_num_splits", "seneca_mdp_sweep", "seneca_mdp_eval", "seneca_split_capacities",
+EXPORTED = ["seneca_mdp_num_splits", "seneca_mdp_sweep", "seneca_mdp_eval", "seneca_epoch_model",
+            "seneca_split_capacities",
             "seneca_metadata_bytes", "seneca_state_bytes", "seneca_init_cache",
             "seneca_ods_next_batch", "seneca_replay_epochs", "seneca_replay_rounds",
             "seneca_read_state", "seneca_sync_status", "seneca_launch_count", "seneca_destroy",
@@ -173,6 +176,21 @@ def mdp_eval(d_profiles, n_profiles: int, splits, d_values, d_counts=None, d_tie
     arr = (Split * len(splits))(*[Split(int(e), int(d), int(a), 0) for e, d, a in splits])
     _check(lib().seneca_mdp_eval(_ptr(d_profiles), n_profiles, arr, len(splits), _ptr(d_values), _ptr(d_counts),
                                  _ptr(d_tiers), _stream(stream)))
+
+
+EPOCH_DTYPE = np.dtype([("epoch_seconds", "<f8"), ("dsi_mix", "<f8"), ("decode_aug_ops", "<u8"),
+                        ("aug_only_ops", "<u8"), ("hit_rate", "<f8")])
+
+
+class EpochMetrics(C.Structure):
+    _fields_ = [("epoch_seconds", C.c_double), ("dsi_mix", C.c_double), ("decode_aug_ops", C.c_uint64),
+                ("aug_only_ops", C.c_uint64), ("hit_rate", C.c_double)]
+
+
+def epoch_model(d_stats, n_rows: int, n_total: int, dsi, d_out, stream=None):
+    """dsi = (DSI_A, DSI_D, DSI_E, DSI_S); d_out: device [n_rows] EPOCH_DTYPE rows."""
+    d = (C.c_double * 4)(*[float(x) for x in dsi])
+    _check(lib().seneca_epoch_model(_ptr(d_stats), n_rows, n_total, d, _ptr(d_out), _stream(stream)))
 
 
 def split_capacities(n_total, s_data, m_num, m_den, cache_bytes, p_e, p_d, p_a):

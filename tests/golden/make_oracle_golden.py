@@ -6,7 +6,7 @@ compare the device replay against these files (per job-epoch counters and
 digests, eviction/refill totals, a hash of the final residency/seen/consumer
 state).
 
-    python tests/golden/make_oracle_golden.py imagenet1k [seed]
+    python tests/golden/make_oracle_golden.py imagenet1k [seed [scale [evict_all]]]
 """
 import hashlib
 import json
@@ -37,18 +37,18 @@ def state_hash(tier, seen, cons):
     return h.hexdigest()
 
 
-def main(name, seed, scale=1):
+def main(name, seed, scale=1, evict_all=False):
     c = synth.ods_config(name, scale=scale, seed=seed)
     ce, cd, ca = caps_for(c)
     t0 = time.time()
-    o = O.ODS(c["n_total"], c["batch"], c["target"], ce, cd, ca, seed)
+    o = O.ODS(c["n_total"], c["batch"], c["target"], ce, cd, ca, seed, evict_all=evict_all)
     rounds = o.replay_epochs(max(c["target"]))
     dt = time.time() - t0
     st, ev, rf = o.stats()
     tier, seen, cons = o.state()
     out = dict(
         config=c["name"], seed=seed, n_total=c["n_total"], batch=c["batch"], target=c["target"],
-        caps=[ce, cd, ca], rounds=int(rounds), evicted=int(ev), refilled=int(rf),
+        caps=[ce, cd, ca], evict_tiers=int(evict_all), rounds=int(rounds), evicted=int(ev), refilled=int(rf),
         stats=[[dict(served=[int(v) for v in st[j, e]["served"]], subst=[int(v) for v in st[j, e]["subst"]],
                      req_hits=[int(v) for v in st[j, e]["req_hits"]], digest=str(int(st[j, e]["digest"])))
                 for e in range(st.shape[1])] for j in range(st.shape[0])],
@@ -56,7 +56,7 @@ def main(name, seed, scale=1):
         oracle_seconds=round(dt, 1),
         generator="tests/golden/make_oracle_golden.py (oracle/ only)",
     )
-    path = os.path.join(HERE, f"oracle_{c['name'].replace('/', '_s')}_seed{seed}.json")
+    path = os.path.join(HERE, f"oracle_{c['name'].replace('/', '_s')}_seed{seed}{'_evictall' if evict_all else ''}.json")
     with open(path, "w") as f:
         json.dump(out, f, indent=1)
     print(path, f"{dt:.1f}s", rounds, "rounds")
@@ -66,4 +66,5 @@ if __name__ == "__main__":
     name = sys.argv[1]
     seed = int(sys.argv[2], 0) if len(sys.argv) > 2 else synth.PERF_SEED
     scale = int(sys.argv[3]) if len(sys.argv) > 3 else 1
-    main(name, seed, scale)
+    evict_all = len(sys.argv) > 4 and sys.argv[4] in ("1", "all", "evict_all")
+    main(name, seed, scale, evict_all)

@@ -108,7 +108,8 @@ def test_ctypes_layouts_match_c_header(lib, tmp_path):
     probe = tmp_path / "probe.c"
     structs = {"seneca_cache_config": S.CacheConfig, "seneca_state_view": S.StateView,
                "seneca_job_epoch_stats": S.JobEpochStats, "seneca_mdp_profile": S.MdpProfile,
-               "seneca_mdp_result": S.MdpResult, "seneca_kernel_stat": S.KernelStat, "seneca_split": S.Split}
+               "seneca_mdp_result": S.MdpResult, "seneca_kernel_stat": S.KernelStat, "seneca_split": S.Split,
+               "seneca_epoch_metrics": S.EpochMetrics}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "seneca.h"', "int main(void) {"]
     for cname, ct in structs.items():
         lines.append(f'printf("{cname} sizeof %zu\\n", sizeof({cname}));')
@@ -141,3 +142,12 @@ def test_replicas_workspace_and_arguments(lib):
         with pytest.raises(S.SenecaError) as ei:
             S.state_bytes(cfg)
         assert ei.value.status == S.EINVAL
+
+
+def test_epoch_model_host_checks(lib):
+    for dsi in ((1.0, 0.0, 1.0, 1.0), (1.0, float("inf"), 1.0, 1.0), (1.0, 1.0, float("nan"), 1.0)):
+        with pytest.raises(S.SenecaError) as ei:
+            S.epoch_model(1, 1, 10, dsi, 1, stream=0)
+        assert ei.value.status == S.EINVAL
+    with pytest.raises(S.SenecaError):
+        S.epoch_model(1, 0, 10, (1.0,) * 4, 1, stream=0)

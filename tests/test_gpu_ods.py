@@ -133,7 +133,8 @@ def test_full_replay_against_oracle_golden(path):
     c = synth.ods_config(gold["config"].split("/")[0], seed=gold["seed"])
     ce, cd, ca = caps_of(c)
     assert [ce, cd, ca] == gold["caps"]
-    g = P.ODSContext(c["n_total"], c["batch"], c["target"], ce, cd, ca, gold["seed"])
+    g = P.ODSContext(c["n_total"], c["batch"], c["target"], ce, cd, ca, gold["seed"],
+                     evict_tiers=gold.get("evict_tiers", 0))
     rounds = g.replay_epochs(max(c["target"]))
     torch.cuda.synchronize()
     g.sync()
@@ -368,3 +369,23 @@ def test_evict_all_next_batch_and_replicas():
                 assert np.array_equal(src_g[k, x, :L_].cpu().numpy(), src_o[x, :L_])
     for k, o in enumerate(oracles):
         compare_replica(o, g, k)
+
+
+# ---------------------------------------------------------------- NEXT-1 epoch model
+@pytest.mark.parametrize("name,scale", [("toy", 1), ("imagenet1k", 64), ("openimages", 64)])
+def test_epoch_model_matches_oracle(name, scale):
+    c = synth.ods_config(name, scale=scale, seed=3)
+    ce, cd, ca = caps_of(c)
+    o, g = make_pair(c["n_total"], c["batch"], c["target"], ce, cd, ca, 3, transcript=False)
+    g.replay_epochs(max(c["target"]))
+    o.replay_epochs(max(c["target"]))
+    torch.cuda.synchronize()
+    dsi = (8014.245267534, 6424.75, 9783.0, 2735.52905131)
+    got = g.epoch_model(dsi)
+    want = O.epoch_metrics(o.stats()[0], c["n_total"], dsi)
+    for f in ("epoch_seconds", "dsi_mix", "hit_rate"):
+        assert np.array_equal(got[f].view(np.uint64), want[f].view(np.uint64)), f
+    for f in ("decode_aug_ops", "aug_only_ops"):
+        assert np.array_equal(got[f], want[f]), f
+    with pytest.raises(S.SenecaError):
+        g.epoch_model((1.0, 0.0, 1.0, 1.0))

@@ -336,3 +336,56 @@ def test_evict_all_uplift_on_encoded_only_cache():
         for e in (1, 2):
             assert s0[j, e]["served"][1:].sum() == 200
             assert s1[j, e]["served"][1:].sum() / 1000 >= 0.30
+
+
+# ------------------------------------------------------------ NEXT-1: epoch model on top of the replay
+def test_epoch_model_preprocessing_ops_pin():
+    """P:L428 / S:L396 through the epoch model: 4 cache-less jobs x 1.79 M samples
+    -> 7.16 M decode+augment ops, 0 augment-only, hit rate 0."""
+    cfg = dict(n_total=1_790_000, batch=[4096] * 4, target=[1] * 4, cap_e=0, cap_d=0, cap_a=0, seed=2)
+    o = run_oracle(cfg, transcript=False)
+    o.replay_epochs(1)
+    st, _, _ = o.stats()
+    m = O.epoch_metrics(st, 1_790_000, (2000.0, 2000.0, 2000.0, 1000.0))
+    assert int(m["decode_aug_ops"].sum()) == 7_160_000 and int(m["aug_only_ops"].sum()) == 0
+    assert np.all(m["hit_rate"] == 0.0)
+
+
+def test_epoch_model_zero_cache_time_is_n_over_dsi_s():
+    """SPEC run example: J = 1, zero cache -> epoch time = N / DSI_S."""
+    cfg = dict(n_total=5000, batch=[64], target=[2], cap_e=0, cap_d=0, cap_a=0, seed=3)
+    o = run_oracle(cfg, transcript=False)
+    o.replay_epochs(2)
+    dsi = (2141.58, 2141.58, 2132.0, 1733.7)
+    m = O.epoch_metrics(o.stats()[0], 5000, dsi)
+    assert np.all(m["epoch_seconds"] == 5000 / 1733.7) and np.all(m["dsi_mix"] == 1733.7)
+
+
+@pytest.mark.parametrize("server", ["in_house", "aws", "azure"])
+def test_epoch_model_static_tiers_equal_eq9(server):
+    """With static tiers (cap_A = 0) every job-epoch serves exactly the split's
+    counts (served_E = N_E, served_D = N_D, served_S = N_S), so the replayed mix
+    evaluated by Eq. 9 is the MDP model's value bit for bit, and the epoch time is
+    the tier sum of S:L376 in exact rationals."""
+    import json
+    import os
+    from fractions import Fraction
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "table4_nominal_vals.json")))
+    g = {k: v for k, v in gold[server].items() if not k.startswith("_")}
+    N, split = 20_000, (30, 25, 0)
+    p = O.make_profile(**dict(g, model_bytes=0.0, n_total=N, nodes=1, gpus_per_node=1, cache_bytes=10**9))
+    na, nd, ne, ns = O.split_counts(p, *split)
+    assert na == 0 and nd > 0 and ne > 0 and ns > 0
+    cfg = dict(n_total=N, batch=[256, 100], target=[2, 1], cap_e=ne, cap_d=nd, cap_a=0, seed=4)
+    o = run_oracle(cfg, transcript=False)
+    o.replay_epochs(2)
+    st, _, _ = o.stats()
+    dsi, _ = O.tiers(p)
+    v, _, _ = O.model_eval(p, *split)
+    m = O.epoch_metrics(st, N, dsi)
+    for j, e in ((0, 0), (0, 1), (1, 0)):
+        assert m[j, e]["dsi_mix"] == v
+        want = sum(Fraction(int(c)) / Fraction(d) for c, d in
+                   zip((st[j, e]["served"][A], st[j, e]["served"][D], st[j, e]["served"][E], st[j, e]["served"][S]),
+                       dsi))
+        assert abs(Fraction(m[j, e]["epoch_seconds"]) - want) <= want * Fraction(1, 10**14)
