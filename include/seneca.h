@@ -174,6 +174,11 @@ typedef struct {
                                       evicted / refilled (the default); 1: every
                                       cached tier (E, D, A) -- SURVEY 8c.3 "evict_tiers = ALL",
                                       DESIGN.md R-O21; E/D hits stay reusable              */
+    uint32_t        sampler;       /* 0: ODS (the method); 1: the uniform no-evict baseline
+                                      (MINIO-like, DESIGN.md R-O22): every
+                                      cached id is a hit, misses go to storage, nothing is
+                                      substituted, evicted or refilled                      */
+    uint32_t        _pad0;
 } seneca_cache_config;
 
 /* Per job-epoch counters (R-O10; digest in DESIGN.md §3).  104 bytes.       */

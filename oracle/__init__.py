@@ -103,7 +103,7 @@ def _declare(L):
     L.oracle_epoch_metrics.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.POINTER(C.c_double), C.c_void_p]
     L.oracle_epoch_metrics.restype = None
     L.oracle_ods_create.argtypes = [C.c_uint64, C.c_uint32, u32p, u32p, C.c_uint64, C.c_uint64,
-                                    C.c_uint64, C.c_uint64, C.c_int, C.c_int]
+                                    C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.c_int]
     L.oracle_ods_create.restype = C.c_void_p
     L.oracle_ods_destroy.argtypes = [C.c_void_p]
     L.oracle_ods_need.argtypes = [C.c_void_p, C.c_uint32]; L.oracle_ods_need.restype = C.c_uint64
@@ -223,10 +223,11 @@ def metadata_bytes(n_total: int, n_jobs: int) -> int:
 
 # --------------------------------------------------------------------------- ODS
 class ODS:
-    """One oracle replay instance (R-O1..R-O21 of DESIGN.md §3); evict_all selects
-    evict_tiers = ALL (R-O21)."""
+    """One oracle replay instance (R-O1..R-O22 of DESIGN.md §3); evict_all selects
+    evict_tiers = ALL (R-O21), baseline the uniform no-evict sampler (R-O22)."""
 
-    def __init__(self, n_total, batch, target, cap_e, cap_d, cap_a, seed, transcript=False, evict_all=False):
+    def __init__(self, n_total, batch, target, cap_e, cap_d, cap_a, seed, transcript=False, evict_all=False,
+                 baseline=False):
         self.N = int(n_total)
         self.batch = np.ascontiguousarray(batch, np.uint32)
         self.target = np.ascontiguousarray(target, np.uint32)
@@ -234,7 +235,7 @@ class ODS:
         self.bmax = int(self.batch.max())
         self.h = lib().oracle_ods_create(self.N, self.J, self.batch, self.target,
                                          int(cap_e), int(cap_d), int(cap_a), int(seed), int(transcript),
-                                         int(bool(evict_all)))
+                                         int(bool(evict_all)), int(bool(baseline)))
         if not self.h:
             raise ValueError("oracle_ods_create rejected the configuration")
         self.max_target = lib().oracle_ods_max_target(self.h)

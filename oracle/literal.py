@@ -64,13 +64,16 @@ class LiteralODS:
     tier by tier A -> D -> E from one keyed rank stream over the round-start
     storage pool."""
 
-    def __init__(self, n_total, batch, target, cap_e, cap_d, cap_a, seed, evict_all=False):
+    def __init__(self, n_total, batch, target, cap_e, cap_d, cap_a, seed, evict_all=False, baseline=False):
         self.N, self.batch, self.target = n_total, list(batch), list(target)
         self.J = len(batch)
         self.cap_a, self.seed = cap_a, seed
         self.cap = {A: cap_a, D: cap_d, E: cap_e}
         self.evict_all = evict_all
         self.cached = (A, D, E) if evict_all else (A,)        # tiers with consumer sets / eviction
+        self.baseline = baseline                              # R-O22: no substitution, no eviction
+        if baseline:
+            self.cached = ()
         self.tier = [S] * n_total
         iota = [perm(key(seed, 1), n_total, p) for p in range(cap_a + cap_d + cap_e)]
         for p, i in enumerate(iota):
@@ -109,13 +112,13 @@ class LiteralODS:
             out, src, misses = [None] * need, [None] * need, []
             for s, i in enumerate(req):
                 t = self.tier[i]
-                if t in (E, D) or (t == A and i not in self.cons[j]):
+                if t in (E, D) or (t == A and (self.baseline or i not in self.cons[j])):
                     out[s], src[s] = i, t
                     self.seen[j].add(i)
                 else:
                     misses.append(s)
             q = 0
-            for t in (A, D, E):
+            for t in (() if self.baseline else (A, D, E)):
                 if q == len(misses):
                     break
                 pool = self.pool(t, j)

@@ -335,10 +335,16 @@ typedef struct {
     uint64_t *transcript;          /* optional [J][max_target][N]: src<<32|id */
     int      evict_all;            /* evict_tiers = ALL (R-O21): consumer sets and
                                       eviction for every cached tier            */
+    int      baseline;             /* the uniform no-evict sampler (R-O22)     */
 } ods_t;
 
-/* tiers that carry consumer sets and can be evicted: A (R-O5), or all (R-O21) */
-static int tracked(const ods_t *o, int t) { return t == T_A || (o->evict_all && t != T_S); }
+/* tiers that carry consumer sets and can be evicted: A (R-O5), or all (R-O21);
+ * none for the no-evict baseline sampler (R-O22) */
+static int tracked(const ods_t *o, int t)
+{
+    if (o->baseline) return 0;
+    return t == T_A || (o->evict_all && t != T_S);
+}
 
 static int  bit_get(const uint64_t *bm, uint64_t i) { return (int)((bm[i >> 6] >> (i & 63)) & 1u); }
 static void bit_set(uint64_t *bm, uint64_t i)       { bm[i >> 6] |= (uint64_t)1 << (i & 63); }
@@ -423,7 +429,7 @@ void oracle_ods_destroy(void *h)
  * positions [0,cap_A) -> A, next cap_D -> D, next cap_E -> E, rest -> S. */
 void *oracle_ods_create(uint64_t N, uint32_t J, const uint32_t *batch, const uint32_t *target,
                         uint64_t cap_e, uint64_t cap_d, uint64_t cap_a, uint64_t seed,
-                        int keep_transcript, int evict_all)
+                        int keep_transcript, int evict_all, int baseline)
 {
     if (N == 0 || N >= ((uint64_t)1 << 32) || J == 0 || J > 32) return NULL;
     if (cap_e + cap_d + cap_a > N) return NULL;
@@ -431,6 +437,7 @@ void *oracle_ods_create(uint64_t N, uint32_t J, const uint32_t *batch, const uin
     o->N = N; o->J = J; o->W = (N + 63) / 64;
     o->cap_e = cap_e; o->cap_d = cap_d; o->cap_a = cap_a; o->seed = seed;
     o->evict_all = evict_all != 0;
+    o->baseline = baseline != 0;
     o->max_target = 0;
     for (uint32_t j = 0; j < J; ++j) {
         if (batch[j] == 0 || target[j] == 0) { free(o); return NULL; }
@@ -524,7 +531,7 @@ int oracle_ods_round(void *h, const uint32_t *jobs, uint32_t n_jobs, const uint3
         for (uint64_t s = 0; s < need; ++s) {
             uint64_t i = R[s];
             int t = tier_of(o, i);
-            if (t == T_E || t == T_D || (t == T_A && !bit_get(cons_j, i))) {
+            if (t == T_E || t == T_D || (t == T_A && (o->baseline || !bit_get(cons_j, i)))) {
                 out[s] = (uint32_t)i; src[s] = (uint8_t)t;
                 bit_set(seen_j, i);
             } else {
@@ -536,7 +543,7 @@ int oracle_ods_round(void *h, const uint32_t *jobs, uint32_t n_jobs, const uint3
          * tiers A -> D -> E, uniform by keyed ranks over the ascending pool (R-O2) */
         uint64_t q = 0;
         const int order[3] = { T_A, T_D, T_E };
-        for (int ti = 0; ti < 3 && q < m; ++ti) {
+        for (int ti = 0; ti < 3 && q < m && !o->baseline; ++ti) {   /* R-O22: no substitution */
             int t = order[ti];
             uint64_t P = pool_size(o, t, j);
             uint64_t k = (m - q) < P ? (m - q) : P;

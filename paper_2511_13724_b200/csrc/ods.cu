@@ -73,7 +73,8 @@ struct Cfg {
     uint32_t N, NW, NB, NS, NBp;     // samples, words/bitmap, blocks, superblocks, padded blocks
     uint32_t J, Bmax, maxT, cap_a, cap_d, cap_e;
     uint32_t evict_all;              // evict_tiers = ALL (R-O21): every cached tier is tracked
-    uint32_t cap_t;                  // capacity of the tracked tiers (cap_a, or cap_a + cap_d + cap_e)
+    uint32_t cap_t;                  // capacity of the tracked tiers (cap_a, or cap_a + cap_d + cap_e; 0 baseline)
+    uint32_t baseline;               // the uniform no-evict sampler (R-O22): no substitution, static tiers
     uint32_t Nrow;                   // row stride of the permutation / lap lists (N rounded up to 64)
     uint32_t FL;                     // capacity of one refill buffer
     uint64_t seed;
@@ -548,14 +549,15 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
             const uint32_t wd = C.cap_d ? ldcg(L.bm_d + w) : 0u;
             const uint32_t we = C.cap_e ? ldcg(L.bm_e + w) : 0u;
             const uint32_t t = (wa & b) ? T_A : (wd & b) ? T_D : (we & b) ? T_E : T_S;
-            const bool hit = (t == T_E || t == T_D || (t == T_A && !(ldcg(cons_j + w) & b)));
+            const bool hit = (t == T_E || t == T_D || (t == T_A && (C.baseline || !(ldcg(cons_j + w) & b))));
             if (hit) {
                 if (P.out_ids) { P.out_ids[row + s] = i; P.out_src[row + s] = (uint8_t)t; }
                 s_oid[s] = i;
                 // kNewCons: j joined the consumer set now (A hits always do; E/D hits
                 // under evict_tiers = ALL unless j consumed them before, R-O21)
                 uint32_t flag = 0;
-                if (t == T_A) { atomicOr(cons_j + w, b); flag = kNewCons; }
+                if (C.baseline) { /* no consumer sets (R-O22) */ }
+                else if (t == T_A) { atomicOr(cons_j + w, b); flag = kNewCons; }
                 else if (C.evict_all && !(atomicOr(cons_j + w, b) & b)) flag = kNewCons;
                 s_osrc[s] = (uint8_t)(t | flag);
                 atomicOr(seen_j + w, b);
@@ -575,9 +577,9 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
         S.tot[0] = pa; S.tot[1] = pd; S.tot[2] = pe;
         const uint32_t m = mbase;
         S.m = m;
-        S.k[0] = min(m, pa);
-        S.k[1] = min(m - S.k[0], pd);
-        S.k[2] = min(m - S.k[0] - S.k[1], pe);
+        S.k[0] = C.baseline ? 0u : min(m, pa);                  // R-O22: no substitution
+        S.k[1] = C.baseline ? 0u : min(m - S.k[0], pd);
+        S.k[2] = C.baseline ? 0u : min(m - S.k[0] - S.k[1], pe);
     }
     __syncthreads();
     TM.tick(1);
@@ -1281,6 +1283,7 @@ seneca_status check_cfg(const seneca_cache_config* cfg) {
     }
     if (cfg->replicas > kMaxReplicas) { set_error("replicas must be <= %u", kMaxReplicas); return SENECA_EINVAL; }
     if (cfg->evict_tiers > 1) { set_error("evict_tiers must be 0 (A only) or 1 (all)"); return SENECA_EINVAL; }
+    if (cfg->sampler > 1) { set_error("sampler must be 0 (ODS) or 1 (uniform no-evict baseline)"); return SENECA_EINVAL; }
     if (cfg->replicas > 1 && cfg->request_mode != 0) {
         set_error("caller-supplied requests (request_mode 1) need replicas <= 1"); return SENECA_EINVAL;
     }
@@ -1319,7 +1322,8 @@ Sizes compute_sizes(const seneca_cache_config* cfg) {
     C.cap_d = (uint32_t)cfg->cap_d;
     C.cap_e = (uint32_t)cfg->cap_e;
     C.evict_all = cfg->evict_tiers;
-    C.cap_t = C.evict_all ? C.cap_a + C.cap_d + C.cap_e : C.cap_a;
+    C.baseline = cfg->sampler;
+    C.cap_t = C.baseline ? 0u : (C.evict_all ? C.cap_a + C.cap_d + C.cap_e : C.cap_a);
     C.seed = cfg->seed;
     C.Nrow = (C.N + 63) & ~63u;
     C.FL = (uint32_t)(std::max<size_t>(C.cap_t, 1) + (size_t)C.J * C.Bmax);

@@ -58,7 +58,7 @@ class CacheConfig(C.Structure):
         ("n_total", C.c_uint64), ("n_jobs", C.c_uint32), ("request_mode", C.c_uint32),
         ("batch_size", C.POINTER(C.c_uint32)), ("target_epochs", C.POINTER(C.c_uint32)),
         ("cap_e", C.c_uint64), ("cap_d", C.c_uint64), ("cap_a", C.c_uint64), ("seed", C.c_uint64),
-        ("replicas", C.c_uint32), ("evict_tiers", C.c_uint32),
+        ("replicas", C.c_uint32), ("evict_tiers", C.c_uint32), ("sampler", C.c_uint32), ("_pad0", C.c_uint32),
     ]
 
 
@@ -212,12 +212,13 @@ def profiles_from_columns(cols: dict) -> np.ndarray:
 
 
 # ------------------------------------------------------------------ ODS
-def make_config(n_total, batch, target, cap_e, cap_d, cap_a, seed, request_mode=0, replicas=1, evict_tiers=0):
+def make_config(n_total, batch, target, cap_e, cap_d, cap_a, seed, request_mode=0, replicas=1, evict_tiers=0,
+                sampler=0):
     b = (C.c_uint32 * len(batch))(*batch)
     t = (C.c_uint32 * len(target))(*target)
     cfg = CacheConfig(n_total=n_total, n_jobs=len(batch), request_mode=request_mode,
                       batch_size=b, target_epochs=t, cap_e=cap_e, cap_d=cap_d, cap_a=cap_a, seed=seed,
-                      replicas=replicas, evict_tiers=evict_tiers)
+                      replicas=replicas, evict_tiers=evict_tiers, sampler=sampler)
     cfg._keep = (b, t)
     return cfg
 

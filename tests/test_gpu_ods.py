@@ -35,9 +35,9 @@ def caps_of(c):
     return caps[0], caps[1], caps[2]
 
 
-def make_pair(n, batch, target, ce, cd, ca, seed, transcript=True, evict_all=False):
-    o = O.ODS(n, batch, target, ce, cd, ca, seed, transcript=transcript, evict_all=evict_all)
-    g = P.ODSContext(n, batch, target, ce, cd, ca, seed, evict_tiers=int(evict_all))
+def make_pair(n, batch, target, ce, cd, ca, seed, transcript=True, evict_all=False, baseline=False):
+    o = O.ODS(n, batch, target, ce, cd, ca, seed, transcript=transcript, evict_all=evict_all, baseline=baseline)
+    g = P.ODSContext(n, batch, target, ce, cd, ca, seed, evict_tiers=int(evict_all), sampler=int(baseline))
     return o, g
 
 
@@ -61,8 +61,8 @@ def compare_state(o, g, check_transcript=None):
     g.sync()
 
 
-def replay_pair(n, batch, target, ce, cd, ca, seed, evict_all=False):
-    o, g = make_pair(n, batch, target, ce, cd, ca, seed, evict_all=evict_all)
+def replay_pair(n, batch, target, ce, cd, ca, seed, evict_all=False, baseline=False):
+    o, g = make_pair(n, batch, target, ce, cd, ca, seed, evict_all=evict_all, baseline=baseline)
     tr = g.new_transcript()
     r_g = g.replay_epochs(max(target), tr)
     r_o = o.replay_epochs(max(target))
@@ -389,3 +389,19 @@ def test_epoch_model_matches_oracle(name, scale):
         assert np.array_equal(got[f], want[f]), f
     with pytest.raises(S.SenecaError):
         g.epoch_model((1.0, 0.0, 1.0, 1.0))
+
+
+# ---------------------------------------------------------------- uniform no-evict baseline sampler (R-O22)
+def test_baseline_sampler_random_tiny_and_scaled():
+    st = synth.Stream(12000)
+    for _ in range(60):
+        c = synth.random_tiny_ods(st)
+        replay_pair(c["n_total"], c["batch"], c["target"], c["cap_e"], c["cap_d"], c["cap_a"], c["seed"],
+                    baseline=True)
+    for name in ("toy", "imagenet1k", "openimages"):
+        c = synth.ods_config(name, scale=1 if name == "toy" else 64, seed=4)
+        ce, cd, ca = caps_of(c)
+        o, g = replay_pair(c["n_total"], c["batch"], c["target"], ce, cd, ca, 4, baseline=True)
+        st_g, ev, rf = g.stats()
+        assert ev == 0 and rf == 0
+        assert np.all(st_g["served"][:, :, 1:].sum(axis=2) == ce + cd + ca)     # hit rate = cached fraction

@@ -389,3 +389,61 @@ def test_epoch_model_static_tiers_equal_eq9(server):
                    zip((st[j, e]["served"][A], st[j, e]["served"][D], st[j, e]["served"][E], st[j, e]["served"][S]),
                        dsi))
         assert abs(Fraction(m[j, e]["epoch_seconds"]) - want) <= want * Fraction(1, 10**14)
+
+
+# ------------------------------------------------------------ the uniform no-evict baseline sampler (NEXT-3, R-O22)
+def run_base(cfg, transcript=True):
+    return O.ODS(cfg["n_total"], cfg["batch"], cfg["target"], cfg["cap_e"], cfg["cap_d"], cfg["cap_a"],
+                 cfg["seed"], transcript=transcript, baseline=True)
+
+
+def test_baseline_hit_rate_is_the_cached_fraction_exactly():
+    """S:L380 / P:L1294 (MINIO-like): the request stream visits every id once per
+    epoch and nothing is substituted or evicted, so every job-epoch hits exactly
+    the cached ids: served_E/D/A = cap_E/D/A, served_S = the rest."""
+    for seed in (1, 2, 3):
+        cfg = dict(n_total=1000, batch=[32, 17, 64], target=[3, 2, 3], cap_e=120, cap_d=50, cap_a=30, seed=seed)
+        o = run_base(cfg)
+        o.replay_epochs(3)
+        st, ev, rf = o.stats()
+        assert ev == 0 and rf == 0
+        for j in range(3):
+            for e in range(cfg["target"][j]):
+                s = st[j, e]
+                assert list(s["served"]) == [800, 120, 50, 30] and s["subst"].sum() == 0
+        tr = o.transcript()
+        ids = (tr[0, 0] & 0xFFFFFFFF).astype(np.int64)
+        assert np.array_equal(np.sort(ids), np.arange(1000))
+
+
+@pytest.mark.parametrize("block", range(4))
+def test_baseline_cross_check_with_literal_transcription(block):
+    st = synth.Stream(11000 + block)
+    for _ in range(60):
+        cfg = synth.random_tiny_ods(st)
+        o = run_base(cfg)
+        o.replay_epochs(max(cfg["target"]))
+        lit = L.LiteralODS(cfg["n_total"], cfg["batch"], cfg["target"], cfg["cap_e"], cfg["cap_d"],
+                           cfg["cap_a"], cfg["seed"], baseline=True)
+        lit.replay_all()
+        tr = o.transcript()
+        for j in range(len(cfg["batch"])):
+            for e in range(cfg["target"][j]):
+                got = [(int(x) & 0xFFFFFFFF, int(x) >> 32) for x in tr[j, e]]
+                assert got == lit.deliveries[j][e], cfg
+
+
+def test_hit_rate_vs_cache_fraction_ods_above_baseline():
+    """The paper's hit-rate experiment (P:L1282-1294, 3 concurrent jobs): with an
+    augmented cache ODS serves well above the cached fraction, which the
+    no-evict baseline serves exactly (SURVEY [A.7] probe: 0.64 at 20 %, 0.86 at 40 %)."""
+    for frac in (0.2, 0.4):
+        cap = int(1000 * frac)
+        cfg = dict(n_total=1000, batch=[32] * 3, target=[3] * 3, cap_e=0, cap_d=0, cap_a=cap, seed=7)
+        ods, base = run_oracle(cfg, transcript=False), run_base(cfg, transcript=False)
+        ods.replay_epochs(3)
+        base.replay_epochs(3)
+        h_ods = ods.stats()[0]["served"][:, 1:, 1:].sum(axis=2) / 1000
+        h_base = base.stats()[0]["served"][:, 1:, 1:].sum(axis=2) / 1000
+        assert np.all(h_base == frac)
+        assert np.all(h_ods >= frac + 0.25)
