@@ -51,12 +51,16 @@ constexpr uint32_t kNewCons = 0x80;          // internal s_osrc flag: consumer s
 constexpr uint32_t kMaxJobs = 32;
 constexpr uint32_t kMaxReplicas = 64;        // independent replay instances per context
 constexpr uint32_t kMaxBatch = 4096;
-constexpr uint32_t kThreads = 512;           // CTA size of the persistent kernel
+#ifndef SENECA_ODS_THREADS
+#define SENECA_ODS_THREADS 512
+#endif
+constexpr uint32_t kThreads = SENECA_ODS_THREADS;   // CTA size of the persistent kernel
 constexpr uint32_t kBlockShift = 7;          // 128 ids (4 words, one 16-B vector) per count block
 constexpr uint32_t kSuperShift = 12;         // 32 blocks = 4096 ids per superblock
 constexpr uint32_t kWordsPerBlock = 4;
 constexpr uint32_t kWalkPerThread = 8;       // list entries examined per thread per walk step
 constexpr uint32_t kWinMax = 1024;           // prefetched walk window (list entries)
+static_assert(2 * kThreads >= kWinMax, "the prefetched walk step covers 2 window entries per thread");
 
 // ------------------------------------------------------------------ layouts
 struct JobDev {           // per-job persistent walk state (workspace)

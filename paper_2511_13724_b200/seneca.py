@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libseneca.so")
+LIB_PATH = os.environ.get("SENECA_LIB") or os.path.join(_HERE, "libseneca.so")   # override: experiments only
 
 OK, EINVAL, ESTATE, EPROTO, ECUDA, ENOSPC = 0, 1, 2, 3, 4, 6
 _NAMES = {0: "OK", 1: "EINVAL", 2: "ESTATE", 3: "EPROTO", 4: "ECUDA", 6: "ENOSPC"}
