@@ -285,7 +285,6 @@ def main():
     ws_bytes = S.state_bytes(cfg)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)      # > 126 MB L2
-    ws_r_holder = []
 
     def barrier():
         if world > 1:
@@ -375,55 +374,64 @@ def main():
     except Exception as e:  # the oracle is only a checker; report, do not fall back
         parity["mdp_vs_oracle_first_200_profiles"] = f"unchecked: {e}"
 
-    # ---- R independent replays in one context (untimed warm-up, then timed steps)
+    # ---- R independent replays in one context (untimed warm-up, then timed steps).
+    #      Candidates: the most replicas with one 512-thread round CTA per SM, and
+    #      with two 256-thread CTAs per SM (the library picks the kernel variant);
+    #      the line reports the faster, both are listed.
     rep_line = None
     if args.replicas != 0:
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
-        R = args.replicas if args.replicas > 0 else min(64, sms // (len(c["batch"]) + 1))
+        J1 = len(c["batch"]) + 1
+        cands = [args.replicas] if args.replicas > 0 else sorted({min(64, sms // J1), min(64, 2 * sms // J1)})
         rseed = (synth.PERF_SEED + 64 * rank) & 0xFFFFFFFFFFFFFFFF
-        rcfg = S.make_config(c["n_total"], c["batch"], c["target"], ce, cd, ca, rseed, replicas=R,
-                             evict_tiers=args.evict_tiers)
-        rbytes = S.state_bytes(rcfg)
-        del ws_r_holder[:]
-        ws_r = torch.empty(rbytes, dtype=torch.uint8, device=dev)
-        ws_r_holder.append(ws_r)
-        rep_ms = []
-        for s in range(1 + args.steps):
-            flush.fill_(s & 0xFF)
-            barrier()
-            torch.cuda.synchronize(dev)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            rctx = S.init_cache(rcfg, ws_r, rbytes, stream)
-            S.replay_epochs(rctx, max(c["target"]), None, stream)
-            e1.record(stream)
-            torch.cuda.synchronize(dev)
-            barrier()
-            if s >= 1:
-                rep_ms.append(e0.elapsed_time(e1))
-                launches_rep = S.launch_count(rctx)
-            if s < args.steps:
-                S.destroy(rctx)
-        S.sync_status(rctx, stream)
-        rv = S.read_state(rctx)
-        served_all = True
-        rep0_digest_ok = None
-        nst1 = len(c["batch"]) * rv.max_target * S.STATS_DTYPE.itemsize
-        for k in range(R):
-            o = rv.d_stats + k * rv.replica_stride - ws_r.data_ptr()
-            stk = ws_r[o:o + nst1].cpu().numpy().view(S.STATS_DTYPE).reshape(len(c["batch"]), rv.max_target)
-            served_all &= bool(np.all(stk["served"].sum(axis=2) == c["n_total"]))
-        S.destroy(rctx)
-        (rep_s,) = D.reduce_times([sum(rep_ms) / 1e3], device=dev)
-        rep_line = dict(R=R, value=R * dec_per_step * args.steps * world / rep_s, unit="decisions/s",
-                        ms_per_step=1e3 * rep_s / args.steps, per_replica_value=dec_per_step * args.steps / rep_s,
-                        round_ctas=R * (len(c["batch"]) + 1), seeds=f"{hex(rseed)} + k, k < {R}",
-                        launches_per_step=launches_rep,
-                        parity=dict(every_replica_served_each_sample_once_per_job_epoch=served_all,
+        tried = []
+        for R in cands:
+            rcfg = S.make_config(c["n_total"], c["batch"], c["target"], ce, cd, ca, rseed, replicas=R,
+                                 evict_tiers=args.evict_tiers)
+            rbytes = S.state_bytes(rcfg)
+            ws_r = torch.empty(rbytes, dtype=torch.uint8, device=dev)
+            rep_ms = []
+            for s in range(1 + args.steps):
+                flush.fill_(s & 0xFF)
+                barrier()
+                torch.cuda.synchronize(dev)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                rctx = S.init_cache(rcfg, ws_r, rbytes, stream)
+                S.replay_epochs(rctx, max(c["target"]), None, stream)
+                e1.record(stream)
+                torch.cuda.synchronize(dev)
+                barrier()
+                if s >= 1:
+                    rep_ms.append(e0.elapsed_time(e1))
+                    launches_rep = S.launch_count(rctx)
+                if s < args.steps:
+                    S.destroy(rctx)
+            S.sync_status(rctx, stream)
+            rv = S.read_state(rctx)
+            served_all = True
+            nst1 = len(c["batch"]) * rv.max_target * S.STATS_DTYPE.itemsize
+            for k in range(R):
+                o = rv.d_stats + k * rv.replica_stride - ws_r.data_ptr()
+                stk = ws_r[o:o + nst1].cpu().numpy().view(S.STATS_DTYPE).reshape(len(c["batch"]), rv.max_target)
+                served_all &= bool(np.all(stk["served"].sum(axis=2) == c["n_total"]))
+            S.destroy(rctx)
+            del ws_r
+            (rep_s,) = D.reduce_times([sum(rep_ms) / 1e3], device=dev)
+            tried.append(dict(R=R, value=R * dec_per_step * args.steps * world / rep_s, unit="decisions/s",
+                              ms_per_step=1e3 * rep_s / args.steps,
+                              per_replica_value=dec_per_step * args.steps / rep_s,
+                              round_ctas=R * J1, ctas_per_sm=1 if R * J1 <= sms else 2,
+                              launches_per_step=launches_rep, served_ok=served_all))
+        best = max(tried, key=lambda t: t["value"])
+        rep_line = dict(best, seeds=f"{hex(rseed)} + k, k < R",
+                        candidates=[{k: t[k] for k in ("R", "value", "per_replica_value", "ctas_per_sm")}
+                                    for t in tried],
+                        parity=dict(every_replica_served_each_sample_once_per_job_epoch=all(t["served_ok"] for t in tried),
                                     note="replica-vs-oracle bit-exactness: tests/test_gpu_ods.py::test_replicas_*"),
                         note="init_cache + replay_epochs of R independent instances of the workload in one "
                              "context (one cooperative launch); L2 flushed between steps")
-        del ws_r_holder[:]
+        rep_line.pop("served_ok", None)
 
     # ---- e2e through the public API with host buffers (pinned), copies inside
     pin_prof = torch.from_numpy(prof_host.view(np.uint8).copy()).pin_memory()

@@ -60,7 +60,7 @@ constexpr uint32_t kSuperShift = 12;         // 32 blocks = 4096 ids per superbl
 constexpr uint32_t kWordsPerBlock = 4;
 constexpr uint32_t kWalkPerThread = 8;       // list entries examined per thread per walk step
 constexpr uint32_t kWinMax = 1024;           // prefetched walk window (list entries)
-static_assert(2 * kThreads >= kWinMax, "the prefetched walk step covers 2 window entries per thread");
+// the prefetched walk step covers 2 window entries per thread: window = min(kWinMax, 2 T)
 
 // ------------------------------------------------------------------ layouts
 struct JobDev {           // per-job persistent walk state (workspace)
@@ -301,7 +301,7 @@ __device__ void prefetch_window(const Lay& L, const Cfg& C, JobSmem& S, uint32_t
                                 uint32_t want) {
     const uint32_t tid = threadIdx.x;
     const uint32_t base = S.cursor & ~3u;
-    uint32_t len = min(kWinMax, (want + (S.cursor - base) + 3) & ~3u);
+    uint32_t len = min(min(kWinMax, 2 * blockDim.x), (want + (S.cursor - base) + 3) & ~3u);
     len = min(len, C.Nrow - base);
     const uint32_t* list = list_ptr(L, C, j, e, S.cur_buf);
     for (uint32_t t = tid; t * 4 < len; t += blockDim.x) cp_async16(s_win + 4 * t, list + base + 4 * t);
@@ -866,8 +866,7 @@ __device__ void job_take_refills(const Lay& L, const Cfg& C, JobSmem& S, uint32_
 // ------------------------------------------------------------------ the persistent round kernel
 // Grid: (J + 1) CTAs per replica; replicas are independent replays (their own
 // workspace slice and seed) that share nothing but the launch.
-__global__ void __launch_bounds__(kThreads, 1)
-ods_rounds(const __grid_constant__ Lays LS, const __grid_constant__ Cfg C, const __grid_constant__ Launch P) {
+__device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, const Launch& P) {
     extern __shared__ __align__(16) uint32_t smem[];
     __shared__ JobSmem S;
     __shared__ MaintSmem M;
@@ -895,9 +894,10 @@ ods_rounds(const __grid_constant__ Lays LS, const __grid_constant__ Cfg C, const
     uint32_t* s_pre = s_sup + 3 * C.NS;                             // [3][NS] prefixes
     const uint32_t o_win = (4 * C.Bmax + 6 * C.NS + 3) & ~3u;       // 16-B aligned (cp.async)
     uint32_t* s_win = smem + o_win;
-    const uint32_t o_wseen = o_win + kWinMax;
+    const uint32_t win = min(kWinMax, 2 * blockDim.x);              // prefetched walk window
+    const uint32_t o_wseen = o_win + win;
     uint4* s_wseen = reinterpret_cast<uint4*>(smem + o_wseen);
-    uint8_t* s_osrc = reinterpret_cast<uint8_t*>(smem + o_wseen + 4 * kWinMax);
+    uint8_t* s_osrc = reinterpret_cast<uint8_t*>(smem + o_wseen + 4 * win);
     WalkPrefetch pfs;
     pfs.wseen = s_wseen;
     const WalkPrefetch* pf = P.mode == 0 ? &pfs : nullptr;
@@ -1112,6 +1112,19 @@ ods_rounds(const __grid_constant__ Lays LS, const __grid_constant__ Cfg C, const
     }
 }
 
+// Two instantiations: 512 threads, one CTA per SM (a single replay: the most
+// memory parallelism per job), and 256 threads, two CTAs per SM (replicas that
+// would not fit one per SM: twice the independent replays per SM).
+__global__ void __launch_bounds__(kThreads, 1)
+ods_rounds(const __grid_constant__ Lays LS, const __grid_constant__ Cfg C, const __grid_constant__ Launch P) {
+    ods_rounds_body(LS, C, P);
+}
+
+__global__ void __launch_bounds__(kThreads / 2, 2)
+ods_rounds_x2(const __grid_constant__ Lays LS, const __grid_constant__ Cfg C, const __grid_constant__ Launch P) {
+    ods_rounds_body(LS, C, P);
+}
+
 // ------------------------------------------------------------------ one-off kernels
 // pi_j,e for every (job, epoch), epoch-major, in chunks; the CTA finishing the
 // last chunk of (j, e) publishes perm_ready[j][e] (release).
@@ -1263,6 +1276,8 @@ struct seneca_ctx {
     uint64_t ksampled[K_NCLASS];
     uint32_t profiling;
     size_t round_smem;
+    const void* round_fn;      // ods_rounds (512 threads, 1 CTA / SM) or ods_rounds_x2 (256, 2 / SM)
+    uint32_t round_threads;
     int device;
     cudaStream_t side;
     cudaEvent_t ev_init;
@@ -1462,7 +1477,7 @@ seneca_status launch_rounds(seneca_ctx* c, uint64_t R, uint32_t jobs_mask, const
     void* args[] = {&c->LS, &c->C, &P};
     cudaError_t le = cudaSuccess;
     timed(c, K_ROUNDS, st, [&] {
-        le = cudaLaunchCooperativeKernel((void*)ods_rounds, dim3((c->C.J + 1) * c->R), dim3(kThreads), args,
+        le = cudaLaunchCooperativeKernel(c->round_fn, dim3((c->C.J + 1) * c->R), dim3(c->round_threads), args,
                                          c->round_smem, st);
     });
     if (le != cudaSuccess) return cuda_status(le, "cudaLaunchCooperativeKernel(ods_rounds)");
@@ -1507,9 +1522,13 @@ extern "C" seneca_status seneca_init_cache(const seneca_cache_config* cfg, void*
     if (ws_bytes < z.total * z.R) {
         set_error("workspace %zu bytes < required %zu", ws_bytes, z.total * z.R); return SENECA_ENOSPC;
     }
-    const size_t o_win = ((size_t)4 * z.C.Bmax + 6 * z.C.NS + 3) & ~(size_t)3;
-    const size_t o_wseen = o_win + kWinMax;
-    const size_t round_smem = (o_wseen + 4 * kWinMax) * 4 + z.C.Bmax;
+    // dynamic shared memory of a round CTA with T threads (window min(kWinMax, 2 T))
+    auto smem_for = [&](uint32_t T) -> size_t {
+        const size_t win = std::min<size_t>(kWinMax, 2 * (size_t)T);
+        const size_t o_win = ((size_t)4 * z.C.Bmax + 6 * z.C.NS + 3) & ~(size_t)3;
+        return (o_win + win + 4 * win) * 4 + z.C.Bmax;
+    };
+    const size_t round_smem = smem_for(kThreads);
     if (round_smem > 200 * 1024) { set_error("batch/dataset too large for the shared-memory indices"); return SENECA_EINVAL; }
     seneca_ctx* c = new (std::nothrow) seneca_ctx();
     if (!c) { set_error("out of host memory"); return SENECA_EINVAL; }
@@ -1527,16 +1546,30 @@ extern "C" seneca_status seneca_init_cache(const seneca_cache_config* cfg, void*
     cudaGetDevice(&c->device);
 #define INIT_TRY(expr) do { cudaError_t _e = (expr); if (_e != cudaSuccess) { delete c; return cuda_status(_e, #expr); } } while (0)
     INIT_TRY(cudaFuncSetAttribute(ods_rounds, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    INIT_TRY(cudaFuncSetAttribute(ods_rounds_x2, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     INIT_TRY(cudaFuncSetAttribute(ods_validate_requests, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-    {   // the cooperative round launch needs every replica's CTAs co-resident
+    {   // the cooperative round launch needs every replica's CTAs co-resident: one
+        // 512-thread CTA per SM when they fit, else two 256-thread CTAs per SM
+        const uint64_t need = (uint64_t)(z.C.J + 1) * z.R;
         int per_sm = 0;
         INIT_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ods_rounds, kThreads, round_smem));
-        const uint64_t slots = (uint64_t)per_sm * num_sms();
-        if ((uint64_t)(z.C.J + 1) * z.R > slots) {
-            set_error("%u replicas x %u CTAs exceed the %llu co-resident CTA slots", z.R, z.C.J + 1,
-                      (unsigned long long)slots);
-            delete c;
-            return SENECA_EINVAL;
+        uint64_t slots = (uint64_t)per_sm * num_sms();
+        c->round_fn = (const void*)ods_rounds;
+        c->round_threads = kThreads;
+        if (need > slots) {
+            const size_t smem2 = smem_for(kThreads / 2);
+            int per_sm2 = 0;
+            INIT_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, ods_rounds_x2, kThreads / 2, smem2));
+            const uint64_t slots2 = (uint64_t)per_sm2 * num_sms();
+            if (need > slots2) {
+                set_error("%u replicas x %u CTAs exceed the %llu co-resident CTA slots", z.R, z.C.J + 1,
+                          (unsigned long long)std::max(slots, slots2));
+                delete c;
+                return SENECA_EINVAL;
+            }
+            c->round_fn = (const void*)ods_rounds_x2;
+            c->round_threads = kThreads / 2;
+            c->round_smem = smem2;
         }
     }
     INIT_TRY(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));

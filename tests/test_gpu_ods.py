@@ -254,11 +254,13 @@ def compare_replica(o, g, k, tr_k=None):
         assert np.array_equal(tr_k.cpu().numpy().view(np.uint64), o.transcript()), k
 
 
-@pytest.mark.parametrize("name,scale,R", [("toy", 1, 48), ("imagenet1k", 64, 4), ("openimages", 64, 3)])
+@pytest.mark.parametrize("name,scale,R", [("toy", 1, 48), ("toy", 1, 64), ("imagenet1k", 64, 4),
+                                          ("openimages", 64, 3), ("imagenet1k", 64, 40)])
 def test_replicas_match_independent_oracles(name, scale, R):
     """R replicas in one context == R independent oracle replays with seeds
-    seed + k (every decision, bitmap and counter), including a launch that fills
-    the GPU with round CTAs (toy: 48 x 3 CTAs)."""
+    seed + k (every decision, bitmap and counter), including launches that fill
+    the GPU with round CTAs: toy 48 x 3 CTAs (one 512-thread CTA per SM), toy
+    64 x 3 and ImageNet-1K/64 40 x 5 (two 256-thread CTAs per SM)."""
     seed = 3
     c = synth.ods_config(name, scale=scale, seed=seed)
     ce, cd, ca = caps_of(c)
@@ -299,7 +301,7 @@ def test_replicas_next_batch():
 
 def test_replicas_that_cannot_be_co_resident_are_rejected():
     with pytest.raises(S.SenecaError) as ei:
-        P.ODSContext(1000, [32, 32], [1, 1], 10, 10, 10, 1, replicas=64)      # 64 x 3 CTAs > 148 SMs
+        P.ODSContext(1000, [32] * 8, [1] * 8, 10, 10, 10, 1, replicas=64)      # 64 x 9 CTAs > 2 x 148
     assert ei.value.status == S.EINVAL
 
 
