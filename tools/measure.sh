@@ -12,6 +12,9 @@ timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=
 for w in openimages imagenet22k; do
   timeout 600 python bench.py --workload $w --no-cpu-baseline > $OUT/bench_$w.json 2>> $OUT/bench.err; echo "bench $w rc=$?"
 done
+for w in imagenet1k imagenet22k; do   # the second eviction mode (R-O21), gated by its oracle golden
+  timeout 600 python bench.py --workload $w --evict-tiers 1 --replicas 0 --no-cpu-baseline > $OUT/bench_${w}_evictall.json 2>> $OUT/bench.err; echo "bench $w evict-all rc=$?"
+done
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > $OUT/bench_reference.json 2>> $OUT/bench.err; echo "reference rc=$?"
 # launch list of one bench step (cold, serialised: compare shares, not absolutes)
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
