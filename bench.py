@@ -519,7 +519,7 @@ def main():
                 cache_entries=ce + cd + ca, mdp_profiles=args.mdp_profiles, mdp_splits=nsplit,
                 job_epochs=sum(c["target"]),
                 mdp_grid=d_grid is not None)
-    tkey = {"ods_rounds": f"ods_rounds@{args.workload}",
+    tkey = {"ods_rounds": f"ods_rounds@{args.workload}{'-evictall' if args.evict_tiers else ''}",
             "mdp_sweep": f"mdp_sweep@{args.mdp_profiles}x{nsplit}{'' if d_grid is not None else '-nogrid'}"}
     roof = roofline_for(dom, kernels[dom], info, hbm_peak, peak_src, ncu_traffic(tkey.get(dom, dom)))
     mdp_roof = roofline_for("mdp_sweep", kernels["mdp_sweep"], info, hbm_peak, peak_src,

@@ -282,6 +282,10 @@ seneca_status seneca_ods_next_batch(seneca_ctx* ctx, const uint32_t* h_jobs, uin
 seneca_status seneca_replay_epochs(seneca_ctx* ctx, uint32_t n_epochs, uint64_t* d_transcript,
                                    uint64_t* h_rounds, void* stream);
 
+/* The same call under the name north_star gives it (seneca_replay_epoch).      */
+seneca_status seneca_replay_epoch(seneca_ctx* ctx, uint32_t n_epochs, uint64_t* d_transcript,
+                                  uint64_t* h_rounds, void* stream);
+
 /* As seneca_replay_epochs but for exactly n_rounds rounds (fewer if every job
  * departs).                                                                    */
 seneca_status seneca_replay_rounds(seneca_ctx* ctx, uint64_t n_rounds, uint64_t* d_transcript,

@@ -1683,6 +1683,11 @@ extern "C" seneca_status seneca_replay_epochs(seneca_ctx* c, uint32_t n_epochs, 
     return replay(c, rounds_for_epochs(c, n_epochs), d_transcript, h_rounds, (cudaStream_t)stream);
 }
 
+extern "C" seneca_status seneca_replay_epoch(seneca_ctx* c, uint32_t n_epochs, uint64_t* d_transcript,
+                                             uint64_t* h_rounds, void* stream) {
+    return seneca_replay_epochs(c, n_epochs, d_transcript, h_rounds, stream);
+}
+
 extern "C" seneca_status seneca_replay_rounds(seneca_ctx* c, uint64_t n_rounds, uint64_t* d_transcript,
                                               uint64_t* h_rounds, void* stream) {
     if (!c) { set_error("bad arguments"); return SENECA_EINVAL; }

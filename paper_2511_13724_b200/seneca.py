@@ -118,6 +118,8 @@ def lib() -> C.CDLL:
         L.seneca_ods_next_batch.restype = C.c_int
         L.seneca_replay_epochs.argtypes = [vp, u32, vp, C.POINTER(u64), vp]
         L.seneca_replay_epochs.restype = C.c_int
+        L.seneca_replay_epoch.argtypes = [vp, u32, vp, C.POINTER(u64), vp]
+        L.seneca_replay_epoch.restype = C.c_int
         L.seneca_replay_rounds.argtypes = [vp, u64, vp, C.POINTER(u64), vp]
         L.seneca_replay_rounds.restype = C.c_int
         L.seneca_read_state.argtypes = [vp, C.POINTER(StateView)]; L.seneca_read_state.restype = C.c_int
@@ -135,7 +137,7 @@ def lib() -> C.CDLL:
 EXPORTED = ["seneca_mdp_num_splits", "seneca_mdp_sweep", "seneca_mdp_eval", "seneca_epoch_model",
             "seneca_split_capacities",
             "seneca_metadata_bytes", "seneca_state_bytes", "seneca_init_cache",
-            "seneca_ods_next_batch", "seneca_replay_epochs", "seneca_replay_rounds",
+            "seneca_ods_next_batch", "seneca_replay_epochs", "seneca_replay_epoch", "seneca_replay_rounds",
             "seneca_read_state", "seneca_sync_status", "seneca_launch_count", "seneca_destroy",
             "seneca_last_error", "seneca_profile", "seneca_profile_read"]
 

@@ -407,3 +407,27 @@ def test_baseline_sampler_random_tiny_and_scaled():
         st_g, ev, rf = g.stats()
         assert ev == 0 and rf == 0
         assert np.all(st_g["served"][:, :, 1:].sum(axis=2) == ce + cd + ca)     # hit rate = cached fraction
+
+
+@pytest.mark.parametrize("evict_all", [False, True])
+def test_thirty_two_jobs(evict_all):
+    """The maximum job count (a full 32-bit active mask, 33 round CTAs), mixed
+    batches and targets (staggered departures), every tier populated."""
+    batch = [1 + (7 * j) % 32 for j in range(32)]
+    target = [1 + j % 3 for j in range(32)]
+    replay_pair(3000, batch, target, 300, 200, 400, 17, evict_all=evict_all)
+
+
+def test_replay_epoch_alias():
+    """seneca_replay_epoch (the north_star name) is seneca_replay_epochs."""
+    import ctypes
+    c = synth.ods_config("toy", seed=6)
+    ce, cd, ca = caps_of(c)
+    a = P.ODSContext(c["n_total"], c["batch"], c["target"], ce, cd, ca, 6)
+    b = P.ODSContext(c["n_total"], c["batch"], c["target"], ce, cd, ca, 6)
+    ra = a.replay_epochs(3)
+    rb = ctypes.c_uint64()
+    assert S.lib().seneca_replay_epoch(b.ctx, 3, None, ctypes.byref(rb),
+                                       torch.cuda.current_stream().cuda_stream) == 0
+    torch.cuda.synchronize()
+    assert ra == rb.value and a.stats()[0].tobytes() == b.stats()[0].tobytes()
