@@ -261,11 +261,20 @@ def main():
     import paper_2511_13724_b200 as P
     from paper_2511_13724_b200 import seneca as S
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # One process per GPU over NCCL.  SENECA_DIST_BACKEND=gloo (test only) runs the
+    # multi-rank host logic with several ranks sharing the GPUs there are
+    # (ranks map to local_rank mod device_count; timings reduce on the CPU).
+    backend = os.environ.get("SENECA_DIST_BACKEND", "nccl")
+    local_dev = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    red_dev = dev if backend == "nccl" else None
     stream = torch.cuda.current_stream(dev)
 
     from paper_2511_13724_b200 import dist as D
@@ -313,7 +322,7 @@ def main():
         S.destroy(ctx)
 
     # ---- timed steps (device time, CUDA events on the launch stream)
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(local_dev)
     clocks.start()
     ods_ms, mdp_ms, launches, rounds_tot = [], [], 0, 0
     kstats = {}
@@ -417,7 +426,7 @@ def main():
                 served_all &= bool(np.all(stk["served"].sum(axis=2) == c["n_total"]))
             S.destroy(rctx)
             del ws_r
-            (rep_s,) = D.reduce_times([sum(rep_ms) / 1e3], device=dev)
+            (rep_s,) = D.reduce_times([sum(rep_ms) / 1e3], device=red_dev)
             tried.append(dict(R=R, value=R * dec_per_step * args.steps * world / rep_s, unit="decisions/s",
                               ms_per_step=1e3 * rep_s / args.steps,
                               per_replica_value=dec_per_step * args.steps / rep_s,
@@ -488,7 +497,7 @@ def main():
     mdp_s = sum(mdp_ms) / 1e3
     e2e_s = sum(e2e_ods)
     e2e_m = sum(e2e_mdp)
-    ods_s, mdp_s, e2e_s, e2e_m = D.reduce_times([ods_s, mdp_s, e2e_s, e2e_m], device=dev)   # max over ranks
+    ods_s, mdp_s, e2e_s, e2e_m = D.reduce_times([ods_s, mdp_s, e2e_s, e2e_m], device=red_dev)   # max over ranks
     total_dec = dec_per_step * args.steps * world
     total_evals = args.mdp_profiles * nsplit * args.steps * world
 
@@ -541,7 +550,7 @@ def main():
                 evict_tiers="all" if args.evict_tiers else "A",
                 mdp_profiles=args.mdp_profiles, mdp_grid_step_pct=args.mdp_grid_step,
                 mdp_grid_written=d_grid is not None,
-                parallelism=f"{world} independent replays (seed+rank) + {world} MDP profile slices",
+                parallelism=f"{world} independent replays (seed+rank) + {world} independent MDP profile sets",
                 l2="flushed between timed steps (512 MiB write)")),
             e2e=dict(value=total_dec / e2e_s, unit="decisions/s",
                      h2d_bytes_per_step=int(pin_prof.numel()), d2h_bytes_per_step=int(nst + pin_res.numel()),
