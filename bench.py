@@ -222,7 +222,10 @@ def algorithmic_bytes(name, info):
     if name == "ods_perm_all":
         return 4 * info["n_total"] * info["job_epochs"]     # ALU-bound (Philox); bytes written
     if name == "ods_recount_all":
-        return (3 * J + 1) * 5 * W4
+        # the init bitmap pass: 3 residency + J seen + J consumer bitmaps (DRAM reads; the
+        # residency re-reads per job hit L2); per pool
+        # (3J + 1) one u8 count per 128 ids and one u32 per 4096 ids written
+        return (3 + 2 * J) * W4 + (3 * J + 1) * (W4 // 16 + W4 // 512 * 4)
     if name == "ods_init_tiers":
         return 4 * info["cache_entries"]
     return 0

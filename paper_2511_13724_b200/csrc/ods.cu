@@ -1174,41 +1174,55 @@ __global__ void ods_init_tiers(const __grid_constant__ Lays LS, const __grid_con
     }
 }
 
-// Pool counts of every job and of the storage pool (init): one CTA of 128
-// threads per superblock (one word each; 4 threads per 128-id block).
-__global__ void __launch_bounds__(128)
+// Pool counts of every job and of the storage pool (init): the bitmap pass.
+// One warp per 4096-id superblock, one 128-id block (a 16-B vector of each
+// bitmap) per lane: the residency vectors are read once, then each job's seen
+// and consumer vectors (every bitmap byte read exactly once, 512 contiguous
+// bytes per warp and bitmap), and the 3J + 1 pool counts are formed in
+// registers: block count = 4 popcounts, 4 lanes' counts packed into one word
+// of the superblock's 32-B count row, the superblock total by a warp sum.
+// blockIdx.z is the job: few registers, many warps in flight (memory-level
+// parallelism); the residency vectors are re-read per job (from L2).
+constexpr uint32_t kRecountWarps = 8;        // superblocks per CTA of the init bitmap pass
+__global__ void __launch_bounds__(kRecountWarps * 32)
 ods_recount_all(const __grid_constant__ Lays LS, const __grid_constant__ Cfg C) {
-    const Lay& L = LS.r[blockIdx.z];
-    const uint32_t sblk = blockIdx.x, pool = blockIdx.y;    // pool < 3J: (j, tier); == 3J: storage
-    const uint32_t w = sblk * 128 + threadIdx.x;
-    uint32_t word;
-    const uint32_t a = L.bm_a[w], d = L.bm_d[w], e = L.bm_e[w];
-    if (pool == 3 * C.J) {
-        word = ~(a | d | e) & valid_mask(C, w);
-    } else {
-        const uint32_t j = pool / 3, tt = pool % 3;
-        const uint32_t s = L.seen[(size_t)j * C.NW + w];
-        word = tt == 0 ? (a & ~s & ~L.cons[(size_t)j * C.NW + w]) : (tt == 1 ? (d & ~s) : (e & ~s));
-    }
-    uint32_t c = __popc(word);                                 // block count over 4 lanes
-    c += __shfl_xor_sync(0xffffffffu, c, 1);
-    c += __shfl_xor_sync(0xffffffffu, c, 2);
-    // pack 4 consecutive block counts (lanes 0,4,8,12 of each 16-lane group) into a word
-    const uint32_t b0 = __shfl_sync(0xffffffffu, c, (threadIdx.x & 16) + 0);
-    const uint32_t b1 = __shfl_sync(0xffffffffu, c, (threadIdx.x & 16) + 4);
-    const uint32_t b2 = __shfl_sync(0xffffffffu, c, (threadIdx.x & 16) + 8);
-    const uint32_t b3 = __shfl_sync(0xffffffffu, c, (threadIdx.x & 16) + 12);
-    if ((threadIdx.x & 15) == 0)
-        L.cnt8[(size_t)pool * (C.NBp >> 2) + (w >> 4)] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
-    __shared__ uint32_t s_w[4];
-    const uint32_t ws = warp_sum(__popc(word));
-    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = ws;
+    const Lay& L = LS.r[blockIdx.y];
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t sblk = blockIdx.x * kRecountWarps + (threadIdx.x >> 5);   // grid (NS/8, replicas, J)
+    __shared__ uint32_t s_tot[4];                                  // this CTA's pool totals: S, A, D, E
+    if (threadIdx.x < 4) s_tot[threadIdx.x] = 0;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        const uint32_t t = s_w[0] + s_w[1] + s_w[2] + s_w[3];
-        L.cnt_sup[(size_t)pool * C.NS + sblk] = t;
-        if (t) atomicAdd(L.cnt_tot + pool, t);
-    }
+    const bool live = sblk < C.NS;
+    const uint32_t blk = sblk * 32 + lane, w0 = blk * kWordsPerBlock;
+    const uint4 z4 = make_uint4(0, 0, 0, 0);
+    const uint4 a = live ? __ldcs(reinterpret_cast<const uint4*>(L.bm_a + w0)) : z4;
+    const uint4 d = live ? __ldcs(reinterpret_cast<const uint4*>(L.bm_d + w0)) : z4;
+    const uint4 e = live ? __ldcs(reinterpret_cast<const uint4*>(L.bm_e + w0)) : z4;
+    auto emit = [&](uint32_t pool, uint32_t slot, uint4 x) {
+        const uint32_t c = __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);   // <= 128: one byte
+        const uint32_t c1 = __shfl_down_sync(0xffffffffu, c, 1);
+        const uint32_t c2 = __shfl_down_sync(0xffffffffu, c, 2);
+        const uint32_t c3 = __shfl_down_sync(0xffffffffu, c, 3);
+        if (live && (lane & 3) == 0)
+            L.cnt8[(size_t)pool * (C.NBp >> 2) + (blk >> 2)] = c | (c1 << 8) | (c2 << 16) | (c3 << 24);
+        const uint32_t t = warp_sum(c);
+        if (live && lane == 0) {
+            L.cnt_sup[(size_t)pool * C.NS + sblk] = t;
+            if (t) atomicAdd(&s_tot[slot], t);
+        }
+    };
+    const uint32_t j = blockIdx.z;
+    const uint4 S_ = live ? __ldcs(reinterpret_cast<const uint4*>(L.seen + (size_t)j * C.NW + w0)) : z4;
+    const uint4 Cv = live ? __ldcs(reinterpret_cast<const uint4*>(L.cons + (size_t)j * C.NW + w0)) : z4;
+    if (j == 0)
+        emit(3 * C.J, 0, make_uint4(~(a.x | d.x | e.x) & valid_mask(C, w0 + 0), ~(a.y | d.y | e.y) & valid_mask(C, w0 + 1),
+                                    ~(a.z | d.z | e.z) & valid_mask(C, w0 + 2), ~(a.w | d.w | e.w) & valid_mask(C, w0 + 3)));
+    emit(j * 3 + 0, 1, make_uint4(a.x & ~S_.x & ~Cv.x, a.y & ~S_.y & ~Cv.y, a.z & ~S_.z & ~Cv.z, a.w & ~S_.w & ~Cv.w));
+    emit(j * 3 + 1, 2, make_uint4(d.x & ~S_.x, d.y & ~S_.y, d.z & ~S_.z, d.w & ~S_.w));
+    emit(j * 3 + 2, 3, make_uint4(e.x & ~S_.x, e.y & ~S_.y, e.z & ~S_.z, e.w & ~S_.w));
+    __syncthreads();                                                // one global add per pool per CTA
+    if (threadIdx.x < 4 && s_tot[threadIdx.x])
+        atomicAdd(L.cnt_tot + (threadIdx.x == 0 ? 3 * C.J : j * 3 + threadIdx.x - 1), s_tot[threadIdx.x]);
 }
 
 __global__ void ods_init_jobs(const __grid_constant__ Lays LS, const __grid_constant__ Cfg C) {
@@ -1585,7 +1599,8 @@ extern "C" seneca_status seneca_init_cache(const seneca_cache_config* cfg, void*
         });
         INIT_TRY(cudaGetLastError());
         timed(c, K_RECOUNT, st, [&] {
-            ods_recount_all<<<dim3(c->C.NS, 3 * c->C.J + 1, c->R), 128, 0, st>>>(c->LS, c->C);
+            ods_recount_all<<<dim3((c->C.NS + kRecountWarps - 1) / kRecountWarps, c->R, c->C.J), kRecountWarps * 32, 0,
+                              st>>>(c->LS, c->C);
         });
         INIT_TRY(cudaGetLastError());
         ods_init_jobs<<<c->R, 32, 0, st>>>(c->LS, c->C);

@@ -27,3 +27,6 @@ for w in imagenet1k openimages imagenet22k; do
 done
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:mdp_sweep -c 1 -o $OUT/ncu_mdp_sweep \
   python tools/profile_ods.py toy 10 --mdp > /dev/null 2>&1; echo "ncu mdp rc=$?"
+# the init bitmap pass (ods_recount_all) at ImageNet-22K size
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:ods_recount_all -c 1 -o $OUT/ncu_recount_imagenet22k \
+  python tools/profile_ods.py imagenet22k 1 > /dev/null 2>&1; echo "ncu recount rc=$?"
