@@ -31,10 +31,14 @@ constexpr int kMaxSteps = 101;  // grid step 1 % -> 101 values per coordinate
 #ifndef SENECA_MDP_CHUNK
 #define SENECA_MDP_CHUNK 512
 #endif
+#ifndef SENECA_MDP_UNROLL
+#define SENECA_MDP_UNROLL 4
+#endif
 #ifndef SENECA_MDP_MINB
 #define SENECA_MDP_MINB 3
 #endif
 constexpr uint32_t kChunk = SENECA_MDP_CHUNK;  // splits per sweep work item (16 per lane)
+constexpr int kUnroll = SENECA_MDP_UNROLL;      // splits in flight per lane
 
 enum : uint8_t { L_CACHE = 0, L_NIC = 1, L_PCIE = 2, L_CPU_AUG = 3, L_CPU_DEC_AUG = 4, L_GPU = 5, L_STORAGE = 6 };
 
@@ -214,7 +218,7 @@ __device__ __forceinline__ void sweep32_chunk(const Sweep32& P, const Row* rows,
     const uint32_t N = P.N;
     const double dN = P.dN, y = P.y, dsiE = P.dsiE, dsiS = P.dsiS;
     const uint32_t lane = threadIdx.x & 31;
-#pragma unroll 4
+#pragma unroll (kUnroll)
     for (uint32_t u = 0; u < kChunk / 32; ++u) {
         const uint32_t idx = i0 + u * 32 + lane;
         if (!kFull && idx >= n_splits) break;
