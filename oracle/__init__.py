@@ -105,6 +105,8 @@ def _declare(L):
     L.oracle_ods_create.argtypes = [C.c_uint64, C.c_uint32, u32p, u32p, C.c_uint64, C.c_uint64,
                                     C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.c_int]
     L.oracle_ods_create.restype = C.c_void_p
+    L.oracle_ods_set_arrivals.argtypes = [C.c_void_p, u32p]
+    L.oracle_ods_set_arrivals.restype = None
     L.oracle_ods_destroy.argtypes = [C.c_void_p]
     L.oracle_ods_need.argtypes = [C.c_void_p, C.c_uint32]; L.oracle_ods_need.restype = C.c_uint64
     L.oracle_ods_round.argtypes = [C.c_void_p, u32p, C.c_uint32, C.c_void_p, C.c_uint32, u32p, u8p, u32p]
@@ -227,7 +229,7 @@ class ODS:
     evict_tiers = ALL (R-O21), baseline the uniform no-evict sampler (R-O22)."""
 
     def __init__(self, n_total, batch, target, cap_e, cap_d, cap_a, seed, transcript=False, evict_all=False,
-                 baseline=False):
+                 baseline=False, arrival=None):
         self.N = int(n_total)
         self.batch = np.ascontiguousarray(batch, np.uint32)
         self.target = np.ascontiguousarray(target, np.uint32)
@@ -238,6 +240,9 @@ class ODS:
                                          int(bool(evict_all)), int(bool(baseline)))
         if not self.h:
             raise ValueError("oracle_ods_create rejected the configuration")
+        if arrival is not None:                                     # R-O23
+            self._arrival = np.ascontiguousarray(arrival, np.uint32)
+            lib().oracle_ods_set_arrivals(self.h, self._arrival)
         self.max_target = lib().oracle_ods_max_target(self.h)
 
     def __del__(self):

@@ -64,7 +64,8 @@ class LiteralODS:
     tier by tier A -> D -> E from one keyed rank stream over the round-start
     storage pool."""
 
-    def __init__(self, n_total, batch, target, cap_e, cap_d, cap_a, seed, evict_all=False, baseline=False):
+    def __init__(self, n_total, batch, target, cap_e, cap_d, cap_a, seed, evict_all=False, baseline=False,
+                 arrival=None):
         self.N, self.batch, self.target = n_total, list(batch), list(target)
         self.J = len(batch)
         self.cap_a, self.seed = cap_a, seed
@@ -83,7 +84,9 @@ class LiteralODS:
         self.c = [0] * self.J
         self.e = [0] * self.J
         self.n = [0] * self.J
-        self.active = [True] * self.J
+        self.arrival = list(arrival) if arrival is not None else [0] * self.J   # R-O23
+        self.pending = [a > 0 for a in self.arrival]
+        self.active = [not p for p in self.pending]
         self.r = 0
         self.deliveries = [[[] for _ in range(max(target))] for _ in range(self.J)]  # (id, src)
         self.evicted = 0
@@ -95,7 +98,13 @@ class LiteralODS:
         return [i for i in range(self.N)
                 if self.tier[i] == t and i not in self.seen[j] and (t != A or i not in self.cons[j])]
 
+    def arrive(self):
+        for j in range(self.J):
+            if self.pending[j] and self.arrival[j] <= self.r:
+                self.pending[j], self.active[j] = False, True
+
     def round(self, jobs):
+        self.arrive()
         departing = set()
         a_served = []
         for j in jobs:
@@ -176,5 +185,9 @@ class LiteralODS:
         self.r += 1
 
     def replay_all(self):
-        while any(self.active):
+        while any(self.active) or any(self.pending):
+            self.arrive()
+            if not any(self.active):
+                self.r += 1                                    # idle round (R-O23)
+                continue
             self.round([j for j in range(self.J) if self.active[j]])

@@ -336,6 +336,8 @@ typedef struct {
     int      evict_all;            /* evict_tiers = ALL (R-O21): consumer sets and
                                       eviction for every cached tier            */
     int      baseline;             /* the uniform no-evict sampler (R-O22)     */
+    uint64_t arrival[32];          /* job arrival rounds (R-O23)              */
+    int      pending[32];          /* not yet arrived                         */
 } ods_t;
 
 /* tiers that carry consumer sets and can be evicted: A (R-O5), or all (R-O21);
@@ -459,6 +461,33 @@ void *oracle_ods_create(uint64_t N, uint32_t J, const uint32_t *batch, const uin
     return o;
 }
 
+/* Job arrivals (R-O23, SURVEY 8(f) NEXT-1 job-arrival traces): job j takes
+ * part from round arrival[j] on (0: from the start).  A round in which no job
+ * is active while arrivals are pending is idle (it only advances the round
+ * counter).  Call before the first round.                                    */
+void oracle_ods_set_arrivals(void *h, const uint32_t *arrival)
+{
+    ods_t *o = h;
+    for (uint32_t j = 0; j < o->J; ++j) {
+        o->arrival[j] = arrival ? arrival[j] : 0;
+        o->pending[j] = o->arrival[j] > o->r;
+        if (o->pending[j]) o->active[j] = 0;
+    }
+}
+
+/* jobs whose arrival round has come join the active set (start of a round) */
+static void arrive(ods_t *o)
+{
+    for (uint32_t j = 0; j < o->J; ++j)
+        if (o->pending[j] && o->arrival[j] <= o->r) { o->pending[j] = 0; o->active[j] = 1; }
+}
+
+static int any_pending(const ods_t *o)
+{
+    for (uint32_t j = 0; j < o->J; ++j) if (o->pending[j]) return 1;
+    return 0;
+}
+
 /* need_j = min(B_j, N - n_j) */
 uint64_t oracle_ods_need(void *h, uint32_t j)
 {
@@ -476,6 +505,7 @@ int oracle_ods_round(void *h, const uint32_t *jobs, uint32_t n_jobs, const uint3
                      uint32_t bmax, uint32_t *out_ids, uint8_t *out_src, uint32_t *out_lens)
 {
     ods_t *o = h;
+    arrive(o);
     if (n_jobs == 0 || n_jobs > o->J) return O_EINVAL;
     for (uint32_t x = 0; x < n_jobs; ++x) {
         if (jobs[x] >= o->J) return O_EINVAL;
@@ -683,9 +713,14 @@ uint64_t oracle_ods_replay_rounds(void *h, uint64_t n_rounds)
     ids = malloc((size_t)o->J * bmax * 4); src = malloc((size_t)o->J * bmax);
     uint64_t done = 0;
     for (; done < n_rounds; ++done) {
+        arrive(o);
         uint32_t nj = 0;
         for (uint32_t j = 0; j < o->J; ++j) if (o->active[j]) jobs[nj++] = j;
-        if (nj == 0) break;
+        if (nj == 0) {
+            if (!any_pending(o)) break;
+            o->r += 1;                                  /* idle round (R-O23) */
+            continue;
+        }
         oracle_ods_round(o, jobs, nj, NULL, bmax, ids, src, lens);
     }
     free(ids); free(src);
@@ -698,11 +733,15 @@ uint64_t oracle_ods_replay_epochs(void *h, uint32_t n_epochs)
 {
     ods_t *o = h;
     uint64_t goal[32]; int tracked[32];
-    for (uint32_t j = 0; j < o->J; ++j) { tracked[j] = o->active[j]; goal[j] = o->e[j] + n_epochs; }
+    for (uint32_t j = 0; j < o->J; ++j) {
+        tracked[j] = o->active[j] || o->pending[j];
+        goal[j] = o->e[j] + n_epochs;
+    }
     uint64_t rounds = 0;
     for (;;) {
         int pending = 0;
-        for (uint32_t j = 0; j < o->J; ++j) if (tracked[j] && o->active[j] && o->e[j] < goal[j]) pending = 1;
+        for (uint32_t j = 0; j < o->J; ++j)
+            if (tracked[j] && (o->active[j] || o->pending[j]) && o->e[j] < goal[j]) pending = 1;
         if (!pending) break;
         rounds += oracle_ods_replay_rounds(o, 1);
     }

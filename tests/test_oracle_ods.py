@@ -447,3 +447,50 @@ def test_hit_rate_vs_cache_fraction_ods_above_baseline():
         h_base = base.stats()[0]["served"][:, 1:, 1:].sum(axis=2) / 1000
         assert np.all(h_base == frac)
         assert np.all(h_ods >= frac + 0.25)
+
+
+# ------------------------------------------------------------ job arrivals (NEXT-1 job-arrival traces, R-O23)
+def _random_arrivals(st, J):
+    return [0 if k == 0 else int(st.u64(1)[0] % 40) for k in range(J)]
+
+
+@pytest.mark.parametrize("block", range(4))
+def test_arrivals_cross_check_with_literal_transcription(block):
+    st = synth.Stream(13000 + block)
+    for _ in range(60):
+        cfg = synth.random_tiny_ods(st)
+        arr = _random_arrivals(st, len(cfg["batch"]))
+        for evict_all in (False, True):
+            o = O.ODS(cfg["n_total"], cfg["batch"], cfg["target"], cfg["cap_e"], cfg["cap_d"], cfg["cap_a"],
+                      cfg["seed"], transcript=True, evict_all=evict_all, arrival=arr)
+            o.replay_epochs(max(cfg["target"]))
+            lit = L.LiteralODS(cfg["n_total"], cfg["batch"], cfg["target"], cfg["cap_e"], cfg["cap_d"],
+                               cfg["cap_a"], cfg["seed"], evict_all=evict_all, arrival=arr)
+            lit.replay_all()
+            tr = o.transcript()
+            for j in range(len(cfg["batch"])):
+                for e in range(cfg["target"][j]):
+                    got = [(int(x) & 0xFFFFFFFF, int(x) >> 32) for x in tr[j, e]]
+                    assert got == lit.deliveries[j][e], (cfg, arr)
+            assert list(o.state()[0]) == lit.tier
+            assert o.r == lit.r
+
+
+def test_arrivals_makespan_trace():
+    """A makespan-style trace (jobs queued, at most two at a time): job
+    k arrives when job k-2 departs, computed from the data-independent schedule
+    (R-O12).  The replay ends when the last job departs; the round count is the
+    makespan in rounds; with a single job at a time the rounds add up exactly."""
+    N, B = 2000, 100
+    cfg = dict(n_total=N, batch=[B] * 4, target=[2] * 4, cap_e=0, cap_d=0, cap_a=400, seed=8)
+    per_job = 2 * ((N + B - 1) // B)                          # rounds a job needs alone: 40
+    serial = [0, per_job, 2 * per_job, 3 * per_job]          # one job at a time
+    o = O.ODS(N, cfg["batch"], cfg["target"], 0, 0, 400, 8, transcript=True, arrival=serial)
+    assert o.replay_epochs(2) == 4 * per_job
+    _check_invariants(o, cfg)
+    two = [0, 0, per_job, per_job]                            # two at a time
+    o2 = O.ODS(N, cfg["batch"], cfg["target"], 0, 0, 400, 8, arrival=two)
+    assert o2.replay_epochs(2) == 2 * per_job
+    gap = [0, 3 * per_job, 3 * per_job, 3 * per_job]          # idle rounds between the jobs
+    o3 = O.ODS(N, cfg["batch"], cfg["target"], 0, 0, 400, 8, arrival=gap)
+    assert o3.replay_epochs(2) == 4 * per_job
