@@ -179,6 +179,12 @@ typedef struct {
                                       cached id is a hit, misses go to storage, nothing is
                                       substituted, evicted or refilled                      */
     uint32_t        _pad0;
+    const uint32_t* arrival_round; /* host [n_jobs] or NULL (all 0): job j takes part from round
+                                      arrival_round[j] on (job-arrival / makespan traces, SURVEY
+                                      8(f) NEXT-1, DESIGN.md R-O23); before it the job is not in
+                                      the active set; a round with no active job while arrivals
+                                      are pending is idle.  next_batch on a job that has not
+                                      arrived is ESTATE                                        */
 } seneca_cache_config;
 
 /* Per job-epoch counters (R-O10; digest in DESIGN.md §3).  104 bytes.       */

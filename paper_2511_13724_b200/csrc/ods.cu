@@ -128,6 +128,8 @@ struct Launch {
     uint32_t subset;                 // jobs taking part in every round (& active)
     uint32_t mode;                   // 0 generated requests, 1 caller-supplied
     uint32_t active0;
+    uint32_t pending0;               // jobs that have not arrived yet (R-O23)
+    uint32_t arrival[kMaxJobs];      // arrival round of each job
     uint32_t n0[kMaxJobs];           // consumed samples of the current epoch at launch
     uint32_t e0[kMaxJobs];           // epoch at launch
     uint32_t row_of_job[kMaxJobs];   // output row of each job
@@ -751,7 +753,7 @@ __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSm
             const uint32_t a_w = C.evict_all ? (ldcg(L.bm_a + w) | ldcg(L.bm_d + w) | ldcg(L.bm_e + w))
                                              : ldcg(L.bm_a + w);
             if (!a_w) continue;
-            uint32_t ev = a_w;
+            uint32_t ev = active ? a_w : 0u;                        // nothing is evicted with no active job
             for (uint32_t m = active; m; m &= m - 1) ev &= ldcg(L.cons + (size_t)(__ffs(m) - 1) * C.NW + w);
             if (ev) {
                 const uint32_t base = atomicAdd(&M.ne, (uint32_t)__popc(ev));
@@ -770,7 +772,7 @@ __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSm
     }
     TM.tick(3);
     const uint32_t ne = M.ne;
-    const uint32_t k = min(M.deficit0 + ne, M.PS);
+    const uint32_t k = active ? min(M.deficit0 + ne, M.PS) : 0u;   // no refill with no active job
     if (!speculated) {
         if (k) prefix_from_smem(C, s_supS, s_pre, M.scan);
         maint_refill_select(L, C, M, s_pre, r, 0, k);
@@ -870,7 +872,7 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
     extern __shared__ __align__(16) uint32_t smem[];
     __shared__ JobSmem S;
     __shared__ MaintSmem M;
-    __shared__ uint32_t s_n[kMaxJobs], s_e[kMaxJobs], s_active;
+    __shared__ uint32_t s_n[kMaxJobs], s_e[kMaxJobs], s_active, s_pending;
     const uint32_t tid = threadIdx.x;
     const uint32_t rep = blockIdx.x / (C.J + 1);
     const uint32_t cta = blockIdx.x - rep * (C.J + 1);
@@ -908,11 +910,21 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
     if (is_maint && !coupled) return;
 
     if (tid < kMaxJobs) { s_n[tid] = P.n0[tid]; s_e[tid] = P.e0[tid]; }
-    if (tid == 0) s_active = P.active0;
+    if (tid == 0) {
+        s_active = P.active0;
+        s_pending = P.pending0;
+        for (uint32_t m = s_pending; m; m &= m - 1) {         // arrivals of the first round (R-O23)
+            const uint32_t jj = __ffs(m) - 1;
+            if (P.arrival[jj] <= P.r0) { s_active |= 1u << jj; s_pending &= ~(1u << jj); }
+        }
+    }
     if (!is_maint && tid == 0) {
         const JobDev jd = L.jobs[j];
         S.cur_buf = jd.cur_buf; S.nxt_buf = jd.nxt_buf; S.cursor = jd.cursor;
         S.cur_len = jd.cur_len; S.nxt_len = jd.nxt_len; S.recount = jd.recount;
+        // a job that has not arrived took no maintain results: its pools are rebuilt
+        // from the bitmaps when it arrives (R-O23)
+        if ((P.pending0 >> j) & 1u) S.recount = 1;
         S.perm_seen = 0;
         S.rep = rep;
         S.dens = 1.0f;
@@ -941,7 +953,8 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
             if (s_n[jj] + need_of(jj) == C.N && s_e[jj] + 1 == C.target[jj]) departing |= 1u << jj;
         }
     };
-    auto advance = [&](uint32_t part, uint32_t departing) {
+    // end of round r: progress, departures, then the arrivals of round r + 1
+    auto advance = [&](uint32_t part, uint32_t departing, uint64_t r) {
         __syncthreads();
         if (tid == 0) {
             for (uint32_t m = part; m; m &= m - 1) {
@@ -950,6 +963,10 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
                 if (s_n[jj] == C.N) { s_n[jj] = 0; s_e[jj] += 1; }
             }
             s_active &= ~departing;
+            for (uint32_t m = s_pending; m; m &= m - 1) {
+                const uint32_t jj = __ffs(m) - 1;
+                if (P.arrival[jj] <= r + 1) { s_active |= 1u << jj; s_pending &= ~(1u << jj); }
+            }
         }
         __syncthreads();
     };
@@ -1011,7 +1028,10 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
             }
             __syncthreads();
             TM.tick(2);
-            if (active_after && C.cap_t > 0) {
+            // a departure rebuilds the consumer counts for the remaining jobs even when
+            // none remains but arrivals are pending (no eviction, no refill then): a
+            // job arriving later must not inherit counts of departed consumers (R-O23)
+            if ((active_after || (departing && s_pending)) && C.cap_t > 0) {
                 if (!spec && tid == 0) set_deficits();
                 __syncthreads();
                 maint_apply(L, C, P, M, s_pre, s_sup, r, active_after, departing != 0, spec, M.ne_push, M.push_base, TM);
@@ -1019,7 +1039,7 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
             __syncthreads();
             if (tid == 0) { __threadfence(); atomicExch(L.bar + 2, rr + 1); }     // release round r's tiers
             TM.tick(5);
-            advance(part, departing);
+            advance(part, departing, r);
             spec = false;
             if (rr + 1 < P.rounds) {
                 uint32_t part2, departing2;
@@ -1074,7 +1094,7 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
                 }
                 TM.tick(0);
             }
-            advance(part, departing);
+            advance(part, departing, r);
             if (rr + 1 < P.rounds && ((s_active & P.subset) >> j & 1u)) {
                 job_walk(L, C, S, s_req, j, s_e[j], need_of(j), TM, s_win, pf);   // next request
                 TM.tick(13);
@@ -1283,6 +1303,8 @@ struct seneca_ctx {
     uint64_t cap_e, cap_d;
     uint64_t e[kMaxJobs], n[kMaxJobs];
     uint32_t active;
+    uint32_t pending;              // jobs that have not arrived (R-O23)
+    uint64_t arrival[kMaxJobs];
     uint64_t r;
     uint64_t launches;
     uint64_t klaunch[K_NCLASS];
@@ -1449,6 +1471,43 @@ void timed(seneca_ctx* c, int cls, cudaStream_t st, F&& launch) {
     if (cudaEventElapsedTime(&ms, c->ev_a, c->ev_b) == cudaSuccess) { c->kms[cls] += ms; c->ksampled[cls]++; }
 }
 
+// Host mirror of the data-independent schedule (R-O12, R-O23): per job the
+// consumed count and epoch, the active and not-yet-arrived sets, the round.
+struct Sched {
+    uint64_t n[kMaxJobs], e[kMaxJobs], arrival[kMaxJobs];
+    uint32_t active, pending;
+    uint64_t r;
+};
+
+Sched sched_of(const seneca_ctx* c) {
+    Sched s;
+    for (uint32_t j = 0; j < kMaxJobs; ++j) { s.n[j] = c->n[j]; s.e[j] = c->e[j]; s.arrival[j] = c->arrival[j]; }
+    s.active = c->active;
+    s.pending = c->pending;
+    s.r = c->r;
+    return s;
+}
+
+void sched_arrive(Sched& s) {               // start of round s.r
+    for (uint32_t m = s.pending; m; m &= m - 1) {
+        const uint32_t j = __builtin_ctz(m);
+        if (s.arrival[j] <= s.r) { s.active |= 1u << j; s.pending &= ~(1u << j); }
+    }
+}
+
+// one round of the jobs in mask (after sched_arrive); an idle round if none is active
+void sched_round(const Cfg& C, Sched& s, uint32_t mask) {
+    const uint32_t part = s.active & mask;
+    uint32_t departing = 0;
+    for (uint32_t m = part; m; m &= m - 1) {
+        const uint32_t j = __builtin_ctz(m);
+        s.n[j] += std::min<uint64_t>(C.batch[j], (uint64_t)C.N - s.n[j]);
+        if (s.n[j] == C.N) { s.n[j] = 0; s.e[j] += 1; if (s.e[j] == C.target[j]) departing |= 1u << j; }
+    }
+    s.active &= ~departing;
+    s.r += 1;
+}
+
 // Launch R rounds.  jobs_mask: the jobs of every round (replay: all active).
 seneca_status launch_rounds(seneca_ctx* c, uint64_t R, uint32_t jobs_mask, const uint32_t* d_requested,
                             uint32_t* out_ids, uint8_t* out_src, uint32_t out_stride, const uint32_t* row_of_job,
@@ -1460,10 +1519,12 @@ seneca_status launch_rounds(seneca_ctx* c, uint64_t R, uint32_t jobs_mask, const
     P.subset = jobs_mask;
     P.mode = c->mode;
     P.active0 = c->active;
+    P.pending0 = c->pending;
     for (uint32_t j = 0; j < c->C.J; ++j) {
         P.n0[j] = (uint32_t)c->n[j];
         P.e0[j] = (uint32_t)c->e[j];
         P.row_of_job[j] = row_of_job ? row_of_job[j] : j;
+        P.arrival[j] = (uint32_t)std::min<uint64_t>(c->arrival[j], 0xffffffffu);
     }
     P.out_stride = out_stride;
     P.out_ids = out_ids;
@@ -1496,22 +1557,17 @@ seneca_status launch_rounds(seneca_ctx* c, uint64_t R, uint32_t jobs_mask, const
     });
     if (le != cudaSuccess) return cuda_status(le, "cudaLaunchCooperativeKernel(ods_rounds)");
     // host mirror of the data-independent schedule
+    Sched sc = sched_of(c);
     for (uint64_t k = 0; k < R; ++k) {
-        const uint32_t part = c->active & jobs_mask;
-        uint32_t departing = 0;
-        for (uint32_t m = part; m; m &= m - 1) {
-            const uint32_t j = __builtin_ctz(m);
-            const uint64_t need = std::min<uint64_t>(c->C.batch[j], (uint64_t)c->C.N - c->n[j]);
-            c->n[j] += need;
-            if (c->n[j] == c->C.N) {
-                c->n[j] = 0;
-                c->e[j] += 1;
-                if (c->e[j] == c->C.target[j]) departing |= 1u << j;
-            }
-        }
-        c->active &= ~departing;
-        c->r += 1;
+        sched_arrive(sc);
+        sched_round(c->C, sc, jobs_mask);
     }
+    // (arrivals are applied at round starts only: a job stays pending until a
+    // launch runs its arrival round, whose kernel rebuilds the job's pools)
+    for (uint32_t j = 0; j < kMaxJobs; ++j) { c->n[j] = sc.n[j]; c->e[j] = sc.e[j]; }
+    c->active = sc.active;
+    c->pending = sc.pending;
+    c->r = sc.r;
     return SENECA_OK;
 }
 
@@ -1555,6 +1611,11 @@ extern "C" seneca_status seneca_init_cache(const seneca_cache_config* cfg, void*
     c->cap_e = cfg->cap_e;
     c->cap_d = cfg->cap_d;
     c->active = cfg->n_jobs == 32 ? 0xffffffffu : ((1u << cfg->n_jobs) - 1);
+    c->pending = 0;
+    for (uint32_t j = 0; j < cfg->n_jobs; ++j) {
+        c->arrival[j] = cfg->arrival_round ? cfg->arrival_round[j] : 0;
+        if (c->arrival[j] > 0) { c->active &= ~(1u << j); c->pending |= 1u << j; }
+    }
     c->round_smem = round_smem;
     cudaStream_t st = (cudaStream_t)stream;
     cudaGetDevice(&c->device);
@@ -1641,7 +1702,11 @@ extern "C" seneca_status seneca_ods_next_batch(seneca_ctx* c, const uint32_t* h_
         if (j >= c->C.J || (mask & (1u << j))) { set_error("bad or duplicate job %u", j); return SENECA_EINVAL; }
         mask |= 1u << j;
         rows[j] = x;
-        if (!(c->active & (1u << j))) { set_error("job %u has departed", j); return SENECA_ESTATE; }
+        const bool arrived = ((c->pending >> j) & 1u) && c->arrival[j] <= c->r;
+        if (!(c->active & (1u << j)) && !arrived) {
+            set_error((c->pending >> j) & 1u ? "job %u has not arrived yet" : "job %u has departed", j);
+            return SENECA_ESTATE;
+        }
     }
     for (uint32_t x = 0; x < n_jobs; ++x) {
         const uint32_t j = h_jobs[x];
@@ -1651,24 +1716,21 @@ extern "C" seneca_status seneca_ods_next_batch(seneca_ctx* c, const uint32_t* h_
                          (cudaStream_t)stream);
 }
 
-// Rounds needed until every tracked job completed n more epochs (or departed).
+// Rounds needed until every tracked job (active or not yet arrived at the call)
+// completed n more epochs or departed; idle rounds before an arrival included.
 static uint64_t rounds_for_epochs(const seneca_ctx* c, uint32_t n_epochs) {
-    uint64_t n[kMaxJobs], e[kMaxJobs], goal[kMaxJobs];
-    uint32_t active = c->active;
-    const uint32_t tracked = active;
-    for (uint32_t j = 0; j < c->C.J; ++j) { n[j] = c->n[j]; e[j] = c->e[j]; goal[j] = c->e[j] + n_epochs; }
+    Sched s = sched_of(c);
+    const uint32_t tracked = s.active | s.pending;
+    uint64_t goal[kMaxJobs];
+    for (uint32_t j = 0; j < kMaxJobs; ++j) goal[j] = s.e[j] + n_epochs;
     uint64_t R = 0;
     for (;;) {
-        bool pending = false;
-        for (uint32_t m = tracked & active; m; m &= m - 1) if (e[__builtin_ctz(m)] < goal[__builtin_ctz(m)]) pending = true;
-        if (!pending || !active) break;
-        uint32_t departing = 0;
-        for (uint32_t m = active; m; m &= m - 1) {
-            const uint32_t j = __builtin_ctz(m);
-            n[j] += std::min<uint64_t>(c->C.batch[j], (uint64_t)c->C.N - n[j]);
-            if (n[j] == c->C.N) { n[j] = 0; e[j] += 1; if (e[j] == c->C.target[j]) departing |= 1u << j; }
-        }
-        active &= ~departing;
+        sched_arrive(s);
+        bool open = false;
+        for (uint32_t m = tracked & (s.active | s.pending); m; m &= m - 1)
+            if (s.e[__builtin_ctz(m)] < goal[__builtin_ctz(m)]) open = true;
+        if (!open || !(s.active | s.pending)) break;
+        sched_round(c->C, s, 0xffffffffu);
         ++R;
     }
     return R;
@@ -1676,10 +1738,10 @@ static uint64_t rounds_for_epochs(const seneca_ctx* c, uint32_t n_epochs) {
 
 static seneca_status replay(seneca_ctx* c, uint64_t R, uint64_t* d_transcript, uint64_t* h_rounds, cudaStream_t st) {
     if (c->mode != 0) { set_error("replay requires request_mode 0"); return SENECA_ESTATE; }
-    if (!c->active) { set_error("no active job"); return SENECA_ESTATE; }
+    if (!(c->active | c->pending)) { set_error("no active job"); return SENECA_ESTATE; }
     uint64_t done = 0;
     const uint64_t kChunk = 1u << 30;
-    while (done < R && c->active) {
+    while (done < R && (c->active | c->pending)) {
         const uint64_t n = std::min<uint64_t>(R - done, kChunk);
         seneca_status s = launch_rounds(c, n, 0xffffffffu, nullptr, nullptr, nullptr, c->C.Bmax, nullptr,
                                         (unsigned long long*)d_transcript, st);
@@ -1694,7 +1756,7 @@ extern "C" seneca_status seneca_replay_epochs(seneca_ctx* c, uint32_t n_epochs, 
                                               uint64_t* h_rounds, void* stream) {
     if (!c || n_epochs == 0) { set_error("bad arguments"); return SENECA_EINVAL; }
     if (c->mode != 0) { set_error("replay requires request_mode 0"); return SENECA_ESTATE; }
-    if (!c->active) { set_error("no active job"); return SENECA_ESTATE; }
+    if (!(c->active | c->pending)) { set_error("no active job"); return SENECA_ESTATE; }
     return replay(c, rounds_for_epochs(c, n_epochs), d_transcript, h_rounds, (cudaStream_t)stream);
 }
 
@@ -1707,21 +1769,15 @@ extern "C" seneca_status seneca_replay_rounds(seneca_ctx* c, uint64_t n_rounds, 
                                               uint64_t* h_rounds, void* stream) {
     if (!c) { set_error("bad arguments"); return SENECA_EINVAL; }
     if (c->mode != 0) { set_error("replay requires request_mode 0"); return SENECA_ESTATE; }
-    if (!c->active) { set_error("no active job"); return SENECA_ESTATE; }
-    // stop early when every job has departed
+    if (!(c->active | c->pending)) { set_error("no active job"); return SENECA_ESTATE; }
+    // stop early when every job has departed (idle rounds before an arrival count)
     uint64_t R = 0;
     {
-        uint64_t n[kMaxJobs], e[kMaxJobs];
-        uint32_t active = c->active;
-        for (uint32_t j = 0; j < c->C.J; ++j) { n[j] = c->n[j]; e[j] = c->e[j]; }
-        while (R < n_rounds && active) {
-            uint32_t departing = 0;
-            for (uint32_t m = active; m; m &= m - 1) {
-                const uint32_t j = __builtin_ctz(m);
-                n[j] += std::min<uint64_t>(c->C.batch[j], (uint64_t)c->C.N - n[j]);
-                if (n[j] == c->C.N) { n[j] = 0; e[j] += 1; if (e[j] == c->C.target[j]) departing |= 1u << j; }
-            }
-            active &= ~departing;
+        Sched s = sched_of(c);
+        for (;;) {
+            sched_arrive(s);
+            if (R >= n_rounds || !(s.active | s.pending)) break;
+            sched_round(c->C, s, 0xffffffffu);
             ++R;
         }
     }
@@ -1747,6 +1803,8 @@ extern "C" seneca_status seneca_read_state(const seneca_ctx* c, seneca_state_vie
     v->round = c->r;
     for (uint32_t j = 0; j < c->C.J; ++j) { v->epoch[j] = c->e[j]; v->consumed[j] = c->n[j]; }
     v->active_mask = c->active;
+    for (uint32_t m = c->pending; m; m &= m - 1)             // arrived at the current round
+        if (c->arrival[__builtin_ctz(m)] <= c->r) v->active_mask |= 1u << __builtin_ctz(m);
     v->replicas = c->R;
     v->replica_stride = c->rep_stride;
     return SENECA_OK;

@@ -431,3 +431,71 @@ def test_replay_epoch_alias():
                                        torch.cuda.current_stream().cuda_stream) == 0
     torch.cuda.synchronize()
     assert ra == rb.value and a.stats()[0].tobytes() == b.stats()[0].tobytes()
+
+
+# ---------------------------------------------------------------- job arrivals (R-O23)
+@pytest.mark.parametrize("block", range(3))
+def test_arrivals_random_tiny_configs(block):
+    st = synth.Stream(14000 + block)
+    for _ in range(40):
+        c = synth.random_tiny_ods(st)
+        J = len(c["batch"])
+        arr = [0 if k == 0 else int(st.u64(1)[0] % 40) for k in range(J)]
+        for evict_all in (False, True):
+            o = O.ODS(c["n_total"], c["batch"], c["target"], c["cap_e"], c["cap_d"], c["cap_a"], c["seed"],
+                      transcript=True, evict_all=evict_all, arrival=arr)
+            g = P.ODSContext(c["n_total"], c["batch"], c["target"], c["cap_e"], c["cap_d"], c["cap_a"], c["seed"],
+                             evict_tiers=int(evict_all), arrival=arr)
+            tr = g.new_transcript()
+            rg = g.replay_epochs(max(c["target"]), tr)
+            ro = o.replay_epochs(max(c["target"]))
+            torch.cuda.synchronize()
+            assert rg == ro, (c, arr)
+            compare_state(o, g, tr)
+
+
+def test_arrivals_makespan_trace_and_replicas():
+    """Two-at-a-time makespan trace on ImageNet-1K/64 (A churn), 3 replicas."""
+    c = synth.ods_config("imagenet1k", scale=64, seed=9)
+    ce, cd, ca = caps_of(c)
+    per_job = c["target"][0] * -(-c["n_total"] // c["batch"][0])
+    arr = [0, 0, per_job, per_job]
+    R = 3
+    g = P.ODSContext(c["n_total"], c["batch"], c["target"], ce, cd, ca, 9, replicas=R, arrival=arr)
+    tr = g.new_transcript()
+    rounds = g.replay_epochs(max(c["target"]), tr)
+    torch.cuda.synchronize()
+    assert rounds == 2 * per_job
+    for k in range(R):
+        o = O.ODS(c["n_total"], c["batch"], c["target"], ce, cd, ca, 9 + k, transcript=True, arrival=arr)
+        assert o.replay_epochs(max(c["target"])) == rounds
+        compare_replica(o, g, k, tr[k])
+
+
+def test_arrivals_next_batch():
+    n, batch, target = 500, [16, 40, 9], [2, 1, 2]
+    arr = [0, 12, 30]
+    o = O.ODS(n, batch, target, 60, 50, 40, 3, arrival=arr)
+    g = P.ODSContext(n, batch, target, 60, 50, 40, 3, arrival=arr)
+    with pytest.raises(S.SenecaError) as ei:
+        g.next_batch([1])                                     # job 1 arrives at round 12
+    assert ei.value.status == S.ESTATE
+    st = synth.Stream(4)
+    for _ in range(200):
+        _, e, _, _ = o.job_state()
+        if all(int(e[j]) >= target[j] for j in range(3)):
+            break
+        live = [j for j in range(3) if arr[j] <= o.r and int(e[j]) < target[j]]
+        if not live:                                         # idle round on both sides
+            assert o.replay_rounds(1) == 1 and g.replay_rounds(1) == 1
+            continue
+        pick = [j for j in live if st.uniform(1)[0] < 0.7] or live[:1]
+        rc, ids_o, src_o, lens_o = o.round(pick)
+        assert rc == 0
+        ids_g, src_g, lens_g = g.next_batch(pick)
+        torch.cuda.synchronize()
+        assert list(lens_o) == lens_g
+        for x, L_ in enumerate(lens_g):
+            assert np.array_equal(ids_g[x, :L_].cpu().numpy().view(np.uint32), ids_o[x, :L_])
+            assert np.array_equal(src_g[x, :L_].cpu().numpy(), src_o[x, :L_])
+    compare_state(o, g)
