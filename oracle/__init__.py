@@ -107,6 +107,8 @@ def _declare(L):
     L.oracle_ods_create.restype = C.c_void_p
     L.oracle_ods_set_arrivals.argtypes = [C.c_void_p, u32p]
     L.oracle_ods_set_arrivals.restype = None
+    L.oracle_ods_set_cold.argtypes = [C.c_void_p]
+    L.oracle_ods_set_cold.restype = None
     L.oracle_ods_destroy.argtypes = [C.c_void_p]
     L.oracle_ods_need.argtypes = [C.c_void_p, C.c_uint32]; L.oracle_ods_need.restype = C.c_uint64
     L.oracle_ods_round.argtypes = [C.c_void_p, u32p, C.c_uint32, C.c_void_p, C.c_uint32, u32p, u8p, u32p]
@@ -225,11 +227,12 @@ def metadata_bytes(n_total: int, n_jobs: int) -> int:
 
 # --------------------------------------------------------------------------- ODS
 class ODS:
-    """One oracle replay instance (R-O1..R-O22 of DESIGN.md §3); evict_all selects
-    evict_tiers = ALL (R-O21), baseline the uniform no-evict sampler (R-O22)."""
+    """One oracle replay instance (R-O1..R-O24 of DESIGN.md §3); evict_all selects
+    evict_tiers = ALL (R-O21), baseline the uniform no-evict sampler (R-O22),
+    arrival the job arrival rounds (R-O23), cold the cold start (R-O24)."""
 
     def __init__(self, n_total, batch, target, cap_e, cap_d, cap_a, seed, transcript=False, evict_all=False,
-                 baseline=False, arrival=None):
+                 baseline=False, arrival=None, cold=False):
         self.N = int(n_total)
         self.batch = np.ascontiguousarray(batch, np.uint32)
         self.target = np.ascontiguousarray(target, np.uint32)
@@ -240,6 +243,8 @@ class ODS:
                                          int(bool(evict_all)), int(bool(baseline)))
         if not self.h:
             raise ValueError("oracle_ods_create rejected the configuration")
+        if cold:                                                    # R-O24
+            lib().oracle_ods_set_cold(self.h)
         if arrival is not None:                                     # R-O23
             self._arrival = np.ascontiguousarray(arrival, np.uint32)
             lib().oracle_ods_set_arrivals(self.h, self._arrival)

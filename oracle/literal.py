@@ -65,7 +65,7 @@ class LiteralODS:
     storage pool."""
 
     def __init__(self, n_total, batch, target, cap_e, cap_d, cap_a, seed, evict_all=False, baseline=False,
-                 arrival=None):
+                 arrival=None, cold=False):
         self.N, self.batch, self.target = n_total, list(batch), list(target)
         self.J = len(batch)
         self.cap_a, self.seed = cap_a, seed
@@ -79,6 +79,9 @@ class LiteralODS:
         iota = [perm(key(seed, 1), n_total, p) for p in range(cap_a + cap_d + cap_e)]
         for p, i in enumerate(iota):
             self.tier[i] = A if p < cap_a else (D if p < cap_a + cap_d else E)
+        self.cold, self.warm = cold, not cold                 # R-O24: empty tiers, admission until full
+        if cold:
+            self.tier = [S] * n_total
         self.seen = [set() for _ in range(self.J)]
         self.cons = [set() for _ in range(self.J)]
         self.c = [0] * self.J
@@ -107,6 +110,7 @@ class LiteralODS:
         self.arrive()
         departing = set()
         a_served = []
+        fetched = {}
         for j in jobs:
             need = min(self.batch[j], self.N - self.n[j])
             K = key(self.seed, 2, j, self.e[j])
@@ -146,6 +150,8 @@ class LiteralODS:
                 if src[s] & 3 in self.cached:
                     self.cons[j].add(out[s])
                     a_served.append(out[s])
+                if src[s] == S and not self.warm:
+                    fetched.setdefault(j, []).append(out[s])
                 self.deliveries[j][self.e[j]].append((out[s], src[s]))
             self.n[j] += need
             if self.n[j] == self.N:
@@ -163,14 +169,24 @@ class LiteralODS:
                     else sorted(set(a_served)))
             evict = [i for i in cand if self.tier[i] in self.cached and
                      all(i in self.cons[a] for a in range(self.J) if self.active[a])]
+            admit = not self.warm
             deficit = {}
             for t in (A, D, E):
                 size = sum(1 for x in self.tier if x == t) - sum(1 for i in evict if self.tier[i] == t)
-                deficit[t] = self.cap[t] - size if t in self.cached else 0
-            pool_s = self.pool(S, 0)
-            k = min(deficit[A] + deficit[D] + deficit[E], len(pool_s))
-            Kr = key(self.seed, 4, 0, self.r)
-            fill = [pool_s[perm(Kr, len(pool_s), u)] for u in range(k)]
+                deficit[t] = self.cap[t] - size if (t in self.cached or admit) else 0
+            want = deficit[A] + deficit[D] + deficit[E]
+            if admit:                                        # R-O24: this round's storage fetches
+                fill = []
+                for j in sorted(fetched):
+                    for i in fetched[j]:
+                        if self.tier[i] == S and i not in fill and len(fill) < want:
+                            fill.append(i)
+                k = len(fill)
+            else:
+                pool_s = self.pool(S, 0)
+                k = min(want, len(pool_s))
+                Kr = key(self.seed, 4, 0, self.r)
+                fill = [pool_s[perm(Kr, len(pool_s), u)] for u in range(k)]
             dest = []
             for t in (A, D, E):                              # tier by tier from one rank stream
                 dest += [t] * min(deficit[t], k - len(dest))
@@ -180,6 +196,8 @@ class LiteralODS:
                     self.cons[a].discard(i)
             for i, t in zip(fill, dest):
                 self.tier[i] = t
+            if admit and all(sum(1 for x in self.tier if x == t) == self.cap[t] for t in (A, D, E)):
+                self.warm = True
             self.evicted += len(evict)
             self.refilled += k
         self.r += 1

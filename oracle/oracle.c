@@ -338,6 +338,7 @@ typedef struct {
     int      baseline;             /* the uniform no-evict sampler (R-O22)     */
     uint64_t arrival[32];          /* job arrival rounds (R-O23)              */
     int      pending[32];          /* not yet arrived                         */
+    int      cold, warm;           /* cold start (R-O24): admission until full */
 } ods_t;
 
 /* tiers that carry consumer sets and can be evicted: A (R-O5), or all (R-O21);
@@ -476,6 +477,17 @@ void oracle_ods_set_arrivals(void *h, const uint32_t *arrival)
 }
 
 /* jobs whose arrival round has come join the active set (start of a round) */
+/* Cold start (R-O24): every tier starts empty; until all
+ * three are full once, the storage-fetched samples of each round are admitted
+ * at the round end instead of random refills.  Call before the first round. */
+void oracle_ods_set_cold(void *h)
+{
+    ods_t *o = h;
+    memset(o->bm_e, 0, o->W * 8); memset(o->bm_d, 0, o->W * 8); memset(o->bm_a, 0, o->W * 8);
+    o->cold = 1;
+    o->warm = 0;
+}
+
 static void arrive(ods_t *o)
 {
     for (uint32_t j = 0; j < o->J; ++j)
@@ -530,6 +542,8 @@ int oracle_ods_round(void *h, const uint32_t *jobs, uint32_t n_jobs, const uint3
     uint64_t a_served_cap = 0;
     for (uint32_t x = 0; x < n_jobs; ++x) a_served_cap += oracle_ods_need(o, jobs[x]);
     uint64_t *a_served = malloc((a_served_cap + 1) * 8), n_a_served = 0;
+    /* storage fetches of the round per job, slot order (cold-start admission, R-O24) */
+    uint64_t *fetched[32] = {0}, n_fetched[32] = {0};
     int departing[32] = {0};
 
     for (uint32_t x = 0; x < n_jobs; ++x) {
@@ -600,6 +614,10 @@ int oracle_ods_round(void *h, const uint32_t *jobs, uint32_t n_jobs, const uint3
             int t = src[s] & 3, sub = (src[s] & SUBST) != 0;
             bit_set(seen_j, i);
             if (tracked(o, t)) { bit_set(cons_j, i); a_served[n_a_served++] = i; }
+            if (src[s] == T_S && o->cold && !o->warm) {
+                if (!fetched[j]) fetched[j] = malloc((need + 1) * 8);
+                fetched[j][n_fetched[j]++] = i;
+            }
             st->served[t]++;
             if (sub) st->subst[t]++;
             else if (t != T_S) st->req_hits[t]++;
@@ -656,12 +674,17 @@ int oracle_ods_round(void *h, const uint32_t *jobs, uint32_t n_jobs, const uint3
         }
         /* refill (R-O8, R-O21): deficit_t = cap_t - |t| after eviction for the
          * tracked tiers; k = min(sum of deficits, |pool_S| at round start) ranks
-         * rho(0..k-1) of one keyed stream, assigned tier by tier A -> D -> E */
+         * rho(0..k-1) of one keyed stream, assigned tier by tier A -> D -> E.
+         * Cold start (R-O24): until every tier has been full once, every tier's
+         * deficit is filled instead from this round's storage fetches -- in
+         * ascending job order, slot order, first occurrence, only ids that were
+         * storage-resident at round start. */
+        const int admit = o->cold && !o->warm;
         uint64_t deficit[4] = {0, 0, 0, 0};
         const uint64_t caps[4] = {0, o->cap_e, o->cap_d, o->cap_a};
         const uint64_t *bms[4] = {NULL, o->bm_e, o->bm_d, o->bm_a};
         for (int t = T_E; t <= T_A; ++t) {
-            if (!tracked(o, t)) continue;
+            if (!tracked(o, t) && !admit) continue;
             uint64_t size = 0;
             for (uint64_t w = 0; w < o->W; ++w) size += (uint64_t)__builtin_popcountll(bms[t][w]);
             deficit[t] = caps[t] - (size - ne_t[t]);
@@ -670,7 +693,21 @@ int oracle_ods_round(void *h, const uint32_t *jobs, uint32_t n_jobs, const uint3
         uint64_t want = deficit[T_A] + deficit[T_D] + deficit[T_E];
         uint64_t k = want < PS ? want : PS;
         uint64_t *fill = NULL;
-        if (k) {
+        if (admit) {
+            uint64_t total = 0;
+            for (uint32_t j = 0; j < o->J; ++j) total += n_fetched[j];
+            fill = malloc((total + 1) * 8);
+            uint64_t nf = 0;
+            for (uint32_t j = 0; j < o->J; ++j)
+                for (uint64_t u = 0; u < n_fetched[j]; ++u) {
+                    uint64_t i = fetched[j][u];
+                    if (tier_of(o, i) != T_S) continue;            /* cached at round start */
+                    int dup = 0;
+                    for (uint64_t v = 0; v < nf && !dup; ++v) dup = fill[v] == i;
+                    if (!dup && nf < want) fill[nf++] = i;
+                }
+            k = nf;
+        } else if (k) {
             uint64_t K = oracle_key(o->seed, PUR_REFILL, 0, o->r, 0);
             uint64_t *ranks = malloc(k * 8);
             fill = malloc(k * 8);
@@ -693,12 +730,22 @@ int oracle_ods_round(void *h, const uint32_t *jobs, uint32_t n_jobs, const uint3
                 for (; u < end; ++u) bit_set(bm, fill[u]);
             }
         }
+        if (admit) {                                            /* warm once every tier is full */
+            uint64_t size[4] = {0, 0, 0, 0};
+            for (uint64_t w = 0; w < o->W; ++w) {
+                size[T_E] += (uint64_t)__builtin_popcountll(o->bm_e[w]);
+                size[T_D] += (uint64_t)__builtin_popcountll(o->bm_d[w]);
+                size[T_A] += (uint64_t)__builtin_popcountll(o->bm_a[w]);
+            }
+            if (size[T_E] == o->cap_e && size[T_D] == o->cap_d && size[T_A] == o->cap_a) o->warm = 1;
+        }
         o->evicted_total += ne;
         o->refilled_total += k;
         free(cand); free(evict); free(fill);
     }
     o->r += 1;
     free(a_served);
+    for (uint32_t j = 0; j < 32; ++j) free(fetched[j]);
     return O_OK;
 }
 

@@ -494,3 +494,51 @@ def test_arrivals_makespan_trace():
     gap = [0, 3 * per_job, 3 * per_job, 3 * per_job]          # idle rounds between the jobs
     o3 = O.ODS(N, cfg["batch"], cfg["target"], 0, 0, 400, 8, arrival=gap)
     assert o3.replay_epochs(2) == 4 * per_job
+
+
+# ------------------------------------------------------------ cold start (NEXT-2, R-O24)
+@pytest.mark.parametrize("block", range(4))
+def test_cold_start_cross_check_with_literal_transcription(block):
+    st = synth.Stream(15000 + block)
+    for _ in range(50):
+        cfg = synth.random_tiny_ods(st)
+        for evict_all, baseline in ((False, False), (True, False), (False, True)):
+            o = O.ODS(cfg["n_total"], cfg["batch"], cfg["target"], cfg["cap_e"], cfg["cap_d"], cfg["cap_a"],
+                      cfg["seed"], transcript=True, evict_all=evict_all, baseline=baseline, cold=True)
+            o.replay_epochs(max(cfg["target"]))
+            lit = L.LiteralODS(cfg["n_total"], cfg["batch"], cfg["target"], cfg["cap_e"], cfg["cap_d"],
+                               cfg["cap_a"], cfg["seed"], evict_all=evict_all, baseline=baseline, cold=True)
+            lit.replay_all()
+            tr = o.transcript()
+            for j in range(len(cfg["batch"])):
+                for e in range(cfg["target"][j]):
+                    got = [(int(x) & 0xFFFFFFFF, int(x) >> 32) for x in tr[j, e]]
+                    assert got == lit.deliveries[j][e], cfg
+            assert list(o.state()[0]) == lit.tier
+            assert o.stats()[1:] == (lit.evicted, lit.refilled)
+
+
+def test_cold_start_first_vs_stable_epoch():
+    """SPEC cold start: the first epoch starts from an empty cache
+    and fills it with what it fetches, so it hits less than the stable epochs;
+    with one job and no churn (baseline sampler, static once full) the first
+    batch is all storage and the cache is full after cap / B rounds."""
+    cfg = dict(n_total=2000, batch=[50], target=[3], cap_e=300, cap_d=200, cap_a=0, seed=5)
+    o = O.ODS(2000, [50], [3], 300, 200, 0, 5, transcript=True, baseline=True, cold=True)
+    o.replay_epochs(3)
+    st, ev, rf = o.stats()
+    tr = o.transcript()
+    first = (tr[0, 0, :50] >> np.uint64(32)) & np.uint64(7)
+    assert np.all(first == S)                                  # nothing cached in the first round
+    assert rf == 500 and ev == 0                               # 300 + 200 admissions, then static
+    hits = st[0, :]["served"][:, 1:].sum(axis=1)
+    assert hits[0] < hits[1] and hits[1] == hits[2] == 500     # stable epochs hit exactly the cache
+    t, _, _ = o.state()
+    assert (t == E).sum() == 300 and (t == D).sum() == 200
+    # the same with ODS (A churn after warm-up): first epoch below the stable ones
+    o2 = O.ODS(2000, [50] * 3, [3] * 3, 0, 0, 400, 6, cold=True)
+    o2.replay_epochs(3)
+    s2 = o2.stats()[0]
+    for j in range(3):
+        h = s2[j, :]["served"][:, 1:].sum(axis=1)
+        assert h[0] < h[1] and h[0] < h[2]
