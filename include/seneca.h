@@ -185,6 +185,14 @@ typedef struct {
                                       the active set; a round with no active job while arrivals
                                       are pending is idle.  next_batch on a job that has not
                                       arrived is ESTATE                                        */
+    uint32_t        cold_start;    /* 0: warm start (R-O9); 1: every tier starts empty and, until
+                                      all three have been full once, each round's storage fetches
+                                      (ascending job, slot order, first occurrence, storage-
+                                      resident at round start) are admitted at the round end
+                                      A -> D -> E up to each tier's capacity instead of random
+                                      refills (DESIGN.md R-O24); refills and
+                                      admissions are both counted in d_refilled               */
+    uint32_t        _pad1;
 } seneca_cache_config;
 
 /* Per job-epoch counters (R-O10; digest in DESIGN.md §3).  104 bytes.       */

@@ -61,12 +61,12 @@ class ODSContext:
     Readback methods take the replica index (default 0)."""
 
     def __init__(self, n_total, batch, target, cap_e, cap_d, cap_a, seed, request_mode=0,
-                 device="cuda", stream=None, replicas=1, evict_tiers=0, sampler=0, arrival=None):
+                 device="cuda", stream=None, replicas=1, evict_tiers=0, sampler=0, arrival=None, cold_start=0):
         torch = _torch()
         self.torch = torch
         self.cfg = seneca.make_config(int(n_total), list(batch), list(target), int(cap_e), int(cap_d),
                                       int(cap_a), int(seed), request_mode, int(replicas), int(evict_tiers),
-                                      int(sampler), arrival)
+                                      int(sampler), arrival, int(cold_start))
         self.R = int(replicas)
         self.N, self.J = int(n_total), len(batch)
         self.bmax = max(batch)

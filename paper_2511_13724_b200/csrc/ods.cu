@@ -79,6 +79,7 @@ struct Cfg {
     uint32_t evict_all;              // evict_tiers = ALL (R-O21): every cached tier is tracked
     uint32_t cap_t;                  // capacity of the tracked tiers (cap_a, or cap_a + cap_d + cap_e; 0 baseline)
     uint32_t baseline;               // the uniform no-evict sampler (R-O22): no substitution, static tiers
+    uint32_t cold;                   // cold start (R-O24): empty tiers, round-end admission until full
     uint32_t Nrow;                   // row stride of the permutation / lap lists (N rounded up to 64)
     uint32_t FL;                     // capacity of one refill buffer
     uint64_t seed;
@@ -107,6 +108,10 @@ struct Lay {
     uint32_t *fill_list;             // [2][FL], FL = max(cap_t,1) + J*Bmax; buffer = round parity
     uint32_t *ev_ed;                 // [2][max(cap_e+cap_d,1)] evicted E/D ids (bit 31: E) per parity
     uint32_t *ev_ed_n;               // [2]
+    uint32_t *fetch;                 // [J][Bmax] storage fetches of the round (cold start, R-O24)
+    uint32_t *fetch_n;               // [J]
+    uint32_t *warm;                  // [1] every tier has been full once (cold start ends)
+    uint32_t *claim;                 // [NW] admission de-duplication scratch (all zero between rounds)
     seneca_job_epoch_stats *stats;   // [J][maxT]
     unsigned long long *evicted, *refilled;
     uint32_t *err;
@@ -286,6 +291,7 @@ struct JobSmem {
     float dens;           // unseen fraction observed by the last walk step (window sizing)
     uint32_t npush;       // evictions pushed by this job this round
     uint32_t rep;         // replica of this CTA
+    uint32_t warm;        // cold start over (read at the round start, R-O24)
     // prefetch of the next walk window (R-O1 walk, see job_walk_prefetched)
     uint32_t pf_state;    // 0 none, 1 list window requested, 2 seen chunks requested
     uint32_t pf_buf, pf_epoch, pf_base, pf_len, pf_vlen;
@@ -625,14 +631,18 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
     __syncthreads();
     if (P.mode == 0 && S.pf_state == 1) prefetch_seen(L, C, S, s_win, s_wseen, j);   // next walk, stage 2
     TM.tick(2);
-    // remaining misses are fetched from storage (R-O18)
+    // remaining misses are fetched from storage (R-O18); during a cold start they
+    // are also listed, in slot order, for the round-end admission (R-O24)
+    const bool record = C.cold && !S.warm;
     for (uint32_t u = q + tid; u < S.m; u += T) {
         const uint32_t s = s_miss[u], i = s_req[s];
         if (P.out_ids) { P.out_ids[row + s] = i; P.out_src[row + s] = (uint8_t)T_S; }
         s_oid[s] = i;
         s_osrc[s] = (uint8_t)T_S;
         atomicOr(seen_j + (i >> 5), 1u << (i & 31));
+        if (record) L.fetch[(size_t)j * C.Bmax + (u - q)] = i;
     }
+    if (record && tid == 0) L.fetch_n[j] = S.m - q;
     // deferred (replaced) misses are requested again on the next lap (R-O1):
     // before a wrap -> the end of the (new) current list, after -> the next list
     uint32_t q1 = 0;
@@ -714,6 +724,8 @@ struct MaintSmem {
     uint32_t def[4];         // round-start deficits cap_t - |t| of the tracked tiers
     uint32_t ne_t[4];        // evictions of this round by tier
     uint32_t ned;            // E/D evictions listed for the job CTAs
+    uint32_t warm;           // cold start over (R-O24)
+    uint32_t nadm;           // admission candidates of this round
     uint32_t ne_push, push_base;
     uint32_t add[kMaxJobs];
     uint32_t scan[33];
@@ -737,15 +749,49 @@ __device__ void maint_refill_select(const Lay& L, const Cfg& C, MaintSmem& M, co
 // as of round start, tier by tier A -> D -> E from one keyed rank stream (R-O8,
 // R-O21), counts kept exact.
 __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSmem& M, uint32_t* s_pre,
-                            uint32_t* s_supS, uint64_t r, uint32_t active, bool full_scan, bool speculated,
-                            uint32_t ne_push, uint32_t push_base, PhaseTimer& TM) {
+                            uint32_t* s_supS, uint64_t r, uint32_t active, uint32_t part_of_round, bool full_scan,
+                            bool speculated, uint32_t ne_push, uint32_t push_base, PhaseTimer& TM) {
     const uint32_t tid = threadIdx.x, T = blockDim.x;
     if (tid == 0) {
         M.ne = full_scan ? 0u : ne_push;
         M.ne_t[0] = M.ne_t[1] = M.ne_t[2] = M.ne_t[3] = 0;
         M.ned = 0;
+        M.nadm = 0;
     }
     __syncthreads();
+    const bool admit = C.cold && !M.warm;
+    uint32_t* fill_w = L.fill_list + (size_t)(r & 1) * C.FL;
+    if (admit && active) {
+        // cold start (R-O24): the storage fetches of the jobs of this round, in
+        // ascending job order and slot order, first occurrence only, that were
+        // storage-resident at round start (tiers read before any eviction applies)
+        for (uint32_t m = part_of_round; m; m &= m - 1) {
+            const uint32_t jj = __ffs(m) - 1;
+            const uint32_t n = ldcg(L.fetch_n + jj);
+            for (uint32_t base = 0; base < n; base += T) {
+                const uint32_t u = base + tid;
+                uint32_t i = 0;
+                bool ok = false;
+                if (u < n) {
+                    i = ldcg(L.fetch + (size_t)jj * C.Bmax + u);
+                    const uint32_t w = i >> 5, b = 1u << (i & 31);
+                    const bool cached = ((ldcg(L.bm_a + w) | ldcg(L.bm_d + w) | ldcg(L.bm_e + w)) & b) != 0;
+                    ok = !cached && !(atomicOr(L.claim + w, b) & b);     // ids within one job are distinct
+                }
+                uint32_t tot;
+                const uint32_t ex = block_exclusive_scan(ok ? 1u : 0u, &tot, M.scan);
+                if (ok) fill_w[M.nadm + ex] = i;
+                __syncthreads();
+                if (tid == 0) M.nadm += tot;
+                __syncthreads();
+            }
+        }
+        for (uint32_t u = tid; u < M.nadm; u += T) {                 // the scratch is zero between rounds
+            const uint32_t i = fill_w[u];
+            atomicAnd(L.claim + (i >> 5), ~(1u << (i & 31)));
+        }
+        __syncthreads();
+    }
     if (full_scan) {
         // the active set changed (R-O6): every tracked entry is a candidate; the
         // consumer counts of the survivors are rebuilt for the new active set
@@ -772,8 +818,10 @@ __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSm
     }
     TM.tick(3);
     const uint32_t ne = M.ne;
-    const uint32_t k = active ? min(M.deficit0 + ne, M.PS) : 0u;   // no refill with no active job
-    if (!speculated) {
+    uint32_t k = active ? min(M.deficit0 + ne, M.PS) : 0u;         // no refill with no active job
+    if (admit) {
+        k = active ? min(M.deficit0 + ne, M.nadm) : 0u;           // admissions instead of refills (R-O24)
+    } else if (!speculated) {
         if (k) prefix_from_smem(C, s_supS, s_pre, M.scan);
         maint_refill_select(L, C, M, s_pre, r, 0, k);
     } else if (k > M.kspec) {
@@ -818,6 +866,10 @@ __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSm
         M.size[T_A] += kA - M.ne_t[T_A];
         M.size[T_D] += kD - M.ne_t[T_D];
         M.size[T_E] += (k - kA - kD) - M.ne_t[T_E];
+        if (admit && M.size[T_A] == C.cap_a && M.size[T_D] == C.cap_d && M.size[T_E] == C.cap_e) {
+            M.warm = 1;                                           // every tier full: the cold start ends
+            *L.warm = 1;
+        }
         *L.evicted += ne;
         *L.refilled += k;
         M.prev_k = k;
@@ -906,7 +958,7 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
     // with no tracked tier (cap_A = 0 and evict_tiers = A) there is no cross-job
     // interaction at all (E and D are static, maintain has nothing to do): the job
     // CTAs run their rounds independently
-    const bool coupled = C.cap_t > 0;
+    const bool coupled = C.cap_t > 0 || C.cold;
     if (is_maint && !coupled) return;
 
     if (tid < kMaxJobs) { s_n[tid] = P.n0[tid]; s_e[tid] = P.e0[tid]; }
@@ -938,6 +990,7 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
             M.prev_k = blockDim.x;
             M.PS = ldcg(L.cnt_tot + 3 * C.J);
             for (int t = 0; t < 4; ++t) M.size[t] = ldcg(L.tsize + t);
+            M.warm = C.cold ? ldcg(L.warm) : 1u;
         }
         for (uint32_t k = tid; k < C.NS; k += blockDim.x) s_sup[k] = ldcg(L.cnt_sup + (size_t)3 * C.J * C.NS + k);
     }
@@ -986,13 +1039,14 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
         auto set_deficits = [&]() {
             M.def[T_S] = 0;
             M.def[T_A] = C.cap_a - M.size[T_A];
-            M.def[T_D] = C.evict_all ? C.cap_d - M.size[T_D] : 0u;
-            M.def[T_E] = C.evict_all ? C.cap_e - M.size[T_E] : 0u;
+            const bool all = C.evict_all || (C.cold && !M.warm);        // cold start fills every tier
+            M.def[T_D] = all ? C.cap_d - M.size[T_D] : 0u;
+            M.def[T_E] = all ? C.cap_e - M.size[T_E] : 0u;
             M.deficit0 = M.def[T_A] + M.def[T_D] + M.def[T_E];
         };
         auto speculate = [&](uint64_t r, uint32_t part, uint32_t departing) -> bool {
             const uint32_t active_after = s_active & ~departing;
-            if (!(active_after && C.cap_t > 0) || departing) return false;
+            if (!(active_after && C.cap_t > 0) || departing || (C.cold && !M.warm)) return false;
             if (tid == 0) set_deficits();
             if (tid == 0) {
                 uint32_t cand = 0;
@@ -1031,10 +1085,15 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
             // a departure rebuilds the consumer counts for the remaining jobs even when
             // none remains but arrivals are pending (no eviction, no refill then): a
             // job arriving later must not inherit counts of departed consumers (R-O23)
-            if ((active_after || (departing && s_pending)) && C.cap_t > 0) {
+            if ((active_after || (departing && s_pending)) && (C.cap_t > 0 || (C.cold && !M.warm))) {
                 if (!spec && tid == 0) set_deficits();
                 __syncthreads();
-                maint_apply(L, C, P, M, s_pre, s_sup, r, active_after, departing != 0, spec, M.ne_push, M.push_base, TM);
+                maint_apply(L, C, P, M, s_pre, s_sup, r, active_after, part, departing != 0, spec, M.ne_push,
+                            M.push_base, TM);
+            } else if (tid == 0) {          // nothing maintained: the job CTAs take an empty round
+                uint32_t* fn = L.fill_n + (r & 1) * 4;
+                fn[0] = fn[1] = fn[2] = 0;
+                L.ev_ed_n[r & 1] = 0;
             }
             __syncthreads();
             if (tid == 0) { __threadfence(); atomicExch(L.bar + 2, rr + 1); }     // release round r's tiers
@@ -1072,6 +1131,7 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
                 __syncthreads();
             }
             TM.tick(4);
+            if (C.cold && tid == 0) S.warm = ldcg(L.warm);        // stable until this round's maintain
             if ((part >> j) & 1u) {
                 if (S.recount) { job_recount(L, C, j, s_sup, S.tot); if (tid == 0) S.recount = 0; __syncthreads(); }
                 else if (coupled && rr > 0) { job_take_refills(L, C, S, j, r - 1, s_sup); __syncthreads(); }
@@ -1183,14 +1243,15 @@ __global__ void ods_init_tiers(const __grid_constant__ Lays LS, const __grid_con
     const Lay& L = LS.r[blockIdx.y];
     const uint64_t key = derive_key(L.seed, PUR_INIT, 0, 0, 0);
     const PermDomain dom = perm_domain(C.N);
-    const uint32_t total = C.cap_a + cap_d + cap_e;
+    const uint32_t total = C.cold ? 0u : C.cap_a + cap_d + cap_e;    // cold start: empty tiers (R-O24)
     for (uint32_t pos = blockIdx.x * blockDim.x + threadIdx.x; pos < total; pos += gridDim.x * blockDim.x) {
         const uint32_t i = perm_apply(key, dom, pos);
         uint32_t* bm = pos < C.cap_a ? L.bm_a : (pos < C.cap_a + cap_d ? L.bm_d : L.bm_e);
         atomicOr(bm + (i >> 5), 1u << (i & 31));
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        L.tsize[T_S] = 0; L.tsize[T_E] = cap_e; L.tsize[T_D] = cap_d; L.tsize[T_A] = C.cap_a;
+        L.tsize[T_S] = 0;
+        L.tsize[T_E] = C.cold ? 0u : cap_e; L.tsize[T_D] = C.cold ? 0u : cap_d; L.tsize[T_A] = C.cold ? 0u : C.cap_a;
     }
 }
 
@@ -1339,6 +1400,7 @@ seneca_status check_cfg(const seneca_cache_config* cfg) {
     if (cfg->replicas > kMaxReplicas) { set_error("replicas must be <= %u", kMaxReplicas); return SENECA_EINVAL; }
     if (cfg->evict_tiers > 1) { set_error("evict_tiers must be 0 (A only) or 1 (all)"); return SENECA_EINVAL; }
     if (cfg->sampler > 1) { set_error("sampler must be 0 (ODS) or 1 (uniform no-evict baseline)"); return SENECA_EINVAL; }
+    if (cfg->cold_start > 1) { set_error("cold_start must be 0 or 1"); return SENECA_EINVAL; }
     if (cfg->replicas > 1 && cfg->request_mode != 0) {
         set_error("caller-supplied requests (request_mode 1) need replicas <= 1"); return SENECA_EINVAL;
     }
@@ -1378,6 +1440,7 @@ Sizes compute_sizes(const seneca_cache_config* cfg) {
     C.cap_e = (uint32_t)cfg->cap_e;
     C.evict_all = cfg->evict_tiers;
     C.baseline = cfg->sampler;
+    C.cold = cfg->cold_start ? 1u : 0u;
     C.cap_t = C.baseline ? 0u : (C.evict_all ? C.cap_a + C.cap_d + C.cap_e : C.cap_a);
     C.seed = cfg->seed;
     C.Nrow = (C.N + 63) & ~63u;
@@ -1401,6 +1464,8 @@ Sizes compute_sizes(const seneca_cache_config* cfg) {
         (size_t)C.J * C.maxT * sizeof(seneca_job_epoch_stats),  // 21 stats
         8, 8, 4, 16, 256,                                   // 22-26 evicted, refilled, err, bar, phase
         C.evict_all ? 2 * edl : 4, 8,                       // 27-28 ev_ed, ev_ed_n
+        C.cold ? (size_t)C.J * C.Bmax * 4 : 4, (size_t)C.J * 4,   // 29-30 fetch, fetch_n
+        4, C.cold ? W : 4,                                  // 31-32 warm, claim
     };
     size_t at = 0;
     for (size_t k = 0; k < sizeof(sz) / sizeof(sz[0]); ++k) {
@@ -1444,6 +1509,10 @@ Lay carve(const Sizes& z, char* base, uint64_t seed) {
     L.phase = (unsigned long long*)(base + z.off[26]);
     L.ev_ed = (uint32_t*)(base + z.off[27]);
     L.ev_ed_n = (uint32_t*)(base + z.off[28]);
+    L.fetch = (uint32_t*)(base + z.off[29]);
+    L.fetch_n = (uint32_t*)(base + z.off[30]);
+    L.warm = (uint32_t*)(base + z.off[31]);
+    L.claim = (uint32_t*)(base + z.off[32]);
     return L;
 }
 

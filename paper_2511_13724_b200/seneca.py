@@ -59,7 +59,7 @@ class CacheConfig(C.Structure):
         ("batch_size", C.POINTER(C.c_uint32)), ("target_epochs", C.POINTER(C.c_uint32)),
         ("cap_e", C.c_uint64), ("cap_d", C.c_uint64), ("cap_a", C.c_uint64), ("seed", C.c_uint64),
         ("replicas", C.c_uint32), ("evict_tiers", C.c_uint32), ("sampler", C.c_uint32), ("_pad0", C.c_uint32),
-        ("arrival_round", C.POINTER(C.c_uint32)),
+        ("arrival_round", C.POINTER(C.c_uint32)), ("cold_start", C.c_uint32), ("_pad1", C.c_uint32),
     ]
 
 
@@ -216,14 +216,15 @@ def profiles_from_columns(cols: dict) -> np.ndarray:
 
 # ------------------------------------------------------------------ ODS
 def make_config(n_total, batch, target, cap_e, cap_d, cap_a, seed, request_mode=0, replicas=1, evict_tiers=0,
-                sampler=0, arrival=None):
+                sampler=0, arrival=None, cold_start=0):
     b = (C.c_uint32 * len(batch))(*batch)
     t = (C.c_uint32 * len(target))(*target)
     arr = (C.c_uint32 * len(batch))(*arrival) if arrival is not None else None
     cfg = CacheConfig(n_total=n_total, n_jobs=len(batch), request_mode=request_mode,
                       batch_size=b, target_epochs=t, cap_e=cap_e, cap_d=cap_d, cap_a=cap_a, seed=seed,
                       replicas=replicas, evict_tiers=evict_tiers, sampler=sampler,
-                      arrival_round=C.cast(arr, C.POINTER(C.c_uint32)) if arr is not None else None)
+                      arrival_round=C.cast(arr, C.POINTER(C.c_uint32)) if arr is not None else None,
+                      cold_start=cold_start)
     cfg._keep = (b, t, arr)
     return cfg
 

@@ -499,3 +499,62 @@ def test_arrivals_next_batch():
             assert np.array_equal(ids_g[x, :L_].cpu().numpy().view(np.uint32), ids_o[x, :L_])
             assert np.array_equal(src_g[x, :L_].cpu().numpy(), src_o[x, :L_])
     compare_state(o, g)
+
+
+# ---------------------------------------------------------------- cold start (R-O24)
+def test_cold_start_random_tiny_configs():
+    st = synth.Stream(16000)
+    for _ in range(50):
+        c = synth.random_tiny_ods(st)
+        for evict_all, baseline in ((False, False), (True, False), (False, True)):
+            o = O.ODS(c["n_total"], c["batch"], c["target"], c["cap_e"], c["cap_d"], c["cap_a"], c["seed"],
+                      transcript=True, evict_all=evict_all, baseline=baseline, cold=True)
+            g = P.ODSContext(c["n_total"], c["batch"], c["target"], c["cap_e"], c["cap_d"], c["cap_a"], c["seed"],
+                             evict_tiers=int(evict_all), sampler=int(baseline), cold_start=1)
+            tr = g.new_transcript()
+            assert g.replay_epochs(max(c["target"]), tr) == o.replay_epochs(max(c["target"]))
+            torch.cuda.synchronize()
+            compare_state(o, g, tr)
+
+
+@pytest.mark.parametrize("name,evict_all", [("toy", False), ("imagenet1k", False), ("imagenet1k", True),
+                                            ("openimages", False)])
+def test_cold_start_scaled_configs(name, evict_all):
+    scale = 1 if name == "toy" else 64
+    c = synth.ods_config(name, scale=scale, seed=12)
+    ce, cd, ca = caps_of(c)
+    o = O.ODS(c["n_total"], c["batch"], c["target"], ce, cd, ca, 12, transcript=True, evict_all=evict_all,
+              cold=True)
+    g = P.ODSContext(c["n_total"], c["batch"], c["target"], ce, cd, ca, 12, evict_tiers=int(evict_all),
+                     cold_start=1, replicas=2)
+    tr = g.new_transcript()
+    assert g.replay_epochs(max(c["target"]), tr) == o.replay_epochs(max(c["target"]))
+    torch.cuda.synchronize()
+    compare_replica(o, g, 0, tr[0])
+    o1 = O.ODS(c["n_total"], c["batch"], c["target"], ce, cd, ca, 13, transcript=True, evict_all=evict_all,
+               cold=True)
+    o1.replay_epochs(max(c["target"]))
+    compare_replica(o1, g, 1, tr[1])
+
+
+def test_cold_start_next_batch_and_arrivals():
+    n, batch, target, arr = 600, [16, 40, 9], [2, 1, 2], [0, 5, 20]
+    o = O.ODS(n, batch, target, 60, 50, 40, 7, cold=True, arrival=arr)
+    g = P.ODSContext(n, batch, target, 60, 50, 40, 7, cold_start=1, arrival=arr)
+    st = synth.Stream(8)
+    for _ in range(200):
+        _, e, _, _ = o.job_state()
+        if all(int(e[j]) >= target[j] for j in range(3)):
+            break
+        live = [j for j in range(3) if arr[j] <= o.r and int(e[j]) < target[j]]
+        if not live:
+            assert o.replay_rounds(1) == 1 and g.replay_rounds(1) == 1
+            continue
+        pick = [j for j in live if st.uniform(1)[0] < 0.7] or live[-1:]
+        rc, ids_o, src_o, lens_o = o.round(pick)
+        ids_g, src_g, lens_g = g.next_batch(pick)
+        torch.cuda.synchronize()
+        for x, L_ in enumerate(lens_g):
+            assert np.array_equal(ids_g[x, :L_].cpu().numpy().view(np.uint32), ids_o[x, :L_])
+            assert np.array_equal(src_g[x, :L_].cpu().numpy(), src_o[x, :L_])
+    compare_state(o, g)
