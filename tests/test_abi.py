@@ -151,3 +151,16 @@ def test_epoch_model_host_checks(lib):
         assert ei.value.status == S.EINVAL
     with pytest.raises(S.SenecaError):
         S.epoch_model(1, 0, 10, (1.0,) * 4, 1, stream=0)
+
+
+def test_mode_fields_validated(lib):
+    c = synth.ods_config("toy")
+    caps = S.split_capacities(c["n_total"], c["s_data"], c["m_num"], c["m_den"], c["cache_bytes"], *c["split"])
+    args = (c["n_total"], c["batch"], c["target"], caps[0], caps[1], caps[2], 1)
+    base = S.state_bytes(S.make_config(*args))
+    for kw in (dict(evict_tiers=1), dict(sampler=1), dict(cold_start=1), dict(arrival=[0, 7])):
+        assert S.state_bytes(S.make_config(*args, **kw)) >= base       # valid modes
+    for kw in (dict(evict_tiers=2), dict(sampler=2), dict(cold_start=2)):
+        with pytest.raises(S.SenecaError) as ei:
+            S.state_bytes(S.make_config(*args, **kw))
+        assert ei.value.status == S.EINVAL
