@@ -1,0 +1,49 @@
+"""The bench.py contract on CPU: the reference arm (the oracle) prints one JSON
+line with the keys the driver reads; the GPU arm's keys are checked by the GPU
+pass (profiles/r1/bench_*.json)."""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_reference_arm_json_line():
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--workload", "toy",
+                          "--steps", "1", "--warmup", "1"], capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "impl", "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is True
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+    assert d["config"]["workload"].startswith("toy")
+
+
+def test_committed_bench_lines_have_the_contract_keys():
+    import glob
+    import re
+    readme = open(os.path.join(ROOT, "profiles", "r1", "README.md")).read()
+    tag = re.search(r"Current pass: \*\*(r1[a-z])\*\*", readme).group(1)      # the pass the README names
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r1", f"bench_*_{tag}.json"))) + \
+        [os.path.join(ROOT, "profiles", "r1", f"bench_{tag}.json")]
+    files = [f for f in files if os.path.exists(f) and "reference" not in f]
+    assert files
+    for f in files:
+        d = json.loads(open(f).read().strip().splitlines()[-1])
+        for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                  "scaling", "vs_baseline", "dtype", "data", "config", "e2e", "roofline", "clocks", "gpu_launches"):
+            assert k in d, (f, k)
+        r = d["roofline"]
+        for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+            assert k in r, (f, k)
+        assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+        assert d["steps"] >= 1 and d["warmup"] >= 3 and d["gpu_launches"] > 0
+        assert d["parity"]["ods_vs_oracle_golden"] == "bit-exact"
+        assert d["parity"]["mdp_vs_oracle_first_200_profiles"] == "bit-exact"
+        assert not set(d["clocks"]["reasons"]) & {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
