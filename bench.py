@@ -234,6 +234,33 @@ def algorithmic_bytes(name, info):
 NCU_TRAFFIC = os.path.join(ROOT, "profiles", "r1", "ncu_traffic.json")
 
 
+def pass_equivalent(c, caps, words, ods_s, steps, world, hbm_peak, replicas=None):
+    """SURVEY §8(d) "How the targets are measured", item 1: the logical bytes a
+    full-pass design moves for this replay -- per job-round one pass over seen_j,
+    every non-empty tier bitmap and (with A) cons_j, i.e. (1 + #tiers + [A]) N/8 B
+    (SURVEY §8(a) row a4); per round with A one storage-pool pass over the three
+    residency bitmaps (3 N/8 B); per job-epoch one seen reset (N/8 B, row a8) --
+    divided by the replay's measured time.  ods_rounds maintains the pool counts
+    incrementally and moves far fewer bytes; this is the rate a
+    pass-based replay would have to sustain to match it, as a fraction of peak."""
+    W = words * 4
+    ce, cd, ca = caps[0], caps[1], caps[2]
+    tiers = (ce > 0) + (cd > 0) + (ca > 0)
+    per_job_round = (1 + tiers + (1 if ca > 0 else 0)) * W
+    job_rounds = sum(t * -(-c["n_total"] // b) for t, b in zip(c["target"], c["batch"]))
+    rounds = max(t * -(-c["n_total"] // b) for t, b in zip(c["target"], c["batch"]))
+    total = per_job_round * job_rounds + (3 * W * rounds if ca > 0 else 0) + W * sum(c["target"])
+    rate = total * steps * world / ods_s / 1e9
+    out = dict(bytes_per_replay=int(total), job_rounds=int(job_rounds), achieved=rate, peak=hbm_peak,
+               unit="GB/s", frac=rate / hbm_peak,
+               note="full-pass logical bytes (SURVEY 8(d) target 1) / measured replay time; not DRAM traffic "
+                    "(ods_rounds keeps pool counts incrementally, see roofline.traffic)")
+    if replicas is not None:
+        rr = replicas["value"] / decisions_of(c)      # replays per second, all ranks
+        out["replicas"] = dict(R=replicas["R"], achieved=total * rr / 1e9, frac=total * rr / 1e9 / hbm_peak)
+    return out
+
+
 def ncu_traffic(key):
     """DRAM bytes (read + write) of one launch, from the committed `ncu --set full`
     capture of the same launch (tools/measure.sh -> tools/ncu_summary.py), or None."""
@@ -561,6 +588,7 @@ def main():
                      note="public API from Python: init_cache + replay_epochs + stats D2H; MDP profiles "
                           "H2D from pinned memory + sweep + results D2H; host wall clock"),
             roofline=roof,
+            pass_equivalent=pass_equivalent(c, caps, v.words, ods_s, args.steps, world, hbm_peak, rep_line),
             mdp=dict(value=total_evals / mdp_s, unit="split-evals/s", dtype="f64", ms_per_step=mdp_ms_step,
                      roofline=mdp_roof),
             replicas=rep_line,

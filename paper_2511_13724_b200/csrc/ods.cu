@@ -196,9 +196,24 @@ __device__ void prefix_from_smem(const Cfg& C, const uint32_t* s_sup_pool, uint3
     __syncthreads();
 }
 
+// Position of the r-th (0-based) set bit of x, r < popc(x): a branch-free
+// halving search on popcounts (5 steps, no data-dependent loop).
+__device__ __forceinline__ uint32_t select_bit(uint32_t x, uint32_t r) {
+    uint32_t pos = 0, c;
+    c = __popc(x & 0xffffu); if (r >= c) { r -= c; x >>= 16; pos += 16; }
+    c = __popc(x & 0xffu);   if (r >= c) { r -= c; x >>= 8;  pos += 8; }
+    c = __popc(x & 0xfu);    if (r >= c) { r -= c; x >>= 4;  pos += 4; }
+    c = __popc(x & 0x3u);    if (r >= c) { r -= c; x >>= 2;  pos += 2; }
+    c = x & 1u;              if (r >= c) { pos += 1; }
+    return pos;
+}
+
 // The rank-th (0-based) member, in ascending id order, of pool (t, j):
 // superblock by binary search in shared memory, then the superblock's 32-B
 // row of block counts (two 16-B loads), then one 16-B vector of each bitmap.
+// The row is scanned word-wise: each word's four byte counts (<= 128 each) are
+// summed in two 16-bit lanes, a running sum over the 8 words picks the word,
+// then at most 3 byte steps pick the block -- a 12-step chain instead of 32.
 __device__ uint32_t pool_select(const Lay& L, const Cfg& C, uint32_t pidx, uint32_t t, uint32_t j,
                                 const uint32_t* s_pre, uint32_t rank) {
     uint32_t lo = 0, hi = C.NS - 1;
@@ -210,20 +225,24 @@ __device__ uint32_t pool_select(const Lay& L, const Cfg& C, uint32_t pidx, uint3
     const uint32_t* crow = L.cnt8 + (size_t)pidx * (C.NBp >> 2) + (size_t)lo * 8u;
     const uint4 c0 = ldcg4(crow), c1 = ldcg4(crow + 4);
     const uint32_t cw[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-    uint32_t k_found = 0;
-    bool found = false;
+    uint32_t run = 0, before = 0, qsel = 0, wsel = cw[0];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const uint32_t c = (cw[q] >> (8 * k)) & 0xffu;
-            if (!found) {
-                if (r < c) { found = true; k_found = q * 4 + k; }
-                else r -= c;
-            }
+        const uint32_t x = (cw[q] & 0x00ff00ffu) + ((cw[q] >> 8) & 0x00ff00ffu);
+        run += (x & 0xffffu) + (x >> 16);
+        if (q < 7 && run <= r) { before = run; qsel = q + 1; wsel = cw[q < 7 ? q + 1 : 7]; }
+    }
+    if (run <= r) { atomicOr(L.err, 1u); return 0; }   // counts inconsistent with the bitmaps
+    r -= before;
+    uint32_t k = 0, b = wsel & 0xffu;
+    if (r >= b) {
+        r -= b; k = 1; b = (wsel >> 8) & 0xffu;
+        if (r >= b) {
+            r -= b; k = 2; b = (wsel >> 16) & 0xffu;
+            if (r >= b) { r -= b; k = 3; }
         }
     }
-    const uint32_t w0 = (lo * 32u + k_found) * kWordsPerBlock;
+    const uint32_t w0 = (lo * 32u + qsel * 4u + k) * kWordsPerBlock;
     uint32_t pw[4];
     if (t == T_S) {
         const uint4 a = ldcg4(L.bm_a + w0), e = ldcg4(L.bm_e + w0), d = ldcg4(L.bm_d + w0);
@@ -233,25 +252,26 @@ __device__ uint32_t pool_select(const Lay& L, const Cfg& C, uint32_t pidx, uint3
         pw[3] = ~(a.w | e.w | d.w) & valid_mask(C, w0 + 3);
     } else {
         const uint4 sv = ldcg4(L.seen + (size_t)j * C.NW + w0);
-        const uint4 b = ldcg4((t == T_A ? L.bm_a : (t == T_D ? L.bm_d : L.bm_e)) + w0);
-        pw[0] = b.x & ~sv.x; pw[1] = b.y & ~sv.y; pw[2] = b.z & ~sv.z; pw[3] = b.w & ~sv.w;
+        const uint4 bv = ldcg4((t == T_A ? L.bm_a : (t == T_D ? L.bm_d : L.bm_e)) + w0);
+        pw[0] = bv.x & ~sv.x; pw[1] = bv.y & ~sv.y; pw[2] = bv.z & ~sv.z; pw[3] = bv.w & ~sv.w;
         if (t == T_A) {
             const uint4 cv = ldcg4(L.cons + (size_t)j * C.NW + w0);
             pw[0] &= ~cv.x; pw[1] &= ~cv.y; pw[2] &= ~cv.z; pw[3] &= ~cv.w;
         }
     }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const uint32_t pc = __popc(pw[k]);
-        if (r < pc) {
-            uint32_t x = pw[k];
-            for (uint32_t s2 = 0; s2 < r; ++s2) x &= x - 1u;
-            return (w0 + k) * 32u + (uint32_t)(__ffs(x) - 1);
+    uint32_t ksel = 0, xsel = pw[0];
+    {
+        const uint32_t p0 = __popc(pw[0]), p1 = __popc(pw[1]), p2 = __popc(pw[2]);
+        if (r >= p0) {
+            r -= p0; ksel = 1; xsel = pw[1];
+            if (r >= p1) {
+                r -= p1; ksel = 2; xsel = pw[2];
+                if (r >= p2) { r -= p2; ksel = 3; xsel = pw[3]; }
+            }
         }
-        r -= pc;
     }
-    atomicOr(L.err, 1u);   // counts inconsistent with the bitmaps
-    return 0;
+    if (r >= (uint32_t)__popc(xsel)) { atomicOr(L.err, 1u); return 0; }   // counts inconsistent with the bitmaps
+    return (w0 + ksel) * 32u + select_bit(xsel, r);
 }
 
 // ------------------------------------------------------------------ barrier among the round CTAs
@@ -268,12 +288,15 @@ __device__ __forceinline__ unsigned long long ld_acquire64(const uint32_t* p) {
 }
 
 // ------------------------------------------------------------------ per-CTA phase timer (profiling)
+// kOn = false (the timed replays) compiles every tick out; the kernel with
+// kOn = true is launched only when seneca_profile bit 1 asks for phase counters.
+template <bool kOn>
 struct PhaseTimer {
     long long last;
     unsigned long long acc[16];
     uint32_t on;
     __device__ __forceinline__ void tick(uint32_t slot) {
-        if (on && threadIdx.x == 0) {
+        if (kOn && on && threadIdx.x == 0) {
             const long long t = clock64();
             acc[slot] += (unsigned long long)(t - last);
             last = t;
@@ -345,8 +368,9 @@ struct WalkPrefetch {
     const uint4* wseen;      // [kWinMax] prefetched 16-B seen chunks
 };
 
+template <class TMr>
 __device__ void job_walk(const Lay& L, const Cfg& C, JobSmem& S, uint32_t* s_req, uint32_t j, uint32_t e, uint32_t need,
-                         PhaseTimer& TM, const uint32_t* s_win, const WalkPrefetch* pf) {
+                         TMr& TM, const uint32_t* s_win, const WalkPrefetch* pf) {
     unsigned long long* iters = TM.on ? &TM.acc[7] : nullptr;
     const uint32_t tid = threadIdx.x, T = blockDim.x;
     const uint32_t* seen_j = L.seen + (size_t)j * C.NW;
@@ -535,9 +559,10 @@ __device__ void job_recount(const Lay& L, const Cfg& C, uint32_t j, uint32_t* s_
 }
 
 // a3-a6 for job j in round r: classify, substitute, respond.
+template <class TMr>
 __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& S, uint32_t* s_req, uint32_t* s_miss,
                           uint32_t* s_sub, uint32_t* s_oid, uint8_t* s_osrc, uint32_t* s_pre, uint32_t j, uint64_t r,
-                          uint32_t e, uint32_t nbase, uint32_t n_act, PhaseTimer& TM, const uint32_t* s_win,
+                          uint32_t e, uint32_t nbase, uint32_t n_act, TMr& TM, const uint32_t* s_win,
                           uint4* s_wseen, uint32_t* s_sup) {
     const uint32_t tid = threadIdx.x, T = blockDim.x;
     const uint32_t need = S.need;
@@ -748,9 +773,10 @@ __device__ void maint_refill_select(const Lay& L, const Cfg& C, MaintSmem& M, co
 // consumed by every active job (R-O5, R-O6, R-O21), refill from the storage pool
 // as of round start, tier by tier A -> D -> E from one keyed rank stream (R-O8,
 // R-O21), counts kept exact.
+template <class TMr>
 __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSmem& M, uint32_t* s_pre,
                             uint32_t* s_supS, uint64_t r, uint32_t active, uint32_t part_of_round, bool full_scan,
-                            bool speculated, uint32_t ne_push, uint32_t push_base, PhaseTimer& TM) {
+                            bool speculated, uint32_t ne_push, uint32_t push_base, TMr& TM) {
     const uint32_t tid = threadIdx.x, T = blockDim.x;
     if (tid == 0) {
         M.ne = full_scan ? 0u : ne_push;
@@ -920,6 +946,7 @@ __device__ void job_take_refills(const Lay& L, const Cfg& C, JobSmem& S, uint32_
 // ------------------------------------------------------------------ the persistent round kernel
 // Grid: (J + 1) CTAs per replica; replicas are independent replays (their own
 // workspace slice and seed) that share nothing but the launch.
+template <bool kTime>
 __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, const Launch& P) {
     extern __shared__ __align__(16) uint32_t smem[];
     __shared__ JobSmem S;
@@ -931,7 +958,7 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
     const Lay& L = LS.r[rep];
     const bool is_maint = cta == C.J;
     const uint32_t j = cta;
-    __shared__ PhaseTimer TM;
+    __shared__ PhaseTimer<kTime> TM;
     if (tid == 0) {
         TM.on = P.timing;
         TM.last = clock64();
@@ -1186,7 +1213,7 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
         jd.cur_buf = S.cur_buf; jd.nxt_buf = S.nxt_buf; jd.cursor = S.cursor;
         jd.cur_len = S.cur_len; jd.nxt_len = S.nxt_len; jd.recount = S.recount;
     }
-    if (P.timing && tid == 0 && (is_maint || cta == 0)) {
+    if (kTime && P.timing && tid == 0 && (is_maint || cta == 0)) {
         const uint32_t base = is_maint ? 16 : 0;
         for (int k = 0; k < 16; ++k) atomicAdd(L.phase + base + k, TM.acc[k]);
     }
@@ -1195,14 +1222,17 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
 // Two instantiations: 512 threads, one CTA per SM (a single replay: the most
 // memory parallelism per job), and 256 threads, two CTAs per SM (replicas that
 // would not fit one per SM: twice the independent replays per SM).
+// (kTime: the phase-counter build, launched only under seneca_profile bit 1.)
+template <bool kTime>
 __global__ void __launch_bounds__(kThreads, 1)
 ods_rounds(const __grid_constant__ Lays LS, const __grid_constant__ Cfg C, const __grid_constant__ Launch P) {
-    ods_rounds_body(LS, C, P);
+    ods_rounds_body<kTime>(LS, C, P);
 }
 
+template <bool kTime>
 __global__ void __launch_bounds__(kThreads / 2, 2)
 ods_rounds_x2(const __grid_constant__ Lays LS, const __grid_constant__ Cfg C, const __grid_constant__ Launch P) {
-    ods_rounds_body(LS, C, P);
+    ods_rounds_body<kTime>(LS, C, P);
 }
 
 // ------------------------------------------------------------------ one-off kernels
@@ -1374,6 +1404,7 @@ struct seneca_ctx {
     uint32_t profiling;
     size_t round_smem;
     const void* round_fn;      // ods_rounds (512 threads, 1 CTA / SM) or ods_rounds_x2 (256, 2 / SM)
+    const void* round_fn_timed; // the same with the phase counters compiled in (seneca_profile bit 1)
     uint32_t round_threads;
     int device;
     cudaStream_t side;
@@ -1621,7 +1652,7 @@ seneca_status launch_rounds(seneca_ctx* c, uint64_t R, uint32_t jobs_mask, const
     void* args[] = {&c->LS, &c->C, &P};
     cudaError_t le = cudaSuccess;
     timed(c, K_ROUNDS, st, [&] {
-        le = cudaLaunchCooperativeKernel(c->round_fn, dim3((c->C.J + 1) * c->R), dim3(c->round_threads), args,
+        le = cudaLaunchCooperativeKernel(P.timing ? c->round_fn_timed : c->round_fn, dim3((c->C.J + 1) * c->R), dim3(c->round_threads), args,
                                          c->round_smem, st);
     });
     if (le != cudaSuccess) return cuda_status(le, "cudaLaunchCooperativeKernel(ods_rounds)");
@@ -1689,21 +1720,32 @@ extern "C" seneca_status seneca_init_cache(const seneca_cache_config* cfg, void*
     cudaStream_t st = (cudaStream_t)stream;
     cudaGetDevice(&c->device);
 #define INIT_TRY(expr) do { cudaError_t _e = (expr); if (_e != cudaSuccess) { delete c; return cuda_status(_e, #expr); } } while (0)
-    INIT_TRY(cudaFuncSetAttribute(ods_rounds, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    INIT_TRY(cudaFuncSetAttribute(ods_rounds_x2, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    INIT_TRY(cudaFuncSetAttribute(ods_rounds<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    INIT_TRY(cudaFuncSetAttribute(ods_rounds_x2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    INIT_TRY(cudaFuncSetAttribute(ods_rounds<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    INIT_TRY(cudaFuncSetAttribute(ods_rounds_x2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     INIT_TRY(cudaFuncSetAttribute(ods_validate_requests, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     {   // the cooperative round launch needs every replica's CTAs co-resident: one
         // 512-thread CTA per SM when they fit, else two 256-thread CTAs per SM
         const uint64_t need = (uint64_t)(z.C.J + 1) * z.R;
         int per_sm = 0;
-        INIT_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ods_rounds, kThreads, round_smem));
+        // (occupancy of the timed variants is checked too: a profiled replay
+        // must fit the same co-resident grid)
+        int per_sm_t = 0;
+        INIT_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ods_rounds<false>, kThreads, round_smem));
+        INIT_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_t, ods_rounds<true>, kThreads, round_smem));
+        per_sm = std::min(per_sm, per_sm_t);
         uint64_t slots = (uint64_t)per_sm * num_sms();
-        c->round_fn = (const void*)ods_rounds;
+        c->round_fn = (const void*)ods_rounds<false>;
+        c->round_fn_timed = (const void*)ods_rounds<true>;
         c->round_threads = kThreads;
         if (need > slots) {
             const size_t smem2 = smem_for(kThreads / 2);
             int per_sm2 = 0;
-            INIT_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, ods_rounds_x2, kThreads / 2, smem2));
+            int per_sm2_t = 0;
+            INIT_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, ods_rounds_x2<false>, kThreads / 2, smem2));
+            INIT_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2_t, ods_rounds_x2<true>, kThreads / 2, smem2));
+            per_sm2 = std::min(per_sm2, per_sm2_t);
             const uint64_t slots2 = (uint64_t)per_sm2 * num_sms();
             if (need > slots2) {
                 set_error("%u replicas x %u CTAs exceed the %llu co-resident CTA slots", z.R, z.C.J + 1,
@@ -1711,7 +1753,8 @@ extern "C" seneca_status seneca_init_cache(const seneca_cache_config* cfg, void*
                 delete c;
                 return SENECA_EINVAL;
             }
-            c->round_fn = (const void*)ods_rounds_x2;
+            c->round_fn = (const void*)ods_rounds_x2<false>;
+            c->round_fn_timed = (const void*)ods_rounds_x2<true>;
             c->round_threads = kThreads / 2;
             c->round_smem = smem2;
         }

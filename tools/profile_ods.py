@@ -1,6 +1,6 @@
 """Drive a bounded ODS replay (and optionally the MDP sweep) for ncu captures.
 
-    python tools/profile_ods.py imagenet1k 2000 [--mdp]
+    python tools/profile_ods.py imagenet1k 2000 [--mdp] [--plain]
 """
 import os
 import sys
@@ -20,7 +20,7 @@ rounds = int(sys.argv[2]) if len(sys.argv) > 2 else 2000
 c = synth.ods_config(name, seed=synth.PERF_SEED)
 caps = S.split_capacities(c["n_total"], c["s_data"], c["m_num"], c["m_den"], c["cache_bytes"], *c["split"])
 g = P.ODSContext(c["n_total"], c["batch"], c["target"], caps[0], caps[1], caps[2], c["seed"])
-g.profile(3)                      # event timing + in-kernel phase counters
+g.profile(0 if "--plain" in sys.argv else 3)   # event timing + in-kernel phase counters (--plain: none)
 g.replay_rounds(rounds)
 torch.cuda.synchronize()
 ph = g.phase_cycles()
