@@ -319,7 +319,6 @@ struct JobSmem {
     uint32_t pf_state;    // 0 none, 1 list window requested, 2 seen chunks requested
     uint32_t pf_buf, pf_epoch, pf_base, pf_len, pf_vlen;
     uint32_t scan[33];
-    unsigned long long red[(kThreads / 32) * 13];
 };
 
 __device__ __forceinline__ const uint32_t* list_ptr(const Lay& L, const Cfg& C, uint32_t j, uint32_t e, uint32_t buf) {
@@ -712,13 +711,15 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
             }
         }
     }
+    // fire-and-forget adds into this job-epoch's counters: the digest (a sum mod
+    // 2^64, order-free) by every warp, the rest by warp 0; S.npush (the coupled
+    // signal) is complete at the barrier below
+    seneca_job_epoch_stats* st = L.stats + (size_t)j * C.maxT + e;
+    unsigned long long* f = reinterpret_cast<unsigned long long*>(st);
     dig = warp_sum(dig);
-    if (lane == 0) S.red[tid >> 5] = dig;
-    __syncthreads();
+    if (lane == 0 && dig) atomicAdd(f + 12, dig);
     TM.tick(11);
-    if (tid < 13) {           // fire-and-forget adds into this job-epoch's counters
-        seneca_job_epoch_stats* st = L.stats + (size_t)j * C.maxT + e;
-        unsigned long long* f = reinterpret_cast<unsigned long long*>(st);
+    if (tid < 12) {
         // hits/k indexed A=0, D=1, E=2; counter tiers S=0, E=1, D=2, A=3
         const uint32_t hA = S.hits[0], hD = S.hits[1], hE = S.hits[2];
         unsigned long long v = 0;
@@ -733,7 +734,6 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
             case 9: v = hE; break;                             // req_hits[E]
             case 10: v = hD; break;                            // req_hits[D]
             case 11: v = hA; break;                            // req_hits[A]
-            case 12: for (uint32_t w = 0; w < T / 32; ++w) v += S.red[w]; break;   // digest
             default: break;
         }
         if (v) atomicAdd(f + tid, v);
@@ -952,6 +952,7 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
     __shared__ JobSmem S;
     __shared__ MaintSmem M;
     __shared__ uint32_t s_n[kMaxJobs], s_e[kMaxJobs], s_active, s_pending;
+    __shared__ uint32_t s_part, s_departing;     // schedule of the current round (warp 0 computes it)
     const uint32_t tid = threadIdx.x;
     const uint32_t rep = blockIdx.x / (C.J + 1);
     const uint32_t cta = blockIdx.x - rep * (C.J + 1);
@@ -1024,32 +1025,43 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
     __syncthreads();
 
     auto need_of = [&](uint32_t jj) -> uint32_t { return min(C.batch[jj], C.N - s_n[jj]); };
-    // data-independent schedule of the current round (R-O12)
+    // data-independent schedule of the current round (R-O12): warp 0 computes it
+    // (lane jj = job jj) after the launch setup and at every round end, every
+    // thread reads it
+    auto schedule_warp0 = [&]() {
+        const uint32_t part = s_active & P.subset;
+        const bool dep = tid < C.J && ((part >> tid) & 1u) && s_n[tid] + need_of(tid) == C.N &&
+                         s_e[tid] + 1 == C.target[tid];
+        const uint32_t departing = __ballot_sync(0xffffffffu, dep);
+        if (tid == 0) { s_part = part; s_departing = departing; }
+    };
     auto schedule = [&](uint32_t& part, uint32_t& departing) {
-        part = s_active & P.subset;
-        departing = 0;
-        for (uint32_t m = part; m; m &= m - 1) {
-            const uint32_t jj = __ffs(m) - 1;
-            if (s_n[jj] + need_of(jj) == C.N && s_e[jj] + 1 == C.target[jj]) departing |= 1u << jj;
-        }
+        part = s_part;
+        departing = s_departing;
     };
     // end of round r: progress, departures, then the arrivals of round r + 1
     auto advance = [&](uint32_t part, uint32_t departing, uint64_t r) {
         __syncthreads();
-        if (tid == 0) {
-            for (uint32_t m = part; m; m &= m - 1) {
-                const uint32_t jj = __ffs(m) - 1;
-                s_n[jj] += need_of(jj);
-                if (s_n[jj] == C.N) { s_n[jj] = 0; s_e[jj] += 1; }
+        if (tid < 32) {
+            if ((part >> tid) & 1u) {
+                uint32_t n = s_n[tid] + need_of(tid);
+                if (n == C.N) { n = 0; s_e[tid] += 1; }
+                s_n[tid] = n;
             }
-            s_active &= ~departing;
-            for (uint32_t m = s_pending; m; m &= m - 1) {
-                const uint32_t jj = __ffs(m) - 1;
-                if (P.arrival[jj] <= r + 1) { s_active |= 1u << jj; s_pending &= ~(1u << jj); }
+            if (tid == 0) {
+                s_active &= ~departing;
+                for (uint32_t m = s_pending; m; m &= m - 1) {
+                    const uint32_t jj = __ffs(m) - 1;
+                    if (P.arrival[jj] <= r + 1) { s_active |= 1u << jj; s_pending &= ~(1u << jj); }
+                }
             }
+            __syncwarp();
+            schedule_warp0();
         }
         __syncthreads();
     };
+    if (tid < 32) schedule_warp0();
+    __syncthreads();
 
     // Coupled rounds synchronise through two one-directional signals (zeroed by
     // the host before every launch): L.bar[0] counts job phases completed, L.bar[1]
