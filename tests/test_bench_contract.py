@@ -47,3 +47,34 @@ def test_committed_bench_lines_have_the_contract_keys():
         assert d["parity"]["ods_vs_oracle_golden"] == "bit-exact"
         assert d["parity"]["mdp_vs_oracle_first_200_profiles"] == "bit-exact"
         assert not set(d["clocks"]["reasons"]) & {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+
+
+def test_pass_equivalent_matches_the_survey_sizes():
+    """bench.pass_equivalent restates SURVEY §8(a) row a4 / §8(d) target 1; pin it to
+    the sizes the survey prints: 22K 2 x 1,774,644 B per job-round (seen + E),
+    IN1K 4 x 160,148 B per job-round (seen, D, A, cons) + 3 x 160,148 B storage
+    pool per round, OpenImages 3 x 217,500 B per job-round."""
+    sys.path.insert(0, ROOT)
+    import bench
+    import synth
+    W = {"imagenet22k": 443661, "imagenet1k": 40037, "openimages": 54375}
+    split_caps = {"imagenet22k": (4376846, 0, 0), "imagenet1k": (0, 42038, 45541),
+                  "openimages": (658561, 118731, 0)}
+    for name, words in W.items():
+        c = synth.ods_config(name, seed=synth.PERF_SEED)
+        pe = bench.pass_equivalent(c, split_caps[name], words, ods_s=1.0, steps=1, world=1, hbm_peak=1000.0)
+        jr = sum(t * -(-c["n_total"] // b) for t, b in zip(c["target"], c["batch"]))
+        if name == "imagenet22k":
+            assert jr == 8 * 2 * 27729                          # 8 jobs x 2 epochs x ceil(14,197,122 / 512)
+            per_round_8jobs = 8 * 2 * 4 * words
+            assert per_round_8jobs == 28394304                  # SURVEY: 28.4 MB per round
+            assert pe["bytes_per_replay"] == 2 * 4 * words * jr + 4 * words * 16
+        elif name == "imagenet1k":
+            rounds = 10 * -(-c["n_total"] // 256)
+            assert 4 * 4 * words * 4 + 3 * 4 * words == 3042812   # SURVEY: 2.56 MB + 0.48 MB per round
+            assert pe["bytes_per_replay"] == 4 * 4 * words * jr + 3 * 4 * words * rounds + 4 * words * 40
+        else:
+            assert 8 * 3 * 4 * words == 5220000                 # SURVEY: 5.22 MB per round
+            assert pe["bytes_per_replay"] == 3 * 4 * words * jr + 4 * words * 40
+        assert abs(pe["frac"] - pe["achieved"] / pe["peak"]) < 1e-12
+        assert abs(pe["achieved"] - pe["bytes_per_replay"] / 1e9) < 1e-6

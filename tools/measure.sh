@@ -23,7 +23,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 # (one ods_rounds launch) and the 10,000-profile MDP sweep with the grid
 for w in imagenet1k openimages imagenet22k; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:ods_rounds -c 1 -o $OUT/ncu_ods_rounds_$w \
-    python tools/profile_ods.py $w 1000000 > /dev/null 2>&1; echo "ncu ods $w rc=$?"
+    python tools/profile_ods.py $w 1000000 --plain > /dev/null 2>&1; echo "ncu ods $w rc=$?"
 done
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:mdp_sweep -c 1 -o $OUT/ncu_mdp_sweep \
   python tools/profile_ods.py toy 10 --mdp > /dev/null 2>&1; echo "ncu mdp rc=$?"
