@@ -124,6 +124,36 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* t
     return res;
 }
 
+// Exclusive scan of a per-thread count given as two flag bits (v = f0 + f1,
+// each 0 or 1) across the block: in-warp prefixes from two ballots, then one
+// warp scans the per-warp totals.  Same contract as block_exclusive_scan
+// (every thread calls it, ends with a barrier), far fewer instructions.
+__device__ __forceinline__ uint32_t block_flag_scan(bool f0, bool f1, uint32_t* total, uint32_t* scratch) {
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint32_t nwarps = blockDim.x >> 5;
+    const uint32_t b0 = __ballot_sync(0xffffffffu, f0), b1 = __ballot_sync(0xffffffffu, f1);
+    const uint32_t lt = (1u << lane) - 1u;
+    const uint32_t ex_w = __popc(b0 & lt) + __popc(b1 & lt);
+    if (lane == 0) scratch[warp] = __popc(b0) + __popc(b1);
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = lane < nwarps ? scratch[lane] : 0u;
+        uint32_t wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= (uint32_t)o) wi += y;
+        }
+        if (lane < nwarps) scratch[lane] = wi - w;
+        if (lane == 31) scratch[32] = wi;
+    }
+    __syncthreads();
+    const uint32_t res = scratch[warp] + ex_w;
+    if (total) *total = scratch[32];
+    __syncthreads();
+    return res;
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll

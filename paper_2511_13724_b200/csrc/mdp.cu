@@ -34,6 +34,9 @@ constexpr int kMaxSteps = 101;  // grid step 1 % -> 101 values per coordinate
 #ifndef SENECA_MDP_UNROLL
 #define SENECA_MDP_UNROLL 4
 #endif
+#ifndef SENECA_MDP_FASTDIV
+#define SENECA_MDP_FASTDIV 1      // 0: capacity floors by the u64 division routine (A/B knob)
+#endif
 #ifndef SENECA_MDP_MINB
 #define SENECA_MDP_MINB 3
 #endif
@@ -137,6 +140,7 @@ static_assert(sizeof(Row) == 40, "Row layout");
 struct Header {
     double dsi[4];
     uint64_t N, Xad, Dad, De, cache_bytes;
+    double rDad, rDe;          // RN(1/Dad), RN(1/De): estimates for the exact floors of Eqs. 5-7
     uint8_t lim[4];
     uint32_t valid;
 };
@@ -168,7 +172,28 @@ __device__ void build_header(const seneca_mdp_profile* __restrict__ profiles, ui
         H.Dad = 100ull * p.m_num * p.s_data;
         H.De = 100ull * p.s_data;
         H.cache_bytes = p.cache_bytes;
+        H.rDad = __drcp_rn(u2d(H.Dad));
+        H.rDe = __drcp_rn(u2d(H.De));
     }
+}
+
+// floor(num / den) exactly, for den < 2^62: q0 = trunc(RN(num) * RN(1/den)) is
+// within 1 of the quotient while it is < 2^50 (relative error < 2^-51); the
+// residual num - q0 den, exact in two's complement because |residual| < 2 den,
+// corrects it.  Larger quotients (or den) take the u64 division routine.
+__device__ __forceinline__ uint64_t floor_div(uint64_t num, uint64_t den, double rden) {
+#if SENECA_MDP_FASTDIV
+    const double qe = __dmul_rn(u2d(num), rden);
+    if (den < (1ull << 62) && qe < 1125899906842624.0) {          // 2^50
+        uint64_t q = (uint64_t)qe;
+        const int64_t r = (int64_t)(num - q * den);
+        if (r < 0) --q;
+        else if ((uint64_t)r >= den) ++q;
+        return q;
+    }
+#endif
+    (void)rden;
+    return num / den;
 }
 
 // Rows k0 .. k0+31 (one per lane, k <= steps) of a valid profile's tables.
@@ -180,7 +205,7 @@ __device__ void build_rows(const Header& H, uint32_t k0, uint32_t g, uint32_t st
     const bool exact_div = N < (1ull << 53);
     const double yN = __drcp_rn(dN);
     const uint64_t pct = (uint64_t)k * g;
-    uint64_t cad = (pct * H.Xad) / H.Dad, ce = (pct * H.cache_bytes) / H.De;   // Eqs. 5-7, exact floors
+    uint64_t cad = floor_div(pct * H.Xad, H.Dad, H.rDad), ce = floor_div(pct * H.cache_bytes, H.De, H.rDe);   // Eqs. 5-7, exact floors
     cad = cad < N ? cad : N;
     ce = ce < N ? ce : N;
     Row& R = rows[k];

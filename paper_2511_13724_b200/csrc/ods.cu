@@ -409,7 +409,7 @@ __device__ void job_walk(const Lay& L, const Cfg& C, JobSmem& S, uint32_t* s_req
                 }
             }
             uint32_t tot;
-            const uint32_t ex = block_exclusive_scan(cnt, &tot, S.scan);
+            const uint32_t ex = block_flag_scan(flags & 1u, (flags >> 1) & 1u, &tot, S.scan);
             uint32_t r = ex;
 #pragma unroll
             for (uint32_t k = 0; k < 2; ++k) {
@@ -604,7 +604,7 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
             }
         }
         uint32_t tot;
-        const uint32_t ex = block_exclusive_scan(is_miss ? 1u : 0u, &tot, S.scan);
+        const uint32_t ex = block_flag_scan(is_miss, false, &tot, S.scan);
         if (is_miss) s_miss[mbase + ex] = s;
         mbase += tot;
     }
