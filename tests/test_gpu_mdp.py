@@ -162,6 +162,32 @@ def test_wide_counts_paths():
         assert_same(res, ores, grid, ogrid)
 
 
+def test_capacity_floor_boundaries():
+    """Eqs. 5-7 floors at exact multiples and +-1 (mdp.cu floor_div: a reciprocal
+    estimate and one integer correction), for small divisors, divisors near the
+    2^62 fast-path limit and above it (the u64 division fallback)."""
+    cols = synth.mdp_profiles(270, seed=1234)
+    rows = O.profiles_from_columns(cols)
+    sd = [1, 7, 114620, 2**33 + 5, 2**45 - 1, 2**53 + 1, 2**55 + 3, 2**56 + 3, 2**57 - 1]
+    lim = (2**64 - 1) // 100                      # 100 * cache_bytes * m_den < 2^64 (m_den = 1)
+    for k in range(len(rows)):
+        s = sd[k % len(sd)]
+        t = 1 + (k // len(sd)) % 10
+        d = (k // (len(sd) * 10)) % 3 - 1
+        base = 100 * (2**24 + 1) if s == 1 else t * s
+        rows["s_data"][k] = s
+        rows["m_num"][k] = 1
+        rows["m_den"][k] = 1
+        rows["n_total"][k] = 2**31 - 1
+        rows["cache_bytes"][k] = np.uint64(max(0, min(base * (t if s == 1 else 1) + d, lim)))
+    for g in (1, 3):
+        if 100 % g:
+            continue
+        ores, ogrid = O.mdp_sweep(rows, g, want_grid=True)
+        res, grid = run_gpu(rows, g)
+        assert_same(res, ores, grid, ogrid)
+
+
 def test_every_grid_step():
     """Every divisor of 100: one to several row items and partial sweep chunks."""
     rows = O.profiles_from_columns(synth.mdp_profiles(700, seed=31))
