@@ -319,6 +319,11 @@ struct JobSmem {
     uint32_t pf_state;    // 0 none, 1 list window requested, 2 seen chunks requested
     uint32_t pf_buf, pf_epoch, pf_base, pf_len, pf_vlen;
     uint32_t scan[33];
+    // this job-epoch's counters, accumulated across rounds and added to memory at
+    // the epoch end / launch end (flush_stats): the digest one running sum per
+    // thread (a sum mod 2^64 is order-free), counter c in acc_cnt[c]
+    unsigned long long acc_cnt[12];
+    unsigned long long acc_dig[kThreads];
 };
 
 __device__ __forceinline__ const uint32_t* list_ptr(const Lay& L, const Cfg& C, uint32_t j, uint32_t e, uint32_t buf) {
@@ -711,13 +716,11 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
             }
         }
     }
-    // fire-and-forget adds into this job-epoch's counters: the digest (a sum mod
-    // 2^64, order-free) by every warp, the rest by warp 0; S.npush (the coupled
-    // signal) is complete at the barrier below
-    seneca_job_epoch_stats* st = L.stats + (size_t)j * C.maxT + e;
-    unsigned long long* f = reinterpret_cast<unsigned long long*>(st);
-    dig = warp_sum(dig);
-    if (lane == 0 && dig) atomicAdd(f + 12, dig);
+    // this job-epoch's counters accumulate in registers (the digest is a sum mod
+    // 2^64, order-free: one running sum per thread; counter c in lane c of warp 0)
+    // and are added to the counters in memory at the epoch end / launch end
+    // (flush_stats); S.npush (the coupled signal) is complete at the barrier below
+    S.acc_dig[tid] += dig;
     TM.tick(11);
     if (tid < 12) {
         // hits/k indexed A=0, D=1, E=2; counter tiers S=0, E=1, D=2, A=3
@@ -736,10 +739,22 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
             case 11: v = hA; break;                            // req_hits[A]
             default: break;
         }
-        if (v) atomicAdd(f + tid, v);
+        S.acc_cnt[tid] += v;
     }
     __syncthreads();
     TM.tick(3);
+}
+
+// Add a job's register-held counters of epoch e to its counter row (every thread
+// of the job CTA calls it: the digest is reduced per warp).
+__device__ __forceinline__ void flush_stats(const Lay& L, const Cfg& C, JobSmem& S, uint32_t j, uint32_t e) {
+    const uint32_t tid = threadIdx.x;
+    unsigned long long* f = reinterpret_cast<unsigned long long*>(L.stats + (size_t)j * C.maxT + e);
+    const unsigned long long d = warp_sum(S.acc_dig[tid]);
+    if ((tid & 31) == 0 && d) atomicAdd(f + 12, d);
+    if (tid < 12 && S.acc_cnt[tid]) atomicAdd(f + tid, S.acc_cnt[tid]);
+    S.acc_dig[tid] = 0;
+    if (tid < 12) S.acc_cnt[tid] = 0;
 }
 
 // ------------------------------------------------------------------ maintain (a7)
@@ -1011,6 +1026,8 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
         S.pf_state = 0;
     }
     if (!is_maint) {
+        S.acc_dig[tid] = 0;
+        if (tid < 12) S.acc_cnt[tid] = 0;
         if (tid < 3) S.tot[tid] = ldcg(L.cnt_tot + j * 3 + tid);
         for (uint32_t k = tid; k < 3 * C.NS; k += blockDim.x) s_sup[k] = ldcg(L.cnt_sup + (size_t)j * 3 * C.NS + k);
     } else {
@@ -1179,6 +1196,7 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
                           __popc(active_after), TM, s_win, s_wseen, s_sup);
                 // a8 (R-O16): the epoch ends with this batch -> reset seen_j and the walk
                 if (s_n[j] + S.need == C.N) {
+                    flush_stats(L, C, S, j, s_e[j]);
                     uint4* sj = reinterpret_cast<uint4*>(L.seen + (size_t)j * C.NW);
                     for (uint32_t k = tid; k < C.NW / 4; k += blockDim.x) sj[k] = make_uint4(0, 0, 0, 0);
                     if (tid == 0) {
@@ -1204,8 +1222,10 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
             TM.tick(5);
         }
     }
-    // epilogue: the last round's refills into this job's A pool; persist the totals
+    // epilogue: the current epoch's counters, the last round's refills into this
+    // job's A pool; persist the totals
     if (!is_maint) {
+        flush_stats(L, C, S, j, s_e[j]);
         if (coupled && P.rounds > 0 && (s_active >> j & 1u)) {
             if (tid == 0) { while (ld_acquire(L.bar + 2) < P.rounds) { } }
             __syncthreads();
