@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--workload", default="imagenet1k", choices=sorted(WORKLOADS))
     ap.add_argument("--mdp-profiles", type=int, default=10_000)
     ap.add_argument("--mdp-grid-step", type=int, default=1)
+    ap.add_argument("--mdp-large", type=int, default=100_000,
+                    help="also time one MDP sweep of this many profiles with the grid written (0: skip)")
     ap.add_argument("--no-grid", action="store_true", help="MDP argmax only (no grid write)")
     ap.add_argument("--no-profile", action="store_true", help="no CUDA-event kernel timing in the timed steps")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -172,6 +174,31 @@ def run_reference(args, rank, world):
 
 
 # --------------------------------------------------------------------------- cpu baseline
+def _oracle_mdp_slice(job):
+    """One worker of the all-cores MDP oracle run (a process: the oracle is
+    single-threaded C)."""
+    rows, g = job
+    import oracle as O
+    O.mdp_sweep(rows, g, want_grid=False)
+    return len(rows)
+
+
+def oracle_mdp_all_cores(args, per_core=1000):
+    """the MDP oracle also on all host cores -- profiles striped over
+    one process per core, each running the unmodified oracle on its slice."""
+    import multiprocessing as mp
+    import oracle as O
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    rows = O.profiles_from_columns(synth.mdp_profiles(per_core * cores, seed=synth.PERF_SEED))
+    jobs = [(rows[k * per_core:(k + 1) * per_core], args.mdp_grid_step) for k in range(cores)]
+    with mp.get_context("fork").Pool(cores) as pool:
+        pool.map(_oracle_mdp_slice, [(rows[:1], args.mdp_grid_step)] * cores)     # start the workers
+        t0 = time.perf_counter()
+        done = sum(pool.map(_oracle_mdp_slice, jobs, chunksize=1))
+        dt = time.perf_counter() - t0
+    return done * O.num_splits(args.mdp_grid_step) / dt, cores, done, dt
+
+
 def cpu_baseline(args, c, caps):
     import oracle as O
     ce, cd, ca = caps
@@ -193,10 +220,14 @@ def cpu_baseline(args, c, caps):
     O.mdp_sweep(rows, args.mdp_grid_step, want_grid=False)
     dm = time.perf_counter() - t1
     ns = O.num_splits(args.mdp_grid_step)
+    mdp_all, mcores, mdone, mdt = oracle_mdp_all_cores(args)
     return dict(value=dec / dt, unit="decisions/s", cores=1, kind="oracle",
                 sample=f"oracle replay of the first {done} rounds ({dec} decisions, {dt:.1f} s) of the same "
-                       f"workload; MDP oracle 1,000 profiles x {ns} splits in {dm:.2f} s",
-                mdp_value=1000 * ns / dm, mdp_unit="split-evals/s")
+                       f"workload (the ODS oracle is a sequential protocol: 1 core); MDP oracle 1,000 profiles x "
+                       f"{ns} splits in {dm:.2f} s on 1 core, {mdone:,} profiles in {mdt:.2f} s on {mcores} cores",
+                mdp_value=1000 * ns / dm, mdp_unit="split-evals/s",
+                mdp_value_all_cores=mdp_all, mdp_cores_all=mcores,
+                mdp_cores_note="processes launched = the affinity count; a CPU quota can leave fewer effective cores")
 
 
 # --------------------------------------------------------------------------- roofline models
@@ -413,6 +444,45 @@ def main():
     except Exception as e:  # the oracle is only a checker; report, do not fall back
         parity["mdp_vs_oracle_first_200_profiles"] = f"unchecked: {e}"
 
+    # ---- MDP at scale ("also measure 10^5-10^6 profiles or grid-dump
+    #      mode"): 100,000 profiles x 5,151 splits, 4.1 GB of grid written; median of 3
+    #      event-timed sweeps after a warm-up, L2 flushed before each; parity on the
+    #      first and last 50 profiles
+    mdp_large = None
+    if args.mdp_large > 0 and not args.no_grid:
+        import oracle as O
+        nl = args.mdp_large
+        cols_l = synth.mdp_profiles(nl, seed=D.rank_seed(synth.PERF_SEED, rank) + 1)
+        d_prof_l = torch.from_numpy(S.profiles_from_columns(cols_l).view(np.uint8).copy()).to(dev)
+        d_res_l = torch.empty(nl * S.RESULT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+        d_grid_l = torch.empty((nl, nsplit), dtype=torch.float64, device=dev)
+        S.mdp_sweep(d_prof_l, nl, args.mdp_grid_step, d_res_l, d_grid_l, stream)
+        times = []
+        for _ in range(3):
+            flush.fill_(3)
+            torch.cuda.synchronize(dev)
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            torch.cuda._sleep(200_000)
+            e[0].record(stream)
+            S.mdp_sweep(d_prof_l, nl, args.mdp_grid_step, d_res_l, d_grid_l, stream)
+            e[1].record(stream)
+            torch.cuda.synchronize(dev)
+            times.append(e[0].elapsed_time(e[1]))
+        ms_l = float(np.median(times))
+        idx = np.r_[0:50, nl - 50:nl]
+        orow = O.profiles_from_columns({f: cols_l[f][idx] for f in cols_l})
+        ores, ogrid = O.mdp_sweep(orow, args.mdp_grid_step, want_grid=True)
+        res = d_res_l.cpu().numpy().view(S.RESULT_DTYPE)[idx]
+        ok = np.array_equal(res["v_best"].view(np.uint64), ores["v"].view(np.uint64)) and \
+            all(np.array_equal(res[f], ores[f]) for f in ("p_e", "p_d", "p_a")) and \
+            np.array_equal(d_grid_l[torch.from_numpy(idx).to(dev)].cpu().numpy().view(np.uint64), ogrid.view(np.uint64))
+        bytes_l = nl * (112 + 48) + 8 * nl * nsplit
+        mdp_large = dict(profiles=nl, splits=nsplit, ms=ms_l, value=nl * nsplit / (ms_l / 1e3), unit="split-evals/s",
+                         grid_bytes=8 * nl * nsplit,
+                         roofline=dict(bound="hbm", achieved=bytes_l / (ms_l / 1e3) / 1e9, unit="GB/s"),
+                         parity="bit-exact (first and last 50 profiles, results and grid rows)" if ok else "MISMATCH")
+        del d_prof_l, d_res_l, d_grid_l
+
     # ---- R independent replays in one context (untimed warm-up, then timed steps).
     #      Candidates: the most replicas with one 512-thread round CTA per SM, and
     #      with two 256-thread CTAs per SM (the library picks the kernel variant);
@@ -538,6 +608,8 @@ def main():
     except OSError:
         pass
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    if mdp_large:
+        mdp_large["roofline"].update(peak=hbm_peak, frac=mdp_large["roofline"]["achieved"] / hbm_peak)
     peak_src = "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"
     kernels = {}
     for name, kv in kstats.items():
@@ -590,7 +662,7 @@ def main():
             roofline=roof,
             pass_equivalent=pass_equivalent(c, caps, v.words, ods_s, args.steps, world, hbm_peak, rep_line),
             mdp=dict(value=total_evals / mdp_s, unit="split-evals/s", dtype="f64", ms_per_step=mdp_ms_step,
-                     roofline=mdp_roof),
+                     roofline=mdp_roof, large=mdp_large),
             replicas=rep_line,
             cpu_baseline=cpu,
             clocks=clk,
