@@ -263,6 +263,7 @@ def algorithmic_bytes(name, info):
 
 
 NCU_TRAFFIC = os.path.join(ROOT, "profiles", "r1", "ncu_traffic.json")
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12      # nominal B200 FP64 (non-tensor), ~37.2 TFLOP/s
 
 
 def pass_equivalent(c, caps, words, ods_s, steps, world, hbm_peak, replicas=None):
@@ -662,7 +663,13 @@ def main():
             roofline=roof,
             pass_equivalent=pass_equivalent(c, caps, v.words, ods_s, args.steps, world, hbm_peak, rep_line),
             mdp=dict(value=total_evals / mdp_s, unit="split-evals/s", dtype="f64", ms_per_step=mdp_ms_step,
-                     roofline=mdp_roof, large=mdp_large),
+                     roofline=mdp_roof, large=mdp_large,
+                     fp64=dict(flops_per_split=11, achieved_tflops=total_evals * 11 / mdp_s / 1e12,
+                               peak_tflops=FP64_PEAK_TFLOPS, frac=total_evals * 11 / mdp_s / 1e12 / FP64_PEAK_TFLOPS,
+                               note="SURVEY 8(d): Eq. 9 is 4 div + 4 mul + 3 add per split (a division counted "
+                                    "once; hardware expands it to ~9-10 FP64-pipe instructions); peak = 148 SMs x "
+                                    "64 FP64 FMA/clk x 2 x 1.965 GHz, nominal (MEASURED_PEAKS.json has no FP64 "
+                                    "figure); the kernel is issue-bound, DESIGN.md 7.3")),
             replicas=rep_line,
             cpu_baseline=cpu,
             clocks=clk,
