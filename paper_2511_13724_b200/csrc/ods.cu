@@ -961,7 +961,7 @@ __device__ void job_take_refills(const Lay& L, const Cfg& C, JobSmem& S, uint32_
 // ------------------------------------------------------------------ the persistent round kernel
 // Grid: (J + 1) CTAs per replica; replicas are independent replays (their own
 // workspace slice and seed) that share nothing but the launch.
-template <bool kTime>
+template <bool kTime, bool kCoupled>
 __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, const Launch& P) {
     extern __shared__ __align__(16) uint32_t smem[];
     __shared__ JobSmem S;
@@ -1001,7 +1001,9 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
     // with no tracked tier (cap_A = 0 and evict_tiers = A) there is no cross-job
     // interaction at all (E and D are static, maintain has nothing to do): the job
     // CTAs run their rounds independently
-    const bool coupled = C.cap_t > 0 || C.cold;
+    // (kCoupled == (C.cap_t > 0 || C.cold), chosen by the host: the uncoupled
+    // instantiation contains no maintain, refill or signal code at all)
+    constexpr bool coupled = kCoupled;
     if (is_maint && !coupled) return;
 
     if (tid < kMaxJobs) { s_n[tid] = P.n0[tid]; s_e[tid] = P.e0[tid]; }
@@ -1254,17 +1256,28 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
 // Two instantiations: 512 threads, one CTA per SM (a single replay: the most
 // memory parallelism per job), and 256 threads, two CTAs per SM (replicas that
 // would not fit one per SM: twice the independent replays per SM).
-// (kTime: the phase-counter build, launched only under seneca_profile bit 1.)
-template <bool kTime>
+// (kTime: the phase-counter build, launched only under seneca_profile bit 1;
+// kCoupled: a tracked tier or a cold start, i.e. jobs interact through maintain.)
+template <bool kTime, bool kCoupled>
 __global__ void __launch_bounds__(kThreads, 1)
 ods_rounds(const __grid_constant__ Lays LS, const __grid_constant__ Cfg C, const __grid_constant__ Launch P) {
-    ods_rounds_body<kTime>(LS, C, P);
+    ods_rounds_body<kTime, kCoupled>(LS, C, P);
 }
 
-template <bool kTime>
+template <bool kTime, bool kCoupled>
 __global__ void __launch_bounds__(kThreads / 2, 2)
 ods_rounds_x2(const __grid_constant__ Lays LS, const __grid_constant__ Cfg C, const __grid_constant__ Launch P) {
-    ods_rounds_body<kTime>(LS, C, P);
+    ods_rounds_body<kTime, kCoupled>(LS, C, P);
+}
+
+// the round kernel for (two CTAs per SM, phase counters, coupled)
+const void* round_kernel(bool x2, bool timed, bool coupled) {
+    if (x2) {
+        if (coupled) return timed ? (const void*)ods_rounds_x2<true, true> : (const void*)ods_rounds_x2<false, true>;
+        return timed ? (const void*)ods_rounds_x2<true, false> : (const void*)ods_rounds_x2<false, false>;
+    }
+    if (coupled) return timed ? (const void*)ods_rounds<true, true> : (const void*)ods_rounds<false, true>;
+    return timed ? (const void*)ods_rounds<true, false> : (const void*)ods_rounds<false, false>;
 }
 
 // ------------------------------------------------------------------ one-off kernels
@@ -1752,10 +1765,11 @@ extern "C" seneca_status seneca_init_cache(const seneca_cache_config* cfg, void*
     cudaStream_t st = (cudaStream_t)stream;
     cudaGetDevice(&c->device);
 #define INIT_TRY(expr) do { cudaError_t _e = (expr); if (_e != cudaSuccess) { delete c; return cuda_status(_e, #expr); } } while (0)
-    INIT_TRY(cudaFuncSetAttribute(ods_rounds<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    INIT_TRY(cudaFuncSetAttribute(ods_rounds_x2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    INIT_TRY(cudaFuncSetAttribute(ods_rounds<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    INIT_TRY(cudaFuncSetAttribute(ods_rounds_x2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    const bool coupled = z.C.cap_t > 0 || z.C.cold;
+    for (int x2 = 0; x2 < 2; ++x2)
+        for (int tm = 0; tm < 2; ++tm)
+            INIT_TRY(cudaFuncSetAttribute(round_kernel(x2, tm, coupled), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          200 * 1024));
     INIT_TRY(cudaFuncSetAttribute(ods_validate_requests, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     {   // the cooperative round launch needs every replica's CTAs co-resident: one
         // 512-thread CTA per SM when they fit, else two 256-thread CTAs per SM
@@ -1764,19 +1778,23 @@ extern "C" seneca_status seneca_init_cache(const seneca_cache_config* cfg, void*
         // (occupancy of the timed variants is checked too: a profiled replay
         // must fit the same co-resident grid)
         int per_sm_t = 0;
-        INIT_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ods_rounds<false>, kThreads, round_smem));
-        INIT_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_t, ods_rounds<true>, kThreads, round_smem));
+        INIT_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, round_kernel(false, false, coupled), kThreads,
+                                                               round_smem));
+        INIT_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_t, round_kernel(false, true, coupled), kThreads,
+                                                               round_smem));
         per_sm = std::min(per_sm, per_sm_t);
         uint64_t slots = (uint64_t)per_sm * num_sms();
-        c->round_fn = (const void*)ods_rounds<false>;
-        c->round_fn_timed = (const void*)ods_rounds<true>;
+        c->round_fn = round_kernel(false, false, coupled);
+        c->round_fn_timed = round_kernel(false, true, coupled);
         c->round_threads = kThreads;
         if (need > slots) {
             const size_t smem2 = smem_for(kThreads / 2);
             int per_sm2 = 0;
             int per_sm2_t = 0;
-            INIT_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, ods_rounds_x2<false>, kThreads / 2, smem2));
-            INIT_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2_t, ods_rounds_x2<true>, kThreads / 2, smem2));
+            INIT_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, round_kernel(true, false, coupled),
+                                                                   kThreads / 2, smem2));
+            INIT_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2_t, round_kernel(true, true, coupled),
+                                                                   kThreads / 2, smem2));
             per_sm2 = std::min(per_sm2, per_sm2_t);
             const uint64_t slots2 = (uint64_t)per_sm2 * num_sms();
             if (need > slots2) {
@@ -1785,8 +1803,8 @@ extern "C" seneca_status seneca_init_cache(const seneca_cache_config* cfg, void*
                 delete c;
                 return SENECA_EINVAL;
             }
-            c->round_fn = (const void*)ods_rounds_x2<false>;
-            c->round_fn_timed = (const void*)ods_rounds_x2<true>;
+            c->round_fn = round_kernel(true, false, coupled);
+            c->round_fn_timed = round_kernel(true, true, coupled);
             c->round_threads = kThreads / 2;
             c->round_smem = smem2;
         }
