@@ -573,9 +573,8 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
     uint32_t* seen_j = L.seen + (size_t)j * C.NW;
     uint32_t* cons_j = L.cons + (size_t)j * C.NW;
     const size_t row = S.rep * P.out_rep + (size_t)P.row_of_job[j] * P.out_stride;
-    if (tid < 3) S.hits[tid] = 0;       // the pool totals S.tot persist across rounds in shared memory
-    if (tid == 0) S.npush = 0;
-    __syncthreads();
+    // (S.hits and S.npush are zero here: reset after their last use of the previous
+    // round; the pool totals S.tot persist across rounds in shared memory)
 
     // a3: hits (E, D, or A not consumed by j, R-O13) join seen_j now
     uint32_t mbase = 0;
@@ -742,6 +741,7 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
         S.acc_cnt[tid] += v;
     }
     __syncthreads();
+    if (tid < 3) S.hits[tid] = 0;      // for the next round (read above, barriers before its next use)
     TM.tick(3);
 }
 
@@ -880,11 +880,12 @@ __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSm
             if (t != T_A) ev_ed[atomicAdd(&M.ned, 1u)] = i | (t == T_E ? 0x80000000u : 0u);
         }
         atomicAnd((t == T_A ? L.bm_a : (t == T_D ? L.bm_d : L.bm_e)) + w, ~b);
-        atomicAdd(&M.ne_t[t], 1u);
+        if (C.evict_all) atomicAdd(&M.ne_t[t], 1u);      // A only: ne_t[A] = ne (set below)
         for (uint32_t a = 0; a < C.J; ++a) atomicAnd(L.cons + (size_t)a * C.NW + w, ~b);
         L.cons_cnt[i] = 0;
         count_add(L, C, spidx, i, 1u, s_supS);
     }
+    if (!C.evict_all && tid == 0) M.ne_t[T_A] = ne;
     __syncthreads();
     // tier split of the k refill positions: A, then D, then E, each up to its deficit
     const uint32_t kA = min(M.def[T_A] + M.ne_t[T_A], k);
@@ -926,12 +927,15 @@ __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSm
 // evicted A entry was consumed by j, so it was in no A pool of j).
 __device__ void job_take_refills(const Lay& L, const Cfg& C, JobSmem& S, uint32_t j, uint64_t r, uint32_t* s_sup) {
     const uint32_t* fn = L.fill_n + (r & 1) * 4;
-    const uint32_t kf = ldcg(fn), kA = ldcg(fn + 1), kD = ldcg(fn + 2);
     const uint32_t* fill = L.fill_list + (size_t)(r & 1) * C.FL;
+    // the first refill entry of this thread is loaded together with the counts (an
+    // entry beyond kf is read but not used; the buffer holds FL entries)
+    const uint32_t i0 = threadIdx.x < C.FL ? ldcg(fill + threadIdx.x) : 0u;
+    const uint32_t kf = ldcg(fn), kA = ldcg(fn + 1), kD = ldcg(fn + 2);
     const uint32_t* seen_j = L.seen + (size_t)j * C.NW;
     uint32_t addA = 0, addD = 0, addE = 0;   // registers (no indexed local array)
     for (uint32_t u = threadIdx.x; u < kf; u += blockDim.x) {
-        const uint32_t i = ldcg(fill + u);
+        const uint32_t i = u == threadIdx.x ? i0 : ldcg(fill + u);
         if (!((ldcg(seen_j + (i >> 5)) >> (i & 31)) & 1u)) {
             const uint32_t tt = u < kA ? 0u : (u < kA + kD ? 1u : 2u);
             count_add(L, C, j * 3 + tt, i, 1u, s_sup + tt * C.NS);
@@ -950,7 +954,9 @@ __device__ void job_take_refills(const Lay& L, const Cfg& C, JobSmem& S, uint32_
             }
         }
     }
-    addA = warp_sum(addA); addD = warp_sum(addD); addE = warp_sum(addE);
+    addA = __reduce_add_sync(0xffffffffu, addA);
+    addD = __reduce_add_sync(0xffffffffu, addD);
+    addE = __reduce_add_sync(0xffffffffu, addE);
     if ((threadIdx.x & 31) == 0) {
         if (addA) atomicAdd(&S.tot[0], addA);
         if (addD) atomicAdd(&S.tot[1], addD);
@@ -1026,10 +1032,12 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
         S.rep = rep;
         S.dens = 1.0f;
         S.pf_state = 0;
+        S.npush = 0;
     }
     if (!is_maint) {
         S.acc_dig[tid] = 0;
         if (tid < 12) S.acc_cnt[tid] = 0;
+        if (tid < 3) S.hits[tid] = 0;
         if (tid < 3) S.tot[tid] = ldcg(L.cnt_tot + j * 3 + tid);
         for (uint32_t k = tid; k < 3 * C.NS; k += blockDim.x) s_sup[k] = ldcg(L.cnt_sup + (size_t)j * 3 * C.NS + k);
     } else {
@@ -1210,6 +1218,7 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
                 if (coupled && tid == 0) {                 // job phase done (+ evictions pushed)
                     __threadfence();
                     atomicAdd(reinterpret_cast<unsigned long long*>(L.bar), 1ull + ((unsigned long long)S.npush << 32));
+                    S.npush = 0;
                 }
                 TM.tick(0);
             }
