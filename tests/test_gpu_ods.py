@@ -123,6 +123,32 @@ def test_full_size_prefix(name, rounds):
     compare_state(o, g)
 
 
+@pytest.mark.parametrize("name,split", [("imagenet1k", None), ("openimages", (52, 48, 0)), ("imagenet22k", (100, 0, 0))])
+def test_replay_in_launches_of_random_length(name, split):
+    """A replay cut into launches of random length (1..300 rounds, epochs ending
+    inside and at the edges of launches) equals the oracle's: the per job-epoch
+    counters and digests the round kernel keeps in shared memory across rounds
+    are added to memory at every epoch end and launch end.  Coupled (ImageNet-1K's
+    A churn) and uncoupled (the paper's OpenImages / ImageNet-22K splits) kernels."""
+    c = synth.ods_config(name, scale=64, seed=3)
+    if split is not None:
+        c["split"] = split
+    ce, cd, ca = caps_of(c)
+    o, g = make_pair(c["n_total"], c["batch"], c["target"], ce, cd, ca, 3)
+    tr = g.new_transcript()
+    st = synth.Stream(4242)
+    total = 0
+    while True:
+        k = int(st.u64(1)[0] % np.uint64(300)) + 1
+        done = g.replay_rounds(k, tr)
+        total += done
+        if done < k or g.view().active_mask == 0:
+            break
+    torch.cuda.synchronize()
+    assert total == o.replay_epochs(max(c["target"]))
+    compare_state(o, g, tr)
+
+
 def _golden_files():
     return sorted(glob.glob(os.path.join(HERE, "golden", "oracle_*_seed*.json")))
 
@@ -264,6 +290,27 @@ def test_replicas_match_independent_oracles(name, scale, R):
     seed = 3
     c = synth.ods_config(name, scale=scale, seed=seed)
     ce, cd, ca = caps_of(c)
+    g = P.ODSContext(c["n_total"], c["batch"], c["target"], ce, cd, ca, seed, replicas=R)
+    tr = g.new_transcript()
+    rounds = g.replay_epochs(max(c["target"]), tr)
+    torch.cuda.synchronize()
+    g.sync()
+    for k in range(R):
+        o = O.ODS(c["n_total"], c["batch"], c["target"], ce, cd, ca, seed + k, transcript=True)
+        assert o.replay_epochs(max(c["target"])) == rounds
+        compare_replica(o, g, k, tr[k])
+
+
+@pytest.mark.parametrize("name,split,R", [("imagenet22k", (100, 0, 0), 4), ("openimages", (52, 48, 0), 20)])
+def test_replicas_uncoupled(name, split, R):
+    """Replicas of the uncoupled instantiation (no tracked tier: the paper's own
+    OpenImages / ImageNet-22K splits), including 20 x 9 CTAs (two 256-thread CTAs
+    per SM) -- each replica equals its independent oracle replay."""
+    seed = 5
+    c = synth.ods_config(name, scale=64, seed=seed)
+    c["split"] = split
+    ce, cd, ca = caps_of(c)
+    assert ca == 0
     g = P.ODSContext(c["n_total"], c["batch"], c["target"], ce, cd, ca, seed, replicas=R)
     tr = g.new_transcript()
     rounds = g.replay_epochs(max(c["target"]), tr)
