@@ -199,6 +199,32 @@ def oracle_mdp_all_cores(args, per_core=1000):
     return done * O.num_splits(args.mdp_grid_step) / dt, cores, done, dt
 
 
+def _oracle_ods_prefix(job):
+    """One worker of the all-cores ODS oracle run: replica k's replay (seed + k) for a
+    fixed number of rounds; returns the decisions it made."""
+    c, caps, k, rounds, evict_all = job
+    import oracle as O
+    ce, cd, ca = caps
+    o = O.ODS(c["n_total"], c["batch"], c["target"], ce, cd, ca, c["seed"] + k, evict_all=evict_all)
+    o.replay_rounds(rounds)
+    _, e, n, _ = o.job_state()
+    return int(sum(int(e[j]) * c["n_total"] + int(n[j]) for j in range(len(c["batch"]))))
+
+
+def oracle_ods_all_cores(args, c, caps, rounds):
+    """"with R replicas, R processes spread over host cores" -- one
+    independent oracle replay (seed + k) per core, each a fixed prefix of rounds;
+    the counterpart of the GPU replicas line."""
+    import multiprocessing as mp
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    jobs = [(c, caps, k, rounds, bool(args.evict_tiers)) for k in range(cores)]
+    with mp.get_context("fork").Pool(cores) as pool:
+        t0 = time.perf_counter()
+        dec = sum(pool.map(_oracle_ods_prefix, jobs, chunksize=1))
+        dt = time.perf_counter() - t0
+    return dec / dt, cores, dec, dt
+
+
 def cpu_baseline(args, c, caps):
     import oracle as O
     ce, cd, ca = caps
@@ -221,11 +247,15 @@ def cpu_baseline(args, c, caps):
     dm = time.perf_counter() - t1
     ns = O.num_splits(args.mdp_grid_step)
     mdp_all, mcores, mdone, mdt = oracle_mdp_all_cores(args)
+    ods_all, ocores, odec, odt = oracle_ods_all_cores(args, c, caps, max(10, done // 4))
     return dict(value=dec / dt, unit="decisions/s", cores=1, kind="oracle",
                 sample=f"oracle replay of the first {done} rounds ({dec} decisions, {dt:.1f} s) of the same "
                        f"workload (the ODS oracle is a sequential protocol: 1 core); MDP oracle 1,000 profiles x "
                        f"{ns} splits in {dm:.2f} s on 1 core, {mdone:,} profiles in {mdt:.2f} s on {mcores} cores",
                 mdp_value=1000 * ns / dm, mdp_unit="split-evals/s",
+                replicas_value_all_cores=ods_all, replicas_cores_all=ocores,
+                replicas_sample=f"{ocores} independent oracle replays (seed + k), {max(10, done // 4)} rounds each "
+                                f"({odec} decisions in {odt:.1f} s), one process per core",
                 mdp_value_all_cores=mdp_all, mdp_cores_all=mcores,
                 mdp_cores_note="processes launched = the affinity count; a CPU quota can leave fewer effective cores")
 
