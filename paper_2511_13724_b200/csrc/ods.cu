@@ -1279,9 +1279,22 @@ ods_rounds_x2(const __grid_constant__ Lays LS, const __grid_constant__ Cfg C, co
     ods_rounds_body<kTime, kCoupled>(LS, C, P);
 }
 
-// the round kernel for (two CTAs per SM, phase counters, coupled)
-const void* round_kernel(bool x2, bool timed, bool coupled) {
-    if (x2) {
+// 256 threads, one CTA per SM: independent jobs whose longest chain of rounds
+// has batches of <= 256 (each round is shorter with fewer, fuller warps)
+template <bool kTime, bool kCoupled>
+__global__ void __launch_bounds__(kThreads / 2, 1)
+ods_rounds_half(const __grid_constant__ Lays LS, const __grid_constant__ Cfg C, const __grid_constant__ Launch P) {
+    ods_rounds_body<kTime, kCoupled>(LS, C, P);
+}
+
+// the round kernel for (variant: 0 512 threads, 1 256 threads two CTAs per SM,
+// 2 256 threads one CTA per SM; phase counters; coupled)
+const void* round_kernel(int variant, bool timed, bool coupled) {
+    if (variant == 2) {
+        if (coupled) return timed ? (const void*)ods_rounds_half<true, true> : (const void*)ods_rounds_half<false, true>;
+        return timed ? (const void*)ods_rounds_half<true, false> : (const void*)ods_rounds_half<false, false>;
+    }
+    if (variant == 1) {
         if (coupled) return timed ? (const void*)ods_rounds_x2<true, true> : (const void*)ods_rounds_x2<false, true>;
         return timed ? (const void*)ods_rounds_x2<true, false> : (const void*)ods_rounds_x2<false, false>;
     }
@@ -1775,9 +1788,9 @@ extern "C" seneca_status seneca_init_cache(const seneca_cache_config* cfg, void*
     cudaGetDevice(&c->device);
 #define INIT_TRY(expr) do { cudaError_t _e = (expr); if (_e != cudaSuccess) { delete c; return cuda_status(_e, #expr); } } while (0)
     const bool coupled = z.C.cap_t > 0 || z.C.cold;
-    for (int x2 = 0; x2 < 2; ++x2)
+    for (int v = 0; v < 3; ++v)
         for (int tm = 0; tm < 2; ++tm)
-            INIT_TRY(cudaFuncSetAttribute(round_kernel(x2, tm, coupled), cudaFuncAttributeMaxDynamicSharedMemorySize,
+            INIT_TRY(cudaFuncSetAttribute(round_kernel(v, tm, coupled), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           200 * 1024));
     INIT_TRY(cudaFuncSetAttribute(ods_validate_requests, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
     {   // the cooperative round launch needs every replica's CTAs co-resident: one
@@ -1787,22 +1800,45 @@ extern "C" seneca_status seneca_init_cache(const seneca_cache_config* cfg, void*
         // (occupancy of the timed variants is checked too: a profiled replay
         // must fit the same co-resident grid)
         int per_sm_t = 0;
-        INIT_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, round_kernel(false, false, coupled), kThreads,
+        INIT_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, round_kernel(0, false, coupled), kThreads,
                                                                round_smem));
-        INIT_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_t, round_kernel(false, true, coupled), kThreads,
+        INIT_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_t, round_kernel(0, true, coupled), kThreads,
                                                                round_smem));
         per_sm = std::min(per_sm, per_sm_t);
         uint64_t slots = (uint64_t)per_sm * num_sms();
-        c->round_fn = round_kernel(false, false, coupled);
-        c->round_fn_timed = round_kernel(false, true, coupled);
+        c->round_fn = round_kernel(0, false, coupled);
+        c->round_fn_timed = round_kernel(0, true, coupled);
         c->round_threads = kThreads;
+        // independent jobs (no maintain coupling): the replay lasts as long as the job
+        // with the most rounds; when that job's batch fits 256 threads, 256-thread
+        // CTAs run its rounds faster (measured: OpenImages)
+        uint32_t jdom = 0;
+        uint64_t rdom = 0;
+        for (uint32_t jj = 0; jj < z.C.J; ++jj) {
+            const uint64_t rj = (uint64_t)z.C.target[jj] * ((z.C.N + z.C.batch[jj] - 1) / z.C.batch[jj]);
+            if (rj > rdom || (rj == rdom && z.C.batch[jj] > z.C.batch[jdom])) { rdom = rj; jdom = jj; }
+        }
+        if (!coupled && z.C.batch[jdom] <= kThreads / 2 && need <= slots) {
+            const size_t smemh = smem_for(kThreads / 2);
+            int per_smh = 0, per_smh_t = 0;
+            INIT_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_smh, round_kernel(2, false, coupled),
+                                                                   kThreads / 2, smemh));
+            INIT_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_smh_t, round_kernel(2, true, coupled),
+                                                                   kThreads / 2, smemh));
+            if (need <= (uint64_t)std::min(per_smh, per_smh_t) * num_sms()) {
+                c->round_fn = round_kernel(2, false, coupled);
+                c->round_fn_timed = round_kernel(2, true, coupled);
+                c->round_threads = kThreads / 2;
+                c->round_smem = smemh;
+            }
+        }
         if (need > slots) {
             const size_t smem2 = smem_for(kThreads / 2);
             int per_sm2 = 0;
             int per_sm2_t = 0;
-            INIT_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, round_kernel(true, false, coupled),
+            INIT_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, round_kernel(1, false, coupled),
                                                                    kThreads / 2, smem2));
-            INIT_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2_t, round_kernel(true, true, coupled),
+            INIT_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2_t, round_kernel(1, true, coupled),
                                                                    kThreads / 2, smem2));
             per_sm2 = std::min(per_sm2, per_sm2_t);
             const uint64_t slots2 = (uint64_t)per_sm2 * num_sms();
@@ -1812,8 +1848,8 @@ extern "C" seneca_status seneca_init_cache(const seneca_cache_config* cfg, void*
                 delete c;
                 return SENECA_EINVAL;
             }
-            c->round_fn = round_kernel(true, false, coupled);
-            c->round_fn_timed = round_kernel(true, true, coupled);
+            c->round_fn = round_kernel(1, false, coupled);
+            c->round_fn_timed = round_kernel(1, true, coupled);
             c->round_threads = kThreads / 2;
             c->round_smem = smem2;
         }
