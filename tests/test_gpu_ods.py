@@ -301,11 +301,13 @@ def test_replicas_match_independent_oracles(name, scale, R):
         compare_replica(o, g, k, tr[k])
 
 
-@pytest.mark.parametrize("name,split,R", [("imagenet22k", (100, 0, 0), 4), ("openimages", (52, 48, 0), 20)])
+@pytest.mark.parametrize("name,split,R", [("imagenet22k", (100, 0, 0), 4), ("openimages", (52, 48, 0), 8),
+                                          ("openimages", (52, 48, 0), 20)])
 def test_replicas_uncoupled(name, split, R):
     """Replicas of the uncoupled instantiation (no tracked tier: the paper's own
-    OpenImages / ImageNet-22K splits), including 20 x 9 CTAs (two 256-thread CTAs
-    per SM) -- each replica equals its independent oracle replay."""
+    OpenImages / ImageNet-22K splits): 512-thread CTAs (22K), 256-thread CTAs one
+    per SM (OpenImages x 8: its longest round chain has batch 128) and two per SM
+    (OpenImages x 20) -- each replica equals its independent oracle replay."""
     seed = 5
     c = synth.ods_config(name, scale=64, seed=seed)
     c["split"] = split
