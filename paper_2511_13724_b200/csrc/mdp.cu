@@ -37,6 +37,9 @@ constexpr int kMaxSteps = 101;  // grid step 1 % -> 101 values per coordinate
 #ifndef SENECA_MDP_FASTDIV
 #define SENECA_MDP_FASTDIV 1      // 0: capacity floors by the u64 division routine (A/B knob)
 #endif
+#ifndef SENECA_MDP_PARHDR
+#define SENECA_MDP_PARHDR 1       // 1: the header's divisions spread over lanes (two levels); 0: serial
+#endif
 #ifndef SENECA_MDP_MINB
 #define SENECA_MDP_MINB 3
 #endif
@@ -122,6 +125,64 @@ __device__ void tier_throughputs(const seneca_mdp_profile& p, double dsi[4], uin
     lim[0] = la; lim[1] = ld; lim[2] = le; lim[3] = ls;
 }
 
+// Eqs. 1-4 by one warp with the nine divisions spread over lanes in two
+// dependency levels (the same IEEE operations on the same operands as
+// tier_throughputs, so the same bits); every lane ends with the results.
+__device__ void tier_throughputs_warp(const seneca_mdp_profile& p, double dsi[4], uint8_t lim[4]) {
+    const uint32_t lane = threadIdx.x & 31;
+    const double Sd = u2d(p.s_data);
+    const uint64_t p_nw = p.comm_mapping ? p.gpus_per_node : p.nodes;                 // R-M1
+    const uint64_t p_pc = p.comm_mapping ? p.nodes : p.gpus_per_node;
+    const double nd = u2d(p.nodes);
+    const double nic = __dmul_rn(nd, p.b_nic);
+    const double pcie = __dmul_rn(nd, p.b_pcie);
+    const double gpu = __dmul_rn(nd, p.t_gpu);
+    // level 1: M x S_data, the two ring fractions 2(n-1)/n, B_cache/S_data, B_storage/S_data
+    double num = 1.0, den = 1.0;
+    if (lane == 0) { num = u2d((uint64_t)p.m_num * p.s_data); den = u2d(p.m_den); }
+    else if (lane == 1 && p_nw > 1) { num = u2d(2ull * (p_nw - 1ull)); den = u2d(p_nw); }
+    else if (lane == 2 && p_pc > 1) { num = u2d(2ull * (p_pc - 1ull)); den = u2d(p_pc); }
+    else if (lane == 3) { num = p.b_cache; den = Sd; }
+    else if (lane == 4) { num = p.b_storage; den = Sd; }
+    const double q1 = __ddiv_rn(num, den);
+    const double MS = __shfl_sync(0xffffffffu, q1, 0);
+    const double f_nw = __shfl_sync(0xffffffffu, q1, 1), f_pc = __shfl_sync(0xffffffffu, q1, 2);
+    const double e_cache = __shfl_sync(0xffffffffu, q1, 3), st = __shfl_sync(0xffffffffu, q1, 4);
+    const double C_nw = (p.nvlink_inter || p_nw <= 1) ? 0.0 : __dmul_rn(f_nw, p.model_bytes);
+    const double C_pc = (p.nvlink_intra || p.nvlink_inter || p_pc <= 1) ? 0.0 : __dmul_rn(f_pc, p.model_bytes);
+    // level 2: the cache, NIC and PCIe terms over M S_data, the NIC term over S_data
+    num = 1.0; den = 1.0;
+    if (lane == 0) { num = p.b_cache; den = MS; }
+    else if (lane == 1) { num = nic; den = __dadd_rn(MS, C_nw); }
+    else if (lane == 2) { num = pcie; den = __dadd_rn(MS, C_pc); }
+    else if (lane == 3) { num = nic; den = __dadd_rn(Sd, C_nw); }
+    const double q2 = __ddiv_rn(num, den);
+    const double cache_ms = __shfl_sync(0xffffffffu, q2, 0), nic_ms = __shfl_sync(0xffffffffu, q2, 1);
+    const double pcie_ms = __shfl_sync(0xffffffffu, q2, 2), e_nic = __shfl_sync(0xffffffffu, q2, 3);
+
+    double a = __longlong_as_double(0x7ff0000000000000ll); uint8_t la = 0xff;       // Eq. 1
+    take_min(cache_ms, L_CACHE, a, la);
+    take_min(nic_ms, L_NIC, a, la);
+    take_min(pcie_ms, L_PCIE, a, la);
+    take_min(gpu, L_GPU, a, la);
+    double d = __longlong_as_double(0x7ff0000000000000ll); uint8_t ld = 0xff;       // Eq. 2 (R-M4)
+    take_min(cache_ms, L_CACHE, d, ld);
+    take_min(nic_ms, L_NIC, d, ld);
+    take_min(__dmul_rn(nd, p.t_augment), L_CPU_AUG, d, ld);
+    take_min(pcie_ms, L_PCIE, d, ld);
+    take_min(gpu, L_GPU, d, ld);
+    double e = __longlong_as_double(0x7ff0000000000000ll); uint8_t le = 0xff;       // Eq. 3
+    take_min(e_cache, L_CACHE, e, le);
+    take_min(e_nic, L_NIC, e, le);
+    take_min(__dmul_rn(nd, p.t_decode_augment), L_CPU_DEC_AUG, e, le);
+    take_min(pcie_ms, L_PCIE, e, le);
+    take_min(gpu, L_GPU, e, le);
+    double s2 = e; uint8_t ls = le;                                                   // Eq. 4
+    if (st < e) { s2 = st; ls = L_STORAGE; }
+    dsi[0] = a; dsi[1] = d; dsi[2] = e; dsi[3] = s2;
+    lim[0] = la; lim[1] = ld; lim[2] = le; lim[3] = ls;
+}
+
 // One row per grid coordinate value k (p = k g %): the capacities clamped to N
 // (exact integers, Eqs. 5-7, R-M6) and the Eq. 9 terms that depend on a single
 // coordinate.  Array-of-rows so that one byte offset per coordinate addresses
@@ -163,7 +224,11 @@ __device__ void build_header(const seneca_mdp_profile* __restrict__ profiles, ui
     const bool ok = profile_valid(p);
     double dsi[4] = {0.0, 0.0, 0.0, 0.0};
     uint8_t lim[4] = {0, 0, 0, 0};
+#if SENECA_MDP_PARHDR
+    if (ok) tier_throughputs_warp(p, dsi, lim);                   // ok is warp-uniform
+#else
     if (ok) tier_throughputs(p, dsi, lim);
+#endif
     if (lane == 0) {
         H.valid = ok;
         for (int t = 0; t < 4; ++t) { H.dsi[t] = dsi[t]; H.lim[t] = lim[t]; }
