@@ -40,6 +40,9 @@ constexpr int kMaxSteps = 101;  // grid step 1 % -> 101 values per coordinate
 #ifndef SENECA_MDP_PARHDR
 #define SENECA_MDP_PARHDR 1       // 1: the header's divisions spread over lanes (two levels); 0: serial
 #endif
+#ifndef SENECA_MDP_REDUX
+#define SENECA_MDP_REDUX 1        // warp argmax by fmax butterfly + REDUX.MIN of the index (A/B knob)
+#endif
 #ifndef SENECA_MDP_MINB
 #define SENECA_MDP_MINB 3
 #endif
@@ -447,12 +450,24 @@ mdp_sweep_kernel(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_pro
                 }
             }
         }
+#if SENECA_MDP_REDUX
+        {   // warp argmax: the maximum by butterfly (values are finite or -inf, no NaN),
+            // then the smallest index among the lanes that hold it (REDUX.MIN) -- the
+            // same (max, first index) as the pairwise reduction
+            double m = best;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+            best_i = __reduce_min_sync(0xffffffffu, best == m ? best_i : 0xffffffffu);
+            best = m;
+        }
+#else
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             const double ov = __shfl_xor_sync(0xffffffffu, best, o);
             const uint32_t oi = __shfl_xor_sync(0xffffffffu, best_i, o);
             if (ov > best || (ov == best && oi < best_i)) { best = ov; best_i = oi; }
         }
+#endif
         if (lane == 0) { s_red_v[buf][w] = best; s_red_i[buf][w] = best_i; }
         __syncthreads();                                            // publishes next rows / headers, this reduction
         if (threadIdx.x == 0) {
