@@ -78,3 +78,19 @@ def test_pass_equivalent_matches_the_survey_sizes():
             assert pe["bytes_per_replay"] == 3 * 4 * words * jr + 4 * words * 40
         assert abs(pe["frac"] - pe["achieved"] / pe["peak"]) < 1e-12
         assert abs(pe["achieved"] - pe["bytes_per_replay"] / 1e9) < 1e-6
+
+
+def test_all_cores_oracle_baselines():
+    """bench.py's all-host-cores oracle figures: one process per core,
+    the MDP oracle on profile slices and independent ODS oracle replays (seed + k)."""
+    import types
+    sys.path.insert(0, ROOT)
+    import bench
+    import synth
+    args = types.SimpleNamespace(mdp_grid_step=10, evict_tiers=0)
+    v, cores, done, dt = bench.oracle_mdp_all_cores(args, per_core=20)
+    assert cores >= 1 and done == 20 * cores and v > 0 and dt > 0
+    c = synth.ods_config("toy", seed=synth.PERF_SEED)
+    v, cores, dec, dt = bench.oracle_ods_all_cores(args, c, bench.caps_of(c), 10)
+    assert dec == cores * 10 * sum(c["batch"])          # every replay plays 10 full rounds of both jobs
+    assert v > 0
