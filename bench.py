@@ -5,9 +5,12 @@
 A step = one pass of the whole hot path over one
 batch of synthetic input:
   * ODS: init_cache + the full trace-driven replay of the workload (default
-    BASELINE configs[1], the ImageNet-1K-shaped trace: 1,281,167 samples, 4 jobs
-    x 256, cache 35 % at split 0-48-52, 10 epochs = 50,050 rounds,
-    51.25 M sample decisions) -- the headline `value` (decisions/s);
+    BASELINE configs[3] on one GPU, the ImageNet-22K-shaped trace the north_star's
+    roofline target names: 14,197,122 samples, 8 jobs x 512, cache 400 GB at
+    split 100-0-0, 2 epochs = 55,458 rounds, 227.15 M sample decisions) -- the
+    headline `value` (decisions/s).  The ImageNet-1K and OpenImages traces
+    (configs[1], configs[2]) are timed in the same run under `workloads`, each
+    gated by its oracle golden;
   * MDP: the sweep over 10,000 synthetic hardware profiles x 5,151 splits (1 %
     grid, configs[4]) with the full grid written to HBM -- reported in `mdp`.
 
@@ -54,7 +57,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="imagenet1k", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="imagenet22k", choices=sorted(WORKLOADS))
+    ap.add_argument("--extra-workloads", default="imagenet1k,openimages",
+                    help="comma list of further workloads timed in the same run ('' : none)")
     ap.add_argument("--mdp-profiles", type=int, default=10_000)
     ap.add_argument("--mdp-grid-step", type=int, default=1)
     ap.add_argument("--mdp-large", type=int, default=100_000,
@@ -71,14 +76,25 @@ def parse():
 
 
 def dist_env():
-    from paper_2511_13724_b200 import dist as D
-    return D.env()
+    """(rank, world, local_rank) from the torchrun environment (read here, so the
+    reference arm imports nothing from the product package)."""
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def oracle_caps(c):
+    """The oracle's own capacities (Eqs. 5-7 in oracle/): every oracle leg uses these."""
+    import oracle as O
+    return tuple(O.config_capacities(c))
 
 
 def caps_of(c):
+    """The product's capacities (seneca_split_capacities), checked against the oracle's."""
     from paper_2511_13724_b200 import seneca as S
     caps = S.split_capacities(c["n_total"], c["s_data"], c["m_num"], c["m_den"], c["cache_bytes"], *c["split"])
-    return caps[0], caps[1], caps[2]
+    caps = (caps[0], caps[1], caps[2])
+    assert caps == oracle_caps(c), (caps, oracle_caps(c))
+    return caps
 
 
 def decisions_of(c):
@@ -148,7 +164,7 @@ def run_reference(args, rank, world):
         return 0
     import oracle as O
     c = synth.ods_config(args.workload, seed=synth.PERF_SEED)
-    ce, cd, ca = caps_of(c)
+    ce, cd, ca = oracle_caps(c)
     rounds_per_step = {"toy": 96, "imagenet1k": 800, "openimages": 500, "imagenet22k": 40}[args.workload]
     decisions = 0
     t_tot = 0.0
@@ -343,6 +359,123 @@ def roofline_for(name, k, info, hbm_peak, peak_src, traffic=None):
                 peak_source=peak_src)
 
 
+# --------------------------------------------------------------------------- latency floor of ods_rounds
+# Inputs measured on B200 (profiles/r1/microbench.md, tools/micro): a dependent
+# ld.global.cg chain costs 267-358 cycles per step (median ~300); one CTA issues
+# ~1 scattered global access (wavefront) per cycle; perm_apply (4 Philox-10 on
+# Z_a x Z_b) takes ~1,790 cycles per call with 512 threads.
+L2_DEP_CYCLES = 300
+PERM_CYCLES = 1790
+
+
+def latency_floor(c, caps, st, rounds, evicted, refilled, sm_mhz):
+    """Per-round floor of the round chain of one job CTA (DESIGN.md §7.1 "latency
+    roofline"): dependent L2 round trips x the measured dependent latency +
+    scattered global accesses at one per cycle + the substitution-rank ALU
+    chain (perm_apply) in rounds that substitute -- each summed per job-round
+    from the replay's own counters, averaged over job-rounds, and compared with
+    the measured microseconds per round of the whole replay (rounds run in
+    lock-step across jobs)."""
+    ce, cd, ca = caps
+    J = len(c["batch"])
+    N = c["n_total"]
+    tiers = (ce > 0) + (cd > 0) + (ca > 0)
+    job_rounds = sum(t * -(-N // b) for t, b in zip(c["target"], c["batch"]))
+    req = float(st["served"].sum())                        # delivered decisions = requests
+    hits = float(st["req_hits"].sum())
+    sub = st["subst"].sum(axis=(0, 1)).astype(float)       # by tier code S0 E1 D2 A3
+    subs = float(sub.sum())
+    a_served = float(st["served"][:, :, 3].sum())
+    # substituting job-rounds (not counted by the kernel): substitutes / mean misses
+    # per job-round -- a lower bound, since a substituting round replaces at most
+    # its misses (so the floor below stays a floor)
+    sub_rounds = min(job_rounds, subs / max(1.0, (req - hits) / job_rounds))
+    # walk: positions examined = first-lap positions + deferred re-requests (R-O1)
+    positions = req + subs
+    scattered = (positions / 4 + positions          # list vectors + per-position seen chunk copies
+                 + req * max(1, tiers)              # residency word gathers (classify)
+                 + req                              # seen RMW (respond)
+                 + hits + subs                      # pool block-count RMW
+                 + 2 * subs                         # 32-B count row (two 16-B loads)
+                 + 2 * sub[1] + 2 * sub[2] + 3 * sub[3]   # bitmap vectors of the selected block
+                 + subs                             # deferral-list store
+                 + 2 * a_served                     # consumer-set RMW + consumer-count RMW
+                 + J * 2 * refilled)                # refill intake: seen gather + count RMW per job
+    dep = job_rounds * 3 + 2 * sub_rounds           # walk prefetch wait, classify, respond RMW; + select
+    if ca > 0:
+        dep += job_rounds * 3                       # maintain: signal, eviction/refill apply, release
+    cyc = dep * L2_DEP_CYCLES + scattered + sub_rounds * PERM_CYCLES
+    floor_us = cyc / job_rounds / sm_mhz
+    return dict(floor_us_per_round=floor_us, cycles_per_job_round=cyc / job_rounds,
+                dependent_trips_per_job_round=dep / job_rounds, scattered_per_job_round=scattered / job_rounds,
+                substituting_job_round_share=sub_rounds / job_rounds,
+                inputs=dict(l2_dependent_cycles=L2_DEP_CYCLES, perm_apply_cycles=PERM_CYCLES,
+                            scattered_per_cycle=1, sm_mhz=sm_mhz, source="profiles/r1/microbench.md"))
+
+
+def golden_gate(name, seed, evict_tiers, st_raw, evicted=None, refilled=None):
+    """Per job-epoch counters + digests (and eviction/refill totals) of a full replay
+    against the oracle's golden file (tests/golden/, written by oracle/ only)."""
+    path = os.path.join(ROOT, "tests", "golden", f"oracle_{name}_seed{seed}{'_evictall' if evict_tiers else ''}.json")
+    if not os.path.exists(path):
+        return "no golden for this seed"
+    gold = json.load(open(path))
+    ok = all(int(st_raw[j, e]["digest"]) == int(s_["digest"]) and
+             [int(x) for x in st_raw[j, e]["served"]] == s_["served"] and
+             [int(x) for x in st_raw[j, e]["subst"]] == s_["subst"]
+             for j, row in enumerate(gold["stats"]) for e, s_ in enumerate(row))
+    if evicted is not None:
+        ok = ok and (evicted, refilled) == (gold["evicted"], gold["refilled"])
+    return "bit-exact" if ok else "MISMATCH"
+
+
+def prefix_gate(c, seed, replicas, ks, rounds, evict_tiers, stream):
+    """The launch configuration bench.py times (same workload, same replica count,
+    hence the same kernel variant and grid), replayed for `rounds` rounds; replica
+    k's residency/seen/consumer bitmaps and counters vs an oracle replay of seed + k
+    (oracle capacities) for the same rounds.  Returns {k: bool}."""
+    import torch
+    import oracle as O
+    import paper_2511_13724_b200 as P
+    ce, cd, ca = caps_of(c)
+    oc = oracle_caps(c)
+    g = P.ODSContext(c["n_total"], c["batch"], c["target"], ce, cd, ca, seed, replicas=replicas,
+                     evict_tiers=evict_tiers, stream=stream)
+    g.replay_rounds(rounds)
+    torch.cuda.synchronize()
+    g.sync()
+    out = {}
+    for k in ks:
+        o = O.ODS(c["n_total"], c["batch"], c["target"], *oc, (seed + k) & 0xFFFFFFFFFFFFFFFF,
+                  evict_all=bool(evict_tiers))
+        o.replay_rounds(rounds)
+        st_o, ev_o, rf_o = o.stats()
+        st_g, ev_g, rf_g = g.stats(k)
+        ok = st_g.tobytes() == st_o.tobytes() and (ev_g, rf_g) == (ev_o, rf_o)
+        if ok:
+            for a, b in zip(g.state(k), o.state()):
+                ok = ok and np.array_equal(a, b)
+        out[k] = bool(ok)
+        del o
+    g.close()
+    return out
+
+
+PREFIX_ROUNDS = {"toy": 96, "imagenet1k": 256, "openimages": 200, "imagenet22k": 48}
+
+
+def read_stats(S, ws, ctx, c, k=0):
+    v = S.read_state(ctx)
+    nst = len(c["batch"]) * v.max_target * S.STATS_DTYPE.itemsize
+    off = v.d_stats + k * v.replica_stride - ws.data_ptr()
+    st = ws[off:off + nst].cpu().numpy().view(S.STATS_DTYPE).reshape(len(c["batch"]), v.max_target).copy()
+    o_ev = v.d_evicted + k * v.replica_stride - ws.data_ptr()
+    o_rf = v.d_refilled + k * v.replica_stride - ws.data_ptr()
+    ev = int(ws[o_ev:o_ev + 8].cpu().numpy().view(np.uint64)[0])
+    rf = int(ws[o_rf:o_rf + 8].cpu().numpy().view(np.uint64)[0])
+    return st, ev, rf
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
@@ -350,8 +483,8 @@ def main():
         return run_reference(args, rank, world)
 
     import torch
-    import paper_2511_13724_b200 as P
     from paper_2511_13724_b200 import seneca as S
+    from paper_2511_13724_b200 import dist as D
 
     # One process per GPU over NCCL.  SENECA_DIST_BACKEND=gloo (test only) runs the
     # multi-rank host logic with several ranks sharing the GPUs there are
@@ -369,14 +502,14 @@ def main():
     red_dev = dev if backend == "nccl" else None
     stream = torch.cuda.current_stream(dev)
 
-    from paper_2511_13724_b200 import dist as D
-    c = synth.ods_config(args.workload, seed=D.rank_seed(synth.PERF_SEED, rank))
+    seed = D.rank_seed(synth.PERF_SEED, rank)
+    c = synth.ods_config(args.workload, seed=seed)
     caps = caps_of(c)
     ce, cd, ca = caps
     dec_per_step = decisions_of(c)
 
     # ---- inputs resident in HBM before timing
-    mdp_cols = synth.mdp_profiles(args.mdp_profiles, seed=D.rank_seed(synth.PERF_SEED, rank))
+    mdp_cols = synth.mdp_profiles(args.mdp_profiles, seed=seed)
     prof_host = S.profiles_from_columns(mdp_cols)
     d_prof = torch.from_numpy(prof_host.view(np.uint8).copy()).to(dev)
     nsplit = S.mdp_num_splits(args.mdp_grid_step)
@@ -444,23 +577,15 @@ def main():
     # ---- parity gates (outside the timed region)
     parity = {}
     S.sync_status(last_ctx, stream)
-    gold_path = os.path.join(ROOT, "tests", "golden", f"oracle_{args.workload}_seed{c['seed']}"
-                             f"{'_evictall' if args.evict_tiers else ''}.json")
-    st_raw = None
     v = S.read_state(last_ctx)
-    off = v.d_stats - ws.data_ptr()
-    st_raw = ws[off:off + len(c["batch"]) * v.max_target * S.STATS_DTYPE.itemsize].cpu().numpy().view(S.STATS_DTYPE)
-    st_raw = st_raw.reshape(len(c["batch"]), v.max_target)
-    served_ok = bool(np.all(st_raw["served"].sum(axis=2) == c["n_total"]))
-    parity["ods_served_per_job_epoch_equals_N"] = served_ok
-    if os.path.exists(gold_path):
-        gold = json.load(open(gold_path))
-        ok = all(int(st_raw[j, e]["digest"]) == int(s_["digest"]) and
-                 [int(x) for x in st_raw[j, e]["served"]] == s_["served"]
-                 for j, row in enumerate(gold["stats"]) for e, s_ in enumerate(row))
-        parity["ods_vs_oracle_golden"] = "bit-exact" if ok else "MISMATCH"
-    else:
-        parity["ods_vs_oracle_golden"] = "no golden for this seed (rank>0 or not generated)"
+    st_raw, ev_tot, rf_tot = read_stats(S, ws, last_ctx, c)
+    parity["ods_served_per_job_epoch_equals_N"] = bool(np.all(st_raw["served"].sum(axis=2) == c["n_total"]))
+    parity["ods_vs_oracle_golden"] = golden_gate(args.workload, c["seed"], args.evict_tiers, st_raw, ev_tot, rf_tot)
+    if parity["ods_vs_oracle_golden"] == "no golden for this seed":
+        # rank > 0 (seed + rank): the same launch configuration for a prefix of
+        # rounds against an oracle replay of this rank's seed
+        pg = prefix_gate(c, c["seed"], 1, [0], PREFIX_ROUNDS[args.workload], args.evict_tiers, stream)
+        parity["ods_vs_oracle_prefix"] = "bit-exact" if pg[0] else "MISMATCH"
     try:
         import oracle as O
         k = min(200, args.mdp_profiles)
@@ -483,7 +608,7 @@ def main():
     if args.mdp_large > 0 and not args.no_grid:
         import oracle as O
         nl = args.mdp_large
-        cols_l = synth.mdp_profiles(nl, seed=D.rank_seed(synth.PERF_SEED, rank) + 1)
+        cols_l = synth.mdp_profiles(nl, seed=seed + 1)
         d_prof_l = torch.from_numpy(S.profiles_from_columns(cols_l).view(np.uint8).copy()).to(dev)
         d_res_l = torch.empty(nl * S.RESULT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
         d_grid_l = torch.empty((nl, nsplit), dtype=torch.float64, device=dev)
@@ -514,10 +639,54 @@ def main():
                          parity="bit-exact (first and last 50 profiles, results and grid rows)" if ok else "MISMATCH")
         del d_prof_l, d_res_l, d_grid_l
 
+    # ---- the other ODS workloads of BASELINE.json, timed the same way (init_cache +
+    #      full replay, L2 flushed, one warm-up), each gated by its oracle golden
+    extra = {}
+    for name in [w for w in args.extra_workloads.split(",") if w and w != args.workload]:
+        cx = synth.ods_config(name, seed=seed)
+        cex, cdx, cax = caps_of(cx)
+        cfgx = S.make_config(cx["n_total"], cx["batch"], cx["target"], cex, cdx, cax, cx["seed"],
+                             evict_tiers=args.evict_tiers)
+        wbx = S.state_bytes(cfgx)
+        wsx = torch.empty(wbx, dtype=torch.uint8, device=dev)
+        msx, ctxx, rx = [], None, 0
+        for s in range(1 + args.steps):
+            flush.fill_(s & 0xFF)
+            barrier()
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ctxx = S.init_cache(cfgx, wsx, wbx, stream)
+            rx = S.replay_epochs(ctxx, max(cx["target"]), None, stream)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            barrier()
+            if s >= 1:
+                msx.append(e0.elapsed_time(e1))
+            if s < args.steps:
+                S.destroy(ctxx)
+        S.sync_status(ctxx, stream)
+        stx, evx, rfx = read_stats(S, wsx, ctxx, cx)
+        gate = golden_gate(name, cx["seed"], args.evict_tiers, stx, evx, rfx)
+        if gate == "no golden for this seed":
+            pg = prefix_gate(cx, cx["seed"], 1, [0], PREFIX_ROUNDS[name], args.evict_tiers, stream)
+            gate = "bit-exact (oracle prefix)" if pg[0] else "MISMATCH"
+        S.destroy(ctxx)
+        del wsx
+        (sx,) = D.reduce_times([sum(msx) / 1e3], device=red_dev)
+        decx = decisions_of(cx)
+        extra[name] = dict(value=decx * args.steps * world / sx, unit="decisions/s", ms_per_step=1e3 * sx / args.steps,
+                           rounds=rx, us_per_round=1e3 * sx / args.steps / rx * 1e3,
+                           config=workload_config(cx, name, dict(rounds_per_step=rx, decisions_per_step=decx)),
+                           parity=gate)
+
     # ---- R independent replays in one context (untimed warm-up, then timed steps).
     #      Candidates: the most replicas with one 512-thread round CTA per SM, and
     #      with two 256-thread CTAs per SM (the library picks the kernel variant);
-    #      the line reports the faster, both are listed.
+    #      the line reports the faster, both are listed.  Gates: replica 0 (seed =
+    #      the golden's at rank 0) digests vs the oracle golden; replicas 1 and 2 of
+    #      the same launch configuration vs oracle replays of seed + 1, seed + 2 for a
+    #      prefix of rounds.
     rep_line = None
     if args.replicas != 0:
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
@@ -548,29 +717,33 @@ def main():
                 if s < args.steps:
                     S.destroy(rctx)
             S.sync_status(rctx, stream)
-            rv = S.read_state(rctx)
             served_all = True
-            nst1 = len(c["batch"]) * rv.max_target * S.STATS_DTYPE.itemsize
             for k in range(R):
-                o = rv.d_stats + k * rv.replica_stride - ws_r.data_ptr()
-                stk = ws_r[o:o + nst1].cpu().numpy().view(S.STATS_DTYPE).reshape(len(c["batch"]), rv.max_target)
+                stk, _, _ = read_stats(S, ws_r, rctx, c, k)
                 served_all &= bool(np.all(stk["served"].sum(axis=2) == c["n_total"]))
+            st0, ev0, rf0 = read_stats(S, ws_r, rctx, c, 0)
+            gate0 = golden_gate(args.workload, rseed, args.evict_tiers, st0, ev0, rf0)
             S.destroy(rctx)
             del ws_r
+            gates = prefix_gate(c, rseed, R, [1, 2] if R > 2 else list(range(R)), PREFIX_ROUNDS[args.workload],
+                                args.evict_tiers, stream)
             (rep_s,) = D.reduce_times([sum(rep_ms) / 1e3], device=red_dev)
             tried.append(dict(R=R, value=R * dec_per_step * args.steps * world / rep_s, unit="decisions/s",
                               ms_per_step=1e3 * rep_s / args.steps,
                               per_replica_value=dec_per_step * args.steps / rep_s,
                               round_ctas=R * J1, ctas_per_sm=1 if R * J1 <= sms else 2,
-                              launches_per_step=launches_rep, served_ok=served_all))
+                              launches_per_step=launches_rep, served_ok=served_all,
+                              parity=dict(replica0_vs_oracle_golden=gate0,
+                                          **{f"replica{k}_vs_oracle_first_{PREFIX_ROUNDS[args.workload]}_rounds":
+                                             "bit-exact" if ok else "MISMATCH" for k, ok in gates.items()})))
         best = max(tried, key=lambda t: t["value"])
         rep_line = dict(best, seeds=f"{hex(rseed)} + k, k < R",
-                        candidates=[{k: t[k] for k in ("R", "value", "per_replica_value", "ctas_per_sm")}
+                        candidates=[{k: t[k] for k in ("R", "value", "per_replica_value", "ctas_per_sm", "parity")}
                                     for t in tried],
-                        parity=dict(every_replica_served_each_sample_once_per_job_epoch=all(t["served_ok"] for t in tried),
-                                    note="replica-vs-oracle bit-exactness: tests/test_gpu_ods.py::test_replicas_*"),
                         note="init_cache + replay_epochs of R independent instances of the workload in one "
                              "context (one cooperative launch); L2 flushed between steps")
+        rep_line["parity"] = dict(best["parity"],
+                                  every_replica_served_each_sample_once_per_job_epoch=all(t["served_ok"] for t in tried))
         rep_line.pop("served_ok", None)
 
     # ---- e2e through the public API with host buffers (pinned), copies inside
@@ -631,6 +804,9 @@ def main():
     ods_s, mdp_s, e2e_s, e2e_m = D.reduce_times([ods_s, mdp_s, e2e_s, e2e_m], device=red_dev)   # max over ranks
     total_dec = dec_per_step * args.steps * world
     total_evals = args.mdp_profiles * nsplit * args.steps * world
+    parity_ok = [1.0 if all(str(x).startswith("bit-exact") or x is True for x in parity.values()) else 0.0]
+    (parity_all,) = D.reduce_sum(parity_ok, device=red_dev)
+    parity["all_ranks_bit_exact"] = f"{int(parity_all)}/{world}"
 
     # ---- roofline of the dominant kernel (sampled CUDA-event durations)
     peaks = {}
@@ -657,22 +833,30 @@ def main():
                 superblocks=(c["n_total"] + 32767) // 32768, jobs=len(c["batch"]), n_total=c["n_total"],
                 rounds=rounds_tot / args.steps, decisions=dec_per_step,
                 substitutes=int(st_raw["subst"].sum()), a_served=int(st_raw["served"][:, :, 3].sum()),
-                refilled=int(ws[v.d_refilled - ws.data_ptr():v.d_refilled - ws.data_ptr() + 8].cpu().numpy().view(np.uint64)[0]),
-                cache_entries=ce + cd + ca, mdp_profiles=args.mdp_profiles, mdp_splits=nsplit,
-                job_epochs=sum(c["target"]),
-                mdp_grid=d_grid is not None)
+                refilled=rf_tot, cache_entries=ce + cd + ca, mdp_profiles=args.mdp_profiles, mdp_splits=nsplit,
+                job_epochs=sum(c["target"]), mdp_grid=d_grid is not None)
     tkey = {"ods_rounds": f"ods_rounds@{args.workload}{'-evictall' if args.evict_tiers else ''}",
             "mdp_sweep": f"mdp_sweep@{args.mdp_profiles}x{nsplit}{'' if d_grid is not None else '-nogrid'}"}
     roof = roofline_for(dom, kernels[dom], info, hbm_peak, peak_src, ncu_traffic(tkey.get(dom, dom)))
+    if dom == "ods_rounds":
+        sm_mhz = clk.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
+        lf = latency_floor(c, caps, st_raw, rounds_tot / args.steps, ev_tot, rf_tot, sm_mhz)
+        ach_us = kernels["ods_rounds"]["avg_us"] / (rounds_tot / args.steps) if kernels["ods_rounds"]["avg_us"] else \
+            1e6 * ods_s / args.steps / (rounds_tot / args.steps)
+        roof["latency"] = dict(bound="latency (dependent round chain on one SM per job)",
+                               achieved_us_per_round=ach_us, frac=lf["floor_us_per_round"] / ach_us, **lf,
+                               note="frac = floor / achieved; the HBM fraction above counts the method's own "
+                                    "bytes (DESIGN.md 7.1)")
     mdp_roof = roofline_for("mdp_sweep", kernels["mdp_sweep"], info, hbm_peak, peak_src,
                             ncu_traffic(tkey["mdp_sweep"]))
     for name in kernels:
         kernels[name]["algorithmic_bytes_per_launch"] = algorithmic_bytes(name, info)
 
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args, synth.ods_config(args.workload, seed=synth.PERF_SEED),
+                           oracle_caps(synth.ods_config(args.workload, seed=synth.PERF_SEED)))
     if rank == 0:
-        cpu = None
-        if world == 1 and not args.no_cpu_baseline:
-            cpu = cpu_baseline(args, synth.ods_config(args.workload, seed=synth.PERF_SEED), caps)
         ms_per_step = 1e3 * (ods_s + mdp_s) / args.steps
         line = dict(
             metric=METRIC, value=total_dec / ods_s, unit="decisions/s", n_gpus=world, steps=args.steps,
@@ -680,6 +864,7 @@ def main():
             vs_baseline=None, dtype="u32", data="synthetic",
             config=workload_config(c, args.workload, dict(
                 rounds_per_step=rounds_tot // args.steps, decisions_per_step=dec_per_step,
+                us_per_round=1e6 * ods_s / args.steps / (rounds_tot / args.steps),
                 evict_tiers="all" if args.evict_tiers else "A",
                 mdp_profiles=args.mdp_profiles, mdp_grid_step_pct=args.mdp_grid_step,
                 mdp_grid_written=d_grid is not None,
@@ -691,7 +876,10 @@ def main():
                      note="public API from Python: init_cache + replay_epochs + stats D2H; MDP profiles "
                           "H2D from pinned memory + sweep + results D2H; host wall clock"),
             roofline=roof,
-            pass_equivalent=pass_equivalent(c, caps, v.words, ods_s, args.steps, world, hbm_peak, rep_line),
+            pass_equivalent=dict(pass_equivalent(c, caps, v.words, ods_s, args.steps, world, hbm_peak, rep_line),
+                                 caveat="NOT a roofline: bytes a pass-based design would stream, which this "
+                                        "kernel never moves; see roofline (own bytes) and roofline.latency"),
+            workloads=extra,
             mdp=dict(value=total_evals / mdp_s, unit="split-evals/s", dtype="f64", ms_per_step=mdp_ms_step,
                      roofline=mdp_roof, large=mdp_large,
                      fp64=dict(flops_per_split=11, achieved_tflops=total_evals * 11 / mdp_s / 1e12,

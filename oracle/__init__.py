@@ -90,6 +90,7 @@ def _declare(L):
     L.oracle_splitmix64.argtypes = [C.c_uint64]; L.oracle_splitmix64.restype = C.c_uint64
     L.oracle_key.argtypes = [C.c_uint64] * 5; L.oracle_key.restype = C.c_uint64
     L.oracle_perm.argtypes = [C.c_uint64] * 3; L.oracle_perm.restype = C.c_uint64
+    L.oracle_perm_block.argtypes = [C.c_uint64] * 4 + [u32p]; L.oracle_perm_block.restype = None
     L.oracle_comm_overhead.argtypes = [C.c_uint64, C.c_double]; L.oracle_comm_overhead.restype = C.c_double
     L.oracle_tiers.argtypes = [C.POINTER(Profile), C.POINTER(C.c_double), C.POINTER(C.c_uint8)]
     L.oracle_split_counts.argtypes = [C.POINTER(Profile), C.c_uint32, C.c_uint32, C.c_uint32, u64p]
@@ -143,6 +144,14 @@ def perm(K: int, n: int, x: int) -> int:
     return lib().oracle_perm(K, n, x)
 
 
+def perm_block(K: int, n: int, x0: int = 0, count: int | None = None) -> np.ndarray:
+    """[perm(K, n, x) for x in x0 .. x0 + count - 1] as uint32 (default: all of [0, n))."""
+    count = n - x0 if count is None else count
+    out = np.zeros(count, np.uint32)
+    lib().oracle_perm_block(K, n, x0, count, out)
+    return out
+
+
 # --------------------------------------------------------------------------- MDP
 def make_profile(**kw) -> Profile:
     p = Profile()
@@ -182,6 +191,22 @@ def split_counts(p: Profile, pe, pd, pa):
     out = np.zeros(4, np.uint64)
     lib().oracle_split_counts(C.byref(p), pe, pd, pa, out)
     return [int(x) for x in out]
+
+
+def capacities(n_total, s_data, m_num, m_den, cache_bytes, pe, pd, pa):
+    """(cap_E, cap_D, cap_A) of a split (Eqs. 5-7, exact floors R-M6),
+    computed by the oracle's own split_counts: the capacities every oracle call
+    site uses (never the product's)."""
+    p = make_profile(t_gpu=1, t_decode_augment=1, t_augment=1, b_nic=1, b_pcie=1, b_cache=1, b_storage=1,
+                     cache_bytes=int(cache_bytes), n_total=int(n_total), s_data=int(s_data),
+                     m_num=int(m_num), m_den=int(m_den), nodes=1, gpus_per_node=1)
+    na, nd, ne, _ = split_counts(p, int(pe), int(pd), int(pa))
+    return ne, nd, na
+
+
+def config_capacities(c: dict):
+    """capacities() of a synth.ods_config workload description."""
+    return capacities(c["n_total"], c["s_data"], c["m_num"], c["m_den"], c["cache_bytes"], *c["split"])
 
 
 def model_eval(p: Profile, pe, pd, pa):

@@ -4,9 +4,12 @@
 // (DESIGN.md §3).  A round is one batch for each listed job, then maintain.
 //
 // Execution:
-//   ods_perm_all      side stream, at init: every (job, epoch) permutation
-//                     pi_j,e(pos) = perm(key(seed, REQ, j, e), N, pos) (R-O3),
-//                     epoch-major, publishing a ready flag per (job, epoch).
+//   ods_perm_all      the (job, epoch) permutations pi_j,e(pos) =
+//                     perm(key(seed, REQ, j, e), N, pos) (R-O3) into a ring of
+//                     K = min(max epochs, 2) slots per job (epoch e in slot e % K),
+//                     publishing a ready flag per (job, epoch); the host fills the
+//                     ring ahead of each round launch and bounds the launch so no
+//                     job enters an epoch that has no slot yet (launch_rounds).
 //   ods_rounds        ONE cooperative launch runs R rounds.  CTA x < J owns job
 //                     x; CTA J is the maintain CTA.  Per round:
 //       job CTAs      classify (a3) -> select (a4, a5) -> finish (a6, a8)
@@ -76,6 +79,7 @@ struct JobDev {           // per-job persistent walk state (workspace)
 struct Cfg {
     uint32_t N, NW, NB, NS, NBp;     // samples, words/bitmap, blocks, superblocks, padded blocks
     uint32_t J, Bmax, maxT, cap_a, cap_d, cap_e;
+    uint32_t K;                      // permutation ring slots per job: min(maxT, 2), a power of two
     uint32_t evict_all;              // evict_tiers = ALL (R-O21): every cached tier is tracked
     uint32_t cap_t;                  // capacity of the tracked tiers (cap_a, or cap_a + cap_d + cap_e; 0 baseline)
     uint32_t baseline;               // the uniform no-evict sampler (R-O22): no substitution, static tiers
@@ -95,10 +99,13 @@ struct Lay {
     uint32_t *cnt_sup;               // [3J+1][NS] superblock counts (kept in shared memory while running)
     uint32_t *cnt_tot;               // [3J+1]
     uint32_t *tsize;                 // [4] tier sizes by tier code (E 1, D 2, A 3)
-    uint32_t *perms;                 // [J][maxT][N]
+    uint32_t *perms;                 // [J][K][Nrow] ring: epoch e of job j in slot e % K
     uint32_t *laps;                  // [J][2][N]
     uint32_t *perm_ready;            // [J][maxT]
     uint32_t *perm_done;             // [J][maxT] positions finished
+    uint32_t *epoch_at;              // [J] epoch job j plays (published at each epoch start, release):
+                                     //     the concurrent ring generator refills slot e % K once it is >= e - K + 1
+    uint32_t *gen_next;              // [1] work counter of the concurrent ring generator
     JobDev *jobs;                    // [J]
     uint32_t *out_ids;               // [J][Bmax] replay scratch
     uint8_t *out_src;                // [J][Bmax]
@@ -114,9 +121,10 @@ struct Lay {
     uint32_t *claim;                 // [NW] admission de-duplication scratch (all zero between rounds)
     seneca_job_epoch_stats *stats;   // [J][maxT]
     unsigned long long *evicted, *refilled;
-    uint32_t *err;
+    uint32_t *err;                   // latched consistency flags (control block, see kCtlBytes)
+    uint32_t *verr;                  // caller-supplied request validation flag (control block)
     uint32_t *bar;                   // [4] signals: u64 {job phases done | evictions pushed << 32},
-                                     //     maintain rounds applied, eviction ring position
+                                     //     maintain rounds applied, eviction ring position (control block)
     unsigned long long *phase;       // [32] accumulated cycles per phase (see seneca.h)
     uint64_t seed;                   // this replica's seed (cfg seed + replica index)
 };
@@ -327,7 +335,8 @@ struct JobSmem {
 };
 
 __device__ __forceinline__ const uint32_t* list_ptr(const Lay& L, const Cfg& C, uint32_t j, uint32_t e, uint32_t buf) {
-    return buf == 0 ? L.perms + ((size_t)j * C.maxT + e) * C.Nrow : L.laps + ((size_t)j * 2 + (buf - 1)) * C.Nrow;
+    return buf == 0 ? L.perms + ((size_t)j * C.K + (e & (C.K - 1))) * C.Nrow
+                    : L.laps + ((size_t)j * 2 + (buf - 1)) * C.Nrow;
 }
 
 // Stage 1 (right after a walk): the next walk window of the current list into
@@ -378,9 +387,11 @@ __device__ void job_walk(const Lay& L, const Cfg& C, JobSmem& S, uint32_t* s_req
     unsigned long long* iters = TM.on ? &TM.acc[7] : nullptr;
     const uint32_t tid = threadIdx.x, T = blockDim.x;
     const uint32_t* seen_j = L.seen + (size_t)j * C.NW;
-    if (tid == 0) { S.wrap_slot = 0; S.need = need; }
-    if (S.cur_buf == 0 && S.perm_seen != e + 1) {   // the epoch's permutation must be published
-        if (tid == 0) {
+    // (thread 0 alone reads and writes the walk bookkeeping here; everyone reads it
+    // after the barrier -- compute-sanitizer racecheck)
+    if (tid == 0) {
+        S.wrap_slot = 0; S.need = need;
+        if (S.cur_buf == 0 && S.perm_seen != e + 1) {   // the epoch's permutation must be published
             const uint32_t* f = L.perm_ready + (size_t)j * C.maxT + e;
             while (ld_acquire(f) == 0) { }
             S.perm_seen = e + 1;
@@ -391,10 +402,11 @@ __device__ void job_walk(const Lay& L, const Cfg& C, JobSmem& S, uint32_t* s_req
     bool wrapped = false;
     if (pf && S.pf_state != 0) {
         // first step from the prefetched window and its prefetched seen chunks
-        cp_async_wait_all();
-        __syncthreads();
+        // (the bookkeeping is read before the barrier: thread 0 resets pf_state below)
         const bool usable = S.pf_state == 2 && S.pf_buf == S.cur_buf && S.pf_epoch == e &&
                             S.cursor >= S.pf_base && S.cursor < S.pf_base + S.pf_vlen;
+        cp_async_wait_all();
+        __syncthreads();
         if (usable) {
             const uint32_t cursor = S.cursor, wend = S.pf_base + S.pf_vlen;
             if (iters && tid == 0) *iters += 1;
@@ -445,8 +457,13 @@ __device__ void job_walk(const Lay& L, const Cfg& C, JobSmem& S, uint32_t* s_req
     }
     while (taken < need) {
         if (S.cursor >= S.cur_len) {
+            // read by every thread before the barrier: thread 0 rewrites the lap
+            // bookkeeping after it (a read after it raced with that write -- found by
+            // compute-sanitizer racecheck/synccheck: a thread could take the error
+            // exit alone and leave the block's barriers unmatched)
+            const bool dead = wrapped || S.nxt_len == 0;
             __syncthreads();
-            if (wrapped || S.nxt_len == 0) {
+            if (dead) {
                 if (tid == 0) atomicOr(L.err, 2u);
                 break;
             }
@@ -1213,7 +1230,13 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
                         S.cur_buf = 0; S.nxt_buf = 1; S.cursor = 0; S.cur_len = C.N; S.nxt_len = 0;
                         S.recount = 1;
                     }
+                    // epoch e is over: no read of its ring slot is in flight any more (the
+                    // prefetched window copies of this CTA are drained), so the slot may be
+                    // refilled with epoch e + K by the concurrent generator
+                    cp_async_wait_all();
                     __syncthreads();
+                    if (tid == 0) { __threadfence(); atomicExch(L.epoch_at + j, s_e[j] + 1); }
+                    if (tid == 0) S.pf_state = 0;
                 }
                 if (coupled && tid == 0) {                 // job phase done (+ evictions pushed)
                     __threadfence();
@@ -1303,21 +1326,78 @@ const void* round_kernel(int variant, bool timed, bool coupled) {
 }
 
 // ------------------------------------------------------------------ one-off kernels
-// pi_j,e for every (job, epoch), epoch-major, in chunks; the CTA finishing the
-// last chunk of (j, e) publishes perm_ready[j][e] (release).
-__global__ void ods_perm_all(const __grid_constant__ Lays LS, const __grid_constant__ Cfg C, uint32_t chunk) {
+// The (job, epoch) pairs one generator launch fills, in the order given
+// (epoch-major, so the earliest needed permutations complete first).
+struct PermWork {
+    uint32_t n;
+    uint32_t j[2 * kMaxJobs], e[2 * kMaxJobs];
+};
+
+// The epochs a single-replica launch's jobs enter during the launch, in the
+// order their ring slots free (refilled concurrently by ods_perm_ring).
+constexpr uint32_t kRingPairs = 1024;
+struct PermRing {
+    uint32_t n;
+    uint32_t j[kRingPairs], e[kRingPairs];
+};
+
+// pi_j,e for the listed (job, epoch) pairs, in chunks, into ring slot e % K; the
+// CTA finishing the last chunk of (j, e) publishes perm_ready[j][e] (release).
+__global__ void ods_perm_all(const __grid_constant__ Lays LS, const __grid_constant__ Cfg C,
+                             const __grid_constant__ PermWork W, uint32_t chunk) {
     const Lay& L = LS.r[blockIdx.y];
     const uint32_t per = (C.N + chunk - 1) / chunk;
-    const uint64_t total = (uint64_t)C.maxT * C.J * per;
+    const uint64_t total = (uint64_t)W.n * per;
     const PermDomain dom = perm_domain(C.N);
     __shared__ uint32_t s_last;
     for (uint64_t c = blockIdx.x; c < total; c += gridDim.x) {
-        const uint32_t e = (uint32_t)(c / ((uint64_t)C.J * per));
-        const uint32_t j = (uint32_t)((c / per) % C.J);
+        const uint32_t pair = (uint32_t)(c / per);
+        const uint32_t e = W.e[pair], j = W.j[pair];
         const uint32_t part = (uint32_t)(c % per);
-        if (e >= C.target[j]) continue;
         const uint64_t key = derive_key(L.seed, PUR_REQ, j, e, 0);
-        uint32_t* out = L.perms + ((size_t)j * C.maxT + e) * C.Nrow;
+        uint32_t* out = L.perms + ((size_t)j * C.K + (e & (C.K - 1))) * C.Nrow;
+        const uint32_t lo = part * chunk, hi = min(lo + chunk, C.N);
+        for (uint32_t pos = lo + threadIdx.x; pos < hi; pos += blockDim.x) out[pos] = perm_apply(key, dom, pos);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            const uint32_t old = atomicAdd(L.perm_done + (size_t)j * C.maxT + e, hi - lo);
+            s_last = old + (hi - lo) == C.N;
+            if (s_last) {
+                __threadfence();
+                atomicExch(L.perm_ready + (size_t)j * C.maxT + e, 1u);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// The ring generator that runs CONCURRENTLY with a single-replica round launch
+// (side stream): it refills slot e % K with epoch e of job j as soon as job j has
+// started epoch e - K + 1 (epoch_at, released by the job CTA at its epoch
+// reset), so no launch has to stop at an epoch boundary.  Work items (pair,
+// chunk) are taken in the given order (pairs sorted by the round their slot
+// frees), one 16 K-position chunk per CTA at a time; the waiting CTA sleeps.
+// The host sizes its grid so the round launch's J + 1 CTAs always fit beside it.
+__global__ void __launch_bounds__(512)
+ods_perm_ring(const __grid_constant__ Lay L, const __grid_constant__ Cfg C, const __grid_constant__ PermRing W,
+              uint32_t chunk) {
+    const uint32_t per = (C.N + chunk - 1) / chunk;
+    const uint32_t total = W.n * per;
+    const PermDomain dom = perm_domain(C.N);
+    __shared__ uint32_t s_item, s_last;
+    for (;;) {
+        if (threadIdx.x == 0) s_item = atomicAdd(L.gen_next, 1u);
+        __syncthreads();
+        const uint32_t item = s_item;
+        if (item >= total) break;
+        const uint32_t pair = item / per, part = item % per;
+        const uint32_t e = W.e[pair], j = W.j[pair];
+        if (threadIdx.x == 0)
+            while (ld_acquire(L.epoch_at + j) + C.K - 1 < e) __nanosleep(2000);
+        __syncthreads();
+        const uint64_t key = derive_key(L.seed, PUR_REQ, j, e, 0);
+        uint32_t* out = L.perms + ((size_t)j * C.K + (e & (C.K - 1))) * C.Nrow;
         const uint32_t lo = part * chunk, hi = min(lo + chunk, C.N);
         for (uint32_t pos = lo + threadIdx.x; pos < hi; pos += blockDim.x) out[pos] = perm_apply(key, dom, pos);
         __syncthreads();
@@ -1430,14 +1510,21 @@ __global__ void ods_validate_requests(const __grid_constant__ Lays LS, const __g
     __syncthreads();
     for (uint32_t s = threadIdx.x; s < need; s += blockDim.x) {
         const uint32_t i = s_row[s];
-        if (i >= C.N) { atomicOr(L.err, 0x100u); continue; }
-        if (L.seen[(size_t)j * C.NW + (i >> 5)] & (1u << (i & 31))) atomicOr(L.err, 0x100u);
+        if (i >= C.N) { atomicOr(L.verr, 1u); continue; }
+        if (L.seen[(size_t)j * C.NW + (i >> 5)] & (1u << (i & 31))) atomicOr(L.verr, 1u);
         for (uint32_t s2 = 0; s2 < s; ++s2)
-            if (s_row[s2] == i) { atomicOr(L.err, 0x100u); break; }
+            if (s_row[s2] == i) { atomicOr(L.verr, 1u); break; }
     }
 }
 
 inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// Control block at the start of the workspace, one 64-B slot per replica:
+// bar[4] at +0, err at +16, verr at +20.  Kept contiguous (not inside the
+// replica slices) so the per-launch signal reset and the status read are one
+// small strided copy whatever the replica slice size.
+constexpr size_t kCtlBytes = 64;
+inline size_t ctl_bytes(uint32_t R) { return align256((size_t)R * kCtlBytes); }
 
 enum KernelClass { K_ROUNDS = 0, K_PERM, K_RECOUNT, K_INIT, K_VALIDATE, K_NCLASS };
 const char* const kKernelNames[K_NCLASS] = {"ods_rounds", "ods_perm_all", "ods_recount_all", "ods_init_tiers",
@@ -1457,6 +1544,7 @@ struct seneca_ctx {
     Lays LS;               // every replica
     uint32_t R;            // replicas
     size_t rep_stride;     // workspace bytes per replica
+    char* ctl;             // control block (kCtlBytes per replica) at the workspace start
     uint32_t mode;
     uint64_t cap_e, cap_d;
     uint64_t e[kMaxJobs], n[kMaxJobs];
@@ -1464,6 +1552,7 @@ struct seneca_ctx {
     uint32_t pending;              // jobs that have not arrived (R-O23)
     uint64_t arrival[kMaxJobs];
     uint64_t r;
+    uint64_t gen_hi[kMaxJobs];     // permutations of epochs < gen_hi[j] have been generated (ring, C.K slots)
     uint64_t launches;
     uint64_t klaunch[K_NCLASS];
     double kms[K_NCLASS];
@@ -1533,6 +1622,7 @@ Sizes compute_sizes(const seneca_cache_config* cfg) {
         C.batch[j] = cfg->batch_size[j];
         C.target[j] = cfg->target_epochs[j];
     }
+    C.K = std::min<uint32_t>(C.maxT, 2);
     C.cap_a = (uint32_t)cfg->cap_a;
     C.cap_d = (uint32_t)cfg->cap_d;
     C.cap_e = (uint32_t)cfg->cap_e;
@@ -1552,7 +1642,7 @@ Sizes compute_sizes(const seneca_cache_config* cfg) {
         (size_t)C.Nrow * 4,                                 // 5 cons_cnt
         P * C.NBp, P * C.NS * 4, P * 4,                     // 6-8 counts
         16,                                                 // 9 tsize
-        (size_t)C.J * C.maxT * C.Nrow * 4,                  // 10 perms
+        (size_t)C.J * C.K * C.Nrow * 4,                     // 10 perms (ring of K epochs per job)
         (size_t)C.J * 2 * C.Nrow * 4,                       // 11 laps
         (size_t)C.J * C.maxT * 4, (size_t)C.J * C.maxT * 4, // 12-13 perm_ready, perm_done
         (size_t)C.J * sizeof(JobDev),                       // 14 jobs
@@ -1560,10 +1650,11 @@ Sizes compute_sizes(const seneca_cache_config* cfg) {
         (size_t)C.J * C.Bmax * 4, 32,                       // 17-18 evict_push, fill_n
         capl, 2 * (capl + (size_t)C.J * C.Bmax * 4),        // 19-20 evict, fill [2]
         (size_t)C.J * C.maxT * sizeof(seneca_job_epoch_stats),  // 21 stats
-        8, 8, 4, 16, 256,                                   // 22-26 evicted, refilled, err, bar, phase
+        8, 8, 0, 0, 256,                                    // 22-26 evicted, refilled, (control block x2), phase
         C.evict_all ? 2 * edl : 4, 8,                       // 27-28 ev_ed, ev_ed_n
         C.cold ? (size_t)C.J * C.Bmax * 4 : 4, (size_t)C.J * 4,   // 29-30 fetch, fetch_n
         4, C.cold ? W : 4,                                  // 31-32 warm, claim
+        (size_t)C.J * 4, 4,                                 // 33-34 epoch_at, gen_next
     };
     size_t at = 0;
     for (size_t k = 0; k < sizeof(sz) / sizeof(sz[0]); ++k) {
@@ -1575,7 +1666,7 @@ Sizes compute_sizes(const seneca_cache_config* cfg) {
     return z;
 }
 
-Lay carve(const Sizes& z, char* base, uint64_t seed) {
+Lay carve(const Sizes& z, char* base, char* ctl, uint64_t seed) {
     Lay L;
     L.seed = seed;
     L.bm_e = (uint32_t*)(base + z.off[0]);
@@ -1602,8 +1693,9 @@ Lay carve(const Sizes& z, char* base, uint64_t seed) {
     L.stats = (seneca_job_epoch_stats*)(base + z.off[21]);
     L.evicted = (unsigned long long*)(base + z.off[22]);
     L.refilled = (unsigned long long*)(base + z.off[23]);
-    L.err = (uint32_t*)(base + z.off[24]);
-    L.bar = (uint32_t*)(base + z.off[25]);
+    L.bar = (uint32_t*)ctl;
+    L.err = (uint32_t*)(ctl + 16);
+    L.verr = (uint32_t*)(ctl + 20);
     L.phase = (unsigned long long*)(base + z.off[26]);
     L.ev_ed = (uint32_t*)(base + z.off[27]);
     L.ev_ed_n = (uint32_t*)(base + z.off[28]);
@@ -1611,6 +1703,8 @@ Lay carve(const Sizes& z, char* base, uint64_t seed) {
     L.fetch_n = (uint32_t*)(base + z.off[30]);
     L.warm = (uint32_t*)(base + z.off[31]);
     L.claim = (uint32_t*)(base + z.off[32]);
+    L.epoch_at = (uint32_t*)(base + z.off[33]);
+    L.gen_next = (uint32_t*)(base + z.off[34]);
     return L;
 }
 
@@ -1675,10 +1769,125 @@ void sched_round(const Cfg& C, Sched& s, uint32_t mask) {
     s.r += 1;
 }
 
-// Launch R rounds.  jobs_mask: the jobs of every round (replay: all active).
-seneca_status launch_rounds(seneca_ctx* c, uint64_t R, uint32_t jobs_mask, const uint32_t* d_requested,
+// Rounds (<= R) a launch may play when the ring is filled only between launches:
+// it stops before the first round in which a participating job would play an
+// epoch whose permutation has not been generated.
+uint64_t rounds_allowed(const seneca_ctx* c, uint64_t R, uint32_t jobs_mask) {
+    if (c->mode != 0) return R;
+    Sched s = sched_of(c);
+    uint64_t k = 0;
+    for (; k < R; ++k) {
+        sched_arrive(s);
+        bool ok = true;
+        for (uint32_t m = s.active & jobs_mask; m; m &= m - 1) {
+            const uint32_t j = __builtin_ctz(m);
+            if (s.e[j] >= c->gen_hi[j]) { ok = false; break; }
+        }
+        if (!ok) break;
+        sched_round(c->C, s, jobs_mask);
+    }
+    return k;
+}
+
+// The permutation ring ahead of a launch of (up to) R rounds; returns in *R_out
+// the rounds the launch may play.
+//  * Epochs a job may need at once (its current one up to K - 1 beyond) that are
+//    not generated yet: ods_perm_all over the whole GPU, before the launch.  Their
+//    slots hold epochs the job has finished (every earlier launch is ordered
+//    before this generator), so no live permutation is overwritten.  One
+//    replica: on the side stream, overlapping the round launch, which waits on
+//    the ready flags; several replicas may fill every SM with round CTAs, so
+//    their generator runs first on the caller's stream.
+//  * One replica with more epochs than slots: the epochs the jobs will enter
+//    during the launch are generated DURING it by ods_perm_ring on the side stream
+//    (a few CTAs beside the J + 1 round CTAs; each slot is refilled once its job
+//    has started the epoch after the slot's old one), so jobs whose epochs end at
+//    different rounds never have to meet at a launch boundary.
+//  * Several replicas: the launch stops before a job would enter an epoch that
+//    is not in the ring (rounds_allowed); the next launch refills it.
+seneca_status prepare_perms(seneca_ctx* c, cudaStream_t st, uint64_t R, uint32_t jobs_mask, uint64_t* R_out) {
+    *R_out = R;
+    if (c->mode != 0) return SENECA_OK;
+    const uint32_t K = c->C.K;
+    uint64_t gen[kMaxJobs];
+    for (uint32_t j = 0; j < kMaxJobs; ++j) gen[j] = c->gen_hi[j];
+    PermWork W;
+    W.n = 0;
+    for (uint32_t k = 0; k < K; ++k)                           // epoch-major
+        for (uint32_t j = 0; j < c->C.J; ++j) {
+            if (!(((c->active | c->pending) >> j) & 1u)) continue;
+            const uint64_t e = c->e[j] + k;
+            if (e < gen[j] || e >= c->C.target[j]) continue;
+            W.j[W.n] = j; W.e[W.n] = (uint32_t)e; ++W.n;
+            gen[j] = e + 1;
+        }
+    const uint32_t chunk = 16384;
+    if (W.n) {
+        cudaStream_t ps = st;
+        if (c->R == 1) {
+            SENECA_CUDA_TRY(cudaEventRecord(c->ev_init, st));
+            SENECA_CUDA_TRY(cudaStreamWaitEvent(c->side, c->ev_init, 0));
+            ps = c->side;
+        }
+        const uint32_t gx = std::max<uint32_t>(1, (uint32_t)num_sms() * 4 / c->R);
+        timed(c, K_PERM, ps, [&] { ods_perm_all<<<dim3(gx, c->R), 512, 0, ps>>>(c->LS, c->C, W, chunk); });
+        SENECA_CUDA_TRY(cudaGetLastError());
+        for (uint32_t j = 0; j < kMaxJobs; ++j) c->gen_hi[j] = gen[j];
+    }
+    if (c->R > 1 || c->C.maxT <= K) {
+        *R_out = rounds_allowed(c, R, jobs_mask);
+        return SENECA_OK;
+    }
+    // one replica: the epochs entered during the launch, refilled concurrently
+    PermRing Q;
+    Q.n = 0;
+    Sched s = sched_of(c);
+    uint64_t k = 0;
+    for (; k < R; ++k) {
+        sched_arrive(s);
+        Sched t = s;
+        sched_round(c->C, t, jobs_mask);
+        uint32_t add = 0;
+        for (uint32_t m = s.active & jobs_mask; m; m &= m - 1) {    // jobs entering epoch e' this round
+            const uint32_t j = __builtin_ctz(m);
+            const uint64_t e = t.e[j] + K - 1;                     // its slot frees now
+            if (t.e[j] != s.e[j] && e < c->C.target[j] && e >= gen[j]) ++add;
+        }
+        if (Q.n + add > kRingPairs) break;                         // the next launch takes over
+        for (uint32_t m = s.active & jobs_mask; m; m &= m - 1) {
+            const uint32_t j = __builtin_ctz(m);
+            const uint64_t e = t.e[j] + K - 1;
+            if (t.e[j] != s.e[j] && e < c->C.target[j] && e >= gen[j]) {
+                Q.j[Q.n] = j; Q.e[Q.n] = (uint32_t)e; ++Q.n;
+                gen[j] = e + 1;
+            }
+        }
+        s = t;
+    }
+    *R_out = k;
+    if (Q.n) {
+        SENECA_CUDA_TRY(cudaEventRecord(c->ev_init, st));
+        SENECA_CUDA_TRY(cudaStreamWaitEvent(c->side, c->ev_init, 0));
+        SENECA_CUDA_TRY(cudaMemsetAsync(c->L.gen_next, 0, 4, c->side));
+        // beside the round launch's J + 1 one-CTA-per-SM CTAs (never timed: it
+        // waits for the round launch that follows it)
+        const uint32_t g = std::max<int>(1, std::min<int>(16, num_sms() - (int)c->C.J - 1));
+        c->launches++;
+        c->klaunch[K_PERM]++;
+        ods_perm_ring<<<g, 512, 0, c->side>>>(c->L, c->C, Q, chunk);
+        SENECA_CUDA_TRY(cudaGetLastError());
+        for (uint32_t j = 0; j < kMaxJobs; ++j) c->gen_hi[j] = gen[j];
+    }
+    return SENECA_OK;
+}
+
+// Launch up to *Rio rounds (fewer when the permutation ring bounds the launch,
+// prepare_perms); *Rio returns the rounds launched.  jobs_mask: the jobs of every
+// round (replay: all active).
+seneca_status launch_rounds(seneca_ctx* c, uint64_t* Rio, uint32_t jobs_mask, const uint32_t* d_requested,
                             uint32_t* out_ids, uint8_t* out_src, uint32_t out_stride, const uint32_t* row_of_job,
                             unsigned long long* transcript, cudaStream_t st) {
+    uint64_t R = *Rio;
     Launch P;
     std::memset(&P, 0, sizeof P);
     P.r0 = c->r;
@@ -1701,21 +1910,30 @@ seneca_status launch_rounds(seneca_ctx* c, uint64_t R, uint32_t jobs_mask, const
     P.out_rep = (uint64_t)out_stride * (row_of_job ? __builtin_popcount(jobs_mask) : c->C.J);
     P.tr_rep = (uint64_t)c->C.J * c->C.maxT * c->C.N;
     P.timing = (c->profiling >> 1) & 1u;
+    {
+        uint64_t Rp = R;
+        seneca_status ps = prepare_perms(c, st, R, jobs_mask, &Rp);
+        if (ps) return ps;
+        if (Rp == 0) { set_error("internal: no round playable within the permutation ring"); return SENECA_ESTATE; }
+        R = Rp;
+        P.rounds = (uint32_t)R;
+        *Rio = R;
+    }
     if (c->mode == 1) {
         timed(c, K_VALIDATE, st, [&] {
             ods_validate_requests<<<__builtin_popcount(jobs_mask), 256, (size_t)c->C.Bmax * 4, st>>>(c->LS, c->C, P);
         });
         SENECA_CUDA_TRY(cudaGetLastError());
         uint32_t err = 0;
-        SENECA_CUDA_TRY(cudaMemcpyAsync(&err, c->L.err, 4, cudaMemcpyDeviceToHost, st));
+        SENECA_CUDA_TRY(cudaMemcpyAsync(&err, c->L.verr, 4, cudaMemcpyDeviceToHost, st));
         SENECA_CUDA_TRY(cudaStreamSynchronize(st));
-        if (err & 0x100u) {
-            SENECA_CUDA_TRY(cudaMemsetAsync(c->L.err, 0, 4, st));
+        if (err) {                      // only the validation flag is cleared; latched flags stay
+            SENECA_CUDA_TRY(cudaMemsetAsync(c->L.verr, 0, 4, st));
             set_error("supplied request ids out of range, duplicated or already seen");
             return SENECA_EPROTO;
         }
     }
-    SENECA_CUDA_TRY(cudaMemset2DAsync(c->L.bar, c->rep_stride, 0, 16, c->R, st));
+    SENECA_CUDA_TRY(cudaMemset2DAsync(c->ctl, kCtlBytes, 0, 16, c->R, st));   // every replica's bar[4]
     void* args[] = {&c->LS, &c->C, &P};
     cudaError_t le = cudaSuccess;
     timed(c, K_ROUNDS, st, [&] {
@@ -1745,7 +1963,7 @@ extern "C" seneca_status seneca_state_bytes(const seneca_cache_config* cfg, size
     if (s) return s;
     if (!bytes) { set_error("NULL bytes"); return SENECA_EINVAL; }
     const Sizes z = compute_sizes(cfg);
-    *bytes = z.total * z.R;
+    *bytes = ctl_bytes(z.R) + z.total * z.R;
     return SENECA_OK;
 }
 
@@ -1756,8 +1974,9 @@ extern "C" seneca_status seneca_init_cache(const seneca_cache_config* cfg, void*
     if (!out || !d_workspace) { set_error("NULL workspace or out"); return SENECA_EINVAL; }
     if ((uintptr_t)d_workspace & 255) { set_error("workspace must be 256-byte aligned"); return SENECA_EINVAL; }
     Sizes z = compute_sizes(cfg);
-    if (ws_bytes < z.total * z.R) {
-        set_error("workspace %zu bytes < required %zu", ws_bytes, z.total * z.R); return SENECA_ENOSPC;
+    const size_t need_bytes = ctl_bytes(z.R) + z.total * z.R;
+    if (ws_bytes < need_bytes) {
+        set_error("workspace %zu bytes < required %zu", ws_bytes, need_bytes); return SENECA_ENOSPC;
     }
     // dynamic shared memory of a round CTA with T threads (window min(kWinMax, 2 T))
     auto smem_for = [&](uint32_t T) -> size_t {
@@ -1772,7 +1991,9 @@ extern "C" seneca_status seneca_init_cache(const seneca_cache_config* cfg, void*
     c->C = z.C;
     c->R = z.R;
     c->rep_stride = z.total;
-    for (uint32_t k = 0; k < z.R; ++k) c->LS.r[k] = carve(z, (char*)d_workspace + k * z.total, cfg->seed + k);
+    c->ctl = (char*)d_workspace;
+    for (uint32_t k = 0; k < z.R; ++k)
+        c->LS.r[k] = carve(z, (char*)d_workspace + ctl_bytes(z.R) + k * z.total, c->ctl + k * kCtlBytes, cfg->seed + k);
     c->L = c->LS.r[0];
     c->mode = cfg->request_mode;
     c->cap_e = cfg->cap_e;
@@ -1858,7 +2079,7 @@ extern "C" seneca_status seneca_init_cache(const seneca_cache_config* cfg, void*
     INIT_TRY(cudaEventCreateWithFlags(&c->ev_init, cudaEventDisableTiming));
     INIT_TRY(cudaEventCreate(&c->ev_a));
     INIT_TRY(cudaEventCreate(&c->ev_b));
-    INIT_TRY(cudaMemsetAsync(d_workspace, 0, z.total * z.R, st));
+    INIT_TRY(cudaMemsetAsync(d_workspace, 0, need_bytes, st));
     {
         const uint32_t total = (uint32_t)(cfg->cap_a + cfg->cap_d + cfg->cap_e);
         const uint32_t blocks = std::max<uint32_t>(1, std::min<uint32_t>((total + 255) / 256, num_sms() * 8));
@@ -1875,19 +2096,12 @@ extern "C" seneca_status seneca_init_cache(const seneca_cache_config* cfg, void*
         c->launches++;
         INIT_TRY(cudaGetLastError());
     }
-    // every epoch's permutation.  One replica: on a side stream, overlapping the
-    // rounds, which wait on the per-(job, epoch) flags.  Several replicas may fill
-    // every SM with round CTAs, so their permutations are generated up front on
-    // the caller's stream (never a round CTA spinning on a generator that cannot
-    // get an SM).
-    INIT_TRY(cudaEventRecord(c->ev_init, st));
-    INIT_TRY(cudaStreamWaitEvent(c->side, c->ev_init, 0));
-    if (c->mode == 0) {
-        const uint32_t chunk = 16384;
-        cudaStream_t ps = c->R == 1 ? c->side : st;
-        const uint32_t gx = std::max<uint32_t>(1, (uint32_t)num_sms() * 4 / c->R);
-        timed(c, K_PERM, ps, [&] { ods_perm_all<<<dim3(gx, c->R), 512, 0, ps>>>(c->LS, c->C, chunk); });
-        INIT_TRY(cudaGetLastError());
+    // the first ring of permutations (epochs 0 .. K-1 of every job), overlapping
+    // the caller's next work when there is one replica (ensure_perms)
+    {
+        uint64_t unused = 0;
+        const seneca_status ps = prepare_perms(c, st, 0, 0xffffffffu, &unused);
+        if (ps) { delete c; return ps; }
     }
 #undef INIT_TRY
     *out = c;
@@ -1919,7 +2133,8 @@ extern "C" seneca_status seneca_ods_next_batch(seneca_ctx* c, const uint32_t* h_
         const uint32_t j = h_jobs[x];
         if (h_out_lens) h_out_lens[x] = (uint32_t)std::min<uint64_t>(c->C.batch[j], (uint64_t)c->C.N - c->n[j]);
     }
-    return launch_rounds(c, 1, mask, d_requested, d_out_ids, d_out_src, c->C.Bmax, rows, nullptr,
+    uint64_t one = 1;
+    return launch_rounds(c, &one, mask, d_requested, d_out_ids, d_out_src, c->C.Bmax, rows, nullptr,
                          (cudaStream_t)stream);
 }
 
@@ -1947,10 +2162,13 @@ static seneca_status replay(seneca_ctx* c, uint64_t R, uint64_t* d_transcript, u
     if (c->mode != 0) { set_error("replay requires request_mode 0"); return SENECA_ESTATE; }
     if (!(c->active | c->pending)) { set_error("no active job"); return SENECA_ESTATE; }
     uint64_t done = 0;
-    const uint64_t kChunk = 1u << 30;
+    // rounds per launch: the 32-bit signal counters (job phases, evictions pushed,
+    // eviction ring position) count at most J (phases) / J * Bmax (pushes) per round
+    // and are zeroed at every launch, so a launch never lets them wrap
+    const uint64_t kChunk = std::min<uint64_t>(1u << 30, 0xffffffffull / ((uint64_t)c->C.J * (c->C.Bmax + 1)));
     while (done < R && (c->active | c->pending)) {
-        const uint64_t n = std::min<uint64_t>(R - done, kChunk);
-        seneca_status s = launch_rounds(c, n, 0xffffffffu, nullptr, nullptr, nullptr, c->C.Bmax, nullptr,
+        uint64_t n = std::min<uint64_t>(R - done, kChunk);
+        seneca_status s = launch_rounds(c, &n, 0xffffffffu, nullptr, nullptr, nullptr, c->C.Bmax, nullptr,
                                         (unsigned long long*)d_transcript, st);
         if (s) return s;
         done += n;
@@ -2020,7 +2238,7 @@ extern "C" seneca_status seneca_read_state(const seneca_ctx* c, seneca_state_vie
 extern "C" seneca_status seneca_sync_status(seneca_ctx* c, void* stream) {
     if (!c) { set_error("bad arguments"); return SENECA_EINVAL; }
     uint32_t err[kMaxReplicas] = {0};
-    SENECA_CUDA_TRY(cudaMemcpy2DAsync(err, 4, c->L.err, c->rep_stride, 4, c->R, cudaMemcpyDeviceToHost,
+    SENECA_CUDA_TRY(cudaMemcpy2DAsync(err, 4, c->L.err, kCtlBytes, 4, c->R, cudaMemcpyDeviceToHost,
                                       (cudaStream_t)stream));
     SENECA_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
     for (uint32_t k = 0; k < c->R; ++k)

@@ -24,11 +24,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 def caps_for(c):
-    p = O.make_profile(t_gpu=1, t_decode_augment=1, t_augment=1, b_nic=1, b_pcie=1, b_cache=1, b_storage=1,
-                       cache_bytes=c["cache_bytes"], n_total=c["n_total"], s_data=c["s_data"],
-                       m_num=c["m_num"], m_den=c["m_den"], nodes=1, gpus_per_node=1)
-    na, nd, ne, ns = O.split_counts(p, *c["split"])
-    return ne, nd, na
+    return O.config_capacities(c)
 
 
 def state_hash(tier, seen, cons):

@@ -134,9 +134,15 @@ def test_replicas_workspace_and_arguments(lib):
     c = synth.ods_config("toy")
     caps = S.split_capacities(c["n_total"], c["s_data"], c["m_num"], c["m_den"], c["cache_bytes"], *c["split"])
     one = S.state_bytes(S.make_config(c["n_total"], c["batch"], c["target"], caps[0], caps[1], caps[2], 1))
+    two = S.state_bytes(S.make_config(c["n_total"], c["batch"], c["target"], caps[0], caps[1], caps[2], 1,
+                                      replicas=2))
+    slice_ = two - one                                         # one 256-aligned slice per replica
+    ctl = one - slice_                                         # + a control block, 64 B per replica
+    assert slice_ % 256 == 0 and ctl == 256
     for r in (0, 1, 2, 7, 64):
         cfg = S.make_config(c["n_total"], c["batch"], c["target"], caps[0], caps[1], caps[2], 1, replicas=r)
-        assert S.state_bytes(cfg) == max(r, 1) * one          # one 256-aligned slice per replica
+        R = max(r, 1)
+        assert S.state_bytes(cfg) == R * slice_ + -(-R * 64 // 256) * 256
     for r, mode in ((65, 0), (2, 1)):                          # too many; caller-supplied requests need R = 1
         cfg = S.make_config(c["n_total"], c["batch"], c["target"], caps[0], caps[1], caps[2], 1, mode, replicas=r)
         with pytest.raises(S.SenecaError) as ei:
@@ -164,3 +170,23 @@ def test_mode_fields_validated(lib):
         with pytest.raises(S.SenecaError) as ei:
             S.state_bytes(S.make_config(*args, **kw))
         assert ei.value.status == S.EINVAL
+
+
+def test_workspace_is_independent_of_target_epochs(lib):
+    """The permutation ring (K = min(epochs, 2) slots per job) keeps the workspace
+    flat in the number of epochs: only the per job-epoch counters (104 B) and the
+    per job-epoch ready/progress flags (8 B) grow.  ImageNet-22K x 50 epochs fits
+    in a few GB (it needed 22.7 GB when every epoch was materialised)."""
+    c = synth.ods_config("imagenet22k")
+    caps = S.split_capacities(c["n_total"], c["s_data"], c["m_num"], c["m_den"], c["cache_bytes"], *c["split"])
+    J = len(c["batch"])
+    sizes = {}
+    for T in (2, 3, 50, 250):
+        cfg = S.make_config(c["n_total"], c["batch"], [T] * J, caps[0], caps[1], caps[2], 1)
+        sizes[T] = S.state_bytes(cfg)
+    for T in (3, 50, 250):
+        grow = sizes[T] - sizes[2]
+        assert 0 <= grow <= J * (T - 2) * (104 + 8) + 3 * 256, (T, grow)
+    assert sizes[250] < 4 * 2**30
+    one = S.make_config(c["n_total"], c["batch"], [1] * J, caps[0], caps[1], caps[2], 1)
+    assert S.state_bytes(one) < sizes[2]          # one epoch: a one-slot ring

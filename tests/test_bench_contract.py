@@ -91,6 +91,6 @@ def test_all_cores_oracle_baselines():
     v, cores, done, dt = bench.oracle_mdp_all_cores(args, per_core=20)
     assert cores >= 1 and done == 20 * cores and v > 0 and dt > 0
     c = synth.ods_config("toy", seed=synth.PERF_SEED)
-    v, cores, dec, dt = bench.oracle_ods_all_cores(args, c, bench.caps_of(c), 10)
+    v, cores, dec, dt = bench.oracle_ods_all_cores(args, c, bench.oracle_caps(c), 10)
     assert dec == cores * 10 * sum(c["batch"])          # every replay plays 10 full rounds of both jobs
     assert v > 0

@@ -31,8 +31,12 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 def caps_of(c):
-    caps = S.split_capacities(c["n_total"], c["s_data"], c["m_num"], c["m_den"], c["cache_bytes"], *c["split"])
-    return caps[0], caps[1], caps[2]
+    """The oracle's own capacities (oracle.config_capacities); the product's
+    seneca_split_capacities must agree (checked here and in tests/test_abi.py)."""
+    caps = O.config_capacities(c)
+    prod = S.split_capacities(c["n_total"], c["s_data"], c["m_num"], c["m_den"], c["cache_bytes"], *c["split"])
+    assert tuple(prod[:3]) == tuple(caps), (prod, caps)
+    return caps
 
 
 def make_pair(n, batch, target, ce, cd, ca, seed, transcript=True, evict_all=False, baseline=False):
@@ -607,3 +611,72 @@ def test_cold_start_next_batch_and_arrivals():
             assert np.array_equal(ids_g[x, :L_].cpu().numpy().view(np.uint32), ids_o[x, :L_])
             assert np.array_equal(src_g[x, :L_].cpu().numpy(), src_o[x, :L_])
     compare_state(o, g)
+
+
+# ---------------------------------------------------------------- permutation ring
+@pytest.mark.parametrize("evict_all,R", [(False, 1), (True, 1), (False, 3), (True, 3)])
+def test_permutation_ring_jobs_at_different_epochs(evict_all, R):
+    """Mixed batches and target epochs (7, 3, 5, 1): the jobs cross epoch
+    boundaries at different rounds.  One replica: the 2-slot ring of each job is
+    refilled DURING the launch by the concurrent generator (ods_perm_ring);
+    replicas: launches stop where a job would enter an epoch that is not in its
+    ring.  Every decision equals the oracle's (transcripts), also with the replay
+    cut into random-length launches on top."""
+    n = 5003
+    batch, target = [64, 512, 200, 1000], [7, 3, 5, 1]
+    ce, cd, ca = 700, 400, 600
+    g = P.ODSContext(n, batch, target, ce, cd, ca, 9, replicas=R, evict_tiers=int(evict_all))
+    tr = g.new_transcript()
+    st = synth.Stream(99)
+    total = 0
+    while g.view().active_mask:
+        k = int(st.u64(1)[0] % np.uint64(97)) + 1
+        done = g.replay_rounds(k, tr)
+        total += done
+        if done < k:
+            break
+    torch.cuda.synchronize()
+    g.sync()
+    for k in range(R):
+        o = O.ODS(n, batch, target, ce, cd, ca, 9 + k, transcript=True, evict_all=evict_all)
+        assert total == o.replay_epochs(max(target))
+        compare_replica(o, g, k, tr if R == 1 else tr[k])
+
+
+def test_permutation_ring_replicas_many_epochs():
+    """Replicas generate their ring on the caller's stream between launches: 12
+    replicas x 12 epochs of ImageNet-1K/64, each equal to its oracle replay."""
+    seed = 4
+    c = synth.ods_config("imagenet1k", scale=64, seed=seed)
+    c["target"] = [12, 11, 12, 9]
+    ce, cd, ca = caps_of(c)
+    R = 12
+    g = P.ODSContext(c["n_total"], c["batch"], c["target"], ce, cd, ca, seed, replicas=R)
+    rounds = g.replay_epochs(max(c["target"]))
+    torch.cuda.synchronize()
+    g.sync()
+    for k in (0, 5, 11):
+        o = O.ODS(c["n_total"], c["batch"], c["target"], ce, cd, ca, seed + k)
+        assert o.replay_epochs(max(c["target"])) == rounds
+        compare_replica(o, g, k)
+
+
+def test_workspace_above_2gib_per_replica():
+    """a replica slice above 2 GiB (32 jobs x 14.2 M samples: rings and
+    lap lists of 3.6 GB each) -- the per-launch signal reset and the status read
+    use the contiguous control block, so two such replicas replay and report OK;
+    replica 1 equals its oracle replay for the rounds played."""
+    c = synth.ods_config("imagenet22k", seed=6)
+    ce, cd, ca = caps_of(c)
+    J = 32
+    batch, target = [128] * J, [2] * J
+    g = P.ODSContext(c["n_total"], batch, target, ce, cd, ca, 6, replicas=2)
+    v = g.view()
+    assert v.replica_stride > 2 ** 31
+    assert g.replay_rounds(3) == 3
+    torch.cuda.synchronize()
+    g.sync()
+    o = O.ODS(c["n_total"], batch, target, ce, cd, ca, 7)
+    o.replay_rounds(3)
+    compare_replica(o, g, 1)
+    g.close()

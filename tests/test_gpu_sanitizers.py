@@ -1,0 +1,47 @@
+"""compute-sanitizer over every kernel instantiation (SURVEY §4/§5 "race
+detection"): memcheck, racecheck (shared-memory hazards), synccheck (barrier
+misuse) and initcheck (reads of uninitialised device memory) on the small
+invocations of tools/sanitize_run.py -- the persistent round kernel's
+inter-CTA release/acquire signals, the eviction ring, the cp.async walk
+prefetch, every launch shape (coupled, uncoupled, 256-thread, two CTAs per SM),
+cold start, evict-all, arrivals, caller-supplied requests and the MDP kernels.
+Each must report 0 errors, and every case is also checked against the oracle."""
+import os
+import re
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+import sanitize_run  # noqa: E402
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck", "initcheck"])
+def test_sanitizer_reports_no_errors(tool):
+    if not os.path.exists(SAN):
+        pytest.skip("compute-sanitizer not installed")
+    extra = ["--racecheck-report", "all"] if tool == "racecheck" else []
+    cmd = [SAN, "--tool", tool, *extra, "--error-exitcode", "99", "--target-processes", "all",
+           sys.executable, os.path.join(ROOT, "tools", "sanitize_run.py"), *sanitize_run.ALL]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    log = out.stdout + out.stderr
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", f"sanitizer_{tool}.log"), "w") as f:
+        f.write(log)
+    for name in sanitize_run.ALL:
+        assert f"case {name} ok" in log, (name, log[-3000:])
+    m = re.search(r"ERROR SUMMARY: (\d+) error", log)
+    assert m is not None, log[-3000:]
+    assert int(m.group(1)) == 0, log[-5000:]
+    assert out.returncode == 0, log[-3000:]

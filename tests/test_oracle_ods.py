@@ -34,6 +34,8 @@ def test_config_capacities_match_survey_table():
     assert caps_for(synth.ods_config("imagenet1k")) == (0, 42_038, 45_541)
     assert caps_for(synth.ods_config("openimages")) == (658_561, 118_731, 0)
     assert caps_for(synth.ods_config("imagenet22k")) == (4_376_846, 0, 0)
+    for name in ("toy", "imagenet1k", "openimages", "imagenet22k"):
+        assert O.config_capacities(synth.ods_config(name)) == caps_for(synth.ods_config(name))
 
 
 def test_spec_worked_example():
