@@ -48,7 +48,7 @@ def perm(K, n, x):
     kk = (K & M32, K >> 32)
     while True:
         left, right = divmod(x, b)
-        for rd in range(4):
+        for rd in range(12 if n < 64 else 4):       # R-O17: more rounds on small domains
             if rd % 2 == 0:
                 left = (left + ((philox((right, rd, 0, 0), kk)[0] * a) >> 32)) % a
             else:

@@ -79,12 +79,14 @@ uint64_t oracle_key(uint64_t seed, uint64_t purpose, uint64_t a, uint64_t b, uin
     return oracle_splitmix64(seed ^ oracle_splitmix64(word));
 }
 
-/* perm(K, n, x): keyed bijection of [0, n), 0 <= x < n (R-O17).  A 4-round
- * Feistel network on Z_a x Z_b with a = ceil(sqrt(n)), b = ceil(n / a)
+/* perm(K, n, x): keyed bijection of [0, n), 0 <= x < n (R-O17).  A Feistel
+ * network on Z_a x Z_b with a = ceil(sqrt(n)), b = ceil(n / a)
  * (a*b >= n, a*b - n < a): x = L*b + R; even rounds L = (L + F) mod a with
  * F = floor(philox((R, rd, 0, 0), K)[0] * a / 2^32), odd rounds
  * R = (R + floor(philox((L, rd, 0, 0), K)[0] * b / 2^32)) mod b; restricted to
- * [0, n) by cycle walking (probability of a step < 1/b).                    */
+ * [0, n) by cycle walking (probability of a step < 1/b).  4 rounds for n >= 64;
+ * 12 rounds for n < 64, where the halves are too small for 4 rounds to mix
+ * (pairs chi-square, tests/test_oracle_prng.py; DESIGN.md R-O17).            */
 static uint64_t isqrt_ceil(uint64_t n)   /* smallest a with a*a >= n */
 {
     uint64_t a = (uint64_t)sqrt((double)n);
@@ -101,7 +103,8 @@ uint64_t oracle_perm(uint64_t K, uint64_t n, uint64_t x)
     uint32_t key[2] = { (uint32_t)K, (uint32_t)(K >> 32) };
     do {
         uint64_t L = x / b, R = x % b;
-        for (uint32_t rd = 0; rd < 4; ++rd) {
+        const uint32_t rounds = n < 64 ? 12u : 4u;
+        for (uint32_t rd = 0; rd < rounds; ++rd) {
             uint32_t o[4];
             if ((rd & 1) == 0) {
                 uint32_t ctr[4] = { (uint32_t)R, rd, 0, 0 };
@@ -116,6 +119,13 @@ uint64_t oracle_perm(uint64_t K, uint64_t n, uint64_t x)
         x = L * b + R;
     } while (x >= n);
     return x;
+}
+
+/* perm(K, n, x) for x = x0 .. x0 + count - 1 into out[] (a loop over
+ * oracle_perm, for the exhaustive / distribution pins in tests/).           */
+void oracle_perm_block(uint64_t K, uint64_t n, uint64_t x0, uint64_t count, uint32_t* out)
+{
+    for (uint64_t t = 0; t < count; ++t) out[t] = (uint32_t)oracle_perm(K, n, x0 + t);
 }
 
 /* ========================================================================= */

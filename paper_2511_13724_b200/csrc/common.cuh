@@ -74,12 +74,26 @@ __device__ __forceinline__ PermDomain perm_domain(uint32_t n) {
     return d;
 }
 
-// 4-round Feistel on Z_a x Z_b (x = L*b + R): even rounds L += F mod a, odd
-// rounds R += F mod b, F = philox((other part, round, 0, 0), key)[0] scaled
-// to the modulus by multiply-high; cycle-walked into [0, n).
+// Feistel on Z_a x Z_b (x = L*b + R): even rounds L += F mod a, odd rounds
+// R += F mod b, F = philox((other part, round, 0, 0), key)[0] scaled to the
+// modulus by multiply-high; cycle-walked into [0, n).  4 rounds; 12 when
+// n < 64 (halves of <= 8 values need more rounds to mix, R-O17) -- a
+// CTA-uniform branch in every caller (one pool size per call site).
 __device__ __forceinline__ uint32_t perm_apply(uint64_t key, const PermDomain& d, uint32_t x) {
     if (d.n <= 1u) return 0u;
     const uint32_t k0 = (uint32_t)key, k1 = (uint32_t)(key >> 32);
+    if (d.n < 64u) {
+        do {
+            uint32_t L = x / d.b, R = x - L * d.b;
+#pragma unroll 1
+            for (uint32_t rd = 0; rd < 12u; rd += 2) {
+                L += __umulhi(philox_w0(R, rd, k0, k1), d.a); L = L >= d.a ? L - d.a : L;
+                R += __umulhi(philox_w0(L, rd + 1, k0, k1), d.b); R = R >= d.b ? R - d.b : R;
+            }
+            x = L * d.b + R;
+        } while (x >= d.n);
+        return x;
+    }
     do {
         uint32_t L = x / d.b, R = x - L * d.b;
         L += __umulhi(philox_w0(R, 0u, k0, k1), d.a); L = L >= d.a ? L - d.a : L;
