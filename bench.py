@@ -70,6 +70,10 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target oracle sample duration")
     ap.add_argument("--evict-tiers", type=int, default=0, choices=[0, 1],
                     help="0: A only (SPEC default, the headline); 1: every cached tier (R-O21)")
+    ap.add_argument("--shards", default="2,4,8",
+                    help="N = 1: shard counts of the emulated sample-ID-range-sharded replay ('' : none)")
+    ap.add_argument("--no-shard-replay", action="store_true",
+                    help="N > 1: skip the replay sharded across the ranks (one shard per GPU)")
     ap.add_argument("--replicas", type=int, default=-1,
                     help="also time R independent replays in one context (-1: as many as fit the GPU, 0: skip)")
     return ap.parse_args()
@@ -495,10 +499,12 @@ def main():
     dev = torch.device("cuda", local_dev)
     if world > 1:
         import torch.distributed as dist
+        import datetime
+        tmo = datetime.timedelta(minutes=5)
         if backend == "nccl":
-            dist.init_process_group("nccl", device_id=dev)
+            dist.init_process_group("nccl", device_id=dev, timeout=tmo)
         else:
-            dist.init_process_group(backend)
+            dist.init_process_group(backend, timeout=tmo)
     red_dev = dev if backend == "nccl" else None
     stream = torch.cuda.current_stream(dev)
 
@@ -746,6 +752,66 @@ def main():
                                   every_replica_served_each_sample_once_per_job_epoch=all(t["served_ok"] for t in tried))
         rep_line.pop("served_ok", None)
 
+    # ---- ONE replay partitioned by sample-ID range, timed like the
+    #      headline (init_cache + the full replay, L2 flushed, one warm-up) and gated
+    #      by the golden digests on every shard.  N = 1: G shards emulated on this
+    #      device (one launch of G x (J + 1) CTAs exchanging through device
+    #      mailboxes); N > 1: rank r is shard r of one replay (mailboxes mapped into
+    #      every rank over NVLink by CUDA IPC, the kernels store into their peers'),
+    #      strong scaling of one replay -- reported beside the headline.
+    sharded = None
+    shard_counts = ([int(x) for x in args.shards.split(",") if x] if world == 1 else
+                    ([] if args.no_shard_replay else [world]))
+    if shard_counts:
+        import paper_2511_13724_b200 as P
+        us1 = 1e6 * (sum(ods_ms) / 1e3) / rounds_tot            # the unsharded headline, this rank
+        sharded = dict(mode="emulated on one device" if world == 1 else "one shard per GPU (CUDA IPC mailboxes)",
+                       workload=args.workload, unsharded_us_per_round=us1, runs=[],
+                       note="exchange_us_per_round = us_per_round - unsharded_us_per_round: the cost of the two "
+                            "per-round exchanges (pool sizes, resolved ids) and the replicated work, DESIGN.md 8")
+        c_sh = synth.ods_config(args.workload, seed=synth.PERF_SEED)
+        for G in shard_counts:
+            try:
+                ms_g, rr_g, gate = [], 0, "bit-exact"
+                for s_ in range(2):
+                    flush.fill_(s_ & 0xFF)
+                    barrier()
+                    torch.cuda.synchronize(dev)
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    kw = dict(shards=G) if world == 1 else dict(shards=G, shard_rank=rank, shard_mode=1)
+                    if world > 1:
+                        gsh = P.ODSContext(c_sh["n_total"], c_sh["batch"], c_sh["target"], ce, cd, ca, c_sh["seed"],
+                                           evict_tiers=args.evict_tiers, stream=stream, **kw)
+                        D.attach_shard_peers(gsh)
+                        torch.cuda.synchronize(dev)
+                        barrier()
+                        e0.record(stream)
+                    else:
+                        e0.record(stream)
+                        gsh = P.ODSContext(c_sh["n_total"], c_sh["batch"], c_sh["target"], ce, cd, ca, c_sh["seed"],
+                                           evict_tiers=args.evict_tiers, stream=stream, **kw)
+                    rr_g = gsh.replay_epochs(max(c_sh["target"]))
+                    e1.record(stream)
+                    torch.cuda.synchronize(dev)
+                    barrier()
+                    if s_ == 1:
+                        ms_g.append(e0.elapsed_time(e1))
+                        gsh.sync()
+                        for k in range(gsh.R):
+                            stk, evk, rfk = gsh.stats(k)
+                            gk = golden_gate(args.workload, c_sh["seed"], args.evict_tiers, stk, evk, rfk)
+                            if gk != "bit-exact":
+                                gate = f"shard {k}: {gk}"
+                    gsh.close()
+                (t_g,) = D.reduce_times([sum(ms_g) / 1e3], device=red_dev)
+                sharded["runs"].append(dict(shards=G, ms=1e3 * t_g, rounds=rr_g,
+                                            us_per_round=1e6 * t_g / rr_g,
+                                            exchange_us_per_round=1e6 * t_g / rr_g - us1,
+                                            value=dec_per_step / t_g, unit="decisions/s (one replay)",
+                                            parity=gate))
+            except Exception as ex:  # report; the headline stands
+                sharded["runs"].append(dict(shards=G, error=f"{type(ex).__name__}: {ex}"[:300]))
+
     # ---- e2e through the public API with host buffers (pinned), copies inside
     pin_prof = torch.from_numpy(prof_host.view(np.uint8).copy()).pin_memory()
     pin_res = torch.empty(d_res.numel(), dtype=torch.uint8).pin_memory()
@@ -889,6 +955,7 @@ def main():
                                     "64 FP64 FMA/clk x 2 x 1.965 GHz, nominal (MEASURED_PEAKS.json has no FP64 "
                                     "figure); the kernel is issue-bound, DESIGN.md 7.3")),
             replicas=rep_line,
+            sharded=sharded,
             cpu_baseline=cpu,
             clocks=clk,
             gpu_launches=int(launches),

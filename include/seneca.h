@@ -193,6 +193,24 @@ typedef struct {
                                       refills (DESIGN.md R-O24); refills and
                                       admissions are both counted in d_refilled               */
     uint32_t        _pad1;
+    /* Sample-ID-range sharding of ONE replay (north_star "partitioned by
+     * sample-ID range ... all-gathering per-shard candidate counts and selections each
+     * batch").  Shard g of G keeps the pool counts of the ids of superblocks
+     * [g*ceil(NS/G), (g+1)*ceil(NS/G)) (NS = ceil(N/4096)) and resolves the substitute /
+     * refill ranks that fall into them; requests, classification, responses, seen and
+     * consumer sets and eviction decisions are replicated on every shard.  Per round and
+     * job two exchanges through device mailboxes: C1 = every shard's pool sizes, C2 = the
+     * ids each shard resolved (the maintain CTA: the storage pool and the refill ids).
+     * Results are identical for every G.                               */
+    uint32_t        shards;        /* G, 0 or 1: unsharded; 2..8                                  */
+    uint32_t        shard_rank;    /* shard_mode 1: this context's shard g < G                     */
+    uint32_t        shard_mode;    /* 0: all G shards in this context on this device (one launch of
+                                      G x (n_jobs + 1) CTAs; exchange through its own workspace);
+                                      1: this context is shard shard_rank only (one per device);
+                                      the peers' mailboxes are attached with seneca_shard_attach
+                                      before the first round.  Both need replicas <= 1 and
+                                      request_mode 0.                                         */
+    uint32_t        _pad2;
 } seneca_cache_config;
 
 /* Per job-epoch counters (R-O10; digest in DESIGN.md §3).  104 bytes.       */
@@ -253,8 +271,10 @@ typedef struct {
     uint64_t epoch[32];                 /* host mirror: current epoch of each job          */
     uint64_t consumed[32];              /* host mirror: samples consumed in current epoch  */
     uint32_t active_mask;               /* bit j set while job j has not departed          */
-    uint32_t replicas;                  /* R; every d_ pointer above is replica 0's --      */
-    uint64_t replica_stride;            /* replica k's is at + k * replica_stride bytes     */
+    uint32_t replicas;                  /* R slices (replicas, or the G shards of an emulated
+                                           sharded replay); every d_ pointer above is slice
+                                           0's --                                          */
+    uint64_t replica_stride;            /* slice k's is at + k * replica_stride bytes       */
 } seneca_state_view;
 
 /* Workspace size for cfg (bytes, 256-aligned pieces; replicas x one replica's).
@@ -306,6 +326,16 @@ seneca_status seneca_replay_rounds(seneca_ctx* ctx, uint64_t n_rounds, uint64_t*
                                    uint64_t* h_rounds, void* stream);
 
 seneca_status seneca_read_state(const seneca_ctx* ctx, seneca_state_view* out);
+
+/* Sharding with one shard per context (shard_mode 1).  seneca_shard_mailbox
+ * returns this shard's mailbox (inside the workspace; peers write into it) so
+ * the caller can map it into the other processes (e.g. CUDA IPC);
+ * seneca_shard_attach takes d_peer_mailboxes[shards] -- every shard's mailbox
+ * as addressable from this context's device (entry shard_rank may be NULL =
+ * its own).  Rounds are ESTATE until attached; EINVAL for an unsharded or
+ * shard_mode 0 context or a NULL peer.                                       */
+seneca_status seneca_shard_mailbox(const seneca_ctx* ctx, void** d_mailbox, size_t* bytes);
+seneca_status seneca_shard_attach(seneca_ctx* ctx, void* const* d_peer_mailboxes);
 
 /* Synchronise `stream` and report a latched device-side error (an internal
  * consistency check failing) as ESTATE.                                        */

@@ -61,13 +61,18 @@ class ODSContext:
     Readback methods take the replica index (default 0)."""
 
     def __init__(self, n_total, batch, target, cap_e, cap_d, cap_a, seed, request_mode=0,
-                 device="cuda", stream=None, replicas=1, evict_tiers=0, sampler=0, arrival=None, cold_start=0):
+                 device="cuda", stream=None, replicas=1, evict_tiers=0, sampler=0, arrival=None, cold_start=0,
+                 shards=1, shard_rank=0, shard_mode=0):
+        """shards > 1: ONE replay partitioned by sample-ID range; with
+        shard_mode 0 all shards run in this context (slice k = shard k, each with
+        the replicated state; readback index = shard)."""
         torch = _torch()
         self.torch = torch
         self.cfg = seneca.make_config(int(n_total), list(batch), list(target), int(cap_e), int(cap_d),
                                       int(cap_a), int(seed), request_mode, int(replicas), int(evict_tiers),
-                                      int(sampler), arrival, int(cold_start))
-        self.R = int(replicas)
+                                      int(sampler), arrival, int(cold_start), int(shards), int(shard_rank),
+                                      int(shard_mode))
+        self.R = int(shards) if int(shards) > 1 and int(shard_mode) == 0 else int(replicas)
         self.N, self.J = int(n_total), len(batch)
         self.bmax = max(batch)
         self.max_target = max(target)

@@ -53,6 +53,7 @@ constexpr uint32_t T_S = 0, T_E = 1, T_D = 2, T_A = 3, SUBST = 4;
 constexpr uint32_t kNewCons = 0x80;          // internal s_osrc flag: consumer set joined this round
 constexpr uint32_t kMaxJobs = 32;
 constexpr uint32_t kMaxReplicas = 64;        // independent replay instances per context
+constexpr uint32_t kMaxShards = 8;           // sample-ID-range shards of one replay
 constexpr uint32_t kMaxBatch = 4096;
 #ifndef SENECA_ODS_THREADS
 #define SENECA_ODS_THREADS 512
@@ -86,6 +87,8 @@ struct Cfg {
     uint32_t cold;                   // cold start (R-O24): empty tiers, round-end admission until full
     uint32_t Nrow;                   // row stride of the permutation / lap lists (N rounded up to 64)
     uint32_t FL;                     // capacity of one refill buffer
+    uint32_t G;                      // sample-ID-range shards (1: unsharded), SURVEY §8(e)
+    uint32_t mb_c1, mb_c2, mb_rf, mb_fl;   // mailbox offsets (u32) of the shard exchange, see Lay.mbox
     uint64_t seed;
     uint32_t batch[kMaxJobs];
     uint32_t target[kMaxJobs];
@@ -127,6 +130,16 @@ struct Lay {
                                      //     maintain rounds applied, eviction ring position (control block)
     unsigned long long *phase;       // [32] accumulated cycles per phase (see seneca.h)
     uint64_t seed;                   // this replica's seed (cfg seed + replica index)
+    // sample-ID-range sharding: this slice is shard `shard` of G and
+    // keeps the pool counts of ids [id_lo, id_hi) = superblocks [sb_lo, sb_hi) only;
+    // everything else is replicated.  Unsharded: shard 0 of 1, the whole range.
+    uint32_t shard, sb_lo, sb_hi, id_lo, id_hi;
+    uint32_t *mbox;                  // this shard's mailbox (peers write into it):
+                                     //   c1 [2][J+1][G][4]  per-shard pool totals (stamp, 3 values)
+                                     //   c2 [2][J][Bmax]    resolved substitute ids
+                                     //   rf [2][FL]         resolved refill ids
+                                     //   fl [2][J+1][G]     "ids of round r written" stamps
+    uint32_t *peer[kMaxShards];      // every shard's mailbox as seen from here (peer[shard] == mbox)
 };
 
 // Per-replica layouts: a kernel parameter (constant bank), indexed by the CTA's
@@ -167,6 +180,90 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+// ------------------------------------------------------------------ shard exchange
+// Mailboxes live in device memory of the receiving shard: in one context (all
+// shards on one device, emulation) the peers' slices of the same workspace; with
+// one shard per device, peer memory mapped over NVLink.  Writers store payloads,
+// then release a per-(round parity, slot, sender) stamp = round + 1 at system
+// scope; readers acquire every sender's stamp, then read the payload uncached.
+// Round parity double-buffers: every shard waits for every other shard's round-r
+// values before it can publish round r + 1's, so a buffer is never overwritten
+// while a peer may still read it.
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t ld_mbox(const uint32_t* p) { return __ldcv(p); }
+
+// Failure detection for the exchange: a peer that has not published within
+// kPeerTimeoutNs (a dead or never-launched shard) latches err bit 4 and traps
+// the launch instead of spinning forever.
+constexpr unsigned long long kPeerTimeoutNs = 20ull * 1000 * 1000 * 1000;
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void wait_stamp(const Lay& L, const uint32_t* p, uint32_t stamp) {
+    if (ld_acquire_sys(p) == stamp) return;
+    const unsigned long long t0 = globaltimer_ns();
+    while (ld_acquire_sys(p) != stamp) {
+        __nanosleep(64);
+        if (globaltimer_ns() - t0 > kPeerTimeoutNs) { atomicOr(L.err, 4u); __threadfence_system(); __trap(); }
+    }
+}
+
+// C1 (thread 0 of the calling CTA): publish (v0, v1, v2) of slot s for round r to
+// every shard, wait for every shard's, return them in out[g][0..2].
+__device__ void shard_c1(const Lay& L, const Cfg& C, uint32_t slot, uint64_t r, uint32_t v0, uint32_t v1, uint32_t v2,
+                         uint32_t (*out)[3]) {
+    const uint32_t stamp = (uint32_t)r + 1u;
+    const size_t row = (((size_t)(r & 1) * (C.J + 1) + slot) * C.G) * 4;
+    for (uint32_t g = 0; g < C.G; ++g) {
+        uint32_t* q = L.peer[g] + C.mb_c1 + row + (size_t)L.shard * 4;
+        q[1] = v0; q[2] = v1; q[3] = v2;
+    }
+    __threadfence_system();
+    for (uint32_t g = 0; g < C.G; ++g) st_release_sys(L.peer[g] + C.mb_c1 + row + (size_t)L.shard * 4, stamp);
+    for (uint32_t g = 0; g < C.G; ++g) {
+        const uint32_t* q = L.mbox + C.mb_c1 + row + (size_t)g * 4;
+        wait_stamp(L, q, stamp);
+        out[g][0] = ld_mbox(q + 1); out[g][1] = ld_mbox(q + 2); out[g][2] = ld_mbox(q + 3);
+    }
+}
+
+// C2 flags (every thread calls it after storing its resolved ids into every
+// shard's mailbox): the barrier orders the CTA's stores before thread 0's
+// system-scope fence and release, then thread 0 waits for every shard's stamp.
+__device__ void shard_c2_sync(const Lay& L, const Cfg& C, uint32_t slot, uint64_t r) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t stamp = (uint32_t)r + 1u;
+        const size_t row = ((size_t)(r & 1) * (C.J + 1) + slot) * C.G;
+        __threadfence_system();
+        for (uint32_t g = 0; g < C.G; ++g) st_release_sys(L.peer[g] + C.mb_fl + row + L.shard, stamp);
+        for (uint32_t g = 0; g < C.G; ++g) wait_stamp(L, L.mbox + C.mb_fl + row + g, stamp);
+    }
+    __syncthreads();
+}
+
+// The shard owning global pool rank `rank` of pool column t (counts cnt[g][t],
+// shards in ascending id order) and the rank within that shard.
+__device__ __forceinline__ uint32_t shard_owner(const Cfg& C, const uint32_t (*cnt)[3], uint32_t t, uint32_t rank,
+                                                uint32_t* local) {
+    uint32_t acc = 0, g = 0;
+    for (; g + 1 < C.G; ++g) {
+        if (rank < acc + cnt[g][t]) break;
+        acc += cnt[g][t];
+    }
+    *local = rank - acc;
+    return g;
+}
+
 __device__ __forceinline__ uint32_t valid_mask(const Cfg& C, uint32_t w) {
     const uint64_t lo = (uint64_t)w * 32u;
     if (lo + 32u <= C.N) return 0xffffffffu;
@@ -182,11 +279,15 @@ __device__ __forceinline__ uint32_t pool_of(uint32_t j, uint32_t t) {   // t: T_
 // byte is updated with a 32-bit add of +-1 shifted into place -- a count never
 // leaves [0, 128], so no carry/borrow crosses bytes), and a u32 count per
 // 4096-id superblock in the shared memory of the CTA that owns the pool.
-__device__ __forceinline__ void count_add(const Lay& L, const Cfg& C, uint32_t pidx, uint32_t id, uint32_t delta,
+// kSh: a shard counts only the ids of its own range (returns whether it did).
+template <bool kSh = false>
+__device__ __forceinline__ bool count_add(const Lay& L, const Cfg& C, uint32_t pidx, uint32_t id, uint32_t delta,
                                           uint32_t* s_sup_pool) {
+    if (kSh && (id < L.id_lo || id >= L.id_hi)) return false;
     const uint32_t blk = id >> kBlockShift;
     atomicAdd(L.cnt8 + (size_t)pidx * (C.NBp >> 2) + (blk >> 2), delta << (8u * (blk & 3u)));
     atomicAdd(s_sup_pool + (id >> kSuperShift), delta);
+    return true;
 }
 
 // Exclusive prefix of the superblock counts (shared memory -> shared memory).
@@ -317,6 +418,8 @@ struct JobSmem {
     uint32_t cur_buf, nxt_buf, cursor, cur_len, nxt_len;
     uint32_t wrap_slot, need, newcursor, walk_err;
     uint32_t m, k[3], tot[3], hits[3];
+    uint32_t hits_loc[3], own[3], glob[3];   // sharded: hits / substitutes in this shard's range, global pool sizes
+    uint32_t cnt[kMaxShards][3];             // sharded: every shard's pool sizes of this round (C1)
     uint32_t recount;
     uint32_t perm_seen;   // epoch+1 whose permutation was observed published (0: none)
     float dens;           // unseen fraction observed by the last walk step (window sizing)
@@ -548,7 +651,7 @@ __device__ void job_recount(const Lay& L, const Cfg& C, uint32_t j, uint32_t* s_
     const uint32_t* cj = L.cons + (size_t)j * C.NW;
     const uint32_t* sj = L.seen + (size_t)j * C.NW;
     uint32_t ta = 0, td = 0, te = 0;
-    for (uint32_t g = tid; g < (C.NBp >> 2); g += T) {          // 4 blocks = 16 words per step
+    for (uint32_t g = L.sb_lo * 8 + tid; g < L.sb_hi * 8; g += T) {   // 4 blocks = 16 words per step (own shard)
         uint32_t pa = 0, pd = 0, pe = 0;
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
@@ -579,8 +682,12 @@ __device__ void job_recount(const Lay& L, const Cfg& C, uint32_t j, uint32_t* s_
     __syncthreads();
 }
 
-// a3-a6 for job j in round r: classify, substitute, respond.
-template <class TMr>
+// a3-a6 for job j in round r: classify, substitute, respond.  kSh: this CTA is
+// one shard of a sample-ID-range-sharded replay: classification,
+// ranks and responses are replicated; the pool counts and the rank -> id
+// selection cover this shard's range, with two exchanges per round (C1: every
+// shard's pool sizes; C2: the ids each shard resolved).
+template <bool kSh, class TMr>
 __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& S, uint32_t* s_req, uint32_t* s_miss,
                           uint32_t* s_sub, uint32_t* s_oid, uint8_t* s_osrc, uint32_t* s_pre, uint32_t j, uint64_t r,
                           uint32_t e, uint32_t nbase, uint32_t n_act, TMr& TM, const uint32_t* s_win,
@@ -618,8 +725,10 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
                 else if (C.evict_all && !(atomicOr(cons_j + w, b) & b)) flag = kNewCons;
                 s_osrc[s] = (uint8_t)(t | flag);
                 atomicOr(seen_j + w, b);
-                count_add(L, C, pool_of(j, t), i, 0xffffffffu, s_sup + (pool_of(j, t) - j * 3) * C.NS);
+                const bool mine = count_add<kSh>(L, C, pool_of(j, t), i, 0xffffffffu,
+                                                 s_sup + (pool_of(j, t) - j * 3) * C.NS);
                 atomicAdd(&S.hits[t == T_A ? 0 : (t == T_D ? 1 : 2)], 1u);
+                if (kSh && mine) atomicAdd(&S.hits_loc[t == T_A ? 0 : (t == T_D ? 1 : 2)], 1u);
             } else {
                 is_miss = true;
             }
@@ -630,8 +739,17 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
         mbase += tot;
     }
     if (tid == 0) {
-        const uint32_t pa = S.tot[0] - S.hits[0], pd = S.tot[1] - S.hits[1], pe = S.tot[2] - S.hits[2];
-        S.tot[0] = pa; S.tot[1] = pd; S.tot[2] = pe;
+        uint32_t pa, pd, pe;                 // the pools' sizes after this round's hits
+        if constexpr (kSh) {
+            S.tot[0] -= S.hits_loc[0]; S.tot[1] -= S.hits_loc[1]; S.tot[2] -= S.hits_loc[2];
+            shard_c1(L, C, j, r, S.tot[0], S.tot[1], S.tot[2], S.cnt);          // C1
+            pa = pd = pe = 0;
+            for (uint32_t g = 0; g < C.G; ++g) { pa += S.cnt[g][0]; pd += S.cnt[g][1]; pe += S.cnt[g][2]; }
+            S.glob[0] = pa; S.glob[1] = pd; S.glob[2] = pe;
+        } else {
+            pa = S.tot[0] - S.hits[0]; pd = S.tot[1] - S.hits[1]; pe = S.tot[2] - S.hits[2];
+            S.tot[0] = pa; S.tot[1] = pd; S.tot[2] = pe;
+        }
         const uint32_t m = mbase;
         S.m = m;
         S.k[0] = C.baseline ? 0u : min(m, pa);                  // R-O22: no substitution
@@ -653,13 +771,37 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
             const uint32_t ul = u - (tt == 0 ? 0u : (tt == 1 ? k0 : k0 + k1));
             const uint32_t t = tt == 0 ? T_A : (tt == 1 ? T_D : T_E);
             const uint64_t key = derive_key(L.seed, PUR_SUB, j, r, t);
-            const uint32_t rank = perm_apply(key, perm_domain(S.tot[tt]), ul);
-            const uint32_t id = pool_select(L, C, j * 3 + tt, t, j, s_pre + tt * C.NS, rank);
-            const uint32_t s = s_miss[u];
-            if (P.out_ids) { P.out_ids[row + s] = id; P.out_src[row + s] = (uint8_t)(t | SUBST); }
-            s_oid[s] = id;
-            s_osrc[s] = (uint8_t)(t | SUBST);
-            s_sub[u] = id;
+            const uint32_t rank = perm_apply(key, perm_domain(kSh ? S.glob[tt] : S.tot[tt]), ul);
+            if constexpr (kSh) {
+                // the shard whose range holds global rank `rank` resolves it and
+                // stores the id into every shard's mailbox (C2)
+                uint32_t local;
+                if (shard_owner(C, S.cnt, tt, rank, &local) == L.shard) {
+                    const uint32_t id = pool_select(L, C, j * 3 + tt, t, j, s_pre + tt * C.NS, local);
+                    const size_t at = C.mb_c2 + ((size_t)(r & 1) * C.J + j) * C.Bmax + u;
+                    for (uint32_t g = 0; g < C.G; ++g) L.peer[g][at] = id;
+                    atomicAdd(&S.own[tt], 1u);
+                }
+            } else {
+                const uint32_t id = pool_select(L, C, j * 3 + tt, t, j, s_pre + tt * C.NS, rank);
+                const uint32_t s = s_miss[u];
+                if (P.out_ids) { P.out_ids[row + s] = id; P.out_src[row + s] = (uint8_t)(t | SUBST); }
+                s_oid[s] = id;
+                s_osrc[s] = (uint8_t)(t | SUBST);
+                s_sub[u] = id;
+            }
+        }
+        if constexpr (kSh) {
+            shard_c2_sync(L, C, j, r);                                             // C2
+            const uint32_t* in = L.mbox + C.mb_c2 + ((size_t)(r & 1) * C.J + j) * C.Bmax;
+            for (uint32_t u = tid; u < q; u += T) {
+                const uint32_t t = u < k0 ? T_A : (u < k0 + k1 ? T_D : T_E);
+                const uint32_t id = ld_mbox(in + u), s = s_miss[u];
+                if (P.out_ids) { P.out_ids[row + s] = id; P.out_src[row + s] = (uint8_t)(t | SUBST); }
+                s_oid[s] = id;
+                s_osrc[s] = (uint8_t)(t | SUBST);
+                s_sub[u] = id;
+            }
         }
         __syncthreads();
         TM.tick(9);
@@ -670,7 +812,7 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
             atomicOr(seen_j + w, b);
             if (tt == 0) { atomicOr(cons_j + w, b); s_osrc[s_miss[u]] |= kNewCons; }
             else if (C.evict_all && !(atomicOr(cons_j + w, b) & b)) s_osrc[s_miss[u]] |= kNewCons;
-            count_add(L, C, j * 3 + tt, id, 0xffffffffu, s_sup + tt * C.NS);
+            count_add<kSh>(L, C, j * 3 + tt, id, 0xffffffffu, s_sup + tt * C.NS);
         }
     }
     __syncthreads();
@@ -709,9 +851,14 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
     TM.tick(10);
     if (tid == 0) {
         if (P.mode == 0) { S.cur_len += q1; S.nxt_len += q - q1; }
-        S.tot[0] -= k0;
-        S.tot[1] -= k1;
-        S.tot[2] -= k2;
+        if constexpr (kSh) {                 // this shard's own substitutes leave its pools
+            S.tot[0] -= S.own[0]; S.tot[1] -= S.own[1]; S.tot[2] -= S.own[2];
+            S.own[0] = S.own[1] = S.own[2] = 0;
+        } else {
+            S.tot[0] -= k0;
+            S.tot[1] -= k1;
+            S.tot[2] -= k2;
+        }
     }
 
     // a6: digest, transcript; a tracked entry whose consumer count reaches
@@ -758,7 +905,7 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
         S.acc_cnt[tid] += v;
     }
     __syncthreads();
-    if (tid < 3) S.hits[tid] = 0;      // for the next round (read above, barriers before its next use)
+    if (tid < 3) { S.hits[tid] = 0; S.hits_loc[tid] = 0; }   // for the next round (barriers before next use)
     TM.tick(3);
 }
 
@@ -786,18 +933,40 @@ struct MaintSmem {
     uint32_t ne_push, push_base;
     uint32_t add[kMaxJobs];
     uint32_t scan[33];
+    uint32_t PSg;                        // sharded: the global storage pool at round start (C1)
+    uint32_t pscnt[kMaxShards][3];       // sharded: every shard's storage pool ([g][0])
+    uint32_t ne_loc, k_loc;              // sharded: evictions / refills inside this shard's range
 };
 
 // keyed refill ranks rho(u) over the storage pool as of round start (R-O8),
 // located through the S-pool counts; the prefix s_pre must be loaded.
+// kSh: the global rank's owning shard resolves it into every shard's mailbox,
+// then every shard copies the complete list (C2 of the maintain CTA, slot J).
+template <bool kSh>
 __device__ void maint_refill_select(const Lay& L, const Cfg& C, MaintSmem& M, const uint32_t* s_pre, uint64_t r,
                                     uint32_t u0, uint32_t u1) {
     if (u1 <= u0) return;
     const uint64_t key = derive_key(L.seed, PUR_REFILL, 0, r, 0);
-    const PermDomain dom = perm_domain(M.PS);
+    const PermDomain dom = perm_domain(kSh ? M.PSg : M.PS);
     uint32_t* fill = L.fill_list + (size_t)(r & 1) * C.FL;
-    for (uint32_t u = u0 + threadIdx.x; u < u1; u += blockDim.x)
-        fill[u] = pool_select(L, C, 3 * C.J, T_S, 0, s_pre, perm_apply(key, dom, u));
+    for (uint32_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
+        const uint32_t rank = perm_apply(key, dom, u);
+        if constexpr (kSh) {
+            uint32_t local;
+            if (shard_owner(C, M.pscnt, 0, rank, &local) == L.shard) {
+                const uint32_t id = pool_select(L, C, 3 * C.J, T_S, 0, s_pre, local);
+                const size_t at = C.mb_rf + (size_t)(r & 1) * C.FL + u;
+                for (uint32_t g = 0; g < C.G; ++g) L.peer[g][at] = id;
+            }
+        } else {
+            fill[u] = pool_select(L, C, 3 * C.J, T_S, 0, s_pre, rank);
+        }
+    }
+    if constexpr (kSh) {
+        shard_c2_sync(L, C, C.J, r);
+        const uint32_t* in = L.mbox + C.mb_rf + (size_t)(r & 1) * C.FL;
+        for (uint32_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) fill[u] = ld_mbox(in + u);
+    }
     __syncthreads();
 }
 
@@ -805,7 +974,7 @@ __device__ void maint_refill_select(const Lay& L, const Cfg& C, MaintSmem& M, co
 // consumed by every active job (R-O5, R-O6, R-O21), refill from the storage pool
 // as of round start, tier by tier A -> D -> E from one keyed rank stream (R-O8,
 // R-O21), counts kept exact.
-template <class TMr>
+template <bool kSh, class TMr>
 __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSmem& M, uint32_t* s_pre,
                             uint32_t* s_supS, uint64_t r, uint32_t active, uint32_t part_of_round, bool full_scan,
                             bool speculated, uint32_t ne_push, uint32_t push_base, TMr& TM) {
@@ -815,6 +984,8 @@ __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSm
         M.ne_t[0] = M.ne_t[1] = M.ne_t[2] = M.ne_t[3] = 0;
         M.ned = 0;
         M.nadm = 0;
+        M.ne_loc = 0;
+        M.k_loc = 0;
     }
     __syncthreads();
     const bool admit = C.cold && !M.warm;
@@ -876,14 +1047,14 @@ __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSm
     }
     TM.tick(3);
     const uint32_t ne = M.ne;
-    uint32_t k = active ? min(M.deficit0 + ne, M.PS) : 0u;         // no refill with no active job
+    uint32_t k = active ? min(M.deficit0 + ne, kSh ? M.PSg : M.PS) : 0u;   // no refill with no active job
     if (admit) {
         k = active ? min(M.deficit0 + ne, M.nadm) : 0u;           // admissions instead of refills (R-O24)
     } else if (!speculated) {
         if (k) prefix_from_smem(C, s_supS, s_pre, M.scan);
-        maint_refill_select(L, C, M, s_pre, r, 0, k);
+        maint_refill_select<kSh>(L, C, M, s_pre, r, 0, k);
     } else if (k > M.kspec) {
-        maint_refill_select(L, C, M, s_pre, r, M.kspec, k);      // beyond the speculated ranks
+        maint_refill_select<kSh>(L, C, M, s_pre, r, M.kspec, k);  // beyond the speculated ranks
     }
     const uint32_t spidx = 3 * C.J;
     const uint32_t ring = C.J * C.Bmax;
@@ -900,7 +1071,7 @@ __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSm
         if (C.evict_all) atomicAdd(&M.ne_t[t], 1u);      // A only: ne_t[A] = ne (set below)
         for (uint32_t a = 0; a < C.J; ++a) atomicAnd(L.cons + (size_t)a * C.NW + w, ~b);
         L.cons_cnt[i] = 0;
-        count_add(L, C, spidx, i, 1u, s_supS);
+        if (count_add<kSh>(L, C, spidx, i, 1u, s_supS) && kSh) atomicAdd(&M.ne_loc, 1u);
     }
     if (!C.evict_all && tid == 0) M.ne_t[T_A] = ne;
     __syncthreads();
@@ -914,14 +1085,15 @@ __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSm
         const uint32_t i = ldcg(fill + u);
         uint32_t* bm = u < kA ? L.bm_a : (u < kA + kD ? L.bm_d : L.bm_e);
         atomicOr(bm + (i >> 5), 1u << (i & 31));
-        count_add(L, C, spidx, i, 0xffffffffu, s_supS);
+        if (count_add<kSh>(L, C, spidx, i, 0xffffffffu, s_supS) && kSh) atomicAdd(&M.k_loc, 1u);
     }
     __syncthreads();
     if (tid == 0) {
         uint32_t* fn = L.fill_n + (r & 1) * 4;
         fn[0] = k; fn[1] = kA; fn[2] = kD;
         L.ev_ed_n[r & 1] = M.ned;
-        M.PS = M.PS + ne - k;          // storage pool and tier sizes live in shared memory while running
+        M.PS = kSh ? M.PS + M.ne_loc - M.k_loc : M.PS + ne - k;   // storage pool and tier sizes live in
+                                                                   // shared memory while running
         M.size[T_A] += kA - M.ne_t[T_A];
         M.size[T_D] += kD - M.ne_t[T_D];
         M.size[T_E] += (k - kA - kD) - M.ne_t[T_E];
@@ -942,6 +1114,7 @@ __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSm
 // seen join the pool of their tier (empty consumer sets), and under
 // evict_tiers = ALL evicted E/D entries it has not seen leave its E/D pool (an
 // evicted A entry was consumed by j, so it was in no A pool of j).
+template <bool kSh>
 __device__ void job_take_refills(const Lay& L, const Cfg& C, JobSmem& S, uint32_t j, uint64_t r, uint32_t* s_sup) {
     const uint32_t* fn = L.fill_n + (r & 1) * 4;
     const uint32_t* fill = L.fill_list + (size_t)(r & 1) * C.FL;
@@ -955,8 +1128,9 @@ __device__ void job_take_refills(const Lay& L, const Cfg& C, JobSmem& S, uint32_
         const uint32_t i = u == threadIdx.x ? i0 : ldcg(fill + u);
         if (!((ldcg(seen_j + (i >> 5)) >> (i & 31)) & 1u)) {
             const uint32_t tt = u < kA ? 0u : (u < kA + kD ? 1u : 2u);
-            count_add(L, C, j * 3 + tt, i, 1u, s_sup + tt * C.NS);
-            addA += tt == 0; addD += tt == 1; addE += tt == 2;
+            if (count_add<kSh>(L, C, j * 3 + tt, i, 1u, s_sup + tt * C.NS)) {
+                addA += tt == 0; addD += tt == 1; addE += tt == 2;
+            }
         }
     }
     if (C.evict_all) {
@@ -966,8 +1140,9 @@ __device__ void job_take_refills(const Lay& L, const Cfg& C, JobSmem& S, uint32_
             const uint32_t x = ldcg(ev + u), i = x & 0x7fffffffu;
             if (!((ldcg(seen_j + (i >> 5)) >> (i & 31)) & 1u)) {
                 const uint32_t tt = (x >> 31) ? 2u : 1u;
-                count_add(L, C, j * 3 + tt, i, 0xffffffffu, s_sup + tt * C.NS);
-                addD -= tt == 1; addE -= tt == 2;   // wraps; the sums below are mod 2^32
+                if (count_add<kSh>(L, C, j * 3 + tt, i, 0xffffffffu, s_sup + tt * C.NS)) {
+                    addD -= tt == 1; addE -= tt == 2;   // wraps; the sums below are mod 2^32
+                }
             }
         }
     }
@@ -984,7 +1159,7 @@ __device__ void job_take_refills(const Lay& L, const Cfg& C, JobSmem& S, uint32_
 // ------------------------------------------------------------------ the persistent round kernel
 // Grid: (J + 1) CTAs per replica; replicas are independent replays (their own
 // workspace slice and seed) that share nothing but the launch.
-template <bool kTime, bool kCoupled>
+template <bool kTime, bool kCoupled, bool kShard>
 __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, const Launch& P) {
     extern __shared__ __align__(16) uint32_t smem[];
     __shared__ JobSmem S;
@@ -1128,6 +1303,7 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
             M.deficit0 = M.def[T_A] + M.def[T_D] + M.def[T_E];
         };
         auto speculate = [&](uint64_t r, uint32_t part, uint32_t departing) -> bool {
+            if (kShard) return false;            // sharded: refill ranks resolved after C1 of the storage pool
             const uint32_t active_after = s_active & ~departing;
             if (!(active_after && C.cap_t > 0) || departing || (C.cold && !M.warm)) return false;
             if (tid == 0) set_deficits();
@@ -1140,7 +1316,7 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
             __syncthreads();
             if (M.kspec) prefix_from_smem(C, s_sup, s_pre, M.scan);
             TM.tick(0);
-            maint_refill_select(L, C, M, s_pre, r, 0, M.kspec);
+            maint_refill_select<false>(L, C, M, s_pre, r, 0, M.kspec);
             TM.tick(1);
             return true;
         };
@@ -1155,6 +1331,12 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
             schedule(part, departing);
             const uint32_t active_after = s_active & ~departing;
             expect += __popc(part);
+            if (kShard && tid == 0) {        // C1 of the storage pool as of round start
+                shard_c1(L, C, C.J, r, M.PS, 0u, 0u, M.pscnt);
+                uint32_t t = 0;
+                for (uint32_t g = 0; g < C.G; ++g) t += M.pscnt[g][0];
+                M.PSg = t;
+            }
             if (tid == 0) {                  // job phases of round r done; evictions they pushed
                 unsigned long long v;
                 while ((uint32_t)(v = ld_acquire64(L.bar)) < expect) { }
@@ -1171,8 +1353,8 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
             if ((active_after || (departing && s_pending)) && (C.cap_t > 0 || (C.cold && !M.warm))) {
                 if (!spec && tid == 0) set_deficits();
                 __syncthreads();
-                maint_apply(L, C, P, M, s_pre, s_sup, r, active_after, part, departing != 0, spec, M.ne_push,
-                            M.push_base, TM);
+                maint_apply<kShard>(L, C, P, M, s_pre, s_sup, r, active_after, part, departing != 0, spec,
+                                    M.ne_push, M.push_base, TM);
             } else if (tid == 0) {          // nothing maintained: the job CTAs take an empty round
                 uint32_t* fn = L.fill_n + (r & 1) * 4;
                 fn[0] = fn[1] = fn[2] = 0;
@@ -1217,9 +1399,9 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
             if (C.cold && tid == 0) S.warm = ldcg(L.warm);        // stable until this round's maintain
             if ((part >> j) & 1u) {
                 if (S.recount) { job_recount(L, C, j, s_sup, S.tot); if (tid == 0) S.recount = 0; __syncthreads(); }
-                else if (coupled && rr > 0) { job_take_refills(L, C, S, j, r - 1, s_sup); __syncthreads(); }
+                else if (coupled && rr > 0) { job_take_refills<kShard>(L, C, S, j, r - 1, s_sup); __syncthreads(); }
                 TM.tick(0);
-                job_round(L, C, P, S, s_req, s_miss, s_sub, s_oid, s_osrc, s_pre, j, r, s_e[j], s_n[j],
+                job_round<kShard>(L, C, P, S, s_req, s_miss, s_sub, s_oid, s_osrc, s_pre, j, r, s_e[j], s_n[j],
                           __popc(active_after), TM, s_win, s_wseen, s_sup);
                 // a8 (R-O16): the epoch ends with this batch -> reset seen_j and the walk
                 if (s_n[j] + S.need == C.N) {
@@ -1263,7 +1445,7 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
         if (coupled && P.rounds > 0 && (s_active >> j & 1u)) {
             if (tid == 0) { while (ld_acquire(L.bar + 2) < P.rounds) { } }
             __syncthreads();
-            if (!S.recount) job_take_refills(L, C, S, j, P.r0 + P.rounds - 1, s_sup);
+            if (!S.recount) job_take_refills<kShard>(L, C, S, j, P.r0 + P.rounds - 1, s_sup);
             __syncthreads();
         }
         if (tid < 3) L.cnt_tot[j * 3 + tid] = S.tot[tid];
@@ -1293,13 +1475,23 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
 template <bool kTime, bool kCoupled>
 __global__ void __launch_bounds__(kThreads, 1)
 ods_rounds(const __grid_constant__ Lays LS, const __grid_constant__ Cfg C, const __grid_constant__ Launch P) {
-    ods_rounds_body<kTime, kCoupled>(LS, C, P);
+    ods_rounds_body<kTime, kCoupled, false>(LS, C, P);
 }
 
 template <bool kTime, bool kCoupled>
 __global__ void __launch_bounds__(kThreads / 2, 2)
 ods_rounds_x2(const __grid_constant__ Lays LS, const __grid_constant__ Cfg C, const __grid_constant__ Launch P) {
-    ods_rounds_body<kTime, kCoupled>(LS, C, P);
+    ods_rounds_body<kTime, kCoupled, false>(LS, C, P);
+}
+
+// One shard of a sample-ID-range-sharded replay per (J + 1)-CTA group (SURVEY
+// §8(e)): the slices of one launch are the shards of ONE replay (emulation on
+// one device), or the launch is this device's shard and its peers' mailboxes
+// are mapped peer memory.
+template <bool kTime, bool kCoupled>
+__global__ void __launch_bounds__(kThreads, 1)
+ods_rounds_sh(const __grid_constant__ Lays LS, const __grid_constant__ Cfg C, const __grid_constant__ Launch P) {
+    ods_rounds_body<kTime, kCoupled, true>(LS, C, P);
 }
 
 // 256 threads, one CTA per SM: independent jobs whose longest chain of rounds
@@ -1307,12 +1499,16 @@ ods_rounds_x2(const __grid_constant__ Lays LS, const __grid_constant__ Cfg C, co
 template <bool kTime, bool kCoupled>
 __global__ void __launch_bounds__(kThreads / 2, 1)
 ods_rounds_half(const __grid_constant__ Lays LS, const __grid_constant__ Cfg C, const __grid_constant__ Launch P) {
-    ods_rounds_body<kTime, kCoupled>(LS, C, P);
+    ods_rounds_body<kTime, kCoupled, false>(LS, C, P);
 }
 
 // the round kernel for (variant: 0 512 threads, 1 256 threads two CTAs per SM,
 // 2 256 threads one CTA per SM; phase counters; coupled)
 const void* round_kernel(int variant, bool timed, bool coupled) {
+    if (variant == 3) {
+        if (coupled) return timed ? (const void*)ods_rounds_sh<true, true> : (const void*)ods_rounds_sh<false, true>;
+        return timed ? (const void*)ods_rounds_sh<true, false> : (const void*)ods_rounds_sh<false, false>;
+    }
     if (variant == 2) {
         if (coupled) return timed ? (const void*)ods_rounds_half<true, true> : (const void*)ods_rounds_half<false, true>;
         return timed ? (const void*)ods_rounds_half<true, false> : (const void*)ods_rounds_half<false, false>;
@@ -1450,7 +1646,7 @@ ods_recount_all(const __grid_constant__ Lays LS, const __grid_constant__ Cfg C) 
     __shared__ uint32_t s_tot[4];                                  // this CTA's pool totals: S, A, D, E
     if (threadIdx.x < 4) s_tot[threadIdx.x] = 0;
     __syncthreads();
-    const bool live = sblk < C.NS;
+    const bool live = sblk >= L.sb_lo && sblk < L.sb_hi;      // this shard's superblocks (all: unsharded)
     const uint32_t blk = sblk * 32 + lane, w0 = blk * kWordsPerBlock;
     const uint4 z4 = make_uint4(0, 0, 0, 0);
     const uint4 a = live ? __ldcs(reinterpret_cast<const uint4*>(L.bm_a + w0)) : z4;
@@ -1553,6 +1749,8 @@ struct seneca_ctx {
     uint64_t arrival[kMaxJobs];
     uint64_t r;
     uint64_t gen_hi[kMaxJobs];     // permutations of epochs < gen_hi[j] have been generated (ring, C.K slots)
+    uint32_t shard_mode;           // sharded (C.G > 1): 0 all shards in this context, 1 one shard
+    bool attached;                 // shard_mode 1: the peers' mailboxes are known
     uint64_t launches;
     uint64_t klaunch[K_NCLASS];
     double kms[K_NCLASS];
@@ -1590,6 +1788,16 @@ seneca_status check_cfg(const seneca_cache_config* cfg) {
     if (cfg->cold_start > 1) { set_error("cold_start must be 0 or 1"); return SENECA_EINVAL; }
     if (cfg->replicas > 1 && cfg->request_mode != 0) {
         set_error("caller-supplied requests (request_mode 1) need replicas <= 1"); return SENECA_EINVAL;
+    }
+    if (cfg->shards > kMaxShards) { set_error("shards must be <= %u", kMaxShards); return SENECA_EINVAL; }
+    if (cfg->shards > 1) {
+        if (cfg->shard_mode > 1) { set_error("shard_mode must be 0 (all shards here) or 1 (one)"); return SENECA_EINVAL; }
+        if (cfg->shard_mode == 1 && cfg->shard_rank >= cfg->shards) {
+            set_error("shard_rank must be < shards"); return SENECA_EINVAL;
+        }
+        if (cfg->replicas > 1 || cfg->request_mode != 0) {
+            set_error("a sharded replay needs replicas <= 1 and request_mode 0"); return SENECA_EINVAL;
+        }
     }
     if (cfg->cap_e > cfg->n_total || cfg->cap_d > cfg->n_total || cfg->cap_a > cfg->n_total ||
         cfg->cap_e + cfg->cap_d + cfg->cap_a > cfg->n_total) {
@@ -1633,6 +1841,12 @@ Sizes compute_sizes(const seneca_cache_config* cfg) {
     C.seed = cfg->seed;
     C.Nrow = (C.N + 63) & ~63u;
     C.FL = (uint32_t)(std::max<size_t>(C.cap_t, 1) + (size_t)C.J * C.Bmax);
+    C.G = cfg->shards > 1 ? cfg->shards : 1u;
+    C.mb_c1 = 0;
+    C.mb_c2 = C.mb_c1 + 2 * (C.J + 1) * C.G * 4;
+    C.mb_rf = C.mb_c2 + 2 * C.J * C.Bmax;
+    C.mb_fl = C.mb_rf + (C.G > 1 ? 2 * C.FL : 0u);
+    const size_t mbox_u32 = C.G > 1 ? (size_t)C.mb_fl + 2 * (C.J + 1) * C.G : 1;
     const size_t W = (size_t)C.NW * 4, P = 3 * (size_t)C.J + 1;
     const size_t capl = std::max<size_t>(C.cap_t, 1) * 4;
     const size_t edl = std::max<size_t>(C.cap_e + C.cap_d, 1) * 4;
@@ -1655,6 +1869,7 @@ Sizes compute_sizes(const seneca_cache_config* cfg) {
         C.cold ? (size_t)C.J * C.Bmax * 4 : 4, (size_t)C.J * 4,   // 29-30 fetch, fetch_n
         4, C.cold ? W : 4,                                  // 31-32 warm, claim
         (size_t)C.J * 4, 4,                                 // 33-34 epoch_at, gen_next
+        mbox_u32 * 4,                                       // 35 shard mailbox
     };
     size_t at = 0;
     for (size_t k = 0; k < sizeof(sz) / sizeof(sz[0]); ++k) {
@@ -1663,6 +1878,7 @@ Sizes compute_sizes(const seneca_cache_config* cfg) {
     }
     z.total = at;
     z.R = cfg->replicas ? cfg->replicas : 1;
+    if (C.G > 1 && cfg->shard_mode == 0) z.R = C.G;          // emulation: one slice per shard
     return z;
 }
 
@@ -1705,6 +1921,9 @@ Lay carve(const Sizes& z, char* base, char* ctl, uint64_t seed) {
     L.claim = (uint32_t*)(base + z.off[32]);
     L.epoch_at = (uint32_t*)(base + z.off[33]);
     L.gen_next = (uint32_t*)(base + z.off[34]);
+    L.mbox = (uint32_t*)(base + z.off[35]);
+    for (uint32_t g = 0; g < kMaxShards; ++g) L.peer[g] = nullptr;
+    L.shard = 0; L.sb_lo = 0; L.sb_hi = z.C.NS; L.id_lo = 0; L.id_hi = z.C.NS * 4096u;
     return L;
 }
 
@@ -1888,6 +2107,7 @@ seneca_status launch_rounds(seneca_ctx* c, uint64_t* Rio, uint32_t jobs_mask, co
                             uint32_t* out_ids, uint8_t* out_src, uint32_t out_stride, const uint32_t* row_of_job,
                             unsigned long long* transcript, cudaStream_t st) {
     uint64_t R = *Rio;
+    if (!c->attached) { set_error("sharded context: attach the peers' mailboxes first"); return SENECA_ESTATE; }
     Launch P;
     std::memset(&P, 0, sizeof P);
     P.r0 = c->r;
@@ -1992,8 +2212,30 @@ extern "C" seneca_status seneca_init_cache(const seneca_cache_config* cfg, void*
     c->R = z.R;
     c->rep_stride = z.total;
     c->ctl = (char*)d_workspace;
-    for (uint32_t k = 0; k < z.R; ++k)
-        c->LS.r[k] = carve(z, (char*)d_workspace + ctl_bytes(z.R) + k * z.total, c->ctl + k * kCtlBytes, cfg->seed + k);
+    const bool sharded = z.C.G > 1;
+    c->shard_mode = sharded ? cfg->shard_mode : 0u;
+    c->attached = !sharded || cfg->shard_mode == 0;
+    for (uint32_t k = 0; k < z.R; ++k) {
+        // emulated shards replay ONE instance: every slice has the configured seed
+        c->LS.r[k] = carve(z, (char*)d_workspace + ctl_bytes(z.R) + k * z.total, c->ctl + k * kCtlBytes,
+                           sharded ? cfg->seed : cfg->seed + k);
+        if (sharded) {
+            Lay& L = c->LS.r[k];
+            const uint32_t g = cfg->shard_mode == 0 ? k : cfg->shard_rank;
+            const uint32_t per = (z.C.NS + z.C.G - 1) / z.C.G;
+            L.shard = g;
+            L.sb_lo = std::min(z.C.NS, g * per);
+            L.sb_hi = std::min(z.C.NS, (g + 1) * per);
+            L.id_lo = L.sb_lo * 4096u;
+            L.id_hi = L.sb_hi * 4096u;
+        }
+    }
+    if (sharded) {
+        for (uint32_t k = 0; k < z.R; ++k)
+            for (uint32_t g = 0; g < z.C.G; ++g)
+                c->LS.r[k].peer[g] = cfg->shard_mode == 0 ? c->LS.r[g].mbox
+                                                          : (g == c->LS.r[k].shard ? c->LS.r[k].mbox : nullptr);
+    }
     c->L = c->LS.r[0];
     c->mode = cfg->request_mode;
     c->cap_e = cfg->cap_e;
@@ -2009,7 +2251,7 @@ extern "C" seneca_status seneca_init_cache(const seneca_cache_config* cfg, void*
     cudaGetDevice(&c->device);
 #define INIT_TRY(expr) do { cudaError_t _e = (expr); if (_e != cudaSuccess) { delete c; return cuda_status(_e, #expr); } } while (0)
     const bool coupled = z.C.cap_t > 0 || z.C.cold;
-    for (int v = 0; v < 3; ++v)
+    for (int v = 0; v < 4; ++v)
         for (int tm = 0; tm < 2; ++tm)
             INIT_TRY(cudaFuncSetAttribute(round_kernel(v, tm, coupled), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           200 * 1024));
@@ -2030,6 +2272,21 @@ extern "C" seneca_status seneca_init_cache(const seneca_cache_config* cfg, void*
         c->round_fn = round_kernel(0, false, coupled);
         c->round_fn_timed = round_kernel(0, true, coupled);
         c->round_threads = kThreads;
+        if (sharded) {                       // 512 threads, one CTA per SM, every shard's CTAs co-resident
+            int per_shd = 0, per_shd_t = 0;
+            INIT_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_shd, round_kernel(3, false, coupled), kThreads,
+                                                                   round_smem));
+            INIT_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_shd_t, round_kernel(3, true, coupled), kThreads,
+                                                                   round_smem));
+            if (need > (uint64_t)std::min(per_shd, per_shd_t) * num_sms()) {
+                set_error("%u shards x %u CTAs exceed the co-resident CTA slots", z.R, z.C.J + 1);
+                delete c;
+                return SENECA_EINVAL;
+            }
+            c->round_fn = round_kernel(3, false, coupled);
+            c->round_fn_timed = round_kernel(3, true, coupled);
+            slots = need;                    // no other variant below
+        }
         // independent jobs (no maintain coupling): the replay lasts as long as the job
         // with the most rounds; when that job's batch fits 256 threads, 256-thread
         // CTAs run its rounds faster (measured: OpenImages)
@@ -2039,7 +2296,7 @@ extern "C" seneca_status seneca_init_cache(const seneca_cache_config* cfg, void*
             const uint64_t rj = (uint64_t)z.C.target[jj] * ((z.C.N + z.C.batch[jj] - 1) / z.C.batch[jj]);
             if (rj > rdom || (rj == rdom && z.C.batch[jj] > z.C.batch[jdom])) { rdom = rj; jdom = jj; }
         }
-        if (!coupled && z.C.batch[jdom] <= kThreads / 2 && need <= slots) {
+        if (!sharded && !coupled && z.C.batch[jdom] <= kThreads / 2 && need <= slots) {
             const size_t smemh = smem_for(kThreads / 2);
             int per_smh = 0, per_smh_t = 0;
             INIT_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_smh, round_kernel(2, false, coupled),
@@ -2232,6 +2489,28 @@ extern "C" seneca_status seneca_read_state(const seneca_ctx* c, seneca_state_vie
         if (c->arrival[__builtin_ctz(m)] <= c->r) v->active_mask |= 1u << __builtin_ctz(m);
     v->replicas = c->R;
     v->replica_stride = c->rep_stride;
+    return SENECA_OK;
+}
+
+extern "C" seneca_status seneca_shard_mailbox(const seneca_ctx* c, void** d_mailbox, size_t* bytes) {
+    if (!c || !d_mailbox || !bytes) { set_error("bad arguments"); return SENECA_EINVAL; }
+    if (c->C.G <= 1 || c->shard_mode != 1) { set_error("not a one-shard-per-context sharded replay"); return SENECA_EINVAL; }
+    *d_mailbox = c->L.mbox;
+    *bytes = ((size_t)c->C.mb_fl + 2 * (c->C.J + 1) * c->C.G) * 4;
+    return SENECA_OK;
+}
+
+extern "C" seneca_status seneca_shard_attach(seneca_ctx* c, void* const* peers) {
+    if (!c || !peers) { set_error("bad arguments"); return SENECA_EINVAL; }
+    if (c->C.G <= 1 || c->shard_mode != 1) { set_error("not a one-shard-per-context sharded replay"); return SENECA_EINVAL; }
+    Lay& L = c->LS.r[0];
+    for (uint32_t g = 0; g < c->C.G; ++g) {
+        void* p = peers[g] ? peers[g] : (g == L.shard ? (void*)L.mbox : nullptr);
+        if (!p) { set_error("NULL mailbox of shard %u", g); return SENECA_EINVAL; }
+        L.peer[g] = (uint32_t*)p;
+    }
+    c->L = L;
+    c->attached = true;
     return SENECA_OK;
 }
 

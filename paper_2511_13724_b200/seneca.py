@@ -60,6 +60,7 @@ class CacheConfig(C.Structure):
         ("cap_e", C.c_uint64), ("cap_d", C.c_uint64), ("cap_a", C.c_uint64), ("seed", C.c_uint64),
         ("replicas", C.c_uint32), ("evict_tiers", C.c_uint32), ("sampler", C.c_uint32), ("_pad0", C.c_uint32),
         ("arrival_round", C.POINTER(C.c_uint32)), ("cold_start", C.c_uint32), ("_pad1", C.c_uint32),
+        ("shards", C.c_uint32), ("shard_rank", C.c_uint32), ("shard_mode", C.c_uint32), ("_pad2", C.c_uint32),
     ]
 
 
@@ -125,6 +126,9 @@ def lib() -> C.CDLL:
         L.seneca_replay_rounds.restype = C.c_int
         L.seneca_read_state.argtypes = [vp, C.POINTER(StateView)]; L.seneca_read_state.restype = C.c_int
         L.seneca_sync_status.argtypes = [vp, vp]; L.seneca_sync_status.restype = C.c_int
+        L.seneca_shard_mailbox.argtypes = [vp, C.POINTER(vp), C.POINTER(C.c_size_t)]
+        L.seneca_shard_mailbox.restype = C.c_int
+        L.seneca_shard_attach.argtypes = [vp, C.POINTER(vp)]; L.seneca_shard_attach.restype = C.c_int
         L.seneca_launch_count.argtypes = [vp]; L.seneca_launch_count.restype = u64
         L.seneca_profile.argtypes = [vp, u32]; L.seneca_profile.restype = C.c_int
         L.seneca_profile_read.argtypes = [vp, C.POINTER(KernelStat), u32, C.POINTER(u32)]
@@ -140,6 +144,7 @@ EXPORTED = ["seneca_mdp_num_splits", "seneca_mdp_sweep", "seneca_mdp_eval", "sen
             "seneca_metadata_bytes", "seneca_state_bytes", "seneca_init_cache",
             "seneca_ods_next_batch", "seneca_replay_epochs", "seneca_replay_epoch", "seneca_replay_rounds",
             "seneca_read_state", "seneca_sync_status", "seneca_launch_count", "seneca_destroy",
+            "seneca_shard_mailbox", "seneca_shard_attach",
             "seneca_last_error", "seneca_profile", "seneca_profile_read"]
 
 
@@ -216,7 +221,7 @@ def profiles_from_columns(cols: dict) -> np.ndarray:
 
 # ------------------------------------------------------------------ ODS
 def make_config(n_total, batch, target, cap_e, cap_d, cap_a, seed, request_mode=0, replicas=1, evict_tiers=0,
-                sampler=0, arrival=None, cold_start=0):
+                sampler=0, arrival=None, cold_start=0, shards=1, shard_rank=0, shard_mode=0):
     b = (C.c_uint32 * len(batch))(*batch)
     t = (C.c_uint32 * len(target))(*target)
     arr = (C.c_uint32 * len(batch))(*arrival) if arrival is not None else None
@@ -224,7 +229,7 @@ def make_config(n_total, batch, target, cap_e, cap_d, cap_a, seed, request_mode=
                       batch_size=b, target_epochs=t, cap_e=cap_e, cap_d=cap_d, cap_a=cap_a, seed=seed,
                       replicas=replicas, evict_tiers=evict_tiers, sampler=sampler,
                       arrival_round=C.cast(arr, C.POINTER(C.c_uint32)) if arr is not None else None,
-                      cold_start=cold_start)
+                      cold_start=cold_start, shards=shards, shard_rank=shard_rank, shard_mode=shard_mode)
     cfg._keep = (b, t, arr)
     return cfg
 
@@ -267,6 +272,19 @@ def read_state(ctx: int) -> StateView:
     v = StateView()
     _check(lib().seneca_read_state(ctx, C.byref(v)))
     return v
+
+
+def shard_mailbox(ctx: int):
+    """(device pointer, bytes) of this shard's mailbox (shard_mode 1)."""
+    p, n = C.c_void_p(), C.c_size_t()
+    _check(lib().seneca_shard_mailbox(ctx, C.byref(p), C.byref(n)))
+    return p.value, n.value
+
+
+def shard_attach(ctx: int, peer_mailboxes):
+    """peer_mailboxes: [shards] device pointers (None for this shard's own)."""
+    arr = (C.c_void_p * len(peer_mailboxes))(*[p if p else None for p in peer_mailboxes])
+    _check(lib().seneca_shard_attach(ctx, arr))
 
 
 def sync_status(ctx: int, stream=None):

@@ -190,3 +190,22 @@ def test_workspace_is_independent_of_target_epochs(lib):
     assert sizes[250] < 4 * 2**30
     one = S.make_config(c["n_total"], c["batch"], [1] * J, caps[0], caps[1], caps[2], 1)
     assert S.state_bytes(one) < sizes[2]          # one epoch: a one-slot ring
+
+
+def test_sharding_arguments_and_workspace(lib):
+    """sample-ID-range sharding: G slices of the replicated state +
+    a mailbox each in emulation; EINVAL for G > 8, replicas or caller-supplied
+    requests with G > 1, a bad shard_mode / shard_rank."""
+    c = synth.ods_config("toy")
+    caps = S.split_capacities(c["n_total"], c["s_data"], c["m_num"], c["m_den"], c["cache_bytes"], *c["split"])
+    mk = lambda **kw: S.make_config(c["n_total"], c["batch"], c["target"], caps[0], caps[1], caps[2], 1, **kw)
+    one = S.state_bytes(mk())
+    for G in (2, 4, 8):
+        b = S.state_bytes(mk(shards=G))
+        assert G * (one - 256) <= b <= G * (one - 256) + 256 + G * 8192, (G, b)
+        assert S.state_bytes(mk(shards=G, shard_mode=1, shard_rank=G - 1)) < b
+    for kw in (dict(shards=9), dict(shards=2, replicas=2), dict(shards=2, request_mode=1),
+               dict(shards=2, shard_mode=2), dict(shards=4, shard_mode=1, shard_rank=4)):
+        with pytest.raises(S.SenecaError) as ei:
+            S.state_bytes(mk(**kw))
+        assert ei.value.status == S.EINVAL, kw

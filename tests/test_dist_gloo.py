@@ -74,3 +74,53 @@ def test_world2_gloo(tmp_path):
         t0, t1, u, seed = open(tmp_path / f"r{r}.txt").read().split()
         assert (float(t0), float(t1), float(u)) == (2.0, 10.0, 300.0)
         assert int(seed) == 7 + r
+
+
+def _shard_worker(rank, world, port, out_dir):
+    """attach_shard_peers' exchange with the CUDA calls replaced: each rank
+    'shares' a fake handle naming its rank, the mailbox sits at a rank-dependent
+    offset in its workspace; every rank must end up with the peers' mailbox
+    addresses in shard order and None for itself."""
+    import types
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = types.SimpleNamespace(ctx=1000 + rank)
+        base = 1 << 40
+        attached = {}
+
+        class Fake:
+            def __init__(self, h):
+                self.h = h
+
+            def data_ptr(self):
+                return (1 << 44) * (self.h["rank"] + 1)          # where peer rank's storage maps here
+
+        peers = D.attach_shard_peers(
+            g, _share=lambda: (base, {"rank": rank}), _open=Fake,
+            _mailbox=lambda ctx: (base + 4096 * (rank + 1), 777),
+            _attach=lambda ctx, p: attached.setdefault(ctx, list(p)))
+        with open(os.path.join(out_dir, f"s{rank}.txt"), "w") as f:
+            f.write(repr((peers, attached[1000 + rank])))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_world3_gloo_shard_mailbox_exchange(tmp_path):
+    port = _free_port()
+    mp.spawn(_shard_worker, args=(3, port, str(tmp_path)), nprocs=3, join=True)
+    for r in range(3):
+        peers, attached = eval(open(tmp_path / f"s{r}.txt").read())
+        assert peers == attached
+        want = [None if p == r else (1 << 44) * (p + 1) + 4096 * (p + 1) for p in range(3)]
+        assert peers == want
+
+
+def test_shard_ranges_partition_by_superblock():
+    for n in (1, 4096, 4097, 1_281_167, 14_197_122):
+        for G in (1, 2, 3, 8):
+            rg = D.shard_ranges(n, G)
+            assert rg[0][0] == 0 and rg[-1][1] == n and len(rg) == G
+            assert all(rg[i][1] == rg[i + 1][0] for i in range(G - 1))
+            assert all(lo % 4096 == 0 or lo == n for lo, _ in rg)

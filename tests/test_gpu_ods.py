@@ -680,3 +680,101 @@ def test_workspace_above_2gib_per_replica():
     o.replay_rounds(3)
     compare_replica(o, g, 1)
     g.close()
+
+
+# ---------------------------------------------------------------- sample-ID-range sharding
+def sharded_replay(c, ce, cd, ca, seed, G, evict_all=False, cold=False, arrival=None, rounds=None):
+    g = P.ODSContext(c["n_total"], c["batch"], c["target"], ce, cd, ca, seed, shards=G,
+                     evict_tiers=int(evict_all), cold_start=int(cold), arrival=arrival)
+    tr = g.new_transcript()
+    r = g.replay_rounds(rounds, tr) if rounds else g.replay_epochs(max(c["target"]), tr)
+    torch.cuda.synchronize()
+    g.sync()
+    return g, tr, r
+
+
+@pytest.mark.parametrize("name,scale", [("toy", 1), ("imagenet1k", 64), ("openimages", 64), ("imagenet22k", 64)])
+def test_sharded_replay_identical_for_every_G(name, scale):
+    """Invariant I8: one replay partitioned by sample-ID range over
+    G = 1, 2, 4, 8 shards (all shards in one launch on this device, exchanging
+    pool sizes and resolved ids through their mailboxes every round) delivers
+    exactly the oracle's transcript on EVERY shard, with identical bitmaps and
+    counters.  Toy (one superblock: shards 1.. own nothing), N/64 configs with
+    A churn (ImageNet-1K), mixed batches (OpenImages) and 55 superblocks (22K)."""
+    seed = 12
+    c = synth.ods_config(name, scale=scale, seed=seed)
+    ce, cd, ca = caps_of(c)
+    o = O.ODS(c["n_total"], c["batch"], c["target"], ce, cd, ca, seed, transcript=True)
+    ro = o.replay_epochs(max(c["target"]))
+    for G in (1, 2, 4, 8):
+        g, tr, r = sharded_replay(c, ce, cd, ca, seed, G)
+        assert r == ro
+        for k in range(G):
+            compare_replica(o, g, k, tr if G == 1 else tr[k])
+        g.close()
+
+
+@pytest.mark.parametrize("mode", ["evict_all", "cold", "arrivals"])
+def test_sharded_replay_variants(mode):
+    """Sharding under evict_tiers = ALL (E/D churn through the exchange), cold start
+    (admissions replicated, counts per shard) and job arrivals (pools rebuilt per
+    shard at arrival), G = 3 and 8, against the oracle."""
+    seed = 13
+    c = synth.ods_config("imagenet1k", scale=64, seed=seed)
+    ce, cd, ca = caps_of(c)
+    kw = dict(evict_all=mode == "evict_all", cold=mode == "cold")
+    arr = None
+    if mode == "arrivals":
+        per_job = c["target"][0] * -(-c["n_total"] // c["batch"][0])
+        arr = [0, 0, per_job // 3, per_job]
+    o = O.ODS(c["n_total"], c["batch"], c["target"], ce, cd, ca, seed, transcript=True, arrival=arr, **kw)
+    ro = o.replay_epochs(max(c["target"]))
+    for G in (3, 8):
+        g, tr, r = sharded_replay(c, ce, cd, ca, seed, G, arrival=arr, **kw)
+        assert r == ro
+        for k in range(G):
+            compare_replica(o, g, k, tr[k])
+        g.close()
+
+
+def test_sharded_full_size_prefix_22k():
+    """The full ImageNet-22K config (3,467 superblocks) split over 8 shards, first
+    160 rounds, every shard against the oracle (bitmaps and counters)."""
+    seed = synth.PERF_SEED
+    c = synth.ods_config("imagenet22k", seed=seed)
+    ce, cd, ca = caps_of(c)
+    g = P.ODSContext(c["n_total"], c["batch"], c["target"], ce, cd, ca, seed, shards=8)
+    assert g.replay_rounds(160) == 160
+    torch.cuda.synchronize()
+    g.sync()
+    o = O.ODS(c["n_total"], c["batch"], c["target"], ce, cd, ca, seed)
+    o.replay_rounds(160)
+    for k in (0, 7):
+        compare_replica(o, g, k)
+
+
+@pytest.mark.parametrize("G,name,scale", [(2, "toy", 1), (4, "imagenet1k", 64)])
+def test_sharded_one_context_per_shard(G, name, scale):
+    """shard_mode 1 (one shard per context, peers attached by mailbox address, as
+    one process per GPU runs it): G contexts on this device replay concurrently
+    on G streams and every shard equals the oracle (subprocess under a timeout:
+    a missing peer would spin)."""
+    import subprocess
+    import sys
+    out = subprocess.run([sys.executable, os.path.join(os.path.dirname(HERE), "tools", "shard_contexts.py"),
+                          str(G), name, str(scale)], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-3000:]
+    assert "ok" in out.stdout
+
+
+def test_sharded_across_processes_cuda_ipc():
+    """Two PROCESSES, one shard each (the one-process-per-GPU layout, both on this
+    device): mailboxes mapped by CUDA IPC through dist.attach_shard_peers (handles
+    all-gathered over gloo); each rank's transcript equals the oracle's.  Without
+    MPS the two processes time-slice the device, so only a toy replay is run."""
+    import subprocess
+    import sys
+    out = subprocess.run([sys.executable, os.path.join(os.path.dirname(HERE), "tools", "shard_ranks.py"), "2"],
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-3000:]
+    assert "all ranks ok" in out.stdout
