@@ -46,6 +46,9 @@ constexpr int kMaxSteps = 101;  // grid step 1 % -> 101 values per coordinate
 #ifndef SENECA_MDP_MINB
 #define SENECA_MDP_MINB 3
 #endif
+#ifndef SENECA_MDP_PAIRS
+#define SENECA_MDP_PAIRS 1        // 1: the paired sweep (mdp_sweep_pairs); 0: mdp_sweep_kernel (A/B knob)
+#endif
 constexpr uint32_t kChunk = SENECA_MDP_CHUNK;  // splits per sweep work item (16 per lane)
 constexpr int kUnroll = SENECA_MDP_UNROLL;      // splits in flight per lane
 
@@ -498,6 +501,182 @@ mdp_sweep_kernel(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_pro
     }
 }
 
+// ------------------------------------------------------------------ the paired sweep
+// Splits mirrored in (p_A, p_D) -- (b, m) and (m, b) with the same p_E -- share
+// every count of Eqs. 5-8 but N_A / N_D: the A and D tiers hold the same
+// number of samples per byte (M x S_data), so capAD(p_A) + capAD(p_D) decides
+// whether D is clamped (capAD(p_D) <= N - capAD(p_A) <=> the sum <= N) and
+// N_E, N_S -- and with them the one per-split quotient N_S/N (or N_E/N) -- are
+// identical for the two.  One pair = one quotient, two Eq. 9 sums: the same
+// IEEE operations on the same operands as the per-split definition (tests
+// compare the whole grid bit for bit).
+//
+// A group of kPairW warps sweeps one profile (named barrier per group, no CTA
+// barrier): every warp derives the header (Eqs. 1-4) itself, the group builds
+// the profile's rows (Eqs. 5-7 exact floors + one-coordinate Eq. 9 terms) in its
+// shared buffer, then its threads take the pairs.  The pair table (row offsets
+// of p_A = b, p_D = m, p_E and the two enumeration indices) is built once per CTA.
+#ifndef SENECA_MDP_PAIRW
+#define SENECA_MDP_PAIRW 2
+#endif
+constexpr uint32_t kPairW = SENECA_MDP_PAIRW;                 // warps per profile group
+constexpr uint32_t kGroups = kThreads / 32 / kPairW;          // groups per CTA
+constexpr uint32_t kMaxPairs = 2601;                          // 1 % grid: sum over rows of ceil((a + 1) / 2)
+
+__device__ __forceinline__ void group_sync(uint32_t gid) {
+    asm volatile("bar.sync %0, %1;" :: "r"(gid + 1), "r"(kPairW * 32) : "memory");
+}
+
+// Eqs. 1-4 of a profile for this warp (all lanes), and its validity.
+struct Hdr {
+    double dsi[4];
+    uint8_t lim[4];
+    bool valid;
+};
+
+__device__ __forceinline__ Hdr warp_header(const seneca_mdp_profile& p) {
+    Hdr h;
+    h.valid = profile_valid(p);
+    for (int t = 0; t < 4; ++t) { h.dsi[t] = 0.0; h.lim[t] = 0; }
+    if (h.valid) tier_throughputs_warp(p, h.dsi, h.lim);            // valid is warp-uniform
+    return h;
+}
+
+__global__ void __launch_bounds__(kThreads, SENECA_MDP_MINB)
+mdp_sweep_pairs(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_profiles, uint32_t g,
+                uint32_t steps, uint32_t n_splits, uint32_t n_pairs, seneca_mdp_result* __restrict__ results,
+                double* __restrict__ grid) {
+    __shared__ Row s_rows[kGroups][kMaxSteps];
+    __shared__ double s_red_v[kGroups][kPairW];
+    __shared__ uint32_t s_red_i[kGroups][kPairW];
+    extern __shared__ uint2 s_pair[];                               // [n_pairs]
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t gid = warp / kPairW, gw = warp % kPairW, gt = gw * 32 + lane;   // group, warp / thread in it
+    // pair table: row a (p_E = 100 - a g) holds positions b = 0..a (p_A = b g,
+    // p_D = (a - b) g) at enumeration index a(a+1)/2 + b (R-M9); pair (b, a - b)
+    // for b <= a / 2.  x = row offset of p_A=b | of p_D=a-b << 12 | p_E row << 24,
+    // y = index of (b, a - b) | index of (a - b, b) << 16.
+    for (uint32_t t = threadIdx.x; t < n_pairs; t += blockDim.x) {
+        uint32_t a = 0, base = 0;                                   // row a holds pairs base .. base + a/2
+        while (base + a / 2 + 1 <= t) { base += a / 2 + 1; ++a; }
+        const uint32_t b = t - base, m = a - b, i0 = a * (a + 1) / 2;
+        s_pair[t] = make_uint2((uint32_t)(b * sizeof(Row)) | (uint32_t)(m * sizeof(Row)) << 12 | (steps - a) << 24,
+                               (i0 + b) | (i0 + m) << 16);
+    }
+    __syncthreads();
+    Row* rows = s_rows[gid];
+    const uint32_t n_groups = gridDim.x * kGroups;
+    for (uint32_t pi = blockIdx.x * kGroups + gid; pi < n_profiles; pi += n_groups) {
+        const seneca_mdp_profile prof = profiles[pi];
+        const Hdr H = warp_header(prof);
+        double best = __longlong_as_double(0xfff0000000000000ll);
+        uint32_t best_i = 0xffffffffu;
+        if (H.valid) {                                              // group-uniform
+            // rows (Eqs. 5-7 exact floors, clamped to N; one-coordinate Eq. 9 terms)
+            Header B;
+            for (int t = 0; t < 4; ++t) B.dsi[t] = H.dsi[t];
+            B.N = prof.n_total;
+            B.Xad = prof.cache_bytes * prof.m_den;
+            B.Dad = 100ull * prof.m_num * prof.s_data;
+            B.De = 100ull * prof.s_data;
+            B.cache_bytes = prof.cache_bytes;
+            B.rDad = __drcp_rn(u2d(B.Dad));
+            B.rDe = __drcp_rn(u2d(B.De));
+            for (uint32_t k0 = gw * 32; k0 <= steps; k0 += kPairW * 32) build_rows(B, k0, g, steps, rows);
+            group_sync(gid);
+            double* grow = grid ? grid + (uint64_t)pi * n_splits : nullptr;
+            if (B.N < (1ull << 31)) {
+                const uint32_t N = (uint32_t)B.N;
+                const double dN = u2d(B.N), y = __drcp_rn(dN), dsiE = H.dsi[2], dsiS = H.dsi[3];
+                const char* rb0 = reinterpret_cast<const char*>(rows);
+#pragma unroll 2
+                for (uint32_t t = gt; t < n_pairs; t += kPairW * 32) {
+                    const uint2 w = s_pair[t];
+                    const Row& rb = *reinterpret_cast<const Row*>(rb0 + (w.x & 0xfffu));
+                    const Row& rm = *reinterpret_cast<const Row*>(rb0 + ((w.x >> 12) & 0xfffu));
+                    const Row& re = rows[w.x >> 24];
+                    const uint32_t cb = rb.capc, cm = rm.capc;
+                    const uint32_t sum = cb + cm;                       // <= 2N < 2^32
+                    const bool dfree = sum <= N;                        // Eq. 6 unclamped (both splits)
+                    const uint32_t r2 = dfree ? N - sum : 0u;
+                    const uint32_t cE = re.cape;
+                    const bool efree = dfree && cE <= r2;               // Eq. 7 unclamped
+                    const uint32_t x = efree ? r2 - cE : r2;            // N_S, or the clamped N_E (0 if D clamped)
+                    const double q = div_by_n(u32_to_d(x), dN, y);
+                    const double prod = __dmul_rn(q, efree ? dsiS : dsiE);
+                    const double tX = efree ? re.tE : 0.0;
+                    const double v0 = __dadd_rn(__dadd_rn(__dadd_rn(rb.tA, dfree ? rm.tD : rb.tDc), tX), prod);
+                    const double v1 = __dadd_rn(__dadd_rn(__dadd_rn(rm.tA, dfree ? rb.tD : rm.tDc), tX), prod);
+                    const uint32_t i0 = w.y & 0xffffu, i1 = w.y >> 16;
+                    if (grow) { __stcs(grow + i0, v0); __stcs(grow + i1, v1); }
+                    if (v0 > best || (v0 == best && i0 < best_i)) { best = v0; best_i = i0; }
+                    if (v1 > best || (v1 == best && i1 < best_i)) { best = v1; best_i = i1; }
+                }
+            } else {                                                // N >= 2^31: 64-bit counts (rare)
+                const uint64_t N = B.N;
+                const double dN = u2d(N);
+                auto capc = [&](uint32_t k) { const uint64_t c = ((uint64_t)k * g * B.Xad) / B.Dad; return c < N ? c : N; };
+                auto cape = [&](uint32_t k) { const uint64_t c = ((uint64_t)k * g * B.cache_bytes) / B.De; return c < N ? c : N; };
+                for (uint32_t t = gt; t < n_pairs; t += kPairW * 32) {
+                    const uint2 w = s_pair[t];
+                    for (int h = 0; h < 2; ++h) {
+                        const uint32_t ka = (h ? (w.x >> 12) & 0xfffu : w.x & 0xfffu) / sizeof(Row);
+                        const uint32_t kd = (h ? w.x & 0xfffu : (w.x >> 12) & 0xfffu) / sizeof(Row);
+                        const uint32_t ke = w.x >> 24, idx = h ? w.y >> 16 : w.y & 0xffffu;
+                        const uint64_t r1 = N - capc(ka);
+                        const uint64_t cD = capc(kd);
+                        const bool dfree = cD <= r1;
+                        const uint64_t r2 = dfree ? r1 - cD : 0ull;
+                        const uint64_t cE = cape(ke);
+                        const bool efree = dfree && cE <= r2;
+                        const uint64_t x = efree ? r2 - cE : r2;
+                        const double prod = __dmul_rn(__ddiv_rn(u2d(x), dN), efree ? H.dsi[3] : H.dsi[2]);
+                        const double tD = dfree ? rows[kd].tD : rows[ka].tDc;
+                        const double tX = efree ? rows[ke].tE : 0.0;
+                        const double v = __dadd_rn(__dadd_rn(__dadd_rn(rows[ka].tA, tD), tX), prod);
+                        if (grow) __stcs(grow + idx, v);
+                        if (v > best || (v == best && idx < best_i)) { best = v; best_i = idx; }
+                    }
+                }
+            }
+        }
+        // argmax: the maximum by butterfly, then the smallest index holding it (R-M8)
+        double mx = best;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        best_i = __reduce_min_sync(0xffffffffu, best == mx ? best_i : 0xffffffffu);
+        if (lane == 0) { s_red_v[gid][gw] = mx; s_red_i[gid][gw] = best_i; }
+        group_sync(gid);                                            // rows free, per-warp maxima visible
+        if (gt == 0) {
+            seneca_mdp_result r = {};
+            if (!H.valid) {
+                r.status = 1;
+            } else {
+                double bv = s_red_v[gid][0];
+                uint32_t bi = s_red_i[gid][0];
+                for (uint32_t k = 1; k < kPairW; ++k) {
+                    const double ov = s_red_v[gid][k];
+                    const uint32_t oi = s_red_i[gid][k];
+                    if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+                }
+                uint32_t ra = 0, rb = bi;
+                while (rb > ra) { rb -= ra + 1; ++ra; }
+                r.p_e = (uint8_t)(100 - ra * g);
+                r.p_d = (uint8_t)((ra - rb) * g);
+                r.p_a = (uint8_t)(rb * g);
+                r.lim_a = H.lim[0]; r.lim_d = H.lim[1]; r.lim_e = H.lim[2]; r.lim_s = H.lim[3];
+                r.status = 0;
+                r.v_best = bv;
+                r.dsi_a = H.dsi[0]; r.dsi_d = H.dsi[1]; r.dsi_e = H.dsi[2]; r.dsi_s = H.dsi[3];
+            }
+            results[pi] = r;
+        }
+        // the next profile's rows are written after this barrier; the per-warp
+        // maxima after the next profile's first barrier, which thread gt == 0
+        // reaches only after reading these
+    }
+}
+
 // ------------------------------------------------------------------ evaluation at given splits
 constexpr uint32_t kMaxEvalSplits = 4096;
 struct EvalSplits {
@@ -578,6 +757,27 @@ extern "C" seneca_status seneca_mdp_sweep(const seneca_mdp_profile* d_profiles, 
     }
     const uint32_t steps = 100 / grid_step_pct;
     const uint32_t ns = (uint32_t)seneca_mdp_num_splits(grid_step_pct);
+#if SENECA_MDP_PAIRS
+    {
+        uint32_t np = 0;
+        for (uint32_t a = 0; a <= steps; ++a) np += a / 2 + 1;
+        static int pslots = 0;
+        if (!pslots) {
+            int dev = 0, sms = 0, per_sm = 0;
+            SENECA_CUDA_TRY(cudaGetDevice(&dev));
+            SENECA_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+            SENECA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mdp_sweep_pairs, kThreads,
+                                                                          kMaxPairs * sizeof(uint2)));
+            pslots = sms * (per_sm > 0 ? per_sm : 1);
+        }
+        const uint32_t want = (n_profiles + kGroups - 1) / kGroups;
+        const uint32_t blocks = want < (uint32_t)pslots ? want : (uint32_t)pslots;
+        mdp_sweep_pairs<<<blocks, kThreads, np * sizeof(uint2), (cudaStream_t)stream>>>(
+            d_profiles, n_profiles, grid_step_pct, steps, ns, np, d_results, d_grid);
+        SENECA_CUDA_TRY(cudaGetLastError());
+        return SENECA_OK;
+    }
+#endif
     // persistent grid: every resident CTA slot of the device, never more CTAs than profiles
     static int slots = 0;
     if (!slots) {

@@ -88,6 +88,7 @@ struct Cfg {
     uint32_t Nrow;                   // row stride of the permutation / lap lists (N rounded up to 64)
     uint32_t FL;                     // capacity of one refill buffer
     uint32_t G;                      // sample-ID-range shards (1: unsharded), SURVEY §8(e)
+    uint32_t xsys;                   // exchange scope: 1 system (peers on other devices), 0 this device
     uint32_t mb_c1, mb_c2, mb_rf, mb_fl;   // mailbox offsets (u32) of the shard exchange, see Lay.mbox
     uint64_t seed;
     uint32_t batch[kMaxJobs];
@@ -126,6 +127,7 @@ struct Lay {
     unsigned long long *evicted, *refilled;
     uint32_t *err;                   // latched consistency flags (control block, see kCtlBytes)
     uint32_t *verr;                  // caller-supplied request validation flag (control block)
+    uint32_t *dbg;                   // [4] first consistency failure: site | pool, rank / round, ... (control block)
     uint32_t *bar;                   // [4] signals: u64 {job phases done | evictions pushed << 32},
                                      //     maintain rounds applied, eviction ring position (control block)
     unsigned long long *phase;       // [32] accumulated cycles per phase (see seneca.h)
@@ -184,17 +186,26 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // Mailboxes live in device memory of the receiving shard: in one context (all
 // shards on one device, emulation) the peers' slices of the same workspace; with
 // one shard per device, peer memory mapped over NVLink.  Writers store payloads,
-// then release a per-(round parity, slot, sender) stamp = round + 1 at system
-// scope; readers acquire every sender's stamp, then read the payload uncached.
-// Round parity double-buffers: every shard waits for every other shard's round-r
-// values before it can publish round r + 1's, so a buffer is never overwritten
-// while a peer may still read it.
-__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
-    asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+// fence, then store a per-(round parity, slot, sender) stamp = round + 1;
+// readers poll the stamps, fence, then read the payload uncached (the fence +
+// relaxed store / relaxed load + fence pairs are release / acquire).  Scope:
+// the device (gpu) when every shard is on this device, the system when the
+// peers are other devices (Cfg.xsys).  Lane g of warp 0 serves peer g, so an
+// exchange costs two fences and one poll round trip, not 2G.  Round parity
+// double-buffers: every shard waits for every other shard's round-r values
+// before it can publish round r + 1's, so a buffer is never overwritten while a
+// peer may still read it.
+__device__ __forceinline__ void xfence(const Cfg& C) {
+    if (C.xsys) __threadfence_system(); else __threadfence();
 }
-__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+__device__ __forceinline__ void st_stamp(const Cfg& C, uint32_t* p, uint32_t v) {
+    if (C.xsys) asm volatile("st.relaxed.sys.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+    else asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_stamp(const Cfg& C, const uint32_t* p) {
     uint32_t v;
-    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    if (C.xsys) asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    else asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
 __device__ __forceinline__ uint32_t ld_mbox(const uint32_t* p) { return __ldcv(p); }
@@ -208,45 +219,50 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-__device__ __forceinline__ void wait_stamp(const Lay& L, const uint32_t* p, uint32_t stamp) {
-    if (ld_acquire_sys(p) == stamp) return;
+__device__ __forceinline__ void wait_stamp(const Lay& L, const Cfg& C, const uint32_t* p, uint32_t stamp) {
+    if (ld_stamp(C, p) == stamp) return;
     const unsigned long long t0 = globaltimer_ns();
-    while (ld_acquire_sys(p) != stamp) {
-        __nanosleep(64);
+    while (ld_stamp(C, p) != stamp) {
         if (globaltimer_ns() - t0 > kPeerTimeoutNs) { atomicOr(L.err, 4u); __threadfence_system(); __trap(); }
     }
 }
 
-// C1 (thread 0 of the calling CTA): publish (v0, v1, v2) of slot s for round r to
-// every shard, wait for every shard's, return them in out[g][0..2].
+// C1 (warp 0 of the calling CTA, every lane): publish (v0, v1, v2) of slot s for
+// round r to every shard, wait for every shard's, lane g stores shard g's values
+// into out[g][0..2].
 __device__ void shard_c1(const Lay& L, const Cfg& C, uint32_t slot, uint64_t r, uint32_t v0, uint32_t v1, uint32_t v2,
                          uint32_t (*out)[3]) {
+    const uint32_t lane = threadIdx.x & 31;
     const uint32_t stamp = (uint32_t)r + 1u;
-    const size_t row = (((size_t)(r & 1) * (C.J + 1) + slot) * C.G) * 4;
-    for (uint32_t g = 0; g < C.G; ++g) {
-        uint32_t* q = L.peer[g] + C.mb_c1 + row + (size_t)L.shard * 4;
+    const size_t row = C.mb_c1 + (((size_t)(r & 1) * (C.J + 1) + slot) * C.G) * 4;
+    if (lane < C.G) {
+        uint32_t* q = L.peer[lane] + row + (size_t)L.shard * 4;
         q[1] = v0; q[2] = v1; q[3] = v2;
     }
-    __threadfence_system();
-    for (uint32_t g = 0; g < C.G; ++g) st_release_sys(L.peer[g] + C.mb_c1 + row + (size_t)L.shard * 4, stamp);
-    for (uint32_t g = 0; g < C.G; ++g) {
-        const uint32_t* q = L.mbox + C.mb_c1 + row + (size_t)g * 4;
-        wait_stamp(L, q, stamp);
-        out[g][0] = ld_mbox(q + 1); out[g][1] = ld_mbox(q + 2); out[g][2] = ld_mbox(q + 3);
+    xfence(C);
+    if (lane < C.G) st_stamp(C, L.peer[lane] + row + (size_t)L.shard * 4, stamp);
+    if (lane < C.G) wait_stamp(L, C, L.mbox + row + (size_t)lane * 4, stamp);
+    xfence(C);
+    if (lane < C.G) {
+        const uint32_t* q = L.mbox + row + (size_t)lane * 4;
+        out[lane][0] = ld_mbox(q + 1); out[lane][1] = ld_mbox(q + 2); out[lane][2] = ld_mbox(q + 3);
     }
+    __syncwarp();
 }
 
 // C2 flags (every thread calls it after storing its resolved ids into every
-// shard's mailbox): the barrier orders the CTA's stores before thread 0's
-// system-scope fence and release, then thread 0 waits for every shard's stamp.
+// shard's mailbox): the barrier orders the CTA's stores before warp 0's fence
+// and stamps (cumulativity), then warp 0 waits for every shard's stamp.
 __device__ void shard_c2_sync(const Lay& L, const Cfg& C, uint32_t slot, uint64_t r) {
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {
+        const uint32_t lane = threadIdx.x;
         const uint32_t stamp = (uint32_t)r + 1u;
-        const size_t row = ((size_t)(r & 1) * (C.J + 1) + slot) * C.G;
-        __threadfence_system();
-        for (uint32_t g = 0; g < C.G; ++g) st_release_sys(L.peer[g] + C.mb_fl + row + L.shard, stamp);
-        for (uint32_t g = 0; g < C.G; ++g) wait_stamp(L, L.mbox + C.mb_fl + row + g, stamp);
+        const size_t row = C.mb_fl + ((size_t)(r & 1) * (C.J + 1) + slot) * C.G;
+        xfence(C);
+        if (lane < C.G) st_stamp(C, L.peer[lane] + row + L.shard, stamp);
+        if (lane < C.G) wait_stamp(L, C, L.mbox + row + lane, stamp);
+        xfence(C);
     }
     __syncthreads();
 }
@@ -341,7 +357,11 @@ __device__ uint32_t pool_select(const Lay& L, const Cfg& C, uint32_t pidx, uint3
         run += (x & 0xffffu) + (x >> 16);
         if (q < 7 && run <= r) { before = run; qsel = q + 1; wsel = cw[q < 7 ? q + 1 : 7]; }
     }
-    if (run <= r) { atomicOr(L.err, 1u); return 0; }   // counts inconsistent with the bitmaps
+    if (run <= r) {                                      // counts inconsistent with the bitmaps
+        if (atomicCAS(L.dbg, 0u, 0x10000u | pidx) == 0u) L.dbg[1] = rank;
+        atomicOr(L.err, 1u);
+        return 0;
+    }
     r -= before;
     uint32_t k = 0, b = wsel & 0xffu;
     if (r >= b) {
@@ -379,7 +399,11 @@ __device__ uint32_t pool_select(const Lay& L, const Cfg& C, uint32_t pidx, uint3
             }
         }
     }
-    if (r >= (uint32_t)__popc(xsel)) { atomicOr(L.err, 1u); return 0; }   // counts inconsistent with the bitmaps
+    if (r >= (uint32_t)__popc(xsel)) {                  // counts inconsistent with the bitmaps
+        if (atomicCAS(L.dbg, 0u, 0x20000u | pidx) == 0u) L.dbg[1] = rank;
+        atomicOr(L.err, 1u);
+        return 0;
+    }
     return (w0 + ksel) * 32u + select_bit(xsel, r);
 }
 
@@ -738,16 +762,25 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
         if (is_miss) s_miss[mbase + ex] = s;
         mbase += tot;
     }
+    if (kSh && tid < 32)                     // C1: this shard's pool sizes after its hits, everyone's back
+        shard_c1(L, C, j, r, S.tot[0] - S.hits_loc[0], S.tot[1] - S.hits_loc[1], S.tot[2] - S.hits_loc[2], S.cnt);
     if (tid == 0) {
         uint32_t pa, pd, pe;                 // the pools' sizes after this round's hits
         if constexpr (kSh) {
             S.tot[0] -= S.hits_loc[0]; S.tot[1] -= S.hits_loc[1]; S.tot[2] -= S.hits_loc[2];
-            shard_c1(L, C, j, r, S.tot[0], S.tot[1], S.tot[2], S.cnt);          // C1
             pa = pd = pe = 0;
             for (uint32_t g = 0; g < C.G; ++g) { pa += S.cnt[g][0]; pd += S.cnt[g][1]; pe += S.cnt[g][2]; }
             S.glob[0] = pa; S.glob[1] = pd; S.glob[2] = pe;
+            if ((pa > C.N || pd > C.N || pe > C.N) && atomicCAS(L.dbg, 0u, 0x80000u | j) == 0u) {
+                L.dbg[1] = (uint32_t)r; L.dbg[2] = S.cnt[0][0]; L.dbg[3] = C.G > 1 ? S.cnt[1][0] : 0u;
+                atomicOr(L.err, 8u);                      // a global pool size above N (diagnostic)
+            }
         } else {
             pa = S.tot[0] - S.hits[0]; pd = S.tot[1] - S.hits[1]; pe = S.tot[2] - S.hits[2];
+            if ((pa > C.N || pd > C.N || pe > C.N) && atomicCAS(L.dbg, 0u, 0x40000u | j) == 0u) {
+                L.dbg[1] = (uint32_t)r; L.dbg[2] = S.tot[0]; L.dbg[3] = S.hits[0];
+                atomicOr(L.err, 8u);                      // a pool total below its hits (diagnostic)
+            }
             S.tot[0] = pa; S.tot[1] = pd; S.tot[2] = pe;
         }
         const uint32_t m = mbase;
@@ -1229,8 +1262,8 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
     if (!is_maint) {
         S.acc_dig[tid] = 0;
         if (tid < 12) S.acc_cnt[tid] = 0;
-        if (tid < 3) S.hits[tid] = 0;
-        if (tid < 3) S.tot[tid] = ldcg(L.cnt_tot + j * 3 + tid);
+        if (tid < 3) { S.hits[tid] = 0; S.hits_loc[tid] = 0; S.own[tid] = 0; }   // (shared memory is not zeroed
+        if (tid < 3) S.tot[tid] = ldcg(L.cnt_tot + j * 3 + tid);                   //  at launch: initcheck-blind)
         for (uint32_t k = tid; k < 3 * C.NS; k += blockDim.x) s_sup[k] = ldcg(L.cnt_sup + (size_t)j * 3 * C.NS + k);
     } else {
         if (tid == 0) {
@@ -1331,11 +1364,13 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
             schedule(part, departing);
             const uint32_t active_after = s_active & ~departing;
             expect += __popc(part);
-            if (kShard && tid == 0) {        // C1 of the storage pool as of round start
+            if (kShard && tid < 32) {        // C1 of the storage pool as of round start
                 shard_c1(L, C, C.J, r, M.PS, 0u, 0u, M.pscnt);
-                uint32_t t = 0;
-                for (uint32_t g = 0; g < C.G; ++g) t += M.pscnt[g][0];
-                M.PSg = t;
+                if (tid == 0) {
+                    uint32_t t = 0;
+                    for (uint32_t g = 0; g < C.G; ++g) t += M.pscnt[g][0];
+                    M.PSg = t;
+                }
             }
             if (tid == 0) {                  // job phases of round r done; evictions they pushed
                 unsigned long long v;
@@ -1842,6 +1877,7 @@ Sizes compute_sizes(const seneca_cache_config* cfg) {
     C.Nrow = (C.N + 63) & ~63u;
     C.FL = (uint32_t)(std::max<size_t>(C.cap_t, 1) + (size_t)C.J * C.Bmax);
     C.G = cfg->shards > 1 ? cfg->shards : 1u;
+    C.xsys = C.G > 1 && cfg->shard_mode == 1 ? 1u : 0u;
     C.mb_c1 = 0;
     C.mb_c2 = C.mb_c1 + 2 * (C.J + 1) * C.G * 4;
     C.mb_rf = C.mb_c2 + 2 * C.J * C.Bmax;
@@ -1912,6 +1948,7 @@ Lay carve(const Sizes& z, char* base, char* ctl, uint64_t seed) {
     L.bar = (uint32_t*)ctl;
     L.err = (uint32_t*)(ctl + 16);
     L.verr = (uint32_t*)(ctl + 20);
+    L.dbg = (uint32_t*)(ctl + 24);
     L.phase = (unsigned long long*)(base + z.off[26]);
     L.ev_ed = (uint32_t*)(base + z.off[27]);
     L.ev_ed_n = (uint32_t*)(base + z.off[28]);
@@ -2516,12 +2553,16 @@ extern "C" seneca_status seneca_shard_attach(seneca_ctx* c, void* const* peers) 
 
 extern "C" seneca_status seneca_sync_status(seneca_ctx* c, void* stream) {
     if (!c) { set_error("bad arguments"); return SENECA_EINVAL; }
-    uint32_t err[kMaxReplicas] = {0};
-    SENECA_CUDA_TRY(cudaMemcpy2DAsync(err, 4, c->L.err, kCtlBytes, 4, c->R, cudaMemcpyDeviceToHost,
+    uint32_t err[kMaxReplicas][8] = {{0}};
+    SENECA_CUDA_TRY(cudaMemcpy2DAsync(err, 32, c->L.err, kCtlBytes, 32, c->R, cudaMemcpyDeviceToHost,
                                       (cudaStream_t)stream));
     SENECA_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
     for (uint32_t k = 0; k < c->R; ++k)
-        if (err[k]) { set_error("device consistency check failed (replica %u, flags 0x%x)", k, err[k]); return SENECA_ESTATE; }
+        if (err[k][0]) {
+            set_error("device consistency check failed (replica %u, flags 0x%x; first: site 0x%x pool/job %u, "
+                      "%u %u %u)", k, err[k][0], err[k][2] >> 16, err[k][2] & 0xffffu, err[k][3], err[k][4], err[k][5]);
+            return SENECA_ESTATE;
+        }
     return SENECA_OK;
 }
 

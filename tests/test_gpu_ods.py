@@ -707,7 +707,10 @@ def test_sharded_replay_identical_for_every_G(name, scale):
     o = O.ODS(c["n_total"], c["batch"], c["target"], ce, cd, ca, seed, transcript=True)
     ro = o.replay_epochs(max(c["target"]))
     for G in (1, 2, 4, 8):
-        g, tr, r = sharded_replay(c, ce, cd, ca, seed, G)
+        try:
+            g, tr, r = sharded_replay(c, ce, cd, ca, seed, G)
+        except Exception as e:
+            raise AssertionError(f"G = {G}: {e}")
         assert r == ro
         for k in range(G):
             compare_replica(o, g, k, tr if G == 1 else tr[k])
