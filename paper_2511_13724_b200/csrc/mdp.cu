@@ -519,9 +519,17 @@ mdp_sweep_kernel(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_pro
 #ifndef SENECA_MDP_PAIRW
 #define SENECA_MDP_PAIRW 2
 #endif
+#ifndef SENECA_MDP_PUNROLL
+#define SENECA_MDP_PUNROLL 2      // pairs in flight per thread
+#endif
+#ifndef SENECA_MDP_HDR1
+#define SENECA_MDP_HDR1 1         // 1: the group's first warp derives the header, shared via shared memory (A/B)
+#endif
 constexpr uint32_t kPairW = SENECA_MDP_PAIRW;                 // warps per profile group
+constexpr int kPUnroll = SENECA_MDP_PUNROLL;
 constexpr uint32_t kGroups = kThreads / 32 / kPairW;          // groups per CTA
 constexpr uint32_t kMaxPairs = 2601;                          // 1 % grid: sum over rows of ceil((a + 1) / 2)
+static_assert(kPairW * 32 >= kMaxSteps / 2 + 1, "a thread must meet at most one pair per row (argmax order)");
 
 __device__ __forceinline__ void group_sync(uint32_t gid) {
     asm volatile("bar.sync %0, %1;" :: "r"(gid + 1), "r"(kPairW * 32) : "memory");
@@ -556,9 +564,13 @@ mdp_sweep_pairs(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_prof
     // p_D = (a - b) g) at enumeration index a(a+1)/2 + b (R-M9); pair (b, a - b)
     // for b <= a / 2.  x = row offset of p_A=b | of p_D=a-b << 12 | p_E row << 24,
     // y = index of (b, a - b) | index of (a - b, b) << 16.
+    // rows before a = 2m hold m(m + 1) pairs, before a = 2m + 1: (m + 1)^2
+    auto pairs_before = [](uint32_t a) { const uint32_t m = a >> 1; return (a & 1) ? (m + 1) * (m + 1) : m * (m + 1); };
     for (uint32_t t = threadIdx.x; t < n_pairs; t += blockDim.x) {
-        uint32_t a = 0, base = 0;                                   // row a holds pairs base .. base + a/2
-        while (base + a / 2 + 1 <= t) { base += a / 2 + 1; ++a; }
+        uint32_t a = 2u * (uint32_t)sqrtf((float)t);                 // row of pair t, then exact fix-up
+        while (a > 0 && pairs_before(a) > t) --a;
+        while (pairs_before(a + 1) <= t) ++a;
+        const uint32_t base = pairs_before(a);                      // row a holds pairs base .. base + a/2
         const uint32_t b = t - base, m = a - b, i0 = a * (a + 1) / 2;
         s_pair[t] = make_uint2((uint32_t)(b * sizeof(Row)) | (uint32_t)(m * sizeof(Row)) << 12 | (steps - a) << 24,
                                (i0 + b) | (i0 + m) << 16);
@@ -568,7 +580,18 @@ mdp_sweep_pairs(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_prof
     const uint32_t n_groups = gridDim.x * kGroups;
     for (uint32_t pi = blockIdx.x * kGroups + gid; pi < n_profiles; pi += n_groups) {
         const seneca_mdp_profile prof = profiles[pi];
+#if SENECA_MDP_HDR1
+        // Eqs. 1-4 by the group's first warp, shared through shared memory
+        __shared__ Hdr s_h[kGroups];
+        if (gw == 0) {
+            const Hdr h0 = warp_header(prof);
+            if (lane == 0) s_h[gid] = h0;
+        }
+        group_sync(gid);
+        const Hdr H = s_h[gid];
+#else
         const Hdr H = warp_header(prof);
+#endif
         double best = __longlong_as_double(0xfff0000000000000ll);
         uint32_t best_i = 0xffffffffu;
         if (H.valid) {                                              // group-uniform
@@ -589,7 +612,7 @@ mdp_sweep_pairs(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_prof
                 const uint32_t N = (uint32_t)B.N;
                 const double dN = u2d(B.N), y = __drcp_rn(dN), dsiE = H.dsi[2], dsiS = H.dsi[3];
                 const char* rb0 = reinterpret_cast<const char*>(rows);
-#pragma unroll 2
+#pragma unroll (kPUnroll)
                 for (uint32_t t = gt; t < n_pairs; t += kPairW * 32) {
                     const uint2 w = s_pair[t];
                     const Row& rb = *reinterpret_cast<const Row*>(rb0 + (w.x & 0xfffu));
@@ -609,8 +632,11 @@ mdp_sweep_pairs(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_prof
                     const double v1 = __dadd_rn(__dadd_rn(__dadd_rn(rm.tA, dfree ? rb.tD : rm.tDc), tX), prod);
                     const uint32_t i0 = w.y & 0xffffu, i1 = w.y >> 16;
                     if (grow) { __stcs(grow + i0, v0); __stcs(grow + i1, v1); }
-                    if (v0 > best || (v0 == best && i0 < best_i)) { best = v0; best_i = i0; }
-                    if (v1 > best || (v1 == best && i1 < best_i)) { best = v1; best_i = i1; }
+                    // a thread meets at most one pair per row (kPairW * 32 >= the 51 pairs
+                    // of the longest row) and i0 <= i1, so its indices only increase:
+                    // strict > keeps the first maximum = the smallest index (R-M8)
+                    if (v0 > best) { best = v0; best_i = i0; }
+                    if (v1 > best) { best = v1; best_i = i1; }
                 }
             } else {                                                // N >= 2^31: 64-bit counts (rare)
                 const uint64_t N = B.N;
