@@ -188,7 +188,8 @@ def run_reference(args, rank, world):
                 higher_is_better=True, scaling="weak", vs_baseline=None, dtype="u32", data="synthetic",
                 config=workload_config(c, args.workload, dict(note="reference arm = the CPU oracle")),
                 cpu_baseline=dict(value=val, unit="decisions/s", cores=1, kind="oracle", sample=sample),
-                e2e=dict(value=val, unit="decisions/s", h2d_bytes_per_step=0, d2h_bytes_per_step=0))
+                e2e=dict(value=val, unit="decisions/s", h2d_bytes_per_step=0, d2h_bytes_per_step=0),
+                so_loaded=repo_so_loaded())
     print(json.dumps(line), flush=True)
     return 0
 
@@ -312,7 +313,18 @@ def algorithmic_bytes(name, info):
     return 0
 
 
-NCU_TRAFFIC = os.path.join(ROOT, "profiles", "r1", "ncu_traffic.json")
+NCU_TRAFFIC = os.path.join(ROOT, "profiles", "r2", "ncu_traffic.json")
+
+
+def repo_so_loaded():
+    """The shared objects of this repository mapped into this process (evidence of
+    which native code ran: the reference arm must show only oracle/liboracle.so)."""
+    try:
+        maps = open("/proc/self/maps").read().split("\n")
+    except OSError:
+        return None
+    return sorted({os.path.relpath(l.split()[-1], ROOT) for l in maps
+                   if l.strip().endswith(".so") and l.split()[-1].startswith(ROOT)})
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12      # nominal B200 FP64 (non-tensor), ~37.2 TFLOP/s
 
 
@@ -962,6 +974,7 @@ def main():
             kernels=kernels,
             ods_round_phase_share=phase_share,
             parity=parity,
+            so_loaded=repo_so_loaded(),
         )
         print(json.dumps(line), flush=True)
     S.destroy(last_ctx)

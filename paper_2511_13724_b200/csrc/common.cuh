@@ -9,6 +9,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>     // header-only NVTX v3: no-op unless a profiler injects itself
 
 #include "../../include/seneca.h"
 
@@ -17,6 +18,15 @@ namespace seneca {
 // ---------------------------------------------------------------- error plumbing
 void set_error(const char* fmt, ...);
 seneca_status cuda_status(cudaError_t e, const char* what);
+
+// Host-side NVTX range over a C-ABI call (tracing: nsys / ncu --nvtx timelines
+// show init, each round launch, the ring generation and the MDP sweep).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 #define SENECA_CUDA_TRY(expr)                                              \
     do {                                                                   \

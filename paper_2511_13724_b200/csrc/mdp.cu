@@ -772,6 +772,7 @@ extern "C" uint64_t seneca_mdp_num_splits(uint32_t g) {
 extern "C" seneca_status seneca_mdp_sweep(const seneca_mdp_profile* d_profiles, uint32_t n_profiles,
                                           uint32_t grid_step_pct, seneca_mdp_result* d_results,
                                           double* d_grid, void* stream) {
+    seneca::NvtxRange nvtx("seneca_mdp_sweep");
     using namespace seneca;
     if (grid_step_pct == 0 || grid_step_pct > 100 || 100 % grid_step_pct) {
         set_error("seneca_mdp_sweep: grid_step_pct %u does not divide 100", grid_step_pct);

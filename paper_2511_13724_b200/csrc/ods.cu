@@ -109,7 +109,8 @@ struct Lay {
     uint32_t *perm_done;             // [J][maxT] positions finished
     uint32_t *epoch_at;              // [J] epoch job j plays (published at each epoch start, release):
                                      //     the concurrent ring generator refills slot e % K once it is >= e - K + 1
-    uint32_t *gen_next;              // [1] work counter of the concurrent ring generator
+    uint32_t *gen_next;              // [1] work counter of the ring generator CTAs
+    uint32_t *ring_pairs;            // [kRingPairs] (job << 24 | epoch) the generator CTAs fill, in order
     JobDev *jobs;                    // [J]
     uint32_t *out_ids;               // [J][Bmax] replay scratch
     uint8_t *out_src;                // [J][Bmax]
@@ -169,6 +170,8 @@ struct Launch {
     unsigned long long* transcript;  // [replica][J][maxT][N] or null
     uint64_t out_rep;                // elements of out_ids / out_src per replica
     uint64_t tr_rep;                 // elements of transcript per replica
+    uint32_t gen_ctas;               // trailing CTAs of the launch that refill the permutation ring (§7.2)
+    uint32_t gen_pairs;              // (job, epoch) pairs they fill, L.ring_pairs of slice 0
 };
 
 __device__ __forceinline__ uint32_t ldcg(const uint32_t* p) { return __ldcg(p); }
@@ -1192,8 +1195,14 @@ __device__ void job_take_refills(const Lay& L, const Cfg& C, JobSmem& S, uint32_
 // ------------------------------------------------------------------ the persistent round kernel
 // Grid: (J + 1) CTAs per replica; replicas are independent replays (their own
 // workspace slice and seed) that share nothing but the launch.
+__device__ __noinline__ void ring_generate(const Lay& L, const Cfg& C, uint32_t n_pairs);
+
 template <bool kTime, bool kCoupled, bool kShard>
 __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, const Launch& P) {
+    if (P.gen_ctas && blockIdx.x >= gridDim.x - P.gen_ctas) {     // the permutation-ring generator CTAs
+        ring_generate(LS.r[0], C, P.gen_pairs);
+        return;
+    }
     extern __shared__ __align__(16) uint32_t smem[];
     __shared__ JobSmem S;
     __shared__ MaintSmem M;
@@ -1565,7 +1574,7 @@ struct PermWork {
 };
 
 // The epochs a single-replica launch's jobs enter during the launch, in the
-// order their ring slots free (refilled concurrently by ods_perm_ring).
+// order their ring slots free (refilled by the launch's generator CTAs).
 constexpr uint32_t kRingPairs = 1024;
 struct PermRing {
     uint32_t n;
@@ -1603,18 +1612,18 @@ __global__ void ods_perm_all(const __grid_constant__ Lays LS, const __grid_const
     }
 }
 
-// The ring generator that runs CONCURRENTLY with a single-replica round launch
-// (side stream): it refills slot e % K with epoch e of job j as soon as job j has
-// started epoch e - K + 1 (epoch_at, released by the job CTA at its epoch
-// reset), so no launch has to stop at an epoch boundary.  Work items (pair,
-// chunk) are taken in the given order (pairs sorted by the round their slot
-// frees), one 16 K-position chunk per CTA at a time; the waiting CTA sleeps.
-// The host sizes its grid so the round launch's J + 1 CTAs always fit beside it.
-__global__ void __launch_bounds__(512)
-ods_perm_ring(const __grid_constant__ Lay L, const __grid_constant__ Cfg C, const __grid_constant__ PermRing W,
-              uint32_t chunk) {
+// The ring generator CTAs of a single-replica round launch (the trailing
+// P.gen_ctas CTAs of the cooperative grid, so they are co-resident with the job
+// CTAs by construction -- no reliance on two concurrent kernels, which a
+// serialising profiler would deadlock): slot e % K is refilled with epoch e of
+// job j as soon as job j has started epoch e - K + 1 (epoch_at, released by the
+// job CTA at its epoch reset), so no launch has to stop at an epoch boundary.
+// Work items (pair, 16 K-position chunk) are taken in list order (pairs sorted
+// by the round their slot frees); a waiting CTA sleeps.
+__device__ __noinline__ void ring_generate(const Lay& L, const Cfg& C, uint32_t n_pairs) {
+    constexpr uint32_t chunk = 16384;
     const uint32_t per = (C.N + chunk - 1) / chunk;
-    const uint32_t total = W.n * per;
+    const uint32_t total = n_pairs * per;
     const PermDomain dom = perm_domain(C.N);
     __shared__ uint32_t s_item, s_last;
     for (;;) {
@@ -1623,9 +1632,10 @@ ods_perm_ring(const __grid_constant__ Lay L, const __grid_constant__ Cfg C, cons
         const uint32_t item = s_item;
         if (item >= total) break;
         const uint32_t pair = item / per, part = item % per;
-        const uint32_t e = W.e[pair], j = W.j[pair];
+        const uint32_t pj = ldcg(L.ring_pairs + pair);
+        const uint32_t e = pj & 0xffffffu, j = pj >> 24;
         if (threadIdx.x == 0)
-            while (ld_acquire(L.epoch_at + j) + C.K - 1 < e) __nanosleep(2000);
+            while (ld_acquire(L.epoch_at + j) + C.K - 1 < e) __nanosleep(1000);
         __syncthreads();
         const uint64_t key = derive_key(L.seed, PUR_REQ, j, e, 0);
         uint32_t* out = L.perms + ((size_t)j * C.K + (e & (C.K - 1))) * C.Nrow;
@@ -1785,6 +1795,8 @@ struct seneca_ctx {
     uint64_t r;
     uint64_t gen_hi[kMaxJobs];     // permutations of epochs < gen_hi[j] have been generated (ring, C.K slots)
     uint32_t shard_mode;           // sharded (C.G > 1): 0 all shards in this context, 1 one shard
+    uint32_t gen_ctas;             // ring generator CTAs appended to single-replica launches (0: none)
+    uint32_t ring_host[1024];      // staging of the generator work list (cudaMemcpyAsync from pageable memory)
     bool attached;                 // shard_mode 1: the peers' mailboxes are known
     uint64_t launches;
     uint64_t klaunch[K_NCLASS];
@@ -1906,6 +1918,7 @@ Sizes compute_sizes(const seneca_cache_config* cfg) {
         4, C.cold ? W : 4,                                  // 31-32 warm, claim
         (size_t)C.J * 4, 4,                                 // 33-34 epoch_at, gen_next
         mbox_u32 * 4,                                       // 35 shard mailbox
+        (size_t)kRingPairs * 4,                             // 36 ring generator work list
     };
     size_t at = 0;
     for (size_t k = 0; k < sizeof(sz) / sizeof(sz[0]); ++k) {
@@ -1959,6 +1972,7 @@ Lay carve(const Sizes& z, char* base, char* ctl, uint64_t seed) {
     L.epoch_at = (uint32_t*)(base + z.off[33]);
     L.gen_next = (uint32_t*)(base + z.off[34]);
     L.mbox = (uint32_t*)(base + z.off[35]);
+    L.ring_pairs = (uint32_t*)(base + z.off[36]);
     for (uint32_t g = 0; g < kMaxShards; ++g) L.peer[g] = nullptr;
     L.shard = 0; L.sb_lo = 0; L.sb_hi = z.C.NS; L.id_lo = 0; L.id_hi = z.C.NS * 4096u;
     return L;
@@ -2061,7 +2075,10 @@ uint64_t rounds_allowed(const seneca_ctx* c, uint64_t R, uint32_t jobs_mask) {
 //    different rounds never have to meet at a launch boundary.
 //  * Several replicas: the launch stops before a job would enter an epoch that
 //    is not in the ring (rounds_allowed); the next launch refills it.
-seneca_status prepare_perms(seneca_ctx* c, cudaStream_t st, uint64_t R, uint32_t jobs_mask, uint64_t* R_out) {
+seneca_status prepare_perms(seneca_ctx* c, cudaStream_t st, uint64_t R, uint32_t jobs_mask, uint64_t* R_out,
+                            uint32_t* gen_pairs) {
+    *gen_pairs = 0;
+    NvtxRange nvtx("seneca permutation ring");
     *R_out = R;
     if (c->mode != 0) return SENECA_OK;
     const uint32_t K = c->C.K;
@@ -2090,7 +2107,7 @@ seneca_status prepare_perms(seneca_ctx* c, cudaStream_t st, uint64_t R, uint32_t
         SENECA_CUDA_TRY(cudaGetLastError());
         for (uint32_t j = 0; j < kMaxJobs; ++j) c->gen_hi[j] = gen[j];
     }
-    if (c->R > 1 || c->C.maxT <= K) {
+    if (c->R > 1 || c->C.maxT <= K || c->gen_ctas == 0) {
         *R_out = rounds_allowed(c, R, jobs_mask);
         return SENECA_OK;
     }
@@ -2122,16 +2139,11 @@ seneca_status prepare_perms(seneca_ctx* c, cudaStream_t st, uint64_t R, uint32_t
     }
     *R_out = k;
     if (Q.n) {
-        SENECA_CUDA_TRY(cudaEventRecord(c->ev_init, st));
-        SENECA_CUDA_TRY(cudaStreamWaitEvent(c->side, c->ev_init, 0));
-        SENECA_CUDA_TRY(cudaMemsetAsync(c->L.gen_next, 0, 4, c->side));
-        // beside the round launch's J + 1 one-CTA-per-SM CTAs (never timed: it
-        // waits for the round launch that follows it)
-        const uint32_t g = std::max<int>(1, std::min<int>(16, num_sms() - (int)c->C.J - 1));
-        c->launches++;
-        c->klaunch[K_PERM]++;
-        ods_perm_ring<<<g, 512, 0, c->side>>>(c->L, c->C, Q, chunk);
-        SENECA_CUDA_TRY(cudaGetLastError());
+        // the launch's trailing generator CTAs fill them (ring_generate)
+        for (uint32_t x = 0; x < Q.n; ++x) c->ring_host[x] = Q.j[x] << 24 | Q.e[x];
+        SENECA_CUDA_TRY(cudaMemcpyAsync(c->L.ring_pairs, c->ring_host, (size_t)Q.n * 4, cudaMemcpyHostToDevice, st));
+        SENECA_CUDA_TRY(cudaMemsetAsync(c->L.gen_next, 0, 4, st));
+        *gen_pairs = Q.n;
         for (uint32_t j = 0; j < kMaxJobs; ++j) c->gen_hi[j] = gen[j];
     }
     return SENECA_OK;
@@ -2143,6 +2155,7 @@ seneca_status prepare_perms(seneca_ctx* c, cudaStream_t st, uint64_t R, uint32_t
 seneca_status launch_rounds(seneca_ctx* c, uint64_t* Rio, uint32_t jobs_mask, const uint32_t* d_requested,
                             uint32_t* out_ids, uint8_t* out_src, uint32_t out_stride, const uint32_t* row_of_job,
                             unsigned long long* transcript, cudaStream_t st) {
+    NvtxRange nvtx("seneca round launch");
     uint64_t R = *Rio;
     if (!c->attached) { set_error("sharded context: attach the peers' mailboxes first"); return SENECA_ESTATE; }
     Launch P;
@@ -2169,8 +2182,11 @@ seneca_status launch_rounds(seneca_ctx* c, uint64_t* Rio, uint32_t jobs_mask, co
     P.timing = (c->profiling >> 1) & 1u;
     {
         uint64_t Rp = R;
-        seneca_status ps = prepare_perms(c, st, R, jobs_mask, &Rp);
+        uint32_t gp = 0;
+        seneca_status ps = prepare_perms(c, st, R, jobs_mask, &Rp, &gp);
         if (ps) return ps;
+        P.gen_pairs = gp;
+        P.gen_ctas = gp ? c->gen_ctas : 0u;
         if (Rp == 0) { set_error("internal: no round playable within the permutation ring"); return SENECA_ESTATE; }
         R = Rp;
         P.rounds = (uint32_t)R;
@@ -2194,7 +2210,8 @@ seneca_status launch_rounds(seneca_ctx* c, uint64_t* Rio, uint32_t jobs_mask, co
     void* args[] = {&c->LS, &c->C, &P};
     cudaError_t le = cudaSuccess;
     timed(c, K_ROUNDS, st, [&] {
-        le = cudaLaunchCooperativeKernel(P.timing ? c->round_fn_timed : c->round_fn, dim3((c->C.J + 1) * c->R), dim3(c->round_threads), args,
+        le = cudaLaunchCooperativeKernel(P.timing ? c->round_fn_timed : c->round_fn,
+                                         dim3((c->C.J + 1) * c->R + P.gen_ctas), dim3(c->round_threads), args,
                                          c->round_smem, st);
     });
     if (le != cudaSuccess) return cuda_status(le, "cudaLaunchCooperativeKernel(ods_rounds)");
@@ -2226,6 +2243,7 @@ extern "C" seneca_status seneca_state_bytes(const seneca_cache_config* cfg, size
 
 extern "C" seneca_status seneca_init_cache(const seneca_cache_config* cfg, void* d_workspace, size_t ws_bytes,
                                            void* stream, seneca_ctx** out) {
+    NvtxRange nvtx("seneca_init_cache");
     seneca_status s = check_cfg(cfg);
     if (s) return s;
     if (!out || !d_workspace) { set_error("NULL workspace or out"); return SENECA_EINVAL; }
@@ -2369,6 +2387,16 @@ extern "C" seneca_status seneca_init_cache(const seneca_cache_config* cfg, void*
             c->round_smem = smem2;
         }
     }
+    if (z.R == 1 && z.C.maxT > z.C.K && cfg->request_mode == 0) {
+        // ring generator CTAs appended to every launch that needs them: as many as
+        // fit beside the J + 1 round CTAs, at most 16 (timed variant checked too)
+        int per = 0, per_t = 0;
+        INIT_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, c->round_fn, c->round_threads, c->round_smem));
+        INIT_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_t, c->round_fn_timed, c->round_threads,
+                                                               c->round_smem));
+        const int64_t room = (int64_t)std::min(per, per_t) * num_sms() - (int64_t)(z.C.J + 1);
+        c->gen_ctas = (uint32_t)std::max<int64_t>(0, std::min<int64_t>(16, room));
+    }
     INIT_TRY(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
     INIT_TRY(cudaEventCreateWithFlags(&c->ev_init, cudaEventDisableTiming));
     INIT_TRY(cudaEventCreate(&c->ev_a));
@@ -2394,7 +2422,8 @@ extern "C" seneca_status seneca_init_cache(const seneca_cache_config* cfg, void*
     // the caller's next work when there is one replica (ensure_perms)
     {
         uint64_t unused = 0;
-        const seneca_status ps = prepare_perms(c, st, 0, 0xffffffffu, &unused);
+        uint32_t unused_pairs = 0;
+        const seneca_status ps = prepare_perms(c, st, 0, 0xffffffffu, &unused, &unused_pairs);
         if (ps) { delete c; return ps; }
     }
 #undef INIT_TRY
@@ -2453,6 +2482,7 @@ static uint64_t rounds_for_epochs(const seneca_ctx* c, uint32_t n_epochs) {
 }
 
 static seneca_status replay(seneca_ctx* c, uint64_t R, uint64_t* d_transcript, uint64_t* h_rounds, cudaStream_t st) {
+    NvtxRange nvtx("seneca_replay");
     if (c->mode != 0) { set_error("replay requires request_mode 0"); return SENECA_ESTATE; }
     if (!(c->active | c->pending)) { set_error("no active job"); return SENECA_ESTATE; }
     uint64_t done = 0;

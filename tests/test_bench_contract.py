@@ -26,27 +26,34 @@ def test_reference_arm_json_line():
 
 
 def test_committed_bench_lines_have_the_contract_keys():
-    import glob
+    """The committed round-2 bench lines (profiles/r2, the pass its README names)
+    carry the driver's keys, a roofline with its latency floor, bit-exact parity
+    gates on every workload, replica and shard count, and the reference arm
+    loads nothing but the oracle."""
     import re
-    readme = open(os.path.join(ROOT, "profiles", "r1", "README.md")).read()
-    tag = re.search(r"Current pass: \*\*(r1[a-z])\*\*", readme).group(1)      # the pass the README names
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r1", f"bench_*_{tag}.json"))) + \
-        [os.path.join(ROOT, "profiles", "r1", f"bench_{tag}.json")]
-    files = [f for f in files if os.path.exists(f) and "reference" not in f]
-    assert files
-    for f in files:
-        d = json.loads(open(f).read().strip().splitlines()[-1])
-        for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
-                  "scaling", "vs_baseline", "dtype", "data", "config", "e2e", "roofline", "clocks", "gpu_launches"):
-            assert k in d, (f, k)
-        r = d["roofline"]
-        for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
-            assert k in r, (f, k)
-        assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
-        assert d["steps"] >= 1 and d["warmup"] >= 3 and d["gpu_launches"] > 0
-        assert d["parity"]["ods_vs_oracle_golden"] == "bit-exact"
-        assert d["parity"]["mdp_vs_oracle_first_200_profiles"] == "bit-exact"
-        assert not set(d["clocks"]["reasons"]) & {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+    readme = open(os.path.join(ROOT, "profiles", "r2", "README.md")).read()
+    tag = re.search(r"Current pass: \*\*(r2[a-z]?)\*\*", readme).group(1)
+    d = json.loads(open(os.path.join(ROOT, "profiles", "r2", f"bench_{tag}.json")).read().strip().splitlines()[-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "e2e", "roofline", "clocks", "gpu_launches",
+              "cpu_baseline"):
+        assert k in d, k
+    r = d["roofline"]
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert k in r, k
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    assert 0 < r["latency"]["frac"] <= 1 and r["latency"]["floor_us_per_round"] > 0
+    assert d["config"]["workload"].startswith("imagenet22k")
+    assert d["steps"] >= 1 and d["warmup"] >= 3 and d["gpu_launches"] > 0
+    assert d["parity"]["ods_vs_oracle_golden"] == "bit-exact"
+    assert d["parity"]["mdp_vs_oracle_first_200_profiles"] == "bit-exact"
+    for w in ("imagenet1k", "openimages"):
+        assert d["workloads"][w]["parity"] == "bit-exact", w
+    assert all(v == "bit-exact" or v is True for v in d["replicas"]["parity"].values())
+    assert all(run["parity"] == "bit-exact" for run in d["sharded"]["runs"])
+    assert not set(d["clocks"]["reasons"]) & {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+    ref = json.loads(open(os.path.join(ROOT, "profiles", "r2", f"bench_reference_{tag}.json")).read().strip())
+    assert ref["impl"] == "reference" and ref["so_loaded"] == ["oracle/liboracle.so"]
 
 
 def test_pass_equivalent_matches_the_survey_sizes():
@@ -94,3 +101,30 @@ def test_all_cores_oracle_baselines():
     v, cores, dec, dt = bench.oracle_ods_all_cores(args, c, bench.oracle_caps(c), 10)
     assert dec == cores * 10 * sum(c["batch"])          # every replay plays 10 full rounds of both jobs
     assert v > 0
+
+
+def test_latency_floor_model():
+    """bench.latency_floor (DESIGN.md 7.1 "latency roofline"): per job-round
+    floor = dependent L2 trips x 300 cycles + scattered accesses x 1 cycle +
+    substituting share x the perm_apply chain (1,790 cycles), from the replay's
+    own counters.  Pinned on a hand-computed case: one job, 1,000 samples,
+    batch 100 (10 job-rounds), E tier only, 400 requested hits and 300
+    substitutes over the epoch, no A."""
+    import numpy as np
+    sys.path.insert(0, ROOT)
+    import bench
+    c = dict(n_total=1000, batch=[100], target=[1])
+    st = np.zeros((1, 1), dtype=[("served", "<u8", 4), ("subst", "<u8", 4), ("req_hits", "<u8", 4), ("digest", "<u8")])
+    st["served"][0, 0] = [300, 700, 0, 0]            # storage 300, E 700 (= 400 hits + 300 substitutes)
+    st["subst"][0, 0] = [0, 300, 0, 0]
+    st["req_hits"][0, 0] = [0, 400, 0, 0]
+    lf = bench.latency_floor(c, (500, 0, 0), st, 10, 0, 0, 2000.0)
+    jr, req, hits, subs = 10, 1000.0, 400.0, 300.0
+    sub_rounds = min(jr, subs / ((req - hits) / jr))                    # 5
+    positions = req + subs
+    scattered = positions / 4 + positions + req * 1 + req + hits + subs + 2 * subs + 2 * subs + subs
+    dep = jr * 3 + 2 * sub_rounds
+    cyc = dep * 300 + scattered + sub_rounds * 1790
+    assert abs(lf["cycles_per_job_round"] - cyc / jr) < 1e-9
+    assert abs(lf["floor_us_per_round"] - cyc / jr / 2000.0) < 1e-12
+    assert abs(lf["substituting_job_round_share"] - 0.5) < 1e-12
