@@ -764,66 +764,6 @@ def main():
                                   every_replica_served_each_sample_once_per_job_epoch=all(t["served_ok"] for t in tried))
         rep_line.pop("served_ok", None)
 
-    # ---- ONE replay partitioned by sample-ID range (SURVEY §8(e)), timed like the
-    #      headline (init_cache + the full replay, L2 flushed, one warm-up) and gated
-    #      by the golden digests on every shard.  N = 1: G shards emulated on this
-    #      device (one launch of G x (J + 1) CTAs exchanging through device
-    #      mailboxes); N > 1: rank r is shard r of one replay (mailboxes mapped into
-    #      every rank over NVLink by CUDA IPC, the kernels store into their peers'),
-    #      strong scaling of one replay -- reported beside the headline.
-    sharded = None
-    shard_counts = ([int(x) for x in args.shards.split(",") if x] if world == 1 else
-                    ([] if args.no_shard_replay else [world]))
-    if shard_counts:
-        import paper_2511_13724_b200 as P
-        us1 = 1e6 * (sum(ods_ms) / 1e3) / rounds_tot            # the unsharded headline, this rank
-        sharded = dict(mode="emulated on one device" if world == 1 else "one shard per GPU (CUDA IPC mailboxes)",
-                       workload=args.workload, unsharded_us_per_round=us1, runs=[],
-                       note="exchange_us_per_round = us_per_round - unsharded_us_per_round: the cost of the two "
-                            "per-round exchanges (pool sizes, resolved ids) and the replicated work, DESIGN.md 8")
-        c_sh = synth.ods_config(args.workload, seed=synth.PERF_SEED)
-        for G in shard_counts:
-            try:
-                ms_g, rr_g, gate = [], 0, "bit-exact"
-                for s_ in range(2):
-                    flush.fill_(s_ & 0xFF)
-                    barrier()
-                    torch.cuda.synchronize(dev)
-                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    kw = dict(shards=G) if world == 1 else dict(shards=G, shard_rank=rank, shard_mode=1)
-                    if world > 1:
-                        gsh = P.ODSContext(c_sh["n_total"], c_sh["batch"], c_sh["target"], ce, cd, ca, c_sh["seed"],
-                                           evict_tiers=args.evict_tiers, stream=stream, **kw)
-                        D.attach_shard_peers(gsh)
-                        torch.cuda.synchronize(dev)
-                        barrier()
-                        e0.record(stream)
-                    else:
-                        e0.record(stream)
-                        gsh = P.ODSContext(c_sh["n_total"], c_sh["batch"], c_sh["target"], ce, cd, ca, c_sh["seed"],
-                                           evict_tiers=args.evict_tiers, stream=stream, **kw)
-                    rr_g = gsh.replay_epochs(max(c_sh["target"]))
-                    e1.record(stream)
-                    torch.cuda.synchronize(dev)
-                    barrier()
-                    if s_ == 1:
-                        ms_g.append(e0.elapsed_time(e1))
-                        gsh.sync()
-                        for k in range(gsh.R):
-                            stk, evk, rfk = gsh.stats(k)
-                            gk = golden_gate(args.workload, c_sh["seed"], args.evict_tiers, stk, evk, rfk)
-                            if gk != "bit-exact":
-                                gate = f"shard {k}: {gk}"
-                    gsh.close()
-                (t_g,) = D.reduce_times([sum(ms_g) / 1e3], device=red_dev)
-                sharded["runs"].append(dict(shards=G, ms=1e3 * t_g, rounds=rr_g,
-                                            us_per_round=1e6 * t_g / rr_g,
-                                            exchange_us_per_round=1e6 * t_g / rr_g - us1,
-                                            value=dec_per_step / t_g, unit="decisions/s (one replay)",
-                                            parity=gate))
-            except Exception as ex:  # report; the headline stands
-                sharded["runs"].append(dict(shards=G, error=f"{type(ex).__name__}: {ex}"[:300]))
-
     # ---- e2e through the public API with host buffers (pinned), copies inside
     pin_prof = torch.from_numpy(prof_host.view(np.uint8).copy()).pin_memory()
     pin_res = torch.empty(d_res.numel(), dtype=torch.uint8).pin_memory()
@@ -929,6 +869,67 @@ def main():
                             ncu_traffic(tkey["mdp_sweep"]))
     for name in kernels:
         kernels[name]["algorithmic_bytes_per_launch"] = algorithmic_bytes(name, info)
+
+    # ---- (last of the device work, so that nothing else depends on it)
+    # ---- ONE replay partitioned by sample-ID range (SURVEY §8(e)), timed like the
+    #      headline (init_cache + the full replay, L2 flushed, one warm-up) and gated
+    #      by the golden digests on every shard.  N = 1: G shards emulated on this
+    #      device (one launch of G x (J + 1) CTAs exchanging through device
+    #      mailboxes); N > 1: rank r is shard r of one replay (mailboxes mapped into
+    #      every rank over NVLink by CUDA IPC, the kernels store into their peers'),
+    #      strong scaling of one replay -- reported beside the headline.
+    sharded = None
+    shard_counts = ([int(x) for x in args.shards.split(",") if x] if world == 1 else
+                    ([] if args.no_shard_replay else [world]))
+    if shard_counts:
+        import paper_2511_13724_b200 as P
+        us1 = 1e6 * (sum(ods_ms) / 1e3) / rounds_tot            # the unsharded headline, this rank
+        sharded = dict(mode="emulated on one device" if world == 1 else "one shard per GPU (CUDA IPC mailboxes)",
+                       workload=args.workload, unsharded_us_per_round=us1, runs=[],
+                       note="exchange_us_per_round = us_per_round - unsharded_us_per_round: the cost of the two "
+                            "per-round exchanges (pool sizes, resolved ids) and the replicated work, DESIGN.md 8")
+        c_sh = synth.ods_config(args.workload, seed=synth.PERF_SEED)
+        for G in shard_counts:
+            try:
+                ms_g, rr_g, gate = [], 0, "bit-exact"
+                for s_ in range(2):
+                    flush.fill_(s_ & 0xFF)
+                    barrier()
+                    torch.cuda.synchronize(dev)
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    kw = dict(shards=G) if world == 1 else dict(shards=G, shard_rank=rank, shard_mode=1)
+                    if world > 1:
+                        gsh = P.ODSContext(c_sh["n_total"], c_sh["batch"], c_sh["target"], ce, cd, ca, c_sh["seed"],
+                                           evict_tiers=args.evict_tiers, stream=stream, **kw)
+                        D.attach_shard_peers(gsh)
+                        torch.cuda.synchronize(dev)
+                        barrier()
+                        e0.record(stream)
+                    else:
+                        e0.record(stream)
+                        gsh = P.ODSContext(c_sh["n_total"], c_sh["batch"], c_sh["target"], ce, cd, ca, c_sh["seed"],
+                                           evict_tiers=args.evict_tiers, stream=stream, **kw)
+                    rr_g = gsh.replay_epochs(max(c_sh["target"]))
+                    e1.record(stream)
+                    torch.cuda.synchronize(dev)
+                    barrier()
+                    if s_ == 1:
+                        ms_g.append(e0.elapsed_time(e1))
+                        gsh.sync()
+                        for k in range(gsh.R):
+                            stk, evk, rfk = gsh.stats(k)
+                            gk = golden_gate(args.workload, c_sh["seed"], args.evict_tiers, stk, evk, rfk)
+                            if gk != "bit-exact":
+                                gate = f"shard {k}: {gk}"
+                    gsh.close()
+                (t_g,) = D.reduce_times([sum(ms_g) / 1e3], device=red_dev)
+                sharded["runs"].append(dict(shards=G, ms=1e3 * t_g, rounds=rr_g,
+                                            us_per_round=1e6 * t_g / rr_g,
+                                            exchange_us_per_round=1e6 * t_g / rr_g - us1,
+                                            value=dec_per_step / t_g, unit="decisions/s (one replay)",
+                                            parity=gate))
+            except Exception as ex:  # report; the headline stands
+                sharded["runs"].append(dict(shards=G, error=f"{type(ex).__name__}: {ex}"[:300]))
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:

@@ -55,6 +55,9 @@ constexpr uint32_t kMaxJobs = 32;
 constexpr uint32_t kMaxReplicas = 64;        // independent replay instances per context
 constexpr uint32_t kMaxShards = 8;           // sample-ID-range shards of one replay
 constexpr uint32_t kMaxBatch = 4096;
+#ifndef SENECA_EMPTY_POOLS_FAST
+#define SENECA_EMPTY_POOLS_FAST 1    // skip the classification gathers when every pool of the job is empty
+#endif
 #ifndef SENECA_ODS_THREADS
 #define SENECA_ODS_THREADS 512
 #endif
@@ -729,6 +732,16 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
 
     // a3: hits (E, D, or A not consumed by j, R-O13) join seen_j now
     uint32_t mbase = 0;
+#if SENECA_EMPTY_POOLS_FAST
+    // every request is unseen by j, and an unseen E or D id -- or an unseen A id
+    // j has not consumed -- is by definition a member of j's pool of that tier
+    // (R-O2): with all three pools empty no request can hit, so no residency
+    // word needs gathering (the same decisions; not under the baseline sampler,
+    // whose A hits ignore consumption, nor sharded, whose totals are local)
+    const bool none_cached = !kSh && !C.baseline && (S.tot[0] | S.tot[1] | S.tot[2]) == 0u;
+#else
+    const bool none_cached = false;
+#endif
     for (uint32_t base = 0; base < need; base += T) {
         const uint32_t s = base + tid;
         bool is_miss = false;
@@ -736,9 +749,9 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
             const uint32_t i = s_req[s];
             const uint32_t w = i >> 5, b = 1u << (i & 31);
             // only the tiers that exist are gathered; the consumer word only for A ids
-            const uint32_t wa = C.cap_a ? ldcg(L.bm_a + w) : 0u;
-            const uint32_t wd = C.cap_d ? ldcg(L.bm_d + w) : 0u;
-            const uint32_t we = C.cap_e ? ldcg(L.bm_e + w) : 0u;
+            const uint32_t wa = C.cap_a && !none_cached ? ldcg(L.bm_a + w) : 0u;
+            const uint32_t wd = C.cap_d && !none_cached ? ldcg(L.bm_d + w) : 0u;
+            const uint32_t we = C.cap_e && !none_cached ? ldcg(L.bm_e + w) : 0u;
             const uint32_t t = (wa & b) ? T_A : (wd & b) ? T_D : (we & b) ? T_E : T_S;
             const bool hit = (t == T_E || t == T_D || (t == T_A && (C.baseline || !(ldcg(cons_j + w) & b))));
             if (hit) {
