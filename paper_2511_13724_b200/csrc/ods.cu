@@ -55,6 +55,9 @@ constexpr uint32_t kMaxJobs = 32;
 constexpr uint32_t kMaxReplicas = 64;        // independent replay instances per context
 constexpr uint32_t kMaxShards = 8;           // sample-ID-range shards of one replay
 constexpr uint32_t kMaxBatch = 4096;
+#ifndef SENECA_LATE_WALK
+#define SENECA_LATE_WALK 1          // storage-list walk once all of a job's pools are empty (Cfg.late)
+#endif
 #ifndef SENECA_EMPTY_POOLS_FAST
 #define SENECA_EMPTY_POOLS_FAST 1    // skip the classification gathers when every pool of the job is empty
 #endif
@@ -67,6 +70,7 @@ constexpr uint32_t kSuperShift = 12;         // 32 blocks = 4096 ids per superbl
 constexpr uint32_t kWordsPerBlock = 4;
 constexpr uint32_t kWalkPerThread = 8;       // list entries examined per thread per walk step
 constexpr uint32_t kWinMax = 1024;           // prefetched walk window (list entries)
+constexpr uint32_t kGenChunk = 16384;        // positions per permutation-generation chunk
 // the prefetched walk step covers 2 window entries per thread: window = min(kWinMax, 2 T)
 
 // ------------------------------------------------------------------ layouts
@@ -77,7 +81,10 @@ struct JobDev {           // per-job persistent walk state (workspace)
     uint32_t cur_len;
     uint32_t nxt_len;
     uint32_t recount;     // pools must be rebuilt before the next classify (epoch start)
-    uint32_t pad[2];
+    uint32_t late;        // storage-list walk of this epoch (see Cfg.late)
+    uint32_t lc, lk;      // late walk position in lap 1: storage-list segment lc, entry lk
+    uint32_t fl, fc, fk, fpos;   // seen-marking frontier of the late rounds (see catch_up_seen)
+    uint32_t pad[3];
 };
 
 struct Cfg {
@@ -90,6 +97,12 @@ struct Cfg {
     uint32_t cold;                   // cold start (R-O24): empty tiers, round-end admission until full
     uint32_t Nrow;                   // row stride of the permutation / lap lists (N rounded up to 64)
     uint32_t FL;                     // capacity of one refill buffer
+    uint32_t late;                   // storage lists: static tiers (no tracked tier, no cold start, ODS sampler,
+                                     // generated requests, one unsharded replica) -- once all of a job's pools
+                                     // are empty its walk takes the epoch's storage ids in permutation order
+                                     // (every unseen id ahead of the cursor is then storage-resident, every
+                                     // cached one seen), no seen test (§7.1 "late rounds")
+    uint32_t nch;                    // generation chunks (16 K positions) per permutation
     uint32_t G;                      // sample-ID-range shards (1: unsharded), SURVEY §8(e)
     uint32_t xsys;                   // exchange scope: 1 system (peers on other devices), 0 this device
     uint32_t mb_c1, mb_c2, mb_rf, mb_fl;   // mailbox offsets (u32) of the shard exchange, see Lay.mbox
@@ -114,6 +127,10 @@ struct Lay {
                                      //     the concurrent ring generator refills slot e % K once it is >= e - K + 1
     uint32_t *gen_next;              // [1] work counter of the ring generator CTAs
     uint32_t *ring_pairs;            // [kRingPairs] (job << 24 | epoch) the generator CTAs fill, in order
+    uint32_t *slist;                 // Cfg.late: [J][K][Nrow] per ring slot, per 16 K-position chunk of the
+                                     //   permutation its storage-resident ids in position order (a segment)
+    uint32_t *scnt;                  //   [J][K][nch] entries of each segment
+    uint32_t *cbits;                 //   [J][K][Nrow/32] bit p: position p holds a storage-resident id
     JobDev *jobs;                    // [J]
     uint32_t *out_ids;               // [J][Bmax] replay scratch
     uint8_t *out_src;                // [J][Bmax]
@@ -451,6 +468,9 @@ struct JobSmem {
     uint32_t hits_loc[3], own[3], glob[3];   // sharded: hits / substitutes in this shard's range, global pool sizes
     uint32_t cnt[kMaxShards][3];             // sharded: every shard's pool sizes of this round (C1)
     uint32_t recount;
+    uint32_t late, lc, lk; // storage-list walk (Cfg.late): on, lap-1 segment and entry
+    uint32_t lcnt;         // entries of segment lc (cached while the walk stays in it)
+    uint32_t fl, fc, fk, fpos; // late rounds' seen-marking frontier: fl 0 lap-1 (segment fc, entry fk), 1 lap list fpos
     uint32_t perm_seen;   // epoch+1 whose permutation was observed published (0: none)
     float dens;           // unseen fraction observed by the last walk step (window sizing)
     uint32_t npush;       // evictions pushed by this job this round
@@ -672,9 +692,134 @@ __device__ void job_walk(const Lay& L, const Cfg& C, JobSmem& S, uint32_t* s_req
     }
 }
 
+// Cfg.late: once every pool of job j is empty (static tiers), every unseen id
+// ahead of the lap-1 cursor is storage-resident and every cached id is seen, and
+// every entry of the lap lists (the deferred, replaced misses: storage ids) is
+// unseen.  The walk then takes the next `need` ids of the epoch's storage-list
+// segments in order, then of the lap lists -- the same ids the seen-testing
+// walk would take, with no seen test.
+__device__ void late_walk(const Lay& L, const Cfg& C, JobSmem& S, uint32_t* s_req, uint32_t j, uint32_t e,
+                          uint32_t need) {
+    const uint32_t tid = threadIdx.x, T = blockDim.x;
+    const size_t slot = (size_t)j * C.K + (e & (C.K - 1));
+    if (tid == 0) { S.wrap_slot = 0; S.need = need; }
+    uint32_t s = 0;
+    while (s < need) {
+        __syncthreads();                             // state of the previous step visible
+        uint32_t take;
+        if (S.cur_buf == 0) {
+            if (S.lc >= C.nch) {                     // lap 1 done: the deferred misses are next
+                __syncthreads();
+                if (tid == 0) {
+                    S.wrap_slot = s;
+                    S.cur_buf = S.nxt_buf; S.cur_len = S.nxt_len; S.cursor = 0;
+                    S.nxt_buf = S.cur_buf == 1 ? 2 : 1; S.nxt_len = 0;
+                }
+                continue;
+            }
+            const uint32_t cnt = S.lcnt;
+            take = min(cnt - S.lk, need - s);
+            const uint32_t* src = L.slist + slot * C.Nrow + (size_t)S.lc * kGenChunk + S.lk;
+            for (uint32_t t = tid; t < take; t += T) s_req[s + t] = ldcg(src + t);
+            __syncthreads();
+            if (tid == 0) {
+                S.lk += take;
+                if (S.lk == cnt) {
+                    S.lc += 1; S.lk = 0;
+                    S.lcnt = S.lc < C.nch ? ldcg(L.scnt + slot * C.nch + S.lc) : 0u;
+                }
+            }
+        } else {
+            take = min(S.cur_len - S.cursor, need - s);
+            if (take == 0) {                         // cannot happen while n_j < N
+                if (tid == 0) atomicOr(L.err, 2u);
+                break;
+            }
+            const uint32_t* src = L.laps + ((size_t)j * 2 + (S.cur_buf - 1)) * C.Nrow + S.cursor;
+            for (uint32_t t = tid; t < take; t += T) s_req[s + t] = ldcg(src + t);
+            __syncthreads();
+            if (tid == 0) S.cursor += take;
+        }
+        s += take;
+    }
+    __syncthreads();
+}
+
+// Switch job j to the storage-list walk (all its pools are empty; every thread
+// calls it): the lap-1 cursor becomes (segment, entry) by counting the
+// storage-resident positions of its chunk before it.
+__device__ __noinline__ void enter_late(const Lay& L, const Cfg& C, JobSmem& S, uint32_t j, uint32_t e) {
+    const uint32_t tid = threadIdx.x;
+    cp_async_wait_all();                              // the seen-testing walk's prefetch is dropped
+    __syncthreads();
+    if (S.cur_buf == 0) {
+        const size_t slot = (size_t)j * C.K + (e & (C.K - 1));
+        const uint32_t* cb = L.cbits + slot * (C.Nrow / 32);
+        const uint32_t cur = S.cursor, lc = cur / kGenChunk;
+        const uint32_t w0 = lc * (kGenChunk / 32), w1 = cur >> 5;
+        uint32_t c = 0;
+        for (uint32_t w = w0 + tid; w <= w1; w += blockDim.x) {
+            if (w < w1) c += __popc(ldcg(cb + w));
+            else if (cur & 31) c += __popc(ldcg(cb + w) & ((1u << (cur & 31)) - 1u));
+        }
+        uint32_t tot;
+        block_exclusive_scan(c, &tot, S.scan);
+        if (tid == 0) {
+            S.lc = lc; S.lk = tot; S.fl = 0; S.fc = lc; S.fk = tot;
+            S.lcnt = lc < C.nch ? ldcg(L.scnt + slot * C.nch + lc) : 0u;
+        }
+    } else if (tid == 0) {
+        S.fl = 1; S.fpos = S.cursor;
+    }
+    if (tid == 0) { S.late = 1; S.pf_state = 0; }
+    __syncthreads();
+}
+
+// Late rounds do not mark their deliveries in seen_j: nothing reads job j's seen
+// bits while its pools are empty (no seen test in the walk, no pool selection,
+// static tiers: no refills) and the epoch end clears them.  A launch that ends
+// mid-epoch in late mode marks the ids delivered since the frontier -- the
+// storage-list entries walked in lap 1, then the lap-list entries -- so the
+// state is exact between launches (every thread calls it).
+__device__ __noinline__ void catch_up_seen(const Lay& L, const Cfg& C, JobSmem& S, uint32_t j, uint32_t e) {
+    const uint32_t tid = threadIdx.x, T = blockDim.x;
+    uint32_t* seen_j = L.seen + (size_t)j * C.NW;
+    __syncthreads();
+    if (S.fl == 0) {
+        const size_t slot = (size_t)j * C.K + (e & (C.K - 1));
+        const bool in1 = S.cur_buf == 0;
+        const uint32_t ec = in1 ? S.lc : C.nch, ek = in1 ? S.lk : 0u;
+        for (uint32_t c = S.fc; c <= ec && c < C.nch; ++c) {
+            const uint32_t k0 = c == S.fc ? S.fk : 0u;
+            const uint32_t k1 = c == ec ? ek : ldcg(L.scnt + slot * C.nch + c);
+            const uint32_t* seg = L.slist + slot * C.Nrow + (size_t)c * kGenChunk;
+            for (uint32_t k = k0 + tid; k < k1; k += T) {
+                const uint32_t i = ldcg(seg + k);
+                atomicOr(seen_j + (i >> 5), 1u << (i & 31));
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {
+            if (in1) { S.fc = S.lc; S.fk = S.lk; }
+            else { S.fl = 1; S.fpos = 0; }
+        }
+        __syncthreads();
+    }
+    if (S.fl == 1 && S.cur_buf != 0) {
+        const uint32_t* list = L.laps + ((size_t)j * 2 + (S.cur_buf - 1)) * C.Nrow;
+        for (uint32_t k = S.fpos + tid; k < S.cursor; k += T) {
+            const uint32_t i = ldcg(list + k);
+            atomicOr(seen_j + (i >> 5), 1u << (i & 31));
+        }
+        __syncthreads();
+        if (tid == 0) S.fpos = S.cursor;
+    }
+    __syncthreads();
+}
+
 // Rebuild the three pool counts of job j (epoch start): block bytes in global
 // memory, superblock counts in this CTA's shared memory, totals in tot3.
-__device__ void job_recount(const Lay& L, const Cfg& C, uint32_t j, uint32_t* s_sup /* [3][NS] */, uint32_t* tot3) {
+__device__ __noinline__ void job_recount(const Lay& L, const Cfg& C, uint32_t j, uint32_t* s_sup /* [3][NS] */, uint32_t* tot3) {
     const uint32_t tid = threadIdx.x, T = blockDim.x;
     for (uint32_t k = tid; k < 3 * C.NS; k += T) s_sup[k] = 0;
     __syncthreads();
@@ -870,12 +1015,13 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
     // remaining misses are fetched from storage (R-O18); during a cold start they
     // are also listed, in slot order, for the round-end admission (R-O24)
     const bool record = C.cold && !S.warm;
+    const bool late = S.late != 0;
     for (uint32_t u = q + tid; u < S.m; u += T) {
         const uint32_t s = s_miss[u], i = s_req[s];
         if (P.out_ids) { P.out_ids[row + s] = i; P.out_src[row + s] = (uint8_t)T_S; }
         s_oid[s] = i;
         s_osrc[s] = (uint8_t)T_S;
-        atomicOr(seen_j + (i >> 5), 1u << (i & 31));
+        if (!late) atomicOr(seen_j + (i >> 5), 1u << (i & 31));     // late rounds: catch_up_seen
         if (record) L.fetch[(size_t)j * C.Bmax + (u - q)] = i;
     }
     if (record && tid == 0) L.fetch_n[j] = S.m - q;
@@ -1272,6 +1418,10 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
         const JobDev jd = L.jobs[j];
         S.cur_buf = jd.cur_buf; S.nxt_buf = jd.nxt_buf; S.cursor = jd.cursor;
         S.cur_len = jd.cur_len; S.nxt_len = jd.nxt_len; S.recount = jd.recount;
+        S.late = jd.late; S.lc = jd.lc; S.lk = jd.lk;
+        if (S.late && S.cur_buf == 0 && S.lc < C.nch)
+            S.lcnt = ldcg(L.scnt + ((size_t)j * C.K + (P.e0[j] & (C.K - 1))) * C.nch + S.lc);
+        S.fl = jd.fl; S.fc = jd.fc; S.fk = jd.fk; S.fpos = jd.fpos;
         // a job that has not arrived took no maintain results: its pools are rebuilt
         // from the bitmaps when it arrives (R-O23)
         if ((P.pending0 >> j) & 1u) S.recount = 1;
@@ -1437,6 +1587,8 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
                     s_req[s] = P.requested[(size_t)P.row_of_job[j] * P.out_stride + s];
                 if (tid == 0) { S.need = need; S.wrap_slot = 0; }
                 __syncthreads();
+            } else if (S.late) {
+                late_walk(L, C, S, s_req, j, s_e[j], need);
             } else {
                 job_walk(L, C, S, s_req, j, s_e[j], need, TM, s_win, nullptr);
                 if (P.rounds > 1)
@@ -1468,6 +1620,7 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
                     if (tid == 0) {
                         S.cur_buf = 0; S.nxt_buf = 1; S.cursor = 0; S.cur_len = C.N; S.nxt_len = 0;
                         S.recount = 1;
+                        S.late = 0;
                     }
                     // epoch e is over: no read of its ring slot is in flight any more (the
                     // prefetched window copies of this CTA are drained), so the slot may be
@@ -1486,11 +1639,19 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
             }
             advance(part, departing, r);
             if (rr + 1 < P.rounds && ((s_active & P.subset) >> j & 1u)) {
-                job_walk(L, C, S, s_req, j, s_e[j], need_of(j), TM, s_win, pf);   // next request
-                TM.tick(13);
-                if (rr + 2 < P.rounds)
-                    prefetch_window(L, C, S, s_win, j, s_e[j], (uint32_t)(C.batch[j] / fmaxf(S.dens, 1.0f / 64.0f) * 1.15f) + 64);
-                TM.tick(14);
+                // (C.late: all pools of the job empty, not at an epoch start -> storage-list walk)
+                if (C.late && !S.late && !S.recount && (S.tot[0] | S.tot[1] | S.tot[2]) == 0u)
+                    enter_late(L, C, S, j, s_e[j]);
+                if (S.late) {
+                    late_walk(L, C, S, s_req, j, s_e[j], need_of(j));
+                    TM.tick(13);
+                } else {
+                    job_walk(L, C, S, s_req, j, s_e[j], need_of(j), TM, s_win, pf);   // next request
+                    TM.tick(13);
+                    if (rr + 2 < P.rounds)
+                        prefetch_window(L, C, S, s_win, j, s_e[j], (uint32_t)(C.batch[j] / fmaxf(S.dens, 1.0f / 64.0f) * 1.15f) + 64);
+                    TM.tick(14);
+                }
             }
             TM.tick(5);
         }
@@ -1499,6 +1660,7 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
     // job's A pool; persist the totals
     if (!is_maint) {
         flush_stats(L, C, S, j, s_e[j]);
+        if (S.late) catch_up_seen(L, C, S, j, s_e[j]);
         if (coupled && P.rounds > 0 && (s_active >> j & 1u)) {
             if (tid == 0) { while (ld_acquire(L.bar + 2) < P.rounds) { } }
             __syncthreads();
@@ -1517,6 +1679,8 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
         JobDev& jd = L.jobs[j];
         jd.cur_buf = S.cur_buf; jd.nxt_buf = S.nxt_buf; jd.cursor = S.cursor;
         jd.cur_len = S.cur_len; jd.nxt_len = S.nxt_len; jd.recount = S.recount;
+        jd.late = S.late; jd.lc = S.lc; jd.lk = S.lk;
+        jd.fl = S.fl; jd.fc = S.fc; jd.fk = S.fk; jd.fpos = S.fpos;
     }
     if (kTime && P.timing && tid == 0 && (is_maint || cta == 0)) {
         const uint32_t base = is_maint ? 16 : 0;
@@ -1594,23 +1758,62 @@ struct PermRing {
     uint32_t j[kRingPairs], e[kRingPairs];
 };
 
+// One 16 K-position chunk [lo, hi) of pi_j,e into ring slot e % K; with
+// Cfg.late also the chunk's storage-list segment (its storage-resident ids in
+// position order, by a block scan per 512 positions), their count, and a bit per
+// position (storage-resident) for locating a cursor in the segments.  Every
+// thread of the CTA calls it (blockDim a multiple of 32, lo a multiple of 16 K).
+__device__ void gen_chunk(const Lay& L, const Cfg& C, uint32_t j, uint32_t e, uint32_t part, uint64_t key,
+                          const PermDomain& dom, uint32_t* s_scan /* 33 u32 */) {
+    const uint32_t lo = part * kGenChunk, hi = min(lo + kGenChunk, C.N);
+    const size_t slot = (size_t)j * C.K + (e & (C.K - 1));
+    uint32_t* out = L.perms + slot * C.Nrow;
+    if (!C.late) {
+        for (uint32_t pos = lo + threadIdx.x; pos < hi; pos += blockDim.x) out[pos] = perm_apply(key, dom, pos);
+        return;
+    }
+    uint32_t* seg = L.slist + slot * C.Nrow + lo;
+    uint32_t* cb = L.cbits + slot * (C.Nrow / 32);
+    uint32_t run = 0;
+    for (uint32_t base = lo; base < hi; base += blockDim.x) {
+        const uint32_t pos = base + threadIdx.x;
+        bool st = false;
+        uint32_t id = 0;
+        if (pos < hi) {
+            id = perm_apply(key, dom, pos);
+            out[pos] = id;
+            const uint32_t w = id >> 5;
+            const uint32_t cached = (C.cap_e ? ldcg(L.bm_e + w) : 0u) | (C.cap_d ? ldcg(L.bm_d + w) : 0u);
+            st = !((cached >> (id & 31)) & 1u);
+        }
+        const uint32_t ball = __ballot_sync(0xffffffffu, st);
+        const uint32_t wbase = base + (threadIdx.x & ~31u);
+        if ((threadIdx.x & 31) == 0 && wbase < hi) cb[wbase >> 5] = ball;
+        uint32_t tot;
+        const uint32_t ex = block_flag_scan(st, false, &tot, s_scan);
+        if (st) seg[run + ex] = id;
+        run += tot;
+    }
+    if (threadIdx.x == 0) L.scnt[slot * C.nch + part] = run;
+}
+
 // pi_j,e for the listed (job, epoch) pairs, in chunks, into ring slot e % K; the
 // CTA finishing the last chunk of (j, e) publishes perm_ready[j][e] (release).
 __global__ void ods_perm_all(const __grid_constant__ Lays LS, const __grid_constant__ Cfg C,
                              const __grid_constant__ PermWork W, uint32_t chunk) {
     const Lay& L = LS.r[blockIdx.y];
-    const uint32_t per = (C.N + chunk - 1) / chunk;
+    (void)chunk;
+    const uint32_t per = C.nch;
     const uint64_t total = (uint64_t)W.n * per;
     const PermDomain dom = perm_domain(C.N);
-    __shared__ uint32_t s_last;
+    __shared__ uint32_t s_last, s_scan[33];
     for (uint64_t c = blockIdx.x; c < total; c += gridDim.x) {
         const uint32_t pair = (uint32_t)(c / per);
         const uint32_t e = W.e[pair], j = W.j[pair];
         const uint32_t part = (uint32_t)(c % per);
         const uint64_t key = derive_key(L.seed, PUR_REQ, j, e, 0);
-        uint32_t* out = L.perms + ((size_t)j * C.K + (e & (C.K - 1))) * C.Nrow;
-        const uint32_t lo = part * chunk, hi = min(lo + chunk, C.N);
-        for (uint32_t pos = lo + threadIdx.x; pos < hi; pos += blockDim.x) out[pos] = perm_apply(key, dom, pos);
+        const uint32_t lo = part * kGenChunk, hi = min(lo + kGenChunk, C.N);
+        gen_chunk(L, C, j, e, part, key, dom, s_scan);
         __syncthreads();
         if (threadIdx.x == 0) {
             __threadfence();
@@ -1634,11 +1837,10 @@ __global__ void ods_perm_all(const __grid_constant__ Lays LS, const __grid_const
 // Work items (pair, 16 K-position chunk) are taken in list order (pairs sorted
 // by the round their slot frees); a waiting CTA sleeps.
 __device__ __noinline__ void ring_generate(const Lay& L, const Cfg& C, uint32_t n_pairs) {
-    constexpr uint32_t chunk = 16384;
-    const uint32_t per = (C.N + chunk - 1) / chunk;
+    const uint32_t per = C.nch;
     const uint32_t total = n_pairs * per;
     const PermDomain dom = perm_domain(C.N);
-    __shared__ uint32_t s_item, s_last;
+    __shared__ uint32_t s_item, s_last, s_scan[33];
     for (;;) {
         if (threadIdx.x == 0) s_item = atomicAdd(L.gen_next, 1u);
         __syncthreads();
@@ -1651,9 +1853,8 @@ __device__ __noinline__ void ring_generate(const Lay& L, const Cfg& C, uint32_t 
             while (ld_acquire(L.epoch_at + j) + C.K - 1 < e) __nanosleep(1000);
         __syncthreads();
         const uint64_t key = derive_key(L.seed, PUR_REQ, j, e, 0);
-        uint32_t* out = L.perms + ((size_t)j * C.K + (e & (C.K - 1))) * C.Nrow;
-        const uint32_t lo = part * chunk, hi = min(lo + chunk, C.N);
-        for (uint32_t pos = lo + threadIdx.x; pos < hi; pos += blockDim.x) out[pos] = perm_apply(key, dom, pos);
+        const uint32_t lo = part * kGenChunk, hi = min(lo + kGenChunk, C.N);
+        gen_chunk(L, C, j, e, part, key, dom, s_scan);
         __syncthreads();
         if (threadIdx.x == 0) {
             __threadfence();
@@ -1743,6 +1944,8 @@ __global__ void ods_init_jobs(const __grid_constant__ Lays LS, const __grid_cons
     if (j < C.J) {
         JobDev& jd = L.jobs[j];
         jd.cur_buf = 0; jd.nxt_buf = 1; jd.cursor = 0; jd.cur_len = C.N; jd.nxt_len = 0; jd.recount = 0;
+        jd.late = 0; jd.lc = 0; jd.lk = 0;
+        jd.fl = 0; jd.fc = 0; jd.fk = 0; jd.fpos = 0;
     }
 }
 
@@ -1868,7 +2071,7 @@ seneca_status check_cfg(const seneca_cache_config* cfg) {
 
 struct Sizes {
     Cfg C;
-    size_t off[40];
+    size_t off[48];
     size_t total;          // one replica
     uint32_t R;
 };
@@ -1901,6 +2104,9 @@ Sizes compute_sizes(const seneca_cache_config* cfg) {
     C.seed = cfg->seed;
     C.Nrow = (C.N + 63) & ~63u;
     C.FL = (uint32_t)(std::max<size_t>(C.cap_t, 1) + (size_t)C.J * C.Bmax);
+    C.nch = (C.N + kGenChunk - 1) / kGenChunk;
+    C.late = (SENECA_LATE_WALK && cfg->cap_a == 0 && !cfg->evict_tiers && !cfg->cold_start && !cfg->sampler &&
+              cfg->request_mode == 0 && cfg->replicas <= 1 && cfg->shards <= 1) ? 1u : 0u;
     C.G = cfg->shards > 1 ? cfg->shards : 1u;
     C.xsys = C.G > 1 && cfg->shard_mode == 1 ? 1u : 0u;
     C.mb_c1 = 0;
@@ -1932,6 +2138,9 @@ Sizes compute_sizes(const seneca_cache_config* cfg) {
         (size_t)C.J * 4, 4,                                 // 33-34 epoch_at, gen_next
         mbox_u32 * 4,                                       // 35 shard mailbox
         (size_t)kRingPairs * 4,                             // 36 ring generator work list
+        C.late ? (size_t)C.J * C.K * C.Nrow * 4 : 4,        // 37 storage-list segments
+        C.late ? (size_t)C.J * C.K * C.nch * 4 : 4,         // 38 segment counts
+        C.late ? (size_t)C.J * C.K * (C.Nrow / 32) * 4 : 4, // 39 storage bit per position
     };
     size_t at = 0;
     for (size_t k = 0; k < sizeof(sz) / sizeof(sz[0]); ++k) {
@@ -1986,6 +2195,9 @@ Lay carve(const Sizes& z, char* base, char* ctl, uint64_t seed) {
     L.gen_next = (uint32_t*)(base + z.off[34]);
     L.mbox = (uint32_t*)(base + z.off[35]);
     L.ring_pairs = (uint32_t*)(base + z.off[36]);
+    L.slist = (uint32_t*)(base + z.off[37]);
+    L.scnt = (uint32_t*)(base + z.off[38]);
+    L.cbits = (uint32_t*)(base + z.off[39]);
     for (uint32_t g = 0; g < kMaxShards; ++g) L.peer[g] = nullptr;
     L.shard = 0; L.sb_lo = 0; L.sb_hi = z.C.NS; L.id_lo = 0; L.id_hi = z.C.NS * 4096u;
     return L;

@@ -781,3 +781,39 @@ def test_sharded_across_processes_cuda_ipc():
                          capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-3000:]
     assert "all ranks ok" in out.stdout
+
+
+# ---------------------------------------------------------------- storage-list walk (static tiers)
+@pytest.mark.parametrize("block", range(3))
+def test_storage_list_walk_random_static_configs(block):
+    """Static tiers (no A tier, ODS sampler, one replica): once all of a job's pools
+    are empty the kernel walks the epoch's storage-list segments and the lap
+    lists without seen tests (Cfg.late).  Random tiny and small
+    configs (N up to 70,000: several 16 K-position generation chunks, empty
+    segments when everything is cached), mixed batches and epochs, replays cut
+    into random-length launches (the late state persists across launches), vs
+    the oracle transcript."""
+    st = synth.Stream(9100 + block)
+    for it in range(12):
+        n = int(st.choice(1, [40, 1000, 16384, 16385, 40000, 70000])[0])
+        J = int(st.choice(1, [1, 2, 3, 4])[0])
+        batch = [int(x) for x in st.choice(J, [7, 64, 100, 512])]
+        target = [int(x) for x in st.choice(J, [1, 2, 3])]
+        frac_e, frac_d = float(st.uniform(1)[0]), float(st.uniform(1)[0])
+        ce = int(n * frac_e * 0.6)
+        cd = int((n - ce) * frac_d * 0.5) if it % 3 else 0
+        if it % 5 == 4:
+            ce, cd = n, 0                                 # everything cached: empty storage segments
+        seed = int(st.u64(1)[0])
+        o, g = make_pair(n, batch, target, ce, cd, 0, seed)
+        tr = g.new_transcript()
+        total = 0
+        while g.view().active_mask:
+            k = int(st.u64(1)[0] % np.uint64(400)) + 1
+            done = g.replay_rounds(k, tr)
+            total += done
+            if done < k:
+                break
+        torch.cuda.synchronize()
+        assert total == o.replay_epochs(max(target)), (n, batch, target, ce, cd)
+        compare_state(o, g, tr)
