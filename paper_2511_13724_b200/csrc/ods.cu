@@ -699,11 +699,35 @@ __device__ void job_walk(const Lay& L, const Cfg& C, JobSmem& S, uint32_t* s_req
 // segments in order, then of the lap lists -- the same ids the seen-testing
 // walk would take, with no seen test.
 __device__ void late_walk(const Lay& L, const Cfg& C, JobSmem& S, uint32_t* s_req, uint32_t j, uint32_t e,
-                          uint32_t need) {
+                          uint32_t need, const uint32_t* s_win) {
     const uint32_t tid = threadIdx.x, T = blockDim.x;
     const size_t slot = (size_t)j * C.K + (e & (C.K - 1));
     if (tid == 0) { S.wrap_slot = 0; S.need = need; }
     uint32_t s = 0;
+    if (S.pf_state == 3) {                           // the first entries, prefetched one round ahead
+        const bool usable = S.pf_buf == S.cur_buf &&
+                            (S.cur_buf == 0 ? (S.pf_epoch == S.lc && S.pf_base == S.lk) : S.pf_base == S.cursor);
+        const uint32_t n = min(S.pf_len, need), off = S.pf_vlen;
+        cp_async_wait_all();
+        __syncthreads();
+        if (usable) {
+            for (uint32_t t = tid; t < n; t += T) s_req[t] = s_win[off + t];
+            s = n;
+            __syncthreads();
+            if (tid == 0) {
+                if (S.cur_buf == 0) {
+                    S.lk += n;
+                    if (S.lk == S.lcnt) {
+                        S.lc += 1; S.lk = 0;
+                        S.lcnt = S.lc < C.nch ? ldcg(L.scnt + slot * C.nch + S.lc) : 0u;
+                    }
+                } else {
+                    S.cursor += n;
+                }
+            }
+        }
+        if (tid == 0) S.pf_state = 0;
+    }
     while (s < need) {
         __syncthreads();                             // state of the previous step visible
         uint32_t take;
@@ -743,6 +767,36 @@ __device__ void late_walk(const Lay& L, const Cfg& C, JobSmem& S, uint32_t* s_re
         s += take;
     }
     __syncthreads();
+}
+
+// The next late walk's first `want` entries -- as far as the current segment or
+// lap list reaches -- copied into s_win with 16-B cp.async (the 16-B-aligned
+// superset; the walk reads from offset pos mod 4): the storage lists stream
+// from DRAM, so the copy is issued a round ahead (every thread calls it).
+__device__ void late_prefetch(const Lay& L, const Cfg& C, JobSmem& S, uint32_t* s_win, uint32_t j, uint32_t e,
+                              uint32_t want) {
+    const uint32_t tid = threadIdx.x;
+    const uint32_t* src;
+    uint32_t pos, avail;
+    if (S.cur_buf == 0) {
+        if (S.lc >= C.nch) return;
+        src = L.slist + ((size_t)j * C.K + (e & (C.K - 1))) * C.Nrow + (size_t)S.lc * kGenChunk;
+        pos = S.lk;
+        avail = S.lcnt - S.lk;
+    } else {
+        src = L.laps + ((size_t)j * 2 + (S.cur_buf - 1)) * C.Nrow;
+        pos = S.cursor;
+        avail = S.cur_len - S.cursor;
+    }
+    const uint32_t n = min(avail, min(want, kWinMax - 4));
+    if (n == 0) return;
+    const uint32_t al = pos & ~3u, end = (pos + n + 3) & ~3u;
+    for (uint32_t t = tid; al + 4 * t < end; t += blockDim.x) cp_async16(s_win + 4 * t, src + al + 4 * t);
+    cp_async_commit();
+    __syncthreads();
+    if (tid == 0) {
+        S.pf_state = 3; S.pf_buf = S.cur_buf; S.pf_epoch = S.lc; S.pf_base = pos; S.pf_len = n; S.pf_vlen = pos - al;
+    }
 }
 
 // Switch job j to the storage-list walk (all its pools are empty; every thread
@@ -1588,7 +1642,7 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
                 if (tid == 0) { S.need = need; S.wrap_slot = 0; }
                 __syncthreads();
             } else if (S.late) {
-                late_walk(L, C, S, s_req, j, s_e[j], need);
+                late_walk(L, C, S, s_req, j, s_e[j], need, s_win);
             } else {
                 job_walk(L, C, S, s_req, j, s_e[j], need, TM, s_win, nullptr);
                 if (P.rounds > 1)
@@ -1643,8 +1697,13 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
                 if (C.late && !S.late && !S.recount && (S.tot[0] | S.tot[1] | S.tot[2]) == 0u)
                     enter_late(L, C, S, j, s_e[j]);
                 if (S.late) {
-                    late_walk(L, C, S, s_req, j, s_e[j], need_of(j));
+                    late_walk(L, C, S, s_req, j, s_e[j], need_of(j), s_win);
                     TM.tick(13);
+                    if (rr + 2 < P.rounds) {              // the round after: prefetch its requests
+                        const uint32_t n2 = s_n[j] + need_of(j);
+                        if (n2 < C.N) late_prefetch(L, C, S, s_win, j, s_e[j], min(C.batch[j], C.N - n2));
+                    }
+                    TM.tick(14);
                 } else {
                     job_walk(L, C, S, s_req, j, s_e[j], need_of(j), TM, s_win, pf);   // next request
                     TM.tick(13);
