@@ -391,7 +391,13 @@ def latency_floor(c, caps, st, rounds, evicted, refilled, sm_mhz):
     chain (perm_apply) in rounds that substitute -- each summed per job-round
     from the replay's own counters, averaged over job-rounds, and compared with
     the measured microseconds per round of the whole replay (rounds run in
-    lock-step across jobs)."""
+    lock-step across jobs).
+
+    Static tiers (no A tier): a job-round whose pools are empty needs no seen
+    test, no residency gather and no seen mark (its requests are the next
+    storage ids in permutation order, DESIGN.md 7.1 "late rounds"), so only the
+    rounds with non-empty pools -- estimated as the substituting ones -- carry
+    per-request scattered accesses; the late rounds are counted at zero."""
     ce, cd, ca = caps
     J = len(c["batch"])
     N = c["n_total"]
@@ -406,27 +412,32 @@ def latency_floor(c, caps, st, rounds, evicted, refilled, sm_mhz):
     # per job-round -- a lower bound, since a substituting round replaces at most
     # its misses (so the floor below stays a floor)
     sub_rounds = min(job_rounds, subs / max(1.0, (req - hits) / job_rounds))
-    # walk: positions examined = first-lap positions + deferred re-requests (R-O1)
-    positions = req + subs
+    static = ca == 0
+    # requests that needed the seen test / residency gather: all of them with an
+    # A tier; with static tiers those of the rounds whose pools were non-empty
+    req_tested = req if not static else min(req, sub_rounds * req / job_rounds)
+    # walk: positions examined = tested requests + deferred re-requests (R-O1)
+    positions = req_tested + (0.0 if static else subs)
     scattered = (positions / 4 + positions          # list vectors + per-position seen chunk copies
-                 + req * max(1, tiers)              # residency word gathers (classify)
-                 + req                              # seen RMW (respond)
+                 + req_tested * max(1, tiers)       # residency word gathers (classify)
+                 + req_tested                       # seen RMW (respond)
                  + hits + subs                      # pool block-count RMW
                  + 2 * subs                         # 32-B count row (two 16-B loads)
                  + 2 * sub[1] + 2 * sub[2] + 3 * sub[3]   # bitmap vectors of the selected block
                  + subs                             # deferral-list store
                  + 2 * a_served                     # consumer-set RMW + consumer-count RMW
                  + J * 2 * refilled)                # refill intake: seen gather + count RMW per job
-    dep = job_rounds * 3 + 2 * sub_rounds           # walk prefetch wait, classify, respond RMW; + select
+    tested_rounds = job_rounds if not static else sub_rounds
+    dep = tested_rounds * 3 + 2 * sub_rounds        # walk prefetch wait, classify, respond RMW; + select
     if ca > 0:
         dep += job_rounds * 3                       # maintain: signal, eviction/refill apply, release
     cyc = dep * L2_DEP_CYCLES + scattered + sub_rounds * PERM_CYCLES
     floor_us = cyc / job_rounds / sm_mhz
     return dict(floor_us_per_round=floor_us, cycles_per_job_round=cyc / job_rounds,
                 dependent_trips_per_job_round=dep / job_rounds, scattered_per_job_round=scattered / job_rounds,
-                substituting_job_round_share=sub_rounds / job_rounds,
+                substituting_job_round_share=sub_rounds / job_rounds, static_tiers=static,
                 inputs=dict(l2_dependent_cycles=L2_DEP_CYCLES, perm_apply_cycles=PERM_CYCLES,
-                            scattered_per_cycle=1, sm_mhz=sm_mhz, source="profiles/r1/microbench.md"))
+                            scattered_per_cycle=1, sm_mhz=sm_mhz, source="profiles/r2/microbench.md"))
 
 
 def golden_gate(name, seed, evict_tiers, st_raw, evicted=None, refilled=None):

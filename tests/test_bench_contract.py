@@ -107,9 +107,10 @@ def test_latency_floor_model():
     """bench.latency_floor (DESIGN.md 7.1 "latency roofline"): per job-round
     floor = dependent L2 trips x 300 cycles + scattered accesses x 1 cycle +
     substituting share x the perm_apply chain (1,790 cycles), from the replay's
-    own counters.  Pinned on a hand-computed case: one job, 1,000 samples,
-    batch 100 (10 job-rounds), E tier only, 400 requested hits and 300
-    substitutes over the epoch, no A."""
+    own counters.  Pinned on hand-computed cases: one job, 1,000 samples, batch
+    100 (10 job-rounds), 400 requested hits and 300 substitutes over the epoch;
+    static tiers (E only: only the rounds with non-empty pools test their
+    requests) and with an A tier (every request tested, maintain trips)."""
     import numpy as np
     sys.path.insert(0, ROOT)
     import bench
@@ -118,13 +119,23 @@ def test_latency_floor_model():
     st["served"][0, 0] = [300, 700, 0, 0]            # storage 300, E 700 (= 400 hits + 300 substitutes)
     st["subst"][0, 0] = [0, 300, 0, 0]
     st["req_hits"][0, 0] = [0, 400, 0, 0]
-    lf = bench.latency_floor(c, (500, 0, 0), st, 10, 0, 0, 2000.0)
     jr, req, hits, subs = 10, 1000.0, 400.0, 300.0
     sub_rounds = min(jr, subs / ((req - hits) / jr))                    # 5
-    positions = req + subs
-    scattered = positions / 4 + positions + req * 1 + req + hits + subs + 2 * subs + 2 * subs + subs
-    dep = jr * 3 + 2 * sub_rounds
+    # static: 5 of 10 rounds test their 100 requests
+    lf = bench.latency_floor(c, (500, 0, 0), st, 10, 0, 0, 2000.0)
+    rt = sub_rounds * req / jr                                          # 500 tested requests
+    scattered = rt / 4 + rt + rt * 1 + rt + hits + subs + 2 * subs + 2 * subs + subs
+    dep = sub_rounds * 3 + 2 * sub_rounds
     cyc = dep * 300 + scattered + sub_rounds * 1790
+    assert lf["static_tiers"] is True
     assert abs(lf["cycles_per_job_round"] - cyc / jr) < 1e-9
     assert abs(lf["floor_us_per_round"] - cyc / jr / 2000.0) < 1e-12
     assert abs(lf["substituting_job_round_share"] - 0.5) < 1e-12
+    # with an A tier (the same counters, caps E 400 / A 100): every request tested
+    lf = bench.latency_floor(c, (400, 0, 100), st, 10, 0, 0, 2000.0)
+    positions = req + subs
+    scattered = positions / 4 + positions + req * 2 + req + hits + subs + 2 * subs + 2 * subs + subs
+    dep = jr * 3 + 2 * sub_rounds + jr * 3
+    cyc = dep * 300 + scattered + sub_rounds * 1790
+    assert lf["static_tiers"] is False
+    assert abs(lf["cycles_per_job_round"] - cyc / jr) < 1e-9

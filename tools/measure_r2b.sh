@@ -1,0 +1,29 @@
+#!/bin/bash
+# Round-2 final measurement pass (run under gpurun from the repo root).
+TAG=${1:-r2b}
+OUT=gpurun_out/$TAG
+mkdir -p $OUT
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks.mem --format=csv > $OUT/gpu.txt
+timeout 1500 python -m pytest tests -q -m gpu > $OUT/gpu_tests.log 2>&1; echo "tests rc=$?"; tail -1 $OUT/gpu_tests.log
+timeout 300 python __graft_entry__.py smoke > $OUT/smoke.log 2>&1; echo "smoke rc=$?"; tail -1 $OUT/smoke.log
+timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?"
+timeout 900 python bench.py > $OUT/bench_repeat.json 2>> $OUT/bench.err; echo "bench2 rc=$?"
+timeout 600 python bench.py --workload imagenet1k --evict-tiers 1 --replicas 0 --extra-workloads "" --shards "" --no-cpu-baseline > $OUT/bench_imagenet1k_evictall.json 2>> $OUT/bench.err; echo "evictall rc=$?"
+timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > $OUT/bench_reference.json 2>> $OUT/bench.err; echo "reference rc=$?"
+SENECA_DIST_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
+  --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 2 --warmup 3 --no-shard-replay \
+  --mdp-large 0 > $OUT/bench_gloo2.json 2> $OUT/bench_gloo2.err; echo "gloo2 rc=$?"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
+  python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-profile --replicas 0 --shards "" --mdp-large 0 \
+  > /dev/null 2>&1; echo "ncu launches rc=$?"
+for w in imagenet22k imagenet1k openimages; do
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:ods_rounds -c 1 -o $OUT/ncu_ods_rounds_$w \
+    python tools/profile_ods.py $w 1000000 --plain > /dev/null 2>&1; echo "ncu ods $w rc=$?"
+done
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:mdp_sweep -s 1 -c 1 -o $OUT/ncu_mdp_sweep \
+  python tools/profile_mdp.py 10000 > /dev/null 2>&1; echo "ncu mdp rc=$?"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:mdp_sweep -s 1 -c 1 -o $OUT/ncu_mdp_sweep_100k \
+  python tools/profile_mdp.py 100000 > /dev/null 2>&1; echo "ncu mdp100k rc=$?"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:ods_recount_all -c 1 -o $OUT/ncu_recount_imagenet22k \
+  python tools/profile_ods.py imagenet22k 1 > /dev/null 2>&1; echo "ncu recount rc=$?"
+cp gpurun_out/sanitizer_*.log $OUT/ 2>/dev/null
