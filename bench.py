@@ -813,7 +813,7 @@ def main():
     ph_names = {0: "job_epoch_start", 1: "job_classify", 8: "job_subst_prefix", 9: "job_subst_ranks_locate",
                 2: "job_subst_apply", 10: "job_storage_deferral", 11: "job_respond_loop", 3: "job_respond_stats",
                 4: "job_wait_maint", 5: "job_advance", 12: "job_walk_prefetched_step", 13: "job_walk_rest",
-                14: "job_prefetch_issue", 6: "job_unused",
+                14: "job_prefetch_issue", 6: "job_late_bulk",
                 16: "maint_spec_prefix", 17: "maint_spec_refill_ranks", 18: "maint_barrier1_wait",
                 19: "maint_evict_decide", 20: "maint_apply", 21: "maint_barrier2_wait"}
     phase_share = {}

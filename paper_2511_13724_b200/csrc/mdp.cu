@@ -703,6 +703,240 @@ mdp_sweep_pairs(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_prof
     }
 }
 
+// ------------------------------------------------------------------ the paired sweep, SoA rows
+// The same pairs and the same IEEE operations as mdp_sweep_pairs, laid out for
+// fewer instructions per pair (the sweep is issue-bound):
+//  * the group's rows are structure-of-arrays with 8-byte slots (k8 = 8 k):
+//    {capc, cape} | tA | tD | tDc | tE, so one byte offset per coordinate
+//    addresses every array with an immediate displacement, and a lane reading
+//    consecutive rows reads consecutive slots (no bank conflicts);
+//  * the pair table entry is {b8 | m8 << 16, e8, i0, i1}: the group's base is
+//    added to both packed offsets with one add, the enumeration indices need no
+//    extraction;
+//  * the tD / tDc choice of Eq. 6 is an address select into two arrays;
+//  * the grid pointer is a template parameter (no per-pair null test).
+#ifndef SENECA_MDP_V2
+#define SENECA_MDP_V2 0           // 1: mdp_sweep_soa; 0: mdp_sweep_pairs (A/B knob)
+#endif
+#ifndef SENECA_MDP_I2F
+#define SENECA_MDP_I2F 0          // 1: N_S/N_E -> double by I2F.F64.U32 (XU pipe) instead of the 2^52 trick
+#endif
+#ifndef SENECA_MDP_SOA_THREADS
+#define SENECA_MDP_SOA_THREADS 256
+#endif
+#ifndef SENECA_MDP_SOA_MINB
+#define SENECA_MDP_SOA_MINB SENECA_MDP_MINB
+#endif
+constexpr uint32_t kSoaThreads = SENECA_MDP_SOA_THREADS;
+constexpr uint32_t kSoaGroups = kSoaThreads / 32 / kPairW;
+constexpr uint32_t kRowSlots = 104;                               // >= kMaxSteps, rows per array
+constexpr uint32_t kOffCE = 0, kOffTA = 8 * kRowSlots, kOffTD = 16 * kRowSlots, kOffTDC = 24 * kRowSlots,
+                   kOffTE = 32 * kRowSlots, kSoaBytes = 40 * kRowSlots;
+
+// Rows k0 .. k0+31 (one per lane, k <= steps) of a valid profile, SoA layout.
+__device__ void build_rows_soa(const Header& H, uint32_t k0, uint32_t g, uint32_t steps, char* base) {
+    const uint32_t k = k0 + (threadIdx.x & 31);
+    if (k > steps) return;
+    const uint64_t N = H.N;
+    const double dN = u2d(N);
+    const bool exact_div = N < (1ull << 53);
+    const double yN = __drcp_rn(dN);
+    const uint64_t pct = (uint64_t)k * g;
+    uint64_t cad = floor_div(pct * H.Xad, H.Dad, H.rDad), ce = floor_div(pct * H.cache_bytes, H.De, H.rDe);   // Eqs. 5-7, exact floors
+    cad = cad < N ? cad : N;
+    ce = ce < N ? ce : N;
+    const double fa = exact_div ? div_by_n(u2d(cad), dN, yN) : __ddiv_rn(u2d(cad), dN);
+    const double fc = exact_div ? div_by_n(u2d(N - cad), dN, yN) : __ddiv_rn(u2d(N - cad), dN);
+    const double fe = exact_div ? div_by_n(u2d(ce), dN, yN) : __ddiv_rn(u2d(ce), dN);
+    char* p = base + 8 * k;
+    *reinterpret_cast<uint2*>(p + kOffCE) = make_uint2((uint32_t)cad, (uint32_t)ce);   // used only when N < 2^31
+    *reinterpret_cast<double*>(p + kOffTA) = __dmul_rn(fa, H.dsi[0]);
+    *reinterpret_cast<double*>(p + kOffTD) = __dmul_rn(fa, H.dsi[1]);
+    *reinterpret_cast<double*>(p + kOffTDC) = __dmul_rn(fc, H.dsi[1]);
+    *reinterpret_cast<double*>(p + kOffTE) = __dmul_rn(fe, H.dsi[2]);
+}
+
+template <typename T>
+__device__ __forceinline__ T lds_at(const char* base, uint32_t off) { return *reinterpret_cast<const T*>(base + off); }
+
+// shared-space loads at a 32-bit address plus an immediate displacement
+template <uint32_t kOff>
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1+%2];" : "=r"(v) : "r"(a), "n"(kOff));
+    return v;
+}
+template <uint32_t kOff>
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(a), "n"(kOff));
+    return v;
+}
+
+// The pairs of one profile taken by thread gt of its group (N < 2^31).  `sb` is
+// the shared-space address of the group's rows; it is below 2^16 (static shared
+// memory of < 17 KB after the 1 KB reserved window), so one add places it in
+// both 16-bit halves of the packed row offsets.
+template <bool kGrid>
+__device__ __forceinline__ void soa_pairs(uint32_t sb, const uint4* __restrict__ s_pair, uint32_t n_pairs,
+                                          uint32_t gt, uint32_t N, double dN, double y, double dsiE, double dsiS,
+                                          double* __restrict__ grow, double& best, uint32_t& best_i) {
+    const uint32_t sb2 = sb | sb << 16;
+    constexpr uint32_t kDelta = kOffTDC - kOffTD;
+#pragma unroll (kPUnroll)
+    for (uint32_t t = gt; t < n_pairs; t += kPairW * 32) {
+        const uint4 w = s_pair[t];
+        const uint32_t bm = w.x + sb2;
+        const uint32_t b = bm & 0xffffu, m = bm >> 16, e = w.y + sb;   // shared addresses of rows p_A, p_D, p_E
+        const uint32_t cb = lds_u32<kOffCE>(b), cm = lds_u32<kOffCE>(m);
+        const uint32_t sum = cb + cm;                               // <= 2N < 2^32
+        const bool dfree = sum <= N;                                // Eq. 6 unclamped (both splits)
+        const uint32_t r2 = dfree ? N - sum : 0u;
+        const uint32_t cE = lds_u32<kOffCE + 4>(e);
+        const bool efree = dfree && cE <= r2;                       // Eq. 7 unclamped
+        const uint32_t x = efree ? r2 - cE : r2;                    // N_S, or the clamped N_E (0 if D clamped)
+#if SENECA_MDP_I2F
+        const double q = div_by_n(__uint2double_rn(x), dN, y);
+#else
+        const double q = div_by_n(u32_to_d(x), dN, y);
+#endif
+        const double prod = __dmul_rn(q, efree ? dsiS : dsiE);
+        const double tE = lds_f64<kOffTE>(e);
+        const double tX = efree ? tE : 0.0;
+        // Eq. 6: tD of the other coordinate when D is free, else tDc of this one
+        const double d0 = lds_f64<kOffTDC>(dfree ? m - kDelta : b);
+        const double d1 = lds_f64<kOffTDC>(dfree ? b - kDelta : m);
+        const double v0 = __dadd_rn(__dadd_rn(__dadd_rn(lds_f64<kOffTA>(b), d0), tX), prod);
+        const double v1 = __dadd_rn(__dadd_rn(__dadd_rn(lds_f64<kOffTA>(m), d1), tX), prod);
+        const uint32_t i0 = w.z, i1 = w.w;
+        if (kGrid) { __stcs(grow + i0, v0); __stcs(grow + i1, v1); }
+        // a thread meets at most one pair per row and i0 <= i1: its indices only
+        // increase, so strict > keeps the first maximum = the smallest index (R-M8)
+        if (v0 > best) { best = v0; best_i = i0; }
+        if (v1 > best) { best = v1; best_i = i1; }
+    }
+}
+
+// enumeration index -> (row a, position b) of R-M9: a(a+1)/2 <= i < (a+1)(a+2)/2
+__device__ __forceinline__ void index_to_split(uint32_t i, uint32_t& a, uint32_t& b) {
+    a = (uint32_t)((sqrtf((float)(8u * i + 1u)) - 1.0f) * 0.5f);
+    while ((a + 1) * (a + 2) / 2 <= i) ++a;
+    while (a * (a + 1) / 2 > i) --a;
+    b = i - a * (a + 1) / 2;
+}
+
+__global__ void __launch_bounds__(kSoaThreads, SENECA_MDP_SOA_MINB)
+mdp_sweep_soa(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_profiles, uint32_t g,
+              uint32_t steps, uint32_t n_splits, uint32_t n_pairs, seneca_mdp_result* __restrict__ results,
+              double* __restrict__ grid) {
+    __shared__ __align__(16) char s_rows[kSoaGroups][kSoaBytes];
+    __shared__ double s_red_v[kSoaGroups][kPairW];
+    __shared__ uint32_t s_red_i[kSoaGroups][kPairW];
+    __shared__ Hdr s_h[kSoaGroups];
+    extern __shared__ uint4 s_pair4[];                              // [n_pairs]
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t gid = warp / kPairW, gw = warp % kPairW, gt = gw * 32 + lane;
+    // pair table (as mdp_sweep_pairs): row a holds pairs (b, a - b), b <= a / 2
+    auto pairs_before = [](uint32_t a) { const uint32_t m = a >> 1; return (a & 1) ? (m + 1) * (m + 1) : m * (m + 1); };
+    for (uint32_t t = threadIdx.x; t < n_pairs; t += blockDim.x) {
+        uint32_t a = 2u * (uint32_t)sqrtf((float)t);
+        while (a > 0 && pairs_before(a) > t) --a;
+        while (pairs_before(a + 1) <= t) ++a;
+        const uint32_t b = t - pairs_before(a), m = a - b, i0 = a * (a + 1) / 2;
+        s_pair4[t] = make_uint4(8u * b | (8u * m) << 16, 8u * (steps - a), i0 + b, i0 + m);
+    }
+    __syncthreads();
+    char* rows = s_rows[gid];
+    const uint32_t n_groups = gridDim.x * kSoaGroups;
+    for (uint32_t pi = blockIdx.x * kSoaGroups + gid; pi < n_profiles; pi += n_groups) {
+        const seneca_mdp_profile prof = profiles[pi];
+        if (gw == 0) {                                              // Eqs. 1-4 by the group's first warp
+            const Hdr h0 = warp_header(prof);
+            if (lane == 0) s_h[gid] = h0;
+        }
+        group_sync(gid);
+        const Hdr H = s_h[gid];
+        double best = __longlong_as_double(0xfff0000000000000ll);
+        uint32_t best_i = 0xffffffffu;
+        if (H.valid) {                                              // group-uniform
+            Header B;
+            for (int t = 0; t < 4; ++t) B.dsi[t] = H.dsi[t];
+            B.N = prof.n_total;
+            B.Xad = prof.cache_bytes * prof.m_den;
+            B.Dad = 100ull * prof.m_num * prof.s_data;
+            B.De = 100ull * prof.s_data;
+            B.cache_bytes = prof.cache_bytes;
+            B.rDad = __drcp_rn(u2d(B.Dad));
+            B.rDe = __drcp_rn(u2d(B.De));
+            for (uint32_t k0 = gw * 32; k0 <= steps; k0 += kPairW * 32) build_rows_soa(B, k0, g, steps, rows);
+            group_sync(gid);
+            double* grow = grid ? grid + (uint64_t)pi * n_splits : nullptr;
+            if (B.N < (1ull << 31)) {
+                const double dN = u2d(B.N), y = __drcp_rn(dN);
+                const uint32_t sb = (uint32_t)__cvta_generic_to_shared(rows);
+                if (grow) soa_pairs<true>(sb, s_pair4, n_pairs, gt, (uint32_t)B.N, dN, y, H.dsi[2], H.dsi[3], grow, best, best_i);
+                else soa_pairs<false>(sb, s_pair4, n_pairs, gt, (uint32_t)B.N, dN, y, H.dsi[2], H.dsi[3], nullptr, best, best_i);
+            } else {                                                // N >= 2^31: 64-bit counts (rare)
+                const uint64_t N = B.N;
+                const double dN = u2d(N);
+                auto capc = [&](uint32_t k) { const uint64_t c = ((uint64_t)k * g * B.Xad) / B.Dad; return c < N ? c : N; };
+                auto cape = [&](uint32_t k) { const uint64_t c = ((uint64_t)k * g * B.cache_bytes) / B.De; return c < N ? c : N; };
+                for (uint32_t t = gt; t < n_pairs; t += kPairW * 32) {
+                    const uint4 w = s_pair4[t];
+                    for (int h = 0; h < 2; ++h) {
+                        const uint32_t a8 = h ? w.x >> 16 : w.x & 0xffffu, d8 = h ? w.x & 0xffffu : w.x >> 16;
+                        const uint32_t ka = a8 / 8, kd = d8 / 8, ke = w.y / 8, idx = h ? w.w : w.z;
+                        const uint64_t r1 = N - capc(ka);
+                        const uint64_t cD = capc(kd);
+                        const bool dfree = cD <= r1;
+                        const uint64_t r2 = dfree ? r1 - cD : 0ull;
+                        const uint64_t cE = cape(ke);
+                        const bool efree = dfree && cE <= r2;
+                        const uint64_t x = efree ? r2 - cE : r2;
+                        const double prod = __dmul_rn(__ddiv_rn(u2d(x), dN), efree ? H.dsi[3] : H.dsi[2]);
+                        const double tD = dfree ? lds_at<double>(rows, d8 + kOffTD) : lds_at<double>(rows, a8 + kOffTDC);
+                        const double tX = efree ? lds_at<double>(rows, w.y + kOffTE) : 0.0;
+                        const double v = __dadd_rn(__dadd_rn(__dadd_rn(lds_at<double>(rows, a8 + kOffTA), tD), tX), prod);
+                        if (grow) __stcs(grow + idx, v);
+                        if (v > best || (v == best && idx < best_i)) { best = v; best_i = idx; }
+                    }
+                }
+            }
+        }
+        // argmax: the maximum by butterfly, then the smallest index holding it (R-M8)
+        double mx = best;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        best_i = __reduce_min_sync(0xffffffffu, best == mx ? best_i : 0xffffffffu);
+        if (lane == 0) { s_red_v[gid][gw] = mx; s_red_i[gid][gw] = best_i; }
+        group_sync(gid);                                            // rows free, per-warp maxima visible
+        if (gt == 0) {
+            seneca_mdp_result r = {};
+            if (!H.valid) {
+                r.status = 1;
+            } else {
+                double bv = s_red_v[gid][0];
+                uint32_t bi = s_red_i[gid][0];
+                for (uint32_t k = 1; k < kPairW; ++k) {
+                    const double ov = s_red_v[gid][k];
+                    const uint32_t oi = s_red_i[gid][k];
+                    if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+                }
+                uint32_t ra, rb;
+                index_to_split(bi, ra, rb);
+                r.p_e = (uint8_t)(100 - ra * g);
+                r.p_d = (uint8_t)((ra - rb) * g);
+                r.p_a = (uint8_t)(rb * g);
+                r.lim_a = H.lim[0]; r.lim_d = H.lim[1]; r.lim_e = H.lim[2]; r.lim_s = H.lim[3];
+                r.status = 0;
+                r.v_best = bv;
+                r.dsi_a = H.dsi[0]; r.dsi_d = H.dsi[1]; r.dsi_e = H.dsi[2]; r.dsi_s = H.dsi[3];
+            }
+            results[pi] = r;
+        }
+    }
+}
+
 // ------------------------------------------------------------------ evaluation at given splits
 constexpr uint32_t kMaxEvalSplits = 4096;
 struct EvalSplits {
@@ -788,6 +1022,27 @@ extern "C" seneca_status seneca_mdp_sweep(const seneca_mdp_profile* d_profiles, 
     {
         uint32_t np = 0;
         for (uint32_t a = 0; a <= steps; ++a) np += a / 2 + 1;
+#if SENECA_MDP_V2
+        static int sslots = 0;
+        if (!sslots) {
+            int dev = 0, sms = 0, per_sm = 0;
+            SENECA_CUDA_TRY(cudaGetDevice(&dev));
+            SENECA_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+            SENECA_CUDA_TRY(cudaFuncSetAttribute(mdp_sweep_soa, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)(kMaxPairs * sizeof(uint4))));
+            SENECA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mdp_sweep_soa, kSoaThreads,
+                                                                          kMaxPairs * sizeof(uint4)));
+            sslots = sms * (per_sm > 0 ? per_sm : 1);
+        }
+        {
+            const uint32_t want = (n_profiles + kSoaGroups - 1) / kSoaGroups;
+            const uint32_t blocks = want < (uint32_t)sslots ? want : (uint32_t)sslots;
+            mdp_sweep_soa<<<blocks, kSoaThreads, np * sizeof(uint4), (cudaStream_t)stream>>>(
+                d_profiles, n_profiles, grid_step_pct, steps, ns, np, d_results, d_grid);
+            SENECA_CUDA_TRY(cudaGetLastError());
+            return SENECA_OK;
+        }
+#endif
         static int pslots = 0;
         if (!pslots) {
             int dev = 0, sms = 0, per_sm = 0;

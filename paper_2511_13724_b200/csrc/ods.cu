@@ -58,6 +58,13 @@ constexpr uint32_t kMaxBatch = 4096;
 #ifndef SENECA_LATE_WALK
 #define SENECA_LATE_WALK 1          // storage-list walk once all of a job's pools are empty (Cfg.late)
 #endif
+#ifndef SENECA_LATE_BULK
+#define SENECA_LATE_BULK 1          // late rounds of an uncoupled job decided in one pass (late_bulk)
+#endif
+#ifndef SENECA_BULK_MIN
+#define SENECA_BULK_MIN 1           // fewest rounds worth a bulk pass
+#endif
+constexpr uint32_t kBulkMin = SENECA_BULK_MIN;
 #ifndef SENECA_EMPTY_POOLS_FAST
 #define SENECA_EMPTY_POOLS_FAST 1    // skip the classification gathers when every pool of the job is empty
 #endif
@@ -457,6 +464,9 @@ struct PhaseTimer {
             acc[slot] += (unsigned long long)(t - last);
             last = t;
         }
+    }
+    __device__ __forceinline__ void count(uint32_t slot, unsigned long long v) {
+        if (kOn && on && threadIdx.x == 0) acc[slot] += v;
     }
 };
 
@@ -869,6 +879,89 @@ __device__ __noinline__ void catch_up_seen(const Lay& L, const Cfg& C, JobSmem& 
         if (tid == 0) S.fpos = S.cursor;
     }
     __syncthreads();
+}
+
+// Late bulk (Cfg.late, uncoupled jobs): once every pool of job j is empty its
+// remaining rounds of the epoch are decided in advance -- each takes the next
+// `need` entries of the storage-list stream (late_walk) and every one is a miss
+// served from storage (no pool to substitute from, R-O2; no tracked tier, so no
+// consumer, eviction or refill) -- and the rounds of an uncoupled job read no
+// state another round writes.  So `cnt` = K full batches of the stream are
+// decided in one pass, positions n .. n + cnt - 1 of the epoch: digest and
+// transcript exactly as job_round writes them for source S, served[S] += cnt.
+// The stream cursor (lc, lk / cur_buf, cursor) ends where K late walks would
+// leave it, and the seen-marking frontier is untouched (catch_up_seen covers
+// these ids like any other late round's).  Every thread calls it.
+__device__ __forceinline__ unsigned long long late_digest(uint32_t id, uint32_t pos, unsigned long long* trow) {
+    if (trow) trow[pos] = id;                                       // (T_S << 32) | id, T_S = 0
+    return splitmix64(((uint64_t)pos << 35) | id);                  // source T_S = 0 (job_round's digest term)
+}
+
+__device__ __noinline__ void late_bulk(const Lay& L, const Cfg& C, const Launch& P, JobSmem& S, uint32_t j, uint32_t e,
+                                       uint32_t n, uint32_t cnt) {
+    const uint32_t tid = threadIdx.x, T = blockDim.x;
+    const size_t slot = (size_t)j * C.K + (e & (C.K - 1));
+    unsigned long long* trow = P.transcript ? P.transcript + S.rep * P.tr_rep + ((size_t)j * C.maxT + e) * C.N : nullptr;
+    cp_async_wait_all();                                 // a prefetched window of the next walk is dropped
+    __syncthreads();
+    if (tid == 0) S.pf_state = 0;
+    unsigned long long dig = 0;
+    uint32_t done = 0;
+    while (done < cnt) {
+        __syncthreads();                                 // the cursor of the previous step visible
+        const uint32_t* src;
+        uint32_t take;
+        if (S.cur_buf == 0) {
+            if (S.lc >= C.nch) {                         // lap 1 done: the deferred misses are next
+                __syncthreads();
+                if (tid == 0) {
+                    S.cur_buf = S.nxt_buf; S.cur_len = S.nxt_len; S.cursor = 0;
+                    S.nxt_buf = S.cur_buf == 1 ? 2 : 1; S.nxt_len = 0;
+                }
+                continue;
+            }
+            take = min(S.lcnt - S.lk, cnt - done);
+            src = L.slist + slot * C.Nrow + (size_t)S.lc * kGenChunk + S.lk;
+        } else {
+            take = min(S.cur_len - S.cursor, cnt - done);
+            if (take == 0) {                             // cannot happen while n_j < N
+                if (tid == 0) atomicOr(L.err, 2u);
+                break;
+            }
+            src = L.laps + ((size_t)j * 2 + (S.cur_buf - 1)) * C.Nrow + S.cursor;
+        }
+        const uint32_t pos0 = n + done;
+        // 16-B vectors between a scalar head and tail (4 vectors in flight per thread)
+        const uint32_t head = min(take, (uint32_t)((16u - ((uint32_t)(uintptr_t)src & 15u)) & 15u) / 4u);
+        if (tid < head) dig += late_digest(ldcg(src + tid), pos0 + tid, trow);
+        const uint4* v = reinterpret_cast<const uint4*>(src + head);
+        const uint32_t nv = (take - head) / 4;
+#pragma unroll 4
+        for (uint32_t q = tid; q < nv; q += T) {
+            const uint4 x = __ldcg(v + q);
+            const uint32_t p = pos0 + head + 4 * q;
+            dig += late_digest(x.x, p, trow) + late_digest(x.y, p + 1, trow) +
+                   late_digest(x.z, p + 2, trow) + late_digest(x.w, p + 3, trow);
+        }
+        const uint32_t t = head + 4 * nv + tid;
+        if (t < take) dig += late_digest(ldcg(src + t), pos0 + t, trow);
+        __syncthreads();                                 // every thread has read the cursor
+        if (tid == 0) {
+            if (S.cur_buf == 0) {
+                S.lk += take;
+                if (S.lk == S.lcnt) {
+                    S.lc += 1; S.lk = 0;
+                    S.lcnt = S.lc < C.nch ? ldcg(L.scnt + slot * C.nch + S.lc) : 0u;
+                }
+            } else {
+                S.cursor += take;
+            }
+        }
+        done += take;
+    }
+    __syncthreads();
+    S.acc_dig[tid] += dig;
+    if (tid == 0) S.acc_cnt[0] += cnt;                   // served[S]
 }
 
 // Rebuild the three pool counts of job j (epoch start): block bytes in global
@@ -1696,6 +1789,46 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
                 // (C.late: all pools of the job empty, not at an epoch start -> storage-list walk)
                 if (C.late && !S.late && !S.recount && (S.tot[0] | S.tot[1] | S.tot[2]) == 0u)
                     enter_late(L, C, S, j, s_e[j]);
+#if SENECA_LATE_BULK
+                // late bulk: rounds rr+1 .. rr+K of an uncoupled job in late mode, all
+                // but the last round of its epoch and of the launch, decided in one
+                // pass; the schedule (progress of every job, departures, arrivals)
+                // advances round by round in warp 0 as `advance` would
+                if (!coupled && !kShard && S.late && P.mode == 0 && !P.out_ids) {
+                    const uint32_t B = C.batch[j], left = (C.N - s_n[j] + B - 1) / B;   // rounds of epoch s_e[j] left
+                    const uint32_t lrest = P.rounds - (rr + 1);                        // rounds of the launch left
+                    const uint32_t K = min(left, lrest) - 1;
+                    if (left >= 2 && lrest >= 2 && K >= kBulkMin) {
+                        late_bulk(L, C, P, S, j, s_e[j], s_n[j], K * B);
+                        if (tid < 32) {
+                            for (uint32_t k = 0; k < K; ++k) {
+                                const uint64_t rs = P.r0 + rr + 1 + k;
+                                const uint32_t part2 = s_part, departing2 = s_departing;
+                                if ((part2 >> tid) & 1u) {
+                                    uint32_t n = s_n[tid] + need_of(tid);
+                                    if (n == C.N) { n = 0; s_e[tid] += 1; }
+                                    s_n[tid] = n;
+                                }
+                                __syncwarp();
+                                if (tid == 0) {
+                                    s_active &= ~departing2;
+                                    for (uint32_t m = s_pending; m; m &= m - 1) {
+                                        const uint32_t jj = __ffs(m) - 1;
+                                        if (P.arrival[jj] <= rs + 1) { s_active |= 1u << jj; s_pending &= ~(1u << jj); }
+                                    }
+                                }
+                                __syncwarp();
+                                schedule_warp0();
+                                __syncwarp();
+                            }
+                        }
+                        __syncthreads();
+                        rr += K;
+                        TM.tick(6);
+                        TM.count(15, K);                 // rounds decided in bulk
+                    }
+                }
+#endif
                 if (S.late) {
                     late_walk(L, C, S, s_req, j, s_e[j], need_of(j), s_win);
                     TM.tick(13);
