@@ -397,7 +397,9 @@ def latency_floor(c, caps, st, rounds, evicted, refilled, sm_mhz):
     test, no residency gather and no seen mark (its requests are the next
     storage ids in permutation order, DESIGN.md 7.1 "late rounds"), so only the
     rounds with non-empty pools -- estimated as the substituting ones -- carry
-    per-request scattered accesses; the late rounds are counted at zero."""
+    per-request scattered accesses; the late rounds are counted at zero (most of
+    them are not on the round chain at all: the late bulk decides them in one
+    pass per stretch)."""
     ce, cd, ca = caps
     J = len(c["batch"])
     N = c["n_total"]
@@ -549,6 +551,13 @@ def main():
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)      # > 126 MB L2
 
+    def l2_flush(v):
+        # evict L2 by writing 512 MiB, then read the first 256 MiB of it back so that
+        # the flush's own dirty lines are written back here, not inside the next timed
+        # region (where they would compete with the kernel's own DRAM writes)
+        flush.fill_(v & 0xFF)
+        flush[: 256 << 20].max()
+
     def barrier():
         if world > 1:
             torch.distributed.barrier()
@@ -582,7 +591,7 @@ def main():
     kstats = {}
     last_ctx = None
     for s in range(args.steps):
-        flush.fill_(s & 0xFF)                                      # evict L2 between steps
+        l2_flush(s & 0xFF)                                      # evict L2 between steps
         barrier()
         torch.cuda.synchronize(dev)
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
@@ -644,7 +653,7 @@ def main():
         S.mdp_sweep(d_prof_l, nl, args.mdp_grid_step, d_res_l, d_grid_l, stream)
         times = []
         for _ in range(3):
-            flush.fill_(3)
+            l2_flush(3)
             torch.cuda.synchronize(dev)
             e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
             torch.cuda._sleep(200_000)
@@ -680,7 +689,7 @@ def main():
         wsx = torch.empty(wbx, dtype=torch.uint8, device=dev)
         msx, ctxx, rx = [], None, 0
         for s in range(1 + args.steps):
-            flush.fill_(s & 0xFF)
+            l2_flush(s & 0xFF)
             barrier()
             torch.cuda.synchronize(dev)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -730,7 +739,7 @@ def main():
             ws_r = torch.empty(rbytes, dtype=torch.uint8, device=dev)
             rep_ms = []
             for s in range(1 + args.steps):
-                flush.fill_(s & 0xFF)
+                l2_flush(s & 0xFF)
                 barrier()
                 torch.cuda.synchronize(dev)
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -782,7 +791,7 @@ def main():
     pin_stats = torch.empty(nst, dtype=torch.uint8).pin_memory()
     e2e_ods, e2e_mdp = [], []
     for s in range(args.steps):
-        flush.fill_(s & 0xFF)
+        l2_flush(s & 0xFF)
         barrier()
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
@@ -823,6 +832,9 @@ def main():
         for k in keys:
             phase_share[ph_names[k]] = round(float(ph[k]) / tot, 4) if tot else None
     phase_share["walk_steps_per_round"] = round(float(ph[7]) / max(1, rounds_tot / args.steps), 3)
+    # rounds of job 0 decided by the late bulk pass (DESIGN.md 7.1 "late bulk") / all its rounds
+    rounds_job0 = int(c["target"][0]) * -(-int(c["n_total"]) // int(c["batch"][0]))
+    phase_share["late_bulk_round_share_job0"] = round(float(ph[15]) / max(1, rounds_job0), 4)
     S.destroy(ctx)
 
     # ---- aggregate over ranks (max time)
@@ -904,7 +916,7 @@ def main():
             try:
                 ms_g, rr_g, gate = [], 0, "bit-exact"
                 for s_ in range(2):
-                    flush.fill_(s_ & 0xFF)
+                    l2_flush(s_ & 0xFF)
                     barrier()
                     torch.cuda.synchronize(dev)
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -959,7 +971,7 @@ def main():
                 mdp_profiles=args.mdp_profiles, mdp_grid_step_pct=args.mdp_grid_step,
                 mdp_grid_written=d_grid is not None,
                 parallelism=f"{world} independent replays (seed+rank) + {world} independent MDP profile sets",
-                l2="flushed between timed steps (512 MiB write)")),
+                l2="flushed between timed steps (512 MiB write, then a 256 MiB read-back so the flush's dirty lines leave L2 before the timed region)")),
             e2e=dict(value=total_dec / e2e_s, unit="decisions/s",
                      h2d_bytes_per_step=int(pin_prof.numel()), d2h_bytes_per_step=int(nst + pin_res.numel()),
                      mdp_value=total_evals / e2e_m, mdp_unit="split-evals/s",

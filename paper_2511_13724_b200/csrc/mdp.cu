@@ -63,6 +63,17 @@ __device__ __forceinline__ double u32_to_d(uint32_t x) {
     return __dsub_rn(__hiloint2double(0x43300000, (int)x), 4503599627370496.0);
 }
 
+#ifndef SENECA_MDP_STCS
+#define SENECA_MDP_STCS 1         // grid stores: 1 st.global.cs (evict-first), 0 plain st.global (A/B knob)
+#endif
+__device__ __forceinline__ void st_grid(double* p, double v) {
+#if SENECA_MDP_STCS
+    __stcs(p, v);
+#else
+    *p = v;
+#endif
+}
+
 __device__ __forceinline__ void take_min(double term, uint8_t code, double& best, uint8_t& lim) {
     if (term < best) { best = term; lim = code; }
 }
@@ -334,7 +345,7 @@ __device__ __forceinline__ void sweep32_chunk(const Sweep32& P, const Row* rows,
         const double tD = dfree ? rd.tD : ra.tDc;
         const double tX = efree ? re.tE : 0.0;
         const double v = __dadd_rn(__dadd_rn(__dadd_rn(ra.tA, tD), tX), prod);
-        if (kGrid) __stcs(grow + idx, v);
+        if (kGrid) st_grid(grow + idx, v);
         if (v > best) { best = v; best_i = idx; }                 // a lane's idx only increases
     }
 }
@@ -550,6 +561,48 @@ __device__ __forceinline__ Hdr warp_header(const seneca_mdp_profile& p) {
     return h;
 }
 
+// enumeration index -> (row a, position b) of R-M9: a(a+1)/2 <= i < (a+1)(a+2)/2
+__device__ __forceinline__ void index_to_split(uint32_t i, uint32_t& a, uint32_t& b) {
+    a = (uint32_t)((sqrtf((float)(8u * i + 1u)) - 1.0f) * 0.5f);
+    while ((a + 1) * (a + 2) / 2 <= i) ++a;
+    while (a * (a + 1) / 2 > i) --a;
+    b = i - a * (a + 1) / 2;
+}
+
+// The pairs of one profile taken by thread gt of its group (N < 2^31), AoS rows.
+template <bool kGrid>
+__device__ __forceinline__ void aos_pairs(const Row* rows, const uint2* __restrict__ s_pair, uint32_t n_pairs, uint32_t gt,
+                                          uint32_t N, double dN, double y, double dsiE, double dsiS,
+                                          double* __restrict__ grow, double& best, uint32_t& best_i) {
+    const char* rb0 = reinterpret_cast<const char*>(rows);
+#pragma unroll (kPUnroll)
+    for (uint32_t t = gt; t < n_pairs; t += kPairW * 32) {
+        const uint2 w = s_pair[t];
+        const Row& rb = *reinterpret_cast<const Row*>(rb0 + (w.x & 0xfffu));
+        const Row& rm = *reinterpret_cast<const Row*>(rb0 + ((w.x >> 12) & 0xfffu));
+        const Row& re = rows[w.x >> 24];
+        const uint32_t cb = rb.capc, cm = rm.capc;
+        const uint32_t sum = cb + cm;                       // <= 2N < 2^32
+        const bool dfree = sum <= N;                        // Eq. 6 unclamped (both splits)
+        const uint32_t r2 = dfree ? N - sum : 0u;
+        const uint32_t cE = re.cape;
+        const bool efree = dfree && cE <= r2;               // Eq. 7 unclamped
+        const uint32_t x = efree ? r2 - cE : r2;            // N_S, or the clamped N_E (0 if D clamped)
+        const double q = div_by_n(u32_to_d(x), dN, y);
+        const double prod = __dmul_rn(q, efree ? dsiS : dsiE);
+        const double tX = efree ? re.tE : 0.0;
+        const double v0 = __dadd_rn(__dadd_rn(__dadd_rn(rb.tA, dfree ? rm.tD : rb.tDc), tX), prod);
+        const double v1 = __dadd_rn(__dadd_rn(__dadd_rn(rm.tA, dfree ? rb.tD : rm.tDc), tX), prod);
+        const uint32_t i0 = w.y & 0xffffu, i1 = w.y >> 16;
+        if (kGrid) { st_grid(grow + i0, v0); st_grid(grow + i1, v1); }
+        // a thread meets at most one pair per row (kPairW * 32 >= the 51 pairs
+        // of the longest row) and i0 <= i1, so its indices only increase:
+        // strict > keeps the first maximum = the smallest index (R-M8)
+        if (v0 > best) { best = v0; best_i = i0; }
+        if (v1 > best) { best = v1; best_i = i1; }
+    }
+}
+
 __global__ void __launch_bounds__(kThreads, SENECA_MDP_MINB)
 mdp_sweep_pairs(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_profiles, uint32_t g,
                 uint32_t steps, uint32_t n_splits, uint32_t n_pairs, seneca_mdp_result* __restrict__ results,
@@ -609,35 +662,9 @@ mdp_sweep_pairs(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_prof
             group_sync(gid);
             double* grow = grid ? grid + (uint64_t)pi * n_splits : nullptr;
             if (B.N < (1ull << 31)) {
-                const uint32_t N = (uint32_t)B.N;
-                const double dN = u2d(B.N), y = __drcp_rn(dN), dsiE = H.dsi[2], dsiS = H.dsi[3];
-                const char* rb0 = reinterpret_cast<const char*>(rows);
-#pragma unroll (kPUnroll)
-                for (uint32_t t = gt; t < n_pairs; t += kPairW * 32) {
-                    const uint2 w = s_pair[t];
-                    const Row& rb = *reinterpret_cast<const Row*>(rb0 + (w.x & 0xfffu));
-                    const Row& rm = *reinterpret_cast<const Row*>(rb0 + ((w.x >> 12) & 0xfffu));
-                    const Row& re = rows[w.x >> 24];
-                    const uint32_t cb = rb.capc, cm = rm.capc;
-                    const uint32_t sum = cb + cm;                       // <= 2N < 2^32
-                    const bool dfree = sum <= N;                        // Eq. 6 unclamped (both splits)
-                    const uint32_t r2 = dfree ? N - sum : 0u;
-                    const uint32_t cE = re.cape;
-                    const bool efree = dfree && cE <= r2;               // Eq. 7 unclamped
-                    const uint32_t x = efree ? r2 - cE : r2;            // N_S, or the clamped N_E (0 if D clamped)
-                    const double q = div_by_n(u32_to_d(x), dN, y);
-                    const double prod = __dmul_rn(q, efree ? dsiS : dsiE);
-                    const double tX = efree ? re.tE : 0.0;
-                    const double v0 = __dadd_rn(__dadd_rn(__dadd_rn(rb.tA, dfree ? rm.tD : rb.tDc), tX), prod);
-                    const double v1 = __dadd_rn(__dadd_rn(__dadd_rn(rm.tA, dfree ? rb.tD : rm.tDc), tX), prod);
-                    const uint32_t i0 = w.y & 0xffffu, i1 = w.y >> 16;
-                    if (grow) { __stcs(grow + i0, v0); __stcs(grow + i1, v1); }
-                    // a thread meets at most one pair per row (kPairW * 32 >= the 51 pairs
-                    // of the longest row) and i0 <= i1, so its indices only increase:
-                    // strict > keeps the first maximum = the smallest index (R-M8)
-                    if (v0 > best) { best = v0; best_i = i0; }
-                    if (v1 > best) { best = v1; best_i = i1; }
-                }
+                const double dN = u2d(B.N), y = __drcp_rn(dN);
+                if (grow) aos_pairs<true>(rows, s_pair, n_pairs, gt, (uint32_t)B.N, dN, y, H.dsi[2], H.dsi[3], grow, best, best_i);
+                else aos_pairs<false>(rows, s_pair, n_pairs, gt, (uint32_t)B.N, dN, y, H.dsi[2], H.dsi[3], nullptr, best, best_i);
             } else {                                                // N >= 2^31: 64-bit counts (rare)
                 const uint64_t N = B.N;
                 const double dN = u2d(N);
@@ -685,8 +712,8 @@ mdp_sweep_pairs(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_prof
                     const uint32_t oi = s_red_i[gid][k];
                     if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
                 }
-                uint32_t ra = 0, rb = bi;
-                while (rb > ra) { rb -= ra + 1; ++ra; }
+                uint32_t ra, rb;
+                index_to_split(bi, ra, rb);
                 r.p_e = (uint8_t)(100 - ra * g);
                 r.p_d = (uint8_t)((ra - rb) * g);
                 r.p_a = (uint8_t)(rb * g);
@@ -809,20 +836,12 @@ __device__ __forceinline__ void soa_pairs(uint32_t sb, const uint4* __restrict__
         const double v0 = __dadd_rn(__dadd_rn(__dadd_rn(lds_f64<kOffTA>(b), d0), tX), prod);
         const double v1 = __dadd_rn(__dadd_rn(__dadd_rn(lds_f64<kOffTA>(m), d1), tX), prod);
         const uint32_t i0 = w.z, i1 = w.w;
-        if (kGrid) { __stcs(grow + i0, v0); __stcs(grow + i1, v1); }
+        if (kGrid) { st_grid(grow + i0, v0); st_grid(grow + i1, v1); }
         // a thread meets at most one pair per row and i0 <= i1: its indices only
         // increase, so strict > keeps the first maximum = the smallest index (R-M8)
         if (v0 > best) { best = v0; best_i = i0; }
         if (v1 > best) { best = v1; best_i = i1; }
     }
-}
-
-// enumeration index -> (row a, position b) of R-M9: a(a+1)/2 <= i < (a+1)(a+2)/2
-__device__ __forceinline__ void index_to_split(uint32_t i, uint32_t& a, uint32_t& b) {
-    a = (uint32_t)((sqrtf((float)(8u * i + 1u)) - 1.0f) * 0.5f);
-    while ((a + 1) * (a + 2) / 2 <= i) ++a;
-    while (a * (a + 1) / 2 > i) --a;
-    b = i - a * (a + 1) / 2;
 }
 
 __global__ void __launch_bounds__(kSoaThreads, SENECA_MDP_SOA_MINB)

@@ -922,6 +922,10 @@ __device__ __noinline__ void late_bulk(const Lay& L, const Cfg& C, const Launch&
             }
             take = min(S.lcnt - S.lk, cnt - done);
             src = L.slist + slot * C.Nrow + (size_t)S.lc * kGenChunk + S.lk;
+            if (S.lc + 1 < C.nch && take < cnt - done) {  // the next segment's lines into L2 meanwhile
+                const uint32_t* nx = L.slist + slot * C.Nrow + (size_t)(S.lc + 1) * kGenChunk;
+                for (uint32_t l = tid; l < kGenChunk / 32; l += T) asm volatile("prefetch.global.L2 [%0];" :: "l"(nx + 32 * l));
+            }
         } else {
             take = min(S.cur_len - S.cursor, cnt - done);
             if (take == 0) {                             // cannot happen while n_j < N
@@ -1503,6 +1507,50 @@ __device__ void job_take_refills(const Lay& L, const Cfg& C, JobSmem& S, uint32_
 // workspace slice and seed) that share nothing but the launch.
 __device__ __noinline__ void ring_generate(const Lay& L, const Cfg& C, uint32_t n_pairs);
 
+// The schedule of rounds rs .. rs+K-1 advanced by warp 0 (lane = job) in
+// closed form, as K calls of `advance` would: every active job of the subset
+// consumes a batch per round (the last round of an epoch takes the rest),
+// departs at the end of the round that completes its last epoch, and a pending
+// job joins at the start of its arrival round (spans are cut at arrivals).
+__device__ __noinline__ void skip_rounds_warp0(const Cfg& C, const Launch& P, uint64_t rs, uint32_t K, uint32_t* s_n,
+                                               uint32_t* s_e, uint32_t& s_active, uint32_t& s_pending) {
+    const uint32_t lane = threadIdx.x & 31u;
+    while (K > 0) {
+        uint64_t span = K;
+        for (uint32_t m = s_pending; m; m &= m - 1) {
+            const uint32_t jj = __ffs(m) - 1;
+            if (P.arrival[jj] > rs) span = min(span, (uint64_t)P.arrival[jj] - rs);
+        }
+        const uint32_t part = s_active & P.subset;
+        bool gone = false;
+        if (lane < C.J && ((part >> lane) & 1u)) {
+            const uint32_t B = C.batch[lane];
+            uint32_t n = s_n[lane], e = s_e[lane];
+            uint64_t R = span;
+            while (R > 0) {
+                const uint32_t r_ep = (C.N - n + B - 1) / B;    // rounds left in epoch e (the last may be short)
+                if (R < r_ep) { n += (uint32_t)R * B; R = 0; }
+                else {
+                    R -= r_ep; n = 0; e += 1;
+                    if (e == C.target[lane]) { gone = true; break; }   // departs after its last round
+                }
+            }
+            s_n[lane] = n; s_e[lane] = e;
+        }
+        const uint32_t departed = __ballot_sync(0xffffffffu, gone);
+        rs += span;
+        K -= (uint32_t)span;
+        if (lane == 0) {
+            s_active &= ~departed;
+            for (uint32_t m = s_pending; m; m &= m - 1) {       // arrivals at the start of round rs
+                const uint32_t jj = __ffs(m) - 1;
+                if (P.arrival[jj] <= rs) { s_active |= 1u << jj; s_pending &= ~(1u << jj); }
+            }
+        }
+        __syncwarp();
+    }
+}
+
 template <bool kTime, bool kCoupled, bool kShard>
 __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, const Launch& P) {
     if (P.gen_ctas && blockIdx.x >= gridDim.x - P.gen_ctas) {     // the permutation-ring generator CTAs
@@ -1800,28 +1848,9 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
                     const uint32_t K = min(left, lrest) - 1;
                     if (left >= 2 && lrest >= 2 && K >= kBulkMin) {
                         late_bulk(L, C, P, S, j, s_e[j], s_n[j], K * B);
-                        if (tid < 32) {
-                            for (uint32_t k = 0; k < K; ++k) {
-                                const uint64_t rs = P.r0 + rr + 1 + k;
-                                const uint32_t part2 = s_part, departing2 = s_departing;
-                                if ((part2 >> tid) & 1u) {
-                                    uint32_t n = s_n[tid] + need_of(tid);
-                                    if (n == C.N) { n = 0; s_e[tid] += 1; }
-                                    s_n[tid] = n;
-                                }
-                                __syncwarp();
-                                if (tid == 0) {
-                                    s_active &= ~departing2;
-                                    for (uint32_t m = s_pending; m; m &= m - 1) {
-                                        const uint32_t jj = __ffs(m) - 1;
-                                        if (P.arrival[jj] <= rs + 1) { s_active |= 1u << jj; s_pending &= ~(1u << jj); }
-                                    }
-                                }
-                                __syncwarp();
-                                schedule_warp0();
-                                __syncwarp();
-                            }
-                        }
+                        if (tid < 32) skip_rounds_warp0(C, P, P.r0 + rr + 1, K, s_n, s_e, s_active, s_pending);
+                        __syncwarp();
+                        if (tid < 32) schedule_warp0();
                         __syncthreads();
                         rr += K;
                         TM.tick(6);
