@@ -730,154 +730,98 @@ mdp_sweep_pairs(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_prof
     }
 }
 
-// ------------------------------------------------------------------ the paired sweep, SoA rows
-// The same pairs and the same IEEE operations as mdp_sweep_pairs, laid out for
-// fewer instructions per pair (the sweep is issue-bound):
-//  * the group's rows are structure-of-arrays with 8-byte slots (k8 = 8 k):
-//    {capc, cape} | tA | tD | tDc | tE, so one byte offset per coordinate
-//    addresses every array with an immediate displacement, and a lane reading
-//    consecutive rows reads consecutive slots (no bank conflicts);
-//  * the pair table entry is {b8 | m8 << 16, e8, i0, i1}: the group's base is
-//    added to both packed offsets with one add, the enumeration indices need no
-//    extraction;
-//  * the tD / tDc choice of Eq. 6 is an address select into two arrays;
-//  * the grid pointer is a template parameter (no per-pair null test).
-#ifndef SENECA_MDP_V2
-#define SENECA_MDP_V2 0           // 1: mdp_sweep_soa; 0: mdp_sweep_pairs (A/B knob)
-#endif
-#ifndef SENECA_MDP_I2F
-#define SENECA_MDP_I2F 0          // 1: N_S/N_E -> double by I2F.F64.U32 (XU pipe) instead of the 2^52 trick
-#endif
-#ifndef SENECA_MDP_SOA_THREADS
-#define SENECA_MDP_SOA_THREADS 256
-#endif
-#ifndef SENECA_MDP_SOA_MINB
-#define SENECA_MDP_SOA_MINB SENECA_MDP_MINB
-#endif
-constexpr uint32_t kSoaThreads = SENECA_MDP_SOA_THREADS;
-constexpr uint32_t kSoaGroups = kSoaThreads / 32 / kPairW;
-constexpr uint32_t kRowSlots = 104;                               // >= kMaxSteps, rows per array
-constexpr uint32_t kOffCE = 0, kOffTA = 8 * kRowSlots, kOffTD = 16 * kRowSlots, kOffTDC = 24 * kRowSlots,
-                   kOffTE = 32 * kRowSlots, kSoaBytes = 40 * kRowSlots;
-
-// Rows k0 .. k0+31 (one per lane, k <= steps) of a valid profile, SoA layout.
-__device__ void build_rows_soa(const Header& H, uint32_t k0, uint32_t g, uint32_t steps, char* base) {
-    const uint32_t k = k0 + (threadIdx.x & 31);
-    if (k > steps) return;
-    const uint64_t N = H.N;
-    const double dN = u2d(N);
-    const bool exact_div = N < (1ull << 53);
-    const double yN = __drcp_rn(dN);
-    const uint64_t pct = (uint64_t)k * g;
-    uint64_t cad = floor_div(pct * H.Xad, H.Dad, H.rDad), ce = floor_div(pct * H.cache_bytes, H.De, H.rDe);   // Eqs. 5-7, exact floors
-    cad = cad < N ? cad : N;
-    ce = ce < N ? ce : N;
-    const double fa = exact_div ? div_by_n(u2d(cad), dN, yN) : __ddiv_rn(u2d(cad), dN);
-    const double fc = exact_div ? div_by_n(u2d(N - cad), dN, yN) : __ddiv_rn(u2d(N - cad), dN);
-    const double fe = exact_div ? div_by_n(u2d(ce), dN, yN) : __ddiv_rn(u2d(ce), dN);
-    char* p = base + 8 * k;
-    *reinterpret_cast<uint2*>(p + kOffCE) = make_uint2((uint32_t)cad, (uint32_t)ce);   // used only when N < 2^31
-    *reinterpret_cast<double*>(p + kOffTA) = __dmul_rn(fa, H.dsi[0]);
-    *reinterpret_cast<double*>(p + kOffTD) = __dmul_rn(fa, H.dsi[1]);
-    *reinterpret_cast<double*>(p + kOffTDC) = __dmul_rn(fc, H.dsi[1]);
-    *reinterpret_cast<double*>(p + kOffTE) = __dmul_rn(fe, H.dsi[2]);
-}
-
-template <typename T>
-__device__ __forceinline__ T lds_at(const char* base, uint32_t off) { return *reinterpret_cast<const T*>(base + off); }
-
-// shared-space loads at a 32-bit address plus an immediate displacement
-template <uint32_t kOff>
-__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
-    uint32_t v;
-    asm volatile("ld.shared.u32 %0, [%1+%2];" : "=r"(v) : "r"(a), "n"(kOff));
-    return v;
-}
-template <uint32_t kOff>
-__device__ __forceinline__ double lds_f64(uint32_t a) {
-    double v;
-    asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(a), "n"(kOff));
-    return v;
-}
-
-// The pairs of one profile taken by thread gt of its group (N < 2^31).  `sb` is
-// the shared-space address of the group's rows; it is below 2^16 (static shared
-// memory of < 17 KB after the 1 KB reserved window), so one add places it in
-// both 16-bit halves of the packed row offsets.
-template <bool kGrid>
-__device__ __forceinline__ void soa_pairs(uint32_t sb, const uint4* __restrict__ s_pair, uint32_t n_pairs,
-                                          uint32_t gt, uint32_t N, double dN, double y, double dsiE, double dsiS,
-                                          double* __restrict__ grow, double& best, uint32_t& best_i) {
-    const uint32_t sb2 = sb | sb << 16;
-    constexpr uint32_t kDelta = kOffTDC - kOffTD;
+// The pairs of one profile taken by thread tid of a 256-thread CTA (N < 2^31),
+// values into the shared staging row (the arithmetic of aos_pairs).  A thread
+// meets at most one pair per row (256 >= 51) and i0 <= i1, so its indices only
+// increase: strict > keeps the first maximum (R-M8).
+__device__ __forceinline__ void stage_pairs(const Row* rows, const uint2* __restrict__ s_pair, uint32_t n_pairs,
+                                            uint32_t tid, uint32_t N, double dN, double y, double dsiE, double dsiS,
+                                            double* srow, double& best, uint32_t& best_i) {
+    const char* rb0 = reinterpret_cast<const char*>(rows);
 #pragma unroll (kPUnroll)
-    for (uint32_t t = gt; t < n_pairs; t += kPairW * 32) {
-        const uint4 w = s_pair[t];
-        const uint32_t bm = w.x + sb2;
-        const uint32_t b = bm & 0xffffu, m = bm >> 16, e = w.y + sb;   // shared addresses of rows p_A, p_D, p_E
-        const uint32_t cb = lds_u32<kOffCE>(b), cm = lds_u32<kOffCE>(m);
-        const uint32_t sum = cb + cm;                               // <= 2N < 2^32
-        const bool dfree = sum <= N;                                // Eq. 6 unclamped (both splits)
+    for (uint32_t t = tid; t < n_pairs; t += kThreads) {
+        const uint2 w = s_pair[t];
+        const Row& rb = *reinterpret_cast<const Row*>(rb0 + (w.x & 0xfffu));
+        const Row& rm = *reinterpret_cast<const Row*>(rb0 + ((w.x >> 12) & 0xfffu));
+        const Row& re = rows[w.x >> 24];
+        const uint32_t sum = rb.capc + rm.capc;             // <= 2N < 2^32
+        const bool dfree = sum <= N;                        // Eq. 6 unclamped (both splits)
         const uint32_t r2 = dfree ? N - sum : 0u;
-        const uint32_t cE = lds_u32<kOffCE + 4>(e);
-        const bool efree = dfree && cE <= r2;                       // Eq. 7 unclamped
-        const uint32_t x = efree ? r2 - cE : r2;                    // N_S, or the clamped N_E (0 if D clamped)
-#if SENECA_MDP_I2F
-        const double q = div_by_n(__uint2double_rn(x), dN, y);
-#else
+        const uint32_t cE = re.cape;
+        const bool efree = dfree && cE <= r2;               // Eq. 7 unclamped
+        const uint32_t x = efree ? r2 - cE : r2;            // N_S, or the clamped N_E (0 if D clamped)
         const double q = div_by_n(u32_to_d(x), dN, y);
-#endif
         const double prod = __dmul_rn(q, efree ? dsiS : dsiE);
-        const double tE = lds_f64<kOffTE>(e);
-        const double tX = efree ? tE : 0.0;
-        // Eq. 6: tD of the other coordinate when D is free, else tDc of this one
-        const double d0 = lds_f64<kOffTDC>(dfree ? m - kDelta : b);
-        const double d1 = lds_f64<kOffTDC>(dfree ? b - kDelta : m);
-        const double v0 = __dadd_rn(__dadd_rn(__dadd_rn(lds_f64<kOffTA>(b), d0), tX), prod);
-        const double v1 = __dadd_rn(__dadd_rn(__dadd_rn(lds_f64<kOffTA>(m), d1), tX), prod);
-        const uint32_t i0 = w.z, i1 = w.w;
-        if (kGrid) { st_grid(grow + i0, v0); st_grid(grow + i1, v1); }
-        // a thread meets at most one pair per row and i0 <= i1: its indices only
-        // increase, so strict > keeps the first maximum = the smallest index (R-M8)
+        const double tX = efree ? re.tE : 0.0;
+        const double v0 = __dadd_rn(__dadd_rn(__dadd_rn(rb.tA, dfree ? rm.tD : rb.tDc), tX), prod);
+        const double v1 = __dadd_rn(__dadd_rn(__dadd_rn(rm.tA, dfree ? rb.tD : rm.tDc), tX), prod);
+        const uint32_t i0 = w.y & 0xffffu, i1 = w.y >> 16;
+        srow[i0] = v0;
+        srow[i1] = v1;
         if (v0 > best) { best = v0; best_i = i0; }
         if (v1 > best) { best = v1; best_i = i1; }
     }
 }
 
-__global__ void __launch_bounds__(kSoaThreads, SENECA_MDP_SOA_MINB)
-mdp_sweep_soa(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_profiles, uint32_t g,
+// ------------------------------------------------------------------ the paired sweep, grid by TMA
+// With the grid requested the sweep is bound by its write pattern, not by its
+// arithmetic: the paired sweep's 8-B stores (i0 ascending, i1 descending, 1,776
+// profile rows in flight) reach ~4.1 TB/s on B200, while whole rows written by
+// one bulk copy each reach ~5.9 (10 k rows) / 6.2 TB/s (100 k rows)
+// (tools/micro/store_pattern.cu).  So here one CTA sweeps one
+// profile at a time: the pairs are computed exactly as in mdp_sweep_pairs
+// (the same operations on the same operands, aos_pairs) into a shared-memory
+// copy of the profile's grid row, and thread 0 writes the row with one
+// cp.async.bulk (TMA) store -- 16-B aligned middle; the 8-B head or tail
+// element by a plain store -- which drains while the CTA builds the next
+// profile's rows.  The staging row is rewritten only after the copy has read it
+// (cp.async.bulk.wait_group.read).
+#ifndef SENECA_MDP_GRID_CTAS
+#define SENECA_MDP_GRID_CTAS 0    // > 0: at most this many CTAs per SM (x148) when the grid is written
+#endif
+#ifndef SENECA_MDP_TMA
+#define SENECA_MDP_TMA 0          // 1: the grid by mdp_sweep_tma; 0: mdp_sweep_pairs writes it (A/B knob)
+#endif
+__host__ __device__ constexpr uint32_t tma_smem_bytes(uint32_t n_pairs, uint32_t n_splits) {
+    return ((n_splits + 2u) * 8u + 15u) / 16u * 16u + n_pairs * 8u;   // staging row (+ head slot) | pair table
+}
+
+__global__ void __launch_bounds__(kThreads, SENECA_MDP_MINB)
+mdp_sweep_tma(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_profiles, uint32_t g,
               uint32_t steps, uint32_t n_splits, uint32_t n_pairs, seneca_mdp_result* __restrict__ results,
               double* __restrict__ grid) {
-    __shared__ __align__(16) char s_rows[kSoaGroups][kSoaBytes];
-    __shared__ double s_red_v[kSoaGroups][kPairW];
-    __shared__ uint32_t s_red_i[kSoaGroups][kPairW];
-    __shared__ Hdr s_h[kSoaGroups];
-    extern __shared__ uint4 s_pair4[];                              // [n_pairs]
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t gid = warp / kPairW, gw = warp % kPairW, gt = gw * 32 + lane;
-    // pair table (as mdp_sweep_pairs): row a holds pairs (b, a - b), b <= a / 2
+    constexpr uint32_t kWarps = kThreads / 32;
+    __shared__ Row s_rows[kMaxSteps];
+    __shared__ double s_red_v[kWarps];
+    __shared__ uint32_t s_red_i[kWarps];
+    __shared__ Hdr s_h;
+    extern __shared__ __align__(16) unsigned char s_dyn[];
+    double* s_row = reinterpret_cast<double*>(s_dyn);                                  // [n_splits + 2]
+    uint2* s_pair = reinterpret_cast<uint2*>(s_dyn + ((n_splits + 2u) * 8u + 15u) / 16u * 16u);
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     auto pairs_before = [](uint32_t a) { const uint32_t m = a >> 1; return (a & 1) ? (m + 1) * (m + 1) : m * (m + 1); };
-    for (uint32_t t = threadIdx.x; t < n_pairs; t += blockDim.x) {
+    for (uint32_t t = tid; t < n_pairs; t += blockDim.x) {          // pair table (as mdp_sweep_pairs)
         uint32_t a = 2u * (uint32_t)sqrtf((float)t);
         while (a > 0 && pairs_before(a) > t) --a;
         while (pairs_before(a + 1) <= t) ++a;
         const uint32_t b = t - pairs_before(a), m = a - b, i0 = a * (a + 1) / 2;
-        s_pair4[t] = make_uint4(8u * b | (8u * m) << 16, 8u * (steps - a), i0 + b, i0 + m);
+        s_pair[t] = make_uint2((uint32_t)(b * sizeof(Row)) | (uint32_t)(m * sizeof(Row)) << 12 | (steps - a) << 24,
+                               (i0 + b) | (i0 + m) << 16);
     }
     __syncthreads();
-    char* rows = s_rows[gid];
-    const uint32_t n_groups = gridDim.x * kSoaGroups;
-    for (uint32_t pi = blockIdx.x * kSoaGroups + gid; pi < n_profiles; pi += n_groups) {
+    for (uint32_t pi = blockIdx.x; pi < n_profiles; pi += gridDim.x) {
         const seneca_mdp_profile prof = profiles[pi];
-        if (gw == 0) {                                              // Eqs. 1-4 by the group's first warp
+        if (warp == 0) {                                            // Eqs. 1-4 by warp 0
             const Hdr h0 = warp_header(prof);
-            if (lane == 0) s_h[gid] = h0;
+            if (lane == 0) s_h = h0;
         }
-        group_sync(gid);
-        const Hdr H = s_h[gid];
+        __syncthreads();                                            // (also: the rows of the last profile are free)
+        const Hdr H = s_h;
         double best = __longlong_as_double(0xfff0000000000000ll);
         uint32_t best_i = 0xffffffffu;
-        if (H.valid) {                                              // group-uniform
+        double* grow = grid + (uint64_t)pi * n_splits;
+        const uint32_t h = (uint32_t)(reinterpret_cast<uintptr_t>(grow) >> 3) & 1u;  // row starts 8 mod 16
+        if (H.valid) {                                              // CTA-uniform
             Header B;
             for (int t = 0; t < 4; ++t) B.dsi[t] = H.dsi[t];
             B.N = prof.n_total;
@@ -887,24 +831,25 @@ mdp_sweep_soa(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_profil
             B.cache_bytes = prof.cache_bytes;
             B.rDad = __drcp_rn(u2d(B.Dad));
             B.rDe = __drcp_rn(u2d(B.De));
-            for (uint32_t k0 = gw * 32; k0 <= steps; k0 += kPairW * 32) build_rows_soa(B, k0, g, steps, rows);
-            group_sync(gid);
-            double* grow = grid ? grid + (uint64_t)pi * n_splits : nullptr;
+            if (warp * 32 <= steps) build_rows(B, warp * 32, g, steps, s_rows);
+            // the staging row is free once the previous profile's copy has read it
+            if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            __syncthreads();
+            double* srow = s_row + h;                               // value i at s_row[h + i]: 16-B aligned with grow
             if (B.N < (1ull << 31)) {
                 const double dN = u2d(B.N), y = __drcp_rn(dN);
-                const uint32_t sb = (uint32_t)__cvta_generic_to_shared(rows);
-                if (grow) soa_pairs<true>(sb, s_pair4, n_pairs, gt, (uint32_t)B.N, dN, y, H.dsi[2], H.dsi[3], grow, best, best_i);
-                else soa_pairs<false>(sb, s_pair4, n_pairs, gt, (uint32_t)B.N, dN, y, H.dsi[2], H.dsi[3], nullptr, best, best_i);
+                stage_pairs(s_rows, s_pair, n_pairs, tid, (uint32_t)B.N, dN, y, H.dsi[2], H.dsi[3], srow, best, best_i);
             } else {                                                // N >= 2^31: 64-bit counts (rare)
                 const uint64_t N = B.N;
                 const double dN = u2d(N);
                 auto capc = [&](uint32_t k) { const uint64_t c = ((uint64_t)k * g * B.Xad) / B.Dad; return c < N ? c : N; };
                 auto cape = [&](uint32_t k) { const uint64_t c = ((uint64_t)k * g * B.cache_bytes) / B.De; return c < N ? c : N; };
-                for (uint32_t t = gt; t < n_pairs; t += kPairW * 32) {
-                    const uint4 w = s_pair4[t];
-                    for (int h = 0; h < 2; ++h) {
-                        const uint32_t a8 = h ? w.x >> 16 : w.x & 0xffffu, d8 = h ? w.x & 0xffffu : w.x >> 16;
-                        const uint32_t ka = a8 / 8, kd = d8 / 8, ke = w.y / 8, idx = h ? w.w : w.z;
+                for (uint32_t t = tid; t < n_pairs; t += blockDim.x) {
+                    const uint2 w = s_pair[t];
+                    for (int hh = 0; hh < 2; ++hh) {
+                        const uint32_t ka = (hh ? (w.x >> 12) & 0xfffu : w.x & 0xfffu) / sizeof(Row);
+                        const uint32_t kd = (hh ? w.x & 0xfffu : (w.x >> 12) & 0xfffu) / sizeof(Row);
+                        const uint32_t ke = w.x >> 24, idx = hh ? w.y >> 16 : w.y & 0xffffu;
                         const uint64_t r1 = N - capc(ka);
                         const uint64_t cD = capc(kd);
                         const bool dfree = cD <= r1;
@@ -913,32 +858,40 @@ mdp_sweep_soa(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_profil
                         const bool efree = dfree && cE <= r2;
                         const uint64_t x = efree ? r2 - cE : r2;
                         const double prod = __dmul_rn(__ddiv_rn(u2d(x), dN), efree ? H.dsi[3] : H.dsi[2]);
-                        const double tD = dfree ? lds_at<double>(rows, d8 + kOffTD) : lds_at<double>(rows, a8 + kOffTDC);
-                        const double tX = efree ? lds_at<double>(rows, w.y + kOffTE) : 0.0;
-                        const double v = __dadd_rn(__dadd_rn(__dadd_rn(lds_at<double>(rows, a8 + kOffTA), tD), tX), prod);
-                        if (grow) __stcs(grow + idx, v);
+                        const double tD = dfree ? s_rows[kd].tD : s_rows[ka].tDc;
+                        const double tX = efree ? s_rows[ke].tE : 0.0;
+                        const double v = __dadd_rn(__dadd_rn(__dadd_rn(s_rows[ka].tA, tD), tX), prod);
+                        srow[idx] = v;
                         if (v > best || (v == best && idx < best_i)) { best = v; best_i = idx; }
                     }
                 }
             }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic-proxy writes -> the bulk copy
         }
         // argmax: the maximum by butterfly, then the smallest index holding it (R-M8)
         double mx = best;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         best_i = __reduce_min_sync(0xffffffffu, best == mx ? best_i : 0xffffffffu);
-        if (lane == 0) { s_red_v[gid][gw] = mx; s_red_i[gid][gw] = best_i; }
-        group_sync(gid);                                            // rows free, per-warp maxima visible
-        if (gt == 0) {
+        if (lane == 0) { s_red_v[warp] = mx; s_red_i[warp] = best_i; }
+        __syncthreads();                                            // the staged row and the per-warp maxima complete
+        if (tid == 0) {
             seneca_mdp_result r = {};
             if (!H.valid) {
                 r.status = 1;
             } else {
-                double bv = s_red_v[gid][0];
-                uint32_t bi = s_red_i[gid][0];
-                for (uint32_t k = 1; k < kPairW; ++k) {
-                    const double ov = s_red_v[gid][k];
-                    const uint32_t oi = s_red_i[gid][k];
+                const uint32_t nb = (n_splits - h) / 2u * 16u;      // 16-B aligned middle
+                const uint32_t sa = (uint32_t)__cvta_generic_to_shared(s_row + 2u * h);
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                             :: "l"(grow + h), "r"(sa), "r"(nb) : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                if (h) grow[0] = s_row[1];                          // the 8-B head
+                if ((n_splits - h) & 1u) grow[n_splits - 1] = s_row[h + n_splits - 1];   // the 8-B tail
+                double bv = s_red_v[0];
+                uint32_t bi = s_red_i[0];
+                for (uint32_t k = 1; k < kWarps; ++k) {
+                    const double ov = s_red_v[k];
+                    const uint32_t oi = s_red_i[k];
                     if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
                 }
                 uint32_t ra, rb;
@@ -953,7 +906,10 @@ mdp_sweep_soa(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_profil
             }
             results[pi] = r;
         }
+        // s_h and the per-warp maxima are rewritten after the next profile's first
+        // barrier, which thread 0 reaches only after reading them
     }
+    if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // ------------------------------------------------------------------ evaluation at given splits
@@ -1041,38 +997,41 @@ extern "C" seneca_status seneca_mdp_sweep(const seneca_mdp_profile* d_profiles, 
     {
         uint32_t np = 0;
         for (uint32_t a = 0; a <= steps; ++a) np += a / 2 + 1;
-#if SENECA_MDP_V2
-        static int sslots = 0;
-        if (!sslots) {
-            int dev = 0, sms = 0, per_sm = 0;
-            SENECA_CUDA_TRY(cudaGetDevice(&dev));
-            SENECA_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-            SENECA_CUDA_TRY(cudaFuncSetAttribute(mdp_sweep_soa, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)(kMaxPairs * sizeof(uint4))));
-            SENECA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mdp_sweep_soa, kSoaThreads,
-                                                                          kMaxPairs * sizeof(uint4)));
-            sslots = sms * (per_sm > 0 ? per_sm : 1);
-        }
-        {
-            const uint32_t want = (n_profiles + kSoaGroups - 1) / kSoaGroups;
-            const uint32_t blocks = want < (uint32_t)sslots ? want : (uint32_t)sslots;
-            mdp_sweep_soa<<<blocks, kSoaThreads, np * sizeof(uint4), (cudaStream_t)stream>>>(
+        if (d_grid && SENECA_MDP_TMA) {
+            static int tslots = 0;
+            if (!tslots) {
+                int dev = 0, sms = 0, per_sm = 0;
+                SENECA_CUDA_TRY(cudaGetDevice(&dev));
+                SENECA_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+                SENECA_CUDA_TRY(cudaFuncSetAttribute(mdp_sweep_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     (int)tma_smem_bytes(kMaxPairs, 5151)));
+                SENECA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mdp_sweep_tma, kThreads,
+                                                                              tma_smem_bytes(kMaxPairs, 5151)));
+                tslots = sms * (per_sm > 0 ? per_sm : 1);
+            }
+            const uint32_t blocks = n_profiles < (uint32_t)tslots ? n_profiles : (uint32_t)tslots;
+            mdp_sweep_tma<<<blocks, kThreads, tma_smem_bytes(np, ns), (cudaStream_t)stream>>>(
                 d_profiles, n_profiles, grid_step_pct, steps, ns, np, d_results, d_grid);
             SENECA_CUDA_TRY(cudaGetLastError());
             return SENECA_OK;
         }
-#endif
-        static int pslots = 0;
+        static int pslots = 0, psms = 0;
         if (!pslots) {
             int dev = 0, sms = 0, per_sm = 0;
             SENECA_CUDA_TRY(cudaGetDevice(&dev));
             SENECA_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+            psms = sms;
             SENECA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mdp_sweep_pairs, kThreads,
                                                                           kMaxPairs * sizeof(uint2)));
             pslots = sms * (per_sm > 0 ? per_sm : 1);
         }
         const uint32_t want = (n_profiles + kGroups - 1) / kGroups;
-        const uint32_t blocks = want < (uint32_t)pslots ? want : (uint32_t)pslots;
+        uint32_t blocks = want < (uint32_t)pslots ? want : (uint32_t)pslots;
+        // with the grid requested, fewer profile rows in flight: the DRAM write rate of
+        // the row-interleaved store pattern falls as concurrent row streams grow
+        // (tools/micro/store_pattern.cu)
+        const uint32_t gcap = (uint32_t)psms * SENECA_MDP_GRID_CTAS;
+        if (d_grid && SENECA_MDP_GRID_CTAS > 0 && blocks > gcap) blocks = gcap;
         mdp_sweep_pairs<<<blocks, kThreads, np * sizeof(uint2), (cudaStream_t)stream>>>(
             d_profiles, n_profiles, grid_step_pct, steps, ns, np, d_results, d_grid);
         SENECA_CUDA_TRY(cudaGetLastError());

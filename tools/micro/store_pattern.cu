@@ -98,21 +98,23 @@ int main(int argc, char** argv) {
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     const int blocks = 148 * 3;
     cudaFuncSetAttribute(patF, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * (kSplits + 3) * 8);
+    const int nb = argc > 2 ? atoi(argv[2]) : 3;     // CTAs per SM for patterns A, B, C, E
+    const int blocks2 = 148 * nb;
     for (int p = 0; p < 6; ++p) {
         float best = 1e9;
         for (int it = 0; it < 12; ++it) {
             cudaEventRecord(e0);
-            if (p == 0) patA<<<blocks, 256>>>(g, rows, dtab);
-            if (p == 1) patB<<<blocks, 256>>>(g, rows);
-            if (p == 2) patC<<<blocks, 256>>>(g, rows);
+            if (p == 0) patA<<<blocks2, 256>>>(g, rows, dtab);
+            if (p == 1) patB<<<blocks2, 256>>>(g, rows);
+            if (p == 2) patC<<<blocks2, 256>>>(g, rows);
             if (p == 3) patD<<<148 * 8, 256>>>(g, n);
-            if (p == 4) patE<<<blocks, 256>>>(g, rows);
-            if (p == 5) patF<<<148 * 2, 256, 2 * (kSplits + 3) * 8>>>(g, rows);
+            if (p == 4) patE<<<blocks2, 256>>>(g, rows);
+            if (p == 5) patF<<<148 * (nb < 2 ? nb : 2), 256, 2 * (kSplits + 3) * 8>>>(g, rows);
             cudaEventRecord(e1); cudaEventSynchronize(e1);
             float ms; cudaEventElapsedTime(&ms, e0, e1);
             if (it >= 2 && ms < best) best = ms;
         }
-        printf("rows %d pattern %c: %.1f us  %.0f GB/s\n", rows, "ABCDEF"[p], best * 1e3, n * 8 / (best * 1e-3) / 1e9);
+        printf("ctas/sm %d rows %d pattern %c: %.1f us  %.0f GB/s\n", nb, rows, "ABCDEF"[p], best * 1e3, n * 8 / (best * 1e-3) / 1e9);
     }
     return cudaGetLastError() != cudaSuccess;
 }

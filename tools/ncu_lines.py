@@ -1,4 +1,4 @@
-"""Top source lines of an ncu report by warp-stall samples (needs -lineinfo and
+"""Top source lines (--by-inst: by instructions executed) of an ncu report by warp-stall samples (needs -lineinfo and
 --import-source on):  python tools/ncu_lines.py REPORT [N] [--nobar]
 --nobar ranks lines by samples that are not barrier waits (where the slowest
 warps spend their time between barriers)."""
@@ -10,6 +10,7 @@ import sys
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2].isdigit() else 40
 nobar = "--nobar" in sys.argv
+byinst = "--by-inst" in sys.argv     # rank by warp instructions executed instead
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
@@ -45,5 +46,5 @@ for r in rows:
 tot = sum(v[0] for v in agg.values())
 print(f"total samples {tot}; by reason:",
       ", ".join(f"{k} {100*v/max(1,sum(reasons.values())):.1f}%" for k, v in sorted(reasons.items(), key=lambda kv: -kv[1])[:9]))
-for (f, l), (s, i, src, t3) in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
+for (f, l), (s, i, src, t3) in sorted(agg.items(), key=lambda kv: -kv[1][1 if byinst else 0])[:top]:
     print(f"{100*s/tot:5.1f}% inst{i:10d} {f}:{l:<5d} {src:80s} {t3}")
