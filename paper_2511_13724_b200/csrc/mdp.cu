@@ -569,6 +569,34 @@ __device__ __forceinline__ void index_to_split(uint32_t i, uint32_t& a, uint32_t
     b = i - a * (a + 1) / 2;
 }
 
+// The pair table of a grid step (every CTA of mdp_sweep_pairs copies it into
+// shared memory): row a (p_E = 100 - a g) holds positions b = 0..a (p_A = b g,
+// p_D = (a - b) g) at enumeration index a(a+1)/2 + b (R-M9); pair (b, a - b) for
+// b <= a / 2.  x = row offset of p_A=b | of p_D=a-b << 12 | p_E row << 24,
+// y = index of (b, a - b) | index of (a - b, b) << 16.  Rows before a = 2m hold
+// m(m + 1) pairs, before a = 2m + 1: (m + 1)^2.
+// one table per grid step (steps = 100 / g for the 9 divisors g of 100), never
+// rewritten once built: concurrent sweeps on other streams may read them
+constexpr uint32_t kStepSlots = 9;
+__device__ __align__(16) uint2 g_pairs[kStepSlots][kMaxPairs + 1];
+__host__ __device__ constexpr uint32_t step_slot(uint32_t steps) {
+    return steps == 100 ? 0 : steps == 50 ? 1 : steps == 25 ? 2 : steps == 20 ? 3 : steps == 10 ? 4
+         : steps == 5 ? 5 : steps == 4 ? 6 : steps == 2 ? 7 : 8;
+}
+
+__global__ void mdp_pair_table(uint32_t steps, uint32_t n_pairs) {
+    uint2* tab = g_pairs[step_slot(steps)];
+    auto pairs_before = [](uint32_t a) { const uint32_t m = a >> 1; return (a & 1) ? (m + 1) * (m + 1) : m * (m + 1); };
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n_pairs; t += gridDim.x * blockDim.x) {
+        uint32_t a = 2u * (uint32_t)sqrtf((float)t);                 // row of pair t, then exact fix-up
+        while (a > 0 && pairs_before(a) > t) --a;
+        while (pairs_before(a + 1) <= t) ++a;
+        const uint32_t b = t - pairs_before(a), m = a - b, i0 = a * (a + 1) / 2;
+        tab[t] = make_uint2((uint32_t)(b * sizeof(Row)) | (uint32_t)(m * sizeof(Row)) << 12 | (steps - a) << 24,
+                                (i0 + b) | (i0 + m) << 16);
+    }
+}
+
 // The pairs of one profile taken by thread gt of its group (N < 2^31), AoS rows.
 template <bool kGrid>
 __device__ __forceinline__ void aos_pairs(const Row* rows, const uint2* __restrict__ s_pair, uint32_t n_pairs, uint32_t gt,
@@ -618,15 +646,14 @@ mdp_sweep_pairs(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_prof
     // for b <= a / 2.  x = row offset of p_A=b | of p_D=a-b << 12 | p_E row << 24,
     // y = index of (b, a - b) | index of (a - b, b) << 16.
     // rows before a = 2m hold m(m + 1) pairs, before a = 2m + 1: (m + 1)^2
-    auto pairs_before = [](uint32_t a) { const uint32_t m = a >> 1; return (a & 1) ? (m + 1) * (m + 1) : m * (m + 1); };
-    for (uint32_t t = threadIdx.x; t < n_pairs; t += blockDim.x) {
-        uint32_t a = 2u * (uint32_t)sqrtf((float)t);                 // row of pair t, then exact fix-up
-        while (a > 0 && pairs_before(a) > t) --a;
-        while (pairs_before(a + 1) <= t) ++a;
-        const uint32_t base = pairs_before(a);                      // row a holds pairs base .. base + a/2
-        const uint32_t b = t - base, m = a - b, i0 = a * (a + 1) / 2;
-        s_pair[t] = make_uint2((uint32_t)(b * sizeof(Row)) | (uint32_t)(m * sizeof(Row)) << 12 | (steps - a) << 24,
-                               (i0 + b) | (i0 + m) << 16);
+    // (built once per device and grid step by mdp_pair_table into g_pairs; copied
+    // here with 16-B loads)
+    {
+        const uint2* tab = g_pairs[step_slot(steps)];
+        const uint4* src = reinterpret_cast<const uint4*>(tab);
+        uint4* dst = reinterpret_cast<uint4*>(s_pair);
+        for (uint32_t t = threadIdx.x; t < n_pairs / 2; t += blockDim.x) dst[t] = src[t];
+        if ((n_pairs & 1u) && threadIdx.x == 0) s_pair[n_pairs - 1] = tab[n_pairs - 1];
     }
     __syncthreads();
     Row* rows = s_rows[gid];
@@ -1024,6 +1051,20 @@ extern "C" seneca_status seneca_mdp_sweep(const seneca_mdp_profile* d_profiles, 
             SENECA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mdp_sweep_pairs, kThreads,
                                                                           kMaxPairs * sizeof(uint2)));
             pslots = sms * (per_sm > 0 ? per_sm : 1);
+        }
+        {   // the pair table of this grid step on this device (stream-ordered before the sweep)
+            static uint16_t built[64] = {};                         // bit step_slot per device
+            int dev = 0;
+            SENECA_CUDA_TRY(cudaGetDevice(&dev));
+            const uint16_t bit = (uint16_t)(1u << step_slot(steps));
+            if (dev < 0 || dev >= 64 || !(built[dev] & bit)) {
+                // first use of this grid step on this device: built once, synchronously,
+                // so that a sweep on any other stream finds it complete
+                mdp_pair_table<<<(np + 255) / 256, 256, 0, (cudaStream_t)stream>>>(steps, np);
+                SENECA_CUDA_TRY(cudaGetLastError());
+                SENECA_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+                if (dev >= 0 && dev < 64) built[dev] |= bit;
+            }
         }
         const uint32_t want = (n_profiles + kGroups - 1) / kGroups;
         uint32_t blocks = want < (uint32_t)pslots ? want : (uint32_t)pslots;
