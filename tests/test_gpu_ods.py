@@ -817,3 +817,40 @@ def test_storage_list_walk_random_static_configs(block):
         torch.cuda.synchronize()
         assert total == o.replay_epochs(max(target)), (n, batch, target, ce, cd)
         compare_state(o, g, tr)
+
+
+@pytest.mark.parametrize("block", range(2))
+def test_late_bulk_with_arrivals_departures_and_launch_cuts(block):
+    """The late bulk: an uncoupled job's late rounds decided in one
+    pass while warp 0 advances the schedule in closed form.  Static tiers (so the
+    bulk applies), jobs arriving at random rounds and departing after different
+    epoch counts (spans of the closed-form skip cut at arrivals, departures inside
+    them), mixed batches, replays cut into launches of random length (bulk spans
+    end at launch edges), vs the oracle transcript, counters and state."""
+    st = synth.Stream(9700 + block)
+    for it in range(10):
+        n = int(st.choice(1, [300, 1000, 16385, 40000])[0])
+        J = int(st.choice(1, [2, 3, 4])[0])
+        batch = [int(x) for x in st.choice(J, [7, 32, 100, 256])]
+        target = [int(x) for x in st.choice(J, [1, 2, 3])]
+        ce = int(n * float(st.uniform(1)[0]) * 0.5)
+        cd = int((n - ce) * float(st.uniform(1)[0]) * 0.3) if it % 2 else 0
+        arr = [0] + [int(st.u64(1)[0] % np.uint64(60)) for _ in range(J - 1)]
+        seed = int(st.u64(1)[0])
+        o = O.ODS(n, batch, target, ce, cd, 0, seed, transcript=True, arrival=arr)
+        g = P.ODSContext(n, batch, target, ce, cd, 0, seed, arrival=arr)
+        tr = g.new_transcript()
+        total = 0
+        while True:                                       # (pending arrivals are not in active_mask)
+            k = int(st.u64(1)[0] % np.uint64(300)) + 1
+            try:
+                done = g.replay_rounds(k, tr)
+            except S.SenecaError as ex:                   # the last launch ended exactly at the end
+                assert ex.status == S.ESTATE
+                break
+            total += done
+            if done < k:
+                break
+        torch.cuda.synchronize()
+        assert total == o.replay_epochs(max(target)), (n, batch, target, ce, cd, arr)
+        compare_state(o, g, tr)
