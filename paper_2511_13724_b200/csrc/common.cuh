@@ -118,7 +118,10 @@ __device__ __forceinline__ uint32_t perm_apply(uint64_t key, const PermDomain& d
 // ---------------------------------------------------------------- block scan
 // Exclusive scan of one uint32 per thread across the block (blockDim.x a
 // multiple of 32, <= 1024).  scratch: 33 uint32 of shared memory.  Every
-// thread must call it; it ends with a barrier so scratch can be reused.
+// thread must call it; it ends with a barrier so scratch can be reused
+// (kTail = false: no trailing barrier -- the caller's next barrier must come
+// before scratch is written again).
+template <bool kTail = true>
 __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* total, uint32_t* scratch) {
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     const uint32_t nwarps = blockDim.x >> 5;
@@ -144,7 +147,7 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* t
     __syncthreads();
     const uint32_t res = scratch[warp] + incl - v;
     if (total) *total = scratch[32];
-    __syncthreads();
+    if (kTail) __syncthreads();
     return res;
 }
 

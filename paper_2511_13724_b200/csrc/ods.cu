@@ -65,6 +65,9 @@ constexpr uint32_t kMaxBatch = 4096;
 #define SENECA_BULK_MIN 1           // fewest rounds worth a bulk pass
 #endif
 constexpr uint32_t kBulkMin = SENECA_BULK_MIN;
+#ifndef SENECA_HOIST_KEYS
+#define SENECA_HOIST_KEYS 1         // substitution keys and rank domains derived once per round and tier
+#endif
 #ifndef SENECA_EMPTY_POOLS_FAST
 #define SENECA_EMPTY_POOLS_FAST 1    // skip the classification gathers when every pool of the job is empty
 #endif
@@ -342,11 +345,23 @@ __device__ void prefix_from_smem(const Cfg& C, const uint32_t* s_sup_pool, uint3
     const uint32_t lo = threadIdx.x * per;
     const uint32_t hi = min(lo + per, C.NS);
     uint32_t sum = 0;
-    for (uint32_t k = lo; k < hi; ++k) sum += s_sup_pool[k];
-    uint32_t run = block_exclusive_scan(sum, nullptr, scratch);
-    for (uint32_t k = lo; k < hi; ++k) {
-        s_pre_pool[k] = run;
-        run += s_sup_pool[k];
+    if (per <= 8) {                          // (ImageNet-22K: 3,467 superblocks, 7 per thread) counts in registers
+        uint32_t v[8];
+#pragma unroll
+        for (uint32_t k = 0; k < 8; ++k) { v[k] = lo + k < hi ? s_sup_pool[lo + k] : 0u; sum += v[k]; }
+        uint32_t run = block_exclusive_scan<false>(sum, nullptr, scratch);   // the barrier below ends it
+#pragma unroll
+        for (uint32_t k = 0; k < 8; ++k) {
+            if (lo + k < hi) s_pre_pool[lo + k] = run;
+            run += v[k];
+        }
+    } else {
+        for (uint32_t k = lo; k < hi; ++k) sum += s_sup_pool[k];
+        uint32_t run = block_exclusive_scan<false>(sum, nullptr, scratch);
+        for (uint32_t k = lo; k < hi; ++k) {
+            s_pre_pool[k] = run;
+            run += s_sup_pool[k];
+        }
     }
     __syncthreads();
 }
@@ -475,6 +490,8 @@ struct JobSmem {
     uint32_t cur_buf, nxt_buf, cursor, cur_len, nxt_len;
     uint32_t wrap_slot, need, newcursor, walk_err;
     uint32_t m, k[3], tot[3], hits[3];
+    unsigned long long key[3];               // this round's substitution key per tier (A, D, E)
+    PermDomain dom[3];                       // and rank domain of the pool after the hits
     uint32_t hits_loc[3], own[3], glob[3];   // sharded: hits / substitutes in this shard's range, global pool sizes
     uint32_t cnt[kMaxShards][3];             // sharded: every shard's pool sizes of this round (C1)
     uint32_t recount;
@@ -1093,7 +1110,9 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
                 L.dbg[1] = (uint32_t)r; L.dbg[2] = S.tot[0]; L.dbg[3] = S.hits[0];
                 atomicOr(L.err, 8u);                      // a pool total below its hits (diagnostic)
             }
+#if !SENECA_HOIST_KEYS
             S.tot[0] = pa; S.tot[1] = pd; S.tot[2] = pe;
+#endif                                                    // (else: the hits leave S.tot at the round end)
         }
         const uint32_t m = mbase;
         S.m = m;
@@ -1101,6 +1120,16 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
         S.k[1] = C.baseline ? 0u : min(m - S.k[0], pd);
         S.k[2] = C.baseline ? 0u : min(m - S.k[0] - S.k[1], pe);
     }
+#if SENECA_HOIST_KEYS
+    // meanwhile, lane 0 of warps 1-3: the key and the rank domain of tier tt for
+    // this round (every substituting thread derived them itself before; the same
+    // values -- derive_key(seed, SUB, j, r, t) and the pool size after the hits)
+    if (!kSh && (tid & 31) == 0 && tid >= 32 && tid <= 96) {
+        const uint32_t tt = (tid >> 5) - 1;
+        S.key[tt] = derive_key(L.seed, PUR_SUB, j, r, tt == 0 ? T_A : (tt == 1 ? T_D : T_E));
+        S.dom[tt] = perm_domain(S.tot[tt] - S.hits[tt]);
+    }
+#endif
     __syncthreads();
     TM.tick(1);
 
@@ -1115,8 +1144,13 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
             const uint32_t tt = u < k0 ? 0u : (u < k0 + k1 ? 1u : 2u);
             const uint32_t ul = u - (tt == 0 ? 0u : (tt == 1 ? k0 : k0 + k1));
             const uint32_t t = tt == 0 ? T_A : (tt == 1 ? T_D : T_E);
+#if SENECA_HOIST_KEYS
+            const uint32_t rank = kSh ? perm_apply(derive_key(L.seed, PUR_SUB, j, r, t), perm_domain(S.glob[tt]), ul)
+                                      : perm_apply(S.key[tt], S.dom[tt], ul);
+#else
             const uint64_t key = derive_key(L.seed, PUR_SUB, j, r, t);
             const uint32_t rank = perm_apply(key, perm_domain(kSh ? S.glob[tt] : S.tot[tt]), ul);
+#endif
             if constexpr (kSh) {
                 // the shard whose range holds global rank `rank` resolves it and
                 // stores the id into every shard's mailbox (C2)
@@ -1201,9 +1235,15 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
             S.tot[0] -= S.own[0]; S.tot[1] -= S.own[1]; S.tot[2] -= S.own[2];
             S.own[0] = S.own[1] = S.own[2] = 0;
         } else {
+#if SENECA_HOIST_KEYS
+            S.tot[0] -= S.hits[0] + k0;
+            S.tot[1] -= S.hits[1] + k1;
+            S.tot[2] -= S.hits[2] + k2;
+#else
             S.tot[0] -= k0;
             S.tot[1] -= k1;
             S.tot[2] -= k2;
+#endif
         }
     }
 
