@@ -757,225 +757,12 @@ mdp_sweep_pairs(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_prof
     }
 }
 
-// The pairs of one profile taken by consumer thread tid of stride threads (N <
-// 2^31), values into the shared staging row (the arithmetic of aos_pairs).  A
-// thread meets at most one pair per row (stride >= 51) and i0 <= i1, so its
-// indices only increase: strict > keeps the first maximum (R-M8).
-__device__ __forceinline__ void stage_pairs(const Row* rows, const uint2* __restrict__ s_pair, uint32_t n_pairs,
-                                            uint32_t tid, uint32_t stride, uint32_t N, double dN, double y, double dsiE,
-                                            double dsiS, double* srow, double& best, uint32_t& best_i) {
-    const char* rb0 = reinterpret_cast<const char*>(rows);
-#pragma unroll (kPUnroll)
-    for (uint32_t t = tid; t < n_pairs; t += stride) {
-        const uint2 w = s_pair[t];
-        const Row& rb = *reinterpret_cast<const Row*>(rb0 + (w.x & 0xfffu));
-        const Row& rm = *reinterpret_cast<const Row*>(rb0 + ((w.x >> 12) & 0xfffu));
-        const Row& re = rows[w.x >> 24];
-        const uint32_t sum = rb.capc + rm.capc;             // <= 2N < 2^32
-        const bool dfree = sum <= N;                        // Eq. 6 unclamped (both splits)
-        const uint32_t r2 = dfree ? N - sum : 0u;
-        const uint32_t cE = re.cape;
-        const bool efree = dfree && cE <= r2;               // Eq. 7 unclamped
-        const uint32_t x = efree ? r2 - cE : r2;            // N_S, or the clamped N_E (0 if D clamped)
-        const double q = div_by_n(u32_to_d(x), dN, y);
-        const double prod = __dmul_rn(q, efree ? dsiS : dsiE);
-        const double tX = efree ? re.tE : 0.0;
-        const double v0 = __dadd_rn(__dadd_rn(__dadd_rn(rb.tA, dfree ? rm.tD : rb.tDc), tX), prod);
-        const double v1 = __dadd_rn(__dadd_rn(__dadd_rn(rm.tA, dfree ? rb.tD : rm.tDc), tX), prod);
-        const uint32_t i0 = w.y & 0xffffu, i1 = w.y >> 16;
-        srow[i0] = v0;
-        srow[i1] = v1;
-        if (v0 > best) { best = v0; best_i = i0; }
-        if (v1 > best) { best = v1; best_i = i1; }
-    }
-}
-
-// ------------------------------------------------------------------ the paired sweep, grid by TMA
-// With the grid requested the sweep is bound by its write pattern as much as by
-// its arithmetic: the paired sweep's 8-B stores (i0 ascending, i1 descending,
-// 1,776 profile rows in flight) reach ~4.1 TB/s on B200, while whole rows
-// written by one bulk copy each from 444 CTAs reach ~5.9 (10 k rows) / 6.2 TB/s
-// (100 k rows) (tools/micro/store_pattern.cu).  Here one CTA
-// sweeps one profile at a time, warp-specialised so that no warp waits for the
-// serial per-profile work:
-//   warps 6, 7 (producers, one per row buffer: warp 6 the even profiles of the
-//                        CTA, warp 7 the odd ones) load a profile, derive
-//                        Eqs. 1-4 and build its 101 rows, one profile ahead;
-//   warps 0-5 (consumers) take the pairs of profile i exactly as
-//                        mdp_sweep_pairs does (stage_pairs: the same operations
-//                        on the same operands), into a shared-memory copy of the
-//                        profile's grid row; consumer thread 0 then writes the
-//                        row with one cp.async.bulk (TMA) store -- 16-B aligned
-//                        middle, the 8-B head or tail element by a plain store --
-//                        which drains while the next profile is swept.
-// Named barriers: FULL[b] (producer arrives, consumers wait), EMPTY[b]
-// (consumers arrive, producer waits), one among the consumers.  The staging row
-// is rewritten only after the previous copy has read it
-// (cp.async.bulk.wait_group.read).
 #ifndef SENECA_MDP_GRID_CTAS
 #define SENECA_MDP_GRID_CTAS 0    // > 0: at most this many mdp_sweep_pairs CTAs per SM when it writes the grid
 #endif
-#ifndef SENECA_MDP_TMA
-#define SENECA_MDP_TMA 0          // 1: the grid by mdp_sweep_ws; 0: mdp_sweep_pairs writes it (A/B knob)
-#endif
-constexpr uint32_t kWsConsumers = kThreads - 64;                  // warps 0-5; warps 6, 7 produce
-__host__ __device__ constexpr uint32_t ws_smem_bytes(uint32_t n_pairs, uint32_t n_splits) {
-    return ((n_splits + 2u) * 8u + 15u) / 16u * 16u + n_pairs * 8u;   // staging row (+ head slot) | pair table
-}
-__device__ __forceinline__ void nb_sync(uint32_t id, uint32_t n) { asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(n) : "memory"); }
-__device__ __forceinline__ void nb_arrive(uint32_t id, uint32_t n) { asm volatile("bar.arrive %0, %1;" :: "r"(id), "r"(n) : "memory"); }
-
-struct WsHdr {
-    Hdr h;
-    uint64_t N, Xad, Dad, De, cache_bytes;   // what the 64-bit path recomputes the capacities from
-};
-
-__global__ void __launch_bounds__(kThreads, SENECA_MDP_MINB)
-mdp_sweep_ws(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_profiles, uint32_t g,
-             uint32_t steps, uint32_t n_splits, uint32_t n_pairs, seneca_mdp_result* __restrict__ results,
-             double* __restrict__ grid) {
-    constexpr uint32_t kCWarps = kWsConsumers / 32;
-    constexpr uint32_t BAR_FULL = 1, BAR_EMPTY = 3, BAR_CONS = 5;  // FULL 1-2, EMPTY 3-4, consumers 5
-    __shared__ Row s_rows[2][kMaxSteps];
-    __shared__ WsHdr s_h[2];
-    __shared__ double s_red_v[kCWarps];
-    __shared__ uint32_t s_red_i[kCWarps];
-    extern __shared__ __align__(16) unsigned char s_dyn[];
-    double* s_row = reinterpret_cast<double*>(s_dyn);                                  // [n_splits + 2]
-    uint2* s_pair = reinterpret_cast<uint2*>(s_dyn + ((n_splits + 2u) * 8u + 15u) / 16u * 16u);
-    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    {   // the pair table of this grid step (built once per device by mdp_pair_table)
-        const uint2* tab = g_pairs[step_slot(steps)];
-        const uint4* src = reinterpret_cast<const uint4*>(tab);
-        uint4* dst = reinterpret_cast<uint4*>(s_pair);
-        for (uint32_t t = tid; t < n_pairs / 2; t += blockDim.x) dst[t] = src[t];
-        if ((n_pairs & 1u) && tid == 0) s_pair[n_pairs - 1] = tab[n_pairs - 1];
-    }
-    __syncthreads();
-    const uint32_t G = gridDim.x;
-    constexpr uint32_t kBarN = kWsConsumers + 32;                  // consumers + one producer warp
-    if (warp >= kCWarps) {
-        // ---------------- producer b: Eqs. 1-4 and the rows of the CTA's profiles it = b, b + 2, ...
-        const uint32_t b = warp - kCWarps;
-        uint32_t it = b;
-        for (uint32_t pi = blockIdx.x + b * G; pi < n_profiles; pi += 2 * G, it += 2) {
-            if (it >= 2) nb_sync(BAR_EMPTY + b, kBarN);             // profile it-2 swept: buffer b free
-            const seneca_mdp_profile prof = profiles[pi];
-            const Hdr h = warp_header(prof);
-            if (h.valid) {                                          // warp-uniform
-                Header B;
-                for (int t = 0; t < 4; ++t) B.dsi[t] = h.dsi[t];
-                B.N = prof.n_total;
-                B.Xad = prof.cache_bytes * prof.m_den;
-                B.Dad = 100ull * prof.m_num * prof.s_data;
-                B.De = 100ull * prof.s_data;
-                B.cache_bytes = prof.cache_bytes;
-                B.rDad = __drcp_rn(u2d(B.Dad));
-                B.rDe = __drcp_rn(u2d(B.De));
-                for (uint32_t k0 = 0; k0 <= steps; k0 += 32) build_rows(B, k0, g, steps, s_rows[b]);
-                if (lane == 0) {
-                    s_h[b].N = B.N; s_h[b].Xad = B.Xad; s_h[b].Dad = B.Dad; s_h[b].De = B.De; s_h[b].cache_bytes = B.cache_bytes;
-                }
-            }
-            if (lane == 0) s_h[b].h = h;
-            __syncwarp();
-            nb_arrive(BAR_FULL + b, kBarN);                         // rows and header of profile `it` ready
-        }
-        return;
-    }
-    // ---------------- consumers: the pairs of each profile, the row by one bulk copy
-    uint32_t it = 0;
-    for (uint32_t pi = blockIdx.x; pi < n_profiles; pi += G, ++it) {
-        const uint32_t b = it & 1u;
-        nb_sync(BAR_FULL + b, kBarN);
-        const Hdr H = s_h[b].h;
-        double best = __longlong_as_double(0xfff0000000000000ll);
-        uint32_t best_i = 0xffffffffu;
-        double* grow = grid + (uint64_t)pi * n_splits;
-        const uint32_t h = (uint32_t)(reinterpret_cast<uintptr_t>(grow) >> 3) & 1u;  // row starts 8 mod 16
-        if (H.valid) {                                              // CTA-uniform
-            if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // staging row free
-            nb_sync(BAR_CONS, kWsConsumers);
-            double* srow = s_row + h;                               // value i at s_row[h + i]: 16-B aligned with grow
-            const uint64_t N = s_h[b].N;
-            const Row* rows = s_rows[b];
-            if (N < (1ull << 31)) {
-                const double dN = u2d(N), y = __drcp_rn(dN);
-                stage_pairs(rows, s_pair, n_pairs, tid, kWsConsumers, (uint32_t)N, dN, y, H.dsi[2], H.dsi[3], srow,
-                            best, best_i);
-            } else {                                                // N >= 2^31: 64-bit counts (rare)
-                const uint64_t Xad = s_h[b].Xad, Dad = s_h[b].Dad, DeE = s_h[b].De, cb = s_h[b].cache_bytes;
-                const double dN = u2d(N);
-                auto capc = [&](uint32_t k) { const uint64_t c = ((uint64_t)k * g * Xad) / Dad; return c < N ? c : N; };
-                auto cape = [&](uint32_t k) { const uint64_t c = ((uint64_t)k * g * cb) / DeE; return c < N ? c : N; };
-                for (uint32_t t = tid; t < n_pairs; t += kWsConsumers) {
-                    const uint2 w = s_pair[t];
-                    for (int hh = 0; hh < 2; ++hh) {
-                        const uint32_t ka = (hh ? (w.x >> 12) & 0xfffu : w.x & 0xfffu) / sizeof(Row);
-                        const uint32_t kd = (hh ? w.x & 0xfffu : (w.x >> 12) & 0xfffu) / sizeof(Row);
-                        const uint32_t ke = w.x >> 24, idx = hh ? w.y >> 16 : w.y & 0xffffu;
-                        const uint64_t r1 = N - capc(ka);
-                        const uint64_t cD = capc(kd);
-                        const bool dfree = cD <= r1;
-                        const uint64_t r2 = dfree ? r1 - cD : 0ull;
-                        const uint64_t cE = cape(ke);
-                        const bool efree = dfree && cE <= r2;
-                        const uint64_t x = efree ? r2 - cE : r2;
-                        const double prod = __dmul_rn(__ddiv_rn(u2d(x), dN), efree ? H.dsi[3] : H.dsi[2]);
-                        const double tD = dfree ? rows[kd].tD : rows[ka].tDc;
-                        const double tX = efree ? rows[ke].tE : 0.0;
-                        const double v = __dadd_rn(__dadd_rn(__dadd_rn(rows[ka].tA, tD), tX), prod);
-                        srow[idx] = v;
-                        if (v > best || (v == best && idx < best_i)) { best = v; best_i = idx; }
-                    }
-                }
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic-proxy writes -> the bulk copy
-        }
-        // argmax: the maximum by butterfly, then the smallest index holding it (R-M8)
-        double mx = best;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        best_i = __reduce_min_sync(0xffffffffu, best == mx ? best_i : 0xffffffffu);
-        if (lane == 0) { s_red_v[warp] = mx; s_red_i[warp] = best_i; }
-        nb_sync(BAR_CONS, kWsConsumers);                            // the staged row and the per-warp maxima complete
-        if (pi + 2 * G < n_profiles) nb_arrive(BAR_EMPTY + b, kBarN);      // rows b free for profile it + 2
-        if (tid == 0) {
-            seneca_mdp_result r = {};
-            if (!H.valid) {
-                r.status = 1;
-            } else {
-                const uint32_t nb = (n_splits - h) / 2u * 16u;      // 16-B aligned middle
-                const uint32_t sa = (uint32_t)__cvta_generic_to_shared(s_row + 2u * h);
-                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
-                             :: "l"(grow + h), "r"(sa), "r"(nb) : "memory");
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                if (h) grow[0] = s_row[1];                          // the 8-B head
-                if ((n_splits - h) & 1u) grow[n_splits - 1] = s_row[h + n_splits - 1];   // the 8-B tail
-                double bv = s_red_v[0];
-                uint32_t bi = s_red_i[0];
-                for (uint32_t k = 1; k < kCWarps; ++k) {
-                    const double ov = s_red_v[k];
-                    const uint32_t oi = s_red_i[k];
-                    if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-                }
-                uint32_t ra, rb;
-                index_to_split(bi, ra, rb);
-                r.p_e = (uint8_t)(100 - ra * g);
-                r.p_d = (uint8_t)((ra - rb) * g);
-                r.p_a = (uint8_t)(rb * g);
-                r.lim_a = H.lim[0]; r.lim_d = H.lim[1]; r.lim_e = H.lim[2]; r.lim_s = H.lim[3];
-                r.status = 0;
-                r.v_best = bv;
-                r.dsi_a = H.dsi[0]; r.dsi_d = H.dsi[1]; r.dsi_e = H.dsi[2]; r.dsi_s = H.dsi[3];
-            }
-            results[pi] = r;
-        }
-        // the per-warp maxima are rewritten after the next profile's consumer
-        // barrier, which thread 0 reaches only after reading them
-    }
-    if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-}
+// (Two TMA-staged grid kernels -- whole profile rows written by one cp.async.bulk
+// store each -- were built and measured slower than this sweep, DESIGN.md 7.3;
+// they are in the history at commit 40d95f7.)
 
 // ------------------------------------------------------------------ evaluation at given splits
 constexpr uint32_t kMaxEvalSplits = 4096;
@@ -1085,24 +872,6 @@ extern "C" seneca_status seneca_mdp_sweep(const seneca_mdp_profile* d_profiles, 
                 SENECA_CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
                 if (dev >= 0 && dev < 64) built[dev] |= bit;
             }
-        }
-        if (d_grid && SENECA_MDP_TMA) {
-            static int wslots = 0;
-            if (!wslots) {
-                int dev = 0, sms = 0, per_sm = 0;
-                SENECA_CUDA_TRY(cudaGetDevice(&dev));
-                SENECA_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-                SENECA_CUDA_TRY(cudaFuncSetAttribute(mdp_sweep_ws, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                     (int)ws_smem_bytes(kMaxPairs, 5151)));
-                SENECA_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mdp_sweep_ws, kThreads,
-                                                                              ws_smem_bytes(kMaxPairs, 5151)));
-                wslots = sms * (per_sm > 0 ? per_sm : 1);
-            }
-            const uint32_t wblocks = n_profiles < (uint32_t)wslots ? n_profiles : (uint32_t)wslots;
-            mdp_sweep_ws<<<wblocks, kThreads, ws_smem_bytes(np, ns), (cudaStream_t)stream>>>(
-                d_profiles, n_profiles, grid_step_pct, steps, ns, np, d_results, d_grid);
-            SENECA_CUDA_TRY(cudaGetLastError());
-            return SENECA_OK;
         }
         const uint32_t want = (n_profiles + kGroups - 1) / kGroups;
         uint32_t blocks = want < (uint32_t)pslots ? want : (uint32_t)pslots;
