@@ -579,6 +579,9 @@ __device__ __forceinline__ void index_to_split(uint32_t i, uint32_t& a, uint32_t
 // rewritten once built: concurrent sweeps on other streams may read them
 constexpr uint32_t kStepSlots = 9;
 __device__ __align__(16) uint2 g_pairs[kStepSlots][kMaxPairs + 1];
+// the same pairs for the structure-of-arrays rows (SENECA_MDP_DENSE): x = row
+// index of p_A = b | of p_D = a - b << 8 | of p_E << 16, y as above
+__device__ __align__(16) uint2 g_pairs_dense[kStepSlots][kMaxPairs + 1];
 __host__ __device__ constexpr uint32_t step_slot(uint32_t steps) {
     return steps == 100 ? 0 : steps == 50 ? 1 : steps == 25 ? 2 : steps == 20 ? 3 : steps == 10 ? 4
          : steps == 5 ? 5 : steps == 4 ? 6 : steps == 2 ? 7 : 8;
@@ -594,6 +597,7 @@ __global__ void mdp_pair_table(uint32_t steps, uint32_t n_pairs) {
         const uint32_t b = t - pairs_before(a), m = a - b, i0 = a * (a + 1) / 2;
         tab[t] = make_uint2((uint32_t)(b * sizeof(Row)) | (uint32_t)(m * sizeof(Row)) << 12 | (steps - a) << 24,
                                 (i0 + b) | (i0 + m) << 16);
+        g_pairs_dense[step_slot(steps)][t] = make_uint2(b | m << 8 | (steps - a) << 16, (i0 + b) | (i0 + m) << 16);
     }
 }
 
@@ -631,11 +635,105 @@ __device__ __forceinline__ void aos_pairs(const Row* rows, const uint2* __restri
     }
 }
 
+#ifndef SENECA_MDP_DENSE
+#define SENECA_MDP_DENSE 1        // rows as dense arrays (fewer shared-memory wavefronts per pair) (A/B knob)
+#endif
+// Structure-of-arrays rows of one group: capc u32[104] | cape u32[104] | tA | tD |
+// tDc | tE f64[104] -- a lane reading consecutive rows reads consecutive words
+// (one wavefront for a 4-B field, two for an 8-B one), where the 40-B Row
+// stride costs two for either.
+constexpr uint32_t kDR = 104;
+constexpr uint32_t kDCapc = 0, kDCape = 4 * kDR, kDTA = 8 * kDR, kDTD = 16 * kDR, kDTDC = 24 * kDR, kDTE = 32 * kDR,
+                   kDBytes = 40 * kDR;
+struct DenseRows {
+    char* p;
+    __device__ uint32_t& capc(uint32_t k) const { return reinterpret_cast<uint32_t*>(p + kDCapc)[k]; }
+    __device__ uint32_t& cape(uint32_t k) const { return reinterpret_cast<uint32_t*>(p + kDCape)[k]; }
+    __device__ double& tA(uint32_t k) const { return reinterpret_cast<double*>(p + kDTA)[k]; }
+    __device__ double& tD(uint32_t k) const { return reinterpret_cast<double*>(p + kDTD)[k]; }
+    __device__ double& tDc(uint32_t k) const { return reinterpret_cast<double*>(p + kDTDC)[k]; }
+    __device__ double& tE(uint32_t k) const { return reinterpret_cast<double*>(p + kDTE)[k]; }
+};
+
+// Rows k0 .. k0+31 (one per lane) of a valid profile, dense layout (the same
+// values as build_rows).
+__device__ void build_rows_dense(const Header& H, uint32_t k0, uint32_t g, uint32_t steps, DenseRows R) {
+    const uint32_t k = k0 + (threadIdx.x & 31);
+    if (k > steps) return;
+    const uint64_t N = H.N;
+    const double dN = u2d(N);
+    const bool exact_div = N < (1ull << 53);
+    const double yN = __drcp_rn(dN);
+    const uint64_t pct = (uint64_t)k * g;
+    uint64_t cad = floor_div(pct * H.Xad, H.Dad, H.rDad), ce = floor_div(pct * H.cache_bytes, H.De, H.rDe);   // Eqs. 5-7, exact floors
+    cad = cad < N ? cad : N;
+    ce = ce < N ? ce : N;
+    const double fa = exact_div ? div_by_n(u2d(cad), dN, yN) : __ddiv_rn(u2d(cad), dN);
+    const double fc = exact_div ? div_by_n(u2d(N - cad), dN, yN) : __ddiv_rn(u2d(N - cad), dN);
+    const double fe = exact_div ? div_by_n(u2d(ce), dN, yN) : __ddiv_rn(u2d(ce), dN);
+    R.capc(k) = (uint32_t)cad;                                       // used only when N < 2^31
+    R.cape(k) = (uint32_t)ce;
+    R.tA(k) = __dmul_rn(fa, H.dsi[0]);
+    R.tD(k) = __dmul_rn(fa, H.dsi[1]);
+    R.tDc(k) = __dmul_rn(fc, H.dsi[1]);
+    R.tE(k) = __dmul_rn(fe, H.dsi[2]);
+}
+
+template <uint32_t kOff>
+__device__ __forceinline__ uint32_t ldsd_u32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1+%2];" : "=r"(v) : "r"(a), "n"(kOff));
+    return v;
+}
+template <uint32_t kOff>
+__device__ __forceinline__ double ldsd_f64(uint32_t a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(a), "n"(kOff));
+    return v;
+}
+
+// The pairs of one profile taken by thread gt of its group (N < 2^31), dense
+// rows at shared address sb: the arithmetic of aos_pairs.
+template <bool kGrid>
+__device__ __forceinline__ void dense_pairs(uint32_t sb, const uint2* __restrict__ s_pair, uint32_t n_pairs, uint32_t gt,
+                                            uint32_t N, double dN, double y, double dsiE, double dsiS,
+                                            double* __restrict__ grow, double& best, uint32_t& best_i) {
+    constexpr uint32_t kDelta = kDTDC - kDTD;
+#pragma unroll (kPUnroll)
+    for (uint32_t t = gt; t < n_pairs; t += kPairW * 32) {
+        const uint2 w = s_pair[t];
+        const uint32_t b = w.x & 0xffu, m = __byte_perm(w.x, 0, 0x4441), e = w.x >> 16;
+        const uint32_t b4 = sb + 4 * b, m4 = sb + 4 * m, b8 = sb + 8 * b, m8 = sb + 8 * m;
+        const uint32_t sum = ldsd_u32<kDCapc>(b4) + ldsd_u32<kDCapc>(m4);   // <= 2N < 2^32
+        const bool dfree = sum <= N;                        // Eq. 6 unclamped (both splits)
+        const uint32_t r2 = dfree ? N - sum : 0u;
+        const uint32_t cE = ldsd_u32<kDCape>(sb + 4 * e);
+        const bool efree = dfree && cE <= r2;               // Eq. 7 unclamped
+        const uint32_t x = efree ? r2 - cE : r2;            // N_S, or the clamped N_E (0 if D clamped)
+        const double q = div_by_n(u32_to_d(x), dN, y);
+        const double prod = __dmul_rn(q, efree ? dsiS : dsiE);
+        const double tX = efree ? ldsd_f64<kDTE>(sb + 8 * e) : 0.0;
+        // Eq. 6: tD of the other coordinate when D is free, else tDc of this one
+        const double d0 = ldsd_f64<kDTDC>(dfree ? m8 - kDelta : b8);
+        const double d1 = ldsd_f64<kDTDC>(dfree ? b8 - kDelta : m8);
+        const double v0 = __dadd_rn(__dadd_rn(__dadd_rn(ldsd_f64<kDTA>(b8), d0), tX), prod);
+        const double v1 = __dadd_rn(__dadd_rn(__dadd_rn(ldsd_f64<kDTA>(m8), d1), tX), prod);
+        const uint32_t i0 = w.y & 0xffffu, i1 = w.y >> 16;
+        if (kGrid) { st_grid(grow + i0, v0); st_grid(grow + i1, v1); }
+        if (v0 > best) { best = v0; best_i = i0; }
+        if (v1 > best) { best = v1; best_i = i1; }
+    }
+}
+
 __global__ void __launch_bounds__(kThreads, SENECA_MDP_MINB)
 mdp_sweep_pairs(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_profiles, uint32_t g,
                 uint32_t steps, uint32_t n_splits, uint32_t n_pairs, seneca_mdp_result* __restrict__ results,
                 double* __restrict__ grid) {
+#if SENECA_MDP_DENSE
+    __shared__ __align__(16) char s_drows[kGroups][kDBytes];
+#else
     __shared__ Row s_rows[kGroups][kMaxSteps];
+#endif
     __shared__ double s_red_v[kGroups][kPairW];
     __shared__ uint32_t s_red_i[kGroups][kPairW];
     extern __shared__ uint2 s_pair[];                               // [n_pairs]
@@ -649,14 +747,22 @@ mdp_sweep_pairs(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_prof
     // (built once per device and grid step by mdp_pair_table into g_pairs; copied
     // here with 16-B loads)
     {
+#if SENECA_MDP_DENSE
+        const uint2* tab = g_pairs_dense[step_slot(steps)];
+#else
         const uint2* tab = g_pairs[step_slot(steps)];
+#endif
         const uint4* src = reinterpret_cast<const uint4*>(tab);
         uint4* dst = reinterpret_cast<uint4*>(s_pair);
         for (uint32_t t = threadIdx.x; t < n_pairs / 2; t += blockDim.x) dst[t] = src[t];
         if ((n_pairs & 1u) && threadIdx.x == 0) s_pair[n_pairs - 1] = tab[n_pairs - 1];
     }
     __syncthreads();
+#if SENECA_MDP_DENSE
+    const DenseRows DR{s_drows[gid]};
+#else
     Row* rows = s_rows[gid];
+#endif
     const uint32_t n_groups = gridDim.x * kGroups;
     for (uint32_t pi = blockIdx.x * kGroups + gid; pi < n_profiles; pi += n_groups) {
         const seneca_mdp_profile prof = profiles[pi];
@@ -685,13 +791,23 @@ mdp_sweep_pairs(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_prof
             B.cache_bytes = prof.cache_bytes;
             B.rDad = __drcp_rn(u2d(B.Dad));
             B.rDe = __drcp_rn(u2d(B.De));
+#if SENECA_MDP_DENSE
+            for (uint32_t k0 = gw * 32; k0 <= steps; k0 += kPairW * 32) build_rows_dense(B, k0, g, steps, DR);
+#else
             for (uint32_t k0 = gw * 32; k0 <= steps; k0 += kPairW * 32) build_rows(B, k0, g, steps, rows);
+#endif
             group_sync(gid);
             double* grow = grid ? grid + (uint64_t)pi * n_splits : nullptr;
             if (B.N < (1ull << 31)) {
                 const double dN = u2d(B.N), y = __drcp_rn(dN);
+#if SENECA_MDP_DENSE
+                const uint32_t sb = (uint32_t)__cvta_generic_to_shared(DR.p);
+                if (grow) dense_pairs<true>(sb, s_pair, n_pairs, gt, (uint32_t)B.N, dN, y, H.dsi[2], H.dsi[3], grow, best, best_i);
+                else dense_pairs<false>(sb, s_pair, n_pairs, gt, (uint32_t)B.N, dN, y, H.dsi[2], H.dsi[3], nullptr, best, best_i);
+#else
                 if (grow) aos_pairs<true>(rows, s_pair, n_pairs, gt, (uint32_t)B.N, dN, y, H.dsi[2], H.dsi[3], grow, best, best_i);
                 else aos_pairs<false>(rows, s_pair, n_pairs, gt, (uint32_t)B.N, dN, y, H.dsi[2], H.dsi[3], nullptr, best, best_i);
+#endif
             } else {                                                // N >= 2^31: 64-bit counts (rare)
                 const uint64_t N = B.N;
                 const double dN = u2d(N);
@@ -700,9 +816,23 @@ mdp_sweep_pairs(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_prof
                 for (uint32_t t = gt; t < n_pairs; t += kPairW * 32) {
                     const uint2 w = s_pair[t];
                     for (int h = 0; h < 2; ++h) {
+#if SENECA_MDP_DENSE
+                        const uint32_t kb = w.x & 0xffu, km = (w.x >> 8) & 0xffu;
+                        const uint32_t ka = h ? km : kb, kd = h ? kb : km, ke = w.x >> 16;
+                        const auto row_tA = [&](uint32_t k) { return DR.tA(k); };
+                        const auto row_tD = [&](uint32_t k) { return DR.tD(k); };
+                        const auto row_tDc = [&](uint32_t k) { return DR.tDc(k); };
+                        const auto row_tE = [&](uint32_t k) { return DR.tE(k); };
+#else
                         const uint32_t ka = (h ? (w.x >> 12) & 0xfffu : w.x & 0xfffu) / sizeof(Row);
                         const uint32_t kd = (h ? w.x & 0xfffu : (w.x >> 12) & 0xfffu) / sizeof(Row);
-                        const uint32_t ke = w.x >> 24, idx = h ? w.y >> 16 : w.y & 0xffffu;
+                        const uint32_t ke = w.x >> 24;
+                        const auto row_tA = [&](uint32_t k) { return rows[k].tA; };
+                        const auto row_tD = [&](uint32_t k) { return rows[k].tD; };
+                        const auto row_tDc = [&](uint32_t k) { return rows[k].tDc; };
+                        const auto row_tE = [&](uint32_t k) { return rows[k].tE; };
+#endif
+                        const uint32_t idx = h ? w.y >> 16 : w.y & 0xffffu;
                         const uint64_t r1 = N - capc(ka);
                         const uint64_t cD = capc(kd);
                         const bool dfree = cD <= r1;
@@ -711,9 +841,9 @@ mdp_sweep_pairs(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_prof
                         const bool efree = dfree && cE <= r2;
                         const uint64_t x = efree ? r2 - cE : r2;
                         const double prod = __dmul_rn(__ddiv_rn(u2d(x), dN), efree ? H.dsi[3] : H.dsi[2]);
-                        const double tD = dfree ? rows[kd].tD : rows[ka].tDc;
-                        const double tX = efree ? rows[ke].tE : 0.0;
-                        const double v = __dadd_rn(__dadd_rn(__dadd_rn(rows[ka].tA, tD), tX), prod);
+                        const double tD = dfree ? row_tD(kd) : row_tDc(ka);
+                        const double tX = efree ? row_tE(ke) : 0.0;
+                        const double v = __dadd_rn(__dadd_rn(__dadd_rn(row_tA(ka), tD), tX), prod);
                         if (grow) __stcs(grow + idx, v);
                         if (v > best || (v == best && idx < best_i)) { best = v; best_i = idx; }
                     }
