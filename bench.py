@@ -551,12 +551,19 @@ def main():
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)      # > 126 MB L2
 
+    fill_ms = []                                                     # the flush's fill_: a pure 512 MiB write
+
     def l2_flush(v):
         # evict L2 by writing 512 MiB, then read the first 256 MiB of it back so that
         # the flush's own dirty lines are written back here, not inside the next timed
         # region (where they would compete with the kernel's own DRAM writes)
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
         flush.fill_(v & 0xFF)
+        f1.record(stream)
         flush[: 256 << 20].max()
+        f1.synchronize()
+        fill_ms.append(f0.elapsed_time(f1))
 
     def barrier():
         if world > 1:
@@ -890,6 +897,14 @@ def main():
                                     "bytes (DESIGN.md 7.1)")
     mdp_roof = roofline_for("mdp_sweep", kernels["mdp_sweep"], info, hbm_peak, peak_src,
                             ncu_traffic(tkey["mdp_sweep"]))
+    if fill_ms:
+        # context: the sweep's own bytes are almost all grid writes; a pure write on this GPU
+        # (the L2 flush's 512 MiB fill_, timed live, best of the run) is the write-only ceiling
+        wr_gbs = (512 << 20) / (min(fill_ms) / 1e3) / 1e9
+        mdp_roof["write_only_ceiling"] = dict(gbs=wr_gbs, frac=mdp_roof["achieved"] / wr_gbs,
+                                              source="torch fill_ of the 512 MiB L2-flush buffer, CUDA events")
+        if mdp_large:
+            mdp_large["roofline"]["write_only_ceiling"] = dict(gbs=wr_gbs, frac=mdp_large["roofline"]["achieved"] / wr_gbs)
     for name in kernels:
         kernels[name]["algorithmic_bytes_per_launch"] = algorithmic_bytes(name, info)
 
