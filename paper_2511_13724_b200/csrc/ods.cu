@@ -71,9 +71,6 @@ constexpr uint32_t kBulkMin = SENECA_BULK_MIN;
 #ifndef SENECA_EMPTY_POOLS_FAST
 #define SENECA_EMPTY_POOLS_FAST 1    // skip the classification gathers when every pool of the job is empty
 #endif
-#ifndef SENECA_FAST_INTAKE
-#define SENECA_FAST_INTAKE 1         // coupled rounds: refill counts in the release word, speculated refills'
-#endif                               // seen flags read before the release, evictions and refills in one pass
 #ifndef SENECA_ODS_THREADS
 #define SENECA_ODS_THREADS 512
 #endif
@@ -163,10 +160,7 @@ struct Lay {
     uint32_t *verr;                  // caller-supplied request validation flag (control block)
     uint32_t *dbg;                   // [4] first consistency failure: site | pool, rank / round, ... (control block)
     uint32_t *bar;                   // [4] signals: u64 {job phases done | evictions pushed << 32},
-                                     //     (unused), eviction ring position (control block)
-    uint32_t *rel;                   // u64 release of maintain: rounds applied | packed refill split << 32
-    uint32_t *spec;                  // [2] u64 per round parity: speculated refills kspec << 32 | iteration + 1
-    uint32_t *sig;                   // [J] u64 per job: evictions pushed this round << 32 | last iteration + 1
+                                     //     maintain rounds applied, eviction ring position (control block)
     unsigned long long *phase;       // [32] accumulated cycles per phase (see seneca.h)
     uint64_t seed;                   // this replica's seed (cfg seed + replica index)
     // sample-ID-range sharding: this slice is shard `shard` of G and
@@ -471,22 +465,6 @@ __device__ __forceinline__ unsigned long long ld_acquire64(const uint32_t* p) {
     return v;
 }
 
-// per-job signal words and eviction segments (unsharded coupled rounds)
-#ifndef SENECA_JOB_SIGNALS
-#define SENECA_JOB_SIGNALS 0         // measured slower on ImageNet-1K (DESIGN 7.1): the shared counter stays
-#endif
-template <bool kSh>
-constexpr bool kSig = SENECA_FAST_INTAKE && SENECA_JOB_SIGNALS && !kSh;
-
-// release operations of one thread after a CTA barrier: they publish every write
-// the CTA made before the barrier (cumulativity through bar.sync)
-__device__ __forceinline__ void red_release_add64(uint32_t* p, unsigned long long v) {
-    asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ void st_release64(uint32_t* p, unsigned long long v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
 // ------------------------------------------------------------------ per-CTA phase timer (profiling)
 // kOn = false (the timed replays) compiles every tick out; the kernel with
 // kOn = true is launched only when seneca_profile bit 1 asks for phase counters.
@@ -523,7 +501,6 @@ struct JobSmem {
     uint32_t perm_seen;   // epoch+1 whose permutation was observed published (0: none)
     float dens;           // unseen fraction observed by the last walk step (window sizing)
     uint32_t npush;       // evictions pushed by this job this round
-    uint32_t relpk, prek; // the release word's refill split; speculated refills loaded before it
     uint32_t rep;         // replica of this CTA
     uint32_t warm;        // cold start over (read at the round start, R-O24)
     // prefetch of the next walk window (R-O1 walk, see job_walk_prefetched)
@@ -1057,10 +1034,7 @@ template <bool kSh, class TMr>
 __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& S, uint32_t* s_req, uint32_t* s_miss,
                           uint32_t* s_sub, uint32_t* s_oid, uint8_t* s_osrc, uint32_t* s_pre, uint32_t j, uint64_t r,
                           uint32_t e, uint32_t nbase, uint32_t n_act, TMr& TM, const uint32_t* s_win,
-                          uint4* s_wseen, uint32_t* s_sup, bool have_pc = false, uint32_t pre_cons = 0) {
-    // have_pc: pre_cons is j's consumer word of request tid, loaded before maintain(r-1)
-    // was applied -- exact for every A-resident request (maintain clears consumer bits
-    // only of the ids it evicts, and an evicted id is no longer A-resident)
+                          uint4* s_wseen, uint32_t* s_sup) {
     const uint32_t tid = threadIdx.x, T = blockDim.x;
     const uint32_t need = S.need;
     uint32_t* seen_j = L.seen + (size_t)j * C.NW;
@@ -1092,8 +1066,7 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
             const uint32_t wd = C.cap_d && !none_cached ? ldcg(L.bm_d + w) : 0u;
             const uint32_t we = C.cap_e && !none_cached ? ldcg(L.bm_e + w) : 0u;
             const uint32_t t = (wa & b) ? T_A : (wd & b) ? T_D : (we & b) ? T_E : T_S;
-            const bool hit = (t == T_E || t == T_D ||
-                              (t == T_A && (C.baseline || !(((base == 0 && have_pc) ? pre_cons : ldcg(cons_j + w)) & b))));
+            const bool hit = (t == T_E || t == T_D || (t == T_A && (C.baseline || !(ldcg(cons_j + w) & b))));
             if (hit) {
                 if (P.out_ids) { P.out_ids[row + s] = i; P.out_src[row + s] = (uint8_t)t; }
                 s_oid[s] = i;
@@ -1287,12 +1260,8 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
         if (trow) trow[nbase + s] = ((unsigned long long)src << 32) | i;
         if (s_osrc[s] & kNewCons) {
             if (atomicAdd(L.cons_cnt + i, 1u) + 1u == n_act) {
-                if constexpr (kSig<kSh>) {               // this job's own segment of the ring
-                    L.evict_push[(size_t)j * C.Bmax + atomicAdd(&S.npush, 1u)] = i;
-                } else {
-                    L.evict_push[atomicAdd(L.bar + 3, 1u) % (C.J * C.Bmax)] = i;
-                    atomicAdd(&S.npush, 1u);
-                }
+                L.evict_push[atomicAdd(L.bar + 3, 1u) % (C.J * C.Bmax)] = i;
+                atomicAdd(&S.npush, 1u);
             }
         }
     }
@@ -1349,13 +1318,10 @@ struct MaintSmem {
     uint32_t nadm;           // admission candidates of this round
     uint32_t ne_push, push_base;
     uint32_t add[kMaxJobs];
-    uint32_t pofs[kMaxJobs];             // per-job signals: first eviction entry of each job this round
     uint32_t scan[33];
     uint32_t PSg;                        // sharded: the global storage pool at round start (C1)
     uint32_t pscnt[kMaxShards][3];       // sharded: every shard's storage pool ([g][0])
     uint32_t ne_loc, k_loc;              // sharded: evictions / refills inside this shard's range
-    uint32_t relpk;                      // this round's refill split packed for the release word (0: none)
-    unsigned long long n_ev, n_rf;       // evictions / refills of this launch
 };
 
 // keyed refill ranks rho(u) over the storage pool as of round start (R-O8),
@@ -1363,11 +1329,9 @@ struct MaintSmem {
 // kSh: the global rank's owning shard resolves it into every shard's mailbox,
 // then every shard copies the complete list (C2 of the maintain CTA, slot J).
 template <bool kSh>
-__device__ uint32_t maint_refill_select(const Lay& L, const Cfg& C, MaintSmem& M, const uint32_t* s_pre, uint64_t r,
-                                        uint32_t u0, uint32_t u1) {
-    // returns refill u0 + threadIdx.x (~0u if that is not below u1): the thread keeps it for maint_apply
-    uint32_t first = ~0u;
-    if (u1 <= u0) return first;
+__device__ void maint_refill_select(const Lay& L, const Cfg& C, MaintSmem& M, const uint32_t* s_pre, uint64_t r,
+                                    uint32_t u0, uint32_t u1) {
+    if (u1 <= u0) return;
     const uint64_t key = derive_key(L.seed, PUR_REFILL, 0, r, 0);
     const PermDomain dom = perm_domain(kSh ? M.PSg : M.PS);
     uint32_t* fill = L.fill_list + (size_t)(r & 1) * C.FL;
@@ -1381,21 +1345,15 @@ __device__ uint32_t maint_refill_select(const Lay& L, const Cfg& C, MaintSmem& M
                 for (uint32_t g = 0; g < C.G; ++g) L.peer[g][at] = id;
             }
         } else {
-            const uint32_t id = pool_select(L, C, 3 * C.J, T_S, 0, s_pre, rank);
-            fill[u] = id;
-            if (u == u0 + threadIdx.x) first = id;
+            fill[u] = pool_select(L, C, 3 * C.J, T_S, 0, s_pre, rank);
         }
     }
     if constexpr (kSh) {
         shard_c2_sync(L, C, C.J, r);
         const uint32_t* in = L.mbox + C.mb_rf + (size_t)(r & 1) * C.FL;
-        for (uint32_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
-            fill[u] = ld_mbox(in + u);
-            if (u == u0 + threadIdx.x) first = fill[u];
-        }
+        for (uint32_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) fill[u] = ld_mbox(in + u);
     }
     __syncthreads();
-    return first;
 }
 
 // eviction of tracked entries (A, or every cached tier under evict_tiers = ALL)
@@ -1405,7 +1363,7 @@ __device__ uint32_t maint_refill_select(const Lay& L, const Cfg& C, MaintSmem& M
 template <bool kSh, class TMr>
 __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSmem& M, uint32_t* s_pre,
                             uint32_t* s_supS, uint64_t r, uint32_t active, uint32_t part_of_round, bool full_scan,
-                            bool speculated, uint32_t ne_push, uint32_t push_base, uint32_t spec_id, TMr& TM) {
+                            bool speculated, uint32_t ne_push, uint32_t push_base, TMr& TM) {
     const uint32_t tid = threadIdx.x, T = blockDim.x;
     if (tid == 0) {
         M.ne = full_scan ? 0u : ne_push;
@@ -1476,41 +1434,19 @@ __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSm
     TM.tick(3);
     const uint32_t ne = M.ne;
     uint32_t k = active ? min(M.deficit0 + ne, kSh ? M.PSg : M.PS) : 0u;   // no refill with no active job
-    // refill `tid` held in a register (valid for tid < own_n): this thread selected it
-    uint32_t own = ~0u, own_n = 0;
     if (admit) {
         k = active ? min(M.deficit0 + ne, M.nadm) : 0u;           // admissions instead of refills (R-O24)
     } else if (!speculated) {
         if (k) prefix_from_smem(C, s_supS, s_pre, M.scan);
-        own = maint_refill_select<kSh>(L, C, M, s_pre, r, 0, k);
-        own_n = k;
-    } else {
-        own = spec_id;
-        own_n = min(M.kspec, k);
-        if (k > M.kspec) maint_refill_select<kSh>(L, C, M, s_pre, r, M.kspec, k);  // beyond the speculated ranks
+        maint_refill_select<kSh>(L, C, M, s_pre, r, 0, k);
+    } else if (k > M.kspec) {
+        maint_refill_select<kSh>(L, C, M, s_pre, r, M.kspec, k);  // beyond the speculated ranks
     }
-#if !SENECA_FAST_INTAKE
-    own_n = 0;
-#endif
-    // A only: evictions and refills touch disjoint ids (refills come from the storage
-    // pool as of round start), their count updates are commutative and stay within
-    // [0, 128] per block in any order, and the tier split is known from ne -- so both
-    // loops run in one pass
-    const bool one_pass = SENECA_FAST_INTAKE && !C.evict_all;
     const uint32_t spidx = 3 * C.J;
     const uint32_t ring = C.J * C.Bmax;
     uint32_t* ev_ed = L.ev_ed + (size_t)(r & 1) * max(C.cap_e + C.cap_d, 1u);
     for (uint32_t u = tid; u < ne; u += T) {
-        uint32_t i;
-        if (full_scan) {
-            i = L.evict_list[u];
-        } else if constexpr (kSig<kSh>) {                // job jj's pushes are entries [pofs[jj], pofs[jj+1])
-            uint32_t jj = 0;
-            while (jj + 1 < C.J && M.pofs[jj + 1] <= u) ++jj;
-            i = ldcg(L.evict_push + (size_t)jj * C.Bmax + (u - M.pofs[jj]));
-        } else {
-            i = ldcg(L.evict_push + (push_base + u) % ring);
-        }
+        const uint32_t i = full_scan ? L.evict_list[u] : ldcg(L.evict_push + (push_base + u) % ring);
         const uint32_t w = i >> 5, b = 1u << (i & 31);
         uint32_t t = T_A;
         if (C.evict_all) {
@@ -1524,15 +1460,15 @@ __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSm
         if (count_add<kSh>(L, C, spidx, i, 1u, s_supS) && kSh) atomicAdd(&M.ne_loc, 1u);
     }
     if (!C.evict_all && tid == 0) M.ne_t[T_A] = ne;
-    if (!one_pass) __syncthreads();
+    __syncthreads();
     // tier split of the k refill positions: A, then D, then E, each up to its deficit
-    const uint32_t kA = one_pass ? min(M.def[T_A] + ne, k) : min(M.def[T_A] + M.ne_t[T_A], k);
-    const uint32_t kD = one_pass ? min(M.def[T_D], k - kA) : min(M.def[T_D] + M.ne_t[T_D], k - kA);
+    const uint32_t kA = min(M.def[T_A] + M.ne_t[T_A], k);
+    const uint32_t kD = min(M.def[T_D] + M.ne_t[T_D], k - kA);
     // refills enter their tier with no consumers; each job CTA adds them to its
     // own pools before its next classification (R-O8)
     const uint32_t* fill = L.fill_list + (size_t)(r & 1) * C.FL;
     for (uint32_t u = tid; u < k; u += T) {
-        const uint32_t i = (u == tid && tid < own_n) ? own : ldcg(fill + u);
+        const uint32_t i = ldcg(fill + u);
         uint32_t* bm = u < kA ? L.bm_a : (u < kA + kD ? L.bm_d : L.bm_e);
         atomicOr(bm + (i >> 5), 1u << (i & 31));
         if (count_add<kSh>(L, C, spidx, i, 0xffffffffu, s_supS) && kSh) atomicAdd(&M.k_loc, 1u);
@@ -1551,10 +1487,9 @@ __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSm
             M.warm = 1;                                           // every tier full: the cold start ends
             *L.warm = 1;
         }
-        M.n_ev += ne;                                              // added to L.evicted / L.refilled
-        M.n_rf += k;                                               // at the launch end
+        *L.evicted += ne;
+        *L.refilled += k;
         M.prev_k = k;
-        M.relpk = k < 1024u ? (0x80000000u | k | (kA << 10) | (kD << 20)) : 0u;
     }
     __syncthreads();
     TM.tick(4);
@@ -1565,28 +1500,19 @@ __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSm
 // seen join the pool of their tier (empty consumer sets), and under
 // evict_tiers = ALL evicted E/D entries it has not seen leave its E/D pool (an
 // evicted A entry was consumed by j, so it was in no A pool of j).
-// relpk: the refill split from the release word (bit 31 set: k | kA << 10 | kD << 20),
-// else read from fill_n; refill threadIdx.x < prek was loaded before the release
-// (pre_id) together with whether j has seen it (pre_unseen: j's seen bits do not
-// change between that load and this intake).
 template <bool kSh>
-__device__ void job_take_refills(const Lay& L, const Cfg& C, JobSmem& S, uint32_t j, uint64_t r, uint32_t* s_sup,
-                                 uint32_t relpk = 0, uint32_t prek = 0, uint32_t pre_id = 0, bool pre_unseen = false) {
+__device__ void job_take_refills(const Lay& L, const Cfg& C, JobSmem& S, uint32_t j, uint64_t r, uint32_t* s_sup) {
     const uint32_t* fn = L.fill_n + (r & 1) * 4;
     const uint32_t* fill = L.fill_list + (size_t)(r & 1) * C.FL;
     // the first refill entry of this thread is loaded together with the counts (an
     // entry beyond kf is read but not used; the buffer holds FL entries)
-    const bool have_pre = threadIdx.x < prek;
-    const uint32_t i0 = have_pre ? pre_id : (threadIdx.x < C.FL ? ldcg(fill + threadIdx.x) : 0u);
-    uint32_t kf, kA, kD;
-    if (relpk >> 31) { kf = relpk & 1023u; kA = (relpk >> 10) & 1023u; kD = (relpk >> 20) & 1023u; }
-    else { kf = ldcg(fn); kA = ldcg(fn + 1); kD = ldcg(fn + 2); }
+    const uint32_t i0 = threadIdx.x < C.FL ? ldcg(fill + threadIdx.x) : 0u;
+    const uint32_t kf = ldcg(fn), kA = ldcg(fn + 1), kD = ldcg(fn + 2);
     const uint32_t* seen_j = L.seen + (size_t)j * C.NW;
     uint32_t addA = 0, addD = 0, addE = 0;   // registers (no indexed local array)
     for (uint32_t u = threadIdx.x; u < kf; u += blockDim.x) {
         const uint32_t i = u == threadIdx.x ? i0 : ldcg(fill + u);
-        const bool unseen = (u == threadIdx.x && have_pre) ? pre_unseen : !((ldcg(seen_j + (i >> 5)) >> (i & 31)) & 1u);
-        if (unseen) {
+        if (!((ldcg(seen_j + (i >> 5)) >> (i & 31)) & 1u)) {
             const uint32_t tt = u < kA ? 0u : (u < kA + kD ? 1u : 2u);
             if (count_add<kSh>(L, C, j * 3 + tt, i, 1u, s_sup + tt * C.NS)) {
                 addA += tt == 0; addD += tt == 1; addE += tt == 2;
@@ -1749,7 +1675,6 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
     } else {
         if (tid == 0) {
             M.prev_k = blockDim.x;
-            M.n_ev = M.n_rf = 0;
             M.PS = ldcg(L.cnt_tot + 3 * C.J);
             for (int t = 0; t < 4; ++t) M.size[t] = ldcg(L.tsize + t);
             M.warm = C.cold ? ldcg(L.warm) : 1u;
@@ -1798,16 +1723,14 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
     __syncthreads();
 
     // Coupled rounds synchronise through two one-directional signals (zeroed by
-    // the host before every launch): L.bar[0] counts job phases completed, L.rel
-    // counts rounds whose maintain has been applied (its high word: the refill
-    // split of that round).  A job CTA only waits for
+    // the host before every launch): L.bar[0] counts job phases completed, L.bar[1]
+    // counts rounds whose maintain has been applied.  A job CTA only waits for
     // maintain(r-1) before classifying round r; the maintain CTA only waits for
     // the job phases of round r -- the next round's walk and speculative refill
     // overlap everything else.
     if (is_maint) {
         uint32_t expect = 0, push_total = 0;
         bool spec = false;
-        uint32_t spec_id = ~0u;          // speculated refill `tid` of the round about to be played
         // speculative refill ranks for the round about to be played: the storage
         // pool as of round start cannot change before this round's maintain
         // round-start deficits of the tracked tiers (A; D and E under evict_tiers = ALL)
@@ -1833,12 +1756,7 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
             __syncthreads();
             if (M.kspec) prefix_from_smem(C, s_sup, s_pre, M.scan);
             TM.tick(0);
-            spec_id = maint_refill_select<false>(L, C, M, s_pre, r, 0, M.kspec);
-#if SENECA_FAST_INTAKE
-            // publish the speculated refills of round r (parity slot): the job CTAs
-            // read them and their seen bits while they wait for this round's maintain
-            if (tid == 0) st_release64(L.spec + 2 * (r & 1), ((unsigned long long)M.kspec << 32) | (uint32_t)(r - P.r0 + 1));
-#endif
+            maint_refill_select<false>(L, C, M, s_pre, r, 0, M.kspec);
             TM.tick(1);
             return true;
         };
@@ -1861,24 +1779,7 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
                     M.PSg = t;
                 }
             }
-            if constexpr (kSig<kShard>) {    // lane jj waits for job jj's phase of round r
-                if (tid < 32) {
-                    uint32_t np = 0;
-                    if (tid < C.J && ((part >> tid) & 1u)) {
-                        unsigned long long v;
-                        while ((uint32_t)(v = ld_acquire64(L.sig + 2 * tid)) < rr + 1) { }
-                        np = (uint32_t)(v >> 32);
-                    }
-                    uint32_t inc = np;
-#pragma unroll
-                    for (uint32_t o = 1; o < 32; o <<= 1) {
-                        const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
-                        if (tid >= o) inc += t;
-                    }
-                    if (tid < C.J) M.pofs[tid] = inc - np;
-                    if (tid == 31) { M.ne_push = inc; M.push_base = 0; }
-                }
-            } else if (tid == 0) {           // job phases of round r done; evictions they pushed
+            if (tid == 0) {                  // job phases of round r done; evictions they pushed
                 unsigned long long v;
                 while ((uint32_t)(v = ld_acquire64(L.bar)) < expect) { }
                 const uint32_t pushed = (uint32_t)(v >> 32);
@@ -1895,22 +1796,14 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
                 if (!spec && tid == 0) set_deficits();
                 __syncthreads();
                 maint_apply<kShard>(L, C, P, M, s_pre, s_sup, r, active_after, part, departing != 0, spec,
-                                    M.ne_push, M.push_base, spec_id, TM);
+                                    M.ne_push, M.push_base, TM);
             } else if (tid == 0) {          // nothing maintained: the job CTAs take an empty round
                 uint32_t* fn = L.fill_n + (r & 1) * 4;
                 fn[0] = fn[1] = fn[2] = 0;
                 L.ev_ed_n[r & 1] = 0;
-                M.relpk = 0x80000000u;
             }
             __syncthreads();
-            if (tid == 0) {                 // release round r's tiers (+ the refill split, when it fits)
-#if SENECA_FAST_INTAKE
-                st_release64(L.rel, ((unsigned long long)M.relpk << 32) | (rr + 1));
-#else
-                __threadfence();
-                atomicExch(reinterpret_cast<unsigned long long*>(L.rel), (unsigned long long)(rr + 1));
-#endif
-            }
+            if (tid == 0) { __threadfence(); atomicExch(L.bar + 2, rr + 1); }     // release round r's tiers
             TM.tick(5);
             advance(part, departing, r);
             spec = false;
@@ -1942,50 +1835,18 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
             uint32_t part, departing;
             schedule(part, departing);
             const uint32_t active_after = s_active & ~departing;
-            uint32_t prek = 0, pre_id = 0, pre_cons = 0;
-            bool pre_unseen = false, have_pc = false;
             if (coupled && rr > 0) {                   // maintain(r-1) applied?
-#if SENECA_FAST_INTAKE
-                // while maintain(r-1) runs: the consumer words of this round's first T
-                // requests (j alone sets its bits; maintain only clears evicted ids')
-                if (C.cap_a && !C.baseline && ((part >> j) & 1u)) {
-                    have_pc = tid < S.need;
-                    if (have_pc) pre_cons = ldcg(L.cons + (size_t)j * C.NW + (s_req[tid] >> 5));
-                }
-                // while maintain(r-1) runs: its speculated refills (published during
-                // round r-1) and whether j has seen them -- j's seen bits are final
-                // for round r-1 and nothing else writes them before the intake
-                if (!kShard && ((part >> j) & 1u) && !S.recount) {
-                    if (tid == 0) {
-                        const unsigned long long v = ld_acquire64(L.spec + 2 * ((r - 1) & 1));
-                        S.prek = (uint32_t)v == rr ? min((uint32_t)(v >> 32), blockDim.x) : 0u;
-                    }
-                    __syncthreads();
-                    prek = S.prek;
-                    if (tid < prek) {
-                        pre_id = ldcg(L.fill_list + (size_t)((r - 1) & 1) * C.FL + tid);
-                        pre_unseen = !((ldcg(L.seen + (size_t)j * C.NW + (pre_id >> 5)) >> (pre_id & 31)) & 1u);
-                    }
-                }
-#endif
-                if (tid == 0) {
-                    unsigned long long v;
-                    while ((uint32_t)(v = ld_acquire64(L.rel)) < rr) { }
-                    S.relpk = (uint32_t)v == rr ? (uint32_t)(v >> 32) : 0u;
-                }
+                if (tid == 0) { while (ld_acquire(L.bar + 2) < rr) { } }
                 __syncthreads();
             }
             TM.tick(4);
             if (C.cold && tid == 0) S.warm = ldcg(L.warm);        // stable until this round's maintain
             if ((part >> j) & 1u) {
                 if (S.recount) { job_recount(L, C, j, s_sup, S.tot); if (tid == 0) S.recount = 0; __syncthreads(); }
-                else if (coupled && rr > 0) {
-                    job_take_refills<kShard>(L, C, S, j, r - 1, s_sup, S.relpk, prek, pre_id, pre_unseen);
-                    __syncthreads();
-                }
+                else if (coupled && rr > 0) { job_take_refills<kShard>(L, C, S, j, r - 1, s_sup); __syncthreads(); }
                 TM.tick(0);
                 job_round<kShard>(L, C, P, S, s_req, s_miss, s_sub, s_oid, s_osrc, s_pre, j, r, s_e[j], s_n[j],
-                          __popc(active_after), TM, s_win, s_wseen, s_sup, have_pc, pre_cons);
+                          __popc(active_after), TM, s_win, s_wseen, s_sup);
                 // a8 (R-O16): the epoch ends with this batch -> reset seen_j and the walk
                 if (s_n[j] + S.need == C.N) {
                     flush_stats(L, C, S, j, s_e[j]);
@@ -2005,18 +1866,11 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
                     if (tid == 0) S.pf_state = 0;
                 }
                 if (coupled && tid == 0) {                 // job phase done (+ evictions pushed)
-#if SENECA_FAST_INTAKE
-                    if constexpr (kSig<kShard>)
-                        st_release64(L.sig + 2 * j, ((unsigned long long)S.npush << 32) | (rr + 1));
-                    else
-                        red_release_add64(L.bar, 1ull + ((unsigned long long)S.npush << 32));
-#else
                     __threadfence();
                     atomicAdd(reinterpret_cast<unsigned long long*>(L.bar), 1ull + ((unsigned long long)S.npush << 32));
-#endif
                     S.npush = 0;
                 }
-                TM.tick(coupled ? 6 : 0);            // (coupled: slot 6 = epoch end + signal)
+                TM.tick(0);
             }
             advance(part, departing, r);
             if (rr + 1 < P.rounds && ((s_active & P.subset) >> j & 1u)) {
@@ -2069,7 +1923,7 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
         flush_stats(L, C, S, j, s_e[j]);
         if (S.late) catch_up_seen(L, C, S, j, s_e[j]);
         if (coupled && P.rounds > 0 && (s_active >> j & 1u)) {
-            if (tid == 0) { while ((uint32_t)ld_acquire64(L.rel) < P.rounds) { } }
+            if (tid == 0) { while (ld_acquire(L.bar + 2) < P.rounds) { } }
             __syncthreads();
             if (!S.recount) job_take_refills<kShard>(L, C, S, j, P.r0 + P.rounds - 1, s_sup);
             __syncthreads();
@@ -2077,12 +1931,7 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
         if (tid < 3) L.cnt_tot[j * 3 + tid] = S.tot[tid];
         for (uint32_t k = tid; k < 3 * C.NS; k += blockDim.x) L.cnt_sup[(size_t)j * 3 * C.NS + k] = s_sup[k];
     } else {
-        if (tid == 0) {
-            L.cnt_tot[3 * C.J] = M.PS;
-            for (int t = 0; t < 4; ++t) L.tsize[t] = M.size[t];
-            *L.evicted += M.n_ev;
-            *L.refilled += M.n_rf;
-        }
+        if (tid == 0) { L.cnt_tot[3 * C.J] = M.PS; for (int t = 0; t < 4; ++t) L.tsize[t] = M.size[t]; }
         for (uint32_t k = tid; k < C.NS; k += blockDim.x) L.cnt_sup[(size_t)3 * C.J * C.NS + k] = s_sup[k];
     }
     cp_async_wait_all();
@@ -2389,11 +2238,10 @@ __global__ void ods_validate_requests(const __grid_constant__ Lays LS, const __g
 inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 // Control block at the start of the workspace, one 64-B slot per replica:
-// bar[4] at +0, err at +16, verr at +20, dbg[4] at +24, rel (u64) at +40,
-// spec[2] (u64) at +48, sig[kMaxJobs] (u64) at +64.  Kept contiguous (not inside the
+// bar[4] at +0, err at +16, verr at +20.  Kept contiguous (not inside the
 // replica slices) so the per-launch signal reset and the status read are one
 // small strided copy whatever the replica slice size.
-constexpr size_t kCtlBytes = 64 + 8 * kMaxJobs;
+constexpr size_t kCtlBytes = 64;
 inline size_t ctl_bytes(uint32_t R) { return align256((size_t)R * kCtlBytes); }
 
 enum KernelClass { K_ROUNDS = 0, K_PERM, K_RECOUNT, K_INIT, K_VALIDATE, K_NCLASS };
@@ -2597,9 +2445,6 @@ Lay carve(const Sizes& z, char* base, char* ctl, uint64_t seed) {
     L.err = (uint32_t*)(ctl + 16);
     L.verr = (uint32_t*)(ctl + 20);
     L.dbg = (uint32_t*)(ctl + 24);
-    L.rel = (uint32_t*)(ctl + 40);
-    L.spec = (uint32_t*)(ctl + 48);
-    L.sig = (uint32_t*)(ctl + 64);
     L.phase = (unsigned long long*)(base + z.off[26]);
     L.ev_ed = (uint32_t*)(base + z.off[27]);
     L.ev_ed_n = (uint32_t*)(base + z.off[28]);
@@ -2848,7 +2693,6 @@ seneca_status launch_rounds(seneca_ctx* c, uint64_t* Rio, uint32_t jobs_mask, co
         }
     }
     SENECA_CUDA_TRY(cudaMemset2DAsync(c->ctl, kCtlBytes, 0, 16, c->R, st));   // every replica's bar[4]
-    SENECA_CUDA_TRY(cudaMemset2DAsync(c->ctl + 40, kCtlBytes, 0, kCtlBytes - 40, c->R, st));   // rel, spec, sig
     void* args[] = {&c->LS, &c->C, &P};
     cudaError_t le = cudaSuccess;
     timed(c, K_ROUNDS, st, [&] {

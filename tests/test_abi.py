@@ -137,13 +137,13 @@ def test_replicas_workspace_and_arguments(lib):
     one = S.state_bytes(S.make_config(c["n_total"], c["batch"], c["target"], caps[0], caps[1], caps[2], 1))
     two = S.state_bytes(S.make_config(c["n_total"], c["batch"], c["target"], caps[0], caps[1], caps[2], 1,
                                       replicas=2))
-    ctl = lambda R: -(-R * 320 // 256) * 256                   # a control block, 320 B per replica
-    slice_ = one - ctl(1)                                      # + one 256-aligned slice per replica
-    assert slice_ % 256 == 0 and two == 2 * slice_ + ctl(2)
+    slice_ = two - one                                         # one 256-aligned slice per replica
+    ctl = one - slice_                                         # + a control block, 64 B per replica
+    assert slice_ % 256 == 0 and ctl == 256
     for r in (0, 1, 2, 7, 64):
         cfg = S.make_config(c["n_total"], c["batch"], c["target"], caps[0], caps[1], caps[2], 1, replicas=r)
         R = max(r, 1)
-        assert S.state_bytes(cfg) == R * slice_ + ctl(R)
+        assert S.state_bytes(cfg) == R * slice_ + -(-R * 64 // 256) * 256
     for r, mode in ((65, 0), (2, 1)):                          # too many; caller-supplied requests need R = 1
         cfg = S.make_config(c["n_total"], c["batch"], c["target"], caps[0], caps[1], caps[2], 1, mode, replicas=r)
         with pytest.raises(S.SenecaError) as ei:
