@@ -559,7 +559,7 @@ def main():
         # region (where they would compete with the kernel's own DRAM writes)
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
-        flush.fill_(v & 0xFF)
+        flush.view(torch.float64).fill_(float(v & 0xFF))              # 8-B elements: full-width stores
         f1.record(stream)
         flush[: 256 << 20].max()
         f1.synchronize()
