@@ -1051,7 +1051,8 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
     // (R-O2): with all three pools empty no request can hit, so no residency
     // word needs gathering (the same decisions; not under the baseline sampler,
     // whose A hits ignore consumption, nor sharded, whose totals are local)
-    const bool none_cached = !kSh && !C.baseline && (S.tot[0] | S.tot[1] | S.tot[2]) == 0u;
+    // (sharded: S.tot is this shard's part; in late mode every pool is empty globally)
+    const bool none_cached = (!kSh && !C.baseline && (S.tot[0] | S.tot[1] | S.tot[2]) == 0u) || (kSh && S.late);
 #else
     const bool none_cached = false;
 #endif
@@ -1091,14 +1092,18 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
         if (is_miss) s_miss[mbase + ex] = s;
         mbase += tot;
     }
-    if (kSh && tid < 32)                     // C1: this shard's pool sizes after its hits, everyone's back
+    // C1: this shard's pool sizes after its hits, everyone's back (not in late mode: every
+    // shard entered it in the same round, after which all pools stay empty globally
+    // until the epoch ends -- no exchange until then)
+    if (kSh && !S.late && tid < 32)
         shard_c1(L, C, j, r, S.tot[0] - S.hits_loc[0], S.tot[1] - S.hits_loc[1], S.tot[2] - S.hits_loc[2], S.cnt);
     if (tid == 0) {
         uint32_t pa, pd, pe;                 // the pools' sizes after this round's hits
         if constexpr (kSh) {
             S.tot[0] -= S.hits_loc[0]; S.tot[1] -= S.hits_loc[1]; S.tot[2] -= S.hits_loc[2];
             pa = pd = pe = 0;
-            for (uint32_t g = 0; g < C.G; ++g) { pa += S.cnt[g][0]; pd += S.cnt[g][1]; pe += S.cnt[g][2]; }
+            if (!S.late)
+                for (uint32_t g = 0; g < C.G; ++g) { pa += S.cnt[g][0]; pd += S.cnt[g][1]; pe += S.cnt[g][2]; }
             S.glob[0] = pa; S.glob[1] = pd; S.glob[2] = pe;
             if ((pa > C.N || pd > C.N || pe > C.N) && atomicCAS(L.dbg, 0u, 0x80000u | j) == 0u) {
                 L.dbg[1] = (uint32_t)r; L.dbg[2] = S.cnt[0][0]; L.dbg[3] = C.G > 1 ? S.cnt[1][0] : 0u;
@@ -1875,14 +1880,17 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
             advance(part, departing, r);
             if (rr + 1 < P.rounds && ((s_active & P.subset) >> j & 1u)) {
                 // (C.late: all pools of the job empty, not at an epoch start -> storage-list walk)
-                if (C.late && !S.late && !S.recount && (S.tot[0] | S.tot[1] | S.tot[2]) == 0u)
+                // (sharded: the global pool sizes after this round's hits less its substitutes)
+                const bool empty = kShard ? ((S.glob[0] - S.k[0]) | (S.glob[1] - S.k[1]) | (S.glob[2] - S.k[2])) == 0u
+                                          : (S.tot[0] | S.tot[1] | S.tot[2]) == 0u;
+                if (C.late && !S.late && !S.recount && empty)
                     enter_late(L, C, S, j, s_e[j]);
 #if SENECA_LATE_BULK
                 // late bulk: rounds rr+1 .. rr+K of an uncoupled job in late mode, all
                 // but the last round of its epoch and of the launch, decided in one
                 // pass; the schedule (progress of every job, departures, arrivals)
                 // advances round by round in warp 0 as `advance` would
-                if (!coupled && !kShard && S.late && P.mode == 0 && !P.out_ids) {
+                if (!coupled && S.late && P.mode == 0 && !P.out_ids) {
                     const uint32_t B = C.batch[j], left = (C.N - s_n[j] + B - 1) / B;   // rounds of epoch s_e[j] left
                     const uint32_t lrest = P.rounds - (rr + 1);                        // rounds of the launch left
                     const uint32_t K = min(left, lrest) - 1;
@@ -2367,7 +2375,7 @@ Sizes compute_sizes(const seneca_cache_config* cfg) {
     C.FL = (uint32_t)(std::max<size_t>(C.cap_t, 1) + (size_t)C.J * C.Bmax);
     C.nch = (C.N + kGenChunk - 1) / kGenChunk;
     C.late = (SENECA_LATE_WALK && cfg->cap_a == 0 && !cfg->evict_tiers && !cfg->cold_start && !cfg->sampler &&
-              cfg->request_mode == 0 && cfg->replicas <= 1 && cfg->shards <= 1) ? 1u : 0u;
+              cfg->request_mode == 0 && cfg->replicas <= 1) ? 1u : 0u;
     C.G = cfg->shards > 1 ? cfg->shards : 1u;
     C.xsys = C.G > 1 && cfg->shard_mode == 1 ? 1u : 0u;
     C.mb_c1 = 0;

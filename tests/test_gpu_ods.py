@@ -756,6 +756,44 @@ def test_sharded_full_size_prefix_22k():
         compare_replica(o, g, k)
 
 
+@pytest.mark.parametrize("block", range(2))
+def test_sharded_late_mode_random_static_configs(block):
+    """Sharded replays with static tiers: once a job's pools are empty GLOBALLY
+    (the sizes every shard learns in C1, less the round's substitutes) every
+    shard enters the storage-list walk in the same round, skips C1/C2 and the
+    classification gathers, and decides the rest of the epoch with the late bulk
+    until the epoch-start recount resumes the exchange.  Random
+    static configs, G = 2 / 3 / 5, replays cut into launches of random length
+    (the late state and the stamps persist across launches), every shard vs the
+    oracle transcript, bitmaps and counters."""
+    st = synth.Stream(9900 + block)
+    for it in range(6):
+        n = int(st.choice(1, [1000, 16385, 40000, 70000])[0])
+        J = int(st.choice(1, [1, 2, 3])[0])
+        batch = [int(x) for x in st.choice(J, [7, 64, 100, 512])]
+        target = [int(x) for x in st.choice(J, [1, 2, 3])]
+        ce = int(n * float(st.uniform(1)[0]) * 0.6)
+        cd = int((n - ce) * float(st.uniform(1)[0]) * 0.5) if it % 2 else 0
+        G = (2, 3, 5)[it % 3]
+        seed = int(st.u64(1)[0])
+        o = O.ODS(n, batch, target, ce, cd, 0, seed, transcript=True)
+        g = P.ODSContext(n, batch, target, ce, cd, 0, seed, shards=G)
+        tr = g.new_transcript()
+        total = 0
+        while g.view().active_mask:
+            k = int(st.u64(1)[0] % np.uint64(400)) + 1
+            done = g.replay_rounds(k, tr)
+            total += done
+            if done < k:
+                break
+        torch.cuda.synchronize()
+        g.sync()
+        assert total == o.replay_epochs(max(target)), (n, batch, target, ce, cd, G)
+        for k in range(G):
+            compare_replica(o, g, k, tr[k])
+        g.close()
+
+
 @pytest.mark.parametrize("G,name,scale", [(2, "toy", 1), (4, "imagenet1k", 64)])
 def test_sharded_one_context_per_shard(G, name, scale):
     """shard_mode 1 (one shard per context, peers attached by mailbox address, as
