@@ -493,6 +493,8 @@ struct JobSmem {
     unsigned long long key[3];               // this round's substitution key per tier (A, D, E)
     PermDomain dom[3];                       // and rank domain of the pool after the hits
     uint32_t hits_loc[3], own[3], glob[3];   // sharded: hits / substitutes in this shard's range, global pool sizes
+    uint32_t hg[kMaxShards][3], sg[kMaxShards][3];   // sharded, static tiers: this round's hits / substitutes
+    uint32_t c1;                                     //   per shard range; 1: the next round exchanges C1
     uint32_t cnt[kMaxShards][3];             // sharded: every shard's pool sizes of this round (C1)
     uint32_t recount;
     uint32_t late, lc, lk; // storage-list walk (Cfg.late): on, lap-1 segment and entry
@@ -1083,6 +1085,8 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
                                                  s_sup + (pool_of(j, t) - j * 3) * C.NS);
                 atomicAdd(&S.hits[t == T_A ? 0 : (t == T_D ? 1 : 2)], 1u);
                 if (kSh && mine) atomicAdd(&S.hits_loc[t == T_A ? 0 : (t == T_D ? 1 : 2)], 1u);
+                if (kSh && C.late)           // every shard classifies every request: it counts every range's hits
+                    atomicAdd(&S.hg[(i >> kSuperShift) / ((C.NS + C.G - 1) / C.G)][t == T_A ? 0 : (t == T_D ? 1 : 2)], 1u);
             } else {
                 is_miss = true;
             }
@@ -1095,8 +1099,18 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
     // C1: this shard's pool sizes after its hits, everyone's back (not in late mode: every
     // shard entered it in the same round, after which all pools stay empty globally
     // until the epoch ends -- no exchange until then)
-    if (kSh && !S.late && tid < 32)
-        shard_c1(L, C, j, r, S.tot[0] - S.hits_loc[0], S.tot[1] - S.hits_loc[1], S.tot[2] - S.hits_loc[2], S.cnt);
+    // With static tiers a shard's pools change only by the round's hits and substitutes,
+    // which every shard sees (classification is replicated; the owner of every rank
+    // follows from the sizes), so every shard keeps every shard's sizes itself and C1
+    // is exchanged only in the first round of a launch and after an epoch-start recount.
+    if (kSh && !S.late && tid < 32) {
+        if (!C.late || S.c1) {
+            shard_c1(L, C, j, r, S.tot[0] - S.hits_loc[0], S.tot[1] - S.hits_loc[1], S.tot[2] - S.hits_loc[2], S.cnt);
+        } else {
+            if (tid < C.G) { S.cnt[tid][0] -= S.hg[tid][0]; S.cnt[tid][1] -= S.hg[tid][1]; S.cnt[tid][2] -= S.hg[tid][2]; }
+            __syncwarp();
+        }
+    }
     if (tid == 0) {
         uint32_t pa, pd, pe;                 // the pools' sizes after this round's hits
         if constexpr (kSh) {
@@ -1160,7 +1174,9 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
                 // the shard whose range holds global rank `rank` resolves it and
                 // stores the id into every shard's mailbox (C2)
                 uint32_t local;
-                if (shard_owner(C, S.cnt, tt, rank, &local) == L.shard) {
+                const uint32_t owner = shard_owner(C, S.cnt, tt, rank, &local);
+                if (C.late) atomicAdd(&S.sg[owner][tt], 1u);
+                if (owner == L.shard) {
                     const uint32_t id = pool_select(L, C, j * 3 + tt, t, j, s_pre + tt * C.NS, local);
                     const size_t at = C.mb_c2 + ((size_t)(r & 1) * C.J + j) * C.Bmax + u;
                     for (uint32_t g = 0; g < C.G; ++g) L.peer[g][at] = id;
@@ -1239,6 +1255,11 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
         if constexpr (kSh) {                 // this shard's own substitutes leave its pools
             S.tot[0] -= S.own[0]; S.tot[1] -= S.own[1]; S.tot[2] -= S.own[2];
             S.own[0] = S.own[1] = S.own[2] = 0;
+            if (C.late && !S.late) {         // every shard's sizes after this round (C1 skipped next round)
+                for (uint32_t g = 0; g < C.G; ++g)
+                    for (uint32_t t3 = 0; t3 < 3; ++t3) { S.cnt[g][t3] -= S.sg[g][t3]; S.sg[g][t3] = 0; }
+                S.c1 = 0;
+            }
         } else {
 #if SENECA_HOIST_KEYS
             S.tot[0] -= S.hits[0] + k0;
@@ -1297,6 +1318,7 @@ __device__ void job_round(const Lay& L, const Cfg& C, const Launch& P, JobSmem& 
     }
     __syncthreads();
     if (tid < 3) { S.hits[tid] = 0; S.hits_loc[tid] = 0; }   // for the next round (barriers before next use)
+    if (kSh && tid < kMaxShards * 3) (&S.hg[0][0])[tid] = 0;
     TM.tick(3);
 }
 
@@ -1674,6 +1696,8 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
     if (!is_maint) {
         S.acc_dig[tid] = 0;
         if (tid < 12) S.acc_cnt[tid] = 0;
+        if (tid < kMaxShards * 3) { (&S.hg[0][0])[tid] = 0; (&S.sg[0][0])[tid] = 0; }
+        if (tid == 0) S.c1 = 1;
         if (tid < 3) { S.hits[tid] = 0; S.hits_loc[tid] = 0; S.own[tid] = 0; }   // (shared memory is not zeroed
         if (tid < 3) S.tot[tid] = ldcg(L.cnt_tot + j * 3 + tid);                   //  at launch: initcheck-blind)
         for (uint32_t k = tid; k < 3 * C.NS; k += blockDim.x) s_sup[k] = ldcg(L.cnt_sup + (size_t)j * 3 * C.NS + k);
@@ -1847,7 +1871,11 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
             TM.tick(4);
             if (C.cold && tid == 0) S.warm = ldcg(L.warm);        // stable until this round's maintain
             if ((part >> j) & 1u) {
-                if (S.recount) { job_recount(L, C, j, s_sup, S.tot); if (tid == 0) S.recount = 0; __syncthreads(); }
+                if (S.recount) {
+                    job_recount(L, C, j, s_sup, S.tot);
+                    if (tid == 0) { S.recount = 0; S.c1 = 1; }     // (sharded: the recounted sizes are exchanged)
+                    __syncthreads();
+                }
                 else if (coupled && rr > 0) { job_take_refills<kShard>(L, C, S, j, r - 1, s_sup); __syncthreads(); }
                 TM.tick(0);
                 job_round<kShard>(L, C, P, S, s_req, s_miss, s_sub, s_oid, s_osrc, s_pre, j, r, s_e[j], s_n[j],
