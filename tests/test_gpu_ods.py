@@ -794,7 +794,8 @@ def test_sharded_late_mode_random_static_configs(block):
         g.close()
 
 
-@pytest.mark.parametrize("G,name,scale", [(2, "toy", 1), (4, "imagenet1k", 64)])
+@pytest.mark.parametrize("G,name,scale", [(2, "toy", 1), (4, "imagenet1k", 64), (2, "openimages", 64),
+                                          (3, "imagenet22k", 64)])
 def test_sharded_one_context_per_shard(G, name, scale):
     """shard_mode 1 (one shard per context, peers attached by mailbox address, as
     one process per GPU runs it): G contexts on this device replay concurrently
