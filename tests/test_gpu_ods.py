@@ -809,14 +809,17 @@ def test_sharded_one_context_per_shard(G, name, scale):
     assert "ok" in out.stdout
 
 
-def test_sharded_across_processes_cuda_ipc():
-    """Two PROCESSES, one shard each (the one-process-per-GPU layout, both on this
+@pytest.mark.parametrize("args", [["2"], ["2", "openimages", "256"], ["3", "imagenet22k", "1024"]])
+def test_sharded_across_processes_cuda_ipc(args):
+    """PROCESSES, one shard each (the one-process-per-GPU layout, all on this
     device): mailboxes mapped by CUDA IPC through dist.attach_shard_peers (handles
     all-gathered over gloo); each rank's transcript equals the oracle's.  Without
-    MPS the two processes time-slice the device, so only a toy replay is run."""
+    MPS the processes time-slice the device, so only small replays are run: the
+    toy (A churn) and two static-tier configs (tracked sizes and late mode across
+    processes)."""
     import subprocess
     import sys
-    out = subprocess.run([sys.executable, os.path.join(os.path.dirname(HERE), "tools", "shard_ranks.py"), "2"],
+    out = subprocess.run([sys.executable, os.path.join(os.path.dirname(HERE), "tools", "shard_ranks.py"), *args],
                          capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-3000:]
     assert "all ranks ok" in out.stdout
