@@ -43,6 +43,9 @@ constexpr int kMaxSteps = 101;  // grid step 1 % -> 101 values per coordinate
 #ifndef SENECA_MDP_REDUX
 #define SENECA_MDP_REDUX 1        // warp argmax by fmax butterfly + REDUX.MIN of the index (A/B knob)
 #endif
+#ifndef SENECA_MDP_DENSE
+#define SENECA_MDP_DENSE 2        // rows as dense arrays; 2: capc|cape in one 8-B slot, pre-scaled pair offsets (A/B knob)
+#endif
 #ifndef SENECA_MDP_MINB
 #define SENECA_MDP_MINB 3
 #endif
@@ -597,7 +600,13 @@ __global__ void mdp_pair_table(uint32_t steps, uint32_t n_pairs) {
         const uint32_t b = t - pairs_before(a), m = a - b, i0 = a * (a + 1) / 2;
         tab[t] = make_uint2((uint32_t)(b * sizeof(Row)) | (uint32_t)(m * sizeof(Row)) << 12 | (steps - a) << 24,
                                 (i0 + b) | (i0 + m) << 16);
+#if SENECA_MDP_DENSE == 2
+        // byte offsets of 8-B row slots and of grid entries, ready to add
+        g_pairs_dense[step_slot(steps)][t] = make_uint2(8 * b | 8 * m << 10 | 8 * (steps - a) << 20,
+                                                        8 * (i0 + b) | 8 * (i0 + m) << 16);
+#else
         g_pairs_dense[step_slot(steps)][t] = make_uint2(b | m << 8 | (steps - a) << 16, (i0 + b) | (i0 + m) << 16);
+#endif
     }
 }
 
@@ -635,20 +644,25 @@ __device__ __forceinline__ void aos_pairs(const Row* rows, const uint2* __restri
     }
 }
 
-#ifndef SENECA_MDP_DENSE
-#define SENECA_MDP_DENSE 1        // rows as dense arrays (fewer shared-memory wavefronts per pair) (A/B knob)
-#endif
 // Structure-of-arrays rows of one group: capc u32[104] | cape u32[104] | tA | tD |
 // tDc | tE f64[104] -- a lane reading consecutive rows reads consecutive words
 // (one wavefront for a 4-B field, two for an 8-B one), where the 40-B Row
 // stride costs two for either.
 constexpr uint32_t kDR = 104;
+#if SENECA_MDP_DENSE == 2
+// (2: capc and cape interleaved in one 8-B slot per row, so every field of row k
+// is at 8k + a constant: one address per row index, the fields by immediates)
+constexpr uint32_t kDCapc = 0, kDCape = 4, kDTA = 8 * kDR, kDTD = 16 * kDR, kDTDC = 24 * kDR, kDTE = 32 * kDR,
+                   kDBytes = 40 * kDR;
+#else
 constexpr uint32_t kDCapc = 0, kDCape = 4 * kDR, kDTA = 8 * kDR, kDTD = 16 * kDR, kDTDC = 24 * kDR, kDTE = 32 * kDR,
                    kDBytes = 40 * kDR;
+#endif
+constexpr uint32_t kDIdx = SENECA_MDP_DENSE == 2 ? 2 : 1;   // u32 index scale of capc / cape
 struct DenseRows {
     char* p;
-    __device__ uint32_t& capc(uint32_t k) const { return reinterpret_cast<uint32_t*>(p + kDCapc)[k]; }
-    __device__ uint32_t& cape(uint32_t k) const { return reinterpret_cast<uint32_t*>(p + kDCape)[k]; }
+    __device__ uint32_t& capc(uint32_t k) const { return reinterpret_cast<uint32_t*>(p + kDCapc)[kDIdx * k]; }
+    __device__ uint32_t& cape(uint32_t k) const { return reinterpret_cast<uint32_t*>(p + kDCape)[kDIdx * k]; }
     __device__ double& tA(uint32_t k) const { return reinterpret_cast<double*>(p + kDTA)[k]; }
     __device__ double& tD(uint32_t k) const { return reinterpret_cast<double*>(p + kDTD)[k]; }
     __device__ double& tDc(uint32_t k) const { return reinterpret_cast<double*>(p + kDTDC)[k]; }
@@ -702,24 +716,37 @@ __device__ __forceinline__ void dense_pairs(uint32_t sb, const uint2* __restrict
 #pragma unroll (kPUnroll)
     for (uint32_t t = gt; t < n_pairs; t += kPairW * 32) {
         const uint2 w = s_pair[t];
+#if SENECA_MDP_DENSE == 2
+        const uint32_t b8 = sb + (w.x & 0x3ffu), m8 = sb + ((w.x >> 10) & 0x3ffu), e8 = sb + (w.x >> 20);
+        const uint32_t sum = ldsd_u32<kDCapc>(b8) + ldsd_u32<kDCapc>(m8);   // <= 2N < 2^32
+        const uint32_t cE = ldsd_u32<kDCape>(e8);
+#else
         const uint32_t b = w.x & 0xffu, m = __byte_perm(w.x, 0, 0x4441), e = w.x >> 16;
-        const uint32_t b4 = sb + 4 * b, m4 = sb + 4 * m, b8 = sb + 8 * b, m8 = sb + 8 * m;
+        const uint32_t b4 = sb + 4 * b, m4 = sb + 4 * m, b8 = sb + 8 * b, m8 = sb + 8 * m, e8 = sb + 8 * e;
         const uint32_t sum = ldsd_u32<kDCapc>(b4) + ldsd_u32<kDCapc>(m4);   // <= 2N < 2^32
+        const uint32_t cE = ldsd_u32<kDCape>(sb + 4 * e);
+#endif
         const bool dfree = sum <= N;                        // Eq. 6 unclamped (both splits)
         const uint32_t r2 = dfree ? N - sum : 0u;
-        const uint32_t cE = ldsd_u32<kDCape>(sb + 4 * e);
         const bool efree = dfree && cE <= r2;               // Eq. 7 unclamped
         const uint32_t x = efree ? r2 - cE : r2;            // N_S, or the clamped N_E (0 if D clamped)
         const double q = div_by_n(u32_to_d(x), dN, y);
         const double prod = __dmul_rn(q, efree ? dsiS : dsiE);
-        const double tX = efree ? ldsd_f64<kDTE>(sb + 8 * e) : 0.0;
+        const double tX = efree ? ldsd_f64<kDTE>(e8) : 0.0;
         // Eq. 6: tD of the other coordinate when D is free, else tDc of this one
         const double d0 = ldsd_f64<kDTDC>(dfree ? m8 - kDelta : b8);
         const double d1 = ldsd_f64<kDTDC>(dfree ? b8 - kDelta : m8);
         const double v0 = __dadd_rn(__dadd_rn(__dadd_rn(ldsd_f64<kDTA>(b8), d0), tX), prod);
         const double v1 = __dadd_rn(__dadd_rn(__dadd_rn(ldsd_f64<kDTA>(m8), d1), tX), prod);
-        const uint32_t i0 = w.y & 0xffffu, i1 = w.y >> 16;
+        const uint32_t i0 = w.y & 0xffffu, i1 = w.y >> 16;   // (DENSE 2: byte offsets, 8 x the index)
+#if SENECA_MDP_DENSE == 2
+        if (kGrid) {
+            st_grid(reinterpret_cast<double*>(reinterpret_cast<char*>(grow) + i0), v0);
+            st_grid(reinterpret_cast<double*>(reinterpret_cast<char*>(grow) + i1), v1);
+        }
+#else
         if (kGrid) { st_grid(grow + i0, v0); st_grid(grow + i1, v1); }
+#endif
         if (v0 > best) { best = v0; best_i = i0; }
         if (v1 > best) { best = v1; best_i = i1; }
     }
@@ -816,7 +843,14 @@ mdp_sweep_pairs(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_prof
                 for (uint32_t t = gt; t < n_pairs; t += kPairW * 32) {
                     const uint2 w = s_pair[t];
                     for (int h = 0; h < 2; ++h) {
-#if SENECA_MDP_DENSE
+#if SENECA_MDP_DENSE == 2
+                        const uint32_t kb = (w.x & 0x3ffu) >> 3, km = ((w.x >> 10) & 0x3ffu) >> 3;
+                        const uint32_t ka = h ? km : kb, kd = h ? kb : km, ke = w.x >> 23;
+                        const auto row_tA = [&](uint32_t k) { return DR.tA(k); };
+                        const auto row_tD = [&](uint32_t k) { return DR.tD(k); };
+                        const auto row_tDc = [&](uint32_t k) { return DR.tDc(k); };
+                        const auto row_tE = [&](uint32_t k) { return DR.tE(k); };
+#elif SENECA_MDP_DENSE
                         const uint32_t kb = w.x & 0xffu, km = (w.x >> 8) & 0xffu;
                         const uint32_t ka = h ? km : kb, kd = h ? kb : km, ke = w.x >> 16;
                         const auto row_tA = [&](uint32_t k) { return DR.tA(k); };
@@ -832,7 +866,7 @@ mdp_sweep_pairs(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_prof
                         const auto row_tDc = [&](uint32_t k) { return rows[k].tDc; };
                         const auto row_tE = [&](uint32_t k) { return rows[k].tE; };
 #endif
-                        const uint32_t idx = h ? w.y >> 16 : w.y & 0xffffu;
+                        const uint32_t idx = (h ? w.y >> 16 : w.y & 0xffffu) / (SENECA_MDP_DENSE == 2 ? 8u : 1u);
                         const uint64_t r1 = N - capc(ka);
                         const uint64_t cD = capc(kd);
                         const bool dfree = cD <= r1;
@@ -845,7 +879,8 @@ mdp_sweep_pairs(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_prof
                         const double tX = efree ? row_tE(ke) : 0.0;
                         const double v = __dadd_rn(__dadd_rn(__dadd_rn(row_tA(ka), tD), tX), prod);
                         if (grow) __stcs(grow + idx, v);
-                        if (v > best || (v == best && idx < best_i)) { best = v; best_i = idx; }
+                        const uint32_t bidx = SENECA_MDP_DENSE == 2 ? 8u * idx : idx;   // (DENSE 2: byte offsets)
+                        if (v > best || (v == best && bidx < best_i)) { best = v; best_i = bidx; }
                     }
                 }
             }
@@ -870,6 +905,7 @@ mdp_sweep_pairs(const seneca_mdp_profile* __restrict__ profiles, uint32_t n_prof
                     if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
                 }
                 uint32_t ra, rb;
+                if (SENECA_MDP_DENSE == 2) bi >>= 3;                // byte offset -> split index
                 index_to_split(bi, ra, rb);
                 r.p_e = (uint8_t)(100 - ra * g);
                 r.p_d = (uint8_t)((ra - rb) * g);
