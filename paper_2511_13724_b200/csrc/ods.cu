@@ -203,6 +203,7 @@ struct Launch {
     uint64_t tr_rep;                 // elements of transcript per replica
     uint32_t gen_ctas;               // trailing CTAs of the launch that refill the permutation ring (§7.2)
     uint32_t gen_pairs;              // (job, epoch) pairs they fill, L.ring_pairs of slice 0
+    uint32_t cluster;                // 1: the J + 1 round CTAs are one thread-block cluster (DSMEM signals)
 };
 
 __device__ __forceinline__ uint32_t ldcg(const uint32_t* p) { return __ldcg(p); }
@@ -464,6 +465,34 @@ __device__ __forceinline__ unsigned long long ld_acquire64(const uint32_t* p) {
     unsigned long long v;
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
+}
+
+// Signals through distributed shared memory (the round CTAs of one replica are one
+// cluster): the writer releases at cluster scope into the reader CTA's shared
+// word, the reader polls its own shared memory with acquire loads.
+__device__ __forceinline__ uint32_t dsmem_addr(const void* local, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"((uint32_t)__cvta_generic_to_shared(local)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void dsmem_red_release_add64(uint32_t addr, unsigned long long v) {
+    asm volatile("red.release.cluster.shared::cluster.add.u64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
+}
+__device__ __forceinline__ void dsmem_st_release32(uint32_t addr, uint32_t v) {
+    asm volatile("st.release.cluster.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long smem_ld_acquire64(const void* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.cluster.shared::cta.u64 %0, [%1];" : "=l"(v) : "r"((uint32_t)__cvta_generic_to_shared(p)) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t smem_ld_acquire32(const void* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.cluster.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"((uint32_t)__cvta_generic_to_shared(p)) : "memory");
+    return v;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 // ------------------------------------------------------------------ per-CTA phase timer (profiling)
@@ -1667,6 +1696,16 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
     // instantiation contains no maintain, refill or signal code at all)
     constexpr bool coupled = kCoupled;
     if (is_maint && !coupled) return;
+    // DSMEM signals (coupled, one cluster of J + 1 CTAs): s_sig in the maintain CTA counts
+    // job phases | evictions pushed << 32; s_rel in each job CTA counts maintains applied
+    __shared__ unsigned long long s_sig;
+    __shared__ uint32_t s_rel;
+    const bool csig = coupled && !kShard && P.cluster != 0;
+    if (csig) {
+        if (tid == 0) { s_sig = 0; s_rel = 0; }
+        __syncthreads();
+        cluster_sync_all();              // every CTA's words are zero before any remote write
+    }
 
     if (tid < kMaxJobs) { s_n[tid] = P.n0[tid]; s_e[tid] = P.e0[tid]; }
     if (tid == 0) {
@@ -1811,7 +1850,8 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
             }
             if (tid == 0) {                  // job phases of round r done; evictions they pushed
                 unsigned long long v;
-                while ((uint32_t)(v = ld_acquire64(L.bar)) < expect) { }
+                if (csig) { while ((uint32_t)(v = smem_ld_acquire64(&s_sig)) < expect) { } }
+                else { while ((uint32_t)(v = ld_acquire64(L.bar)) < expect) { } }
                 const uint32_t pushed = (uint32_t)(v >> 32);
                 M.ne_push = pushed - push_total;
                 M.push_base = push_total;
@@ -1833,7 +1873,11 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
                 L.ev_ed_n[r & 1] = 0;
             }
             __syncthreads();
-            if (tid == 0) { __threadfence(); atomicExch(L.bar + 2, rr + 1); }     // release round r's tiers
+            if (csig) {                     // release round r's tiers into every job CTA (lane = job)
+                if (tid < C.J) dsmem_st_release32(dsmem_addr(&s_rel, tid), rr + 1);
+            } else if (tid == 0) {
+                __threadfence(); atomicExch(L.bar + 2, rr + 1);
+            }
             TM.tick(5);
             advance(part, departing, r);
             spec = false;
@@ -1866,7 +1910,10 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
             schedule(part, departing);
             const uint32_t active_after = s_active & ~departing;
             if (coupled && rr > 0) {                   // maintain(r-1) applied?
-                if (tid == 0) { while (ld_acquire(L.bar + 2) < rr) { } }
+                if (tid == 0) {
+                    if (csig) { while (smem_ld_acquire32(&s_rel) < rr) { } }
+                    else { while (ld_acquire(L.bar + 2) < rr) { } }
+                }
                 __syncthreads();
             }
             TM.tick(4);
@@ -1900,8 +1947,12 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
                     if (tid == 0) S.pf_state = 0;
                 }
                 if (coupled && tid == 0) {                 // job phase done (+ evictions pushed)
-                    __threadfence();
-                    atomicAdd(reinterpret_cast<unsigned long long*>(L.bar), 1ull + ((unsigned long long)S.npush << 32));
+                    if (csig) {
+                        dsmem_red_release_add64(dsmem_addr(&s_sig, C.J), 1ull + ((unsigned long long)S.npush << 32));
+                    } else {
+                        __threadfence();
+                        atomicAdd(reinterpret_cast<unsigned long long*>(L.bar), 1ull + ((unsigned long long)S.npush << 32));
+                    }
                     S.npush = 0;
                 }
                 TM.tick(0);
@@ -1960,7 +2011,10 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
         flush_stats(L, C, S, j, s_e[j]);
         if (S.late) catch_up_seen(L, C, S, j, s_e[j]);
         if (coupled && P.rounds > 0 && (s_active >> j & 1u)) {
-            if (tid == 0) { while (ld_acquire(L.bar + 2) < P.rounds) { } }
+            if (tid == 0) {
+                if (csig) { while (smem_ld_acquire32(&s_rel) < P.rounds) { } }
+                else { while (ld_acquire(L.bar + 2) < P.rounds) { } }
+            }
             __syncthreads();
             if (!S.recount) job_take_refills<kShard>(L, C, S, j, P.r0 + P.rounds - 1, s_sup);
             __syncthreads();
@@ -1984,6 +2038,7 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
         const uint32_t base = is_maint ? 16 : 0;
         for (int k = 0; k < 16; ++k) atomicAdd(L.phase + base + k, TM.acc[k]);
     }
+    if (csig) cluster_sync_all();        // no CTA leaves while a peer may still write its signal word
 }
 
 // Two instantiations: 512 threads, one CTA per SM (a single replay: the most
@@ -2738,6 +2793,8 @@ seneca_status launch_rounds(seneca_ctx* c, uint64_t* Rio, uint32_t jobs_mask, co
     const uint32_t cs = c->C.J + 1;
     const bool clustered = want_cluster && c->R == 1 && cs >= 2 && cs <= 8;
     if (clustered && P.gen_ctas) P.gen_ctas += (cs - (cs + P.gen_ctas) % cs) % cs;
+    static const int want_dsig = [] { const char* e = getenv("SENECA_DSMEM_SIGNALS"); return e ? atoi(e) : 1; }();
+    P.cluster = clustered && want_dsig ? 1u : 0u;
     void* args[] = {&c->LS, &c->C, &P};
     cudaError_t le = cudaSuccess;
     timed(c, K_ROUNDS, st, [&] {
@@ -2757,6 +2814,7 @@ seneca_status launch_rounds(seneca_ctx* c, uint64_t* Rio, uint32_t jobs_mask, co
             le = cudaLaunchKernelExC(&lc, P.timing ? c->round_fn_timed : c->round_fn, args);
             if (le != cudaSuccess) {     // (a configuration error: nothing was launched)
                 (void)cudaGetLastError();
+                P.cluster = 0;
                 le = cudaLaunchCooperativeKernel(P.timing ? c->round_fn_timed : c->round_fn,
                                                  lc.gridDim, lc.blockDim, args, c->round_smem, st);
             }
