@@ -470,6 +470,11 @@ __device__ __forceinline__ unsigned long long ld_acquire64(const uint32_t* p) {
 // Signals through distributed shared memory (the round CTAs of one replica are one
 // cluster): the writer releases at cluster scope into the reader CTA's shared
 // word, the reader polls its own shared memory with acquire loads.
+__device__ __forceinline__ uint32_t dsmem_addr_raw(uint32_t local_shared, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_shared), "r"(rank));
+    return r;
+}
 __device__ __forceinline__ uint32_t dsmem_addr(const void* local, uint32_t rank) {
     uint32_t r;
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"((uint32_t)__cvta_generic_to_shared(local)), "r"(rank));
@@ -477,6 +482,13 @@ __device__ __forceinline__ uint32_t dsmem_addr(const void* local, uint32_t rank)
 }
 __device__ __forceinline__ void dsmem_red_release_add64(uint32_t addr, unsigned long long v) {
     asm volatile("red.release.cluster.shared::cluster.add.u64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
+}
+constexpr uint32_t kFillBuf = 512;   // refill ids pushed into each job CTA's shared memory (DSMEM signals)
+__device__ __forceinline__ void dsmem_st32(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void dsmem_st_release64(uint32_t addr, unsigned long long v) {
+    asm volatile("st.release.cluster.shared::cluster.u64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
 }
 __device__ __forceinline__ void dsmem_st_release32(uint32_t addr, uint32_t v) {
     asm volatile("st.release.cluster.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
@@ -1379,6 +1391,7 @@ struct MaintSmem {
     uint32_t PSg;                        // sharded: the global storage pool at round start (C1)
     uint32_t pscnt[kMaxShards][3];       // sharded: every shard's storage pool ([g][0])
     uint32_t ne_loc, k_loc;              // sharded: evictions / refills inside this shard's range
+    uint32_t relpk;                      // DSMEM signals: this round's refill split for the release word
 };
 
 // keyed refill ranks rho(u) over the storage pool as of round start (R-O8),
@@ -1420,7 +1433,9 @@ __device__ void maint_refill_select(const Lay& L, const Cfg& C, MaintSmem& M, co
 template <bool kSh, class TMr>
 __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSmem& M, uint32_t* s_pre,
                             uint32_t* s_supS, uint64_t r, uint32_t active, uint32_t part_of_round, bool full_scan,
-                            bool speculated, uint32_t ne_push, uint32_t push_base, TMr& TM) {
+                            bool speculated, uint32_t ne_push, uint32_t push_base, TMr& TM,
+                            uint32_t dfill = 0) {
+    // dfill: shared address of the job CTAs' refill buffer (DSMEM signals), 0: none
     const uint32_t tid = threadIdx.x, T = blockDim.x;
     if (tid == 0) {
         M.ne = full_scan ? 0u : ne_push;
@@ -1524,8 +1539,11 @@ __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSm
     // refills enter their tier with no consumers; each job CTA adds them to its
     // own pools before its next classification (R-O8)
     const uint32_t* fill = L.fill_list + (size_t)(r & 1) * C.FL;
+    const bool push = dfill && k <= kFillBuf;       // the ids into every job CTA's shared memory
     for (uint32_t u = tid; u < k; u += T) {
         const uint32_t i = ldcg(fill + u);
+        if (push)
+            for (uint32_t jj = 0; jj < C.J; ++jj) dsmem_st32(dsmem_addr_raw(dfill + 4u * u, jj), i);
         uint32_t* bm = u < kA ? L.bm_a : (u < kA + kD ? L.bm_d : L.bm_e);
         atomicOr(bm + (i >> 5), 1u << (i & 31));
         if (count_add<kSh>(L, C, spidx, i, 0xffffffffu, s_supS) && kSh) atomicAdd(&M.k_loc, 1u);
@@ -1534,6 +1552,7 @@ __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSm
     if (tid == 0) {
         uint32_t* fn = L.fill_n + (r & 1) * 4;
         fn[0] = k; fn[1] = kA; fn[2] = kD;
+        M.relpk = push ? (0x80000000u | k | (kA << 10) | (kD << 20)) : 0u;
         L.ev_ed_n[r & 1] = M.ned;
         M.PS = kSh ? M.PS + M.ne_loc - M.k_loc : M.PS + ne - k;   // storage pool and tier sizes live in
                                                                    // shared memory while running
@@ -1557,18 +1576,28 @@ __device__ void maint_apply(const Lay& L, const Cfg& C, const Launch& P, MaintSm
 // seen join the pool of their tier (empty consumer sets), and under
 // evict_tiers = ALL evicted E/D entries it has not seen leave its E/D pool (an
 // evicted A entry was consumed by j, so it was in no A pool of j).
+// relpk (DSMEM signals): bit 31 set -> the split k | kA << 10 | kD << 20 came with the
+// release and the ids are in this CTA's shared buffer s_fill (pushed by maintain).
 template <bool kSh>
-__device__ void job_take_refills(const Lay& L, const Cfg& C, JobSmem& S, uint32_t j, uint64_t r, uint32_t* s_sup) {
+__device__ void job_take_refills(const Lay& L, const Cfg& C, JobSmem& S, uint32_t j, uint64_t r, uint32_t* s_sup,
+                                 uint32_t relpk = 0, const uint32_t* s_fill = nullptr) {
     const uint32_t* fn = L.fill_n + (r & 1) * 4;
     const uint32_t* fill = L.fill_list + (size_t)(r & 1) * C.FL;
-    // the first refill entry of this thread is loaded together with the counts (an
-    // entry beyond kf is read but not used; the buffer holds FL entries)
-    const uint32_t i0 = threadIdx.x < C.FL ? ldcg(fill + threadIdx.x) : 0u;
-    const uint32_t kf = ldcg(fn), kA = ldcg(fn + 1), kD = ldcg(fn + 2);
+    const bool local = (relpk >> 31) != 0;
+    uint32_t i0, kf, kA, kD;
+    if (local) {
+        kf = relpk & 1023u; kA = (relpk >> 10) & 1023u; kD = (relpk >> 20) & 1023u;
+        i0 = threadIdx.x < kf ? s_fill[threadIdx.x] : 0u;
+    } else {
+        // the first refill entry of this thread is loaded together with the counts (an
+        // entry beyond kf is read but not used; the buffer holds FL entries)
+        i0 = threadIdx.x < C.FL ? ldcg(fill + threadIdx.x) : 0u;
+        kf = ldcg(fn); kA = ldcg(fn + 1); kD = ldcg(fn + 2);
+    }
     const uint32_t* seen_j = L.seen + (size_t)j * C.NW;
     uint32_t addA = 0, addD = 0, addE = 0;   // registers (no indexed local array)
     for (uint32_t u = threadIdx.x; u < kf; u += blockDim.x) {
-        const uint32_t i = u == threadIdx.x ? i0 : ldcg(fill + u);
+        const uint32_t i = u == threadIdx.x ? i0 : (local ? s_fill[u] : ldcg(fill + u));
         if (!((ldcg(seen_j + (i >> 5)) >> (i & 31)) & 1u)) {
             const uint32_t tt = u < kA ? 0u : (u < kA + kD ? 1u : 2u);
             if (count_add<kSh>(L, C, j * 3 + tt, i, 1u, s_sup + tt * C.NS)) {
@@ -1699,7 +1728,9 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
     // DSMEM signals (coupled, one cluster of J + 1 CTAs): s_sig in the maintain CTA counts
     // job phases | evictions pushed << 32; s_rel in each job CTA counts maintains applied
     __shared__ unsigned long long s_sig;
-    __shared__ uint32_t s_rel;
+    __shared__ unsigned long long s_rel;           // rounds applied | refill split << 32
+    __shared__ uint32_t s_fill[kFillBuf];          // the refill ids of the last maintain (job CTAs)
+    __shared__ uint32_t s_relpk;
     const bool csig = coupled && !kShard && P.cluster != 0;
     if (csig) {
         if (tid == 0) { s_sig = 0; s_rel = 0; }
@@ -1866,15 +1897,17 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
                 if (!spec && tid == 0) set_deficits();
                 __syncthreads();
                 maint_apply<kShard>(L, C, P, M, s_pre, s_sup, r, active_after, part, departing != 0, spec,
-                                    M.ne_push, M.push_base, TM);
+                                    M.ne_push, M.push_base, TM,
+                                    csig ? (uint32_t)__cvta_generic_to_shared(s_fill) : 0u);
             } else if (tid == 0) {          // nothing maintained: the job CTAs take an empty round
                 uint32_t* fn = L.fill_n + (r & 1) * 4;
                 fn[0] = fn[1] = fn[2] = 0;
                 L.ev_ed_n[r & 1] = 0;
+                M.relpk = 0x80000000u;       // (DSMEM signals: an empty split with the release)
             }
             __syncthreads();
             if (csig) {                     // release round r's tiers into every job CTA (lane = job)
-                if (tid < C.J) dsmem_st_release32(dsmem_addr(&s_rel, tid), rr + 1);
+                if (tid < C.J) dsmem_st_release64(dsmem_addr(&s_rel, tid), ((unsigned long long)M.relpk << 32) | (rr + 1));
             } else if (tid == 0) {
                 __threadfence(); atomicExch(L.bar + 2, rr + 1);
             }
@@ -1911,8 +1944,14 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
             const uint32_t active_after = s_active & ~departing;
             if (coupled && rr > 0) {                   // maintain(r-1) applied?
                 if (tid == 0) {
-                    if (csig) { while (smem_ld_acquire32(&s_rel) < rr) { } }
-                    else { while (ld_acquire(L.bar + 2) < rr) { } }
+                    s_relpk = 0;
+                    if (csig) {
+                        unsigned long long v;
+                        while ((uint32_t)(v = smem_ld_acquire64(&s_rel)) < rr) { }
+                        if ((uint32_t)v == rr) s_relpk = (uint32_t)(v >> 32);
+                    } else {
+                        while (ld_acquire(L.bar + 2) < rr) { }
+                    }
                 }
                 __syncthreads();
             }
@@ -1924,7 +1963,7 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
                     if (tid == 0) { S.recount = 0; S.c1 = 1; }     // (sharded: the recounted sizes are exchanged)
                     __syncthreads();
                 }
-                else if (coupled && rr > 0) { job_take_refills<kShard>(L, C, S, j, r - 1, s_sup); __syncthreads(); }
+                else if (coupled && rr > 0) { job_take_refills<kShard>(L, C, S, j, r - 1, s_sup, s_relpk, s_fill); __syncthreads(); }
                 TM.tick(0);
                 job_round<kShard>(L, C, P, S, s_req, s_miss, s_sub, s_oid, s_osrc, s_pre, j, r, s_e[j], s_n[j],
                           __popc(active_after), TM, s_win, s_wseen, s_sup);
@@ -2012,11 +2051,17 @@ __device__ __forceinline__ void ods_rounds_body(const Lays& LS, const Cfg& C, co
         if (S.late) catch_up_seen(L, C, S, j, s_e[j]);
         if (coupled && P.rounds > 0 && (s_active >> j & 1u)) {
             if (tid == 0) {
-                if (csig) { while (smem_ld_acquire32(&s_rel) < P.rounds) { } }
-                else { while (ld_acquire(L.bar + 2) < P.rounds) { } }
+                s_relpk = 0;
+                if (csig) {
+                    unsigned long long v;
+                    while ((uint32_t)(v = smem_ld_acquire64(&s_rel)) < P.rounds) { }
+                    if ((uint32_t)v == P.rounds) s_relpk = (uint32_t)(v >> 32);
+                } else {
+                    while (ld_acquire(L.bar + 2) < P.rounds) { }
+                }
             }
             __syncthreads();
-            if (!S.recount) job_take_refills<kShard>(L, C, S, j, P.r0 + P.rounds - 1, s_sup);
+            if (!S.recount) job_take_refills<kShard>(L, C, S, j, P.r0 + P.rounds - 1, s_sup, s_relpk, s_fill);
             __syncthreads();
         }
         if (tid < 3) L.cnt_tot[j * 3 + tid] = S.tot[tid];
