@@ -2834,7 +2834,20 @@ seneca_status launch_rounds(seneca_ctx* c, uint64_t* Rio, uint32_t jobs_mask, co
     // hence same die; ImageNet-1K 9.01 -> 8.93 us per round, tools/s4q.sh); the generator
     // CTAs are padded so the grid is a multiple of the cluster size.  SENECA_ROUND_CLUSTER=0
     // turns it off; a cluster launch the device refuses falls back to the plain one.
-    static const int want_cluster = [] { const char* e = getenv("SENECA_ROUND_CLUSTER"); return e ? atoi(e) : 1; }();
+    // (Nsight Compute cannot replay a cooperative cluster launch -- "LaunchFailed" --
+    // so under an injected tool (ncu's NV_COMPUTE_PROFILER_PERFWORKS_DIR / NV_TPS_* /
+    // NV_NSIGHT_INJECTION_*, any CUDA_INJECTION64_PATH) the plain cooperative launch
+    // with global-memory signals is used)
+    static const int want_cluster = [] {
+        const char* e = getenv("SENECA_ROUND_CLUSTER");
+        if (e) return atoi(e);
+        for (const char* v : {"CUDA_INJECTION64_PATH", "NV_COMPUTE_PROFILER_PERFWORKS_DIR", "NV_TPS_LAUNCH_TOKEN",
+                              "NV_NSIGHT_INJECTION_TRANSPORT_TYPE"}) {
+            const char* x = getenv(v);
+            if (x && *x) return 0;
+        }
+        return 1;
+    }();
     const uint32_t cs = c->C.J + 1;
     const bool clustered = want_cluster && c->R == 1 && cs >= 2 && cs <= 8;
     if (clustered && P.gen_ctas) P.gen_ctas += (cs - (cs + P.gen_ctas) % cs) % cs;
