@@ -682,6 +682,22 @@ def test_workspace_above_2gib_per_replica():
     g.close()
 
 
+@pytest.mark.parametrize("env", [{}, {"SENECA_ROUND_CLUSTER": "0"}, {"SENECA_DSMEM_SIGNALS": "0"}])
+def test_coupled_signal_paths(env):
+    """The three signal paths of a coupled replay: the J + 1 CTAs as
+    one cluster with DSMEM signals (default), the plain cooperative launch with
+    global-memory signals (SENECA_ROUND_CLUSTER=0, also what runs under ncu), and
+    the cluster launch with global signals (SENECA_DSMEM_SIGNALS=0) -- A churn,
+    evict-all and cold start in launches of random length, vs the oracle (the
+    knobs are read once per process, hence a subprocess)."""
+    import subprocess
+    import sys
+    out = subprocess.run([sys.executable, os.path.join(os.path.dirname(HERE), "tools", "signal_paths.py")],
+                         capture_output=True, text=True, timeout=600, env=dict(os.environ, **env))
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-3000:]
+    assert "signal paths ok" in out.stdout
+
+
 # ---------------------------------------------------------------- sample-ID-range sharding (SURVEY §8(e))
 def sharded_replay(c, ce, cd, ca, seed, G, evict_all=False, cold=False, arrival=None, rounds=None):
     g = P.ODSContext(c["n_total"], c["batch"], c["target"], ce, cd, ca, seed, shards=G,
